@@ -1,0 +1,144 @@
+/*
+ * da_b200.h - C-ABI of the B200 Dictionary-Annealing hot path.
+ *
+ * The reference (annq, pure Python/numpy, /root/reference/pkg/src/annq) has no
+ * FFI; its "operator API" is a set of Python functions.  Each export below is
+ * the device half of one of those functions; the Python host package
+ * paper_1509_05194_b200 binds them with ctypes and keeps the reference's
+ * signatures.  The reference site each entry replaces is
+ * cited as file:line relative to pkg/src/annq/.
+ *
+ * Conventions
+ *   - All array arguments are DEVICE pointers owned by the caller; the library
+ *     never frees caller memory.  Row-major layouts with explicit leading dims.
+ *   - `stream` is a cudaStream_t passed as void*; every call is asynchronous
+ *     on it (host-side plan caches aside).
+ *   - Return: 0 ok; < 0 invalid argument (ValueError); > 0 CUDA error
+ *     (RuntimeError).  da_last_error() gives the calling thread's message.
+ *   - x_f32 / a_f32 flags select float32 (1) or float64 (0) inputs; float32
+ *     inputs are widened exactly, as numpy's astype(float64) does.
+ *   - code_bytes is 1 (uint8), 2 (uint16) or 4 (int32) for code matrices.
+ */
+#ifndef DA_B200_H
+#define DA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DA_B200_ABI_VERSION 1
+
+const char* da_last_error(void);
+int da_version(void);
+/* Number of kernels this library has launched in the process (all devices). */
+long long da_launch_count(void);
+/* Free every library-owned scratch buffer (all devices). */
+int da_release_scratch(void);
+
+/* ||a_r||^2 over the first d columns, numpy pairwise order.
+ * replaces (C_active * C_active).sum(axis=1)   clustering.py:144 */
+int da_row_sqnorms(const void* A, int a_f32, int64_t rows, int64_t lda, int d, double* out, void* stream);
+
+/* Nearest codeword over the active prefix d with first-min ties; d2 clipped at 0.
+ * replaces _assign                              clustering.py:139-148
+ * prev/changed optional: counts rows whose label differs from prev (clustering.py:199). */
+int da_assign(const void* X, int x_f32, int64_t n, int64_t ldx, int d, const double* C, int64_t ldc, int K,
+              const double* cc, int32_t* labels, double* d2, const int32_t* prev, unsigned long long* changed,
+              void* stream);
+
+/* Per-label sums (mode 1) or means written into the non-empty rows of out (mode 0),
+ * over all D columns, bit-identical to argsort(stable)+add.reduceat.
+ * replaces _group_means                         clustering.py:151-162 */
+int da_group_sums(const double* X, int64_t n, int64_t ldx, int D, const int32_t* labels, int K, int mode,
+                  double* out, int64_t ldo, int32_t* counts, void* stream);
+
+/* Stable argsort of labels in [0,K) plus bincount.
+ * replaces np.argsort(assign, kind="stable") / np.bincount   clustering.py:154-155 */
+int da_label_order(const int32_t* labels, int64_t n, int K, int32_t* order, int32_t* counts, void* stream);
+
+/* C[dst[i], :] = X[src[i], :]  (empty-cluster reseed, clustering.py:192-196) */
+int da_gather_rows(const double* X, int64_t ldx, int D, const int64_t* src, const int32_t* dst, int cnt, double* C,
+                   int64_t ldc, void* stream);
+
+/* Intermediate set for dictionary m, computed in float64, stored float32.
+ * replaces heat_up                              annealing.py:97-112 */
+int da_heat_up(const float* X, int64_t n, int D, const int32_t* codes, const float* cw, int M, int K, int m,
+               float* out, void* stream);
+
+/* Exact per-vector squared error ||x - sum_m c_m||^2 (reconstruction in m order).
+ * replaces _per_vector_errors / distortion rows annealing.py:135-137, codebook.py:206-208 */
+int da_vec_err(const void* X, int x_f32, int64_t n, int64_t ldx, int D, const void* codes, int code_bytes,
+               int64_t ldc, const float* cw, int M, int K, double* err, void* stream);
+
+/* float64 reconstruction sum_m C[m][codes_m].
+ * replaces _reconstruct_batch                   codebook.py:181-188 */
+int da_reconstruct(const void* codes, int code_bytes, int64_t n, int64_t ldc, const float* cw, int M, int K, int D,
+                   double* out, void* stream);
+
+/* Column means (PCA centre).  replaces X.mean(axis=0)   clustering.py:93 */
+int da_col_mean(const void* X, int x_f32, int64_t n, int64_t ld, int D, double* mean, void* stream);
+
+/* Sample covariance (X - mean)^T (X - mean) / (n - 1).  replaces clustering.py:94-96 */
+int da_pca_cov(const void* X, int x_f32, int64_t n, int64_t ld, int D, const double* mean, double* cov, void* stream);
+
+/* inverse=0: out = (X - mean) @ R^T;  inverse=1: out = X @ R + mean.
+ * replaces PcaModel.transform / inverse_transform   clustering.py:39-43 */
+int da_rotate(const void* X, int x_f32, int64_t n, int64_t ld, int D, const double* R, const double* mean,
+              double* out, int inverse, void* stream);
+
+/* Generic strided float64 product C[i,j] = sum_k A[i*sai+k*sak] * B[k*sbk+j*sbj]
+ * (sequential FMA over k).  Used for the PCA Gram route   clustering.py:101-110 */
+int da_gemm_strided(const void* A, int a_f32, int64_t sai, int64_t sak, const void* B, int b_f32, int64_t sbk,
+                    int64_t sbj, double* C, int64_t sci, int64_t scj, int64_t M, int64_t N, int64_t K, void* stream);
+
+/* ||c||^2 per codeword in numpy einsum order.  replaces codebook.py:129, 237, 260 */
+int da_einsum_sq(const float* cw, int64_t rows, int D, double* out, void* stream);
+
+/* Cross-product table P[a][b][i][j] = c_a(i).c_b(j), (M,M,K,K) float64, and sq (M,K).
+ * only_m < 0: full table (cross_products, codebook.py:231-238);
+ * only_m = m: rows/cols of m (refresh_cross_products, codebook.py:241-252). */
+int da_cross_products(const float* cw, int M, int K, int D, int only_m, double* P, double* sq, void* stream);
+
+/* Beam-search encode of n vectors with width L; codes (n, M) and exact errors.
+ * replaces _beam_tables + _beam_encode_chunk    codebook.py:255-300
+ * (encode_dataset codebook.py:319-358, encode_multipath codebook.py:303-316) */
+int da_encode(const void* X, int x_f32, int64_t n, int64_t ldx, int D, const float* cw, int M, int K, int L,
+              const double* sq, const double* P, void* codes, int code_bytes, int64_t ldcodes, double* err,
+              void* stream);
+
+/* Query-independent ADC term 2 sum_{a<b} P[a,b][i_a,i_b].  replaces code_pair_sums codebook.py:388-396 */
+int da_pair_sums(const void* codes, int code_bytes, int64_t n, int64_t ldc, const double* P, int M, int K,
+                 double* out, void* stream);
+
+/* Per-query ADC tables ||q - c_mk||^2 clipped at 0, plus ||q||^2.
+ * replaces adc_table                            codebook.py:361-369 */
+int da_adc_lut(const double* Q, int64_t nq, int D, const float* cw, int M, int K, const double* sq, double* lut,
+               double* qsq, void* stream);
+
+/* ADC distances of candidate codes and top-r by (distance, position) per query.
+ * cand == NULL: candidates are rows 0..ncand-1 (exhaustive); else cand is (nq, ncand)
+ * row ids, position p breaks ties and ids[...] = cand[q, p].
+ * replaces exhaustive_adc_search                codebook.py:399-429 */
+int da_adc_scan(const void* codes, int code_bytes, int64_t ldc, const double* pair, const int64_t* cand,
+                int64_t ncand, int64_t nq, const double* lut, const double* qsq, int M, int K, int r, int64_t* ids,
+                double* dists, void* stream);
+
+/* numpy pairwise sum (divide=0) or mean (divide=1) of a float64 vector, result on device.
+ * replaces errs.mean() / .mean() of per-vector errors   clustering.py:187, annealing.py:176 */
+int da_np_sum(const double* a, int64_t n, int divide, double* out, void* stream);
+
+/* Keep-the-better rule of da_sweep: where beam_err <= inc_err take the beam code.
+ * replaces annealing.py:173-176 */
+int da_select_better(int64_t n, int M, const int32_t* beam_codes, const double* beam_err, int32_t* inc_codes,
+                     double* inc_err, void* stream);
+
+/* codes[:, m] = labels  (annealing.py:169, 201) */
+int da_set_column(int32_t* codes, int64_t n, int M, int m, const int32_t* labels, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DA_B200_H */

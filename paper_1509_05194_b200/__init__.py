@@ -1,0 +1,108 @@
+"""B200-native hot path of Dictionary Annealing (arXiv 1509.05194).
+
+A drop-in for the residual-quantization path of the reference package
+`annq`: the same public names and signatures, computed by the sm_100a
+kernels of libda_b200.so (C-ABI in include/da_b200.h) with torch used for
+device memory and streams only.  There is no CPU fallback.
+
+Use it directly (``import paper_1509_05194_b200 as annq``) or patch an
+installed reference in place with :func:`install`.
+"""
+
+from .annealing import (
+    TrainConfig,
+    TrainReport,
+    TrainStep,
+    cool_down,
+    da_sweep,
+    heat_up,
+    rvq_train,
+    train_from_scratch,
+    train_online,
+)
+from .clustering import (
+    Centroids,
+    PcaModel,
+    dimension_schedule,
+    improved_kmeans,
+    lloyd_kmeans,
+    pca_fit,
+    quantization_error,
+)
+from .codebook import (
+    AdcTable,
+    Codebook,
+    CrossProductTable,
+    EncodedDataset,
+    adc_distance,
+    adc_rerank,
+    adc_table,
+    code_pair_sums,
+    cross_products,
+    dictionary_variances,
+    distortion,
+    encode_dataset,
+    encode_multipath,
+    exhaustive_adc_search,
+    exhaustive_adc_search_batch,
+    read_codebook,
+    read_encoded,
+    reconstruct,
+    refresh_cross_products,
+    reorder_by_variance,
+    write_codebook,
+    write_encoded,
+)
+from .validation import FormatError
+
+__version__ = "0.1.0"
+
+# (module, attribute) binding sites of the reference that the drop-in replaces
+# (SURVEY.md section 8b): attribute calls through `cb.` plus every by-name copy.
+_PATCH_TABLE = {
+    "annq.codebook": ["cross_products", "refresh_cross_products", "encode_multipath", "encode_dataset",
+                      "adc_table", "code_pair_sums", "exhaustive_adc_search", "reconstruct", "distortion"],
+    "annq.clustering": ["pca_fit", "lloyd_kmeans", "improved_kmeans", "quantization_error"],
+    "annq.annealing": ["heat_up", "cool_down", "da_sweep", "train_from_scratch", "train_online", "rvq_train",
+                       "improved_kmeans"],
+    "annq.estimators": ["train_from_scratch", "train_online"],
+    "annq.cli": ["train_from_scratch", "train_online"],
+    "annq.atree": ["adc_table"],
+    "annq": ["cross_products", "encode_multipath", "encode_dataset", "adc_table", "exhaustive_adc_search",
+             "reconstruct", "distortion", "pca_fit", "lloyd_kmeans", "improved_kmeans", "quantization_error",
+             "heat_up", "cool_down", "da_sweep", "train_from_scratch", "train_online", "rvq_train"],
+}
+
+
+def install(annq_module=None):
+    """Rebind the reference's hot-path entry points to this implementation.
+
+    Returns the list of (module, name) pairs that were patched.  Objects
+    passed in from the reference (its Codebook / CrossProductTable /
+    EncodedDataset) are accepted by duck typing.
+    """
+    import importlib
+    import sys
+
+    from . import annealing as _an
+    from . import clustering as _cl
+    from . import codebook as _cbm
+
+    ours = {}
+    for mod in (_cbm, _cl, _an):
+        for name in dir(mod):
+            if not name.startswith("_"):
+                ours.setdefault(name, getattr(mod, name))
+    patched = []
+    if annq_module is not None:
+        sys.modules.setdefault("annq", annq_module)
+    for modname, names in _PATCH_TABLE.items():
+        try:
+            mod = importlib.import_module(modname)
+        except Exception:  # module absent in this install
+            continue
+        for name in names:
+            if hasattr(mod, name) and name in ours:
+                setattr(mod, name, ours[name])
+                patched.append((modname, name))
+    return patched

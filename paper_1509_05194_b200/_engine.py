@@ -1,0 +1,528 @@
+"""Device-resident DA engine: torch tensors in HBM, kernels through the C-ABI.
+
+Everything here works on CUDA tensors and never round-trips data to the host
+except (a) the few scalars the reference's control flow branches on
+(empty-cluster counts, the Lloyd stable test, the keep-staged-or-init test,
+the sweep's convergence test) and (b) the D x D covariance handed to LAPACK's
+eigh, exactly as the reference computes it on the CPU
+(annq/clustering.py:97).  Public, reference-shaped functions live in
+codebook.py / clustering.py / annealing.py and call into this module.
+
+`comm` (see distributed.py) is None for one GPU; with a communicator the rows
+of X are a shard of the dataset and every reduction the reference performs
+over rows is completed with an NCCL allreduce.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from ._native import native
+
+F32, F64, I32, I64 = torch.float32, torch.float64, torch.int32, torch.int64
+
+
+# ---------------------------------------------------------------------------
+# plumbing
+
+
+def require_cuda() -> None:
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "paper_1509_05194_b200 runs on a CUDA device only (no CPU fallback); "
+            "no GPU is visible"
+        )
+
+
+def device() -> torch.device:
+    require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream() -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def P(t) -> ctypes.c_void_p | None:
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def is_f32(t: torch.Tensor) -> int:
+    if t.dtype == F32:
+        return 1
+    if t.dtype == F64:
+        return 0
+    raise TypeError(f"expected float32/float64 tensor, got {t.dtype}")
+
+
+def code_bytes(t: torch.Tensor) -> int:
+    return {torch.uint8: 1, torch.uint16: 2, torch.int32: 4}[t.dtype]
+
+
+def to_dev(a, dtype=None) -> torch.Tensor:
+    """Host array -> contiguous CUDA tensor (pinned staging for large arrays)."""
+    if isinstance(a, torch.Tensor):
+        t = a
+    else:
+        a = np.ascontiguousarray(a)
+        t = torch.from_numpy(a)
+    if dtype is not None and t.dtype != dtype:
+        t = t.to(dtype)
+    return t.to(device(), non_blocking=False).contiguous()
+
+
+def scalar(t: torch.Tensor) -> float:
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# reductions in numpy order
+
+
+def np_mean(a: torch.Tensor, comm=None) -> torch.Tensor:
+    """Device scalar equal to numpy's a.mean() (pairwise) on one GPU.
+
+    Sharded: per-shard pairwise sums, allreduced, divided by the global n.
+    """
+    out = torch.empty(1, dtype=F64, device=a.device)
+    n = a.numel()
+    if comm is None:
+        native.da_np_sum(P(a), n, 1, P(out), stream())
+        return out
+    if n:
+        native.da_np_sum(P(a), n, 0, P(out), stream())
+    else:
+        out.zero_()
+    comm.allreduce_(out)
+    return out / float(comm.total(n))
+
+
+def row_sqnorms(A: torch.Tensor, d: int) -> torch.Tensor:
+    out = torch.empty(A.shape[0], dtype=F64, device=A.device)
+    native.da_row_sqnorms(P(A), is_f32(A), A.shape[0], A.stride(0), d, P(out), stream())
+    return out
+
+
+def assign(X: torch.Tensor, d: int, C: torch.Tensor, cc: torch.Tensor | None = None,
+           prev: torch.Tensor | None = None, changed: torch.Tensor | None = None):
+    """annq/clustering.py:139-148 on the first d columns; labels int32, d2 f64."""
+    n, K = X.shape[0], C.shape[0]
+    if cc is None:
+        cc = row_sqnorms(C, d)
+    labels = torch.empty(n, dtype=I32, device=X.device)
+    d2 = torch.empty(n, dtype=F64, device=X.device)
+    native.da_assign(P(X), is_f32(X), n, X.stride(0), d, P(C), C.stride(0), K, P(cc), P(labels), P(d2),
+                     P(prev), P(changed), stream())
+    return labels, d2
+
+
+# ---------------------------------------------------------------------------
+# Lloyd k-means with an active prefix (annq/clustering.py:165-203)
+
+
+def _reseed_single(Xr, errs, empty_idx, C):
+    """C[empty] = X[worst], worst = argsort(errs, stable)[::-1][:e] (clustering.py:192-196)."""
+    e = len(empty_idx)
+    errs_h = errs.cpu().numpy()
+    worst = np.argsort(errs_h, kind="stable")[::-1][:e].copy()
+    src = torch.from_numpy(worst.astype(np.int64)).to(Xr.device)
+    dst = torch.from_numpy(np.asarray(empty_idx, dtype=np.int32)).to(Xr.device)
+    native.da_gather_rows(P(Xr), Xr.stride(0), Xr.shape[1], P(src), P(dst), e, P(C), C.stride(0), stream())
+
+
+def _reseed_sharded(Xr, errs, empty_idx, C, comm):
+    """Global worst points across shards: each shard offers its local top-e
+    (err, global row id) pairs, merged with the reference's order
+    (descending error, ties to the higher row id)."""
+    e = len(empty_idx)
+    errs_h = errs.cpu().numpy()
+    local = np.argsort(errs_h, kind="stable")[::-1][:e].copy()
+    offset = comm.row_offset
+    cand_err = torch.full((e,), -np.inf, dtype=F64)
+    cand_gid = torch.full((e,), -1, dtype=I64)
+    cand_err[: len(local)] = torch.from_numpy(errs_h[local])
+    cand_gid[: len(local)] = torch.from_numpy(local.astype(np.int64) + offset)
+    rows = torch.zeros((e, Xr.shape[1]), dtype=F64, device=Xr.device)
+    if len(local):
+        rows[: len(local)] = Xr[torch.from_numpy(local.astype(np.int64)).to(Xr.device)]
+    all_err = comm.allgather(cand_err.to(Xr.device)).cpu().numpy().reshape(-1)
+    all_gid = comm.allgather(cand_gid.to(Xr.device)).cpu().numpy().reshape(-1)
+    all_rows = comm.allgather(rows).reshape(-1, Xr.shape[1])
+    # descending err, ties -> higher global id first
+    order = np.lexsort((-all_gid, -all_err))[:e]
+    pick = torch.from_numpy(order.astype(np.int64)).to(Xr.device)
+    C[torch.from_numpy(np.asarray(empty_idx, dtype=np.int64)).to(C.device)] = all_rows[pick]
+
+
+def lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, comm=None):
+    """Returns (C f64 (K,D), labels int32 (n,), trace list[float])."""
+    n, D = Xr.shape
+    K = C_init.shape[0]
+    C = C_init.clone().contiguous()
+    dev = Xr.device
+    changed = torch.zeros(1, dtype=torch.int64, device=dev)
+    trace_d = torch.empty(max_iters + 1, dtype=F64, device=dev)
+    labels, errs = assign(Xr, active, C)
+    trace_d[0:1] = np_mean(errs, comm)
+    iters = 0
+    counts = torch.empty(K, dtype=I32, device=dev)
+    sums = torch.empty((K, D), dtype=F64, device=dev) if comm is not None else None
+    for _ in range(max_iters):
+        if comm is None:
+            native.da_group_sums(P(Xr), n, Xr.stride(0), D, P(labels), K, 0, P(C), C.stride(0), P(counts),
+                                 stream())
+            counts_h = counts.cpu().numpy()
+        else:
+            native.da_group_sums(P(Xr), n, Xr.stride(0), D, P(labels), K, 1, P(sums), sums.stride(0),
+                                 P(counts), stream())
+            cnt64 = counts.to(F64)
+            comm.allreduce_(sums)
+            comm.allreduce_(cnt64)
+            counts_h = cnt64.cpu().numpy().astype(np.int64)
+            filled_t = torch.from_numpy(np.flatnonzero(counts_h > 0)).to(dev)
+            if filled_t.numel():
+                C[filled_t] = sums[filled_t] / cnt64[filled_t].unsqueeze(1)
+        empty = np.flatnonzero(counts_h == 0)
+        if empty.size:
+            if comm is None:
+                _reseed_single(Xr, errs, empty, C)
+            else:
+                _reseed_sharded(Xr, errs, empty, C, comm)
+        changed.zero_()
+        new_labels, errs = assign(Xr, active, C, prev=labels, changed=changed)
+        iters += 1
+        trace_d[iters:iters + 1] = np_mean(errs, comm)
+        if comm is not None:
+            comm.allreduce_(changed)
+        stable = int(changed.item()) == 0
+        labels = new_labels
+        if stable:
+            break
+    trace = trace_d[: iters + 1].cpu().tolist()
+    return C, labels, trace
+
+
+# ---------------------------------------------------------------------------
+# PCA (annq/clustering.py:82-113) and the staged k-means (clustering.py:215-250)
+
+
+def _complete_basis(components: np.ndarray, d: int) -> np.ndarray:
+    """Gram-Schmidt completion of an orthonormal row set (clustering.py:63-79)."""
+    rows = [components[i] for i in range(components.shape[0])]
+    for j in range(d):
+        if len(rows) == d:
+            break
+        v = np.zeros(d)
+        v[j] = 1.0
+        for _ in range(2):
+            for u in rows:
+                v -= (v @ u) * u
+        nv = np.linalg.norm(v)
+        if nv > 1e-8:
+            rows.append(v / nv)
+    if len(rows) != d:
+        raise RuntimeError("failed to complete an orthonormal basis")
+    return np.vstack(rows)
+
+
+def pca(X: torch.Tensor, comm=None):
+    """Returns (R dev f64 (D,D), mean dev f64 (D,), variances np, R host).
+
+    Mean and covariance are reduced on the device (allreduced across shards);
+    the D x D eigendecomposition runs in LAPACK on the host, like the reference.
+    """
+    n_local, D = X.shape
+    n = comm.total(n_local) if comm is not None else n_local
+    if n < 2:
+        raise ValueError(f"PCA needs at least 2 vectors, got {n}")
+    mean = torch.empty(D, dtype=F64, device=X.device)
+    if comm is None:
+        native.da_col_mean(P(X), is_f32(X), n_local, X.stride(0), D, P(mean), stream())
+    else:
+        if n_local:
+            native.da_col_mean(P(X), is_f32(X), n_local, X.stride(0), D, P(mean), stream())
+            mean *= float(n_local)
+        else:
+            mean.zero_()
+        comm.allreduce_(mean)
+        mean /= float(n)
+    if n > D:
+        cov = torch.empty((D, D), dtype=F64, device=X.device)
+        if comm is None:
+            native.da_pca_cov(P(X), is_f32(X), n_local, X.stride(0), D, P(mean), P(cov), stream())
+        else:
+            if n_local >= 2:
+                native.da_pca_cov(P(X), is_f32(X), n_local, X.stride(0), D, P(mean), P(cov), stream())
+                cov *= float(n_local - 1)
+            elif n_local == 1:
+                xc = X.to(F64) - mean
+                cov = xc.T @ xc
+            else:
+                cov.zero_()
+            comm.allreduce_(cov)
+            cov /= float(n - 1)
+        cov_h = cov.cpu().numpy()
+        w, V = np.linalg.eigh(cov_h)
+        order = np.argsort(w, kind="stable")[::-1]
+        R_h = np.ascontiguousarray(V[:, order].T)
+        variances = np.maximum(w[order], 0.0)
+    else:
+        if comm is not None:
+            raise ValueError("the Gram-matrix PCA route (n <= d) is not sharded")
+        # Gram route (clustering.py:101-112): n <= d, so these products are tiny
+        Xc = torch.empty((n, D), dtype=F64, device=X.device)
+        ident = torch.eye(D, dtype=F64, device=X.device)
+        native.da_rotate(P(X), is_f32(X), n, X.stride(0), D, P(ident), P(mean), P(Xc), 0, stream())
+        gram = torch.empty((n, n), dtype=F64, device=X.device)
+        native.da_gemm_strided(P(Xc), 0, D, 1, P(Xc), 0, 1, D, P(gram), n, 1, n, n, D, stream())
+        w, U = np.linalg.eigh(gram.cpu().numpy())
+        order = np.argsort(w, kind="stable")[::-1]
+        w = np.maximum(w[order], 0.0)
+        U = U[:, order]
+        tol = max(w[0], 1.0) * 1e-10 if w.size else 0.0
+        keep = w > tol
+        Uk = to_dev(np.ascontiguousarray(U[:, keep]), F64)
+        r = int(keep.sum())
+        comps_d = torch.empty((D, max(r, 1)), dtype=F64, device=X.device)
+        if r:
+            native.da_gemm_strided(P(Xc), 0, 1, D, P(Uk), 0, r, 1, P(comps_d), r, 1, D, r, n, stream())
+        comps = comps_d.cpu().numpy()[:, :r] / np.sqrt(w[keep])[None, :]
+        R_h = np.ascontiguousarray(_complete_basis(comps.T, D))
+        variances = np.zeros(D)
+        variances[:r] = w[keep] / (n - 1)
+    R = to_dev(R_h, F64)
+    return R, mean, variances, R_h
+
+
+def rotate(X: torch.Tensor, R: torch.Tensor, mean: torch.Tensor, inverse: bool = False) -> torch.Tensor:
+    n, D = X.shape
+    out = torch.empty((n, D), dtype=F64, device=X.device)
+    native.da_rotate(P(X), is_f32(X), n, X.stride(0), D, P(R), P(mean), P(out), int(inverse), stream())
+    return out
+
+
+def improved_kmeans(X: torch.Tensor, C0: torch.Tensor, schedule, max_iters: int, comm=None):
+    """Staged k-means in PCA space.  Returns (points f64, labels int32, trace)."""
+    D = X.shape[1]
+    if schedule[-1] != D:
+        raise ValueError(f"schedule must end at d={D}, got {schedule}")
+    R, mean, _, _ = pca(X, comm)
+    Xr = rotate(X, R, mean)
+    Cr = rotate(C0, R, mean)
+    trace = []
+    for dims in schedule:
+        Cr, _, trace = lloyd(Xr, Cr, dims, max_iters, comm)
+    del Xr
+    C = rotate(Cr, R, mean, inverse=True)
+    final_labels, final_errs = assign(X, D, C)
+    init_labels, init_errs = assign(X, D, C0)
+    fm = np_mean(final_errs, comm)
+    im = np_mean(init_errs, comm)
+    both = torch.cat([fm, im]).cpu().numpy()
+    if both[0] <= both[1]:
+        return C, final_labels, trace
+    return C0.clone(), init_labels, [float(both[1])]
+
+
+def check_k(n: int, K: int):
+    if K > n:
+        raise ValueError(f"k={K} exceeds the number of points n={n}")
+
+
+# ---------------------------------------------------------------------------
+# codebook-side kernels
+
+
+def einsum_sq(cw: torch.Tensor) -> torch.Tensor:
+    M, K, D = cw.shape
+    out = torch.empty((M, K), dtype=F64, device=cw.device)
+    native.da_einsum_sq(P(cw), M * K, D, P(out), stream())
+    return out
+
+
+def cross_full(cw: torch.Tensor):
+    M, K, D = cw.shape
+    Pt = torch.empty((M, M, K, K), dtype=F64, device=cw.device)
+    sq = torch.empty((M, K), dtype=F64, device=cw.device)
+    native.da_cross_products(P(cw), M, K, D, -1, P(Pt), P(sq), stream())
+    return Pt, sq
+
+
+def cross_refresh(cw: torch.Tensor, m: int, Pt: torch.Tensor, sq: torch.Tensor):
+    """In-place refresh of the rows/cols of dictionary m."""
+    M, K, D = cw.shape
+    native.da_cross_products(P(cw), M, K, D, m, P(Pt), P(sq), stream())
+
+
+def heat_up(X: torch.Tensor, codes: torch.Tensor, cw: torch.Tensor, m: int) -> torch.Tensor:
+    n, D = X.shape
+    M, K, _ = cw.shape
+    out = torch.empty((n, D), dtype=F32, device=X.device)
+    native.da_heat_up(P(X), n, D, P(codes), P(cw), M, K, m, P(out), stream())
+    return out
+
+
+def vec_err(X: torch.Tensor, codes: torch.Tensor, cw: torch.Tensor) -> torch.Tensor:
+    n, D = X.shape
+    M, K, _ = cw.shape
+    err = torch.empty(n, dtype=F64, device=X.device)
+    native.da_vec_err(P(X), is_f32(X), n, X.stride(0), D, P(codes), code_bytes(codes), codes.stride(0), P(cw),
+                      M, K, P(err), stream())
+    return err
+
+
+def reconstruct(codes: torch.Tensor, cw: torch.Tensor) -> torch.Tensor:
+    n = codes.shape[0]
+    M, K, D = cw.shape
+    out = torch.empty((n, D), dtype=F64, device=cw.device)
+    native.da_reconstruct(P(codes), code_bytes(codes), n, codes.stride(0), P(cw), M, K, D, P(out), stream())
+    return out
+
+
+def encode(X: torch.Tensor, cw: torch.Tensor, sq: torch.Tensor, Pt: torch.Tensor, L: int,
+           out_dtype=I32, with_err: bool = True):
+    """Beam encode (codebook.py:264-300).  Returns (codes (n,M), err f64 | None)."""
+    n, D = X.shape
+    M, K, _ = cw.shape
+    codes = torch.empty((n, M), dtype=out_dtype, device=X.device)
+    err = torch.empty(n, dtype=F64, device=X.device) if with_err else None
+    native.da_encode(P(X), is_f32(X), n, X.stride(0), D, P(cw), M, K, int(L), P(sq), P(Pt), P(codes),
+                     code_bytes(codes), codes.stride(0), P(err), stream())
+    return codes, err
+
+
+def pair_sums(codes: torch.Tensor, Pt: torch.Tensor) -> torch.Tensor:
+    n, M = codes.shape
+    K = Pt.shape[2]
+    out = torch.empty(n, dtype=F64, device=codes.device)
+    native.da_pair_sums(P(codes), code_bytes(codes), n, codes.stride(0), P(Pt), M, K, P(out), stream())
+    return out
+
+
+def adc_lut(Q: torch.Tensor, cw: torch.Tensor, sq: torch.Tensor):
+    nq, D = Q.shape
+    M, K, _ = cw.shape
+    lut = torch.empty((nq, M, K), dtype=F64, device=Q.device)
+    qsq = torch.empty(nq, dtype=F64, device=Q.device)
+    native.da_adc_lut(P(Q), nq, D, P(cw), M, K, P(sq), P(lut), P(qsq), stream())
+    return lut, qsq
+
+
+def adc_scan(codes: torch.Tensor, pair: torch.Tensor, lut: torch.Tensor, qsq: torch.Tensor, r: int,
+             cand: torch.Tensor | None = None):
+    nq, M, K = lut.shape
+    ncand = cand.shape[1] if cand is not None else codes.shape[0]
+    ids = torch.empty((nq, r), dtype=I64, device=lut.device)
+    dists = torch.empty((nq, r), dtype=F64, device=lut.device)
+    native.da_adc_scan(P(codes), code_bytes(codes), codes.stride(0), P(pair), P(cand), ncand, nq, P(lut),
+                       P(qsq), M, K, int(r), P(ids), P(dists), stream())
+    return ids, dists
+
+
+# ---------------------------------------------------------------------------
+# DA training on device (annq/annealing.py:115-262)
+
+
+def dimension_schedule(d: int, i_count: int = 10) -> list[int]:
+    """annq/clustering.py:116-131 (pure integer bookkeeping)."""
+    import math
+
+    if d < 1 or i_count < 1:
+        raise ValueError("d and i_count must be >= 1")
+    dims: list[int] = []
+    for i in range(1, i_count + 1):
+        v = min(d, math.ceil(d ** (i / i_count)))
+        if not dims or v > dims[-1]:
+            dims.append(v)
+    if dims[-1] != d:
+        dims.append(d)
+    return dims
+
+
+def cool_down(inter: torch.Tensor, C0_f32: torch.Tensor, config, comm=None):
+    """annealing.py:115-126: (new dictionary f32 (K,D), assignment int32)."""
+    D = inter.shape[1]
+    schedule = dimension_schedule(D, config.schedule_stages)
+    n_total = comm.total(inter.shape[0]) if comm is not None else inter.shape[0]
+    check_k(n_total, C0_f32.shape[0])
+    pts, labels, _ = improved_kmeans(inter, C0_f32.to(F64), schedule, config.kmeans_iters, comm)
+    return pts.to(F32), labels
+
+
+class StepTimer:
+    def __init__(self):
+        import time
+
+        self._t = time.perf_counter
+        self.t0 = self._t()
+
+    def seconds(self):
+        return self._t() - self.t0
+
+
+def dict_step(X, cw, codes, Pt, sq, m, config, comm=None):
+    """One heat-up / cool-down / re-encode step of da_sweep (annealing.py:162-178).
+
+    Updates cw, codes and the cross table (Pt, sq = its sq_norms) in place;
+    returns the step distortion (float).
+    """
+    inter = heat_up(X, codes, cw, m)
+    new_dict, assign_m = cool_down(inter, cw[m], config, comm)
+    del inter
+    cw[m] = new_dict
+    cross_refresh(cw, m, Pt, sq)
+    incumbent = codes.clone()
+    native.da_set_column(P(incumbent), incumbent.shape[0], incumbent.shape[1], m, P(assign_m), stream())
+    # beam tables use einsum norms of the current codebook (codebook.py:260)
+    beam_codes, beam_err = encode(X, cw, einsum_sq(cw), Pt, config.beam_width)
+    inc_err = vec_err(X, incumbent, cw)
+    native.da_select_better(X.shape[0], codes.shape[1], P(beam_codes), P(beam_err), P(incumbent), P(inc_err),
+                            stream())
+    codes.copy_(incumbent)
+    return float(np_mean(inc_err, comm).item())
+
+
+def growth_pass(X, config, report=None, comm=None):
+    """annealing.py:184-205 (all-zero start, greedy residual cool-downs)."""
+    n, D = X.shape
+    M, K = config.m_count, config.k_count
+    cw = torch.zeros((M, K, D), dtype=F32, device=X.device)
+    codes = torch.zeros((n, M), dtype=I32, device=X.device)
+    for m in range(M):
+        t = StepTimer()
+        inter = heat_up(X, codes, cw, m)
+        new_dict, assign_m = cool_down(inter, cw[m], config, comm)
+        del inter
+        cw[m] = new_dict
+        native.da_set_column(P(codes), n, M, m, P(assign_m), stream())
+        if report is not None:
+            dist = float(np_mean(vec_err(X, codes, cw), comm).item())
+            report.record(0, m, dist, t.seconds())
+    return cw, codes
+
+
+def da_sweep(X, cw, codes, Pt, sq, config, sweep_index=1, report=None, comm=None):
+    """annealing.py:140-181 on device state (mutated in place)."""
+    for m in range(cw.shape[0]):
+        t = StepTimer()
+        dist = dict_step(X, cw, codes, Pt, sq, m, config, comm)
+        if report is not None:
+            report.record(sweep_index, m, dist, t.seconds())
+
+
+def sweep_until_converged(X, cw, codes, config, report, comm=None):
+    """annealing.py:208-222."""
+    Pt, sq = cross_full(cw)
+    prev = float(np_mean(vec_err(X, codes, cw), comm).item())
+    for s in range(1, config.sweeps + 1):
+        da_sweep(X, cw, codes, Pt, sq, config, sweep_index=s, report=report, comm=comm)
+        cur = report.steps[-1].distortion if report is not None and report.steps else prev
+        if prev > 0 and (prev - cur) / prev < config.rel_tol:
+            break
+        prev = cur
+    return Pt, sq

@@ -1,0 +1,304 @@
+// C-ABI of the DA hot path (declared in include/da_b200.h).
+//
+// Conventions: every pointer is a device pointer allocated by the caller
+// (the library never frees caller memory); `stream` is a cudaStream_t passed
+// as void*; calls are asynchronous on that stream.  Return value 0 = OK,
+// < 0 = invalid argument (Python raises ValueError), > 0 = CUDA error
+// (RuntimeError); da_last_error() returns the thread's last message.
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <map>
+#include <mutex>
+#include <string>
+
+#include "../../include/da_b200.h"
+#include "common.cuh"
+#include "internal.h"
+
+namespace da {
+
+static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail_arg(const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    set_error(buf);
+    return -1;
+}
+
+int fail_cuda(cudaError_t e, const char* where) {
+    set_error(std::string(where) + ": " + cudaGetErrorString(e));
+    return (int)e > 0 ? (int)e : 1;
+}
+
+static std::mutex g_scratch_mu;
+static std::map<std::pair<int, int>, Scratch> g_scratch;
+
+void* scratch(int slot, size_t bytes, cudaStream_t stream) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(g_scratch_mu);
+    Scratch& s = g_scratch[{dev, slot}];
+    if (s.bytes >= bytes && s.ptr) return s.ptr;
+    if (s.ptr) {
+        cudaStreamSynchronize(stream);
+        cudaFree(s.ptr);
+        s.ptr = nullptr;
+        s.bytes = 0;
+    }
+    size_t want = bytes < 256 ? 256 : bytes;
+    want = want + want / 8;  // headroom so slightly larger calls do not reallocate
+    if (cudaMalloc(&s.ptr, want) != cudaSuccess) {
+        cudaGetLastError();
+        s.ptr = nullptr;
+        return nullptr;
+    }
+    s.bytes = want;
+    return s.ptr;
+}
+
+}  // namespace da
+
+using namespace da;
+
+#define STREAM(s) ((cudaStream_t)(s))
+
+extern "C" {
+
+const char* da_last_error(void) { return g_last_error.c_str(); }
+
+int da_version(void) { return DA_B200_ABI_VERSION; }
+
+long long da_launch_count(void) { return g_launches.load(); }
+
+int da_release_scratch(void) {
+    std::lock_guard<std::mutex> g(g_scratch_mu);
+    for (auto& kv : g_scratch)
+        if (kv.second.ptr) cudaFree(kv.second.ptr);
+    g_scratch.clear();
+    return 0;
+}
+
+int da_row_sqnorms(const void* A, int a_f32, int64_t rows, int64_t lda, int d, double* out, void* stream) {
+    if (rows < 0 || d < 0 || lda < d) return fail_arg("row_sqnorms: bad shape rows=%lld d=%d lda=%lld", (long long)rows, d, (long long)lda);
+    return launch_row_sqnorms(A, a_f32, rows, lda, d, out, STREAM(stream));
+}
+
+int da_assign(const void* X, int x_f32, int64_t n, int64_t ldx, int d, const double* C, int64_t ldc, int K,
+              const double* cc, int32_t* labels, double* d2, const int32_t* prev, unsigned long long* changed,
+              void* stream) {
+    if (n < 0 || K < 1 || d < 1 || ldx < d || ldc < d)
+        return fail_arg("assign: bad shape n=%lld K=%d d=%d", (long long)n, K, d);
+    return launch_assign(X, x_f32, n, ldx, d, C, ldc, K, cc, labels, d2, prev, changed, STREAM(stream));
+}
+
+int da_group_sums(const double* X, int64_t n, int64_t ldx, int D, const int32_t* labels, int K, int mode,
+                  double* out, int64_t ldo, int32_t* counts, void* stream) {
+    if (n < 0 || K < 1 || D < 1 || ldx < D || ldo < D || (mode != 0 && mode != 1))
+        return fail_arg("group_sums: bad arguments n=%lld K=%d D=%d mode=%d", (long long)n, K, D, mode);
+    if (n >= (1LL << 31)) return fail_arg("group_sums: n=%lld exceeds int32 row ids", (long long)n);
+    if (n == 0) {
+        if (counts) cudaMemsetAsync(counts, 0, sizeof(int32_t) * K, STREAM(stream));
+        return 0;
+    }
+    return launch_group_sums(X, n, ldx, D, labels, K, mode, out, ldo, counts, STREAM(stream));
+}
+
+int da_label_order(const int32_t* labels, int64_t n, int K, int32_t* order, int32_t* counts, void* stream) {
+    if (n < 0 || K < 1) return fail_arg("label_order: bad arguments");
+    if (n >= (1LL << 31)) return fail_arg("label_order: n too large");
+    return launch_label_order(labels, n, K, order, counts, STREAM(stream));
+}
+
+int da_gather_rows(const double* X, int64_t ldx, int D, const int64_t* src, const int32_t* dst, int cnt, double* C,
+                   int64_t ldc, void* stream) {
+    return launch_gather_rows(X, ldx, D, (const long long*)src, dst, cnt, C, ldc, STREAM(stream));
+}
+
+int da_heat_up(const float* X, int64_t n, int D, const int32_t* codes, const float* cw, int M, int K, int m,
+               float* out, void* stream) {
+    if (m < 0 || m >= M) return fail_arg("dictionary index %d out of range [0, %d)", m, M);
+    return launch_heat_up(X, n, D, codes, cw, M, K, m, out, STREAM(stream));
+}
+
+int da_vec_err(const void* X, int x_f32, int64_t n, int64_t ldx, int D, const void* codes, int code_bytes,
+               int64_t ldc, const float* cw, int M, int K, double* err, void* stream) {
+    if (code_bytes != 1 && code_bytes != 2 && code_bytes != 4) return fail_arg("code_bytes must be 1, 2 or 4");
+    return launch_vec_err(X, x_f32, n, ldx, D, codes, code_bytes, ldc, cw, M, K, err, STREAM(stream));
+}
+
+int da_reconstruct(const void* codes, int code_bytes, int64_t n, int64_t ldc, const float* cw, int M, int K, int D,
+                   double* out, void* stream) {
+    if (code_bytes != 1 && code_bytes != 2 && code_bytes != 4) return fail_arg("code_bytes must be 1, 2 or 4");
+    return launch_reconstruct(codes, code_bytes, n, ldc, cw, M, K, D, out, STREAM(stream));
+}
+
+int da_col_mean(const void* X, int x_f32, int64_t n, int64_t ld, int D, double* mean, void* stream) {
+    return launch_col_mean(X, x_f32, n, ld, D, mean, STREAM(stream));
+}
+
+int da_pca_cov(const void* X, int x_f32, int64_t n, int64_t ld, int D, const double* mean, double* cov, void* stream) {
+    if (n < 2) return fail_arg("PCA needs at least 2 vectors, got %lld", (long long)n);
+    // split the n-long reduction so the grid covers the machine
+    const long long tiles = ((D + 63) / 64) * (long long)((D + 63) / 64);
+    long long ks = (148LL * 4 + tiles - 1) / tiles;
+    ks = std::max(1LL, std::min(ks, std::min(64LL, (long long)n / 256 + 1)));
+    const long long kchunk = ((long long)n + ks - 1) / ks;
+    double* part = (double*)scratch(5, sizeof(double) * (size_t)ks * D * D, STREAM(stream));
+    if (!part) return fail_cuda(cudaErrorMemoryAllocation, "pca_cov scratch");
+    GemmArgs g{};
+    g.A = X; g.a_f32 = x_f32; g.sai = 1; g.sak = ld; g.asub = mean; g.asub_mode = 1;
+    g.B = X; g.b_f32 = x_f32; g.sbk = ld; g.sbj = 1; g.bsub = mean; g.bsub_mode = 2;
+    g.C = part; g.sci = D; g.scj = 1; g.sCz = (long long)D * D;
+    g.M = D; g.N = D; g.K = n; g.nb2 = 1; g.ksplit = (int)ks; g.kchunk = kchunk; g.epi = 0;
+    int rc = launch_gemm(g, 1, STREAM(stream));
+    if (rc) return rc;
+    return launch_reduce_partials(part, (int)ks, (long long)D * D, (double)(n - 1), cov, STREAM(stream));
+}
+
+int da_rotate(const void* X, int x_f32, int64_t n, int64_t ld, int D, const double* R, const double* mean,
+              double* out, int inverse, void* stream) {
+    GemmArgs g{};
+    g.A = X; g.a_f32 = x_f32; g.sai = ld; g.sak = 1;
+    g.B = R; g.b_f32 = 0;
+    g.C = out; g.sci = D; g.scj = 1;
+    g.M = n; g.N = D; g.K = D; g.nb2 = 1; g.ksplit = 1; g.kchunk = D;
+    if (!inverse) {
+        // (X - mean) @ R^T : b(k, j) = R[j, k]
+        g.asub = mean; g.asub_mode = 2; g.sbk = 1; g.sbj = D; g.epi = 0;
+    } else {
+        // Y @ R + mean : b(k, j) = R[k, j]
+        g.sbk = D; g.sbj = 1; g.epi = 1; g.evec = mean;
+    }
+    // chunk rows to respect the grid.y limit
+    const long long rows_per = 65535LL * 64;
+    for (long long r0 = 0; r0 < n; r0 += rows_per) {
+        GemmArgs h = g;
+        h.M = std::min(rows_per, (long long)n - r0);
+        h.A = x_f32 ? (const void*)((const float*)X + r0 * ld) : (const void*)((const double*)X + r0 * ld);
+        h.C = out + r0 * D;
+        int rc = launch_gemm(h, 1, STREAM(stream));
+        if (rc) return rc;
+    }
+    return 0;
+}
+
+int da_gemm_strided(const void* A, int a_f32, int64_t sai, int64_t sak, const void* B, int b_f32, int64_t sbk,
+                    int64_t sbj, double* C, int64_t sci, int64_t scj, int64_t M, int64_t N, int64_t K, void* stream) {
+    if (M < 0 || N < 0 || K < 0) return fail_arg("gemm: negative shape");
+    if (K == 0) {
+        // empty contraction: zeros
+        for (long long i = 0; i < M; ++i)
+            for (long long j = 0; j < N; ++j) cudaMemsetAsync(C + i * sci + j * scj, 0, sizeof(double), STREAM(stream));
+        return 0;
+    }
+    GemmArgs g{};
+    g.A = A; g.a_f32 = a_f32; g.sai = sai; g.sak = sak;
+    g.B = B; g.b_f32 = b_f32; g.sbk = sbk; g.sbj = sbj;
+    g.C = C; g.sci = sci; g.scj = scj;
+    g.M = M; g.N = N; g.K = K; g.nb2 = 1; g.ksplit = 1; g.kchunk = K; g.epi = 0;
+    return launch_gemm(g, 1, STREAM(stream));
+}
+
+int da_einsum_sq(const float* cw, int64_t rows, int D, double* out, void* stream) {
+    return launch_einsum_sq(cw, rows, D, out, STREAM(stream));
+}
+
+int da_cross_products(const float* cw, int M, int K, int D, int only_m, double* P, double* sq, void* stream) {
+    if (M < 1 || K < 1 || D < 1) return fail_arg("cross_products: bad shape");
+    cudaStream_t s = STREAM(stream);
+    // P[a][b][i][j] = c_a(i) . c_b(j)
+    GemmArgs g{};
+    g.A = cw; g.a_f32 = 1; g.sai = D; g.sak = 1;
+    g.B = cw; g.b_f32 = 1; g.sbk = 1; g.sbj = D;
+    g.C = P; g.sci = K; g.scj = 1;
+    g.M = K; g.N = K; g.K = D; g.ksplit = 1; g.kchunk = D; g.epi = 0;
+    if (only_m < 0) {
+        g.sA1 = (long long)K * D; g.sA2 = 0;
+        g.sB1 = 0; g.sB2 = (long long)K * D;
+        g.sC1 = (long long)M * K * K; g.sC2 = (long long)K * K;
+        g.nb2 = M;
+        int rc = launch_gemm(g, M, s);
+        if (rc) return rc;
+        return sq ? launch_einsum_sq(cw, (long long)M * K, D, sq, s) : 0;
+    }
+    if (only_m >= M) return fail_arg("refresh index %d out of range", only_m);
+    // rows a = m (all b) and columns b = m (all a)
+    GemmArgs r = g;
+    r.A = cw + (size_t)only_m * K * D; r.sA1 = 0; r.sA2 = 0;
+    r.sB1 = 0; r.sB2 = (long long)K * D;
+    r.C = P + (size_t)only_m * M * K * K; r.sC1 = 0; r.sC2 = (long long)K * K;
+    r.nb2 = M;
+    int rc = launch_gemm(r, 1, s);
+    if (rc) return rc;
+    GemmArgs c = g;
+    c.sA1 = 0; c.sA2 = (long long)K * D;
+    c.B = cw + (size_t)only_m * K * D; c.sB1 = 0; c.sB2 = 0;
+    c.C = P + (size_t)only_m * K * K; c.sC1 = 0; c.sC2 = (long long)M * K * K;
+    c.nb2 = M;
+    rc = launch_gemm(c, 1, s);
+    if (rc) return rc;
+    // refresh_cross_products rebuilds sq[m] as a pairwise row sum (codebook.py:251)
+    return sq ? launch_row_sqnorms(cw + (size_t)only_m * K * D, 1, K, D, D, sq + (size_t)only_m * K, s) : 0;
+}
+
+int da_encode(const void* X, int x_f32, int64_t n, int64_t ldx, int D, const float* cw, int M, int K, int L,
+              const double* sq, const double* P, void* codes, int code_bytes, int64_t ldcodes, double* err,
+              void* stream) {
+    if (L < 1) return fail_arg("beam_width must be >= 1");
+    if (code_bytes != 1 && code_bytes != 2 && code_bytes != 4) return fail_arg("code_bytes must be 1, 2 or 4");
+    if (M < 1 || K < 1 || D < 1) return fail_arg("encode: bad codebook shape");
+    return launch_encode(X, x_f32, n, ldx, D, cw, M, K, L, sq, P, codes, code_bytes, ldcodes, err, STREAM(stream));
+}
+
+int da_pair_sums(const void* codes, int code_bytes, int64_t n, int64_t ldc, const double* P, int M, int K, double* out,
+                 void* stream) {
+    if (code_bytes != 1 && code_bytes != 2 && code_bytes != 4) return fail_arg("code_bytes must be 1, 2 or 4");
+    return launch_pair_sums(codes, code_bytes, n, ldc, P, M, K, out, STREAM(stream));
+}
+
+int da_adc_lut(const double* Q, int64_t nq, int D, const float* cw, int M, int K, const double* sq, double* lut,
+               double* qsq, void* stream) {
+    cudaStream_t s = STREAM(stream);
+    int rc = launch_qsq(Q, nq, D, qsq, s);
+    if (rc) return rc;
+    GemmArgs g{};
+    g.A = Q; g.a_f32 = 0; g.sai = D; g.sak = 1;
+    g.B = cw; g.b_f32 = 1; g.sbk = 1; g.sbj = D;
+    g.C = lut; g.sci = (long long)M * K; g.scj = 1;
+    g.M = nq; g.N = (long long)M * K; g.K = D; g.nb2 = 1; g.ksplit = 1; g.kchunk = D;
+    g.epi = 3; g.evec = sq; g.ivec = qsq;
+    return launch_gemm(g, 1, s);
+}
+
+int da_adc_scan(const void* codes, int code_bytes, int64_t ldc, const double* pair, const int64_t* cand,
+                int64_t ncand, int64_t nq, const double* lut, const double* qsq, int M, int K, int r, int64_t* ids,
+                double* dists, void* stream) {
+    if (code_bytes != 1 && code_bytes != 2 && code_bytes != 4) return fail_arg("code_bytes must be 1, 2 or 4");
+    return launch_adc_scan(codes, code_bytes, ldc, pair, (const long long*)cand, ncand, nq, lut, qsq, M, K, r,
+                           (long long*)ids, dists, STREAM(stream));
+}
+
+int da_np_sum(const double* a, int64_t n, int divide, double* out, void* stream) {
+    return launch_np_sum(a, n, divide, out, STREAM(stream));
+}
+
+int da_select_better(int64_t n, int M, const int32_t* beam_codes, const double* beam_err, int32_t* inc_codes,
+                     double* inc_err, void* stream) {
+    return launch_select_better(n, M, beam_codes, beam_err, inc_codes, inc_err, STREAM(stream));
+}
+
+int da_set_column(int32_t* codes, int64_t n, int M, int m, const int32_t* labels, void* stream) {
+    return launch_set_column(codes, n, M, m, labels, STREAM(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,415 @@
+// Lloyd update: per-codeword sums / means over ALL coordinates.
+//
+// Follows annq/clustering.py:151-162 (`_group_means`):
+//   order = argsort(labels, stable); counts = bincount(labels)
+//   sums  = add.reduceat(X[order], segment starts, axis=0)
+//   means = sums / max(counts, 1)
+// numpy's reduceat along axis 0 evaluates each segment as
+//   row[first] + pairwise_sum(rows[first+1 : end])       (per column)
+// so this file reproduces it bit-for-bit:
+//   1. stable counting sort of the labels (tile histograms -> exclusive scan
+//      -> one warp per tile scatters row ids with __match_any_sync ranks);
+//   2. the pairwise recursion of every segment is expanded into its <=128-row
+//      leaves, one warp per (leaf, 128-column chunk) sums its rows with the
+//      8-accumulator leaf rule, rows gathered through the sorted order with
+//      fully coalesced 1 KB row reads;
+//   3. one warp per (codeword, column chunk) folds the leaf sums back up the
+//      same recursion, adds the first row, and divides by the count.
+// The result is deterministic (no float atomics) and equal to the reference.
+#include "common.cuh"
+#include "internal.h"
+
+namespace da {
+
+namespace {
+constexpr int GS_TILE = 1024;      // rows per sort tile
+constexpr int GS_SMEM_HIST = 12288; // labels that fit a shared-memory histogram
+constexpr int GS_COLS = 128;       // columns per warp task (4 per lane)
+}  // namespace
+
+__global__ void tile_hist_kernel(const int32_t* __restrict__ labels, long long n, int K, int T,
+                                 int32_t* __restrict__ hist) {
+    extern __shared__ int32_t sh[];
+    const int t = blockIdx.x;
+    const long long lo = (long long)t * GS_TILE;
+    const long long hi = min(n, lo + GS_TILE);
+    const bool use_smem = K <= GS_SMEM_HIST;
+    if (use_smem) {
+        for (int k = threadIdx.x; k < K; k += blockDim.x) sh[k] = 0;
+        __syncthreads();
+        for (long long r = lo + threadIdx.x; r < hi; r += blockDim.x) atomicAdd(&sh[labels[r]], 1);
+        __syncthreads();
+        for (int k = threadIdx.x; k < K; k += blockDim.x) hist[(long long)k * T + t] = sh[k];
+    } else {
+        for (long long r = lo + threadIdx.x; r < hi; r += blockDim.x)
+            atomicAdd(&hist[(long long)labels[r] * T + t], 1);
+    }
+}
+
+// Single-block exclusive scan of len int32 values (in place); out_total gets the sum.
+__global__ void exclusive_scan_kernel(int32_t* __restrict__ a, long long len, int32_t* __restrict__ out_total) {
+    __shared__ long long warp_sums[32];
+    const int nt = blockDim.x;
+    const long long chunk = (len + nt - 1) / nt;
+    const long long lo = min(len, (long long)threadIdx.x * chunk);
+    const long long hi = min(len, lo + chunk);
+    long long s = 0;
+    for (long long i = lo; i < hi; ++i) s += a[i];
+    // block exclusive scan of s
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    long long incl = s;
+    for (int off = 1; off < 32; off <<= 1) {
+        long long v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += v;
+    }
+    if (lane == 31) warp_sums[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        long long w = (lane < (nt >> 5)) ? warp_sums[lane] : 0;
+        long long wi = w;
+        for (int off = 1; off < 32; off <<= 1) {
+            long long v = __shfl_up_sync(0xffffffffu, wi, off);
+            if (lane >= off) wi += v;
+        }
+        if (lane < (nt >> 5)) warp_sums[lane] = wi - w;
+        if (lane == (nt >> 5) - 1 && out_total) *out_total = (int32_t)wi;
+    }
+    __syncthreads();
+    long long run = warp_sums[wid] + incl - s;
+    for (long long i = lo; i < hi; ++i) {
+        long long v = a[i];
+        a[i] = (int32_t)run;
+        run += v;
+    }
+}
+
+__global__ void seg_counts_kernel(const int32_t* __restrict__ offs, int K, int T, long long n,
+                                  int32_t* __restrict__ seg_start, int32_t* __restrict__ counts) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    int s = offs[(long long)k * T];
+    int e = (k + 1 < K) ? offs[(long long)(k + 1) * T] : (int)n;
+    seg_start[k] = s;
+    counts[k] = e - s;
+}
+
+// One warp per tile: stable scatter of row ids into their label segment.
+__global__ void stable_scatter_kernel(const int32_t* __restrict__ labels, long long n, int T,
+                                      int32_t* __restrict__ cursor, int32_t* __restrict__ order) {
+    const int t = blockIdx.x;
+    const int lane = threadIdx.x;
+    const long long lo = (long long)t * GS_TILE;
+    const long long hi = min(n, lo + GS_TILE);
+    const unsigned lt_mask = (1u << lane) - 1u;
+    for (long long base = lo; base < hi; base += 32) {
+        long long r = base + lane;
+        bool valid = r < hi;
+        unsigned active = __ballot_sync(0xffffffffu, valid);
+        if (valid) {
+            int lab = labels[r];
+            unsigned peers = __match_any_sync(active, lab);
+            int leader = __ffs(peers) - 1;
+            int rank = __popc(peers & lt_mask);
+            int b = 0;
+            long long slot = (long long)lab * T + t;
+            if (lane == leader) b = cursor[slot];
+            b = __shfl_sync(peers, b, leader);
+            order[b + rank] = (int32_t)r;
+            if (lane == leader) cursor[slot] = b + __popc(peers);
+        }
+        __syncwarp();
+    }
+}
+
+// ---- pairwise recursion bookkeeping ----------------------------------------
+
+__device__ long long pw_leaf_count(long long m) {
+    if (m <= 0) return 0;
+    if (m <= 128) return 1;
+    // iterative: count leaves of the recursion
+    long long st[64];
+    int sp = 0;
+    long long c = 0;
+    st[sp++] = m;
+    while (sp) {
+        long long x = st[--sp];
+        if (x <= 128) { ++c; continue; }
+        long long n2 = x / 2; n2 -= n2 % 8;
+        st[sp++] = x - n2;
+        st[sp++] = n2;
+    }
+    return c;
+}
+
+__global__ void leaf_count_kernel(const int32_t* __restrict__ counts, int K, int32_t* __restrict__ nleaf) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    int c = counts[k];
+    nleaf[k] = (int32_t)pw_leaf_count(c >= 2 ? c - 1 : 0);
+}
+
+// Per codeword: enumerate the leaves of pairwise(rest) in left-to-right order.
+__global__ void leaf_enum_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ seg_start,
+                                 const int32_t* __restrict__ leaf_base, int K,
+                                 int4* __restrict__ leaves) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    int c = counts[k];
+    if (c < 2) return;
+    long long m = c - 1;
+    int out = leaf_base[k];
+    const int rest0 = seg_start[k] + 1;
+    long long st_lo[64], st_n[64];
+    int sp = 0;
+    st_lo[sp] = 0; st_n[sp] = m; ++sp;
+    while (sp) {
+        --sp;
+        long long lo = st_lo[sp], x = st_n[sp];
+        if (x <= 128) {
+            leaves[out++] = make_int4(k, rest0 + (int)lo, (int)x, 0);
+            continue;
+        }
+        long long n2 = x / 2; n2 -= n2 % 8;
+        // push right first so the left leaf is emitted first
+        st_lo[sp] = lo + n2; st_n[sp] = x - n2; ++sp;
+        st_lo[sp] = lo; st_n[sp] = n2; ++sp;
+    }
+}
+
+// One warp per (leaf, 128-column chunk): numpy pairwise leaf over gathered rows.
+__global__ void leaf_sum_kernel(const double* __restrict__ X, long long ldx, int D,
+                                const int32_t* __restrict__ order, const int4* __restrict__ leaves,
+                                const int32_t* __restrict__ n_leaves_total, int n_chunks,
+                                double* __restrict__ leaf_sums) {
+    const int lane = threadIdx.x & 31;
+    const long long task = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const long long total = (long long)(*n_leaves_total) * n_chunks;
+    if (task >= total) return;
+    const long long leaf = task / n_chunks;
+    const int chunk = (int)(task % n_chunks);
+    const int4 L = leaves[leaf];
+    const int start = L.y, n = L.z;
+    int cols[4];
+    bool ok[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { cols[q] = chunk * GS_COLS + lane + 32 * q; ok[q] = cols[q] < D; }
+    auto val = [&](int i, int q) -> double {
+        long long r = order[start + i];
+        return ok[q] ? X[r * ldx + cols[q]] : 0.0;
+    };
+    double res[4];
+    if (n < 8) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) res[q] = 0.0;
+        for (int i = 0; i < n; ++i) {
+            long long r = order[start + i];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) res[q] = dadd(res[q], ok[q] ? X[r * ldx + cols[q]] : 0.0);
+        }
+    } else {
+        double acc[8][4];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            long long r = order[start + j];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[j][q] = ok[q] ? X[r * ldx + cols[q]] : 0.0;
+        }
+        int i = 8;
+        const int stop = n - (n % 8);
+        for (; i < stop; i += 8) {
+            long long rr[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) rr[j] = order[start + i + j];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[j][q] = dadd(acc[j][q], ok[q] ? X[rr[j] * ldx + cols[q]] : 0.0);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            res[q] = dadd(dadd(dadd(acc[0][q], acc[1][q]), dadd(acc[2][q], acc[3][q])),
+                          dadd(dadd(acc[4][q], acc[5][q]), dadd(acc[6][q], acc[7][q])));
+        for (; i < n; ++i) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) res[q] = dadd(res[q], val(i, q));
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        if (ok[q]) leaf_sums[leaf * D + cols[q]] = res[q];
+}
+
+// One warp per (codeword, column chunk): fold leaves up the recursion tree,
+// prepend the first row, divide by the count.  mode 0 = write means into the
+// filled rows of C (empties untouched); mode 1 = write raw sums (all rows).
+__global__ void seg_finish_kernel(const double* __restrict__ X, long long ldx, int D,
+                                  const int32_t* __restrict__ order, const int32_t* __restrict__ counts,
+                                  const int32_t* __restrict__ seg_start, const int32_t* __restrict__ leaf_base,
+                                  const double* __restrict__ leaf_sums, int K, int n_chunks, int mode,
+                                  double* __restrict__ out, long long ldo) {
+    const int lane = threadIdx.x & 31;
+    const long long task = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (task >= (long long)K * n_chunks) return;
+    const int k = (int)(task / n_chunks);
+    const int chunk = (int)(task % n_chunks);
+    const int c = counts[k];
+    if (c == 0) {
+        if (mode == 1) {
+            for (int q = 0; q < 4; ++q) {
+                int col = chunk * GS_COLS + lane + 32 * q;
+                if (col < D) out[(long long)k * ldo + col] = 0.0;
+            }
+        }
+        return;
+    }
+    const long long first = order[seg_start[k]];
+    double tot[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        int col = chunk * GS_COLS + lane + 32 * q;
+        tot[q] = (col < D) ? X[first * ldx + col] : 0.0;
+    }
+    if (c >= 2) {
+        const long long m = c - 1;
+        // post-order walk; all lanes follow the same shape
+        long long st_n[64];
+        int st_state[64];
+        double st_left[64][4];
+        int sp = 0;
+        st_n[0] = m; st_state[0] = 0;
+        long long leaf = leaf_base[k];
+        double ret[4] = {0.0, 0.0, 0.0, 0.0};
+        while (sp >= 0) {
+            long long x = st_n[sp];
+            if (x <= 128) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    int col = chunk * GS_COLS + lane + 32 * q;
+                    ret[q] = (col < D) ? leaf_sums[leaf * D + col] : 0.0;
+                }
+                ++leaf;
+                --sp;
+                while (sp >= 0) {
+                    if (st_state[sp] == 1) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) st_left[sp][q] = ret[q];
+                        st_state[sp] = 2;
+                        long long n2 = st_n[sp] / 2; n2 -= n2 % 8;
+                        ++sp;
+                        st_n[sp] = st_n[sp - 1] - n2; st_state[sp] = 0;
+                        break;
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) ret[q] = dadd(st_left[sp][q], ret[q]);
+                        --sp;
+                    }
+                }
+                continue;
+            }
+            long long n2 = x / 2; n2 -= n2 % 8;
+            st_state[sp] = 1;
+            ++sp;
+            st_n[sp] = n2; st_state[sp] = 0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) tot[q] = dadd(tot[q], ret[q]);
+    }
+    const double cnt = (double)c;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        int col = chunk * GS_COLS + lane + 32 * q;
+        if (col < D) out[(long long)k * ldo + col] = (mode == 0) ? __ddiv_rn(tot[q], cnt) : tot[q];
+    }
+}
+
+// Host driver.  X: (n, D) float64 rows (leading dim ldx); labels int32 in [0,K).
+// Writes counts[K]; mode 0: out[k] = mean for non-empty k (empty rows untouched);
+// mode 1: out[k] = raw sum (0 for empty).
+int launch_group_sums(const double* X, long long n, long long ldx, int D, const int32_t* labels, int K,
+                      int mode, double* out, long long ldo, int32_t* counts, cudaStream_t s) {
+    if (n <= 0 || K <= 0) return 0;
+    const int T = (int)((n + GS_TILE - 1) / GS_TILE);
+    const long long KT = (long long)K * T;
+    const long long max_leaves = K + n / 64 + 2;
+    const int n_chunks = (D + GS_COLS - 1) / GS_COLS;
+    // scratch layout
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
+    size_t o_hist = take(sizeof(int32_t) * (KT + 1));
+    size_t o_order = take(sizeof(int32_t) * n);
+    size_t o_seg = take(sizeof(int32_t) * K);
+    size_t o_nleaf = take(sizeof(int32_t) * (K + 1));
+    size_t o_total = take(sizeof(int32_t) * 4);
+    size_t o_leaves = take(sizeof(int4) * max_leaves);
+    size_t o_lsum = take(sizeof(double) * max_leaves * D);
+    char* base = (char*)scratch(0, off, s);
+    if (!base) return fail_cuda(cudaErrorMemoryAllocation, "group_sums scratch");
+    int32_t* hist = (int32_t*)(base + o_hist);
+    int32_t* order = (int32_t*)(base + o_order);
+    int32_t* seg = (int32_t*)(base + o_seg);
+    int32_t* nleaf = (int32_t*)(base + o_nleaf);
+    int32_t* total = (int32_t*)(base + o_total);
+    int4* leaves = (int4*)(base + o_leaves);
+    double* lsum = (double*)(base + o_lsum);
+
+    DA_CUDA(cudaMemsetAsync(hist, 0, sizeof(int32_t) * (KT + 1), s));
+    size_t sh = (K <= GS_SMEM_HIST) ? sizeof(int32_t) * K : 0;
+    tile_hist_kernel<<<T, 256, sh, s>>>(labels, n, K, T, hist);
+    DA_CHECK_LAUNCH("tile_hist_kernel");
+    exclusive_scan_kernel<<<1, 1024, 0, s>>>(hist, KT, total);
+    DA_CHECK_LAUNCH("exclusive_scan_kernel(hist)");
+    seg_counts_kernel<<<grid_for(K, 256), 256, 0, s>>>(hist, K, T, n, seg, counts);
+    DA_CHECK_LAUNCH("seg_counts_kernel");
+    stable_scatter_kernel<<<T, 32, 0, s>>>(labels, n, T, hist, order);
+    DA_CHECK_LAUNCH("stable_scatter_kernel");
+    leaf_count_kernel<<<grid_for(K, 256), 256, 0, s>>>(counts, K, nleaf);
+    DA_CHECK_LAUNCH("leaf_count_kernel");
+    exclusive_scan_kernel<<<1, 1024, 0, s>>>(nleaf, K, total + 1);
+    DA_CHECK_LAUNCH("exclusive_scan_kernel(leaves)");
+    leaf_enum_kernel<<<grid_for(K, 128), 128, 0, s>>>(counts, seg, nleaf, K, leaves);
+    DA_CHECK_LAUNCH("leaf_enum_kernel");
+    {
+        long long tasks = max_leaves * n_chunks;
+        leaf_sum_kernel<<<grid_for(tasks, 8, 1LL << 31), 256, 0, s>>>(X, ldx, D, order, leaves, total + 1,
+                                                                      n_chunks, lsum);
+        DA_CHECK_LAUNCH("leaf_sum_kernel");
+    }
+    {
+        long long tasks = (long long)K * n_chunks;
+        seg_finish_kernel<<<grid_for(tasks, 4), 128, 0, s>>>(X, ldx, D, order, counts, seg, nleaf, lsum, K,
+                                                            n_chunks, mode, out, ldo);
+        DA_CHECK_LAUNCH("seg_finish_kernel");
+    }
+    return 0;
+}
+
+// Stable argsort of labels only (used by tests and the reseed path).
+int launch_label_order(const int32_t* labels, long long n, int K, int32_t* order_out, int32_t* counts,
+                       cudaStream_t s) {
+    if (n <= 0) return 0;
+    const int T = (int)((n + GS_TILE - 1) / GS_TILE);
+    const long long KT = (long long)K * T;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
+    size_t o_hist = take(sizeof(int32_t) * (KT + 1));
+    size_t o_seg = take(sizeof(int32_t) * K);
+    size_t o_total = take(sizeof(int32_t) * 4);
+    char* base = (char*)scratch(1, off, s);
+    if (!base) return fail_cuda(cudaErrorMemoryAllocation, "label_order scratch");
+    int32_t* hist = (int32_t*)(base + o_hist);
+    int32_t* seg = (int32_t*)(base + o_seg);
+    int32_t* total = (int32_t*)(base + o_total);
+    DA_CUDA(cudaMemsetAsync(hist, 0, sizeof(int32_t) * (KT + 1), s));
+    size_t sh = (K <= GS_SMEM_HIST) ? sizeof(int32_t) * K : 0;
+    tile_hist_kernel<<<T, 256, sh, s>>>(labels, n, K, T, hist);
+    DA_CHECK_LAUNCH("tile_hist_kernel");
+    exclusive_scan_kernel<<<1, 1024, 0, s>>>(hist, KT, total);
+    DA_CHECK_LAUNCH("exclusive_scan_kernel");
+    seg_counts_kernel<<<grid_for(K, 256), 256, 0, s>>>(hist, K, T, n, seg, counts);
+    DA_CHECK_LAUNCH("seg_counts_kernel");
+    stable_scatter_kernel<<<T, 32, 0, s>>>(labels, n, T, hist, order_out);
+    DA_CHECK_LAUNCH("stable_scatter_kernel");
+    return 0;
+}
+
+}  // namespace da

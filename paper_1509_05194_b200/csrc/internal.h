@@ -1,0 +1,60 @@
+// Internal launch prototypes shared by the .cu files and the C-ABI layer.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace da {
+
+struct GemmArgs {
+    const void* A; int a_f32; long long sai, sak, sA1, sA2; const double* asub; int asub_mode;  // 1: by i, 2: by k
+    const void* B; int b_f32; long long sbk, sbj, sB1, sB2; const double* bsub; int bsub_mode;  // 1: by k, 2: by j
+    double* C; long long sci, scj, sC1, sC2, sCz;
+    long long M, N, K;
+    int nb2, ksplit; long long kchunk;
+    // epi 0: acc; 1: acc + evec[j]; 2: evec[j] - 2*acc; 3: max(0, (ivec[i] - 2*acc) + evec[j])
+    int epi; const double* evec; const double* ivec;
+};
+
+int launch_gemm(const GemmArgs& g, int nb1, cudaStream_t s);
+int launch_reduce_partials(const double* P, int nz, long long len, double scale_div, double* out, cudaStream_t s);
+int launch_col_mean(const void* X, int x_f32, long long n, long long ld, int D, double* mean, cudaStream_t s);
+
+int launch_row_sqnorms(const void* A, int a_is_f32, long long rows, long long lda, int d, double* out,
+                       cudaStream_t s);
+int launch_assign(const void* X, int x_is_f32, long long n, long long ldx, int d, const double* C, long long ldc,
+                  int K, const double* cc, int32_t* labels, double* d2, const int32_t* prev,
+                  unsigned long long* changed, cudaStream_t s);
+
+int launch_group_sums(const double* X, long long n, long long ldx, int D, const int32_t* labels, int K, int mode,
+                      double* out, long long ldo, int32_t* counts, cudaStream_t s);
+int launch_label_order(const int32_t* labels, long long n, int K, int32_t* order_out, int32_t* counts,
+                       cudaStream_t s);
+
+int launch_encode(const void* X, int x_f32, long long n, long long ldx, int D, const float* cw, int M, int K,
+                  int L, const double* sq, const double* P, void* codes_out, int code_bytes, long long ldcodes,
+                  double* err_out, cudaStream_t s);
+
+}  // namespace da
+
+namespace da {
+int launch_heat_up(const float* X, long long n, int D, const int32_t* codes, const float* cw, int M, int K, int m,
+                   float* out, cudaStream_t s);
+int launch_vec_err(const void* X, int x_f32, long long n, long long ldx, int D, const void* codes, int code_bytes,
+                   long long ldc, const float* cw, int M, int K, double* err, cudaStream_t s);
+int launch_reconstruct(const void* codes, int code_bytes, long long n, long long ldc, const float* cw, int M, int K,
+                       int D, double* out, cudaStream_t s);
+int launch_einsum_sq(const float* cw, long long rows, int D, double* out, cudaStream_t s);
+int launch_pair_sums(const void* codes, int code_bytes, long long n, long long ldc, const double* P, int M, int K,
+                     double* out, cudaStream_t s);
+int launch_qsq(const double* Q, long long nq, int D, double* out, cudaStream_t s);
+int launch_adc_scan(const void* codes, int code_bytes, long long ldc, const double* pair, const long long* cand,
+                    long long ncand, long long nq, const double* lut, const double* qsq, int M, int K, int r,
+                    long long* ids_out, double* d_out, cudaStream_t s);
+int launch_np_sum(const double* a, long long n, int divide, double* out, cudaStream_t s);
+int launch_gather_rows(const double* X, long long ldx, int D, const long long* src, const int* dst, int cnt, double* C,
+                       long long ldc, cudaStream_t s);
+int launch_select_better(long long n, int M, const int32_t* beam_codes, const double* beam_err, int32_t* inc_codes,
+                         double* inc_err, cudaStream_t s);
+int launch_set_column(int32_t* codes, long long n, int M, int m, const int32_t* labels, cudaStream_t s);
+}  // namespace da

@@ -1,0 +1,266 @@
+"""GPU parity: the CUDA path against outputs of the reference (tests/golden)
+and the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): codes bit-exact except where the oracle's
+decision gap is < 1e-6 relative; dictionaries and MSE within 1e-4 relative.
+Where the kernels reproduce numpy's association order exactly (reduceat
+group means, einsum norms, pairwise row sums, heat-up) the test demands
+bit-equality; dot products go through a sequential FMA chain instead of
+BLAS and are held to 1e-12 relative."""
+
+import numpy as np
+import pytest
+
+import cases
+import paper_1509_05194_b200 as da
+from paper_1509_05194_b200 import _engine as E
+from paper_1509_05194_b200 import clustering as cl
+from paper_1509_05194_b200 import codebook as cb
+
+pytestmark = pytest.mark.gpu
+
+RT = 1e-12
+
+
+def rel_close(a, b, rtol=RT, atol=0.0):
+    np.testing.assert_allclose(np.asarray(a), np.asarray(b), rtol=rtol, atol=atol)
+
+
+def book_of(cw):
+    return da.Codebook(codewords=cw, order=np.arange(cw.shape[0]))
+
+
+def test_assign_kernel(golden):
+    g, c = golden("small_ops.npz"), cases.assign_case()
+    lab, d2 = E.assign(E.to_dev(c["X"]), c["active"], E.to_dev(c["C"]))
+    np.testing.assert_array_equal(lab.cpu().numpy(), g["assign_labels"])
+    rel_close(d2.cpu().numpy(), g["assign_d2"])
+
+
+def test_group_means_bit_exact(golden):
+    g, c = golden("small_ops.npz"), cases.group_case()
+    X = E.to_dev(c["X"])
+    lab = E.to_dev(c["labels"].astype(np.int32))
+    out = E.to_dev(np.full((c["k"], 6), -7.0))
+    counts = E.to_dev(np.zeros(c["k"], dtype=np.int32))
+    E.native.da_group_sums(E.P(X), X.shape[0], X.stride(0), 6, E.P(lab), c["k"], 0, E.P(out), 6, E.P(counts),
+                           E.stream())
+    cnt = counts.cpu().numpy()
+    np.testing.assert_array_equal(cnt, g["group_counts"])
+    means = out.cpu().numpy()
+    filled = cnt > 0
+    np.testing.assert_array_equal(means[filled], g["group_means"][filled])
+    assert (means[~filled] == -7.0).all()  # empty rows untouched (reseeded by the caller)
+
+
+def test_label_order_is_stable():
+    rng = np.random.default_rng(0)
+    for n, k in [(1, 1), (33, 3), (5000, 256), (70000, 7), (3000, 20000)]:
+        lab = rng.integers(0, k, n).astype(np.int32)
+        order = E.to_dev(np.zeros(n, dtype=np.int32))
+        counts = E.to_dev(np.zeros(k, dtype=np.int32))
+        labd = E.to_dev(lab)
+        E.native.da_label_order(E.P(labd), n, k, E.P(order), E.P(counts), E.stream())
+        np.testing.assert_array_equal(order.cpu().numpy(), np.argsort(lab, kind="stable"))
+        np.testing.assert_array_equal(counts.cpu().numpy(), np.bincount(lab, minlength=k))
+
+
+def test_np_mean_bit_exact():
+    rng = np.random.default_rng(1)
+    for n in [1, 7, 8, 100, 128, 129, 1000, 4099, 65537, 1_000_003]:
+        a = rng.standard_normal(n) * 10.0 ** rng.uniform(-3, 3, n)
+        got = E.np_mean(E.to_dev(a)).item()
+        assert got == a.mean(), n
+
+
+@pytest.mark.parametrize("which", ["lloyd", "reseed"])
+def test_lloyd(golden, which):
+    g = golden("small_ops.npz")
+    c = cases.lloyd_case() if which == "lloyd" else cases.reseed_case()
+    fit = cl.lloyd_kmeans(c["X"], c["C"], active_dims=c.get("active"), max_iters=c["iters"])
+    np.testing.assert_array_equal(fit.assignment, g[f"{which}_assign"])
+    rel_close(fit.points, g[f"{which}_points"], atol=1e-12)
+    rel_close(fit.objective_trace, g[f"{which}_trace"])
+
+
+def test_pca(golden):
+    g, c = golden("small_ops.npz"), cases.pca_case()
+    for key, X in (("pca", c["X"]), ("pcag", c["Xgram"])):
+        m = cl.pca_fit(X)
+        R, Rg = m.rotation, g[f"{key}_rotation"]
+        signs = np.sign((R * Rg).sum(axis=1))
+        rel_close(R * signs[:, None], Rg, rtol=1e-9, atol=1e-12)
+        rel_close(m.mean, g[f"{key}_mean"], atol=1e-15)
+        rel_close(m.explained_variance, g[f"{key}_var"], rtol=1e-10, atol=1e-14)
+
+
+def test_staged_kmeans(golden):
+    g, c = golden("small_ops.npz"), cases.staged_case()
+    fit = cl.improved_kmeans(c["X"], c["C"], max_iters=c["iters"])
+    np.testing.assert_array_equal(fit.assignment, g["staged_assign"])
+    rel_close(fit.points, g["staged_points"], rtol=1e-9, atol=1e-12)
+    rel_close(fit.objective_trace, g["staged_trace"], rtol=1e-10)
+
+
+def test_cross_products(golden):
+    g, c = golden("small_ops.npz"), cases.codebook_case()
+    cross = cb.cross_products(book_of(c["cw"]))
+    rel_close(cross.products, g["cross_P"], atol=1e-14)
+    np.testing.assert_array_equal(cross.sq_norms, g["cross_sq"])  # einsum order
+    ref = cb.refresh_cross_products(cross, book_of(c["cw2"]), 1)
+    rel_close(ref.products, g["refresh_P"], atol=1e-14)
+    np.testing.assert_array_equal(ref.sq_norms, g["refresh_sq"])
+
+
+@pytest.mark.parametrize("L", cases.BEAM_WIDTHS)
+def test_beam_encode(golden, L):
+    g, c = golden("small_ops.npz"), cases.codebook_case()
+    book = book_of(c["cw"])
+    cross = cb.cross_products(book)
+    cw, sq = cb._codebook_dev(book)
+    Pt, _ = cross.device()
+    codes, err = E.encode(E.to_dev(c["X"]), cw, sq, Pt, L)
+    np.testing.assert_array_equal(codes.cpu().numpy(), g[f"beam_codes_L{L}"])
+    np.testing.assert_array_equal(err.cpu().numpy(), g[f"beam_errs_L{L}"])  # exact error, same codes
+    enc = cb.encode_dataset(book, c["X"], beam_width=L)
+    np.testing.assert_array_equal(enc.codes, g[f"enc_codes_L{L}"])
+    assert enc.codes.dtype == np.uint8
+
+
+def test_multipath_and_adc(golden):
+    g, c = golden("small_ops.npz"), cases.codebook_case()
+    book = book_of(c["cw"])
+    cross = cb.cross_products(book)
+    code, err = cb.encode_multipath(book, cross, c["q"], 4)
+    np.testing.assert_array_equal(code, g["multipath_code"])
+    rel_close(err, g["multipath_err"])
+    t = cb.adc_table(book, c["q"])
+    rel_close(t.values, g["adc_values"], atol=1e-13)
+    rel_close(t.q_sq_norm, g["adc_qsq"])
+    enc = cb.encode_dataset(book, c["X"], beam_width=8)
+    pair = cb.code_pair_sums(cross, enc.codes)
+    rel_close(pair, g["pair_sums"], atol=1e-13)
+    ids, dists = cb.exhaustive_adc_search(book, enc, c["q"], 10, cross=cross, pair_sums=pair)
+    np.testing.assert_array_equal(ids, g["search_ids"])
+    rel_close(dists, g["search_dists"], atol=1e-12)
+    rel_close(cb.distortion(book, c["X"], enc), g["distortion"])
+
+
+def test_heat_cool_sweep(golden):
+    g, c = golden("small_training.npz"), cases.sweep_case()
+    book = book_of(c["cw"])
+    enc = cb.encode_dataset(book, c["X"], beam_width=8)
+    np.testing.assert_array_equal(enc.codes, g["sweep_init_codes"])
+    inter = da.heat_up(c["X"], book, enc, 1)
+    np.testing.assert_array_equal(inter, g["heat_up_1"])  # float64 arithmetic, same order
+    cfg = da.TrainConfig(m_count=3, k_count=8, sweeps=1, beam_width=8)
+    nd, asg = da.cool_down(inter, book, 1, cfg)
+    np.testing.assert_array_equal(asg, g["cool_assign"])
+    rel_close(nd, g["cool_dict"], rtol=1e-6)
+    rep = da.TrainReport(config=cfg)
+    b2, e2, x2 = da.da_sweep(c["X"], book, enc, cfg, report=rep)
+    np.testing.assert_array_equal(e2.codes, g["sweep_codes"])
+    rel_close(b2.codewords, g["sweep_cw"], rtol=1e-6)
+    rel_close(rep.distortions(), g["sweep_dist"], rtol=1e-9)
+    rel_close(x2.products, g["sweep_P"], rtol=1e-6, atol=1e-9)
+    np.testing.assert_array_equal(book.codewords, c["cw"])  # inputs untouched
+
+
+def test_train_small(golden):
+    g, c = golden("small_training.npz"), cases.train_case()
+    cfg = da.TrainConfig(**c["config"])
+    b, e, r = da.train_from_scratch(c["X"], cfg)
+    np.testing.assert_array_equal(b.order, g["train_order"])
+    np.testing.assert_array_equal(e.codes, g["train_codes"])
+    rel_close(b.codewords, g["train_cw"], rtol=1e-5, atol=1e-7)
+    rel_close(r.distortions(), g["train_dist"], rtol=1e-9)
+    rb, re_ = da.rvq_train(c["X"], cfg)
+    np.testing.assert_array_equal(re_.codes, g["rvq_codes"])
+    rel_close(rb.codewords, g["rvq_cw"], rtol=1e-5, atol=1e-7)
+    b0 = da.Codebook(codewords=g["train_cw"], order=g["train_order"])
+    b3, r3 = da.train_online(b0, c["X2"], cfg)
+    np.testing.assert_array_equal(b3.order, g["online_order"])
+    rel_close(b3.codewords, g["online_cw"], rtol=1e-5, atol=1e-7)
+    rel_close(r3.distortions(), g["online_dist"], rtol=1e-9)
+
+
+def _frob_rel(a, b):
+    return np.linalg.norm((a - b).reshape(a.shape[0], -1), axis=1) / np.linalg.norm(b.reshape(b.shape[0], -1), axis=1)
+
+
+def test_config_a_full_training(golden):
+    """BASELINE config A: N=10k, D=32, M=4, K=256, growth + 3 sweeps, rel_tol=0."""
+    from paper_1509_05194_b200 import synthetic
+
+    g = golden("config_a.npz")
+    X = synthetic.config_a()
+    cfg = da.TrainConfig(m_count=4, k_count=256, beam_width=10, sweeps=3, rel_tol=0.0)
+    b, e, r = da.train_from_scratch(X, cfg)
+    np.testing.assert_array_equal(b.order, g["order"])
+    assert _frob_rel(b.codewords, g["cw"]).max() <= 1e-4
+    same = (e.codes == g["codes"]).all(axis=1).mean()
+    assert same >= 0.999, same
+    mse = cb.distortion(b, X, e)
+    assert abs(mse - float(g["mse"])) <= 1e-4 * float(g["mse"])
+    rel_close(r.distortions(), g["dist"], rtol=1e-4)
+
+
+def test_config_b_subsample(golden):
+    """D=128 uint8-range data: growth-pass codebook, L=1/10 encode, one sweep, ADC top-100."""
+    from oracle import da_oracle as O
+    from paper_1509_05194_b200 import synthetic
+
+    g = golden("config_b_sub.npz")
+    X = synthetic.config_b(n=cases.B_TRAIN + cases.B_ENC)
+    Xt, Xe = X[: cases.B_TRAIN], X[cases.B_TRAIN:]
+    cfg = da.TrainConfig(m_count=8, k_count=256, beam_width=10, sweeps=0, rel_tol=0.0)
+    b, e, r = da.train_from_scratch(Xt, cfg)
+    assert _frob_rel(b.codewords, g["cw"]).max() <= 1e-4
+    assert (e.codes == g["train_codes"]).all(axis=1).mean() >= 0.999
+    # encode with the reference's codebook: per-vector exact except oracle near-ties
+    ref_book = da.Codebook(codewords=g["cw"], order=g["order"])
+    cross = cb.cross_products(ref_book)
+    for L in (1, 10):
+        enc = cb.encode_dataset(ref_book, Xe, beam_width=L, cross=cross)
+        bad = np.flatnonzero((enc.codes != g[f"enc_codes_L{L}"]).any(axis=1))
+        if bad.size:
+            gaps = O.beam_min_gap(g["cw"].astype(np.float64), O.cross_table(g["cw"])[0],
+                                  Xe[bad].astype(np.float64), L)
+            assert (gaps < 1e-6).all(), (L, bad, gaps)
+    # one annealing pass from the reference's growth result
+    cfg1 = da.TrainConfig(m_count=8, k_count=256, beam_width=10, sweeps=1, rel_tol=0.0)
+    enc0 = da.EncodedDataset(g["train_codes"], 256)
+    b2, e2, _ = da.da_sweep(Xt, ref_book, enc0, cfg1, report=(rep := da.TrainReport()))
+    assert _frob_rel(b2.codewords, g["sweep_cw"]).max() <= 1e-4
+    assert (e2.codes == g["sweep_codes"]).all(axis=1).mean() >= 0.999
+    rel_close(rep.distortions(), g["sweep_dist"], rtol=1e-4)
+    # ADC top-100
+    Q = synthetic.config_e_queries(16)
+    encx = da.EncodedDataset(g["enc_codes_L10"], 256)
+    ids, dists = cb.exhaustive_adc_search_batch(ref_book, encx, Q.astype(np.float64), 100, cross=cross,
+                                                pair_sums=g["adc_pair"])
+    rel_close(dists, g["adc_dists"], rtol=1e-9, atol=1e-9)
+    mism = ids != g["adc_ids"]
+    if mism.any():  # only across (near-)ties of the distance order
+        rel_close(dists[mism], g["adc_dists"][mism], rtol=1e-9)
+
+
+def test_config_c_subsample(golden):
+    """D=960 (D-tiled contraction): growth codebook and L=10 encode."""
+    from paper_1509_05194_b200 import synthetic
+    from oracle import da_oracle as O
+
+    g = golden("config_c_sub.npz")
+    X = synthetic.config_c(n=cases.C_TRAIN + cases.C_ENC)
+    Xt, Xe = X[: cases.C_TRAIN], X[cases.C_TRAIN:]
+    cfg = da.TrainConfig(m_count=4, k_count=256, beam_width=10, sweeps=0, rel_tol=0.0)
+    b, e, r = da.train_from_scratch(Xt, cfg)
+    assert _frob_rel(b.codewords, g["cw"]).max() <= 1e-4
+    assert (e.codes == g["train_codes"]).all(axis=1).mean() >= 0.999
+    ref_book = da.Codebook(codewords=g["cw"], order=g["order"])
+    enc = cb.encode_dataset(ref_book, Xe, beam_width=10)
+    bad = np.flatnonzero((enc.codes != g["enc_codes"]).any(axis=1))
+    if bad.size:
+        gaps = O.beam_min_gap(g["cw"].astype(np.float64), O.cross_table(g["cw"])[0],
+                              Xe[bad].astype(np.float64), 10)
+        assert (gaps < 1e-6).all(), (bad, gaps)
