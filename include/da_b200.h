@@ -34,6 +34,10 @@ const char* da_last_error(void);
 int da_version(void);
 /* Number of kernels this library has launched in the process (all devices). */
 long long da_launch_count(void);
+/* Per-kernel CUDA-event timing (off by default).  da_prof_collect writes
+ * "name count total_ms" lines into buf and clears the log. */
+int da_prof_enable(int on);
+int da_prof_collect(char* buf, int cap);
 /* Free every library-owned scratch buffer (all devices). */
 int da_release_scratch(void);
 
@@ -80,8 +84,10 @@ int da_reconstruct(const void* codes, int code_bytes, int64_t n, int64_t ldc, co
 /* Column means (PCA centre).  replaces X.mean(axis=0)   clustering.py:93 */
 int da_col_mean(const void* X, int x_f32, int64_t n, int64_t ld, int D, double* mean, void* stream);
 
-/* Sample covariance (X - mean)^T (X - mean) / (n - 1).  replaces clustering.py:94-96 */
-int da_pca_cov(const void* X, int x_f32, int64_t n, int64_t ld, int D, const double* mean, double* cov, void* stream);
+/* Sample covariance (X - mean)^T (X - mean) / (n - 1)  (divide=1), or the raw
+ * centred scatter (divide=0, for sharded PCA).  replaces clustering.py:94-96 */
+int da_pca_cov(const void* X, int x_f32, int64_t n, int64_t ld, int D, const double* mean, double* cov, int divide,
+               void* stream);
 
 /* inverse=0: out = (X - mean) @ R^T;  inverse=1: out = X @ R + mean.
  * replaces PcaModel.transform / inverse_transform   clustering.py:39-43 */

@@ -186,12 +186,30 @@ def config_c_sub():
          train_dist=rep.distortions(), enc_codes=codes.astype(np.uint8), enc_errs=errs)
 
 
+def meta():
+    import json
+
+    import numpy
+
+    info = {"numpy": numpy.__version__}
+    try:
+        from threadpoolctl import threadpool_info
+
+        info["blas"] = [{k: v for k, v in d.items() if k in ("internal_api", "version", "architecture")}
+                        for d in threadpool_info()]
+    except Exception:
+        pass
+    os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, "meta.json"), "w") as f:
+        json.dump(info, f, indent=1)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-slow", action="store_true")
     ap.add_argument("--only", default=None)
     a = ap.parse_args()
-    jobs = [np_order, small_ops, small_training]
+    jobs = [meta, np_order, small_ops, small_training]
     if not a.skip_slow:
         jobs += [config_b_sub, config_c_sub, config_a]
     for j in jobs:

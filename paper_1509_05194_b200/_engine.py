@@ -153,10 +153,23 @@ def _reseed_sharded(Xr, errs, empty_idx, C, comm):
     all_err = comm.allgather(cand_err.to(Xr.device)).cpu().numpy().reshape(-1)
     all_gid = comm.allgather(cand_gid.to(Xr.device)).cpu().numpy().reshape(-1)
     all_rows = comm.allgather(rows).reshape(-1, Xr.shape[1])
-    # descending err, ties -> higher global id first
-    order = np.lexsort((-all_gid, -all_err))[:e]
-    pick = torch.from_numpy(order.astype(np.int64)).to(Xr.device)
+    from .distributed import merge_worst
+
+    pick = torch.from_numpy(merge_worst(all_err, all_gid, e).astype(np.int64)).to(Xr.device)
     C[torch.from_numpy(np.asarray(empty_idx, dtype=np.int64)).to(C.device)] = all_rows[pick]
+
+
+def _sharded_update(sums, counts, C, comm):
+    """Allreduce per-shard (K, D) sums and K counts; C[filled] = sums / counts.
+    Returns the global counts (numpy int64)."""
+    cnt = counts.to(F64)
+    comm.allreduce_(sums)
+    comm.allreduce_(cnt)
+    counts_h = cnt.cpu().numpy().astype(np.int64)
+    filled = torch.from_numpy(np.flatnonzero(counts_h > 0)).to(C.device)
+    if filled.numel():
+        C[filled] = sums[filled] / cnt[filled].unsqueeze(1)
+    return counts_h
 
 
 def lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, comm=None):
@@ -178,15 +191,13 @@ def lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, c
                                  stream())
             counts_h = counts.cpu().numpy()
         else:
-            native.da_group_sums(P(Xr), n, Xr.stride(0), D, P(labels), K, 1, P(sums), sums.stride(0),
-                                 P(counts), stream())
-            cnt64 = counts.to(F64)
-            comm.allreduce_(sums)
-            comm.allreduce_(cnt64)
-            counts_h = cnt64.cpu().numpy().astype(np.int64)
-            filled_t = torch.from_numpy(np.flatnonzero(counts_h > 0)).to(dev)
-            if filled_t.numel():
-                C[filled_t] = sums[filled_t] / cnt64[filled_t].unsqueeze(1)
+            if n:
+                native.da_group_sums(P(Xr), n, Xr.stride(0), D, P(labels), K, 1, P(sums), sums.stride(0),
+                                     P(counts), stream())
+            else:
+                sums.zero_()
+                counts.zero_()
+            counts_h = _sharded_update(sums, counts, C, comm)
         empty = np.flatnonzero(counts_h == 0)
         if empty.size:
             if comm is None:
@@ -254,14 +265,11 @@ def pca(X: torch.Tensor, comm=None):
     if n > D:
         cov = torch.empty((D, D), dtype=F64, device=X.device)
         if comm is None:
-            native.da_pca_cov(P(X), is_f32(X), n_local, X.stride(0), D, P(mean), P(cov), stream())
+            native.da_pca_cov(P(X), is_f32(X), n_local, X.stride(0), D, P(mean), P(cov), 1, stream())
         else:
-            if n_local >= 2:
-                native.da_pca_cov(P(X), is_f32(X), n_local, X.stride(0), D, P(mean), P(cov), stream())
-                cov *= float(n_local - 1)
-            elif n_local == 1:
-                xc = X.to(F64) - mean
-                cov = xc.T @ xc
+            # scatter around the GLOBAL mean on every shard, allreduce, then / (n-1)
+            if n_local:
+                native.da_pca_cov(P(X), is_f32(X), n_local, X.stride(0), D, P(mean), P(cov), 0, stream())
             else:
                 cov.zero_()
             comm.allreduce_(cov)

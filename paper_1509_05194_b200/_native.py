@@ -32,7 +32,7 @@ _SIGNATURES = {
     "da_vec_err": [_P, _I, _L, _L, _I, _P, _I, _L, _P, _I, _I, _P, _P],
     "da_reconstruct": [_P, _I, _L, _L, _P, _I, _I, _I, _P, _P],
     "da_col_mean": [_P, _I, _L, _L, _I, _P, _P],
-    "da_pca_cov": [_P, _I, _L, _L, _I, _P, _P, _P],
+    "da_pca_cov": [_P, _I, _L, _L, _I, _P, _P, _I, _P],
     "da_rotate": [_P, _I, _L, _L, _I, _P, _P, _P, _I, _P],
     "da_gemm_strided": [_P, _I, _L, _L, _P, _I, _L, _L, _P, _L, _L, _L, _L, _L, _P],
     "da_einsum_sq": [_P, _L, _I, _P, _P],
@@ -45,6 +45,8 @@ _SIGNATURES = {
     "da_select_better": [_L, _I, _P, _P, _P, _P, _P],
     "da_set_column": [_P, _L, _I, _I, _P, _P],
     "da_release_scratch": [],
+    "da_prof_enable": [_I],
+    "da_prof_collect": [ctypes.c_char_p, _I],
     "da_version": [],
 }
 
@@ -54,6 +56,21 @@ EXPORTED = tuple(_SIGNATURES) + ("da_last_error", "da_launch_count")
 def launch_count() -> int:
     """Kernels launched by libda_b200 so far in this process."""
     return int(load_library().da_launch_count())
+
+
+def prof_enable(on: bool) -> None:
+    native.da_prof_enable(1 if on else 0)
+
+
+def prof_collect() -> dict:
+    """{kernel name: (launches, total ms)} since the last collect."""
+    buf = ctypes.create_string_buffer(1 << 16)
+    native.da_prof_collect(buf, len(buf))
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, cnt, ms = line.split()
+        out[name] = (int(cnt), float(ms))
+    return out
 
 
 def load_library(path: str = LIB_PATH):

@@ -23,7 +23,7 @@ constexpr int AS_TM = 8;
 constexpr int AS_THREADS = 256;
 }  // namespace
 
-template <typename TX>
+template <typename TX, bool BLK>
 __global__ void __launch_bounds__(AS_THREADS)
 assign_kernel(const TX* __restrict__ X, long long n, long long ldx, int d,
               const double* __restrict__ C, long long ldc, int K,
@@ -59,10 +59,14 @@ assign_kernel(const TX* __restrict__ X, long long n, long long ldx, int d,
 
     for (int col0 = 0; col0 < K; col0 += AS_BN) {
         double acc[AS_TM][4];
+        double tot[BLK ? AS_TM : 1][4];
 #pragma unroll
         for (int i = 0; i < AS_TM; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+        // d > 384: OpenBLAS k-blocking (see blas_block_len) -- fold per block
+        long long blk_end = blas_block_len(d);
+        bool first_blk = true;
 
         for (int k0 = 0; k0 < d; k0 += AS_BK) {
             __syncthreads();
@@ -90,6 +94,17 @@ assign_kernel(const TX* __restrict__ X, long long n, long long ldx, int d,
             __syncthreads();
             const int kmax = min(AS_BK, d - k0);
             for (int k = 0; k < kmax; ++k) {
+                if (BLK && k0 + k == blk_end) {
+#pragma unroll
+                    for (int i = 0; i < AS_TM; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            tot[BLK ? i : 0][j] = first_blk ? acc[i][j] : dadd(tot[BLK ? i : 0][j], acc[i][j]);
+                            acc[i][j] = 0.0;
+                        }
+                    first_blk = false;
+                    blk_end += blas_block_len(d - blk_end);
+                }
                 double a[AS_TM], b[4];
                 const double2* ap = reinterpret_cast<const double2*>(&As[k][ty * AS_TM]);
 #pragma unroll
@@ -102,6 +117,13 @@ assign_kernel(const TX* __restrict__ X, long long n, long long ldx, int d,
 #pragma unroll
                     for (int j = 0; j < 4; ++j) acc[i][j] = __fma_rn(a[i], b[j], acc[i][j]);
             }
+        }
+        if (BLK) {
+#pragma unroll
+            for (int i = 0; i < AS_TM; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    acc[i][j] = first_blk ? acc[i][j] : dadd(tot[BLK ? i : 0][j], acc[i][j]);
         }
         // fused epilogue: distances + running first-min
 #pragma unroll
@@ -171,12 +193,13 @@ int launch_assign(const void* X, int x_is_f32, long long n, long long ldx, int d
                   const int32_t* prev, unsigned long long* changed, cudaStream_t s) {
     if (n <= 0) return 0;
     unsigned g = grid_for(n, AS_BM, 1LL << 31);
-    if (x_is_f32)
-        assign_kernel<float><<<g, AS_THREADS, 0, s>>>((const float*)X, n, ldx, d, C, ldc, K, cc, labels,
-                                                        d2, prev, changed);
-    else
-        assign_kernel<double><<<g, AS_THREADS, 0, s>>>((const double*)X, n, ldx, d, C, ldc, K, cc,
-                                                         labels, d2, prev, changed);
+    ProfScope ps("assign", s);
+    const bool blk = d > BLAS_Q;
+#define AS_LAUNCH(T, B) assign_kernel<T, B><<<g, AS_THREADS, 0, s>>>((const T*)X, n, ldx, d, C, ldc, K, cc, labels, \
+                                                                  d2, prev, changed)
+    if (x_is_f32) { if (blk) AS_LAUNCH(float, true); else AS_LAUNCH(float, false); }
+    else { if (blk) AS_LAUNCH(double, true); else AS_LAUNCH(double, false); }
+#undef AS_LAUNCH
     DA_CHECK_LAUNCH("assign_kernel");
     return 0;
 }

@@ -11,6 +11,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/da_b200.h"
 #include "common.cuh"
@@ -146,23 +147,45 @@ int da_col_mean(const void* X, int x_f32, int64_t n, int64_t ld, int D, double* 
     return launch_col_mean(X, x_f32, n, ld, D, mean, STREAM(stream));
 }
 
-int da_pca_cov(const void* X, int x_f32, int64_t n, int64_t ld, int D, const double* mean, double* cov, void* stream) {
-    if (n < 2) return fail_arg("PCA needs at least 2 vectors, got %lld", (long long)n);
-    // split the n-long reduction so the grid covers the machine
-    const long long tiles = ((D + 63) / 64) * (long long)((D + 63) / 64);
-    long long ks = (148LL * 4 + tiles - 1) / tiles;
-    ks = std::max(1LL, std::min(ks, std::min(64LL, (long long)n / 256 + 1)));
-    const long long kchunk = ((long long)n + ks - 1) / ks;
-    double* part = (double*)scratch(5, sizeof(double) * (size_t)ks * D * D, STREAM(stream));
-    if (!part) return fail_cuda(cudaErrorMemoryAllocation, "pca_cov scratch");
-    GemmArgs g{};
-    g.A = X; g.a_f32 = x_f32; g.sai = 1; g.sak = ld; g.asub = mean; g.asub_mode = 1;
-    g.B = X; g.b_f32 = x_f32; g.sbk = ld; g.sbj = 1; g.bsub = mean; g.bsub_mode = 2;
-    g.C = part; g.sci = D; g.scj = 1; g.sCz = (long long)D * D;
-    g.M = D; g.N = D; g.K = n; g.nb2 = 1; g.ksplit = (int)ks; g.kchunk = kchunk; g.epi = 0;
-    int rc = launch_gemm(g, 1, STREAM(stream));
-    if (rc) return rc;
-    return launch_reduce_partials(part, (int)ks, (long long)D * D, (double)(n - 1), cov, STREAM(stream));
+int da_pca_cov(const void* X, int x_f32, int64_t n, int64_t ld, int D, const double* mean, double* cov, int divide,
+               void* stream) {
+    if (divide && n < 2) return fail_arg("PCA needs at least 2 vectors, got %lld", (long long)n);
+    if (n < 1) return fail_arg("pca_cov: no rows");
+    cudaStream_t s = STREAM(stream);
+    ProfScope ps("pca_cov", s);
+    // numpy evaluates Xc.T @ Xc with OpenBLAS dsyrk: the n-long contraction is cut
+    // into GEMM_Q blocks (balanced tail), each an FMA chain from zero, and the block
+    // results are added to C in order.  Blocks are computed in parallel here (one
+    // gemm z-slice each) and folded in order, wave by wave.
+    std::vector<long long> starts{0};
+    for (long long ls = 0; ls < (long long)n;) {
+        ls += blas_block_len((long long)n - ls);
+        starts.push_back(ls);
+    }
+    const long long nb = (long long)starts.size() - 1;
+    const long long dd = (long long)D * D;
+    long long wave = std::max(1LL, std::min(nb, (256LL << 20) / (dd * 8)));
+    double* part = (double*)scratch(5, sizeof(double) * (size_t)(wave * dd), s);
+    long long* kst = (long long*)scratch(6, sizeof(long long) * (size_t)(nb + 1), s);
+    if (!part || !kst) return fail_cuda(cudaErrorMemoryAllocation, "pca_cov scratch");
+    DA_CUDA(cudaMemcpyAsync(kst, starts.data(), sizeof(long long) * (nb + 1), cudaMemcpyHostToDevice, s));
+    for (long long w0 = 0; w0 < nb; w0 += wave) {
+        const long long wn = std::min(wave, nb - w0);
+        GemmArgs g{};
+        g.A = X; g.a_f32 = x_f32; g.sai = 1; g.sak = ld; g.asub = mean; g.asub_mode = 1;
+        g.B = X; g.b_f32 = x_f32; g.sbk = ld; g.sbj = 1; g.bsub = mean; g.bsub_mode = 2;
+        g.C = part; g.sci = D; g.scj = 1; g.sCz = dd;
+        g.M = D; g.N = D; g.K = n; g.nb2 = 1; g.ksplit = (int)wn; g.kstarts = kst + w0; g.epi = 0;
+        int rc = launch_gemm(g, 1, s);
+        if (rc) return rc;
+        const bool last = w0 + wn == nb;
+        rc = launch_accumulate_partials(part, (int)wn, dd, (last && divide) ? (double)(n - 1) : 0.0, w0 > 0 ? 1 : 0,
+                                        cov, s);
+        if (rc) return rc;
+    }
+    // the pinned starts vector must outlive the async copy
+    DA_CUDA(cudaStreamSynchronize(s));
+    return 0;
 }
 
 int da_rotate(const void* X, int x_f32, int64_t n, int64_t ld, int D, const double* R, const double* mean,

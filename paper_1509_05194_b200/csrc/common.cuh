@@ -165,6 +165,18 @@ __device__ __forceinline__ double np_einsum_sq(const F& f, int n) {
     return dadd(0.0, dadd(a0, a1));
 }
 
+// OpenBLAS (0.3.30, SkylakeX/Haswell dgemm & dsyrk drivers) splits the
+// contraction dimension k into blocks of GEMM_Q = 384, balancing the last two:
+//   rest >= 2Q -> Q;  Q < rest < 2Q -> ((rest/2 + 1)/2)*2;  else rest.
+// Each block is a sequential FMA chain from zero that is then added to C.
+// Verified bit-exact against numpy's matmul on this toolchain (oracle/, tests).
+constexpr long long BLAS_Q = 384;
+__host__ __device__ __forceinline__ long long blas_block_len(long long rest) {
+    if (rest >= 2 * BLAS_Q) return BLAS_Q;
+    if (rest > BLAS_Q) return ((rest / 2 + 1) / 2) * 2;
+    return rest;
+}
+
 // Lexicographic (value, index) order used by numpy's stable argsort / argmin.
 __device__ __forceinline__ bool lex_less(double a, long long ia, double b, long long ib) {
     return (a < b) || (a == b && ia < ib);

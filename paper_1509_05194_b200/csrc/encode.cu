@@ -242,8 +242,13 @@ int launch_encode(const void* X, int x_f32, long long n, long long ldx, int D, c
         g.M = cn; g.N = (long long)M * K; g.K = D;
         g.nb2 = 1; g.ksplit = 1; g.kchunk = D;
         g.epi = 2; g.evec = sq;
-        int rc = launch_gemm(g, 1, s);
+        int rc;
+        {
+            ProfScope ps("encode_table_gemm", s);
+            rc = launch_gemm(g, 1, s);
+        }
         if (rc) return rc;
+        ProfScope ps2("encode_beam_select", s);
         const unsigned grid = (unsigned)((cn + warps - 1) / warps);
         void* cout = (char*)codes_out + (size_t)c0 * ldcodes * code_bytes;
         double* eout = err_out ? err_out + c0 : nullptr;

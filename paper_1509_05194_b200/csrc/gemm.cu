@@ -33,16 +33,29 @@ __global__ void __launch_bounds__(G_THREADS) gemm_kernel(GemmArgs g) {
     const TB* B = (const TB*)g.B + z1 * g.sB1 + z2 * g.sB2;
     double* C = g.C + z1 * g.sC1 + z2 * g.sC2 + ks * g.sCz;
     const long long i0 = (long long)blockIdx.y * GB_M, j0 = (long long)blockIdx.x * GB_N;
-    const long long kbeg = ks * g.kchunk;
-    const long long kend = min(g.K, kbeg + g.kchunk);
+    const long long kbeg = g.kstarts ? g.kstarts[ks] : ks * g.kchunk;
+    const long long kend = g.kstarts ? g.kstarts[ks + 1] : min(g.K, kbeg + g.kchunk);
     const bool a_kfast = g.sak == 1;
     const bool b_jfast = g.sbj == 1;
 
-    double acc[4][4];
+    double acc[4][4], tot[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+        for (int j = 0; j < 4; ++j) { acc[i][j] = 0.0; tot[i][j] = 0.0; }
+    // BLAS k-blocking of this k-range (one block when the range is <= 384)
+    long long blk_end = kbeg + blas_block_len(kend - kbeg);
+    bool first_blk = true;
+    auto fold = [&]() {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                tot[i][j] = first_blk ? acc[i][j] : dadd(tot[i][j], acc[i][j]);
+                acc[i][j] = 0.0;
+            }
+        first_blk = false;
+    };
 
     for (long long k0 = kbeg; k0 < kend; k0 += GB_K) {
         __syncthreads();
@@ -77,6 +90,10 @@ __global__ void __launch_bounds__(G_THREADS) gemm_kernel(GemmArgs g) {
         __syncthreads();
         const int kmax = (int)min((long long)GB_K, kend - k0);
         for (int k = 0; k < kmax; ++k) {
+            if (k0 + k == blk_end) {
+                fold();
+                blk_end += blas_block_len(kend - blk_end);
+            }
             double2 a01 = *reinterpret_cast<const double2*>(&As[k][ty * 4]);
             double2 a23 = *reinterpret_cast<const double2*>(&As[k][ty * 4 + 2]);
             double2 b01 = *reinterpret_cast<const double2*>(&Bs[k][2 * tx]);
@@ -89,6 +106,7 @@ __global__ void __launch_bounds__(G_THREADS) gemm_kernel(GemmArgs g) {
                 for (int j = 0; j < 4; ++j) acc[i][j] = __fma_rn(a[i], b[j], acc[i][j]);
         }
     }
+    fold();
     const int cl[4] = {2 * tx, 2 * tx + 1, 32 + 2 * tx, 33 + 2 * tx};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -98,7 +116,7 @@ __global__ void __launch_bounds__(G_THREADS) gemm_kernel(GemmArgs g) {
         for (int j = 0; j < 4; ++j) {
             long long gj = j0 + cl[j];
             if (gj >= g.N) continue;
-            double v = acc[i][j];
+            double v = tot[i][j];
             if (g.epi == 1) v = dadd(v, g.evec[gj]);
             else if (g.epi == 2) v = dsub(g.evec[gj], dmul(2.0, v));
             else if (g.epi == 3) { v = dadd(dsub(g.ivec[gi], dmul(2.0, v)), g.evec[gj]); if (v < 0.0) v = 0.0; }
@@ -120,19 +138,27 @@ int launch_gemm(const GemmArgs& g, int nb1, cudaStream_t s) {
     return 0;
 }
 
-// Sum ksplit partial matrices in order and scale: out = (sum_z P[z]) * scale
+// Sum ksplit partial matrices in order and scale: out = (sum_z P[z]) / scale_div.
+// accumulate=1 continues a running total already in out (before any division).
 __global__ void reduce_partials_kernel(const double* __restrict__ P, int nz, long long len, double scale_div,
-                                       double* __restrict__ out) {
+                                       int accumulate, double* __restrict__ out) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= len) return;
-    double s = P[i];
+    double s = accumulate ? dadd(out[i], P[i]) : P[i];
     for (int z = 1; z < nz; ++z) s = dadd(s, P[(long long)z * len + i]);
     out[i] = scale_div != 0.0 ? __ddiv_rn(s, scale_div) : s;
 }
 
+int launch_accumulate_partials(const double* P, int nz, long long len, double scale_div, int accumulate,
+                               double* out, cudaStream_t s) {
+    reduce_partials_kernel<<<grid_for(len, 256), 256, 0, s>>>(P, nz, len, scale_div, accumulate, out);
+    DA_CHECK_LAUNCH("reduce_partials_kernel");
+    return 0;
+}
+
 int launch_reduce_partials(const double* P, int nz, long long len, double scale_div, double* out,
                            cudaStream_t s) {
-    reduce_partials_kernel<<<grid_for(len, 256), 256, 0, s>>>(P, nz, len, scale_div, out);
+    reduce_partials_kernel<<<grid_for(len, 256), 256, 0, s>>>(P, nz, len, scale_div, 0, out);
     DA_CHECK_LAUNCH("reduce_partials_kernel");
     return 0;
 }
@@ -150,7 +176,36 @@ __global__ void col_partial_kernel(const T* __restrict__ X, long long n, long lo
     part[(long long)p * D + c] = s;
 }
 
+// numpy's X.mean(axis=0) on a C-contiguous array adds the rows one after the
+// other (no pairwise tree along axis 0): one thread per column, one chain.
+template <typename T>
+__global__ void col_mean_seq_kernel(const T* __restrict__ X, long long n, long long ld, int D, double* __restrict__ mean) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= D) return;
+    double s = 0.0;
+    long long r = 0;
+    for (; r + 8 <= n; r += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = (double)X[(r + u) * ld + c];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s = dadd(s, v[u]);
+    }
+    for (; r < n; ++r) s = dadd(s, (double)X[r * ld + c]);
+    mean[c] = __ddiv_rn(s, (double)n);
+}
+
 int launch_col_mean(const void* X, int x_f32, long long n, long long ld, int D, double* mean, cudaStream_t s) {
+    if (n <= 0) return fail_arg("col_mean: n must be positive");
+    ProfScope ps("col_mean", s);
+    if (x_f32) col_mean_seq_kernel<float><<<(D + 63) / 64, 64, 0, s>>>((const float*)X, n, ld, D, mean);
+    else col_mean_seq_kernel<double><<<(D + 63) / 64, 64, 0, s>>>((const double*)X, n, ld, D, mean);
+    DA_CHECK_LAUNCH("col_mean_seq_kernel");
+    return 0;
+}
+
+// Chunked variant (used for shard-local sums where exact order is moot).
+int launch_col_mean_chunked(const void* X, int x_f32, long long n, long long ld, int D, double* mean, cudaStream_t s) {
     if (n <= 0) return fail_arg("col_mean: n must be positive");
     int P = (int)min(256LL, max(1LL, n / 2048));
     long long chunk = (n + P - 1) / P;

@@ -352,6 +352,7 @@ int launch_group_sums(const double* X, long long n, long long ldx, int D, const 
     int4* leaves = (int4*)(base + o_leaves);
     double* lsum = (double*)(base + o_lsum);
 
+    ProfScope ps("group_sums", s);
     DA_CUDA(cudaMemsetAsync(hist, 0, sizeof(int32_t) * (KT + 1), s));
     size_t sh = (K <= GS_SMEM_HIST) ? sizeof(int32_t) * K : 0;
     tile_hist_kernel<<<T, 256, sh, s>>>(labels, n, K, T, hist);
@@ -370,6 +371,7 @@ int launch_group_sums(const double* X, long long n, long long ldx, int D, const 
     DA_CHECK_LAUNCH("leaf_enum_kernel");
     {
         long long tasks = max_leaves * n_chunks;
+        ProfScope ps3("group_sums_leaf", s);
         leaf_sum_kernel<<<grid_for(tasks, 8, 1LL << 31), 256, 0, s>>>(X, ldx, D, order, leaves, total + 1,
                                                                       n_chunks, lsum);
         DA_CHECK_LAUNCH("leaf_sum_kernel");

@@ -6,12 +6,22 @@
 
 namespace da {
 
+// RAII timing scope (prof.cu): records a CUDA event pair on stream s when
+// profiling is enabled through da_prof_enable().
+struct ProfScope {
+    ProfScope(const char* name, cudaStream_t s);
+    ~ProfScope();
+    const char* name_;
+    cudaStream_t s_;
+    void* a_;
+};
+
 struct GemmArgs {
     const void* A; int a_f32; long long sai, sak, sA1, sA2; const double* asub; int asub_mode;  // 1: by i, 2: by k
     const void* B; int b_f32; long long sbk, sbj, sB1, sB2; const double* bsub; int bsub_mode;  // 1: by k, 2: by j
     double* C; long long sci, scj, sC1, sC2, sCz;
     long long M, N, K;
-    int nb2, ksplit; long long kchunk;
+    int nb2, ksplit; long long kchunk; const long long* kstarts;  // kstarts[ksplit+1] overrides kchunk
     // epi 0: acc; 1: acc + evec[j]; 2: evec[j] - 2*acc; 3: max(0, (ivec[i] - 2*acc) + evec[j])
     int epi; const double* evec; const double* ivec;
 };
@@ -19,6 +29,9 @@ struct GemmArgs {
 int launch_gemm(const GemmArgs& g, int nb1, cudaStream_t s);
 int launch_reduce_partials(const double* P, int nz, long long len, double scale_div, double* out, cudaStream_t s);
 int launch_col_mean(const void* X, int x_f32, long long n, long long ld, int D, double* mean, cudaStream_t s);
+int launch_col_mean_chunked(const void* X, int x_f32, long long n, long long ld, int D, double* mean, cudaStream_t s);
+int launch_accumulate_partials(const double* P, int nz, long long len, double scale_div, int accumulate,
+                               double* out, cudaStream_t s);
 
 int launch_row_sqnorms(const void* A, int a_is_f32, long long rows, long long lda, int d, double* out,
                        cudaStream_t s);

@@ -328,6 +328,7 @@ int launch_adc_scan(const void* codes, int code_bytes, long long ldc, const doub
     while (warps > 1 && lut_b + (size_t)warps * r * 16 > 200 * 1024) warps >>= 1;
     const size_t smem = lut_b + (size_t)warps * r * 16;
     if (smem > 220 * 1024) return fail_arg("adc_scan: r=%d with M*K=%d exceeds shared memory", r, M * K);
+    ProfScope ps("adc_scan", s);
 #define ADC_LAUNCH(TC)                                                                                       \
     do {                                                                                                     \
         auto kf = adc_scan_kernel<TC>;                                                                       \

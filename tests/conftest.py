@@ -1,7 +1,14 @@
 import os
 import sys
 
-import numpy as np
+# The golden fixtures were produced by the reference with numpy's bundled
+# OpenBLAS running its SkylakeX kernels (oracle/make_golden.py records this in
+# tests/golden/meta.json).  LAPACK's eigh, which both the reference and this
+# build run on the host, depends on those kernels at the ulp level, so the
+# test process pins the same core type before numpy loads.
+os.environ.setdefault("OPENBLAS_CORETYPE", "SkylakeX")
+
+import numpy as np  # noqa: E402
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

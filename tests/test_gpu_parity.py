@@ -3,10 +3,13 @@ and the CPU oracle on the same seeded inputs.
 
 Bars (BASELINE.json north_star): codes bit-exact except where the oracle's
 decision gap is < 1e-6 relative; dictionaries and MSE within 1e-4 relative.
-Where the kernels reproduce numpy's association order exactly (reduceat
-group means, einsum norms, pairwise row sums, heat-up) the test demands
-bit-equality; dot products go through a sequential FMA chain instead of
-BLAS and are held to 1e-12 relative."""
+This build goes further: every float64 reduction follows numpy's / OpenBLAS'
+association order (pairwise row sums, reduceat group means, einsum norms,
+sequential axis-0 means, dgemm/dsyrk k-blocking of 384 with FMA chains), so
+wherever the reference calls a matrix product (not a matrix-vector product)
+the tests demand BIT-EQUALITY with the reference's own outputs, including a
+full config-A training run.  Single-vector paths (numpy routes them to
+dgemv/ddot, whose order is not emulated) are held to 1e-12 relative."""
 
 import numpy as np
 import pytest
@@ -34,7 +37,7 @@ def test_assign_kernel(golden):
     g, c = golden("small_ops.npz"), cases.assign_case()
     lab, d2 = E.assign(E.to_dev(c["X"]), c["active"], E.to_dev(c["C"]))
     np.testing.assert_array_equal(lab.cpu().numpy(), g["assign_labels"])
-    rel_close(d2.cpu().numpy(), g["assign_d2"])
+    np.testing.assert_array_equal(d2.cpu().numpy(), g["assign_d2"])
 
 
 def test_group_means_bit_exact(golden):
@@ -79,8 +82,8 @@ def test_lloyd(golden, which):
     c = cases.lloyd_case() if which == "lloyd" else cases.reseed_case()
     fit = cl.lloyd_kmeans(c["X"], c["C"], active_dims=c.get("active"), max_iters=c["iters"])
     np.testing.assert_array_equal(fit.assignment, g[f"{which}_assign"])
-    rel_close(fit.points, g[f"{which}_points"], atol=1e-12)
-    rel_close(fit.objective_trace, g[f"{which}_trace"])
+    np.testing.assert_array_equal(fit.points, g[f"{which}_points"])
+    np.testing.assert_array_equal(fit.objective_trace, g[f"{which}_trace"])
 
 
 def test_pca(golden):
@@ -88,27 +91,31 @@ def test_pca(golden):
     for key, X in (("pca", c["X"]), ("pcag", c["Xgram"])):
         m = cl.pca_fit(X)
         R, Rg = m.rotation, g[f"{key}_rotation"]
-        signs = np.sign((R * Rg).sum(axis=1))
-        rel_close(R * signs[:, None], Rg, rtol=1e-9, atol=1e-12)
-        rel_close(m.mean, g[f"{key}_mean"], atol=1e-15)
-        rel_close(m.explained_variance, g[f"{key}_var"], rtol=1e-10, atol=1e-14)
+        np.testing.assert_array_equal(R, Rg)
+        np.testing.assert_array_equal(m.mean, g[f"{key}_mean"])
+        np.testing.assert_array_equal(m.explained_variance, g[f"{key}_var"])
 
 
 def test_staged_kmeans(golden):
     g, c = golden("small_ops.npz"), cases.staged_case()
     fit = cl.improved_kmeans(c["X"], c["C"], max_iters=c["iters"])
     np.testing.assert_array_equal(fit.assignment, g["staged_assign"])
-    rel_close(fit.points, g["staged_points"], rtol=1e-9, atol=1e-12)
-    rel_close(fit.objective_trace, g["staged_trace"], rtol=1e-10)
+    # d=12 is not a multiple of 8: OpenBLAS' SkylakeX dsyrk handles the 4-wide
+    # edge of the covariance with a 2-accumulator micro-kernel this build does
+    # not emulate, so the rotation (and everything after it) agrees to ~1e-14
+    # rather than bit-for-bit.  Widths that are multiples of 8 (every BASELINE
+    # config: 32, 128, 960) are bit-exact, see test_config_*.
+    rel_close(fit.points, g["staged_points"], rtol=1e-12, atol=1e-13)
+    rel_close(fit.objective_trace, g["staged_trace"], rtol=1e-12)
 
 
 def test_cross_products(golden):
     g, c = golden("small_ops.npz"), cases.codebook_case()
     cross = cb.cross_products(book_of(c["cw"]))
-    rel_close(cross.products, g["cross_P"], atol=1e-14)
+    np.testing.assert_array_equal(cross.products, g["cross_P"])
     np.testing.assert_array_equal(cross.sq_norms, g["cross_sq"])  # einsum order
     ref = cb.refresh_cross_products(cross, book_of(c["cw2"]), 1)
-    rel_close(ref.products, g["refresh_P"], atol=1e-14)
+    np.testing.assert_array_equal(ref.products, g["refresh_P"])
     np.testing.assert_array_equal(ref.sq_norms, g["refresh_sq"])
 
 
@@ -139,11 +146,11 @@ def test_multipath_and_adc(golden):
     rel_close(t.q_sq_norm, g["adc_qsq"])
     enc = cb.encode_dataset(book, c["X"], beam_width=8)
     pair = cb.code_pair_sums(cross, enc.codes)
-    rel_close(pair, g["pair_sums"], atol=1e-13)
+    np.testing.assert_array_equal(pair, g["pair_sums"])
     ids, dists = cb.exhaustive_adc_search(book, enc, c["q"], 10, cross=cross, pair_sums=pair)
     np.testing.assert_array_equal(ids, g["search_ids"])
     rel_close(dists, g["search_dists"], atol=1e-12)
-    rel_close(cb.distortion(book, c["X"], enc), g["distortion"])
+    assert cb.distortion(book, c["X"], enc) == float(g["distortion"])
 
 
 def test_heat_cool_sweep(golden):
@@ -156,13 +163,13 @@ def test_heat_cool_sweep(golden):
     cfg = da.TrainConfig(m_count=3, k_count=8, sweeps=1, beam_width=8)
     nd, asg = da.cool_down(inter, book, 1, cfg)
     np.testing.assert_array_equal(asg, g["cool_assign"])
-    rel_close(nd, g["cool_dict"], rtol=1e-6)
+    np.testing.assert_array_equal(nd, g["cool_dict"])
     rep = da.TrainReport(config=cfg)
     b2, e2, x2 = da.da_sweep(c["X"], book, enc, cfg, report=rep)
     np.testing.assert_array_equal(e2.codes, g["sweep_codes"])
-    rel_close(b2.codewords, g["sweep_cw"], rtol=1e-6)
-    rel_close(rep.distortions(), g["sweep_dist"], rtol=1e-9)
-    rel_close(x2.products, g["sweep_P"], rtol=1e-6, atol=1e-9)
+    np.testing.assert_array_equal(b2.codewords, g["sweep_cw"])
+    np.testing.assert_array_equal(rep.distortions(), g["sweep_dist"])
+    np.testing.assert_array_equal(x2.products, g["sweep_P"])
     np.testing.assert_array_equal(book.codewords, c["cw"])  # inputs untouched
 
 
@@ -172,16 +179,16 @@ def test_train_small(golden):
     b, e, r = da.train_from_scratch(c["X"], cfg)
     np.testing.assert_array_equal(b.order, g["train_order"])
     np.testing.assert_array_equal(e.codes, g["train_codes"])
-    rel_close(b.codewords, g["train_cw"], rtol=1e-5, atol=1e-7)
-    rel_close(r.distortions(), g["train_dist"], rtol=1e-9)
+    np.testing.assert_array_equal(b.codewords, g["train_cw"])
+    np.testing.assert_array_equal(r.distortions(), g["train_dist"])
     rb, re_ = da.rvq_train(c["X"], cfg)
     np.testing.assert_array_equal(re_.codes, g["rvq_codes"])
-    rel_close(rb.codewords, g["rvq_cw"], rtol=1e-5, atol=1e-7)
+    np.testing.assert_array_equal(rb.codewords, g["rvq_cw"])
     b0 = da.Codebook(codewords=g["train_cw"], order=g["train_order"])
     b3, r3 = da.train_online(b0, c["X2"], cfg)
     np.testing.assert_array_equal(b3.order, g["online_order"])
-    rel_close(b3.codewords, g["online_cw"], rtol=1e-5, atol=1e-7)
-    rel_close(r3.distortions(), g["online_dist"], rtol=1e-9)
+    np.testing.assert_array_equal(b3.codewords, g["online_cw"])
+    np.testing.assert_array_equal(r3.distortions(), g["online_dist"])
 
 
 def _frob_rel(a, b):
@@ -197,12 +204,11 @@ def test_config_a_full_training(golden):
     cfg = da.TrainConfig(m_count=4, k_count=256, beam_width=10, sweeps=3, rel_tol=0.0)
     b, e, r = da.train_from_scratch(X, cfg)
     np.testing.assert_array_equal(b.order, g["order"])
-    assert _frob_rel(b.codewords, g["cw"]).max() <= 1e-4
-    same = (e.codes == g["codes"]).all(axis=1).mean()
-    assert same >= 0.999, same
-    mse = cb.distortion(b, X, e)
-    assert abs(mse - float(g["mse"])) <= 1e-4 * float(g["mse"])
-    rel_close(r.distortions(), g["dist"], rtol=1e-4)
+    # bit-identical to the reference's 16-step training run
+    np.testing.assert_array_equal(b.codewords, g["cw"])
+    np.testing.assert_array_equal(e.codes, g["codes"])
+    np.testing.assert_array_equal(r.distortions(), g["dist"])
+    assert cb.distortion(b, X, e) == float(g["mse"])
 
 
 def test_config_b_subsample(golden):
@@ -215,11 +221,14 @@ def test_config_b_subsample(golden):
     Xt, Xe = X[: cases.B_TRAIN], X[cases.B_TRAIN:]
     cfg = da.TrainConfig(m_count=8, k_count=256, beam_width=10, sweeps=0, rel_tol=0.0)
     b, e, r = da.train_from_scratch(Xt, cfg)
-    assert _frob_rel(b.codewords, g["cw"]).max() <= 1e-4
-    assert (e.codes == g["train_codes"]).all(axis=1).mean() >= 0.999
-    # encode with the reference's codebook: per-vector exact except oracle near-ties
+    np.testing.assert_array_equal(b.codewords, g["cw"])
+    np.testing.assert_array_equal(e.codes, g["train_codes"])
+    np.testing.assert_array_equal(r.distortions(), g["train_dist"])
+    # encode with the reference's codebook; the north-star bar (exact except
+    # oracle near-ties < 1e-6) is checked first, then bit-equality.
     ref_book = da.Codebook(codewords=g["cw"], order=g["order"])
     cross = cb.cross_products(ref_book)
+    cw_d, sq_d = cb._codebook_dev(ref_book)
     for L in (1, 10):
         enc = cb.encode_dataset(ref_book, Xe, beam_width=L, cross=cross)
         bad = np.flatnonzero((enc.codes != g[f"enc_codes_L{L}"]).any(axis=1))
@@ -227,13 +236,16 @@ def test_config_b_subsample(golden):
             gaps = O.beam_min_gap(g["cw"].astype(np.float64), O.cross_table(g["cw"])[0],
                                   Xe[bad].astype(np.float64), L)
             assert (gaps < 1e-6).all(), (L, bad, gaps)
+        np.testing.assert_array_equal(enc.codes, g[f"enc_codes_L{L}"])
+        _, err = E.encode(E.to_dev(Xe), cw_d, sq_d, cross.device()[0], L)
+        np.testing.assert_array_equal(err.cpu().numpy(), g[f"enc_errs_L{L}"])
     # one annealing pass from the reference's growth result
     cfg1 = da.TrainConfig(m_count=8, k_count=256, beam_width=10, sweeps=1, rel_tol=0.0)
     enc0 = da.EncodedDataset(g["train_codes"], 256)
     b2, e2, _ = da.da_sweep(Xt, ref_book, enc0, cfg1, report=(rep := da.TrainReport()))
-    assert _frob_rel(b2.codewords, g["sweep_cw"]).max() <= 1e-4
-    assert (e2.codes == g["sweep_codes"]).all(axis=1).mean() >= 0.999
-    rel_close(rep.distortions(), g["sweep_dist"], rtol=1e-4)
+    np.testing.assert_array_equal(b2.codewords, g["sweep_cw"])
+    np.testing.assert_array_equal(e2.codes, g["sweep_codes"])
+    np.testing.assert_array_equal(rep.distortions(), g["sweep_dist"])
     # ADC top-100
     Q = synthetic.config_e_queries(16)
     encx = da.EncodedDataset(g["enc_codes_L10"], 256)
@@ -255,8 +267,12 @@ def test_config_c_subsample(golden):
     Xt, Xe = X[: cases.C_TRAIN], X[cases.C_TRAIN:]
     cfg = da.TrainConfig(m_count=4, k_count=256, beam_width=10, sweeps=0, rel_tol=0.0)
     b, e, r = da.train_from_scratch(Xt, cfg)
-    assert _frob_rel(b.codewords, g["cw"]).max() <= 1e-4
-    assert (e.codes == g["train_codes"]).all(axis=1).mean() >= 0.999
+    # D=960: agreement to a float32 ulp on ~8% of codeword entries (one of the
+    # >384 k-blocked products differs from OpenBLAS at the ulp level); codes
+    # and the reported distortions are identical.
+    assert _frob_rel(b.codewords, g["cw"]).max() <= 1e-6
+    np.testing.assert_array_equal(e.codes, g["train_codes"])
+    rel_close(r.distortions(), g["train_dist"], rtol=1e-9)
     ref_book = da.Codebook(codewords=g["cw"], order=g["order"])
     enc = cb.encode_dataset(ref_book, Xe, beam_width=10)
     bad = np.flatnonzero((enc.codes != g["enc_codes"]).any(axis=1))
@@ -264,3 +280,4 @@ def test_config_c_subsample(golden):
         gaps = O.beam_min_gap(g["cw"].astype(np.float64), O.cross_table(g["cw"])[0],
                               Xe[bad].astype(np.float64), 10)
         assert (gaps < 1e-6).all(), (bad, gaps)
+    np.testing.assert_array_equal(enc.codes, g["enc_codes"])
