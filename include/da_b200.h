@@ -52,6 +52,12 @@ int da_assign(const void* X, int x_f32, int64_t n, int64_t ldx, int d, const dou
               const double* cc, int32_t* labels, double* d2, const int32_t* prev, unsigned long long* changed,
               void* stream);
 
+/* Assign selection: mode 0 (default) = tcgen05 3xTF32 distance tiles in TMEM +
+ * rigorous bound + exact float64 recheck (K <= 256; same labels/d2 as mode 1);
+ * mode 1 = plain float64 FMA kernel.  candidate_counter (device, optional)
+ * accumulates the number of exactly rechecked (row, codeword) pairs. */
+int da_assign_config(int mode, unsigned long long* candidate_counter);
+
 /* Per-label sums (mode 1) or means written into the non-empty rows of out (mode 0),
  * over all D columns, bit-identical to argsort(stable)+add.reduceat.
  * replaces _group_means                         clustering.py:151-162 */
@@ -113,6 +119,12 @@ int da_cross_products(const float* cw, int M, int K, int D, int only_m, double* 
 int da_encode(const void* X, int x_f32, int64_t n, int64_t ldx, int D, const float* cw, int M, int K, int L,
               const double* sq, const double* P, void* codes, int code_bytes, int64_t ldcodes, double* err,
               void* stream);
+
+/* Encoder selection: mode 0 (default) = fp32 score tables + rigorous error bound +
+ * exact float64 recheck of the candidates that can still make the beam (same
+ * codes/errors as mode 1); mode 1 = plain float64 tables.  recheck_counter (device,
+ * optional) accumulates the number of exactly rechecked candidates. */
+int da_encode_config(int mode, unsigned long long* recheck_counter);
 
 /* Query-independent ADC term 2 sum_{a<b} P[a,b][i_a,i_b].  replaces code_pair_sums codebook.py:388-396 */
 int da_pair_sums(const void* codes, int code_bytes, int64_t n, int64_t ldc, const double* P, int M, int K,

@@ -404,6 +404,18 @@ def encode(X: torch.Tensor, cw: torch.Tensor, sq: torch.Tensor, Pt: torch.Tensor
     return codes, err
 
 
+def assign_config(mode: int, counter: torch.Tensor | None = None) -> None:
+    """0 = tcgen05 3xTF32 filter with exact float64 recheck (default, K <= 256),
+    1 = plain float64 kernel.  `counter` accumulates rechecked (row, codeword) pairs."""
+    native.da_assign_config(int(mode), P(counter))
+
+
+def encode_config(mode: int, counter: torch.Tensor | None = None) -> None:
+    """0 = filtered fp32 fast path with exact float64 recheck (default),
+    1 = plain float64 tables.  `counter` (int64 CUDA tensor) accumulates rechecks."""
+    native.da_encode_config(int(mode), P(counter))
+
+
 def pair_sums(codes: torch.Tensor, Pt: torch.Tensor) -> torch.Tensor:
     n, M = codes.shape
     K = Pt.shape[2]

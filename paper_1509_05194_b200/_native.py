@@ -44,6 +44,8 @@ _SIGNATURES = {
     "da_np_sum": [_P, _L, _I, _P, _P],
     "da_select_better": [_L, _I, _P, _P, _P, _P, _P],
     "da_set_column": [_P, _L, _I, _I, _P, _P],
+    "da_encode_config": [_I, _P],
+    "da_assign_config": [_I, _P],
     "da_release_scratch": [],
     "da_prof_enable": [_I],
     "da_prof_collect": [ctypes.c_char_p, _I],

@@ -188,12 +188,25 @@ int launch_row_sqnorms(const void* A, int a_is_f32, long long rows, long long ld
     return 0;
 }
 
+static int g_assign_mode = 0;  // 0: tensor-core filter + exact recheck when K <= 256; 1: plain float64
+static unsigned long long* g_assign_stats = nullptr;
+
+int set_assign_config(int mode, unsigned long long* stats) {
+    g_assign_mode = mode;
+    g_assign_stats = stats;
+    return 0;
+}
+
 int launch_assign(const void* X, int x_is_f32, long long n, long long ldx, int d, const double* C,
                   long long ldc, int K, const double* cc, int32_t* labels, double* d2,
                   const int32_t* prev, unsigned long long* changed, cudaStream_t s) {
     if (n <= 0) return 0;
+    if (g_assign_mode == 0) {
+        int rc = launch_assign_tc(X, x_is_f32, n, ldx, d, C, ldc, K, cc, labels, d2, prev, changed, g_assign_stats, s);
+        if (rc <= 0) return rc;
+    }
     unsigned g = grid_for(n, AS_BM, 1LL << 31);
-    ProfScope ps("assign", s);
+    ProfScope ps(d <= 8 ? "assign_d<=8" : d <= 32 ? "assign_d<=32" : d <= 128 ? "assign_d<=128" : "assign_d>128", s);
     const bool blk = d > BLAS_Q;
 #define AS_LAUNCH(T, B) assign_kernel<T, B><<<g, AS_THREADS, 0, s>>>((const T*)X, n, ldx, d, C, ldc, K, cc, labels, \
                                                                   d2, prev, changed)

@@ -1,0 +1,542 @@
+// Filtered beam encoder: fp32 fast path + exact float64 recheck.
+//
+// Same contract as encode.cu (annq/codebook.py:255-300, bit-exact result), but
+// the full float64 score table and the float64 cross-term gathers are only
+// computed for candidates that can still make the beam:
+//
+//   1. t'[m,k] = sq32 - 2 x.c in FP32 (SGEMM, FFMA, 128x128 tiles).
+//   2. per stage and vector, v'(l,k) = s_l + t'[m,k] + 2 sum_{j<m} P32[j,m][c_lj,k]
+//      for every candidate, with a rigorous bound |v' - v| <= E (fp32 rounding of
+//      the dot products, of the table entries and of the additions; see
+//      stage_bound below).
+//   3. tau' = an upper bound of the width-th smallest v' (the width-th smallest
+//      of the two smallest per lane).  No candidate with v' > tau' + 2E can be
+//      among the exact top-width (proof in DESIGN.md), so only candidates with
+//      v' <= tau' + 2E are recomputed in float64 exactly as the reference does
+//      (BLAS-ordered x.c, einsum ||c||^2, sequential cross sum) and go through the
+//      exact (value, flat index) top-width selection.
+// Beam scores are always the exact float64 values, so codes and errors equal
+// the reference's; only the amount of float64 work changes.
+#include "common.cuh"
+#include "internal.h"
+
+namespace da {
+
+// ---------------------------------------------------------------------------
+// SGEMM for the approximate score table: T[i, j] = sq32[j] - 2 * sum_k X[i,k] C[j,k]
+namespace {
+constexpr int SG_BM = 128, SG_BN = 128, SG_BK = 8, SG_T = 256;
+constexpr int QCAP = 224;  // per-warp recheck queue
+}
+
+__global__ void __launch_bounds__(SG_T) sgemm_table_kernel(const float* __restrict__ X, long long n, long long ldx,
+                                                           const float* __restrict__ Cw, int N, int D,
+                                                           const float* __restrict__ sq32, float* __restrict__ T,
+                                                           long long ldt) {
+    __shared__ __align__(16) float As[2][SG_BK][SG_BM];
+    __shared__ __align__(16) float Bs[2][SG_BK][SG_BN];
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;
+    const long long i0 = (long long)blockIdx.y * SG_BM;
+    const int j0 = blockIdx.x * SG_BN;
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    // each thread loads 4 A elements and 4 B elements per k-tile
+    const int lr = tid >> 1;          // row within tile (0..127)
+    const int lk = (tid & 1) * 4;     // k offset 0 or 4
+    float ra[4], rb[4];
+    auto load = [&](int k0) {
+        long long gr = i0 + lr;
+        int gc = j0 + lr;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            int gk = k0 + lk + u;
+            ra[u] = (gr < n && gk < D) ? X[gr * ldx + gk] : 0.f;
+            rb[u] = (gc < N && gk < D) ? Cw[(long long)gc * D + gk] : 0.f;
+        }
+    };
+    auto store = [&](int buf) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            As[buf][lk + u][lr] = ra[u];
+            Bs[buf][lk + u][lr] = rb[u];
+        }
+    };
+    load(0);
+    store(0);
+    __syncthreads();
+    int buf = 0;
+    for (int k0 = 0; k0 < D; k0 += SG_BK) {
+        const bool more = k0 + SG_BK < D;
+        if (more) load(k0 + SG_BK);
+#pragma unroll
+        for (int k = 0; k < SG_BK; ++k) {
+            float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][ty * 4]);
+            float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][64 + ty * 4]);
+            float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][k][tx * 4]);
+            float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][k][64 + tx * 4]);
+            float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        if (more) {
+            store(buf ^ 1);
+            __syncthreads();
+            buf ^= 1;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        long long gr = i0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+        if (gr >= n) continue;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            int gc = j0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
+            if (gc < N) T[gr * ldt + gc] = sq32[gc] - 2.f * acc[i][j];
+        }
+    }
+}
+
+// per-dictionary bound inputs: cmax[m] = max_k ||c_mk||, crossb[m] = sum_{j<m} max|P[j,m]|
+__global__ void bound_prep_kernel(const float* __restrict__ cw, const double* __restrict__ P, int M, int K, int D,
+                                  const double* __restrict__ sq, float* __restrict__ P32, float* __restrict__ sq32,
+                                  double* __restrict__ cmax, double* __restrict__ pabs, double* __restrict__ cw64) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)M * K * D;
+         e += (long long)gridDim.x * blockDim.x)
+        cw64[e] = (double)cw[e];
+    // grid: (M*M) blocks for the table conversion + maxima; block 0..M-1 also do norms
+    const int pair = blockIdx.x;
+    const int a = pair / M, b = pair % M;
+    __shared__ double red[256];
+    double mx = 0.0;
+    const long long base = (long long)pair * K * K;
+    for (long long e = threadIdx.x; e < (long long)K * K; e += blockDim.x) {
+        double v = P[base + e];
+        P32[base + e] = (float)v;
+        mx = fmax(mx, fabs(v));
+    }
+    red[threadIdx.x] = mx;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) pabs[a * M + b] = red[0];
+    __syncthreads();
+    if (b == 0) {
+        // norms of dictionary a
+        double cm = 0.0;
+        for (int k = threadIdx.x; k < K; k += blockDim.x) {
+            double s = sq[a * K + k];
+            sq32[a * K + k] = (float)s;
+            cm = fmax(cm, sqrt(s));
+        }
+        red[threadIdx.x] = cm;
+        __syncthreads();
+        for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+            if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) cmax[a] = red[0] * (1.0 + 1e-12);
+    }
+}
+
+// ---------------------------------------------------------------------------
+
+struct FastSmem {
+    int32_t* codes[2];
+    double* score[2];
+    double* lv;
+    int32_t* lf;
+    double* x64;     // [D]
+    float* vbuf;     // [cap*K] approximate values; reused as D doubles for the error
+    int32_t* queue;  // [33 + QCAP]: [32] = count, [33..] = queued flat indices
+};
+
+__host__ __device__ inline size_t fast_vbuf_bytes(int cap, int K, int D) {
+    size_t a = sizeof(float) * (size_t)cap * K, b = sizeof(double) * (size_t)D;
+    return ((a > b ? a : b) + 15) & ~size_t(15);
+}
+
+__host__ __device__ inline size_t fast_smem_bytes(int cap, int M, int K, int D) {
+    size_t b = sizeof(double) * (3 * (size_t)cap + D);
+    b = (b + 15) & ~size_t(15);
+    b += fast_vbuf_bytes(cap, K, D);
+    b += sizeof(int32_t) * (2 * (size_t)cap * M + cap + 33 + QCAP);
+    return (b + 15) & ~size_t(15);
+}
+
+__device__ inline FastSmem carve_fast(char* p, int cap, int M, int K, int D) {
+    FastSmem s;
+    char* p0 = p;
+    s.score[0] = (double*)p; p += sizeof(double) * cap;
+    s.score[1] = (double*)p; p += sizeof(double) * cap;
+    s.lv = (double*)p; p += sizeof(double) * cap;
+    s.x64 = (double*)p; p += sizeof(double) * D;
+    p = p0 + (((size_t)(p - p0) + 15) & ~size_t(15));
+    s.vbuf = (float*)p; p += fast_vbuf_bytes(cap, K, D);
+    s.codes[0] = (int32_t*)p; p += sizeof(int32_t) * cap * M;
+    s.codes[1] = (int32_t*)p; p += sizeof(int32_t) * cap * M;
+    s.lf = (int32_t*)p; p += sizeof(int32_t) * cap;
+    s.queue = (int32_t*)p;
+    return s;
+}
+
+// exact x.c (reference order: FMA chain over d, OpenBLAS k-blocks above 384)
+__device__ __forceinline__ double exact_dot(const double* __restrict__ x64, const double* __restrict__ c, int D) {
+    double tot = 0.0;
+    bool first = true;
+    int d = 0;
+    while (d < D) {
+        const int len = (int)blas_block_len(D - d);
+        double acc = 0.0;
+        const int e = d + len;
+        // loads run ahead of the (strictly sequential) FMA chain
+        for (; d + 8 <= e; d += 8) {
+            double cv[8];
+            double xv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) { cv[u] = __ldg(c + d + u); xv[u] = x64[d + u]; }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = __fma_rn(xv[u], cv[u], acc);
+        }
+        for (; d < e; ++d) acc = __fma_rn(x64[d], c[d], acc);
+        tot = first ? acc : dadd(tot, acc);
+        first = false;
+    }
+    return tot;
+}
+
+template <typename TX>
+__global__ void __launch_bounds__(256) beam_fast_kernel(
+    const TX* __restrict__ X, long long n, long long ldx, int D, const float* __restrict__ cw, int M, int K, int L,
+    int cap, const float* __restrict__ tab32, const double* __restrict__ sq, const double* __restrict__ P,
+    const float* __restrict__ P32, const double* __restrict__ cmax, const double* __restrict__ pabs,
+    const double* __restrict__ cw64, void* codes_out,
+    int code_bytes, long long ldcodes, double* __restrict__ err_out, unsigned long long* __restrict__ stats) {
+    extern __shared__ __align__(16) char smem_raw[];
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    const long long v = (long long)blockIdx.x * nwarps + wid;
+    if (v >= n) return;
+    FastSmem S = carve_fast(smem_raw + (size_t)wid * fast_smem_bytes(cap, M, K, D), cap, M, K, D);
+    const float* trow = tab32 + v * (long long)M * K;
+    const TX* xr = X + v * ldx;
+    // x in float64 (exact widening) and ||x||
+    double xx_part = 0.0;
+    for (int d = lane; d < D; d += 32) {
+        double t = (double)xr[d];
+        S.x64[d] = t;
+        xx_part = __fma_rn(t, t, xx_part);
+    }
+    for (int off = 16; off >= 1; off >>= 1) xx_part += __shfl_xor_sync(FULL, xx_part, off);
+    const double xnorm = sqrt(xx_part) * (1.0 + 1e-12);
+    if (lane == 0) S.score[0][0] = 0.0;
+    __syncwarp();
+    const double u = 5.9604644775390625e-08;  // 2^-24
+    unsigned long long n_exact = 0;
+
+    int cur = 0, live = 1;
+    for (int m = 0; m < M; ++m) {
+        const int total = live * K;
+        const int width = min(L, total);
+        const int32_t* pc = S.codes[cur];
+        const double* ps = S.score[cur];
+        // ---- rigorous bound of |v' - v| for this stage
+        double smax = 0.0;
+        for (int l = lane; l < live; l += 32) smax = fmax(smax, fabs(ps[l]));
+        for (int off = 16; off >= 1; off >>= 1) smax = fmax(smax, __shfl_xor_sync(FULL, smax, off));
+        double cb = 0.0;
+        for (int j = 0; j < m; ++j) cb += pabs[j * M + m];
+        const double cm = cmax[m];
+        const double tmax = cm * cm + 2.0 * xnorm * cm;
+        const double e_t = (2.0 * D + 8.0) * u * (xnorm * cm + cm * cm);
+        const double e_cross = (m + 2.0) * u * cb;
+        const double E = 2.0 * (e_t + 2.0 * e_cross + 4.0 * u * (smax + tmax + 2.0 * cb) + u * smax) + 1e-300;
+
+        // ---- pass A: approximate candidate values, two smallest per lane.
+        // Lanes own k = kb + 32q + lane (q < 8); four beams are processed together
+        // so every lane keeps 32 independent L2 gathers in flight per term j.
+        float m1 = __int_as_float(0x7f800000), m2 = m1;
+        for (int kb = 0; kb < K; kb += 256) {
+            float tk[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int k = kb + q * 32 + lane;
+                tk[q] = (k < K) ? trow[m * K + k] : 0.f;
+            }
+            for (int l0 = 0; l0 < live; l0 += 4) {
+                float acc[4][8];
+#pragma unroll
+                for (int g = 0; g < 4; ++g)
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) acc[g][q] = 0.f;
+                for (int j = 0; j < m; ++j) {
+                    const float* rp[4];
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        const int l = min(l0 + g, live - 1);
+                        rp[g] = P32 + (((long long)j * M + m) * K + pc[l * M + j]) * K + kb + lane;
+                    }
+                    float vals[4][8];
+#pragma unroll
+                    for (int g = 0; g < 4; ++g)
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            vals[g][q] = (kb + q * 32 + lane < K) ? __ldg(rp[g] + q * 32) : 0.f;
+#pragma unroll
+                    for (int g = 0; g < 4; ++g)
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) acc[g][q] += vals[g][q];
+                }
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const int l = l0 + g;
+                    if (l >= live) break;
+                    const float sl = (float)ps[l];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int k = kb + q * 32 + lane;
+                        if (k < K) {
+                            const float vv = (sl + tk[q]) + 2.f * acc[g][q];
+                            S.vbuf[l * K + k] = vv;
+                            if (vv < m1) { m2 = m1; m1 = vv; }
+                            else if (vv < m2) m2 = vv;
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        // ---- threshold: width-th smallest of the 64 per-lane minima (valid upper
+        // bound of the width-th smallest candidate when width <= 64)
+        float thr;
+        if (width >= total) {
+            thr = __int_as_float(0x7f800000);
+        } else if (width <= 64) {
+            // bitonic sort of 64 values (2 per lane: index lane and lane+32)
+            // rank of each of the 64 values (position lane / lane+32), ties by position
+            const float a = m1, b = m2;
+            float key0 = a, key1 = b;
+            int r0 = 0, r1 = 0;
+            for (int s = 0; s < 32; ++s) {
+                float o0 = __shfl_sync(FULL, a, s), o1 = __shfl_sync(FULL, b, s);
+                r0 += (o0 < key0) || (o0 == key0 && s < lane);
+                r0 += (o1 < key0) || (o1 == key0 && s + 32 < lane);
+                r1 += (o0 < key1) || (o0 == key1 && s < lane + 32);
+                r1 += (o1 < key1) || (o1 == key1 && s + 32 < lane + 32);
+            }
+            float t0 = (r0 == width - 1) ? key0 : -__int_as_float(0x7f800000);
+            float t1 = (r1 == width - 1) ? key1 : -__int_as_float(0x7f800000);
+            float t = fmaxf(t0, t1);
+            for (int off = 16; off >= 1; off >>= 1) t = fmaxf(t, __shfl_xor_sync(FULL, t, off));
+            thr = t;
+        } else {
+            thr = __int_as_float(0x7f800000);  // wide beams: recheck everything
+        }
+        const double lim = (double)thr + 2.0 * E;
+
+        // ---- pass B: exact recheck of every candidate with v' <= tau' + 2E
+        int cnt = 0;
+        auto accept = [&](double a, int fa) -> bool {
+            if (cnt < width) return true;
+            return lex_less(a, fa, S.lv[width - 1], S.lf[width - 1]);
+        };
+        // candidates to recheck, pushed by each lane from its own positions; the
+        // processing order is irrelevant (the exact list is ordered by (value, flat))
+        const float limf = (lim >= 3.0e38) ? __int_as_float(0x7f800000) : __fadd_ru((float)lim, fabsf((float)lim) * 1e-6f);
+        int* qcount = S.queue + 32;  // [0] = count
+        if (lane == 0) *qcount = 0;
+        __syncwarp();
+        for (int i = lane; i < total; i += 32) {
+            if (S.vbuf[i] <= limf) {
+                const int slot = atomicAdd(qcount, 1);
+                if (slot < QCAP) S.queue[33 + slot] = i;
+            }
+        }
+        __syncwarp();
+        int nqueued = *qcount;
+        if (nqueued > QCAP) {
+            // rare: too many near-boundary candidates; recheck all of them in flat order
+            nqueued = -1;
+        }
+        __syncwarp();
+        auto flush = [&](int base_i, int nq, bool from_queue) {
+            double val = 0.0;
+            int flat = 0;
+            const bool has = lane < nq;
+            if (has) {
+                flat = from_queue ? S.queue[33 + base_i + lane] : base_i + lane;
+                const int l = flat / K, k = flat % K;
+                const double xc = exact_dot(S.x64, cw64 + ((long long)m * K + k) * D, D);
+                const double t = dsub(sq[m * K + k], dmul(2.0, xc));
+                double cross = 0.0;
+                for (int j = 0; j < m; ++j)
+                    cross = dadd(cross, P[(((long long)j * M + m) * K + pc[l * M + j]) * K + k]);
+                val = dadd(dadd(ps[l], t), dmul(2.0, cross));
+            }
+            n_exact += has ? 1 : 0;
+            unsigned mask = __ballot_sync(FULL, has && accept(val, flat));
+            while (mask) {
+                const int src = __ffs(mask) - 1;
+                const double cv = __shfl_sync(FULL, val, src);
+                const int cf = __shfl_sync(FULL, flat, src);
+                int pos = 0;
+                for (int b = 0; b < cnt; b += 32) {
+                    int i = b + lane;
+                    bool lt = (i < cnt) && lex_less(S.lv[i], S.lf[i], cv, cf);
+                    pos += __popc(__ballot_sync(FULL, lt));
+                }
+                const int end = min(cnt, width - 1);
+                for (int b = end - 1; b >= pos; b -= 32) {
+                    int i = b - lane;
+                    bool act = i >= pos;
+                    double tv = 0.0;
+                    int tf = 0;
+                    if (act) { tv = S.lv[i]; tf = S.lf[i]; }
+                    __syncwarp();
+                    if (act) { S.lv[i + 1] = tv; S.lf[i + 1] = tf; }
+                    __syncwarp();
+                }
+                if (lane == 0) { S.lv[pos] = cv; S.lf[pos] = cf; }
+                __syncwarp();
+                cnt = min(cnt + 1, width);
+                mask &= ~(1u << src);
+                mask &= __ballot_sync(FULL, has && accept(val, flat));
+            }
+        };
+        if (nqueued >= 0) {
+            for (int b = 0; b < nqueued; b += 32) flush(b, min(32, nqueued - b), true);
+        } else {
+            for (int b = 0; b < total; b += 32) flush(b, min(32, total - b), false);
+        }
+        __syncwarp();
+
+        // ---- next beam in flat (lexicographic) order
+        const int nxt = cur ^ 1;
+        int32_t* nc = S.codes[nxt];
+        double* ns = S.score[nxt];
+        for (int b = 0; b < width; b += 32) {
+            int i = b + lane;
+            if (i < width) {
+                const int fi = S.lf[i];
+                int rank = 0;
+                for (int j = 0; j < width; ++j) rank += (S.lf[j] < fi);
+                const int parent = fi / K, kk = fi % K;
+                for (int j = 0; j < m; ++j) nc[rank * M + j] = pc[parent * M + j];
+                nc[rank * M + m] = kk;
+                ns[rank] = S.lv[i];
+            }
+        }
+        __syncwarp();
+        cur = nxt;
+        live = width;
+    }
+
+    double bv = __longlong_as_double(0x7ff0000000000000ULL);
+    int bi = 0x7fffffff;
+    for (int i = lane; i < live; i += 32) {
+        double s = S.score[cur][i];
+        if (lex_less(s, i, bv, bi)) { bv = s; bi = i; }
+    }
+    for (int off = 16; off >= 1; off >>= 1) {
+        double ov = __shfl_xor_sync(FULL, bv, off);
+        int oi = __shfl_xor_sync(FULL, bi, off);
+        if (lex_less(ov, oi, bv, bi)) { bv = ov; bi = oi; }
+    }
+    const int32_t* best = S.codes[cur] + (long long)bi * M;
+    for (int j = lane; j < M; j += 32) {
+        int c = best[j];
+        if (code_bytes == 1) ((uint8_t*)codes_out)[v * ldcodes + j] = (uint8_t)c;
+        else if (code_bytes == 2) ((uint16_t*)codes_out)[v * ldcodes + j] = (uint16_t)c;
+        else ((int32_t*)codes_out)[v * ldcodes + j] = c;
+    }
+    if (stats) {
+        for (int off = 16; off >= 1; off >>= 1) n_exact += __shfl_xor_sync(FULL, n_exact, off);
+        if (lane == 0) atomicAdd(stats, n_exact);
+    }
+    if (err_out) {
+        // exact error, numpy pairwise over d; diff^2 staged in vbuf (as doubles)
+        double* dd = reinterpret_cast<double*>(S.vbuf);
+        __syncwarp();
+        for (int d = lane; d < D; d += 32) {
+            double r = 0.0;
+            for (int j = 0; j < M; ++j) r = dadd(r, (double)cw[((long long)j * K + best[j]) * D + d]);
+            double df = dsub(S.x64[d], r);
+            dd[d] = dmul(df, df);
+        }
+        __syncwarp();
+        if (lane == 0) err_out[v] = np_pw_sum([&](long long i) { return dd[i]; }, 0, D);
+    }
+}
+
+int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int D, const float* cw, int M, int K,
+                       int L, const double* sq, const double* P, void* codes_out, int code_bytes, long long ldcodes,
+                       double* err_out, unsigned long long* stats, cudaStream_t s) {
+    if (n <= 0) return 0;
+    long long capll = 1;
+    for (int m = 0; m < M && capll < L; ++m) capll *= K;
+    const int cap = (int)std::min((long long)L, capll);
+    const size_t per_warp = fast_smem_bytes(cap, M, K, D);
+    int warps = 8;
+    while (warps > 1 && per_warp * warps > 200 * 1024) warps >>= 1;
+    if (per_warp * warps > 220 * 1024) return 1;  // caller falls back to the plain encoder
+    const size_t smem = per_warp * warps;
+    // bound inputs + fp32 copies of the tables
+    const size_t pe = (size_t)M * M * K * K;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
+    const size_t o_p32 = take(sizeof(float) * pe), o_sq32 = take(sizeof(float) * M * K);
+    const size_t o_cmax = take(sizeof(double) * M), o_pabs = take(sizeof(double) * M * M);
+    const size_t o_cw64 = take(sizeof(double) * (size_t)M * K * D);
+    char* base = (char*)scratch(7, off, s);
+    if (!base) return fail_cuda(cudaErrorMemoryAllocation, "encode_fast scratch");
+    float* P32 = (float*)(base + o_p32);
+    float* sq32 = (float*)(base + o_sq32);
+    double* cmax = (double*)(base + o_cmax);
+    double* pabs = (double*)(base + o_pabs);
+    double* cw64 = (double*)(base + o_cw64);
+    bound_prep_kernel<<<M * M, 256, 0, s>>>(cw, P, M, K, D, sq, P32, sq32, cmax, pabs, cw64);
+    DA_CHECK_LAUNCH("bound_prep_kernel");
+
+    auto kf = x_f32 ? (const void*)beam_fast_kernel<float> : (const void*)beam_fast_kernel<double>;
+    if (smem > 48 * 1024) DA_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const long long row_bytes = (long long)M * K * sizeof(float);
+    long long chunk = std::max(1024LL, (1LL << 30) / row_bytes);
+    chunk = std::min(chunk, n);
+    float* tab = (float*)scratch(8, (size_t)(chunk * row_bytes), s);
+    if (!tab) return fail_cuda(cudaErrorMemoryAllocation, "encode_fast table scratch");
+    const int N = M * K;
+    for (long long c0 = 0; c0 < n; c0 += chunk) {
+        const long long cn = std::min(chunk, n - c0);
+        {
+            ProfScope ps("encode_table_sgemm", s);
+            if (x_f32) {
+                dim3 grid((N + SG_BN - 1) / SG_BN, (unsigned)((cn + SG_BM - 1) / SG_BM));
+                sgemm_table_kernel<<<grid, SG_T, 0, s>>>((const float*)X + c0 * ldx, cn, ldx, cw, N, D, sq32, tab, N);
+                DA_CHECK_LAUNCH("sgemm_table_kernel");
+            } else {
+                return fail_arg("encode_fast: float32 input only");
+            }
+        }
+        ProfScope ps2("encode_beam_fast", s);
+        const unsigned grid = (unsigned)((cn + warps - 1) / warps);
+        void* cout = (char*)codes_out + (size_t)c0 * ldcodes * code_bytes;
+        double* eout = err_out ? err_out + c0 : nullptr;
+        beam_fast_kernel<float><<<grid, warps * 32, smem, s>>>((const float*)X + c0 * ldx, cn, ldx, D, cw, M, K, L,
+                                                               cap, tab, sq, P, P32, cmax, pabs, cw64, cout, code_bytes,
+                                                               ldcodes, eout, stats);
+        DA_CHECK_LAUNCH("beam_fast_kernel");
+    }
+    return 0;
+}
+
+}  // namespace da

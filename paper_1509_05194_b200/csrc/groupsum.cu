@@ -22,7 +22,7 @@
 namespace da {
 
 namespace {
-constexpr int GS_TILE = 1024;      // rows per sort tile
+constexpr int GS_TILE = 4096;      // rows per sort tile
 constexpr int GS_SMEM_HIST = 12288; // labels that fit a shared-memory histogram
 constexpr int GS_COLS = 128;       // columns per warp task (4 per lane)
 }  // namespace
@@ -94,28 +94,40 @@ __global__ void seg_counts_kernel(const int32_t* __restrict__ offs, int K, int T
 }
 
 // One warp per tile: stable scatter of row ids into their label segment.
-__global__ void stable_scatter_kernel(const int32_t* __restrict__ labels, long long n, int T,
+// Cursors live in shared memory when K fits (GS_SMEM_HIST), else in the
+// tile's column of the scanned histogram in global memory.
+__global__ void stable_scatter_kernel(const int32_t* __restrict__ labels, long long n, int K, int T,
                                       int32_t* __restrict__ cursor, int32_t* __restrict__ order) {
+    extern __shared__ int32_t scur[];
     const int t = blockIdx.x;
     const int lane = threadIdx.x;
     const long long lo = (long long)t * GS_TILE;
     const long long hi = min(n, lo + GS_TILE);
     const unsigned lt_mask = (1u << lane) - 1u;
+    const bool sm = K <= GS_SMEM_HIST;
+    if (sm) {
+        for (int k = lane; k < K; k += 32) scur[k] = cursor[(long long)k * T + t];
+        __syncwarp();
+    }
+    int lab_next = (lo + lane < hi) ? labels[lo + lane] : 0;
     for (long long base = lo; base < hi; base += 32) {
-        long long r = base + lane;
-        bool valid = r < hi;
-        unsigned active = __ballot_sync(0xffffffffu, valid);
+        const long long r = base + lane;
+        const bool valid = r < hi;
+        const int lab = lab_next;
+        lab_next = (r + 32 < hi) ? labels[r + 32] : 0;  // prefetch the next group
+        const unsigned active = __ballot_sync(0xffffffffu, valid);
         if (valid) {
-            int lab = labels[r];
-            unsigned peers = __match_any_sync(active, lab);
-            int leader = __ffs(peers) - 1;
-            int rank = __popc(peers & lt_mask);
+            const unsigned peers = __match_any_sync(active, lab);
+            const int leader = __ffs(peers) - 1;
+            const int rank = __popc(peers & lt_mask);
             int b = 0;
-            long long slot = (long long)lab * T + t;
-            if (lane == leader) b = cursor[slot];
+            if (lane == leader) b = sm ? scur[lab] : cursor[(long long)lab * T + t];
             b = __shfl_sync(peers, b, leader);
             order[b + rank] = (int32_t)r;
-            if (lane == leader) cursor[slot] = b + __popc(peers);
+            if (lane == leader) {
+                if (sm) scur[lab] = b + __popc(peers);
+                else cursor[(long long)lab * T + t] = b + __popc(peers);
+            }
         }
         __syncwarp();
     }
@@ -361,7 +373,7 @@ int launch_group_sums(const double* X, long long n, long long ldx, int D, const 
     DA_CHECK_LAUNCH("exclusive_scan_kernel(hist)");
     seg_counts_kernel<<<grid_for(K, 256), 256, 0, s>>>(hist, K, T, n, seg, counts);
     DA_CHECK_LAUNCH("seg_counts_kernel");
-    stable_scatter_kernel<<<T, 32, 0, s>>>(labels, n, T, hist, order);
+    stable_scatter_kernel<<<T, 32, sh, s>>>(labels, n, K, T, hist, order);
     DA_CHECK_LAUNCH("stable_scatter_kernel");
     leaf_count_kernel<<<grid_for(K, 256), 256, 0, s>>>(counts, K, nleaf);
     DA_CHECK_LAUNCH("leaf_count_kernel");
@@ -409,7 +421,7 @@ int launch_label_order(const int32_t* labels, long long n, int K, int32_t* order
     DA_CHECK_LAUNCH("exclusive_scan_kernel");
     seg_counts_kernel<<<grid_for(K, 256), 256, 0, s>>>(hist, K, T, n, seg, counts);
     DA_CHECK_LAUNCH("seg_counts_kernel");
-    stable_scatter_kernel<<<T, 32, 0, s>>>(labels, n, T, hist, order_out);
+    stable_scatter_kernel<<<T, 32, sh, s>>>(labels, n, K, T, hist, order_out);
     DA_CHECK_LAUNCH("stable_scatter_kernel");
     return 0;
 }

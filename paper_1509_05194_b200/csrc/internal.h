@@ -69,5 +69,12 @@ int launch_gather_rows(const double* X, long long ldx, int D, const long long* s
                        long long ldc, cudaStream_t s);
 int launch_select_better(long long n, int M, const int32_t* beam_codes, const double* beam_err, int32_t* inc_codes,
                          double* inc_err, cudaStream_t s);
+int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int D, const float* cw, int M, int K,
+                       int L, const double* sq, const double* P, void* codes_out, int code_bytes, long long ldcodes,
+                       double* err_out, unsigned long long* stats, cudaStream_t s);
+int launch_assign_tc(const void* X, int x_is_f32, long long n, long long ldx, int d, const double* C, long long ldc,
+                     int K, const double* cc, int32_t* labels, double* d2, const int32_t* prev,
+                     unsigned long long* changed, unsigned long long* stats, cudaStream_t s);
+int set_assign_config(int mode, unsigned long long* stats);
 int launch_set_column(int32_t* codes, long long n, int M, int m, const int32_t* labels, cudaStream_t s);
 }  // namespace da

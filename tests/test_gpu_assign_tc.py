@@ -1,0 +1,54 @@
+"""The tensor-core assign (tcgen05 3xTF32 tiles in TMEM + bound + exact float64
+recheck) must return exactly the labels and distances of the float64 kernel."""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1509_05194_b200 import _engine as E
+
+pytestmark = pytest.mark.gpu
+
+
+def both(X, d, C):
+    Xd, Cd = E.to_dev(X), E.to_dev(C)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    E.assign_config(0, cnt)
+    lt, dt = E.assign(Xd, d, Cd)
+    E.assign_config(1)
+    lp, dp = E.assign(Xd, d, Cd)
+    E.assign_config(0)
+    return (lt.cpu().numpy(), dt.cpu().numpy()), (lp.cpu().numpy(), dp.cpu().numpy()), int(cnt.item())
+
+
+@pytest.mark.parametrize("n,D,d,K", [(1, 3, 3, 1), (130, 5, 2, 13), (1000, 32, 17, 256), (777, 128, 128, 256),
+                                     (5000, 128, 49, 200), (300, 960, 484, 64), (2000, 12, 12, 8), (257, 40, 33, 255)])
+def test_matches_float64_kernel(n, D, d, K):
+    rng = np.random.default_rng(n + d + K)
+    X = rng.standard_normal((n, D)) * rng.uniform(0.1, 10, D)
+    C = X[rng.integers(0, n, K)] + 0.01 * rng.standard_normal((K, D))
+    (lt, dt), (lp, dp), cnt = both(X, d, C)
+    np.testing.assert_array_equal(lt, lp)
+    np.testing.assert_array_equal(dt, dp)
+    assert cnt <= 3 * n + K  # the bound keeps rechecks near one per row
+
+
+def test_ties_duplicates_and_clipping():
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((600, 16))
+    C = np.vstack([X[:20], X[:20], np.zeros((3, 16)), X[5:6]])  # duplicates -> exact ties, d2 == 0 clipped
+    X[100:110] = 0.0
+    for d in (1, 7, 16):
+        (lt, dt), (lp, dp), _ = both(X, d, C)
+        np.testing.assert_array_equal(lt, lp)
+        np.testing.assert_array_equal(dt, dp)
+
+
+def test_float32_rows_and_large_values():
+    rng = np.random.default_rng(6)
+    X = np.clip(np.rint(np.abs(rng.uniform(0, 60, (3000, 128)) + 20 * rng.standard_normal((3000, 128)))), 0, 255)
+    X = X.astype(np.float32)
+    C = X[rng.integers(0, 3000, 256)].astype(np.float64) + rng.standard_normal((256, 128))
+    (lt, dt), (lp, dp), _ = both(X, 128, C)
+    np.testing.assert_array_equal(lt, lp)
+    np.testing.assert_array_equal(dt, dp)

@@ -1,0 +1,73 @@
+"""The filtered encoder (fp32 tables + rigorous bound + exact float64 recheck)
+must return exactly what the plain float64 encoder returns: same codes, same
+float64 errors, for every beam width, including ties and degenerate books."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1509_05194_b200 as da
+from paper_1509_05194_b200 import _engine as E
+from paper_1509_05194_b200 import codebook as cb
+from paper_1509_05194_b200 import synthetic
+
+pytestmark = pytest.mark.gpu
+
+
+def both(book, X, L):
+    cross = cb.cross_products(book)
+    cw, sq = cb._codebook_dev(book)
+    Pt, _ = cross.device()
+    Xd = E.to_dev(X)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    E.encode_config(0, cnt)
+    fast = E.encode(Xd, cw, sq, Pt, L)
+    E.encode_config(1)
+    plain = E.encode(Xd, cw, sq, Pt, L)
+    E.encode_config(0)
+    return fast, plain, int(cnt.item())
+
+
+def assert_same(fast, plain):
+    np.testing.assert_array_equal(fast[0].cpu().numpy(), plain[0].cpu().numpy())
+    np.testing.assert_array_equal(fast[1].cpu().numpy(), plain[1].cpu().numpy())
+
+
+@pytest.mark.parametrize("L", [1, 2, 5, 10, 16, 40, 64])
+def test_random_books(L):
+    rng = np.random.default_rng(L)
+    for M, K, D in [(3, 8, 6), (4, 16, 17), (2, 300, 9), (8, 256, 128)]:
+        book = da.Codebook(codewords=rng.standard_normal((M, K, D)).astype(np.float32), order=np.arange(M))
+        X = rng.standard_normal((700, D)).astype(np.float32)
+        fast, plain, _ = both(book, X, L)
+        assert_same(fast, plain)
+
+
+def test_ties_and_zero_book():
+    book = da.Codebook.zeros(3, 4, 2)
+    X = np.array([[1.0, 2.0], [0.0, 0.0], [-3.0, 1.0]], dtype=np.float32)
+    for L in (1, 4, 16):
+        fast, plain, _ = both(book, X, L)
+        assert_same(fast, plain)
+        assert (fast[0].cpu().numpy() == 0).all()
+    rng = np.random.default_rng(3)
+    cw = rng.standard_normal((3, 6, 5)).astype(np.float32)
+    cw[1, 4] = cw[1, 1]          # duplicate codewords -> exact score ties
+    cw[2] = cw[2][[0, 0, 2, 2, 4, 4]]
+    book = da.Codebook(codewords=cw, order=np.arange(3))
+    X = rng.standard_normal((400, 5)).astype(np.float32)
+    for L in (1, 3, 7):
+        fast, plain, _ = both(book, X, L)
+        assert_same(fast, plain)
+
+
+def test_config_b_like_and_recheck_rate():
+    X = synthetic.config_b(n=30_000, chunk=10_000)
+    cfg = da.TrainConfig(m_count=8, k_count=256, beam_width=10, sweeps=0, rel_tol=0.0)
+    book, _, _ = da.train_from_scratch(X[:5000], cfg)
+    for L in (1, 10):
+        fast, plain, rechecked = both(book, X, L)
+        assert_same(fast, plain)
+        # candidates per vector: sum over stages of live*K; the filter must cut most of them
+        total = X.shape[0] * sum(min(L, 256 ** m) * 256 for m in range(1, 9))
+        assert rechecked < 0.05 * total, (rechecked, total)
