@@ -109,14 +109,15 @@ def row_sqnorms(A: torch.Tensor, d: int) -> torch.Tensor:
 
 
 def assign(X: torch.Tensor, d: int, C: torch.Tensor, cc: torch.Tensor | None = None,
-           prev: torch.Tensor | None = None, changed: torch.Tensor | None = None):
-    """annq/clustering.py:139-148 on the first d columns; labels int32, d2 f64."""
+           prev: torch.Tensor | None = None, changed: torch.Tensor | None = None, xx: torch.Tensor | None = None):
+    """annq/clustering.py:139-148 on the first d columns; labels int32, d2 f64.
+    `xx` = row_sqnorms(X, d) may be passed to reuse it across Lloyd iterations."""
     n, K = X.shape[0], C.shape[0]
     if cc is None:
         cc = row_sqnorms(C, d)
     labels = torch.empty(n, dtype=I32, device=X.device)
     d2 = torch.empty(n, dtype=F64, device=X.device)
-    native.da_assign(P(X), is_f32(X), n, X.stride(0), d, P(C), C.stride(0), K, P(cc), P(labels), P(d2),
+    native.da_assign(P(X), is_f32(X), n, X.stride(0), d, P(C), C.stride(0), K, P(cc), P(xx), P(labels), P(d2),
                      P(prev), P(changed), stream())
     return labels, d2
 
@@ -180,7 +181,8 @@ def lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, c
     dev = Xr.device
     changed = torch.zeros(1, dtype=torch.int64, device=dev)
     trace_d = torch.empty(max_iters + 1, dtype=F64, device=dev)
-    labels, errs = assign(Xr, active, C)
+    xx = row_sqnorms(Xr, active) if n else None  # fixed for the whole stage
+    labels, errs = assign(Xr, active, C, xx=xx)
     trace_d[0:1] = np_mean(errs, comm)
     iters = 0
     counts = torch.empty(K, dtype=I32, device=dev)
@@ -205,7 +207,7 @@ def lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, c
             else:
                 _reseed_sharded(Xr, errs, empty, C, comm)
         changed.zero_()
-        new_labels, errs = assign(Xr, active, C, prev=labels, changed=changed)
+        new_labels, errs = assign(Xr, active, C, prev=labels, changed=changed, xx=xx)
         iters += 1
         trace_d[iters:iters + 1] = np_mean(errs, comm)
         if comm is not None:

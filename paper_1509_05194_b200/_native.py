@@ -24,7 +24,7 @@ _L = ctypes.c_int64
 # name -> argtypes (all return int unless noted)
 _SIGNATURES = {
     "da_row_sqnorms": [_P, _I, _L, _L, _I, _P, _P],
-    "da_assign": [_P, _I, _L, _L, _I, _P, _L, _I, _P, _P, _P, _P, _P, _P],
+    "da_assign": [_P, _I, _L, _L, _I, _P, _L, _I, _P, _P, _P, _P, _P, _P, _P],
     "da_group_sums": [_P, _L, _L, _I, _P, _I, _I, _P, _L, _P, _P],
     "da_label_order": [_P, _L, _I, _P, _P, _P],
     "da_gather_rows": [_P, _L, _I, _P, _P, _I, _P, _L, _P],

@@ -27,7 +27,7 @@ template <typename TX, bool BLK>
 __global__ void __launch_bounds__(AS_THREADS)
 assign_kernel(const TX* __restrict__ X, long long n, long long ldx, int d,
               const double* __restrict__ C, long long ldc, int K,
-              const double* __restrict__ cc,
+              const double* __restrict__ cc, const double* __restrict__ xx_in,
               int32_t* __restrict__ labels, double* __restrict__ d2_out,
               const int32_t* __restrict__ prev, unsigned long long* __restrict__ changed) {
     __shared__ __align__(16) double As[AS_BK][AS_BM];
@@ -45,7 +45,7 @@ assign_kernel(const TX* __restrict__ X, long long n, long long ldx, int d,
         double v = 0.0;
         if (r < n) {
             const TX* xr = X + r * ldx;
-            v = np_pw_sum([&](long long i) { double t = (double)xr[i]; return dmul(t, t); }, 0, d);
+            v = xx_in ? xx_in[r] : np_pw_sum([&](long long i) { double t = (double)xr[i]; return dmul(t, t); }, 0, d);
         }
         xxs[tid] = v;
     }
@@ -198,18 +198,18 @@ int set_assign_config(int mode, unsigned long long* stats) {
 }
 
 int launch_assign(const void* X, int x_is_f32, long long n, long long ldx, int d, const double* C,
-                  long long ldc, int K, const double* cc, int32_t* labels, double* d2,
+                  long long ldc, int K, const double* cc, const double* xx, int32_t* labels, double* d2,
                   const int32_t* prev, unsigned long long* changed, cudaStream_t s) {
     if (n <= 0) return 0;
     if (g_assign_mode == 0) {
-        int rc = launch_assign_tc(X, x_is_f32, n, ldx, d, C, ldc, K, cc, labels, d2, prev, changed, g_assign_stats, s);
+        int rc = launch_assign_tc(X, x_is_f32, n, ldx, d, C, ldc, K, cc, xx, labels, d2, prev, changed, g_assign_stats, s);
         if (rc <= 0) return rc;
     }
     unsigned g = grid_for(n, AS_BM, 1LL << 31);
     ProfScope ps(d <= 8 ? "assign_d<=8" : d <= 32 ? "assign_d<=32" : d <= 128 ? "assign_d<=128" : "assign_d>128", s);
     const bool blk = d > BLAS_Q;
-#define AS_LAUNCH(T, B) assign_kernel<T, B><<<g, AS_THREADS, 0, s>>>((const T*)X, n, ldx, d, C, ldc, K, cc, labels, \
-                                                                  d2, prev, changed)
+#define AS_LAUNCH(T, B) assign_kernel<T, B><<<g, AS_THREADS, 0, s>>>((const T*)X, n, ldx, d, C, ldc, K, cc, xx, \
+                                                                  labels, d2, prev, changed)
     if (x_is_f32) { if (blk) AS_LAUNCH(float, true); else AS_LAUNCH(float, false); }
     else { if (blk) AS_LAUNCH(double, true); else AS_LAUNCH(double, false); }
 #undef AS_LAUNCH

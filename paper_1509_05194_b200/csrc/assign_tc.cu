@@ -13,6 +13,7 @@
 // Operands are staged to shared memory by the CTA's threads (f64 -> tf32 hi/lo
 // split) in the canonical K-major no-swizzle UMMA layout; one elected thread
 // issues the MMAs and commits them to an mbarrier.
+#include <algorithm>
 #include <cstdint>
 
 #include "common.cuh"
@@ -112,220 +113,328 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+template <typename TX>
+__device__ __forceinline__ double fma_chain(const TX* __restrict__ xr, const double* __restrict__ cr, int k, int e,
+                                            double acc) {
+    // loads are issued 8 ahead of the (strictly sequential) FMA chain
+    for (; k + 8 <= e; k += 8) {
+        double xv[8], cv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { xv[u] = (double)xr[k + u]; cv[u] = cr[k + u]; }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = __fma_rn(xv[u], cv[u], acc);
+    }
+    for (; k < e; ++k) acc = __fma_rn((double)xr[k], cr[k], acc);
+    return acc;
+}
+
 template <typename TX, bool BLK>
 __device__ __forceinline__ double exact_xc(const TX* __restrict__ xr, const double* __restrict__ cr, int d) {
-    if (!BLK) {
-        double acc = 0.0;
-        for (int k = 0; k < d; ++k) acc = __fma_rn((double)xr[k], cr[k], acc);
-        return acc;
-    }
+    if (!BLK) return fma_chain(xr, cr, 0, d, 0.0);
     double tot = 0.0;
     bool first = true;
     int k = 0;
     while (k < d) {
         const int e = k + (int)blas_block_len(d - k);
-        double acc = 0.0;
-        for (; k < e; ++k) acc = __fma_rn((double)xr[k], cr[k], acc);
+        const double acc = fma_chain(xr, cr, k, e, 0.0);
+        k = e;
         tot = first ? acc : dadd(tot, acc);
         first = false;
     }
     return tot;
 }
 
+// Codewords (K x d, float64) -> per-chunk tf32 hi/lo tiles in the exact shared
+// memory image the MMA reads (zero padded to 256 rows / 32 columns), so CTAs
+// fetch each chunk with one bulk copy.
+__global__ void cw_tf32_prep_kernel(const double* __restrict__ C, long long ldc, int K, int d, int nch,
+                                    float* __restrict__ out) {
+    const long long total = (long long)nch * TC_NMAX * TC_BK;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        const int ch = (int)(e / (TC_NMAX * TC_BK));
+        const int rem = (int)(e % (TC_NMAX * TC_BK));
+        const int r = rem / TC_BK, k = rem % TC_BK;
+        const int gk = ch * TC_BK + k;
+        float h = 0.f, l = 0.f;
+        if (r < K && gk < d) {
+            const double v = C[(long long)r * ldc + gk];
+            h = to_tf32((float)v);
+            l = to_tf32((float)(v - (double)h));
+        }
+        float* base = out + (size_t)ch * 2 * TC_NMAX * TC_BK;
+        const uint32_t o = kmajor_off(r, k) >> 2;
+        base[o] = h;
+        base[TC_NMAX * TC_BK + o] = l;
+    }
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// Persistent, software-pipelined kernel: one CTA (8 warps) per SM walks row
+// tiles.  Per (tile, k-chunk) step the warps stage 16 rows each as tf32 hi/lo
+// (coalesced 256-B row segments) while a bulk copy brings the matching codeword
+// chunk (kept resident when d <= 32), and thread 0 issues 3 x (<= 4)
+// tcgen05.mma into one of two TMEM accumulators (2 x 256 columns).  The epilogue
+// of tile i-1 (two threads per row, one per half of the codewords) runs while
+// the tensor cores work on tile i.
+constexpr int TC_T2 = 256;
+
 template <typename TX>
-__global__ void __launch_bounds__(TC_THREADS) assign_tc_kernel(
+__global__ void __launch_bounds__(TC_T2, 1) assign_tc_kernel(
     const TX* __restrict__ X, long long n, long long ldx, int d, const double* __restrict__ C, long long ldc, int K,
-    const double* __restrict__ cc, int32_t* __restrict__ labels, double* __restrict__ d2_out,
-    const int32_t* __restrict__ prev, unsigned long long* __restrict__ changed,
-    unsigned long long* __restrict__ stats) {
+    const double* __restrict__ cc, const double* __restrict__ xx_in, const float* __restrict__ Bg,
+    int32_t* __restrict__ labels, double* __restrict__ d2_out, const int32_t* __restrict__ prev,
+    unsigned long long* __restrict__ changed, unsigned long long* __restrict__ stats) {
     extern __shared__ __align__(1024) unsigned char smem[];
-    float* a_hi = reinterpret_cast<float*>(smem);
-    float* a_lo = a_hi + TC_M * TC_BK;
-    float* b_hi = a_lo + TC_M * TC_BK;
-    float* b_lo = b_hi + TC_NMAX * TC_BK;
-    __shared__ uint64_t mbar;
+    constexpr int A_ELEMS = TC_M * TC_BK, B_ELEMS = TC_NMAX * TC_BK;
+    float* Abuf = reinterpret_cast<float*>(smem);                    // [2 stages][hi, lo][A_ELEMS]
+    float* Bbuf = Abuf + 2 * 2 * A_ELEMS;                             // [2 stages][hi, lo][B_ELEMS]
+    double* ccs = reinterpret_cast<double*>(Bbuf + 2 * 2 * B_ELEMS);  // [TC_NMAX]
+    float* ccf = reinterpret_cast<float*>(ccs + TC_NMAX);            // [TC_NMAX], +inf beyond K
+    double* wmin_h = reinterpret_cast<double*>(ccf + TC_NMAX);        // [2][TC_M]
+    int* cand = reinterpret_cast<int*>(wmin_h + 2 * TC_M);            // [2][TC_M][TC_CMAX]
+    int* ncand = cand + 2 * TC_M * TC_CMAX;                           // [2][TC_M]
+    __shared__ uint64_t full_bar[2], empty_bar[2], acc_bar[2];
     __shared__ uint32_t tmem_base_sh;
-    __shared__ double ccmax_sh;
+    __shared__ double red[8];
 
     const int tid = threadIdx.x;
-    const int warp = tid >> 5;
-    const long long row0 = (long long)blockIdx.x * TC_M;
+    const int warp = tid >> 5, lane = tid & 31;
     const int N = (K + 7) & ~7;
+    const int nch = (d + TC_BK - 1) / TC_BK;
+    const bool b_resident = nch == 1;
+    const long long ntiles = (n + TC_M - 1) / TC_M;
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
-                     "r"(TC_NMAX));
+                     "r"(2 * TC_NMAX));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
-        mbar_init(&mbar, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&full_bar[i], 1);
+            mbar_init(&empty_bar[i], 1);
+            mbar_init(&acc_bar[i], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // max codeword norm for the bound
     double cm = 0.0;
-    for (int k = tid; k < K; k += TC_THREADS) cm = fmax(cm, cc[k]);
+    for (int k = tid; k < TC_NMAX; k += TC_T2) {
+        const double v = k < K ? cc[k] : 0.0;
+        ccs[k] = v;
+        ccf[k] = k < K ? (float)v : __int_as_float(0x7f800000);
+        cm = fmax(cm, v);
+    }
     for (int off = 16; off >= 1; off >>= 1) cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, off));
-    __shared__ double red[4];
-    if ((tid & 31) == 0) red[warp] = cm;
+    if (lane == 0) red[warp] = cm;
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
-    if (tid == 0) ccmax_sh = fmax(fmax(red[0], red[1]), fmax(red[2], red[3]));
     const uint32_t tmem = tmem_base_sh;
+    double ccmax = 0.0;
+    for (int w = 0; w < 8; ++w) ccmax = fmax(ccmax, red[w]);
+    const double sc = sqrt(ccmax);
     const uint32_t idesc = make_idesc_tf32(TC_M, N);
-
-    uint32_t phase = 0;
-    const int nchunks = (d + TC_BK - 1) / TC_BK;
-    for (int ch = 0; ch < nchunks; ++ch) {
-        const int k0 = ch * TC_BK;
-        if (ch > 0) {
-            mbar_wait(&mbar, phase);  // previous MMAs done reading smem
-            phase ^= 1;
-        }
-        // stage A: row tid
-        {
-            const long long r = row0 + tid;
-            const TX* xr = X + r * ldx;
-#pragma unroll 4
-            for (int k = 0; k < TC_BK; ++k) {
-                float h = 0.f, l = 0.f;
-                const int gk = k0 + k;
-                if (r < n && gk < d) {
-                    const double v = (double)xr[gk];
-                    h = to_tf32((float)v);
-                    l = to_tf32((float)(v - (double)h));
-                }
-                const uint32_t o = kmajor_off(tid, k) >> 2;
-                a_hi[o] = h;
-                a_lo[o] = l;
-            }
-        }
-        // stage B: codeword rows tid, tid+128
-        for (int rr = tid; rr < TC_NMAX; rr += TC_THREADS) {
-            const double* crow = C + (long long)rr * ldc;
-#pragma unroll 4
-            for (int k = 0; k < TC_BK; ++k) {
-                float h = 0.f, l = 0.f;
-                const int gk = k0 + k;
-                if (rr < K && gk < d) {
-                    const double v = crow[gk];
-                    h = to_tf32((float)v);
-                    l = to_tf32((float)(v - (double)h));
-                }
-                const uint32_t o = kmajor_off(rr, k) >> 2;
-                b_hi[o] = h;
-                b_lo[o] = l;
-            }
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        if (tid == 0) {
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint32_t sa_hi = smem_u32(a_hi), sa_lo = smem_u32(a_lo);
-            const uint32_t sb_hi = smem_u32(b_hi), sb_lo = smem_u32(b_lo);
-#pragma unroll
-            for (int s = 0; s < TC_BK / 8; ++s) {
-                const uint32_t off = (uint32_t)s * 256;  // two 16-B chunks = 8 tf32 of K
-                const uint32_t acc0 = (ch > 0 || s > 0) ? 1u : 0u;
-                mma_tf32(tmem, make_desc(sa_hi + off), make_desc(sb_hi + off), idesc, acc0);
-                mma_tf32(tmem, make_desc(sa_hi + off), make_desc(sb_lo + off), idesc, 1u);
-                mma_tf32(tmem, make_desc(sa_lo + off), make_desc(sb_hi + off), idesc, 1u);
-            }
-            mma_commit(&mbar);
-        }
-    }
-    mbar_wait(&mbar, phase);
-    asm volatile("tcgen05.fence::after_thread_sync;");
-
-    // ---- epilogue: thread tid owns row row0+tid (TMEM lane tid)
-    const long long r = row0 + tid;
-    const bool valid = r < n;
-    const TX* xr = X + (valid ? r : 0) * ldx;
-    double xx = 0.0;
-    if (valid) xx = np_pw_sum([&](long long i) { double t = (double)xr[i]; return dmul(t, t); }, 0, d);
     const double u22 = 2.384185791015625e-07;  // 2^-22
-    const double sx = sqrt(xx), sc = sqrt(ccmax_sh);
-    // 3xTF32 representation + fp32 accumulation error of 2 x.c, plus float64
-    // rounding of the window arithmetic
-    const double E = 2.0 * (4.0 * d + 16.0) * u22 * sx * sc * (1.0 + 1e-9) +
-                     8.8817841970012523e-16 * (xx + ccmax_sh + 2.0 * sx * sc) + 1e-300;
-    const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
-    float v[32];
-    // pass 1: smallest approximate (cc - 2 x.c)
-    double wmin = __longlong_as_double(0x7ff0000000000000ULL);
-    for (int c0 = 0; c0 < N; c0 += 32) {
-        tmem_ld32(lane_addr + c0, v);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            const int k = c0 + i;
-            if (k < K) wmin = fmin(wmin, cc[k] - 2.0 * (double)v[i]);
-        }
+    const bool blk = d > (int)BLAS_Q;
+    if (b_resident && tid == 0) {  // the whole (single-chunk) codebook once
+        mbar_arrive_expect_tx(&full_bar[0], (uint32_t)(2 * B_ELEMS * sizeof(float)));
+        bulk_g2s(Bbuf, Bg, (uint32_t)(2 * B_ELEMS * sizeof(float)), &full_bar[0]);
     }
-    const double ub = fmax(xx + wmin + E, 0.0);  // >= the exact clipped minimum
-    // pass 2: candidates whose exact clipped distance can still be <= ub
-    int cand[TC_CMAX];
-    int nc = 0;
-    bool overflow = false;
-    for (int c0 = 0; c0 < N; c0 += 32) {
-        tmem_ld32(lane_addr + c0, v);
+
+    const int erow = tid & (TC_M - 1);   // TMEM lane / tile row owned in the epilogue
+    const int ehalf = tid >> 7;          // 0: codewords [0,128), 1: [128,256)
+    auto epilogue = [&](long long tile, int accb) {
+        const long long r = tile * TC_M + erow;
+        const bool valid = r < n;
+        const TX* xr = X + (valid ? r : 0) * ldx;
+        double xx = 0.0;
+        if (valid) {
+            if (xx_in) xx = xx_in[r];
+            else xx = np_pw_sum([&](long long i) { double t = (double)xr[i]; return dmul(t, t); }, 0, d);
+        }
+        const double sx = sqrt(xx);
+        // bound on |w' - (cc - 2 x.c)| for w' = fmaf(-2, dot', (float)cc): 3xTF32 + fp32
+        // accumulation of the dot, fp32 rounding of cc and of the fma, float64
+        // rounding of the window arithmetic
+        const double E = 2.0 * (4.0 * d + 16.0) * u22 * sx * sc * (1.0 + 1e-9) +
+                         2.384185791015625e-07 * (ccmax + 2.0 * sx * sc) +
+                         8.8817841970012523e-16 * (xx + ccmax + 2.0 * sx * sc) + 1e-300;
+        const int cbeg = ehalf * 128, cend = min(N, cbeg + 128);
+        const uint32_t taddr = tmem + (uint32_t)(accb * TC_NMAX) + ((uint32_t)((warp & 3) * 32) << 16);
+        float v[32];
+        float wminf = __int_as_float(0x7f800000);
+        for (int c0 = cbeg; c0 < cend; c0 += 32) {
+            tmem_ld32(taddr + c0, v);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            const int k = c0 + i;
-            if (k < K && fmax(xx + (cc[k] - 2.0 * (double)v[i]) - E, 0.0) <= ub) {
-                if (nc < TC_CMAX) cand[nc] = k;
+            for (int i = 0; i < 32; ++i) wminf = fminf(wminf, fmaf(-2.f, v[i], ccf[c0 + i]));
+        }
+        wmin_h[ehalf * TC_M + erow] = (double)wminf;
+        __syncthreads();
+        const double wmin = fmin(wmin_h[erow], wmin_h[TC_M + erow]);
+        const double ub = fmax(xx + wmin + E, 0.0);
+        // candidate k iff max(xx + w'_k - E, 0) <= ub  <=>  w'_k <= ub - xx + E (ub >= 0)
+        const double tlim = ub - xx + E;
+        const float tf = (tlim >= 3.0e38) ? __int_as_float(0x7f800000)
+                                          : __fadd_ru((float)tlim, fabsf((float)tlim) * 1e-6f + 1e-30f);
+        int nc = 0;
+        int* my = cand + (ehalf * TC_M + erow) * TC_CMAX;
+        for (int c0 = cbeg; c0 < cend; c0 += 32) {
+            tmem_ld32(taddr + c0, v);
+            uint32_t hit = 0;  // branch-free test, then walk the (rare) set bits
+#pragma unroll
+            for (int i = 0; i < 32; ++i) hit |= (uint32_t)(fmaf(-2.f, v[i], ccf[c0 + i]) <= tf) << i;
+            while (hit) {
+                const int i = __ffs(hit) - 1;
+                hit &= hit - 1;
+                if (nc < TC_CMAX) my[nc] = c0 + i;
                 ++nc;
             }
         }
-    }
-    overflow = nc > TC_CMAX;
-    if (valid) {
+        ncand[ehalf * TC_M + erow] = nc;
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        if (ehalf != 0 || !valid) return;
         double best = __longlong_as_double(0x7ff0000000000000ULL);
         int bk = 0x7fffffff;
-        const bool blk = d > (int)BLAS_Q;
         auto consider = [&](int k) {
             const double* crow = C + (long long)k * ldc;
             const double xc = blk ? exact_xc<TX, true>(xr, crow, d) : exact_xc<TX, false>(xr, crow, d);
-            double dv = dadd(dsub(xx, dmul(2.0, xc)), cc[k]);
+            double dv = dadd(dsub(xx, dmul(2.0, xc)), ccs[k]);
             if (dv < 0.0) dv = 0.0;
             if (lex_less(dv, k, best, bk)) { best = dv; bk = k; }
         };
+        const int n0 = ncand[erow], n1 = ncand[TC_M + erow];
+        const bool overflow = n0 > TC_CMAX || n1 > TC_CMAX;
         if (!overflow) {
-            for (int i = 0; i < nc; ++i) consider(cand[i]);
+            for (int i = 0; i < n0; ++i) consider(cand[erow * TC_CMAX + i]);
+            for (int i = 0; i < n1; ++i) consider(cand[(TC_M + erow) * TC_CMAX + i]);
         } else {
             for (int k = 0; k < K; ++k) consider(k);
         }
         labels[r] = bk;
         d2_out[r] = best;
-        if (stats) atomicAdd(stats, (unsigned long long)(overflow ? K : nc));
+        if (stats) atomicAdd(stats, (unsigned long long)(overflow ? K : n0 + n1));
         if (changed != nullptr && prev != nullptr && prev[r] != bk) atomicAdd(changed, 1ULL);
+    };
+
+    long long q = 0;  // (tile, chunk) steps issued by this CTA
+    long long it = 0; // tiles issued by this CTA
+    long long prev_tile = -1;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int accb = (int)(it & 1);
+        const long long row0 = tile * TC_M;
+        for (int ch = 0; ch < nch; ++ch, ++q) {
+            const int st = (int)(q & 1);
+            if (q >= 2) mbar_wait(&empty_bar[st], (uint32_t)(((q >> 1) - 1) & 1));
+            float* Ah = Abuf + st * 2 * A_ELEMS;
+            float* Al = Ah + A_ELEMS;
+            float* Bs = b_resident ? Bbuf : Bbuf + st * 2 * B_ELEMS;
+            if (!b_resident && tid == 0) {
+                mbar_arrive_expect_tx(&full_bar[st], (uint32_t)(2 * B_ELEMS * sizeof(float)));
+                bulk_g2s(Bs, Bg + (size_t)ch * 2 * B_ELEMS, (uint32_t)(2 * B_ELEMS * sizeof(float)), &full_bar[st]);
+            }
+            // stage 16 rows per warp, one coalesced row segment per iteration
+            const int k0 = ch * TC_BK;
+            const int gk = k0 + lane;
+            double xv[TC_M / 8];
+#pragma unroll
+            for (int i = 0; i < TC_M / 8; ++i) {  // all 16 row loads in flight first
+                const long long r = row0 + warp * (TC_M / 8) + i;
+                xv[i] = (r < n && gk < d) ? (double)X[r * ldx + gk] : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < TC_M / 8; ++i) {
+                const int rr = warp * (TC_M / 8) + i;
+                const float h = to_tf32((float)xv[i]);
+                const float l = to_tf32((float)(xv[i] - (double)h));
+                const uint32_t o = kmajor_off(rr, lane) >> 2;
+                Ah[o] = h;
+                Al[o] = l;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (tid == 0) {
+                if (!b_resident) mbar_wait(&full_bar[st], (uint32_t)((q >> 1) & 1));
+                else if (q == 0) mbar_wait(&full_bar[0], 0);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t sa_hi = smem_u32(Ah), sa_lo = smem_u32(Al);
+                const uint32_t sb_hi = smem_u32(Bs), sb_lo = smem_u32(Bs + B_ELEMS);
+                const uint32_t dacc = tmem + (uint32_t)(accb * TC_NMAX);
+                const int ks = min(TC_BK / 8, (d - k0 + 7) / 8);
+                for (int s2 = 0; s2 < ks; ++s2) {
+                    const uint32_t off = (uint32_t)s2 * 256;
+                    const uint32_t acc0 = (ch > 0 || s2 > 0) ? 1u : 0u;
+                    mma_tf32(dacc, make_desc(sa_hi + off), make_desc(sb_hi + off), idesc, acc0);
+                    mma_tf32(dacc, make_desc(sa_hi + off), make_desc(sb_lo + off), idesc, 1u);
+                    mma_tf32(dacc, make_desc(sa_lo + off), make_desc(sb_hi + off), idesc, 1u);
+                }
+                mma_commit(&empty_bar[st]);
+                if (ch == nch - 1) mma_commit(&acc_bar[accb]);
+            }
+        }
+        if (prev_tile >= 0) {
+            const int pb = (int)((it - 1) & 1);
+            mbar_wait(&acc_bar[pb], (uint32_t)(((it - 1) >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            epilogue(prev_tile, pb);
+        }
+        prev_tile = tile;
+    }
+    if (prev_tile >= 0) {
+        const int pb = (int)((it - 1) & 1);
+        mbar_wait(&acc_bar[pb], (uint32_t)(((it - 1) >> 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        epilogue(prev_tile, pb);
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_NMAX));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TC_NMAX));
     }
 }
 
 // Returns 1 (without launching) when the shape is outside the tensor-core path.
 int launch_assign_tc(const void* X, int x_is_f32, long long n, long long ldx, int d, const double* C, long long ldc,
-                     int K, const double* cc, int32_t* labels, double* d2, const int32_t* prev,
+                     int K, const double* cc, const double* xx, int32_t* labels, double* d2, const int32_t* prev,
                      unsigned long long* changed, unsigned long long* stats, cudaStream_t s) {
     if (K > TC_NMAX || K < 1 || d < 1) return 1;
     if (n <= 0) return 0;
-    const size_t smem = sizeof(float) * (2 * TC_M + 2 * TC_NMAX) * TC_BK;
-    const unsigned grid = (unsigned)((n + TC_M - 1) / TC_M);
+    const int nch = (d + TC_BK - 1) / TC_BK;
+    float* Bg = (float*)scratch(9, sizeof(float) * (size_t)nch * 2 * TC_NMAX * TC_BK, s);
+    if (!Bg) return fail_cuda(cudaErrorMemoryAllocation, "assign_tc scratch");
     ProfScope ps(d <= 8 ? "assign_tc_d<=8" : d <= 32 ? "assign_tc_d<=32" : d <= 128 ? "assign_tc_d<=128" : "assign_tc_d>128",
                  s);
+    cw_tf32_prep_kernel<<<grid_for((long long)nch * TC_NMAX * TC_BK, 256, 4096), 256, 0, s>>>(C, ldc, K, d, nch, Bg);
+    DA_CHECK_LAUNCH("cw_tf32_prep_kernel");
+    const size_t smem = sizeof(float) * (2 * 2 * TC_M * TC_BK + 2 * 2 * TC_NMAX * TC_BK) + sizeof(double) * TC_NMAX +
+                        sizeof(float) * TC_NMAX +
+                        sizeof(double) * 2 * TC_M + sizeof(int) * (2 * TC_M * TC_CMAX + 2 * TC_M);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long ntiles = (n + TC_M - 1) / TC_M;
+    const unsigned grid = (unsigned)std::min<long long>(ntiles, sms);
     if (x_is_f32) {
         auto kf = assign_tc_kernel<float>;
         DA_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kf<<<grid, TC_THREADS, smem, s>>>((const float*)X, n, ldx, d, C, ldc, K, cc, labels, d2, prev, changed, stats);
+        kf<<<grid, TC_T2, smem, s>>>((const float*)X, n, ldx, d, C, ldc, K, cc, xx, Bg, labels, d2, prev, changed,
+                                     stats);
     } else {
         auto kf = assign_tc_kernel<double>;
         DA_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kf<<<grid, TC_THREADS, smem, s>>>((const double*)X, n, ldx, d, C, ldc, K, cc, labels, d2, prev, changed,
-                                          stats);
+        kf<<<grid, TC_T2, smem, s>>>((const double*)X, n, ldx, d, C, ldc, K, cc, xx, Bg, labels, d2, prev, changed,
+                                     stats);
     }
     DA_CHECK_LAUNCH("assign_tc_kernel");
     return 0;

@@ -109,11 +109,11 @@ int da_row_sqnorms(const void* A, int a_f32, int64_t rows, int64_t lda, int d, d
 }
 
 int da_assign(const void* X, int x_f32, int64_t n, int64_t ldx, int d, const double* C, int64_t ldc, int K,
-              const double* cc, int32_t* labels, double* d2, const int32_t* prev, unsigned long long* changed,
-              void* stream) {
+              const double* cc, const double* xx, int32_t* labels, double* d2, const int32_t* prev,
+              unsigned long long* changed, void* stream) {
     if (n < 0 || K < 1 || d < 1 || ldx < d || ldc < d)
         return fail_arg("assign: bad shape n=%lld K=%d d=%d", (long long)n, K, d);
-    return launch_assign(X, x_f32, n, ldx, d, C, ldc, K, cc, labels, d2, prev, changed, STREAM(stream));
+    return launch_assign(X, x_f32, n, ldx, d, C, ldc, K, cc, xx, labels, d2, prev, changed, STREAM(stream));
 }
 
 int da_group_sums(const double* X, int64_t n, int64_t ldx, int D, const int32_t* labels, int K, int mode,
@@ -190,8 +190,13 @@ int da_pca_cov(const void* X, int x_f32, int64_t n, int64_t ld, int D, const dou
         g.B = X; g.b_f32 = x_f32; g.sbk = ld; g.sbj = 1; g.bsub = mean; g.bsub_mode = 2;
         g.C = part; g.sci = D; g.scj = 1; g.sCz = dd;
         g.M = D; g.N = D; g.K = n; g.nb2 = 1; g.ksplit = (int)wn; g.kstarts = kst + w0; g.epi = 0;
-        int rc = launch_gemm(g, 1, s);
+        int rc;
+        {
+            ProfScope p1("pca_cov_gemm", s);
+            rc = launch_gemm(g, 1, s);
+        }
         if (rc) return rc;
+        ProfScope p2("pca_cov_fold", s);
         const bool last = w0 + wn == nb;
         rc = launch_accumulate_partials(part, (int)wn, dd, (last && divide) ? (double)(n - 1) : 0.0, w0 > 0 ? 1 : 0,
                                         cov, s);

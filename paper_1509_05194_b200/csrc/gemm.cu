@@ -145,7 +145,15 @@ __global__ void reduce_partials_kernel(const double* __restrict__ P, int nz, lon
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= len) return;
     double s = accumulate ? dadd(out[i], P[i]) : P[i];
-    for (int z = 1; z < nz; ++z) s = dadd(s, P[(long long)z * len + i]);
+    int z = 1;
+    for (; z + 8 <= nz; z += 8) {  // loads run ahead of the ordered add chain
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = P[(long long)(z + u) * len + i];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s = dadd(s, v[u]);
+    }
+    for (; z < nz; ++z) s = dadd(s, P[(long long)z * len + i]);
     out[i] = scale_div != 0.0 ? __ddiv_rn(s, scale_div) : s;
 }
 
@@ -177,29 +185,57 @@ __global__ void col_partial_kernel(const T* __restrict__ X, long long n, long lo
 }
 
 // numpy's X.mean(axis=0) on a C-contiguous array adds the rows one after the
-// other (no pairwise tree along axis 0): one thread per column, one chain.
+// other (no pairwise tree along axis 0), so every column is one dependent add
+// chain.  A block owns 8 columns: all 256 threads stream row chunks into shared
+// memory (double-buffered, coalesced 8-column segments) while 8 threads of warp
+// 0 run the chains out of shared memory.
+constexpr int CM_COLS = 8, CM_ROWS = 256, CM_T = 256;
+
 template <typename T>
-__global__ void col_mean_seq_kernel(const T* __restrict__ X, long long n, long long ld, int D, double* __restrict__ mean) {
-    int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= D) return;
+__global__ void __launch_bounds__(CM_T) col_mean_seq_kernel(const T* __restrict__ X, long long n, long long ld, int D,
+                                                             double* __restrict__ mean) {
+    __shared__ double buf[2][CM_ROWS][CM_COLS];
+    const int c0 = blockIdx.x * CM_COLS;
+    const int tid = threadIdx.x;
+    auto load = [&](long long r0, int b) {
+        for (int e = tid; e < CM_ROWS * CM_COLS; e += CM_T) {
+            const int rr = e / CM_COLS, cc = e % CM_COLS;
+            const long long r = r0 + rr;
+            double v = 0.0;
+            if (r < n && c0 + cc < D) v = (double)X[r * ld + c0 + cc];
+            buf[b][rr][cc] = v;
+        }
+    };
     double s = 0.0;
-    long long r = 0;
-    for (; r + 8 <= n; r += 8) {
-        double v[8];
+    const long long nchunks = (n + CM_ROWS - 1) / CM_ROWS;
+    load(0, 0);
+    __syncthreads();
+    for (long long ch = 0; ch < nchunks; ++ch) {
+        const int b = (int)(ch & 1);
+        if (ch + 1 < nchunks) load((ch + 1) * CM_ROWS, b ^ 1);
+        if (tid < CM_COLS) {
+            const int rows = (int)min((long long)CM_ROWS, n - ch * CM_ROWS);
+            int rr = 0;
+            for (; rr + 8 <= rows; rr += 8) {
+                double v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = (double)X[(r + u) * ld + c];
+                for (int u = 0; u < 8; ++u) v[u] = buf[b][rr + u][tid];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) s = dadd(s, v[u]);
+                for (int u = 0; u < 8; ++u) s = dadd(s, v[u]);
+            }
+            for (; rr < rows; ++rr) s = dadd(s, buf[b][rr][tid]);
+        }
+        __syncthreads();
     }
-    for (; r < n; ++r) s = dadd(s, (double)X[r * ld + c]);
-    mean[c] = __ddiv_rn(s, (double)n);
+    if (tid < CM_COLS && c0 + tid < D) mean[c0 + tid] = __ddiv_rn(s, (double)n);
 }
 
 int launch_col_mean(const void* X, int x_f32, long long n, long long ld, int D, double* mean, cudaStream_t s) {
     if (n <= 0) return fail_arg("col_mean: n must be positive");
     ProfScope ps("col_mean", s);
-    if (x_f32) col_mean_seq_kernel<float><<<(D + 63) / 64, 64, 0, s>>>((const float*)X, n, ld, D, mean);
-    else col_mean_seq_kernel<double><<<(D + 63) / 64, 64, 0, s>>>((const double*)X, n, ld, D, mean);
+    const unsigned g = (unsigned)((D + CM_COLS - 1) / CM_COLS);
+    if (x_f32) col_mean_seq_kernel<float><<<g, CM_T, 0, s>>>((const float*)X, n, ld, D, mean);
+    else col_mean_seq_kernel<double><<<g, CM_T, 0, s>>>((const double*)X, n, ld, D, mean);
     DA_CHECK_LAUNCH("col_mean_seq_kernel");
     return 0;
 }

@@ -36,7 +36,7 @@ int launch_accumulate_partials(const double* P, int nz, long long len, double sc
 int launch_row_sqnorms(const void* A, int a_is_f32, long long rows, long long lda, int d, double* out,
                        cudaStream_t s);
 int launch_assign(const void* X, int x_is_f32, long long n, long long ldx, int d, const double* C, long long ldc,
-                  int K, const double* cc, int32_t* labels, double* d2, const int32_t* prev,
+                  int K, const double* cc, const double* xx, int32_t* labels, double* d2, const int32_t* prev,
                   unsigned long long* changed, cudaStream_t s);
 
 int launch_group_sums(const double* X, long long n, long long ldx, int D, const int32_t* labels, int K, int mode,
@@ -73,7 +73,7 @@ int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int
                        int L, const double* sq, const double* P, void* codes_out, int code_bytes, long long ldcodes,
                        double* err_out, unsigned long long* stats, cudaStream_t s);
 int launch_assign_tc(const void* X, int x_is_f32, long long n, long long ldx, int d, const double* C, long long ldc,
-                     int K, const double* cc, int32_t* labels, double* d2, const int32_t* prev,
+                     int K, const double* cc, const double* xx, int32_t* labels, double* d2, const int32_t* prev,
                      unsigned long long* changed, unsigned long long* stats, cudaStream_t s);
 int set_assign_config(int mode, unsigned long long* stats);
 int launch_set_column(int32_t* codes, long long n, int M, int m, const int32_t* labels, cudaStream_t s);
