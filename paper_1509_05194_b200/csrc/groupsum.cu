@@ -22,7 +22,7 @@
 namespace da {
 
 namespace {
-constexpr int GS_TILE = 4096;      // rows per sort tile
+constexpr int GS_TILE = 1024;      // rows per sort tile
 constexpr int GS_SMEM_HIST = 12288; // labels that fit a shared-memory histogram
 constexpr int GS_COLS = 128;       // columns per warp task (4 per lane)
 }  // namespace
@@ -91,6 +91,34 @@ __global__ void seg_counts_kernel(const int32_t* __restrict__ offs, int K, int T
     int e = (k + 1 < K) ? offs[(long long)(k + 1) * T] : (int)n;
     seg_start[k] = s;
     counts[k] = e - s;
+}
+
+// One warp per label: exclusive scan of hist[k][0..T) in place; counts[k] = total.
+__global__ void label_tile_scan_kernel(int32_t* __restrict__ hist, int K, int T, int32_t* __restrict__ counts) {
+    const int lane = threadIdx.x & 31;
+    const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (k >= K) return;
+    int32_t* row = hist + (long long)k * T;
+    int carry = 0;
+    for (int b = 0; b < T; b += 32) {
+        const int t = b + lane;
+        const int v = t < T ? row[t] : 0;
+        int incl = v;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int o = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += o;
+        }
+        if (t < T) row[t] = carry + incl - v;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) counts[k] = carry;
+}
+
+// hist[k][t] += seg_start[k] (turns within-label offsets into global cursors)
+__global__ void add_seg_start_kernel(int32_t* __restrict__ hist, int K, int T, const int32_t* __restrict__ seg_start) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (long long)K * T) return;
+    hist[e] += seg_start[e / T];
 }
 
 // One warp per tile: stable scatter of row ids into their label segment.
@@ -189,7 +217,9 @@ __global__ void leaf_enum_kernel(const int32_t* __restrict__ counts, const int32
 }
 
 // One warp per (leaf, 128-column chunk): numpy pairwise leaf over gathered rows.
-__global__ void leaf_sum_kernel(const double* __restrict__ X, long long ldx, int D,
+// Lane l owns columns {2l, 2l+1, 64+2l, 65+2l} of the chunk (two 16-B loads per
+// row); the 8 interleaved accumulators follow the row index mod 8.
+__global__ void __launch_bounds__(256, 2) leaf_sum_kernel(const double* __restrict__ X, long long ldx, int D,
                                 const int32_t* __restrict__ order, const int4* __restrict__ leaves,
                                 const int32_t* __restrict__ n_leaves_total, int n_chunks,
                                 double* __restrict__ leaf_sums) {
@@ -201,54 +231,62 @@ __global__ void leaf_sum_kernel(const double* __restrict__ X, long long ldx, int
     const int chunk = (int)(task % n_chunks);
     const int4 L = leaves[leaf];
     const int start = L.y, n = L.z;
-    int cols[4];
-    bool ok[4];
+    const int cbase = chunk * GS_COLS;
+    const int cols[4] = {cbase + 2 * lane, cbase + 2 * lane + 1, cbase + 64 + 2 * lane, cbase + 65 + 2 * lane};
+    const bool vec = ((ldx & 1) == 0) && (cbase + GS_COLS <= D);  // aligned full chunk: 16-B loads
+    auto load_row = [&](long long r, double* out4) {
+        const double* p = X + r * ldx;
+        if (vec) {
+            const double2 a = *reinterpret_cast<const double2*>(p + cols[0]);
+            const double2 b = *reinterpret_cast<const double2*>(p + cols[2]);
+            out4[0] = a.x; out4[1] = a.y; out4[2] = b.x; out4[3] = b.y;
+        } else {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) { cols[q] = chunk * GS_COLS + lane + 32 * q; ok[q] = cols[q] < D; }
-    auto val = [&](int i, int q) -> double {
-        long long r = order[start + i];
-        return ok[q] ? X[r * ldx + cols[q]] : 0.0;
+            for (int q = 0; q < 4; ++q) out4[q] = cols[q] < D ? p[cols[q]] : 0.0;
+        }
     };
     double res[4];
     if (n < 8) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) res[q] = 0.0;
         for (int i = 0; i < n; ++i) {
-            long long r = order[start + i];
+            double v[4];
+            load_row(order[start + i], v);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) res[q] = dadd(res[q], ok[q] ? X[r * ldx + cols[q]] : 0.0);
+            for (int q = 0; q < 4; ++q) res[q] = dadd(res[q], v[q]);
         }
     } else {
         double acc[8][4];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            long long r = order[start + j];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) acc[j][q] = ok[q] ? X[r * ldx + cols[q]] : 0.0;
-        }
+        for (int j = 0; j < 8; ++j) load_row(order[start + j], acc[j]);
         int i = 8;
         const int stop = n - (n % 8);
         for (; i < stop; i += 8) {
-            long long rr[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) rr[j] = order[start + i + j];
+            for (int h = 0; h < 8; h += 4) {
+                double v[4][4];
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
+                for (int j = 0; j < 4; ++j) load_row(order[start + i + h + j], v[j]);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) acc[j][q] = dadd(acc[j][q], ok[q] ? X[rr[j] * ldx + cols[q]] : 0.0);
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc[h + j][q] = dadd(acc[h + j][q], v[j][q]);
+            }
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q)
             res[q] = dadd(dadd(dadd(acc[0][q], acc[1][q]), dadd(acc[2][q], acc[3][q])),
                           dadd(dadd(acc[4][q], acc[5][q]), dadd(acc[6][q], acc[7][q])));
         for (; i < n; ++i) {
+            double v[4];
+            load_row(order[start + i], v);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) res[q] = dadd(res[q], val(i, q));
+            for (int q = 0; q < 4; ++q) res[q] = dadd(res[q], v[q]);
         }
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-        if (ok[q]) leaf_sums[leaf * D + cols[q]] = res[q];
+        if (cols[q] < D) leaf_sums[leaf * D + cols[q]] = res[q];
 }
 
 // One warp per (codeword, column chunk): fold leaves up the recursion tree,
@@ -369,10 +407,13 @@ int launch_group_sums(const double* X, long long n, long long ldx, int D, const 
     size_t sh = (K <= GS_SMEM_HIST) ? sizeof(int32_t) * K : 0;
     tile_hist_kernel<<<T, 256, sh, s>>>(labels, n, K, T, hist);
     DA_CHECK_LAUNCH("tile_hist_kernel");
-    exclusive_scan_kernel<<<1, 1024, 0, s>>>(hist, KT, total);
-    DA_CHECK_LAUNCH("exclusive_scan_kernel(hist)");
-    seg_counts_kernel<<<grid_for(K, 256), 256, 0, s>>>(hist, K, T, n, seg, counts);
-    DA_CHECK_LAUNCH("seg_counts_kernel");
+    label_tile_scan_kernel<<<grid_for(K, 8), 256, 0, s>>>(hist, K, T, counts);
+    DA_CHECK_LAUNCH("label_tile_scan_kernel");
+    DA_CUDA(cudaMemcpyAsync(seg, counts, sizeof(int32_t) * K, cudaMemcpyDeviceToDevice, s));
+    exclusive_scan_kernel<<<1, 1024, 0, s>>>(seg, K, total);
+    DA_CHECK_LAUNCH("exclusive_scan_kernel(counts)");
+    add_seg_start_kernel<<<grid_for(KT, 256, 1LL << 31), 256, 0, s>>>(hist, K, T, seg);
+    DA_CHECK_LAUNCH("add_seg_start_kernel");
     stable_scatter_kernel<<<T, 32, sh, s>>>(labels, n, K, T, hist, order);
     DA_CHECK_LAUNCH("stable_scatter_kernel");
     leaf_count_kernel<<<grid_for(K, 256), 256, 0, s>>>(counts, K, nleaf);
