@@ -289,15 +289,28 @@ def main():
         Pt_a, sq_a = E.cross_full(cw_a)
         cfg1 = da.TrainConfig(m_count=M, k_count=K, beam_width=L, sweeps=1, rel_tol=0.0)
         rep = da.TrainReport(config=cfg1)
+        comm = None
+        if dist is not None:
+            from paper_1509_05194_b200 import distributed as DD
+
+            comm = DD.Comm()  # NCCL: per-iteration allreduce of K x D sums + counts
         _native.prof_enable(True)
         barrier()
         t0 = time.perf_counter()
-        E.da_sweep(X, cw_a, codes_a, Pt_a, sq_a, cfg1, report=rep, comm=None)
+        if comm is None:
+            E.da_sweep(X, cw_a, codes_a, Pt_a, sq_a, cfg1, report=rep, comm=None)
+        else:
+            DD.da_sweep_sharded(X, cw_a, codes_a, Pt_a, sq_a, cfg1, comm, report=rep)
         torch.cuda.synchronize()
         anneal_s = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([anneal_s], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            anneal_s = float(t.item())
         _native.prof_enable(False)
         aprof = _native.prof_collect()
-        anneal = {"seconds": anneal_s, "per_dictionary_s": [round(s.seconds, 4) for s in rep.steps],
+        anneal = {"seconds": anneal_s, "rows": n * world, "gpus": world,
+                  "per_dictionary_s": [round(s.seconds, 4) for s in rep.steps],
                   "distortion_after": rep.steps[-1].distortion,
                   "kernels_ms": {k: round(v[1], 3) for k, v in aprof.items()}}
 

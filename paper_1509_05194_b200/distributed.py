@@ -38,18 +38,30 @@ class Comm:
         self._sizes = {}
         self.row_offset = 0
 
+    @property
+    def _host_staged(self) -> bool:
+        # gloo reduces on the host; NCCL works on device memory directly
+        return self.dist.get_backend(self.group) != "nccl"
+
     def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
+        if self._host_staged and t.is_cuda:
+            h = t.cpu()
+            self.dist.all_reduce(h, op=self.dist.ReduceOp.SUM, group=self.group)
+            t.copy_(h)
+            return t
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return t
 
     def allgather(self, t: torch.Tensor) -> torch.Tensor:
-        parts = [torch.empty_like(t) for _ in range(self.world)]
-        self.dist.all_gather(parts, t.contiguous(), group=self.group)
-        return torch.cat(parts, dim=0)
+        src = t.contiguous().cpu() if (self._host_staged and t.is_cuda) else t.contiguous()
+        parts = [torch.empty_like(src) for _ in range(self.world)]
+        self.dist.all_gather(parts, src, group=self.group)
+        out = torch.cat(parts, dim=0)
+        return out.to(t.device) if t.is_cuda else out
 
     def sizes(self, n_local: int) -> list:
         if n_local not in self._sizes:
-            dev = "cuda" if torch.cuda.is_available() and self.dist.get_backend(self.group) == "nccl" else "cpu"
+            dev = "cpu" if self._host_staged else "cuda"
             t = torch.tensor([n_local], dtype=torch.int64, device=dev)
             self._sizes[n_local] = [int(x) for x in self.allgather(t).cpu().tolist()]
         return self._sizes[n_local]
