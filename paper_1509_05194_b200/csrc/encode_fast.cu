@@ -161,7 +161,10 @@ struct FastSmem {
 
 __host__ __device__ inline size_t fast_vbuf_bytes(int cap, int K, int D) {
     size_t a = sizeof(float) * (size_t)cap * K, b = sizeof(double) * (size_t)D;
-    return ((a > b ? a : b) + 15) & ~size_t(15);
+    size_t c = (sizeof(double) + sizeof(int)) * (size_t)QCAP;  // exact (value, flat) of queued candidates
+    size_t m = a > b ? a : b;
+    m = m > c ? m : c;
+    return (m + 15) & ~size_t(15);
 }
 
 __host__ __device__ inline size_t fast_smem_bytes(int cap, int M, int K, int D) {
@@ -262,16 +265,28 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
         const double e_cross = (m + 2.0) * u * cb;
         const double E = 2.0 * (e_t + 2.0 * e_cross + 4.0 * u * (smax + tmax + 2.0 * cb) + u * smax) + 1e-300;
 
-        // ---- pass A: approximate candidate values, two smallest per lane.
-        // Lanes own k = kb + 32q + lane (q < 8); four beams are processed together
-        // so every lane keeps 32 independent L2 gathers in flight per term j.
+        // ---- pass A: approximate candidate values; per lane the two smallest
+        // (and the index of the smallest).  With K % 256 == 0 a lane owns
+        // k = kb + 4*lane + {0..3} and kb + 128 + 4*lane + {0..3} (16-B gathers),
+        // otherwise k = kb + 32q + lane.  Four beams are processed together.
+        const bool vec = (K & 255) == 0;
+        auto kof = [&](int kb, int q) -> int {
+            return vec ? kb + (q >> 2) * 128 + 4 * lane + (q & 3) : kb + 32 * q + lane;
+        };
         float m1 = __int_as_float(0x7f800000), m2 = m1;
+        int i1 = -1;
         for (int kb = 0; kb < K; kb += 256) {
             float tk[8];
+            if (vec) {
+                const float4 a = *reinterpret_cast<const float4*>(trow + m * K + kb + 4 * lane);
+                const float4 b = *reinterpret_cast<const float4*>(trow + m * K + kb + 128 + 4 * lane);
+                tk[0] = a.x; tk[1] = a.y; tk[2] = a.z; tk[3] = a.w; tk[4] = b.x; tk[5] = b.y; tk[6] = b.z; tk[7] = b.w;
+            } else {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int k = kb + q * 32 + lane;
-                tk[q] = (k < K) ? trow[m * K + k] : 0.f;
+                for (int q = 0; q < 8; ++q) {
+                    const int k = kof(kb, q);
+                    tk[q] = (k < K) ? trow[m * K + k] : 0.f;
+                }
             }
             for (int l0 = 0; l0 < live; l0 += 4) {
                 float acc[4][8];
@@ -284,14 +299,24 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
 #pragma unroll
                     for (int g = 0; g < 4; ++g) {
                         const int l = min(l0 + g, live - 1);
-                        rp[g] = P32 + (((long long)j * M + m) * K + pc[l * M + j]) * K + kb + lane;
+                        rp[g] = P32 + (((long long)j * M + m) * K + pc[l * M + j]) * K + kb;
                     }
                     float vals[4][8];
+                    if (vec) {
 #pragma unroll
-                    for (int g = 0; g < 4; ++g)
+                        for (int g = 0; g < 4; ++g) {
+                            const float4 a = __ldg(reinterpret_cast<const float4*>(rp[g] + 4 * lane));
+                            const float4 b = __ldg(reinterpret_cast<const float4*>(rp[g] + 128 + 4 * lane));
+                            vals[g][0] = a.x; vals[g][1] = a.y; vals[g][2] = a.z; vals[g][3] = a.w;
+                            vals[g][4] = b.x; vals[g][5] = b.y; vals[g][6] = b.z; vals[g][7] = b.w;
+                        }
+                    } else {
 #pragma unroll
-                        for (int q = 0; q < 8; ++q)
-                            vals[g][q] = (kb + q * 32 + lane < K) ? __ldg(rp[g] + q * 32) : 0.f;
+                        for (int g = 0; g < 4; ++g)
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                vals[g][q] = (kof(kb, q) < K) ? __ldg(rp[g] + 32 * q + lane) : 0.f;
+                    }
 #pragma unroll
                     for (int g = 0; g < 4; ++g)
 #pragma unroll
@@ -302,14 +327,21 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
                     const int l = l0 + g;
                     if (l >= live) break;
                     const float sl = (float)ps[l];
+                    float vv[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) vv[q] = (sl + tk[q]) + 2.f * acc[g][q];
+                    if (vec) {
+                        *reinterpret_cast<float4*>(S.vbuf + l * K + kb + 4 * lane) = make_float4(vv[0], vv[1], vv[2], vv[3]);
+                        *reinterpret_cast<float4*>(S.vbuf + l * K + kb + 128 + 4 * lane) =
+                            make_float4(vv[4], vv[5], vv[6], vv[7]);
+                    }
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
-                        const int k = kb + q * 32 + lane;
+                        const int k = kof(kb, q);
                         if (k < K) {
-                            const float vv = (sl + tk[q]) + 2.f * acc[g][q];
-                            S.vbuf[l * K + k] = vv;
-                            if (vv < m1) { m2 = m1; m1 = vv; }
-                            else if (vv < m2) m2 = vv;
+                            if (!vec) S.vbuf[l * K + k] = vv[q];
+                            if (vv[q] < m1) { m2 = m1; m1 = vv[q]; i1 = l * K + k; }
+                            else if (vv[q] < m2) m2 = vv[q];
                         }
                     }
                 }
@@ -322,20 +354,17 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
         if (width >= total) {
             thr = __int_as_float(0x7f800000);
         } else if (width <= 64) {
-            // bitonic sort of 64 values (2 per lane: index lane and lane+32)
-            // rank of each of the 64 values (position lane / lane+32), ties by position
             const float a = m1, b = m2;
-            float key0 = a, key1 = b;
             int r0 = 0, r1 = 0;
-            for (int s = 0; s < 32; ++s) {
-                float o0 = __shfl_sync(FULL, a, s), o1 = __shfl_sync(FULL, b, s);
-                r0 += (o0 < key0) || (o0 == key0 && s < lane);
-                r0 += (o1 < key0) || (o1 == key0 && s + 32 < lane);
-                r1 += (o0 < key1) || (o0 == key1 && s < lane + 32);
-                r1 += (o1 < key1) || (o1 == key1 && s + 32 < lane + 32);
+            for (int s2 = 0; s2 < 32; ++s2) {
+                const float o0 = __shfl_sync(FULL, a, s2), o1 = __shfl_sync(FULL, b, s2);
+                r0 += (o0 < a) || (o0 == a && s2 < lane);
+                r0 += (o1 < a);
+                r1 += (o0 < b) || (o0 == b);
+                r1 += (o1 < b) || (o1 == b && s2 < lane);
             }
-            float t0 = (r0 == width - 1) ? key0 : -__int_as_float(0x7f800000);
-            float t1 = (r1 == width - 1) ? key1 : -__int_as_float(0x7f800000);
+            float t0 = (r0 == width - 1) ? a : -__int_as_float(0x7f800000);
+            float t1 = (r1 == width - 1) ? b : -__int_as_float(0x7f800000);
             float t = fmaxf(t0, t1);
             for (int off = 16; off >= 1; off >>= 1) t = fmaxf(t, __shfl_xor_sync(FULL, t, off));
             thr = t;
@@ -343,82 +372,124 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
             thr = __int_as_float(0x7f800000);  // wide beams: recheck everything
         }
         const double lim = (double)thr + 2.0 * E;
-
-        // ---- pass B: exact recheck of every candidate with v' <= tau' + 2E
-        int cnt = 0;
-        auto accept = [&](double a, int fa) -> bool {
-            if (cnt < width) return true;
-            return lex_less(a, fa, S.lv[width - 1], S.lf[width - 1]);
-        };
-        // candidates to recheck, pushed by each lane from its own positions; the
-        // processing order is irrelevant (the exact list is ordered by (value, flat))
         const float limf = (lim >= 3.0e38) ? __int_as_float(0x7f800000) : __fadd_ru((float)lim, fabsf((float)lim) * 1e-6f);
-        int* qcount = S.queue + 32;  // [0] = count
+
+        // ---- queue every candidate with v' <= lim: a lane whose second smallest is
+        // above lim contributes at most its smallest; the (few) other lanes are
+        // rescanned by the whole warp.
+        int* qcount = S.queue + 32;
         if (lane == 0) *qcount = 0;
         __syncwarp();
-        for (int i = lane; i < total; i += 32) {
-            if (S.vbuf[i] <= limf) {
-                const int slot = atomicAdd(qcount, 1);
-                if (slot < QCAP) S.queue[33 + slot] = i;
+        const bool multi = m2 <= limf;
+        if (m1 <= limf && !multi) {
+            const int slot = atomicAdd(qcount, 1);
+            if (slot < QCAP) S.queue[33 + slot] = i1;
+        }
+        unsigned flagged = __ballot_sync(FULL, multi);
+        const int per_lane = live * ((K + 31) / 32);
+        while (flagged) {
+            const int f = __ffs(flagged) - 1;
+            flagged &= flagged - 1;
+            for (int t = lane; t < per_lane; t += 32) {
+                // t enumerates (l, kb, q) of lane f's candidates
+                const int l = t / ((K + 31) / 32);
+                const int rem = t % ((K + 31) / 32);
+                const int kb = (rem >> 3) * 256, q = rem & 7;
+                const int k = vec ? kb + (q >> 2) * 128 + 4 * f + (q & 3) : kb + 32 * q + f;
+                if (k < K && S.vbuf[l * K + k] <= limf) {
+                    const int slot = atomicAdd(qcount, 1);
+                    if (slot < QCAP) S.queue[33 + slot] = l * K + k;
+                }
             }
         }
         __syncwarp();
-        int nqueued = *qcount;
-        if (nqueued > QCAP) {
-            // rare: too many near-boundary candidates; recheck all of them in flat order
-            nqueued = -1;
-        }
+        const int nqueued = *qcount;
         __syncwarp();
-        auto flush = [&](int base_i, int nq, bool from_queue) {
-            double val = 0.0;
-            int flat = 0;
-            const bool has = lane < nq;
-            if (has) {
-                flat = from_queue ? S.queue[33 + base_i + lane] : base_i + lane;
-                const int l = flat / K, k = flat % K;
-                const double xc = exact_dot(S.x64, cw64 + ((long long)m * K + k) * D, D);
-                const double t = dsub(sq[m * K + k], dmul(2.0, xc));
-                double cross = 0.0;
-                for (int j = 0; j < m; ++j)
-                    cross = dadd(cross, P[(((long long)j * M + m) * K + pc[l * M + j]) * K + k]);
-                val = dadd(dadd(ps[l], t), dmul(2.0, cross));
-            }
-            n_exact += has ? 1 : 0;
-            unsigned mask = __ballot_sync(FULL, has && accept(val, flat));
-            while (mask) {
-                const int src = __ffs(mask) - 1;
-                const double cv = __shfl_sync(FULL, val, src);
-                const int cf = __shfl_sync(FULL, flat, src);
-                int pos = 0;
-                for (int b = 0; b < cnt; b += 32) {
-                    int i = b + lane;
-                    bool lt = (i < cnt) && lex_less(S.lv[i], S.lf[i], cv, cf);
-                    pos += __popc(__ballot_sync(FULL, lt));
-                }
-                const int end = min(cnt, width - 1);
-                for (int b = end - 1; b >= pos; b -= 32) {
-                    int i = b - lane;
-                    bool act = i >= pos;
-                    double tv = 0.0;
-                    int tf = 0;
-                    if (act) { tv = S.lv[i]; tf = S.lf[i]; }
-                    __syncwarp();
-                    if (act) { S.lv[i + 1] = tv; S.lf[i + 1] = tf; }
-                    __syncwarp();
-                }
-                if (lane == 0) { S.lv[pos] = cv; S.lf[pos] = cf; }
-                __syncwarp();
-                cnt = min(cnt + 1, width);
-                mask &= ~(1u << src);
-                mask &= __ballot_sync(FULL, has && accept(val, flat));
-            }
+        auto exact_value = [&](int flat) -> double {
+            const int l = flat / K, k = flat % K;
+            const double xc = exact_dot(S.x64, cw64 + ((long long)m * K + k) * D, D);
+            const double t = dsub(sq[m * K + k], dmul(2.0, xc));
+            double cross = 0.0;
+            for (int j = 0; j < m; ++j) cross = dadd(cross, P[(((long long)j * M + m) * K + pc[l * M + j]) * K + k]);
+            return dadd(dadd(ps[l], t), dmul(2.0, cross));
         };
-        if (nqueued >= 0) {
-            for (int b = 0; b < nqueued; b += 32) flush(b, min(32, nqueued - b), true);
+        int cnt = 0;
+        if (nqueued <= QCAP) {
+            // exact values of the queued candidates, then exact top-width by
+            // (value, flat) rank; queue entries are distinct
+            double* ev = reinterpret_cast<double*>(S.vbuf);
+            int* ef = reinterpret_cast<int*>(ev + QCAP);
+            int qf[QCAP / 32 + 1];
+            double qv[QCAP / 32 + 1];
+            int nmine = 0;
+            for (int b = 0; b < nqueued; b += 32) {
+                const int i = b + lane;
+                if (i < nqueued) {
+                    const int flat = S.queue[33 + i];
+                    qf[nmine] = flat;
+                    qv[nmine] = exact_value(flat);
+                    ++nmine;
+                }
+            }
+            n_exact += nmine;
+            __syncwarp();
+            for (int b = 0, t = 0; b < nqueued; b += 32, ++t) {
+                const int i = b + lane;
+                if (i < nqueued) { ev[i] = qv[t]; ef[i] = qf[t]; }
+            }
+            __syncwarp();
+            for (int b = 0, t = 0; b < nqueued; b += 32, ++t) {
+                const int i = b + lane;
+                if (i < nqueued) {
+                    int rank = 0;
+                    for (int j = 0; j < nqueued; ++j) rank += lex_less(ev[j], ef[j], qv[t], qf[t]);
+                    if (rank < width) { S.lv[rank] = qv[t]; S.lf[rank] = qf[t]; }
+                }
+            }
+            cnt = width;
+            __syncwarp();
         } else {
-            for (int b = 0; b < total; b += 32) flush(b, min(32, total - b), false);
+            // rare: too many near-boundary candidates -> exact streaming selection over all
+            auto accept = [&](double a, int fa) -> bool {
+                if (cnt < width) return true;
+                return lex_less(a, fa, S.lv[width - 1], S.lf[width - 1]);
+            };
+            for (int b = 0; b < total; b += 32) {
+                const int flat = b + lane;
+                const bool has = flat < total;
+                const double val = has ? exact_value(flat) : 0.0;
+                n_exact += has ? 1 : 0;
+                unsigned mask = __ballot_sync(FULL, has && accept(val, flat));
+                while (mask) {
+                    const int src = __ffs(mask) - 1;
+                    const double cv = __shfl_sync(FULL, val, src);
+                    const int cf = __shfl_sync(FULL, flat, src);
+                    int pos = 0;
+                    for (int bb = 0; bb < cnt; bb += 32) {
+                        int i = bb + lane;
+                        bool lt = (i < cnt) && lex_less(S.lv[i], S.lf[i], cv, cf);
+                        pos += __popc(__ballot_sync(FULL, lt));
+                    }
+                    const int endp = min(cnt, width - 1);
+                    for (int bb = endp - 1; bb >= pos; bb -= 32) {
+                        int i = bb - lane;
+                        bool act = i >= pos;
+                        double tv = 0.0;
+                        int tf = 0;
+                        if (act) { tv = S.lv[i]; tf = S.lf[i]; }
+                        __syncwarp();
+                        if (act) { S.lv[i + 1] = tv; S.lf[i + 1] = tf; }
+                        __syncwarp();
+                    }
+                    if (lane == 0) { S.lv[pos] = cv; S.lf[pos] = cf; }
+                    __syncwarp();
+                    cnt = min(cnt + 1, width);
+                    mask &= ~(1u << src);
+                    mask &= __ballot_sync(FULL, has && accept(val, flat));
+                }
+            }
+            __syncwarp();
         }
-        __syncwarp();
 
         // ---- next beam in flat (lexicographic) order
         const int nxt = cur ^ 1;
