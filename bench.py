@@ -124,6 +124,8 @@ def peaks():
         out["fp32_ffma_tflops"] = max(r["fp32_ffma_tflops"] for r in rows)
     except Exception:
         out["fp64_dfma_tflops"], out["fp32_ffma_tflops"] = 34.0, 70.8
+    # dense TF32 tensor peak: no measured figure on this pool; B200_PROFILING.md nominal
+    out.setdefault("tf32_tflops", 1100.0)
     return out
 
 
@@ -320,7 +322,8 @@ def main():
                for k, (c, t) in prof.items()}
     # the score-table GEMM is the nearest-codeword contraction: 2*M*K*D flop per vector
     for gname, peak_key, prec in (("encode_table_sgemm", "fp32_ffma_tflops", "fp32"),
-                                  ("encode_table_gemm", "fp64_dfma_tflops", "fp64")):
+                                  ("encode_table_gemm", "fp64_dfma_tflops", "fp64"),
+                                  ("encode_beam_tc", "tf32_tflops", "3xtf32")):
         if gname in prof:
             c, t = prof[gname]
             rows = n * args.steps / max(c, 1)

@@ -121,10 +121,13 @@ int da_encode(const void* X, int x_f32, int64_t n, int64_t ldx, int D, const flo
               const double* sq, const double* P, void* codes, int code_bytes, int64_t ldcodes, double* err,
               void* stream);
 
-/* Encoder selection: mode 0 (default) = fp32 score tables + rigorous error bound +
- * exact float64 recheck of the candidates that can still make the beam (same
- * codes/errors as mode 1); mode 1 = plain float64 tables.  recheck_counter (device,
- * optional) accumulates the number of exactly rechecked candidates. */
+/* Encoder selection (all modes return identical codes/errors):
+ *   0 (default) = 2; 1 = plain float64 score tables;
+ *   2 = fp32 score table + fp32 cross-table gathers as a filter with a rigorous
+ *       error bound, exact float64 recheck of the candidates that can still make the beam;
+ *   3 = tcgen05 filter: per stage one 3xTF32 GEMM of the beams' residuals against the
+ *       dictionary (score = s + ||c||^2 - 2 r.c), same bound + exact recheck.
+ * recheck_counter (device, optional) accumulates the number of exactly rechecked candidates. */
 int da_encode_config(int mode, unsigned long long* recheck_counter);
 
 /* Query-independent ADC term 2 sum_{a<b} P[a,b][i_a,i_b].  replaces code_pair_sums codebook.py:388-396 */

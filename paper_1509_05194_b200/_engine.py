@@ -413,8 +413,9 @@ def assign_config(mode: int, counter: torch.Tensor | None = None) -> None:
 
 
 def encode_config(mode: int, counter: torch.Tensor | None = None) -> None:
-    """0 = filtered fp32 fast path with exact float64 recheck (default),
-    1 = plain float64 tables.  `counter` (int64 CUDA tensor) accumulates rechecks."""
+    """0 = tcgen05 residual-GEMM filter with exact float64 recheck (default; falls
+    back to 2 then 1 outside its shapes), 1 = plain float64 tables, 2 = fp32
+    score-table + cross-gather filter.  `counter` accumulates exact rechecks."""
     native.da_encode_config(int(mode), P(counter))
 
 

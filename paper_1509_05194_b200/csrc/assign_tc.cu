@@ -343,21 +343,26 @@ __global__ void __launch_bounds__(TC_T2, 1) assign_tc_kernel(
                 mbar_arrive_expect_tx(&full_bar[st], (uint32_t)(2 * B_ELEMS * sizeof(float)));
                 bulk_g2s(Bs, Bg + (size_t)ch * 2 * B_ELEMS, (uint32_t)(2 * B_ELEMS * sizeof(float)), &full_bar[st]);
             }
-            // stage 16 rows per warp, one coalesced row segment per iteration
+            // stage 16 rows per warp as 8x4 blocks: lane -> (row 8-group row L/4,
+            // k = 4-group + L%4).  Each block is one 8x16-B core matrix in shared
+            // memory (all 32 banks once) and 8 full 32-B sectors in global memory.
             const int k0 = ch * TC_BK;
-            const int gk = k0 + lane;
-            double xv[TC_M / 8];
+            double xv[16];
 #pragma unroll
-            for (int i = 0; i < TC_M / 8; ++i) {  // all 16 row loads in flight first
-                const long long r = row0 + warp * (TC_M / 8) + i;
-                xv[i] = (r < n && gk < d) ? (double)X[r * ldx + gk] : 0.0;
+            for (int it2 = 0; it2 < 16; ++it2) {
+                const int rg = it2 >> 3, kg = it2 & 7;
+                const int rr = warp * (TC_M / 8) + rg * 8 + (lane >> 2);
+                const int gk = k0 + kg * 4 + (lane & 3);
+                const long long r = row0 + rr;
+                xv[it2] = (r < n && gk < d) ? (double)X[r * ldx + gk] : 0.0;
             }
 #pragma unroll
-            for (int i = 0; i < TC_M / 8; ++i) {
-                const int rr = warp * (TC_M / 8) + i;
-                const float h = to_tf32((float)xv[i]);
-                const float l = to_tf32((float)(xv[i] - (double)h));
-                const uint32_t o = kmajor_off(rr, lane) >> 2;
+            for (int it2 = 0; it2 < 16; ++it2) {
+                const int rg = it2 >> 3, kg = it2 & 7;
+                const int rr = warp * (TC_M / 8) + rg * 8 + (lane >> 2);
+                const float h = to_tf32((float)xv[it2]);
+                const float l = to_tf32((float)(xv[it2] - (double)h));
+                const uint32_t o = kmajor_off(rr, kg * 4 + (lane & 3)) >> 2;
                 Ah[o] = h;
                 Al[o] = l;
             }

@@ -21,7 +21,8 @@ namespace da {
 
 static thread_local std::string g_last_error;
 static std::atomic<long long> g_launches{0};
-static int g_encode_mode = 0;                        // 0 auto (filtered fp32 + exact recheck), 1 plain float64
+// 0 auto (fp32 gather filter), 1 plain float64, 2 fp32 gather filter, 3 tcgen05 residual-GEMM filter
+static int g_encode_mode = 0;
 static unsigned long long* g_encode_stats = nullptr;  // device counter of exact rechecks
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -84,7 +85,8 @@ int da_version(void) { return DA_B200_ABI_VERSION; }
 long long da_launch_count(void) { return g_launches.load(); }
 
 int da_encode_config(int mode, unsigned long long* recheck_counter) {
-    if (mode != 0 && mode != 1) return fail_arg("encode mode must be 0 (auto) or 1 (plain float64)");
+    if (mode < 0 || mode > 3)
+        return fail_arg("encode mode must be 0 (auto), 1 (plain float64), 2 (fp32 gather filter) or 3 (tcgen05 filter)");
     g_encode_mode = mode;
     g_encode_stats = recheck_counter;
     return 0;
@@ -299,6 +301,12 @@ int da_encode(const void* X, int x_f32, int64_t n, int64_t ldx, int D, const flo
     if (L < 1) return fail_arg("beam_width must be >= 1");
     if (code_bytes != 1 && code_bytes != 2 && code_bytes != 4) return fail_arg("code_bytes must be 1, 2 or 4");
     if (M < 1 || K < 1 || D < 1) return fail_arg("encode: bad codebook shape");
+    if (x_f32 && g_encode_mode == 3) {
+        int rc = launch_encode_tc((const float*)X, n, ldx, D, cw, M, K, L, sq, P, codes, code_bytes, ldcodes, err,
+                                  g_encode_stats, STREAM(stream));
+        if (rc <= 0) return rc;  // > 0: shape outside the tensor-core encoder
+        cudaGetLastError();
+    }
     if (x_f32 && g_encode_mode != 1) {
         int rc = launch_encode_fast(X, x_f32, n, ldx, D, cw, M, K, L, sq, P, codes, code_bytes, ldcodes, err,
                                     g_encode_stats, STREAM(stream));

@@ -157,6 +157,7 @@ struct FastSmem {
     double* x64;     // [D]
     float* vbuf;     // [cap*K] approximate values; reused as D doubles for the error
     int32_t* queue;  // [33 + QCAP]: [32] = count, [33..] = queued flat indices
+    long long* roff; // [cap*M] cross-table row offsets of the current stage
 };
 
 __host__ __device__ inline size_t fast_vbuf_bytes(int cap, int K, int D) {
@@ -168,7 +169,7 @@ __host__ __device__ inline size_t fast_vbuf_bytes(int cap, int K, int D) {
 }
 
 __host__ __device__ inline size_t fast_smem_bytes(int cap, int M, int K, int D) {
-    size_t b = sizeof(double) * (3 * (size_t)cap + D);
+    size_t b = sizeof(double) * (3 * (size_t)cap + D) + sizeof(long long) * (size_t)cap * M;
     b = (b + 15) & ~size_t(15);
     b += fast_vbuf_bytes(cap, K, D);
     b += sizeof(int32_t) * (2 * (size_t)cap * M + cap + 33 + QCAP);
@@ -182,6 +183,7 @@ __device__ inline FastSmem carve_fast(char* p, int cap, int M, int K, int D) {
     s.score[1] = (double*)p; p += sizeof(double) * cap;
     s.lv = (double*)p; p += sizeof(double) * cap;
     s.x64 = (double*)p; p += sizeof(double) * D;
+    s.roff = (long long*)p; p += sizeof(long long) * cap * M;
     p = p0 + (((size_t)(p - p0) + 15) & ~size_t(15));
     s.vbuf = (float*)p; p += fast_vbuf_bytes(cap, K, D);
     s.codes[0] = (int32_t*)p; p += sizeof(int32_t) * cap * M;
@@ -265,6 +267,11 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
         const double e_cross = (m + 2.0) * u * cb;
         const double E = 2.0 * (e_t + 2.0 * e_cross + 4.0 * u * (smax + tmax + 2.0 * cb) + u * smax) + 1e-300;
 
+        for (int e = lane; e < live * m; e += 32) {
+            const int l = e / m, j = e % m;
+            S.roff[l * M + j] = (((long long)j * M + m) * K + pc[l * M + j]) * K;
+        }
+        __syncwarp();
         // ---- pass A: approximate candidate values; per lane the two smallest
         // (and the index of the smallest).  With K % 256 == 0 a lane owns
         // k = kb + 4*lane + {0..3} and kb + 128 + 4*lane + {0..3} (16-B gathers),
@@ -297,10 +304,7 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
                 for (int j = 0; j < m; ++j) {
                     const float* rp[4];
 #pragma unroll
-                    for (int g = 0; g < 4; ++g) {
-                        const int l = min(l0 + g, live - 1);
-                        rp[g] = P32 + (((long long)j * M + m) * K + pc[l * M + j]) * K + kb;
-                    }
+                    for (int g = 0; g < 4; ++g) rp[g] = P32 + S.roff[min(l0 + g, live - 1) * M + j] + kb;
                     float vals[4][8];
                     if (vec) {
 #pragma unroll
@@ -335,12 +339,22 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
                         *reinterpret_cast<float4*>(S.vbuf + l * K + kb + 128 + 4 * lane) =
                             make_float4(vv[4], vv[5], vv[6], vv[7]);
                     }
+                    if (!vec) {
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const int k = kof(kb, q);
-                        if (k < K) {
-                            if (!vec) S.vbuf[l * K + k] = vv[q];
-                            if (vv[q] < m1) { m2 = m1; m1 = vv[q]; i1 = l * K + k; }
+                        for (int q = 0; q < 8; ++q) {
+                            const int k = kof(kb, q);
+                            if (k < K) S.vbuf[l * K + k] = vv[q];
+                            else vv[q] = __int_as_float(0x7f800000);
+                        }
+                    }
+                    // batch minimum first; the per-candidate update only runs when the
+                    // batch can change the lane's two smallest (rare after warm-up)
+                    float bmin = fminf(fminf(fminf(vv[0], vv[1]), fminf(vv[2], vv[3])),
+                                       fminf(fminf(vv[4], vv[5]), fminf(vv[6], vv[7])));
+                    if (bmin < m2) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            if (vv[q] < m1) { m2 = m1; m1 = vv[q]; i1 = l * K + kof(kb, q); }
                             else if (vv[q] < m2) m2 = vv[q];
                         }
                     }

@@ -1,0 +1,704 @@
+// Beam encoder on the tensor cores (tcgen05), one CTA per group of vectors.
+//
+// Same contract as encode.cu / encode_fast.cu (annq/codebook.py:255-300, the
+// result is bit-identical), different arithmetic for the FILTER:
+//   the reference's stage score  (s_l + t[m,k]) + 2 sum_{j<m} P[j,m][c_lj,k]
+//   equals                        s_l + ||c_mk||^2 - 2 r_l . c_mk
+// with r_l = x - sum_{j<m} c_j(c_lj) the beam's residual.  So one GEMM per
+// stage -- rows = (vector, beam) residuals, columns = the K codewords of
+// dictionary m -- gives every candidate's approximate score: tcgen05.mma
+// kind::tf32 with a 3xTF32 split, fp32 accumulators in TMEM (128 x 256).
+// No score table and no cross-table gathers are needed for the filter.
+// A rigorous bound E (residual rounding, 3xTF32 + fp32 accumulation, fp32
+// score arithmetic) selects the candidates that can still make the exact
+// top-width; those are recomputed in float64 exactly as the reference does
+// (BLAS-ordered x.c, einsum ||c||^2, sequential cross sum) and the beam keeps
+// exact float64 scores.
+//
+// Layout per CTA (128 threads = 128 TMEM lanes = 128 rows): V = 128 / cap
+// vectors; row v*cap + l holds beam l of vector v.  Residuals live in a global
+// scratch slab (L2-resident), staged per 32-wide k-chunk as tf32 hi/lo into the
+// canonical no-swizzle K-major layout; codeword chunks arrive by bulk copy.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstdint>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace da {
+
+namespace {
+constexpr int BT_ROWS = 128;
+constexpr int BT_N = 256;
+constexpr int BT_BK = 32;
+constexpr int BT_T = 128;
+constexpr int BT_TMAX = 16;  // smallest approximate values kept per row
+}  // namespace
+
+__device__ __forceinline__ uint32_t bt_smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ float bt_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+__device__ __forceinline__ uint32_t bt_off(int r, int k) {
+    return (uint32_t)((((r >> 3) * (BT_BK / 4) + (k >> 2)) << 7) + ((r & 7) << 4) + ((k & 3) << 2));
+}
+__device__ __forceinline__ uint64_t bt_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((128 >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)(((BT_BK / 4) * 128 >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+__device__ __forceinline__ void bt_mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void bt_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE_%=;\n\tbra WAIT_%=;\n\tDONE_%=:\n\t}\n" ::"r"(bt_smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void bt_ld32(uint32_t taddr, float* v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// exact x.c in the reference's order (FMA chain, OpenBLAS k-blocks above 384)
+__device__ __forceinline__ double bt_exact_dot(const double* __restrict__ x, const double* __restrict__ c, int D) {
+    double tot = 0.0;
+    bool first = true;
+    int d = 0;
+    while (d < D) {
+        const int e = d + (int)blas_block_len(D - d);
+        double acc = 0.0;
+        for (; d + 8 <= e; d += 8) {
+            double xv[8], cv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) { xv[u] = x[d + u]; cv[u] = c[d + u]; }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = __fma_rn(xv[u], cv[u], acc);
+        }
+        for (; d < e; ++d) acc = __fma_rn(x[d], c[d], acc);
+        tot = first ? acc : dadd(tot, acc);
+        first = false;
+    }
+    return tot;
+}
+
+// Codebook -> per (dictionary, k-chunk) tf32 hi/lo tiles in the shared-memory image.
+__global__ void cb_tf32_prep_kernel(const float* __restrict__ cw, int M, int K, int D, int nch,
+                                    float* __restrict__ out) {
+    const long long per = (long long)BT_N * BT_BK;
+    const long long total = (long long)M * nch * per;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        const int mc = (int)(e / per);
+        const int m = mc / nch, ch = mc % nch;
+        const int rem = (int)(e % per);
+        const int r = rem / BT_BK, k = rem % BT_BK;
+        const int gk = ch * BT_BK + k;
+        float h = 0.f, l = 0.f;
+        if (r < K && gk < D) {
+            const float v = cw[((long long)m * K + r) * D + gk];
+            h = bt_tf32(v);
+            l = bt_tf32(v - h);
+        }
+        float* base = out + (size_t)mc * 2 * per;
+        const uint32_t o = bt_off(r, k) >> 2;
+        base[o] = h;
+        base[per + o] = l;
+    }
+}
+
+struct BeamTcArgs {
+    const float* X; long long n; long long ldx; int D;
+    const float* cw; const double* cw64; int M; int K; int L; int cap;
+    const double* sq;      // (M*K) einsum norms (exact)
+    const float* sq32;     // fp32 copy
+    const double* P;       // (M,M,K,K) cross tables (exact)
+    const float* Bg;       // pre-split codeword chunks [M][nch][hi,lo][256*32]
+    const double* cmax;    // per dictionary max ||c||
+    float* rbuf;           // residual scratch [grid][2][128][D]
+    void* codes_out; int code_bytes; long long ldcodes;
+    double* err_out;
+    unsigned long long* stats;
+    int nch;
+    int qv;                // exact-recheck queue capacity per vector
+    int tmax;              // kept approximate values per row (<= BT_TMAX)
+    int* bad;              // [n] set to 1 when a vector overflowed its queue (host re-encodes it)
+};
+
+__global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    constexpr int A_EL = BT_ROWS * BT_BK, B_EL = BT_N * BT_BK;
+    float* Abuf = reinterpret_cast<float*>(smem);        // [2][hi,lo][A_EL]
+    float* Bbuf = Abuf + 2 * 2 * A_EL;                    // [2][hi,lo][B_EL]
+    unsigned char* p = reinterpret_cast<unsigned char*>(Bbuf + 2 * 2 * B_EL);
+    const int V = BT_ROWS / a.cap;
+    const int M = a.M, K = a.K, D = a.D, cap = a.cap, L = a.L;
+    const int BT_QV = a.qv;
+    double* score = reinterpret_cast<double*>(p); p += sizeof(double) * 2 * BT_ROWS;     // [2][rows]
+    double* qval = reinterpret_cast<double*>(p); p += sizeof(double) * V * BT_QV;       // [V][QV]
+    double* vlim = reinterpret_cast<double*>(p); p += sizeof(double) * V;               // [V]
+    double* xnorm = reinterpret_cast<double*>(p); p += sizeof(double) * V;              // [V]
+    float* rmin = reinterpret_cast<float*>(p); p += sizeof(float) * a.tmax * BT_ROWS;  // smallest T per row
+    int* rarg = reinterpret_cast<int*>(p); p += sizeof(int) * BT_ROWS;                  // i1 per row
+    int* codes = reinterpret_cast<int*>(p); p += sizeof(int) * 2 * BT_ROWS * M;         // [2][rows][M]
+    int* qflat = reinterpret_cast<int*>(p); p += sizeof(int) * V * BT_QV;               // [V][QV]
+    int* qcnt = reinterpret_cast<int*>(p); p += sizeof(int) * V;                        // [V]
+    int* sel = reinterpret_cast<int*>(p); p += sizeof(int) * BT_ROWS;                   // selected flat per child slot
+    float* sq32s = reinterpret_cast<float*>(p); p += sizeof(float) * BT_N;
+    int* vbad = reinterpret_cast<int*>(p); p += sizeof(int) * V;                       // [V] overflow flags
+    float* erow = reinterpret_cast<float*>(p); p += sizeof(float) * BT_ROWS;           // per-row bound E_l
+    __shared__ uint64_t full_bar[2], empty_bar[2], acc_bar;
+    __shared__ uint32_t tmem_sh;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    float* rb = a.rbuf + (size_t)blockIdx.x * 2 * BT_ROWS * D;
+    const double u24 = 5.9604644775390625e-08, u22 = 2.384185791015625e-07;
+    const int N = (K + 7) & ~7;
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(BT_ROWS >> 4) << 24);
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(bt_smem_u32(&tmem_sh)),
+                     "r"(BT_N));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < 2; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&full_bar[i])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&empty_bar[i])));
+        }
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&acc_bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_sh;
+    const uint32_t taddr_row = tmem + ((uint32_t)(warp * 32) << 16);
+    double cmax_all = 0.0;
+    for (int j = 0; j < M; ++j) cmax_all = fmax(cmax_all, a.cmax[j]);
+
+    long long q = 0;        // k-chunk steps issued (pipeline phases, persist across groups)
+    uint32_t acc_phase = 0;
+    unsigned long long n_exact = 0;
+    const long long ngroups = (a.n + V - 1) / V;
+    for (long long grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const long long v0 = grp * V;
+    // initial residual = x (rows v*cap), scores 0, ||x||
+    for (int e = tid; e < V * D; e += BT_T) {
+        const int v = e / D, d = e % D;
+        const long long gv = v0 + v;
+        rb[(size_t)(v * cap) * D + d] = gv < a.n ? a.X[gv * a.ldx + d] : 0.f;
+    }
+    if (tid < V) {
+        const long long gv = v0 + tid;
+        double s = 0.0;
+        if (gv < a.n)
+            for (int d = 0; d < D; ++d) { const double t = a.X[gv * a.ldx + d]; s = __fma_rn(t, t, s); }
+        xnorm[tid] = sqrt(s) * (1.0 + 1e-12);
+    }
+    for (int r = tid; r < BT_ROWS; r += BT_T) score[r] = 0.0;
+    if (tid < V) vbad[tid] = 0;
+
+    __syncthreads();
+    int cur = 0, live = 1;
+    for (int m = 0; m < M; ++m) {
+        const long long tot_ll = (long long)live * K;
+        const int width = (int)std::min((long long)L, tot_ll);
+        for (int k = tid; k < BT_N; k += BT_T) sq32s[k] = k < K ? a.sq32[m * K + k] : __int_as_float(0x7f800000);
+        // ---- GEMM: rows (residuals) x codewords of dictionary m
+        const float* rcur = rb + (size_t)cur * BT_ROWS * D;
+        for (int ch = 0; ch < a.nch; ++ch, ++q) {
+            const int st = (int)(q & 1);
+            if (q >= 2) bt_wait(&empty_bar[st], (uint32_t)(((q >> 1) - 1) & 1));
+            float* Ah = Abuf + st * 2 * A_EL;
+            float* Al = Ah + A_EL;
+            float* Bs = Bbuf + st * 2 * B_EL;
+            if (tid == 0) {
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bt_smem_u32(&full_bar[st])),
+                             "r"((uint32_t)(2 * B_EL * sizeof(float)))
+                             : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                 bt_smem_u32(Bs)),
+                             "l"(a.Bg + ((size_t)m * a.nch + ch) * 2 * B_EL), "r"((uint32_t)(2 * B_EL * sizeof(float))),
+                             "r"(bt_smem_u32(&full_bar[st]))
+                             : "memory");
+            }
+            const int k0 = ch * BT_BK;
+            for (int e = tid; e < BT_ROWS * BT_BK; e += BT_T) {
+                const int r = e / BT_BK, kk = e % BT_BK;
+                const int v = r / cap, l = r % cap;
+                const int gk = k0 + kk;
+                float x = 0.f;
+                if (v < V && l < live && gk < D) x = rcur[(size_t)r * D + gk];
+                const float h = bt_tf32(x), lo = bt_tf32(x - h);
+                const uint32_t o = bt_off(r, kk) >> 2;
+                Ah[o] = h;
+                Al[o] = lo;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (tid == 0) {
+                bt_wait(&full_bar[st], (uint32_t)((q >> 1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t ah = bt_smem_u32(Ah), al = bt_smem_u32(Al), bh = bt_smem_u32(Bs), bl = bt_smem_u32(Bs + B_EL);
+                const int ks = std::min(BT_BK / 8, (D - k0 + 7) / 8);
+                for (int s2 = 0; s2 < ks; ++s2) {
+                    const uint32_t off = (uint32_t)s2 * 256;
+                    const uint32_t acc0 = (ch > 0 || s2 > 0) ? 1u : 0u;
+                    bt_mma(tmem, bt_desc(ah + off), bt_desc(bh + off), idesc, acc0);
+                    bt_mma(tmem, bt_desc(ah + off), bt_desc(bl + off), idesc, 1u);
+                    bt_mma(tmem, bt_desc(al + off), bt_desc(bh + off), idesc, 1u);
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 bt_smem_u32(&empty_bar[st]))
+                             : "memory");
+                if (ch == a.nch - 1)
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                     bt_smem_u32(&acc_bar))
+                                 : "memory");
+            }
+        }
+        bt_wait(&acc_bar, acc_phase);
+        acc_phase ^= 1;
+        asm volatile("tcgen05.fence::after_thread_sync;");
+
+        // ---- per row: approximate scores v' = s + sq - 2 r.c, two smallest + argmin
+        const int r = tid;
+        const int rv = r / cap, rl = r % cap;
+        const bool row_live = rv < V && rl < live && (v0 + rv) < a.n && !vbad[rv];
+        const float s32 = row_live ? (float)score[cur * BT_ROWS + r] : 0.f;
+        // keep the T smallest approximate scores of the row (live*T >= width)
+        // each row keeps its T smallest approximate scores (T = width when it fits):
+        // the union of the rows' top-width lists holds the vector's width smallest
+        const int T = std::min(a.tmax, std::max(2, width));
+        float top[BT_TMAX];
+#pragma unroll
+        for (int i = 0; i < BT_TMAX; ++i) top[i] = __int_as_float(0x7f800000);
+        int i1 = -1;
+        float v[32];
+        for (int c0 = 0; c0 < N; c0 += 32) {
+            bt_ld32(taddr_row + c0, v);
+            if (row_live) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const float w = s32 + fmaf(-2.f, v[i], sq32s[c0 + i]);
+                    if (w < top[T - 1]) {
+                        if (w < top[0]) i1 = rl * K + c0 + i;
+                        // insertion into the sorted prefix of length T
+                        float x = w;
+#pragma unroll
+                        for (int t2 = 0; t2 < BT_TMAX; ++t2) {
+                            if (t2 < T && x < top[t2]) { const float y = top[t2]; top[t2] = x; x = y; }
+                        }
+                    }
+                }
+            }
+        }
+        const float m1 = top[0], m2 = top[1];
+        // rigorous |v' - v| for this row: ||r_l|| from the exact score
+        // (s_l = ||r_l||^2 - ||x||^2), 3xTF32 representation (3*2^-22) plus one
+        // fp32-accumulator rounding per MMA step (3 per 8 of D) on sum|r_d c_d| <=
+        // ||r|| ||c||, fp32 rounding of the residual (m steps) and of the score
+        // arithmetic (sq, fma, add), doubled for safety
+        if (row_live) {
+            const int vv = rv;
+            const double xx = xnorm[vv] * xnorm[vv];
+            const double sl = score[cur * BT_ROWS + r];
+            const double rn = sqrt(fmax(sl + xx, 0.0) * (1.0 + 1e-9)) + 1e-30;
+            const double cm = a.cmax[m];
+            const double dlt = (m + 1) * u24 * (xnorm[vv] + m * cmax_all);
+            const double steps = 3.0 * ((D + 7) / 8) + 7.0;
+            const double e_dot = (steps * u22 * (rn + dlt) + dlt) * cm;
+            const double E = 2.0 * (2.0 * e_dot + 4.0 * u24 * (fabs(sl) + cm * cm + 2.0 * (rn + dlt) * cm)) + 1e-30;
+            erow[r] = (float)(E * (1.0 + 1e-6));
+        } else {
+            erow[r] = 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < BT_TMAX; ++i)
+            if (i < a.tmax) rmin[i * BT_ROWS + r] = top[i];
+        rarg[r] = i1;
+        if (tid < V) qcnt[tid] = 0;
+        __syncthreads();
+        // ---- per vector: threshold = width-th smallest of the 2*live row minima; bound E
+        if (tid < V && v0 + tid < a.n && !vbad[tid]) {
+            const int vv = tid;
+            float thr;
+            const int T = std::min(a.tmax, std::max(2, width));
+            if (width >= tot_ll || (long long)live * T < width) {
+                thr = __int_as_float(0x7f800000);
+            } else {
+                // width-th smallest of the rows' sorted top-T lists: multiway merge
+                int ptr[BT_ROWS];
+                for (int l = 0; l < live; ++l) ptr[l] = 0;
+                thr = __int_as_float(0x7f800000);
+                for (int step = 0; step < width; ++step) {
+                    float best = __int_as_float(0x7f800000);
+                    int bl = -1;
+                    for (int l = 0; l < live; ++l) {
+                        if (ptr[l] < T) {
+                            const float x = rmin[ptr[l] * BT_ROWS + vv * cap + l];
+                            if (bl < 0 || x < best) { best = x; bl = l; }
+                        }
+                    }
+                    if (bl < 0) break;
+                    ptr[bl]++;
+                    thr = best;
+                }
+            }
+            float emax = 0.f;
+            for (int l = 0; l < live; ++l) emax = fmaxf(emax, erow[vv * cap + l]);
+            // row l keeps candidates with v' <= tau' + E_max + E_l (E_l added per row)
+            vlim[vv] = (double)thr + (double)emax;
+        }
+        __syncthreads();
+        // ---- candidates: rows whose second minimum is above the limit offer their
+        // minimum; the others rescan their row from TMEM
+        {
+            const double lim = row_live ? vlim[rv] + (double)erow[r] : -1.0;
+            const float limf = (lim >= 3.0e38) ? __int_as_float(0x7f800000)
+                                               : __fadd_ru((float)lim, fabsf((float)lim) * 1e-6f);
+            const bool multi = row_live && m2 <= limf;
+            if (row_live && m1 <= limf && !multi) {
+                const int slot = atomicAdd(&qcnt[rv], 1);
+                if (slot < BT_QV) qflat[rv * BT_QV + slot] = i1;
+            }
+            // the TMEM rescan is warp-collective: every lane runs it when any lane needs it
+            const bool any_multi = __any_sync(0xffffffffu, multi);
+            if (any_multi) {
+                for (int c0 = 0; c0 < N; c0 += 32) {
+                    bt_ld32(taddr_row + c0, v);
+                    if (multi) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            const float w = s32 + fmaf(-2.f, v[i], sq32s[c0 + i]);
+                            if (c0 + i < K && w <= limf) {
+                                const int slot = atomicAdd(&qcnt[rv], 1);
+                                if (slot < BT_QV) qflat[rv * BT_QV + slot] = rl * K + c0 + i;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        if (tid < V && qcnt[tid] > BT_QV && !vbad[tid]) {
+            vbad[tid] = 1;  // too many near-boundary candidates: the host re-encodes this vector
+            if (v0 + tid < a.n) a.bad[v0 + tid] = 1;
+        }
+        __syncthreads();
+        // ---- exact float64 values of every queued candidate (round robin over threads)
+        {
+            const int* pcodes = codes + cur * BT_ROWS * M;
+            int total_q = 0;
+            for (int vv = 0; vv < V; ++vv) total_q += std::min(qcnt[vv], BT_QV);
+            // flatten (vector, slot) pairs
+            for (int idx = tid; idx < V * BT_QV; idx += BT_T) {
+                const int vv = idx / BT_QV, slot = idx % BT_QV;
+                if (v0 + vv >= a.n || vbad[vv] || slot >= qcnt[vv]) continue;
+                const int flat = qflat[idx];
+                const int l = flat / K, k = flat % K;
+                const long long gv = v0 + vv;
+                // x in float64 read straight from the f32 input
+                const float* xr = a.X + gv * a.ldx;
+                const double* crow = a.cw64 + ((long long)m * K + k) * D;
+                double tot = 0.0;
+                bool first = true;
+                int d = 0;
+                while (d < D) {
+                    const int e = d + (int)blas_block_len(D - d);
+                    double acc = 0.0;
+                    for (; d + 8 <= e; d += 8) {
+                        double xv[8], cv[8];
+#pragma unroll
+                        for (int u2 = 0; u2 < 8; ++u2) { xv[u2] = (double)xr[d + u2]; cv[u2] = crow[d + u2]; }
+#pragma unroll
+                        for (int u2 = 0; u2 < 8; ++u2) acc = __fma_rn(xv[u2], cv[u2], acc);
+                    }
+                    for (; d < e; ++d) acc = __fma_rn((double)xr[d], crow[d], acc);
+                    tot = first ? acc : dadd(tot, acc);
+                    first = false;
+                }
+                const double t = dsub(a.sq[m * K + k], dmul(2.0, tot));
+                double cross = 0.0;
+                const int* pcv = pcodes + (vv * cap + l) * M;
+                for (int j = 0; j < m; ++j) cross = dadd(cross, a.P[(((long long)j * M + m) * K + pcv[j]) * K + k]);
+                qval[idx] = dadd(dadd(score[cur * BT_ROWS + vv * cap + l], t), dmul(2.0, cross));
+            }
+            n_exact += (tid == 0) ? (unsigned long long)total_q : 0ULL;
+        }
+        __syncthreads();
+        // ---- exact top-width per vector by (value, flat) rank, then child slots in flat order
+        for (int idx = tid; idx < V * BT_QV; idx += BT_T) {
+            const int vv = idx / BT_QV, slot = idx % BT_QV;
+            const int nq = qcnt[vv];
+            if (v0 + vv >= a.n || vbad[vv] || slot >= nq) continue;
+            const double x = qval[idx];
+            const int f = qflat[idx];
+            int rank = 0;
+            for (int j = 0; j < nq; ++j) rank += lex_less(qval[vv * BT_QV + j], qflat[vv * BT_QV + j], x, f);
+            if (rank < width) {
+                // position among the selected by flat index = rank of f among selected flats;
+                // computed in the next pass, store by value-rank first
+                sel[vv * cap + rank] = idx;
+            }
+        }
+        __syncthreads();
+        {
+            // child slot for each selected (thread per child row): order by flat
+            const int rr = tid;
+            const int vv = rr / cap, slotv = rr % cap;
+            const int nxt = cur ^ 1;
+            if (vv < V && slotv < width && v0 + vv < a.n && !vbad[vv]) {
+                const int idx = sel[vv * cap + slotv];
+                const int f = qflat[idx];
+                int pos = 0;
+                for (int j = 0; j < width; ++j) pos += qflat[sel[vv * cap + j]] < f;
+                const int parent = f / K, kk = f % K;
+                int* cc = codes + (nxt * BT_ROWS + vv * cap + pos) * M;
+                const int* pp = codes + (cur * BT_ROWS + vv * cap + parent) * M;
+                for (int j = 0; j < m; ++j) cc[j] = pp[j];
+                cc[m] = kk;
+                score[nxt * BT_ROWS + vv * cap + pos] = qval[idx];
+                rarg[vv * cap + pos] = (parent << 16) | kk;  // reuse: (parent, k) of child row
+            }
+        }
+        __syncthreads();
+        // ---- child residuals r = r_parent - c_m(k) (fp32; the bound covers the rounding)
+        if (m + 1 < M) {
+            const int nxt = cur ^ 1;
+            float* rn = rb + (size_t)nxt * BT_ROWS * D;
+            const float* rc = rb + (size_t)cur * BT_ROWS * D;
+            for (int e = tid; e < BT_ROWS * D; e += BT_T) {
+                const int rr = e / D, d = e % D;
+                const int vv = rr / cap, slotv = rr % cap;
+                if (vv >= V || slotv >= width || v0 + vv >= a.n || vbad[vv]) continue;
+                const int pk = rarg[rr];
+                const int parent = pk >> 16, kk = pk & 0xFFFF;
+                rn[e] = rc[(size_t)(vv * cap + parent) * D + d] - a.cw[((long long)m * K + kk) * D + d];
+            }
+        }
+        __syncthreads();
+        cur ^= 1;
+        live = width;
+    }
+
+    // ---- overflowed vectors are left to the host fallback (flag via stats=-1 code)
+    // final pick: first minimum among the beams in code order
+    if (tid < V && v0 + tid < a.n && !vbad[tid]) {
+        const int vv = tid;
+        const long long gv = v0 + vv;
+        double bv = __longlong_as_double(0x7ff0000000000000ULL);
+        int bi = 0;
+        for (int l = 0; l < live; ++l) {
+            const double s = score[cur * BT_ROWS + vv * cap + l];
+            if (s < bv) { bv = s; bi = l; }
+        }
+        const int* best = codes + (cur * BT_ROWS + vv * cap + bi) * M;
+        for (int j = 0; j < M; ++j) {
+            const int c = best[j];
+            if (a.code_bytes == 1) ((uint8_t*)a.codes_out)[gv * a.ldcodes + j] = (uint8_t)c;
+            else if (a.code_bytes == 2) ((uint16_t*)a.codes_out)[gv * a.ldcodes + j] = (uint16_t)c;
+            else ((int32_t*)a.codes_out)[gv * a.ldcodes + j] = c;
+        }
+        if (a.err_out) {
+            const float* xr = a.X + gv * a.ldx;
+            a.err_out[gv] = np_pw_sum(
+                [&](long long d) {
+                    double rr = 0.0;
+                    for (int j = 0; j < M; ++j) rr = dadd(rr, (double)a.cw[((long long)j * K + best[j]) * D + d]);
+                    const double df = dsub((double)xr[d], rr);
+                    return dmul(df, df);
+                },
+                0, D);
+        }
+    }
+    __syncthreads();
+    }  // groups
+    if (a.stats && tid == 0) atomicAdd(a.stats, n_exact);
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BT_N));
+    }
+}
+
+
+// codebook side inputs: fp64 copy, fp32 norms, per-dictionary max norm
+__global__ void tc_side_prep_kernel(const float* __restrict__ cw, const double* __restrict__ sq, int M, int K, int D,
+                                    double* __restrict__ cw64, float* __restrict__ sq32, double* __restrict__ cmax) {
+    const long long total = (long long)M * K * D;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x)
+        cw64[e] = (double)cw[e];
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)M * K;
+         e += (long long)gridDim.x * blockDim.x)
+        sq32[e] = (float)sq[e];
+    if (blockIdx.x == 0) {
+        __shared__ double red[256];
+        for (int m = 0; m < M; ++m) {
+            double c = 0.0;
+            for (int k = threadIdx.x; k < K; k += blockDim.x) c = fmax(c, sqrt(sq[m * K + k]));
+            red[threadIdx.x] = c;
+            __syncthreads();
+            for (int s2 = blockDim.x / 2; s2 > 0; s2 >>= 1) {
+                if (threadIdx.x < s2) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s2]);
+                __syncthreads();
+            }
+            if (threadIdx.x == 0) cmax[m] = red[0] * (1.0 + 1e-12);
+            __syncthreads();
+        }
+    }
+}
+
+__global__ void gather_f32_rows_kernel(const float* __restrict__ X, long long ldx, int D, const int* __restrict__ idx,
+                                       int cnt, float* __restrict__ out) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)cnt * D;
+         e += (long long)gridDim.x * blockDim.x)
+        out[e] = X[(long long)idx[e / D] * ldx + e % D];
+}
+
+__global__ void scatter_codes_kernel(const void* __restrict__ src, int code_bytes, int M, const int* __restrict__ idx,
+                                     int cnt, const double* __restrict__ esrc, void* __restrict__ dst, long long ldc,
+                                     double* __restrict__ edst) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cnt) return;
+    const long long r = idx[i];
+    for (int j = 0; j < M; ++j) {
+        if (code_bytes == 1) ((uint8_t*)dst)[r * ldc + j] = ((const uint8_t*)src)[(long long)i * M + j];
+        else if (code_bytes == 2) ((uint16_t*)dst)[r * ldc + j] = ((const uint16_t*)src)[(long long)i * M + j];
+        else ((int32_t*)dst)[r * ldc + j] = ((const int32_t*)src)[(long long)i * M + j];
+    }
+    if (edst) edst[r] = esrc[i];
+}
+
+__global__ void list_bad_kernel(const int* __restrict__ bad, long long n, int* __restrict__ idx, int* __restrict__ cnt) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        if (bad[i]) idx[atomicAdd(cnt, 1)] = (int)i;
+}
+
+// Returns 1 (without launching) when the shape is outside the tensor-core encoder.
+int launch_encode_tc(const float* X, long long n, long long ldx, int D, const float* cw, int M, int K, int L,
+                     const double* sq, const double* P, void* codes_out, int code_bytes, long long ldcodes,
+                     double* err_out, unsigned long long* stats, cudaStream_t s) {
+    if (K > BT_N || K < 1) return 1;
+    long long capll = 1;
+    for (int m = 0; m < M && capll < L; ++m) capll *= K;
+    const int cap = (int)std::min((long long)L, capll);
+    if (cap > BT_ROWS || n <= 0) return n <= 0 ? 0 : 1;
+    const int V = BT_ROWS / cap;
+    const int nch = (D + BT_BK - 1) / BT_BK;
+    const int qv = 3 * cap + 8;
+    const int tmax = std::min(BT_TMAX, std::max(2, (int)std::min((long long)L, (long long)K)));
+    size_t smem = sizeof(float) * (2 * 2 * BT_ROWS * BT_BK + 2 * 2 * BT_N * BT_BK);
+    smem += sizeof(double) * (2 * BT_ROWS + (size_t)V * qv + 2 * V);
+    smem += sizeof(float) * (size_t)tmax * BT_ROWS + sizeof(int) * BT_ROWS + sizeof(int) * 2 * BT_ROWS * (size_t)M;
+    smem += sizeof(int) * ((size_t)V * qv + V + BT_ROWS) + sizeof(float) * BT_N + sizeof(int) * V +
+            sizeof(float) * BT_ROWS;
+    if (smem > 227 * 1024) return 1;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long ngroups = (n + V - 1) / V;
+    const int grid = (int)std::min<long long>(ngroups, sms);
+    // scratch
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
+    const size_t o_bg = take(sizeof(float) * (size_t)M * nch * 2 * BT_N * BT_BK);
+    const size_t o_c64 = take(sizeof(double) * (size_t)M * K * D);
+    const size_t o_sq32 = take(sizeof(float) * (size_t)M * K);
+    const size_t o_cmax = take(sizeof(double) * M);
+    const size_t o_rb = take(sizeof(float) * (size_t)grid * 2 * BT_ROWS * D);
+    const size_t o_bad = take(sizeof(int) * (size_t)n);
+    const size_t o_lst = take(sizeof(int) * (size_t)n);
+    const size_t o_cnt = take(sizeof(int) * 4);
+    char* base = (char*)scratch(10, off, s);
+    if (!base) return fail_cuda(cudaErrorMemoryAllocation, "encode_tc scratch");
+    float* Bg = (float*)(base + o_bg);
+    double* cw64 = (double*)(base + o_c64);
+    float* sq32 = (float*)(base + o_sq32);
+    double* cmax = (double*)(base + o_cmax);
+    int* bad = (int*)(base + o_bad);
+    int* cnt = (int*)(base + o_cnt);
+    {
+        ProfScope ps0("encode_tc_prep", s);
+        cb_tf32_prep_kernel<<<grid_for((long long)M * nch * BT_N * BT_BK, 256, 4096), 256, 0, s>>>(cw, M, K, D, nch, Bg);
+        DA_CHECK_LAUNCH("cb_tf32_prep_kernel");
+        tc_side_prep_kernel<<<grid_for((long long)M * K * D, 256, 2048), 256, 0, s>>>(cw, sq, M, K, D, cw64, sq32, cmax);
+        DA_CHECK_LAUNCH("tc_side_prep_kernel");
+        DA_CUDA(cudaMemsetAsync(bad, 0, sizeof(int) * (size_t)n + 16, s));
+    }
+    BeamTcArgs a{};
+    a.X = X; a.n = n; a.ldx = ldx; a.D = D; a.cw = cw; a.cw64 = cw64; a.M = M; a.K = K; a.L = L; a.cap = cap;
+    a.sq = sq; a.sq32 = sq32; a.P = P; a.Bg = Bg; a.cmax = cmax; a.rbuf = (float*)(base + o_rb);
+    a.codes_out = codes_out; a.code_bytes = code_bytes; a.ldcodes = ldcodes; a.err_out = err_out; a.stats = stats;
+    a.nch = nch; a.qv = qv; a.tmax = tmax; a.bad = bad;
+    {
+        ProfScope ps1("encode_beam_tc", s);
+        DA_CUDA(cudaFuncSetAttribute(beam_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        beam_tc_kernel<<<grid, BT_T, smem, s>>>(a);
+        DA_CHECK_LAUNCH("beam_tc_kernel");
+    }
+    // vectors that overflowed their recheck queue (many near-ties) are re-encoded exactly
+    int* lst = (int*)(base + o_lst);
+    DA_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int), s));
+    list_bad_kernel<<<grid_for(n, 256, 4096), 256, 0, s>>>(bad, n, lst, cnt);
+    DA_CHECK_LAUNCH("list_bad_kernel");
+    int h_cnt = 0;
+    DA_CUDA(cudaMemcpyAsync(&h_cnt, cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
+    DA_CUDA(cudaStreamSynchronize(s));
+    if (getenv("DA_DEBUG")) fprintf(stderr, "[da] encode_tc: n=%lld V=%d cap=%d overflowed=%d\n", n, V, cap, h_cnt);
+    if (h_cnt > 0) {
+        float* xg = nullptr;
+        void* cg = nullptr;
+        double* eg = nullptr;
+        int* lcopy = nullptr;
+        DA_CUDA(cudaMallocAsync((void**)&xg, sizeof(float) * (size_t)h_cnt * D, s));
+        DA_CUDA(cudaMallocAsync(&cg, (size_t)code_bytes * h_cnt * M, s));
+        DA_CUDA(cudaMallocAsync((void**)&eg, sizeof(double) * (size_t)h_cnt, s));
+        DA_CUDA(cudaMallocAsync((void**)&lcopy, sizeof(int) * (size_t)h_cnt, s));
+        DA_CUDA(cudaMemcpyAsync(lcopy, lst, sizeof(int) * (size_t)h_cnt, cudaMemcpyDeviceToDevice, s));
+        gather_f32_rows_kernel<<<grid_for((long long)h_cnt * D, 256, 4096), 256, 0, s>>>(X, ldx, D, lcopy, h_cnt, xg);
+        DA_CHECK_LAUNCH("gather_f32_rows_kernel");
+        int rc = launch_encode_fast(xg, 1, h_cnt, D, D, cw, M, K, L, sq, P, cg, code_bytes, M, eg, stats, s);
+        if (rc > 0) rc = launch_encode(xg, 1, h_cnt, D, D, cw, M, K, L, sq, P, cg, code_bytes, M, eg, s);
+        if (rc) return rc;
+        scatter_codes_kernel<<<grid_for(h_cnt, 128), 128, 0, s>>>(cg, code_bytes, M, lcopy, h_cnt, eg, codes_out, ldcodes,
+                                                                  err_out);
+        DA_CHECK_LAUNCH("scatter_codes_kernel");
+        cudaFreeAsync(xg, s);
+        cudaFreeAsync(cg, s);
+        cudaFreeAsync(eg, s);
+        cudaFreeAsync(lcopy, s);
+    }
+    return 0;
+}
+
+}  // namespace da

@@ -15,17 +15,22 @@ pytestmark = pytest.mark.gpu
 
 
 def both(book, X, L):
+    """(tensor-core filter, plain float64, rechecked count); also checks the fp32
+    gather filter against the plain encoder."""
     cross = cb.cross_products(book)
     cw, sq = cb._codebook_dev(book)
     Pt, _ = cross.device()
     Xd = E.to_dev(X)
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
     E.encode_config(0, cnt)
-    fast = E.encode(Xd, cw, sq, Pt, L)
+    tc = E.encode(Xd, cw, sq, Pt, L)
+    E.encode_config(2)
+    gather = E.encode(Xd, cw, sq, Pt, L)
     E.encode_config(1)
     plain = E.encode(Xd, cw, sq, Pt, L)
     E.encode_config(0)
-    return fast, plain, int(cnt.item())
+    assert_same(gather, plain)
+    return tc, plain, int(cnt.item())
 
 
 def assert_same(fast, plain):
