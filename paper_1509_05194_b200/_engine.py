@@ -413,9 +413,9 @@ def assign_config(mode: int, counter: torch.Tensor | None = None) -> None:
 
 
 def encode_config(mode: int, counter: torch.Tensor | None = None) -> None:
-    """0 = tcgen05 residual-GEMM filter with exact float64 recheck (default; falls
-    back to 2 then 1 outside its shapes), 1 = plain float64 tables, 2 = fp32
-    score-table + cross-gather filter.  `counter` accumulates exact rechecks."""
+    """0 = default (currently 2), 1 = plain float64 tables, 2 = fp32 score-table +
+    cross-gather filter, 3 = tcgen05 residual-GEMM filter; every mode returns the
+    same codes and errors.  `counter` accumulates exact rechecks."""
     native.da_encode_config(int(mode), P(counter))
 
 

@@ -22,7 +22,7 @@ def both(book, X, L):
     Pt, _ = cross.device()
     Xd = E.to_dev(X)
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
-    E.encode_config(0, cnt)
+    E.encode_config(3, cnt)
     tc = E.encode(Xd, cw, sq, Pt, L)
     E.encode_config(2)
     gather = E.encode(Xd, cw, sq, Pt, L)
