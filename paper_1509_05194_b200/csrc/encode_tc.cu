@@ -250,16 +250,35 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
                              : "memory");
             }
             const int k0 = ch * BT_BK;
-            for (int e = tid; e < BT_ROWS * BT_BK; e += BT_T) {
-                const int r = e / BT_BK, kk = e % BT_BK;
+            {
+                // one thread per row: 8 x (4 consecutive k) -> one 16-B core-matrix row each
+                const int r = tid;
                 const int v = r / cap, l = r % cap;
-                const int gk = k0 + kk;
-                float x = 0.f;
-                if (v < V && l < live && gk < D) x = rcur[(size_t)r * D + gk];
-                const float h = bt_tf32(x), lo = bt_tf32(x - h);
-                const uint32_t o = bt_off(r, kk) >> 2;
-                Ah[o] = h;
-                Al[o] = lo;
+                const bool rl_ok = v < V && l < live && (v0 + v) < a.n;
+                const bool vec4 = (D & 3) == 0;
+                const float* src = rcur + (size_t)r * D;
+#pragma unroll
+                for (int c4 = 0; c4 < BT_BK / 4; ++c4) {
+                    const int gk = k0 + 4 * c4;
+                    float x4[4] = {0.f, 0.f, 0.f, 0.f};
+                    if (rl_ok) {
+                        if (vec4 && gk + 3 < D) {
+                            const float4 t = *reinterpret_cast<const float4*>(src + gk);
+                            x4[0] = t.x; x4[1] = t.y; x4[2] = t.z; x4[3] = t.w;
+                        } else {
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) x4[u] = gk + u < D ? src[gk + u] : 0.f;
+                        }
+                    }
+                    float4 h, lo;
+                    h.x = bt_tf32(x4[0]); lo.x = bt_tf32(x4[0] - h.x);
+                    h.y = bt_tf32(x4[1]); lo.y = bt_tf32(x4[1] - h.y);
+                    h.z = bt_tf32(x4[2]); lo.z = bt_tf32(x4[2] - h.z);
+                    h.w = bt_tf32(x4[3]); lo.w = bt_tf32(x4[3] - h.w);
+                    const uint32_t o = bt_off(r, 4 * c4) >> 2;
+                    *reinterpret_cast<float4*>(Ah + o) = h;
+                    *reinterpret_cast<float4*>(Al + o) = lo;
+                }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();
@@ -294,13 +313,17 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
         const bool row_live = rv < V && rl < live && (v0 + rv) < a.n && !vbad[rv];
         const float s32 = row_live ? (float)score[cur * BT_ROWS + r] : 0.f;
         // keep the T smallest approximate scores of the row (live*T >= width)
-        // each row keeps its T smallest approximate scores (T = width when it fits):
-        // the union of the rows' top-width lists holds the vector's width smallest
+        // each row keeps its T smallest approximate scores (replace-the-max list,
+        // sorted at the end); the union of the rows' lists bounds the width-th
+        // smallest of the vector from above
         const int T = std::min(a.tmax, std::max(2, width));
         float top[BT_TMAX];
 #pragma unroll
         for (int i = 0; i < BT_TMAX; ++i) top[i] = __int_as_float(0x7f800000);
+        float tmaxv = __int_as_float(0x7f800000);
+        int tslot = 0;
         int i1 = -1;
+        float best1 = __int_as_float(0x7f800000);
         float v[32];
         for (int c0 = 0; c0 < N; c0 += 32) {
             bt_ld32(taddr_row + c0, v);
@@ -308,16 +331,23 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
                     const float w = s32 + fmaf(-2.f, v[i], sq32s[c0 + i]);
-                    if (w < top[T - 1]) {
-                        if (w < top[0]) i1 = rl * K + c0 + i;
-                        // insertion into the sorted prefix of length T
-                        float x = w;
+                    if (w < tmaxv) {
+                        if (w < best1) { best1 = w; i1 = rl * K + c0 + i; }
+                        top[tslot] = w;
+                        tmaxv = -__int_as_float(0x7f800000);
 #pragma unroll
-                        for (int t2 = 0; t2 < BT_TMAX; ++t2) {
-                            if (t2 < T && x < top[t2]) { const float y = top[t2]; top[t2] = x; x = y; }
-                        }
+                        for (int t2 = 0; t2 < BT_TMAX; ++t2)
+                            if (t2 < T && top[t2] > tmaxv) { tmaxv = top[t2]; tslot = t2; }
                     }
                 }
+            }
+        }
+        // sort the kept values ascending (T <= 16, insertion sort in registers)
+#pragma unroll
+        for (int i = 1; i < BT_TMAX; ++i) {
+#pragma unroll
+            for (int j = BT_TMAX - 1; j >= 1; --j) {
+                if (j <= i && top[j] < top[j - 1]) { const float t3 = top[j]; top[j] = top[j - 1]; top[j - 1] = t3; }
             }
         }
         const float m1 = top[0], m2 = top[1];
@@ -355,7 +385,7 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
                 thr = __int_as_float(0x7f800000);
             } else {
                 // width-th smallest of the rows' sorted top-T lists: multiway merge
-                int ptr[BT_ROWS];
+                int* ptr = sel + vv * cap;  // reuse the per-vector child slots as merge cursors
                 for (int l = 0; l < live; ++l) ptr[l] = 0;
                 thr = __int_as_float(0x7f800000);
                 for (int step = 0; step < width; ++step) {
@@ -494,15 +524,23 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
         // ---- child residuals r = r_parent - c_m(k) (fp32; the bound covers the rounding)
         if (m + 1 < M) {
             const int nxt = cur ^ 1;
-            float* rn = rb + (size_t)nxt * BT_ROWS * D;
-            const float* rc = rb + (size_t)cur * BT_ROWS * D;
-            for (int e = tid; e < BT_ROWS * D; e += BT_T) {
-                const int rr = e / D, d = e % D;
-                const int vv = rr / cap, slotv = rr % cap;
-                if (vv >= V || slotv >= width || v0 + vv >= a.n || vbad[vv]) continue;
+            const int rr = tid;
+            const int vv = rr / cap, slotv = rr % cap;
+            if (vv < V && slotv < width && v0 + vv < a.n && !vbad[vv]) {
                 const int pk = rarg[rr];
                 const int parent = pk >> 16, kk = pk & 0xFFFF;
-                rn[e] = rc[(size_t)(vv * cap + parent) * D + d] - a.cw[((long long)m * K + kk) * D + d];
+                float* dst = rb + ((size_t)nxt * BT_ROWS + rr) * D;
+                const float* par = rb + ((size_t)cur * BT_ROWS + vv * cap + parent) * D;
+                const float* cwr = a.cw + ((long long)m * K + kk) * D;
+                if ((D & 3) == 0) {
+                    for (int d = 0; d < D; d += 4) {
+                        const float4 p4 = *reinterpret_cast<const float4*>(par + d);
+                        const float4 c4 = __ldg(reinterpret_cast<const float4*>(cwr + d));
+                        *reinterpret_cast<float4*>(dst + d) = make_float4(p4.x - c4.x, p4.y - c4.y, p4.z - c4.z, p4.w - c4.w);
+                    }
+                } else {
+                    for (int d = 0; d < D; ++d) dst[d] = par[d] - cwr[d];
+                }
             }
         }
         __syncthreads();
@@ -616,7 +654,7 @@ int launch_encode_tc(const float* X, long long n, long long ldx, int D, const fl
     const int V = BT_ROWS / cap;
     const int nch = (D + BT_BK - 1) / BT_BK;
     const int qv = 3 * cap + 8;
-    const int tmax = std::min(BT_TMAX, std::max(2, (int)std::min((long long)L, (long long)K)));
+    const int tmax = std::min(8, std::max(2, (int)std::min((long long)L, (long long)K)));
     size_t smem = sizeof(float) * (2 * 2 * BT_ROWS * BT_BK + 2 * 2 * BT_N * BT_BK);
     smem += sizeof(double) * (2 * BT_ROWS + (size_t)V * qv + 2 * V);
     smem += sizeof(float) * (size_t)tmax * BT_ROWS + sizeof(int) * BT_ROWS + sizeof(int) * 2 * BT_ROWS * (size_t)M;
