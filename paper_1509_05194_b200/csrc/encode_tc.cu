@@ -32,9 +32,10 @@ namespace da {
 namespace {
 constexpr int BT_ROWS = 128;
 constexpr int BT_N = 256;
-constexpr int BT_BK = 32;
+constexpr int BT_BK = 8;
+constexpr int BT_NST = 3;  // shared-memory ring depth (k-chunks in flight)
 constexpr int BT_T = 128;
-constexpr int BT_TMAX = 16;  // smallest approximate values kept per row
+constexpr int BT_S = 16;  // column slices per row for the beam threshold
 }  // namespace
 
 __device__ __forceinline__ uint32_t bt_smem_u32(const void* p) {
@@ -132,6 +133,82 @@ __global__ void cb_tf32_prep_kernel(const float* __restrict__ cw, int M, int K, 
     }
 }
 
+// x -> tf32 hi (at o) and lo = tf32(x - hi) (at o + A_EL), one 16-B core-matrix row each
+__device__ __forceinline__ void bt_store_split(float* chunk, uint32_t o, const float* x4) {
+    float4 h, lo;
+    h.x = bt_tf32(x4[0]); lo.x = bt_tf32(x4[0] - h.x);
+    h.y = bt_tf32(x4[1]); lo.y = bt_tf32(x4[1] - h.y);
+    h.z = bt_tf32(x4[2]); lo.z = bt_tf32(x4[2] - h.z);
+    h.w = bt_tf32(x4[3]); lo.w = bt_tf32(x4[3] - h.w);
+    *reinterpret_cast<float4*>(chunk + o) = h;
+    *reinterpret_cast<float4*>(chunk + BT_ROWS * BT_BK + o) = lo;
+}
+
+__device__ __forceinline__ void bt_bulk(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     bt_smem_u32(dst_smem)),
+                 "l"(src), "r"(bytes), "r"(bt_smem_u32(bar))
+                 : "memory");
+}
+
+// float -> unsigned key with the same order (for redux.sync.min)
+__device__ __forceinline__ unsigned bt_key(float f) {
+    const unsigned b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float bt_unkey(unsigned k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+// One row's approximate scores v' = s + sq - 2 r.c from TMEM, branch-free:
+// the minimum of each of BT_S column slices (slice = column mod BT_S) sorted
+// ascending into out[i * BT_ROWS], the two smallest values m1 <= m2 and the flat
+// index i1 of the first minimum.  Every slice minimum is a distinct candidate,
+// so the width-th smallest over a vector's slice minima bounds its width-th
+// smallest candidate from above.  TMEM loads are warp-collective.
+__device__ __forceinline__ void bt_row_slices(uint32_t taddr_row, int N, int K, bool row_live, float s32,
+                                              const float* __restrict__ sq32s, int rl, float* __restrict__ out,
+                                              float& m1, float& m2, int& i1) {
+    const float INF = __int_as_float(0x7f800000);
+    float sm[BT_S];
+#pragma unroll
+    for (int i = 0; i < BT_S; ++i) sm[i] = INF;
+    m1 = INF;
+    m2 = INF;
+    i1 = -1;
+    float v[32];
+    for (int c0 = 0; c0 < N; c0 += 32) {
+        bt_ld32(taddr_row + c0, v);
+        if (row_live) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const float w = s32 + fmaf(-2.f, v[i], sq32s[c0 + i]);
+                sm[i % BT_S] = fminf(sm[i % BT_S], w);
+                m2 = fminf(m2, fmaxf(m1, w));
+                if (w < m1) i1 = rl * K + c0 + i;
+                m1 = fminf(m1, w);
+            }
+        }
+    }
+    // bitonic sorting network (ascending)
+#pragma unroll
+    for (int k = 2; k <= BT_S; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+            for (int i = 0; i < BT_S; ++i) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const float lo = fminf(sm[i], sm[l]), hi = fmaxf(sm[i], sm[l]);
+                    if ((i & k) == 0) { sm[i] = lo; sm[l] = hi; } else { sm[i] = hi; sm[l] = lo; }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < BT_S; ++i) out[i * BT_ROWS] = sm[i];
+}
+
 struct BeamTcArgs {
     const float* X; long long n; long long ldx; int D;
     const float* cw; const double* cw64; int M; int K; int L; int cap;
@@ -140,22 +217,21 @@ struct BeamTcArgs {
     const double* P;       // (M,M,K,K) cross tables (exact)
     const float* Bg;       // pre-split codeword chunks [M][nch][hi,lo][256*32]
     const double* cmax;    // per dictionary max ||c||
-    float* rbuf;           // residual scratch [grid][2][128][D]
+    float* img;            // residual images [grid][2][nch][hi,lo][128*BK] (shared-memory layout)
     void* codes_out; int code_bytes; long long ldcodes;
     double* err_out;
     unsigned long long* stats;
     int nch;
     int qv;                // exact-recheck queue capacity per vector
-    int tmax;              // kept approximate values per row (<= BT_TMAX)
     int* bad;              // [n] set to 1 when a vector overflowed its queue (host re-encodes it)
 };
 
-__global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
+__global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int A_EL = BT_ROWS * BT_BK, B_EL = BT_N * BT_BK;
-    float* Abuf = reinterpret_cast<float*>(smem);        // [2][hi,lo][A_EL]
-    float* Bbuf = Abuf + 2 * 2 * A_EL;                    // [2][hi,lo][B_EL]
-    unsigned char* p = reinterpret_cast<unsigned char*>(Bbuf + 2 * 2 * B_EL);
+    float* Abuf = reinterpret_cast<float*>(smem);        // [NST][hi,lo][A_EL]
+    float* Bbuf = Abuf + BT_NST * 2 * A_EL;               // [NST][hi,lo][B_EL]
+    unsigned char* p = reinterpret_cast<unsigned char*>(Bbuf + BT_NST * 2 * B_EL);
     const int V = BT_ROWS / a.cap;
     const int M = a.M, K = a.K, D = a.D, cap = a.cap, L = a.L;
     const int BT_QV = a.qv;
@@ -163,21 +239,22 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
     double* qval = reinterpret_cast<double*>(p); p += sizeof(double) * V * BT_QV;       // [V][QV]
     double* vlim = reinterpret_cast<double*>(p); p += sizeof(double) * V;               // [V]
     double* xnorm = reinterpret_cast<double*>(p); p += sizeof(double) * V;              // [V]
-    float* rmin = reinterpret_cast<float*>(p); p += sizeof(float) * a.tmax * BT_ROWS;  // smallest T per row
+    float* rmin = reinterpret_cast<float*>(p); p += sizeof(float) * BT_S * BT_ROWS;  // sorted slice minima per row
     int* rarg = reinterpret_cast<int*>(p); p += sizeof(int) * BT_ROWS;                  // i1 per row
-    int* codes = reinterpret_cast<int*>(p); p += sizeof(int) * 2 * BT_ROWS * M;         // [2][rows][M]
+    uint8_t* codes = p; p += (2 * BT_ROWS * M + 15) & ~15;                               // [2][rows][M] (K <= 256)
     int* qflat = reinterpret_cast<int*>(p); p += sizeof(int) * V * BT_QV;               // [V][QV]
     int* qcnt = reinterpret_cast<int*>(p); p += sizeof(int) * V;                        // [V]
     int* sel = reinterpret_cast<int*>(p); p += sizeof(int) * BT_ROWS;                   // selected flat per child slot
     float* sq32s = reinterpret_cast<float*>(p); p += sizeof(float) * BT_N;
     int* vbad = reinterpret_cast<int*>(p); p += sizeof(int) * V;                       // [V] overflow flags
     float* erow = reinterpret_cast<float*>(p); p += sizeof(float) * BT_ROWS;           // per-row bound E_l
-    __shared__ uint64_t full_bar[2], empty_bar[2], acc_bar;
+    __shared__ uint64_t full_bar[BT_NST], empty_bar[BT_NST], acc_bar;
     __shared__ uint32_t tmem_sh;
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
-    float* rb = a.rbuf + (size_t)blockIdx.x * 2 * BT_ROWS * D;
+    const int nch = a.nch;
+    float* img = a.img + (size_t)blockIdx.x * 2 * nch * 2 * A_EL;
     const double u24 = 5.9604644775390625e-08, u22 = 2.384185791015625e-07;
     const int N = (K + 7) & ~7;
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(BT_ROWS >> 4) << 24);
@@ -188,7 +265,7 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < BT_NST; ++i) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&full_bar[i])));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&empty_bar[i])));
         }
@@ -209,11 +286,16 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
     const long long ngroups = (a.n + V - 1) / V;
     for (long long grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
     const long long v0 = grp * V;
-    // initial residual = x (rows v*cap), scores 0, ||x||
-    for (int e = tid; e < V * D; e += BT_T) {
-        const int v = e / D, d = e % D;
+    // initial residual = x (rows v*cap) as a tf32 hi/lo image, scores 0, ||x||
+    for (int e = tid; e < V * nch * (BT_BK / 4); e += BT_T) {
+        const int v = e / (nch * (BT_BK / 4)), rem = e % (nch * (BT_BK / 4));
+        const int ch = rem / (BT_BK / 4), c4 = rem % (BT_BK / 4);
         const long long gv = v0 + v;
-        rb[(size_t)(v * cap) * D + d] = gv < a.n ? a.X[gv * a.ldx + d] : 0.f;
+        const int k = ch * BT_BK + 4 * c4;
+        float x4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x4[u] = (gv < a.n && k + u < D) ? a.X[gv * a.ldx + k + u] : 0.f;
+        bt_store_split(img + (size_t)ch * 2 * A_EL, bt_off(v * cap, 4 * c4) >> 2, x4);
     }
     if (tid < V) {
         const long long gv = v0 + tid;
@@ -231,62 +313,38 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
         const long long tot_ll = (long long)live * K;
         const int width = (int)std::min((long long)L, tot_ll);
         for (int k = tid; k < BT_N; k += BT_T) sq32s[k] = k < K ? a.sq32[m * K + k] : __int_as_float(0x7f800000);
-        // ---- GEMM: rows (residuals) x codewords of dictionary m
-        const float* rcur = rb + (size_t)cur * BT_ROWS * D;
-        for (int ch = 0; ch < a.nch; ++ch, ++q) {
-            const int st = (int)(q & 1);
-            if (q >= 2) bt_wait(&empty_bar[st], (uint32_t)(((q >> 1) - 1) & 1));
-            float* Ah = Abuf + st * 2 * A_EL;
-            float* Al = Ah + A_EL;
-            float* Bs = Bbuf + st * 2 * B_EL;
-            if (tid == 0) {
+        // residual images written by threads (generic proxy) are read by bulk copies (async proxy)
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __syncthreads();
+        // ---- GEMM: rows (residual images) x codewords of dictionary m.  One thread
+        // streams both operands into the shared-memory ring with bulk copies and
+        // issues the MMAs; the others wait for the accumulator.
+        if (tid == 0) {
+            const float* Ag = img + (size_t)cur * nch * 2 * A_EL;
+            const float* Bm = a.Bg + (size_t)m * nch * 2 * B_EL;
+            constexpr uint32_t bytes_a = 2 * A_EL * sizeof(float), bytes_b = 2 * B_EL * sizeof(float);
+            auto issue = [&](int ch) {
+                const long long qq = q + ch;
+                const int st = (int)(qq % BT_NST);
+                const long long lap = qq / BT_NST;
+                if (lap >= 1) bt_wait(&empty_bar[st], (uint32_t)((lap - 1) & 1));
+                float* As = Abuf + st * 2 * A_EL;
+                float* Bs = Bbuf + st * 2 * B_EL;
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bt_smem_u32(&full_bar[st])),
-                             "r"((uint32_t)(2 * B_EL * sizeof(float)))
+                             "r"(bytes_a + bytes_b)
                              : "memory");
-                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                                 bt_smem_u32(Bs)),
-                             "l"(a.Bg + ((size_t)m * a.nch + ch) * 2 * B_EL), "r"((uint32_t)(2 * B_EL * sizeof(float))),
-                             "r"(bt_smem_u32(&full_bar[st]))
-                             : "memory");
-            }
-            const int k0 = ch * BT_BK;
-            {
-                // one thread per row: 8 x (4 consecutive k) -> one 16-B core-matrix row each
-                const int r = tid;
-                const int v = r / cap, l = r % cap;
-                const bool rl_ok = v < V && l < live && (v0 + v) < a.n;
-                const bool vec4 = (D & 3) == 0;
-                const float* src = rcur + (size_t)r * D;
-#pragma unroll
-                for (int c4 = 0; c4 < BT_BK / 4; ++c4) {
-                    const int gk = k0 + 4 * c4;
-                    float x4[4] = {0.f, 0.f, 0.f, 0.f};
-                    if (rl_ok) {
-                        if (vec4 && gk + 3 < D) {
-                            const float4 t = *reinterpret_cast<const float4*>(src + gk);
-                            x4[0] = t.x; x4[1] = t.y; x4[2] = t.z; x4[3] = t.w;
-                        } else {
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) x4[u] = gk + u < D ? src[gk + u] : 0.f;
-                        }
-                    }
-                    float4 h, lo;
-                    h.x = bt_tf32(x4[0]); lo.x = bt_tf32(x4[0] - h.x);
-                    h.y = bt_tf32(x4[1]); lo.y = bt_tf32(x4[1] - h.y);
-                    h.z = bt_tf32(x4[2]); lo.z = bt_tf32(x4[2] - h.z);
-                    h.w = bt_tf32(x4[3]); lo.w = bt_tf32(x4[3] - h.w);
-                    const uint32_t o = bt_off(r, 4 * c4) >> 2;
-                    *reinterpret_cast<float4*>(Ah + o) = h;
-                    *reinterpret_cast<float4*>(Al + o) = lo;
-                }
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncthreads();
-            if (tid == 0) {
-                bt_wait(&full_bar[st], (uint32_t)((q >> 1) & 1));
+                bt_bulk(As, Ag + (size_t)ch * 2 * A_EL, bytes_a, &full_bar[st]);
+                bt_bulk(Bs, Bm + (size_t)ch * 2 * B_EL, bytes_b, &full_bar[st]);
+            };
+            for (int ch = 0; ch < std::min(BT_NST - 1, nch); ++ch) issue(ch);
+            for (int ch = 0; ch < nch; ++ch) {
+                const long long qq = q + ch;
+                const int st = (int)(qq % BT_NST);
+                bt_wait(&full_bar[st], (uint32_t)((qq / BT_NST) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t ah = bt_smem_u32(Ah), al = bt_smem_u32(Al), bh = bt_smem_u32(Bs), bl = bt_smem_u32(Bs + B_EL);
-                const int ks = std::min(BT_BK / 8, (D - k0 + 7) / 8);
+                const uint32_t ah = bt_smem_u32(Abuf + st * 2 * A_EL), al = ah + A_EL * 4;
+                const uint32_t bh = bt_smem_u32(Bbuf + st * 2 * B_EL), bl = bh + B_EL * 4;
+                const int ks = std::min(BT_BK / 8, (D - ch * BT_BK + 7) / 8);
                 for (int s2 = 0; s2 < ks; ++s2) {
                     const uint32_t off = (uint32_t)s2 * 256;
                     const uint32_t acc0 = (ch > 0 || s2 > 0) ? 1u : 0u;
@@ -297,12 +355,15 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                                  bt_smem_u32(&empty_bar[st]))
                              : "memory");
-                if (ch == a.nch - 1)
+                if (ch == nch - 1)
                     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                                      bt_smem_u32(&acc_bar))
                                  : "memory");
+                // refill the slot of the previous chunk (its MMAs were issued before this one's)
+                if (ch + BT_NST - 1 < nch) issue(ch + BT_NST - 1);
             }
         }
+        q += nch;
         bt_wait(&acc_bar, acc_phase);
         acc_phase ^= 1;
         asm volatile("tcgen05.fence::after_thread_sync;");
@@ -312,45 +373,9 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
         const int rv = r / cap, rl = r % cap;
         const bool row_live = rv < V && rl < live && (v0 + rv) < a.n && !vbad[rv];
         const float s32 = row_live ? (float)score[cur * BT_ROWS + r] : 0.f;
-        // keep the T smallest approximate scores of the row (live*T >= width)
-        // each row keeps its T smallest approximate scores (replace-the-max list,
-        // sorted at the end); the union of the rows' lists bounds the width-th
-        // smallest of the vector from above
-        const int T = std::min(a.tmax, std::max(2, width));
-        float top[BT_TMAX];
-#pragma unroll
-        for (int i = 0; i < BT_TMAX; ++i) top[i] = __int_as_float(0x7f800000);
-        float tmaxv = __int_as_float(0x7f800000);
-        int tslot = 0;
-        int i1 = -1;
-        float best1 = __int_as_float(0x7f800000);
-        float v[32];
-        for (int c0 = 0; c0 < N; c0 += 32) {
-            bt_ld32(taddr_row + c0, v);
-            if (row_live) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const float w = s32 + fmaf(-2.f, v[i], sq32s[c0 + i]);
-                    if (w < tmaxv) {
-                        if (w < best1) { best1 = w; i1 = rl * K + c0 + i; }
-                        top[tslot] = w;
-                        tmaxv = -__int_as_float(0x7f800000);
-#pragma unroll
-                        for (int t2 = 0; t2 < BT_TMAX; ++t2)
-                            if (t2 < T && top[t2] > tmaxv) { tmaxv = top[t2]; tslot = t2; }
-                    }
-                }
-            }
-        }
-        // sort the kept values ascending (T <= 16, insertion sort in registers)
-#pragma unroll
-        for (int i = 1; i < BT_TMAX; ++i) {
-#pragma unroll
-            for (int j = BT_TMAX - 1; j >= 1; --j) {
-                if (j <= i && top[j] < top[j - 1]) { const float t3 = top[j]; top[j] = top[j - 1]; top[j - 1] = t3; }
-            }
-        }
-        const float m1 = top[0], m2 = top[1];
+        float m1, m2;
+        int i1;
+        bt_row_slices(taddr_row, N, K, row_live, s32, sq32s, rl, rmin + r, m1, m2, i1);
         // rigorous |v' - v| for this row: ||r_l|| from the exact score
         // (s_l = ||r_l||^2 - ||x||^2), 3xTF32 representation (3*2^-22) plus one
         // fp32-accumulator rounding per MMA step (3 per 8 of D) on sum|r_d c_d| <=
@@ -362,7 +387,8 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
             const double sl = score[cur * BT_ROWS + r];
             const double rn = sqrt(fmax(sl + xx, 0.0) * (1.0 + 1e-9)) + 1e-30;
             const double cm = a.cmax[m];
-            const double dlt = (m + 1) * u24 * (xnorm[vv] + m * cmax_all);
+            // stored residual = tf32 hi + lo of the fp32 difference: u24 + 2^-22 per stage
+            const double dlt = (m + 1) * (u24 + u22) * (xnorm[vv] + m * cmax_all);
             const double steps = 3.0 * ((D + 7) / 8) + 7.0;
             const double e_dot = (steps * u22 * (rn + dlt) + dlt) * cm;
             const double E = 2.0 * (2.0 * e_dot + 4.0 * u24 * (fabs(sl) + cm * cm + 2.0 * (rn + dlt) * cm)) + 1e-30;
@@ -370,42 +396,51 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
         } else {
             erow[r] = 0.f;
         }
-#pragma unroll
-        for (int i = 0; i < BT_TMAX; ++i)
-            if (i < a.tmax) rmin[i * BT_ROWS + r] = top[i];
         rarg[r] = i1;
         if (tid < V) qcnt[tid] = 0;
         __syncthreads();
-        // ---- per vector: threshold = width-th smallest of the 2*live row minima; bound E
-        if (tid < V && v0 + tid < a.n && !vbad[tid]) {
-            const int vv = tid;
-            float thr;
-            const int T = std::min(a.tmax, std::max(2, width));
-            if (width >= tot_ll || (long long)live * T < width) {
-                thr = __int_as_float(0x7f800000);
-            } else {
-                // width-th smallest of the rows' sorted top-T lists: multiway merge
-                int* ptr = sel + vv * cap;  // reuse the per-vector child slots as merge cursors
-                for (int l = 0; l < live; ++l) ptr[l] = 0;
-                thr = __int_as_float(0x7f800000);
+        // ---- per vector (one warp each): threshold = width-th smallest of the rows'
+        // sorted slice minima by a multiway merge with redux.sync; limit adds E
+        for (int vv = warp; vv < V; vv += BT_T / 32) {
+            if (v0 + vv >= a.n || vbad[vv]) continue;
+            const int lane = tid & 31;
+            float thr = __int_as_float(0x7f800000);
+            if (width < tot_ll && (long long)live * BT_S >= width) {
+                int ptr[BT_ROWS / 32];
+                float head[BT_ROWS / 32];
+#pragma unroll
+                for (int j = 0; j < BT_ROWS / 32; ++j) {
+                    const int l = lane + 32 * j;
+                    ptr[j] = 0;
+                    head[j] = l < live ? rmin[vv * cap + l] : __int_as_float(0x7f800000);
+                }
                 for (int step = 0; step < width; ++step) {
-                    float best = __int_as_float(0x7f800000);
-                    int bl = -1;
-                    for (int l = 0; l < live; ++l) {
-                        if (ptr[l] < T) {
-                            const float x = rmin[ptr[l] * BT_ROWS + vv * cap + l];
-                            if (bl < 0 || x < best) { best = x; bl = l; }
-                        }
+                    float mine = head[0];
+#pragma unroll
+                    for (int j = 1; j < BT_ROWS / 32; ++j) mine = fminf(mine, head[j]);
+                    const unsigned key = __reduce_min_sync(0xffffffffu, bt_key(mine));
+                    thr = bt_unkey(key);
+                    const unsigned own = __ballot_sync(0xffffffffu, bt_key(mine) == key);
+                    bool adv = lane == __ffs(own) - 1;
+#pragma unroll
+                    for (int j = 0; j < BT_ROWS / 32; ++j) {
+                        const bool hit = adv && head[j] == mine;
+                        adv = adv && !hit;
+                        const int pj = ptr[j] + (hit ? 1 : 0);
+                        const float nx = (hit && pj < BT_S) ? rmin[pj * BT_ROWS + vv * cap + lane + 32 * j]
+                                                            : __int_as_float(0x7f800000);
+                        ptr[j] = pj;
+                        head[j] = hit ? nx : head[j];
                     }
-                    if (bl < 0) break;
-                    ptr[bl]++;
-                    thr = best;
+                    __syncwarp();
                 }
             }
             float emax = 0.f;
-            for (int l = 0; l < live; ++l) emax = fmaxf(emax, erow[vv * cap + l]);
+            for (int l = lane; l < live; l += 32) emax = fmaxf(emax, erow[vv * cap + l]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
             // row l keeps candidates with v' <= tau' + E_max + E_l (E_l added per row)
-            vlim[vv] = (double)thr + (double)emax;
+            if (lane == 0) vlim[vv] = (double)thr + (double)emax;
         }
         __syncthreads();
         // ---- candidates: rows whose second minimum is above the limit offer their
@@ -423,6 +458,7 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
             const bool any_multi = __any_sync(0xffffffffu, multi);
             if (any_multi) {
                 for (int c0 = 0; c0 < N; c0 += 32) {
+                    float v[32];
                     bt_ld32(taddr_row + c0, v);
                     if (multi) {
 #pragma unroll
@@ -439,14 +475,16 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncthreads();
-        if (tid < V && qcnt[tid] > BT_QV && !vbad[tid]) {
+        // a queue that overflowed, or that holds fewer than width entries (cannot
+        // happen with a valid bound; kept as a guard), sends the vector to the exact path
+        if (tid < V && (qcnt[tid] > BT_QV || qcnt[tid] < width) && !vbad[tid]) {
             vbad[tid] = 1;  // too many near-boundary candidates: the host re-encodes this vector
             if (v0 + tid < a.n) a.bad[v0 + tid] = 1;
         }
         __syncthreads();
         // ---- exact float64 values of every queued candidate (round robin over threads)
         {
-            const int* pcodes = codes + cur * BT_ROWS * M;
+            const uint8_t* pcodes = codes + cur * BT_ROWS * M;
             int total_q = 0;
             for (int vv = 0; vv < V; ++vv) total_q += std::min(qcnt[vv], BT_QV);
             // flatten (vector, slot) pairs
@@ -478,7 +516,7 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
                 }
                 const double t = dsub(a.sq[m * K + k], dmul(2.0, tot));
                 double cross = 0.0;
-                const int* pcv = pcodes + (vv * cap + l) * M;
+                const uint8_t* pcv = pcodes + (vv * cap + l) * M;
                 for (int j = 0; j < m; ++j) cross = dadd(cross, a.P[(((long long)j * M + m) * K + pcv[j]) * K + k]);
                 qval[idx] = dadd(dadd(score[cur * BT_ROWS + vv * cap + l], t), dmul(2.0, cross));
             }
@@ -512,16 +550,17 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
                 int pos = 0;
                 for (int j = 0; j < width; ++j) pos += qflat[sel[vv * cap + j]] < f;
                 const int parent = f / K, kk = f % K;
-                int* cc = codes + (nxt * BT_ROWS + vv * cap + pos) * M;
-                const int* pp = codes + (cur * BT_ROWS + vv * cap + parent) * M;
+                uint8_t* cc = codes + (nxt * BT_ROWS + vv * cap + pos) * M;
+                const uint8_t* pp = codes + (cur * BT_ROWS + vv * cap + parent) * M;
                 for (int j = 0; j < m; ++j) cc[j] = pp[j];
-                cc[m] = kk;
+                cc[m] = (uint8_t)kk;
                 score[nxt * BT_ROWS + vv * cap + pos] = qval[idx];
                 rarg[vv * cap + pos] = (parent << 16) | kk;  // reuse: (parent, k) of child row
             }
         }
         __syncthreads();
-        // ---- child residuals r = r_parent - c_m(k) (fp32; the bound covers the rounding)
+        // ---- child residual images r = (hi + lo)_parent - c_m(k), split again (fp32;
+        // the bound covers both roundings).  Thread per child row.
         if (m + 1 < M) {
             const int nxt = cur ^ 1;
             const int rr = tid;
@@ -529,17 +568,30 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
             if (vv < V && slotv < width && v0 + vv < a.n && !vbad[vv]) {
                 const int pk = rarg[rr];
                 const int parent = pk >> 16, kk = pk & 0xFFFF;
-                float* dst = rb + ((size_t)nxt * BT_ROWS + rr) * D;
-                const float* par = rb + ((size_t)cur * BT_ROWS + vv * cap + parent) * D;
+                const float* src = img + (size_t)cur * nch * 2 * A_EL;
+                float* dst = img + (size_t)nxt * nch * 2 * A_EL;
                 const float* cwr = a.cw + ((long long)m * K + kk) * D;
-                if ((D & 3) == 0) {
-                    for (int d = 0; d < D; d += 4) {
-                        const float4 p4 = *reinterpret_cast<const float4*>(par + d);
-                        const float4 c4 = __ldg(reinterpret_cast<const float4*>(cwr + d));
-                        *reinterpret_cast<float4*>(dst + d) = make_float4(p4.x - c4.x, p4.y - c4.y, p4.z - c4.z, p4.w - c4.w);
+                const int pr = vv * cap + parent;
+                const bool vec4 = (D & 3) == 0;
+#pragma unroll 4
+                for (int ch = 0; ch < nch; ++ch) {
+#pragma unroll
+                    for (int c4 = 0; c4 < BT_BK / 4; ++c4) {
+                        const int k = ch * BT_BK + 4 * c4;
+                        const uint32_t po = bt_off(pr, 4 * c4) >> 2;
+                        const float4 h4 = *reinterpret_cast<const float4*>(src + (size_t)ch * 2 * A_EL + po);
+                        const float4 l4 = *reinterpret_cast<const float4*>(src + (size_t)ch * 2 * A_EL + A_EL + po);
+                        float c[4];
+                        if (vec4 && k + 3 < D) {
+                            const float4 t = __ldg(reinterpret_cast<const float4*>(cwr + k));
+                            c[0] = t.x; c[1] = t.y; c[2] = t.z; c[3] = t.w;
+                        } else {
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) c[u] = k + u < D ? cwr[k + u] : 0.f;
+                        }
+                        float x4[4] = {(h4.x + l4.x) - c[0], (h4.y + l4.y) - c[1], (h4.z + l4.z) - c[2], (h4.w + l4.w) - c[3]};
+                        bt_store_split(dst + (size_t)ch * 2 * A_EL, bt_off(rr, 4 * c4) >> 2, x4);
                     }
-                } else {
-                    for (int d = 0; d < D; ++d) dst[d] = par[d] - cwr[d];
                 }
             }
         }
@@ -559,7 +611,7 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
             const double s = score[cur * BT_ROWS + vv * cap + l];
             if (s < bv) { bv = s; bi = l; }
         }
-        const int* best = codes + (cur * BT_ROWS + vv * cap + bi) * M;
+        const uint8_t* best = codes + (cur * BT_ROWS + vv * cap + bi) * M;
         for (int j = 0; j < M; ++j) {
             const int c = best[j];
             if (a.code_bytes == 1) ((uint8_t*)a.codes_out)[gv * a.ldcodes + j] = (uint8_t)c;
@@ -653,11 +705,11 @@ int launch_encode_tc(const float* X, long long n, long long ldx, int D, const fl
     if (cap > BT_ROWS || n <= 0) return n <= 0 ? 0 : 1;
     const int V = BT_ROWS / cap;
     const int nch = (D + BT_BK - 1) / BT_BK;
-    const int qv = 3 * cap + 8;
-    const int tmax = std::min(8, std::max(2, (int)std::min((long long)L, (long long)K)));
-    size_t smem = sizeof(float) * (2 * 2 * BT_ROWS * BT_BK + 2 * 2 * BT_N * BT_BK);
+    // a single first-stage row cannot cover beams wider than 16: then all K go to the exact pass
+    const int qv = cap > BT_S ? std::max(3 * cap + 8, K) : 3 * cap + 8;
+    size_t smem = sizeof(float) * (BT_NST * 2 * BT_ROWS * BT_BK + BT_NST * 2 * BT_N * BT_BK);
     smem += sizeof(double) * (2 * BT_ROWS + (size_t)V * qv + 2 * V);
-    smem += sizeof(float) * (size_t)tmax * BT_ROWS + sizeof(int) * BT_ROWS + sizeof(int) * 2 * BT_ROWS * (size_t)M;
+    smem += sizeof(float) * (size_t)BT_S * BT_ROWS + sizeof(int) * BT_ROWS + ((2 * BT_ROWS * (size_t)M + 15) & ~size_t(15));
     smem += sizeof(int) * ((size_t)V * qv + V + BT_ROWS) + sizeof(float) * BT_N + sizeof(int) * V +
             sizeof(float) * BT_ROWS;
     if (smem > 227 * 1024) return 1;
@@ -665,7 +717,16 @@ int launch_encode_tc(const float* X, long long n, long long ldx, int D, const fl
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const long long ngroups = (n + V - 1) / V;
-    const int grid = (int)std::min<long long>(ngroups, sms);
+    // two CTAs per SM when the shared-memory image allows it (TMEM: 2 x 256 columns):
+    // one CTA's epilogue overlaps the other's MMAs
+    DA_CUDA(cudaFuncSetAttribute(beam_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DA_CUDA(cudaFuncSetAttribute(beam_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    int per_sm = 1, smem_sm = 0;
+    cudaFuncAttributes fa{};
+    DA_CUDA(cudaFuncGetAttributes(&fa, beam_tc_kernel));
+    DA_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+    if (2 * (smem + fa.sharedSizeBytes + 1024) <= (size_t)smem_sm) per_sm = 2;
+    const int grid = (int)std::min<long long>(ngroups, (long long)sms * per_sm);
     // scratch
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
@@ -673,7 +734,7 @@ int launch_encode_tc(const float* X, long long n, long long ldx, int D, const fl
     const size_t o_c64 = take(sizeof(double) * (size_t)M * K * D);
     const size_t o_sq32 = take(sizeof(float) * (size_t)M * K);
     const size_t o_cmax = take(sizeof(double) * M);
-    const size_t o_rb = take(sizeof(float) * (size_t)grid * 2 * BT_ROWS * D);
+    const size_t o_rb = take(sizeof(float) * (size_t)grid * 2 * nch * 2 * BT_ROWS * BT_BK);
     const size_t o_bad = take(sizeof(int) * (size_t)n);
     const size_t o_lst = take(sizeof(int) * (size_t)n);
     const size_t o_cnt = take(sizeof(int) * 4);
@@ -695,12 +756,11 @@ int launch_encode_tc(const float* X, long long n, long long ldx, int D, const fl
     }
     BeamTcArgs a{};
     a.X = X; a.n = n; a.ldx = ldx; a.D = D; a.cw = cw; a.cw64 = cw64; a.M = M; a.K = K; a.L = L; a.cap = cap;
-    a.sq = sq; a.sq32 = sq32; a.P = P; a.Bg = Bg; a.cmax = cmax; a.rbuf = (float*)(base + o_rb);
+    a.sq = sq; a.sq32 = sq32; a.P = P; a.Bg = Bg; a.cmax = cmax; a.img = (float*)(base + o_rb);
     a.codes_out = codes_out; a.code_bytes = code_bytes; a.ldcodes = ldcodes; a.err_out = err_out; a.stats = stats;
-    a.nch = nch; a.qv = qv; a.tmax = tmax; a.bad = bad;
+    a.nch = nch; a.qv = qv; a.bad = bad;
     {
         ProfScope ps1("encode_beam_tc", s);
-        DA_CUDA(cudaFuncSetAttribute(beam_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         beam_tc_kernel<<<grid, BT_T, smem, s>>>(a);
         DA_CHECK_LAUNCH("beam_tc_kernel");
     }
@@ -712,7 +772,7 @@ int launch_encode_tc(const float* X, long long n, long long ldx, int D, const fl
     int h_cnt = 0;
     DA_CUDA(cudaMemcpyAsync(&h_cnt, cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
     DA_CUDA(cudaStreamSynchronize(s));
-    if (getenv("DA_DEBUG")) fprintf(stderr, "[da] encode_tc: n=%lld V=%d cap=%d overflowed=%d\n", n, V, cap, h_cnt);
+    if (getenv("DA_DEBUG")) fprintf(stderr, "[da] encode_tc: n=%lld V=%d cap=%d grid=%d per_sm=%d smem=%zu overflowed=%d\n", n, V, cap, grid, per_sm, smem, h_cnt);
     if (h_cnt > 0) {
         float* xg = nullptr;
         void* cg = nullptr;
