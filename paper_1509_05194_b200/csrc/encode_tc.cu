@@ -16,9 +16,21 @@
 // exact float64 scores.
 //
 // Layout per CTA (128 threads = 128 TMEM lanes = 128 rows): V = 128 / cap
-// vectors; row v*cap + l holds beam l of vector v.  Residuals live in a global
-// scratch slab (L2-resident), staged per 32-wide k-chunk as tf32 hi/lo into the
-// canonical no-swizzle K-major layout; codeword chunks arrive by bulk copy.
+// vectors; row v*cap + l holds beam l of vector v.  Operands are extended by one
+// k column so the MMA returns the whole approximate term directly:
+//   A row = [ r_l , 1 ]          (tf32 hi/lo image of the fp32 residual)
+//   B row = [ -2 c_mk , ||c_mk||^2 ]   (rows k >= K carry a 1e30 sentinel)
+// Residual images live in a per-CTA global slab (L2-resident) already in the
+// canonical no-swizzle K-major shared-memory layout, so both operands arrive by
+// bulk copy (cp.async.bulk) into a 3-deep ring; one thread issues copies and MMAs.
+//
+// Per stage, thread = row: one pass over the 256 TMEM columns keeps, for each of
+// 16 contiguous 16-column slices, the smallest and second smallest value (the
+// column index is embedded in the 4 low mantissa bits, covered by the bound).
+// A warp per vector selects the width-th smallest slice minimum (redux.sync),
+// which bounds the vector's width-th smallest candidate from above.  Slices whose
+// minimum is under the limit queue that one candidate; the rare slices whose
+// second minimum is also under it are rescanned.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -63,13 +75,26 @@ __device__ __forceinline__ void bt_mma(uint32_t tmem_d, uint64_t a, uint64_t b, 
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
-__device__ __forceinline__ void bt_wait(uint64_t* bar, uint32_t phase) {
+__device__ __forceinline__ bool bt_try_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t ok;
     asm volatile(
-        "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@P1 bra DONE_%=;\n\tbra WAIT_%=;\n\tDONE_%=:\n\t}\n" ::"r"(bt_smem_u32(bar)),
-        "r"(phase)
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(ok)
+        : "r"(bt_smem_u32(bar)), "r"(phase)
         : "memory");
+    return ok != 0;
+}
+// bounded spin: a lost arrival traps (with a message) instead of hanging the GPU
+__device__ __forceinline__ void bt_wait(uint64_t* bar, uint32_t phase) {
+    long long spins = 0;
+    while (!bt_try_wait(bar, phase)) {
+        if (++spins > (1ll << 26)) {
+            printf("[da] beam_tc: mbarrier wait timed out (block %d thread %d)\n", blockIdx.x, threadIdx.x);
+            __trap();
+        }
+    }
 }
 __device__ __forceinline__ void bt_ld32(uint32_t taddr, float* v) {
     uint32_t r[32];
@@ -87,31 +112,43 @@ __device__ __forceinline__ void bt_ld32(uint32_t taddr, float* v) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// exact x.c in the reference's order (FMA chain, OpenBLAS k-blocks above 384)
-__device__ __forceinline__ double bt_exact_dot(const double* __restrict__ x, const double* __restrict__ c, int D) {
+
+// exact x.c in the reference's order (FMA chain, OpenBLAS k-blocks above 384);
+// both operands fp32 in memory (exact in float64)
+__device__ __forceinline__ double bt_exact_dot(const float* __restrict__ x, const float* __restrict__ c, int D, bool v4) {
     double tot = 0.0;
     bool first = true;
     int d = 0;
     while (d < D) {
         const int e = d + (int)blas_block_len(D - d);
         double acc = 0.0;
-        for (; d + 8 <= e; d += 8) {
-            double xv[8], cv[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) { xv[u] = x[d + u]; cv[u] = c[d + u]; }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) acc = __fma_rn(xv[u], cv[u], acc);
+        if (v4) {
+            for (; d + 8 <= e; d += 8) {
+                const float4 x0 = __ldg(reinterpret_cast<const float4*>(x + d));
+                const float4 x1 = __ldg(reinterpret_cast<const float4*>(x + d + 4));
+                const float4 c0 = __ldg(reinterpret_cast<const float4*>(c + d));
+                const float4 c1 = __ldg(reinterpret_cast<const float4*>(c + d + 4));
+                acc = __fma_rn((double)x0.x, (double)c0.x, acc);
+                acc = __fma_rn((double)x0.y, (double)c0.y, acc);
+                acc = __fma_rn((double)x0.z, (double)c0.z, acc);
+                acc = __fma_rn((double)x0.w, (double)c0.w, acc);
+                acc = __fma_rn((double)x1.x, (double)c1.x, acc);
+                acc = __fma_rn((double)x1.y, (double)c1.y, acc);
+                acc = __fma_rn((double)x1.z, (double)c1.z, acc);
+                acc = __fma_rn((double)x1.w, (double)c1.w, acc);
+            }
         }
-        for (; d < e; ++d) acc = __fma_rn(x[d], c[d], acc);
+        for (; d < e; ++d) acc = __fma_rn((double)x[d], (double)c[d], acc);
         tot = first ? acc : dadd(tot, acc);
         first = false;
     }
     return tot;
 }
 
-// Codebook -> per (dictionary, k-chunk) tf32 hi/lo tiles in the shared-memory image.
-__global__ void cb_tf32_prep_kernel(const float* __restrict__ cw, int M, int K, int D, int nch,
-                                    float* __restrict__ out) {
+// Codebook -> per (dictionary, k-chunk) tf32 hi/lo images of B = [-2c, ||c||^2],
+// sentinel 1e30 in the norm column of the padding rows k >= K.
+__global__ void cb_tf32_prep_kernel(const float* __restrict__ cw, const double* __restrict__ sq, int M, int K, int D,
+                                    int nch, float* __restrict__ out) {
     const long long per = (long long)BT_N * BT_BK;
     const long long total = (long long)M * nch * per;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
@@ -120,12 +157,10 @@ __global__ void cb_tf32_prep_kernel(const float* __restrict__ cw, int M, int K, 
         const int rem = (int)(e % per);
         const int r = rem / BT_BK, k = rem % BT_BK;
         const int gk = ch * BT_BK + k;
-        float h = 0.f, l = 0.f;
-        if (r < K && gk < D) {
-            const float v = cw[((long long)m * K + r) * D + gk];
-            h = bt_tf32(v);
-            l = bt_tf32(v - h);
-        }
+        float v = 0.f;
+        if (gk < D) v = r < K ? -2.f * cw[((long long)m * K + r) * D + gk] : 0.f;
+        else if (gk == D) v = r < K ? (float)sq[(long long)m * K + r] : 1e30f;
+        const float h = bt_tf32(v), l = bt_tf32(v - h);
         float* base = out + (size_t)mc * 2 * per;
         const uint32_t o = bt_off(r, k) >> 2;
         base[o] = h;
@@ -160,64 +195,38 @@ __device__ __forceinline__ float bt_unkey(unsigned k) {
     return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
 
-// One row's approximate scores v' = s + sq - 2 r.c from TMEM, branch-free:
-// the minimum of each of BT_S column slices (slice = column mod BT_S) sorted
-// ascending into out[i * BT_ROWS], the two smallest values m1 <= m2 and the flat
-// index i1 of the first minimum.  Every slice minimum is a distinct candidate,
-// so the width-th smallest over a vector's slice minima bounds its width-th
-// smallest candidate from above.  TMEM loads are warp-collective.
-__device__ __forceinline__ void bt_row_slices(uint32_t taddr_row, int N, int K, bool row_live, float s32,
-                                              const float* __restrict__ sq32s, int rl, float* __restrict__ out,
-                                              float& m1, float& m2, int& i1) {
-    const float INF = __int_as_float(0x7f800000);
-    float sm[BT_S];
+
+// One row's pass over the 256 TMEM columns: per slice the smallest (s1) and
+// second smallest (s2) value, the slice-local position embedded in the 4 low
+// mantissa bits of s1/s2.  CONTIG: slice = column / 16 (position = column % 16);
+// else slice = column % 16 (position = column / 16).  Loads are warp-collective.
+template <bool CONTIG>
+__device__ __forceinline__ void bt_row_pass(uint32_t taddr_row, bool row_live, float* s1, float* s2) {
 #pragma unroll
-    for (int i = 0; i < BT_S; ++i) sm[i] = INF;
-    m1 = INF;
-    m2 = INF;
-    i1 = -1;
-    float v[32];
-    for (int c0 = 0; c0 < N; c0 += 32) {
-        bt_ld32(taddr_row + c0, v);
+    for (int c = 0; c < BT_N / 32; ++c) {
+        float v[32];
+        bt_ld32(taddr_row + 32 * c, v);
         if (row_live) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
-                const float w = s32 + fmaf(-2.f, v[i], sq32s[c0 + i]);
-                sm[i % BT_S] = fminf(sm[i % BT_S], w);
-                m2 = fminf(m2, fmaxf(m1, w));
-                if (w < m1) i1 = rl * K + c0 + i;
-                m1 = fminf(m1, w);
+                const int sl = CONTIG ? 2 * c + (i >> 4) : (i & 15);
+                const uint32_t pos = CONTIG ? (uint32_t)(i & 15) : (uint32_t)(2 * c + (i >> 4));
+                const float w = __uint_as_float((__float_as_uint(v[i]) & ~15u) | pos);
+                s2[sl] = fminf(s2[sl], fmaxf(s1[sl], w));
+                s1[sl] = fminf(s1[sl], w);
             }
         }
     }
-    // bitonic sorting network (ascending)
-#pragma unroll
-    for (int k = 2; k <= BT_S; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-#pragma unroll
-            for (int i = 0; i < BT_S; ++i) {
-                const int l = i ^ j;
-                if (l > i) {
-                    const float lo = fminf(sm[i], sm[l]), hi = fmaxf(sm[i], sm[l]);
-                    if ((i & k) == 0) { sm[i] = lo; sm[l] = hi; } else { sm[i] = hi; sm[l] = lo; }
-                }
-            }
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < BT_S; ++i) out[i * BT_ROWS] = sm[i];
 }
 
 struct BeamTcArgs {
     const float* X; long long n; long long ldx; int D;
-    const float* cw; const double* cw64; int M; int K; int L; int cap;
+    const float* cw; int M; int K; int L; int cap;
     const double* sq;      // (M*K) einsum norms (exact)
-    const float* sq32;     // fp32 copy
     const double* P;       // (M,M,K,K) cross tables (exact)
-    const float* Bg;       // pre-split codeword chunks [M][nch][hi,lo][256*32]
-    const double* cmax;    // per dictionary max ||c||
-    float* img;            // residual images [grid][2][nch][hi,lo][128*BK] (shared-memory layout)
+    const float* Bg;       // codeword images [M][nch][hi,lo][256*BK]
+    const double* cmax;    // per dictionary: [max ||c||, max ||c||^2]
+    float* img;            // residual images [grid][2][nch][hi,lo][128*BK]
     void* codes_out; int code_bytes; long long ldcodes;
     double* err_out;
     unsigned long long* stats;
@@ -234,30 +243,31 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
     unsigned char* p = reinterpret_cast<unsigned char*>(Bbuf + BT_NST * 2 * B_EL);
     const int V = BT_ROWS / a.cap;
     const int M = a.M, K = a.K, D = a.D, cap = a.cap, L = a.L;
-    const int BT_QV = a.qv;
+    const int QV = a.qv;
     double* score = reinterpret_cast<double*>(p); p += sizeof(double) * 2 * BT_ROWS;     // [2][rows]
-    double* qval = reinterpret_cast<double*>(p); p += sizeof(double) * V * BT_QV;       // [V][QV]
+    double* qval = reinterpret_cast<double*>(p); p += sizeof(double) * V * QV;          // [V][QV]
     double* vlim = reinterpret_cast<double*>(p); p += sizeof(double) * V;               // [V]
     double* xnorm = reinterpret_cast<double*>(p); p += sizeof(double) * V;              // [V]
-    float* rmin = reinterpret_cast<float*>(p); p += sizeof(float) * BT_S * BT_ROWS;  // sorted slice minima per row
-    int* rarg = reinterpret_cast<int*>(p); p += sizeof(int) * BT_ROWS;                  // i1 per row
-    uint8_t* codes = p; p += (2 * BT_ROWS * M + 15) & ~15;                               // [2][rows][M] (K <= 256)
-    int* qflat = reinterpret_cast<int*>(p); p += sizeof(int) * V * BT_QV;               // [V][QV]
+    float* slist = reinterpret_cast<float*>(p); p += sizeof(float) * BT_S * BT_ROWS;   // [S][rows] slice minima
+    int* rarg = reinterpret_cast<int*>(p); p += sizeof(int) * BT_ROWS;                  // (parent, k) per child
+    int* qflat = reinterpret_cast<int*>(p); p += sizeof(int) * V * QV;                  // [V][QV]
     int* qcnt = reinterpret_cast<int*>(p); p += sizeof(int) * V;                        // [V]
-    int* sel = reinterpret_cast<int*>(p); p += sizeof(int) * BT_ROWS;                   // selected flat per child slot
-    float* sq32s = reinterpret_cast<float*>(p); p += sizeof(float) * BT_N;
+    int* sel = reinterpret_cast<int*>(p); p += sizeof(int) * BT_ROWS;                   // selected entry per child slot
     int* vbad = reinterpret_cast<int*>(p); p += sizeof(int) * V;                       // [V] overflow flags
     float* erow = reinterpret_cast<float*>(p); p += sizeof(float) * BT_ROWS;           // per-row bound E_l
+    uint8_t* codes = p;                                                                 // [2][rows][M] (K <= 256)
     __shared__ uint64_t full_bar[BT_NST], empty_bar[BT_NST], acc_bar;
     __shared__ uint32_t tmem_sh;
 
     const int tid = threadIdx.x;
-    const int warp = tid >> 5;
+    const int warp = tid >> 5, lane = tid & 31;
     const int nch = a.nch;
     float* img = a.img + (size_t)blockIdx.x * 2 * nch * 2 * A_EL;
-    const double u24 = 5.9604644775390625e-08, u22 = 2.384185791015625e-07;
-    const int N = (K + 7) & ~7;
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(BT_ROWS >> 4) << 24);
+    const double u24 = 5.9604644775390625e-08, u22 = 2.384185791015625e-07, u19 = 1.9073486328125e-06;
+    const float INF = __int_as_float(0x7f800000);
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BT_N >> 3) << 17) | ((uint32_t)(BT_ROWS >> 4) << 24);
+    const bool xv4 = ((D & 3) == 0) && ((a.ldx & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(a.cw) & 15) == 0);
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(bt_smem_u32(&tmem_sh)),
@@ -278,15 +288,18 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
     const uint32_t tmem = tmem_sh;
     const uint32_t taddr_row = tmem + ((uint32_t)(warp * 32) << 16);
     double cmax_all = 0.0;
-    for (int j = 0; j < M; ++j) cmax_all = fmax(cmax_all, a.cmax[j]);
+    for (int j = 0; j < M; ++j) cmax_all = fmax(cmax_all, a.cmax[2 * j]);
+    const double steps = 3.0 * nch * (BT_BK / 8) + 7.0;   // fp32 accumulations per TMEM value (+ slack)
+    // slices: 16 contiguous 16-column blocks when K fills the row, else column mod 16
+    const bool contig = K > 128;
 
-    long long q = 0;        // k-chunk steps issued (pipeline phases, persist across groups)
+    long long q = 0;        // k-chunks streamed (ring phases persist across groups)
     uint32_t acc_phase = 0;
     unsigned long long n_exact = 0;
     const long long ngroups = (a.n + V - 1) / V;
     for (long long grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
     const long long v0 = grp * V;
-    // initial residual = x (rows v*cap) as a tf32 hi/lo image, scores 0, ||x||
+    // initial residual image: rows v*cap = [x, 1, 0...]; scores 0; ||x||
     for (int e = tid; e < V * nch * (BT_BK / 4); e += BT_T) {
         const int v = e / (nch * (BT_BK / 4)), rem = e % (nch * (BT_BK / 4));
         const int ch = rem / (BT_BK / 4), c4 = rem % (BT_BK / 4);
@@ -294,31 +307,30 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
         const int k = ch * BT_BK + 4 * c4;
         float x4[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) x4[u] = (gv < a.n && k + u < D) ? a.X[gv * a.ldx + k + u] : 0.f;
+        for (int u = 0; u < 4; ++u) {
+            const int kk = k + u;
+            x4[u] = kk < D ? (gv < a.n ? a.X[gv * a.ldx + kk] : 0.f) : (kk == D ? 1.f : 0.f);
+        }
         bt_store_split(img + (size_t)ch * 2 * A_EL, bt_off(v * cap, 4 * c4) >> 2, x4);
     }
     if (tid < V) {
         const long long gv = v0 + tid;
-        double s = 0.0;
+        double s2 = 0.0;
         if (gv < a.n)
-            for (int d = 0; d < D; ++d) { const double t = a.X[gv * a.ldx + d]; s = __fma_rn(t, t, s); }
-        xnorm[tid] = sqrt(s) * (1.0 + 1e-12);
+            for (int d = 0; d < D; ++d) { const double t = a.X[gv * a.ldx + d]; s2 = __fma_rn(t, t, s2); }
+        xnorm[tid] = sqrt(s2) * (1.0 + 1e-12);
+        vbad[tid] = 0;
     }
     for (int r = tid; r < BT_ROWS; r += BT_T) score[r] = 0.0;
-    if (tid < V) vbad[tid] = 0;
 
-    __syncthreads();
     int cur = 0, live = 1;
     for (int m = 0; m < M; ++m) {
         const long long tot_ll = (long long)live * K;
         const int width = (int)std::min((long long)L, tot_ll);
-        for (int k = tid; k < BT_N; k += BT_T) sq32s[k] = k < K ? a.sq32[m * K + k] : __int_as_float(0x7f800000);
         // residual images written by threads (generic proxy) are read by bulk copies (async proxy)
         asm volatile("fence.proxy.async.global;" ::: "memory");
         __syncthreads();
-        // ---- GEMM: rows (residual images) x codewords of dictionary m.  One thread
-        // streams both operands into the shared-memory ring with bulk copies and
-        // issues the MMAs; the others wait for the accumulator.
+        // ---- GEMM: TMEM[row][k] = ||c_k||^2 - 2 r_row . c_k  (3xTF32, fp32 accumulate)
         if (tid == 0) {
             const float* Ag = img + (size_t)cur * nch * 2 * A_EL;
             const float* Bm = a.Bg + (size_t)m * nch * 2 * B_EL;
@@ -328,13 +340,11 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
                 const int st = (int)(qq % BT_NST);
                 const long long lap = qq / BT_NST;
                 if (lap >= 1) bt_wait(&empty_bar[st], (uint32_t)((lap - 1) & 1));
-                float* As = Abuf + st * 2 * A_EL;
-                float* Bs = Bbuf + st * 2 * B_EL;
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bt_smem_u32(&full_bar[st])),
                              "r"(bytes_a + bytes_b)
                              : "memory");
-                bt_bulk(As, Ag + (size_t)ch * 2 * A_EL, bytes_a, &full_bar[st]);
-                bt_bulk(Bs, Bm + (size_t)ch * 2 * B_EL, bytes_b, &full_bar[st]);
+                bt_bulk(Abuf + st * 2 * A_EL, Ag + (size_t)ch * 2 * A_EL, bytes_a, &full_bar[st]);
+                bt_bulk(Bbuf + st * 2 * B_EL, Bm + (size_t)ch * 2 * B_EL, bytes_b, &full_bar[st]);
             };
             for (int ch = 0; ch < std::min(BT_NST - 1, nch); ++ch) issue(ch);
             for (int ch = 0; ch < nch; ++ch) {
@@ -344,8 +354,8 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t ah = bt_smem_u32(Abuf + st * 2 * A_EL), al = ah + A_EL * 4;
                 const uint32_t bh = bt_smem_u32(Bbuf + st * 2 * B_EL), bl = bh + B_EL * 4;
-                const int ks = std::min(BT_BK / 8, (D - ch * BT_BK + 7) / 8);
-                for (int s2 = 0; s2 < ks; ++s2) {
+#pragma unroll
+                for (int s2 = 0; s2 < BT_BK / 8; ++s2) {
                     const uint32_t off = (uint32_t)s2 * 256;
                     const uint32_t acc0 = (ch > 0 || s2 > 0) ? 1u : 0u;
                     bt_mma(tmem, bt_desc(ah + off), bt_desc(bh + off), idesc, acc0);
@@ -368,69 +378,64 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
         acc_phase ^= 1;
         asm volatile("tcgen05.fence::after_thread_sync;");
 
-        // ---- per row: approximate scores v' = s + sq - 2 r.c, two smallest + argmin
+        // ---- row pass: per 16-column slice the smallest / second smallest value
+        // (column index in the 4 low mantissa bits), branch-free
         const int r = tid;
         const int rv = r / cap, rl = r % cap;
         const bool row_live = rv < V && rl < live && (v0 + rv) < a.n && !vbad[rv];
         const float s32 = row_live ? (float)score[cur * BT_ROWS + r] : 0.f;
-        float m1, m2;
-        int i1;
-        bt_row_slices(taddr_row, N, K, row_live, s32, sq32s, rl, rmin + r, m1, m2, i1);
-        // rigorous |v' - v| for this row: ||r_l|| from the exact score
-        // (s_l = ||r_l||^2 - ||x||^2), 3xTF32 representation (3*2^-22) plus one
-        // fp32-accumulator rounding per MMA step (3 per 8 of D) on sum|r_d c_d| <=
-        // ||r|| ||c||, fp32 rounding of the residual (m steps) and of the score
-        // arithmetic (sq, fma, add), doubled for safety
+        float s1[BT_S], s2v[BT_S];
+#pragma unroll
+        for (int i = 0; i < BT_S; ++i) { s1[i] = INF; s2v[i] = INF; }
+        if (contig) bt_row_pass<true>(taddr_row, row_live, s1, s2v);
+        else bt_row_pass<false>(taddr_row, row_live, s1, s2v);
+#pragma unroll
+        for (int i = 0; i < BT_S; ++i) slist[i * BT_ROWS + r] = row_live ? s32 + s1[i] : INF;
+        // rigorous |w' - v| for this row (v = the exact float64 score):
+        //   3xTF32 (B rounding, lo*lo dropped): 2^-21 sum|a||b|; fp32 accumulation
+        //   (steps * 2^-22 of the running sum); residual drift dlt (fp32 difference
+        //   u24 + hi/lo truncation 2^-22 per stage); embedded index (16 ulp) and the
+        //   fp32 score arithmetic; doubled for safety
         if (row_live) {
-            const int vv = rv;
-            const double xx = xnorm[vv] * xnorm[vv];
+            const double xx = xnorm[rv] * xnorm[rv];
             const double sl = score[cur * BT_ROWS + r];
             const double rn = sqrt(fmax(sl + xx, 0.0) * (1.0 + 1e-9)) + 1e-30;
-            const double cm = a.cmax[m];
-            // stored residual = tf32 hi + lo of the fp32 difference: u24 + 2^-22 per stage
-            const double dlt = (m + 1) * (u24 + u22) * (xnorm[vv] + m * cmax_all);
-            const double steps = 3.0 * ((D + 7) / 8) + 7.0;
-            const double e_dot = (steps * u22 * (rn + dlt) + dlt) * cm;
-            const double E = 2.0 * (2.0 * e_dot + 4.0 * u24 * (fabs(sl) + cm * cm + 2.0 * (rn + dlt) * cm)) + 1e-30;
+            const double cm = a.cmax[2 * m], cm2 = a.cmax[2 * m + 1];
+            const double dlt = (m + 1) * (u24 + u22) * (xnorm[rv] + m * cmax_all);
+            const double mag = 2.0 * (rn + dlt) * cm + cm2;
+            const double E = 2.0 * ((2.0 * u22 + steps * u22) * mag + 2.0 * dlt * cm +
+                                    (u19 + 2.0 * u24) * (fabs(sl) + mag)) + 1e-30;
             erow[r] = (float)(E * (1.0 + 1e-6));
         } else {
             erow[r] = 0.f;
         }
-        rarg[r] = i1;
         if (tid < V) qcnt[tid] = 0;
         __syncthreads();
-        // ---- per vector (one warp each): threshold = width-th smallest of the rows'
-        // sorted slice minima by a multiway merge with redux.sync; limit adds E
+        // ---- per vector (warp each): tau' = width-th smallest slice minimum
         for (int vv = warp; vv < V; vv += BT_T / 32) {
             if (v0 + vv >= a.n || vbad[vv]) continue;
-            const int lane = tid & 31;
-            float thr = __int_as_float(0x7f800000);
-            if (width < tot_ll && (long long)live * BT_S >= width) {
-                int ptr[BT_ROWS / 32];
-                float head[BT_ROWS / 32];
-#pragma unroll
-                for (int j = 0; j < BT_ROWS / 32; ++j) {
-                    const int l = lane + 32 * j;
-                    ptr[j] = 0;
-                    head[j] = l < live ? rmin[vv * cap + l] : __int_as_float(0x7f800000);
+            float thr = INF;
+            const int items = live * BT_S;
+            if (width < tot_ll && items >= width) {
+                // lane's items: e = lane + 32 j -> (slice e / live, row e % live)
+                float best = INF;
+                int bpos = -1;
+                for (int e = lane; e < items; e += 32) {
+                    const float x = slist[(e / live) * BT_ROWS + vv * cap + e % live];
+                    if (x < best) { best = x; bpos = e; }
                 }
                 for (int step = 0; step < width; ++step) {
-                    float mine = head[0];
-#pragma unroll
-                    for (int j = 1; j < BT_ROWS / 32; ++j) mine = fminf(mine, head[j]);
-                    const unsigned key = __reduce_min_sync(0xffffffffu, bt_key(mine));
+                    const unsigned key = __reduce_min_sync(0xffffffffu, bt_key(best));
                     thr = bt_unkey(key);
-                    const unsigned own = __ballot_sync(0xffffffffu, bt_key(mine) == key);
-                    bool adv = lane == __ffs(own) - 1;
-#pragma unroll
-                    for (int j = 0; j < BT_ROWS / 32; ++j) {
-                        const bool hit = adv && head[j] == mine;
-                        adv = adv && !hit;
-                        const int pj = ptr[j] + (hit ? 1 : 0);
-                        const float nx = (hit && pj < BT_S) ? rmin[pj * BT_ROWS + vv * cap + lane + 32 * j]
-                                                            : __int_as_float(0x7f800000);
-                        ptr[j] = pj;
-                        head[j] = hit ? nx : head[j];
+                    const unsigned own = __ballot_sync(0xffffffffu, bt_key(best) == key);
+                    if (lane == __ffs(own) - 1 && bpos >= 0) {
+                        slist[(bpos / live) * BT_ROWS + vv * cap + bpos % live] = INF;
+                        best = INF;
+                        bpos = -1;
+                        for (int e = lane; e < items; e += 32) {
+                            const float x = slist[(e / live) * BT_ROWS + vv * cap + e % live];
+                            if (x < best) { best = x; bpos = e; }
+                        }
                     }
                     __syncwarp();
                 }
@@ -439,34 +444,47 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
             for (int l = lane; l < live; l += 32) emax = fmaxf(emax, erow[vv * cap + l]);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
-            // row l keeps candidates with v' <= tau' + E_max + E_l (E_l added per row)
+            // row l keeps candidates with w' <= tau' + E_max + E_l
             if (lane == 0) vlim[vv] = (double)thr + (double)emax;
         }
         __syncthreads();
-        // ---- candidates: rows whose second minimum is above the limit offer their
-        // minimum; the others rescan their row from TMEM
+        // ---- queue: slice minima under the limit; slices with two or more rescan
         {
             const double lim = row_live ? vlim[rv] + (double)erow[r] : -1.0;
-            const float limf = (lim >= 3.0e38) ? __int_as_float(0x7f800000)
-                                               : __fadd_ru((float)lim, fabsf((float)lim) * 1e-6f);
-            const bool multi = row_live && m2 <= limf;
-            if (row_live && m1 <= limf && !multi) {
-                const int slot = atomicAdd(&qcnt[rv], 1);
-                if (slot < BT_QV) qflat[rv * BT_QV + slot] = i1;
+            const float limf = (lim >= 3.0e38) ? INF : __fadd_ru((float)lim, fabsf((float)lim) * 1e-6f);
+            uint32_t flag = 0;
+            if (row_live) {
+#pragma unroll
+                for (int i = 0; i < BT_S; ++i) {
+                    if (s32 + s1[i] <= limf) {
+                        if (s32 + s2v[i] <= limf) {
+                            flag |= 1u << i;
+                        } else {
+                            const int e = (int)(__float_as_uint(s1[i]) & 15u);
+                            const int k = contig ? 16 * i + e : 16 * e + i;
+                            if (k < K) {
+                                const int slot = atomicAdd(&qcnt[rv], 1);
+                                if (slot < QV) qflat[rv * QV + slot] = rl * K + k;
+                            }
+                        }
+                    }
+                }
             }
-            // the TMEM rescan is warp-collective: every lane runs it when any lane needs it
-            const bool any_multi = __any_sync(0xffffffffu, multi);
-            if (any_multi) {
-                for (int c0 = 0; c0 < N; c0 += 32) {
+#pragma unroll
+            for (int c = 0; c < BT_N / 32; ++c) {
+                // contiguous slices 2c, 2c+1 live in chunk c; interleaved slices in every chunk < K
+                const uint32_t fc = contig ? (flag >> (2 * c)) & 3u : (32 * c < K ? flag : 0u);
+                if (__any_sync(0xffffffffu, fc != 0)) {
                     float v[32];
-                    bt_ld32(taddr_row + c0, v);
-                    if (multi) {
+                    bt_ld32(taddr_row + 32 * c, v);
+                    if (fc) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i) {
-                            const float w = s32 + fmaf(-2.f, v[i], sq32s[c0 + i]);
-                            if (c0 + i < K && w <= limf) {
+                            const int k = 32 * c + i;
+                            const uint32_t bit = contig ? (fc >> (i >> 4)) & 1u : (fc >> (i & 15)) & 1u;
+                            if (bit && k < K && s32 + v[i] <= limf) {
                                 const int slot = atomicAdd(&qcnt[rv], 1);
-                                if (slot < BT_QV) qflat[rv * BT_QV + slot] = rl * K + c0 + i;
+                                if (slot < QV) qflat[rv * QV + slot] = rl * K + k;
                             }
                         }
                     }
@@ -477,44 +495,24 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
         __syncthreads();
         // a queue that overflowed, or that holds fewer than width entries (cannot
         // happen with a valid bound; kept as a guard), sends the vector to the exact path
-        if (tid < V && (qcnt[tid] > BT_QV || qcnt[tid] < width) && !vbad[tid]) {
-            vbad[tid] = 1;  // too many near-boundary candidates: the host re-encodes this vector
-            if (v0 + tid < a.n) a.bad[v0 + tid] = 1;
+        if (tid < V && v0 + tid < a.n && !vbad[tid] && (qcnt[tid] > QV || qcnt[tid] < width)) {
+            vbad[tid] = 1;
+            a.bad[v0 + tid] = 1;
         }
         __syncthreads();
-        // ---- exact float64 values of every queued candidate (round robin over threads)
+        // ---- exact float64 value of every queued candidate (round robin over threads)
         {
             const uint8_t* pcodes = codes + cur * BT_ROWS * M;
             int total_q = 0;
-            for (int vv = 0; vv < V; ++vv) total_q += std::min(qcnt[vv], BT_QV);
-            // flatten (vector, slot) pairs
-            for (int idx = tid; idx < V * BT_QV; idx += BT_T) {
-                const int vv = idx / BT_QV, slot = idx % BT_QV;
+            for (int vv = 0; vv < V; ++vv) total_q += vbad[vv] ? 0 : qcnt[vv];
+            for (int idx = tid; idx < V * QV; idx += BT_T) {
+                const int vv = idx / QV, slot = idx % QV;
                 if (v0 + vv >= a.n || vbad[vv] || slot >= qcnt[vv]) continue;
                 const int flat = qflat[idx];
                 const int l = flat / K, k = flat % K;
                 const long long gv = v0 + vv;
-                // x in float64 read straight from the f32 input
-                const float* xr = a.X + gv * a.ldx;
-                const double* crow = a.cw64 + ((long long)m * K + k) * D;
-                double tot = 0.0;
-                bool first = true;
-                int d = 0;
-                while (d < D) {
-                    const int e = d + (int)blas_block_len(D - d);
-                    double acc = 0.0;
-                    for (; d + 8 <= e; d += 8) {
-                        double xv[8], cv[8];
-#pragma unroll
-                        for (int u2 = 0; u2 < 8; ++u2) { xv[u2] = (double)xr[d + u2]; cv[u2] = crow[d + u2]; }
-#pragma unroll
-                        for (int u2 = 0; u2 < 8; ++u2) acc = __fma_rn(xv[u2], cv[u2], acc);
-                    }
-                    for (; d < e; ++d) acc = __fma_rn((double)xr[d], crow[d], acc);
-                    tot = first ? acc : dadd(tot, acc);
-                    first = false;
-                }
-                const double t = dsub(a.sq[m * K + k], dmul(2.0, tot));
+                const double dot = bt_exact_dot(a.X + gv * a.ldx, a.cw + ((long long)m * K + k) * D, D, xv4);
+                const double t = dsub(a.sq[m * K + k], dmul(2.0, dot));
                 double cross = 0.0;
                 const uint8_t* pcv = pcodes + (vv * cap + l) * M;
                 for (int j = 0; j < m; ++j) cross = dadd(cross, a.P[(((long long)j * M + m) * K + pcv[j]) * K + k]);
@@ -523,26 +521,21 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
             n_exact += (tid == 0) ? (unsigned long long)total_q : 0ULL;
         }
         __syncthreads();
-        // ---- exact top-width per vector by (value, flat) rank, then child slots in flat order
-        for (int idx = tid; idx < V * BT_QV; idx += BT_T) {
-            const int vv = idx / BT_QV, slot = idx % BT_QV;
+        // ---- exact top-width per vector by (value, flat) rank
+        for (int idx = tid; idx < V * QV; idx += BT_T) {
+            const int vv = idx / QV, slot = idx % QV;
             const int nq = qcnt[vv];
             if (v0 + vv >= a.n || vbad[vv] || slot >= nq) continue;
             const double x = qval[idx];
             const int f = qflat[idx];
             int rank = 0;
-            for (int j = 0; j < nq; ++j) rank += lex_less(qval[vv * BT_QV + j], qflat[vv * BT_QV + j], x, f);
-            if (rank < width) {
-                // position among the selected by flat index = rank of f among selected flats;
-                // computed in the next pass, store by value-rank first
-                sel[vv * cap + rank] = idx;
-            }
+            for (int j = 0; j < nq; ++j) rank += lex_less(qval[vv * QV + j], qflat[vv * QV + j], x, f);
+            if (rank < width) sel[vv * cap + rank] = idx;
         }
         __syncthreads();
+        // ---- children in flat order (thread per child row)
         {
-            // child slot for each selected (thread per child row): order by flat
-            const int rr = tid;
-            const int vv = rr / cap, slotv = rr % cap;
+            const int vv = r / cap, slotv = r % cap;
             const int nxt = cur ^ 1;
             if (vv < V && slotv < width && v0 + vv < a.n && !vbad[vv]) {
                 const int idx = sel[vv * cap + slotv];
@@ -555,24 +548,22 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
                 for (int j = 0; j < m; ++j) cc[j] = pp[j];
                 cc[m] = (uint8_t)kk;
                 score[nxt * BT_ROWS + vv * cap + pos] = qval[idx];
-                rarg[vv * cap + pos] = (parent << 16) | kk;  // reuse: (parent, k) of child row
+                rarg[vv * cap + pos] = (parent << 16) | kk;
             }
         }
         __syncthreads();
-        // ---- child residual images r = (hi + lo)_parent - c_m(k), split again (fp32;
-        // the bound covers both roundings).  Thread per child row.
+        // ---- child residual images r = (hi + lo)_parent - c_m(k), split again
+        // (fp32; the bound covers both roundings); column D stays 1
         if (m + 1 < M) {
             const int nxt = cur ^ 1;
-            const int rr = tid;
-            const int vv = rr / cap, slotv = rr % cap;
+            const int vv = r / cap, slotv = r % cap;
             if (vv < V && slotv < width && v0 + vv < a.n && !vbad[vv]) {
-                const int pk = rarg[rr];
+                const int pk = rarg[r];
                 const int parent = pk >> 16, kk = pk & 0xFFFF;
                 const float* src = img + (size_t)cur * nch * 2 * A_EL;
                 float* dst = img + (size_t)nxt * nch * 2 * A_EL;
                 const float* cwr = a.cw + ((long long)m * K + kk) * D;
                 const int pr = vv * cap + parent;
-                const bool vec4 = (D & 3) == 0;
 #pragma unroll 4
                 for (int ch = 0; ch < nch; ++ch) {
 #pragma unroll
@@ -582,7 +573,7 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
                         const float4 h4 = *reinterpret_cast<const float4*>(src + (size_t)ch * 2 * A_EL + po);
                         const float4 l4 = *reinterpret_cast<const float4*>(src + (size_t)ch * 2 * A_EL + A_EL + po);
                         float c[4];
-                        if (vec4 && k + 3 < D) {
+                        if (xv4 && k + 3 < D) {
                             const float4 t = __ldg(reinterpret_cast<const float4*>(cwr + k));
                             c[0] = t.x; c[1] = t.y; c[2] = t.z; c[3] = t.w;
                         } else {
@@ -590,7 +581,7 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
                             for (int u = 0; u < 4; ++u) c[u] = k + u < D ? cwr[k + u] : 0.f;
                         }
                         float x4[4] = {(h4.x + l4.x) - c[0], (h4.y + l4.y) - c[1], (h4.z + l4.z) - c[2], (h4.w + l4.w) - c[3]};
-                        bt_store_split(dst + (size_t)ch * 2 * A_EL, bt_off(rr, 4 * c4) >> 2, x4);
+                        bt_store_split(dst + (size_t)ch * 2 * A_EL, bt_off(r, 4 * c4) >> 2, x4);
                     }
                 }
             }
@@ -600,7 +591,6 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
         live = width;
     }
 
-    // ---- overflowed vectors are left to the host fallback (flag via stats=-1 code)
     // final pick: first minimum among the beams in code order
     if (tid < V && v0 + tid < a.n && !vbad[tid]) {
         const int vv = tid;
@@ -608,8 +598,8 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
         double bv = __longlong_as_double(0x7ff0000000000000ULL);
         int bi = 0;
         for (int l = 0; l < live; ++l) {
-            const double s = score[cur * BT_ROWS + vv * cap + l];
-            if (s < bv) { bv = s; bi = l; }
+            const double sc = score[cur * BT_ROWS + vv * cap + l];
+            if (sc < bv) { bv = sc; bi = l; }
         }
         const uint8_t* best = codes + (cur * BT_ROWS + vv * cap + bi) * M;
         for (int j = 0; j < M; ++j) {
@@ -641,30 +631,23 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
     }
 }
 
-
-// codebook side inputs: fp64 copy, fp32 norms, per-dictionary max norm
-__global__ void tc_side_prep_kernel(const float* __restrict__ cw, const double* __restrict__ sq, int M, int K, int D,
-                                    double* __restrict__ cw64, float* __restrict__ sq32, double* __restrict__ cmax) {
-    const long long total = (long long)M * K * D;
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x)
-        cw64[e] = (double)cw[e];
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)M * K;
-         e += (long long)gridDim.x * blockDim.x)
-        sq32[e] = (float)sq[e];
-    if (blockIdx.x == 0) {
-        __shared__ double red[256];
-        for (int m = 0; m < M; ++m) {
-            double c = 0.0;
-            for (int k = threadIdx.x; k < K; k += blockDim.x) c = fmax(c, sqrt(sq[m * K + k]));
-            red[threadIdx.x] = c;
-            __syncthreads();
-            for (int s2 = blockDim.x / 2; s2 > 0; s2 >>= 1) {
-                if (threadIdx.x < s2) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s2]);
-                __syncthreads();
-            }
-            if (threadIdx.x == 0) cmax[m] = red[0] * (1.0 + 1e-12);
+// per dictionary: max ||c|| and max ||c||^2 (from the exact einsum norms)
+__global__ void tc_side_prep_kernel(const double* __restrict__ sq, int M, int K, double* __restrict__ cmax) {
+    __shared__ double red[256];
+    for (int m = 0; m < M; ++m) {
+        double c = 0.0;
+        for (int k = threadIdx.x; k < K; k += blockDim.x) c = fmax(c, sq[m * K + k]);
+        red[threadIdx.x] = c;
+        __syncthreads();
+        for (int s2 = blockDim.x / 2; s2 > 0; s2 >>= 1) {
+            if (threadIdx.x < s2) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s2]);
             __syncthreads();
         }
+        if (threadIdx.x == 0) {
+            cmax[2 * m] = sqrt(red[0]) * (1.0 + 1e-12);
+            cmax[2 * m + 1] = red[0] * (1.0 + 1e-12);
+        }
+        __syncthreads();
     }
 }
 
@@ -704,13 +687,13 @@ int launch_encode_tc(const float* X, long long n, long long ldx, int D, const fl
     const int cap = (int)std::min((long long)L, capll);
     if (cap > BT_ROWS || n <= 0) return n <= 0 ? 0 : 1;
     const int V = BT_ROWS / cap;
-    const int nch = (D + BT_BK - 1) / BT_BK;
+    const int nch = (D + 1 + BT_BK - 1) / BT_BK;   // + the norm column
     // a single first-stage row cannot cover beams wider than 16: then all K go to the exact pass
     const int qv = cap > BT_S ? std::max(3 * cap + 8, K) : 3 * cap + 8;
     size_t smem = sizeof(float) * (BT_NST * 2 * BT_ROWS * BT_BK + BT_NST * 2 * BT_N * BT_BK);
     smem += sizeof(double) * (2 * BT_ROWS + (size_t)V * qv + 2 * V);
-    smem += sizeof(float) * (size_t)BT_S * BT_ROWS + sizeof(int) * BT_ROWS + ((2 * BT_ROWS * (size_t)M + 15) & ~size_t(15));
-    smem += sizeof(int) * ((size_t)V * qv + V + BT_ROWS) + sizeof(float) * BT_N + sizeof(int) * V +
+    smem += sizeof(float) * (size_t)BT_S * BT_ROWS + sizeof(int) * BT_ROWS + 2 * BT_ROWS * (size_t)M;
+    smem += sizeof(int) * ((size_t)V * qv + V + BT_ROWS) + sizeof(int) * V +
             sizeof(float) * BT_ROWS;
     if (smem > 227 * 1024) return 1;
     int dev = 0, sms = 148;
@@ -731,9 +714,7 @@ int launch_encode_tc(const float* X, long long n, long long ldx, int D, const fl
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
     const size_t o_bg = take(sizeof(float) * (size_t)M * nch * 2 * BT_N * BT_BK);
-    const size_t o_c64 = take(sizeof(double) * (size_t)M * K * D);
-    const size_t o_sq32 = take(sizeof(float) * (size_t)M * K);
-    const size_t o_cmax = take(sizeof(double) * M);
+    const size_t o_cmax = take(sizeof(double) * 2 * M);
     const size_t o_rb = take(sizeof(float) * (size_t)grid * 2 * nch * 2 * BT_ROWS * BT_BK);
     const size_t o_bad = take(sizeof(int) * (size_t)n);
     const size_t o_lst = take(sizeof(int) * (size_t)n);
@@ -741,22 +722,20 @@ int launch_encode_tc(const float* X, long long n, long long ldx, int D, const fl
     char* base = (char*)scratch(10, off, s);
     if (!base) return fail_cuda(cudaErrorMemoryAllocation, "encode_tc scratch");
     float* Bg = (float*)(base + o_bg);
-    double* cw64 = (double*)(base + o_c64);
-    float* sq32 = (float*)(base + o_sq32);
     double* cmax = (double*)(base + o_cmax);
     int* bad = (int*)(base + o_bad);
     int* cnt = (int*)(base + o_cnt);
     {
         ProfScope ps0("encode_tc_prep", s);
-        cb_tf32_prep_kernel<<<grid_for((long long)M * nch * BT_N * BT_BK, 256, 4096), 256, 0, s>>>(cw, M, K, D, nch, Bg);
+        cb_tf32_prep_kernel<<<grid_for((long long)M * nch * BT_N * BT_BK, 256, 4096), 256, 0, s>>>(cw, sq, M, K, D, nch, Bg);
         DA_CHECK_LAUNCH("cb_tf32_prep_kernel");
-        tc_side_prep_kernel<<<grid_for((long long)M * K * D, 256, 2048), 256, 0, s>>>(cw, sq, M, K, D, cw64, sq32, cmax);
+        tc_side_prep_kernel<<<1, 256, 0, s>>>(sq, M, K, cmax);
         DA_CHECK_LAUNCH("tc_side_prep_kernel");
         DA_CUDA(cudaMemsetAsync(bad, 0, sizeof(int) * (size_t)n + 16, s));
     }
     BeamTcArgs a{};
-    a.X = X; a.n = n; a.ldx = ldx; a.D = D; a.cw = cw; a.cw64 = cw64; a.M = M; a.K = K; a.L = L; a.cap = cap;
-    a.sq = sq; a.sq32 = sq32; a.P = P; a.Bg = Bg; a.cmax = cmax; a.img = (float*)(base + o_rb);
+    a.X = X; a.n = n; a.ldx = ldx; a.D = D; a.cw = cw; a.M = M; a.K = K; a.L = L; a.cap = cap;
+    a.sq = sq; a.P = P; a.Bg = Bg; a.cmax = cmax; a.img = (float*)(base + o_rb);
     a.codes_out = codes_out; a.code_bytes = code_bytes; a.ldcodes = ldcodes; a.err_out = err_out; a.stats = stats;
     a.nch = nch; a.qv = qv; a.bad = bad;
     {
