@@ -248,7 +248,8 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
     double* qval = reinterpret_cast<double*>(p); p += sizeof(double) * V * QV;          // [V][QV]
     double* vlim = reinterpret_cast<double*>(p); p += sizeof(double) * V;               // [V]
     double* xnorm = reinterpret_cast<double*>(p); p += sizeof(double) * V;              // [V]
-    float* slist = reinterpret_cast<float*>(p); p += sizeof(float) * BT_S * BT_ROWS;   // [S][rows] slice minima
+    p = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+    float* slist = reinterpret_cast<float*>(p); p += sizeof(float) * BT_S * BT_ROWS;   // [rows][S] slice minima
     int* rarg = reinterpret_cast<int*>(p); p += sizeof(int) * BT_ROWS;                  // (parent, k) per child
     int* qflat = reinterpret_cast<int*>(p); p += sizeof(int) * V * QV;                  // [V][QV]
     int* qcnt = reinterpret_cast<int*>(p); p += sizeof(int) * V;                        // [V]
@@ -390,7 +391,14 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
         if (contig) bt_row_pass<true>(taddr_row, row_live, s1, s2v);
         else bt_row_pass<false>(taddr_row, row_live, s1, s2v);
 #pragma unroll
-        for (int i = 0; i < BT_S; ++i) slist[i * BT_ROWS + r] = row_live ? s32 + s1[i] : INF;
+        for (int i = 0; i < BT_S; i += 4) {
+            float4 t4;
+            t4.x = row_live ? s32 + s1[i] : INF;
+            t4.y = row_live ? s32 + s1[i + 1] : INF;
+            t4.z = row_live ? s32 + s1[i + 2] : INF;
+            t4.w = row_live ? s32 + s1[i + 3] : INF;
+            *reinterpret_cast<float4*>(slist + r * BT_S + i) = t4;   // [row][slice]
+        }
         // rigorous |w' - v| for this row (v = the exact float64 score):
         //   3xTF32 (B rounding, lo*lo dropped): 2^-21 sum|a||b|; fp32 accumulation
         //   (steps * 2^-22 of the running sum); residual drift dlt (fp32 difference
@@ -417,27 +425,45 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
             float thr = INF;
             const int items = live * BT_S;
             if (width < tot_ll && items >= width) {
-                // lane's items: e = lane + 32 j -> (slice e / live, row e % live)
-                float best = INF;
-                int bpos = -1;
-                for (int e = lane; e < items; e += 32) {
-                    const float x = slist[(e / live) * BT_ROWS + vv * cap + e % live];
-                    if (x < best) { best = x; bpos = e; }
-                }
-                for (int step = 0; step < width; ++step) {
-                    const unsigned key = __reduce_min_sync(0xffffffffu, bt_key(best));
-                    thr = bt_unkey(key);
-                    const unsigned own = __ballot_sync(0xffffffffu, bt_key(best) == key);
-                    if (lane == __ffs(own) - 1 && bpos >= 0) {
-                        slist[(bpos / live) * BT_ROWS + vv * cap + bpos % live] = INF;
-                        best = INF;
-                        bpos = -1;
-                        for (int e = lane; e < items; e += 32) {
-                            const float x = slist[(e / live) * BT_ROWS + vv * cap + e % live];
-                            if (x < best) { best = x; bpos = e; }
+                // the vector's live rows are contiguous in slist: items e = row * S + slice
+                float* it0 = slist + vv * cap * BT_S;
+                if (items <= 32 * 8) {
+                    float it[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) it[j] = lane + 32 * j < items ? it0[lane + 32 * j] : INF;
+                    for (int step = 0; step < width; ++step) {
+                        float best = it[0];
+#pragma unroll
+                        for (int j = 1; j < 8; ++j) best = fminf(best, it[j]);
+                        const unsigned key = __reduce_min_sync(0xffffffffu, bt_key(best));
+                        thr = bt_unkey(key);
+                        const unsigned own = __ballot_sync(0xffffffffu, bt_key(best) == key);
+                        bool rm = lane == __ffs(own) - 1;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const bool h = rm && it[j] == best;
+                            it[j] = h ? INF : it[j];
+                            rm = rm && !h;
                         }
                     }
-                    __syncwarp();
+                } else {
+                    float best = INF;
+                    int bpos = -1;
+                    for (int e = lane; e < items; e += 32)
+                        if (it0[e] < best) { best = it0[e]; bpos = e; }
+                    for (int step = 0; step < width; ++step) {
+                        const unsigned key = __reduce_min_sync(0xffffffffu, bt_key(best));
+                        thr = bt_unkey(key);
+                        const unsigned own = __ballot_sync(0xffffffffu, bt_key(best) == key);
+                        if (lane == __ffs(own) - 1 && bpos >= 0) {
+                            it0[bpos] = INF;
+                            best = INF;
+                            bpos = -1;
+                            for (int e = lane; e < items; e += 32)
+                                if (it0[e] < best) { best = it0[e]; bpos = e; }
+                        }
+                        __syncwarp();
+                    }
                 }
             }
             float emax = 0.f;
@@ -692,7 +718,7 @@ int launch_encode_tc(const float* X, long long n, long long ldx, int D, const fl
     const int qv = cap > BT_S ? std::max(3 * cap + 8, K) : 3 * cap + 8;
     size_t smem = sizeof(float) * (BT_NST * 2 * BT_ROWS * BT_BK + BT_NST * 2 * BT_N * BT_BK);
     smem += sizeof(double) * (2 * BT_ROWS + (size_t)V * qv + 2 * V);
-    smem += sizeof(float) * (size_t)BT_S * BT_ROWS + sizeof(int) * BT_ROWS + 2 * BT_ROWS * (size_t)M;
+    smem += 16 + sizeof(float) * (size_t)BT_S * BT_ROWS + sizeof(int) * BT_ROWS + 2 * BT_ROWS * (size_t)M;
     smem += sizeof(int) * ((size_t)V * qv + V + BT_ROWS) + sizeof(int) * V +
             sizeof(float) * BT_ROWS;
     if (smem > 227 * 1024) return 1;
