@@ -304,7 +304,7 @@ int da_encode(const void* X, int x_f32, int64_t n, int64_t ldx, int D, const flo
     if (x_f32 && g_encode_mode == 3) {
         int rc = launch_encode_tc((const float*)X, n, ldx, D, cw, M, K, L, sq, P, codes, code_bytes, ldcodes, err,
                                   g_encode_stats, STREAM(stream));
-        if (rc <= 0) return rc;  // > 0: shape outside the tensor-core encoder
+        if (rc != kNotApplicable) return rc;  // done, or a real failure
         cudaGetLastError();
     }
     if (x_f32 && g_encode_mode != 1) {

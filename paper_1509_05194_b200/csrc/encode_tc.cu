@@ -45,9 +45,12 @@ namespace {
 constexpr int BT_ROWS = 128;
 constexpr int BT_N = 256;
 constexpr int BT_BK = 8;
-constexpr int BT_NST = 3;  // shared-memory ring depth (k-chunks in flight)
-constexpr int BT_T = 128;
-constexpr int BT_S = 16;  // column slices per row for the beam threshold
+constexpr int BT_NST = 6;  // shared-memory ring depth (k-chunks in flight)
+constexpr int BT_T = 256;   // two threads per row: column halves
+#ifndef BT_PREFETCH
+#define BT_PREFETCH 1
+#endif
+constexpr int BT_S = 16;  // column slices per half row for the beam threshold (32 per row)
 }  // namespace
 
 __device__ __forceinline__ uint32_t bt_smem_u32(const void* p) {
@@ -145,6 +148,38 @@ __device__ __forceinline__ double bt_exact_dot(const float* __restrict__ x, cons
     return tot;
 }
 
+// Same value for D <= 384 (one BLAS k-block) with x already in float64 (shared
+// memory) and the codeword row streamed from fp32 global memory in prefetched
+// 32-wide batches, so the FMA chain is not serialised behind each load.
+__device__ __forceinline__ double bt_exact_dot_s(const double* __restrict__ xs, const float* __restrict__ c, int D) {
+    double acc = 0.0;
+    float4 cur[8], nxt[8];
+    const int D32 = D & ~31;
+    if (D32 > 0) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) cur[u] = __ldg(reinterpret_cast<const float4*>(c) + u);
+    }
+    for (int d0 = 0; d0 < D32; d0 += 32) {
+        if (d0 + 32 < D32) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) nxt[u] = __ldg(reinterpret_cast<const float4*>(c + d0 + 32) + u);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const double2 x01 = *reinterpret_cast<const double2*>(xs + d0 + 4 * u);
+            const double2 x23 = *reinterpret_cast<const double2*>(xs + d0 + 4 * u + 2);
+            acc = __fma_rn(x01.x, (double)cur[u].x, acc);
+            acc = __fma_rn(x01.y, (double)cur[u].y, acc);
+            acc = __fma_rn(x23.x, (double)cur[u].z, acc);
+            acc = __fma_rn(x23.y, (double)cur[u].w, acc);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
+    }
+    for (int d = D32; d < D; ++d) acc = __fma_rn(xs[d], (double)c[d], acc);
+    return acc;
+}
+
 // Codebook -> per (dictionary, k-chunk) tf32 hi/lo images of B = [-2c, ||c||^2],
 // sentinel 1e30 in the norm column of the padding rows k >= K.
 __global__ void cb_tf32_prep_kernel(const float* __restrict__ cw, const double* __restrict__ sq, int M, int K, int D,
@@ -196,21 +231,21 @@ __device__ __forceinline__ float bt_unkey(unsigned k) {
 }
 
 
-// One row's pass over the 256 TMEM columns: per slice the smallest (s1) and
+// One half row's pass over 128 TMEM columns: per slice the smallest (s1) and
 // second smallest (s2) value, the slice-local position embedded in the 4 low
-// mantissa bits of s1/s2.  CONTIG: slice = column / 16 (position = column % 16);
-// else slice = column % 16 (position = column / 16).  Loads are warp-collective.
+// mantissa bits.  CONTIG: slice = column / 8 (position = column % 8); else
+// slice = column % 16 (position = column / 16).  Loads are warp-collective.
 template <bool CONTIG>
 __device__ __forceinline__ void bt_row_pass(uint32_t taddr_row, bool row_live, float* s1, float* s2) {
 #pragma unroll
-    for (int c = 0; c < BT_N / 32; ++c) {
+    for (int c = 0; c < 4; ++c) {
         float v[32];
         bt_ld32(taddr_row + 32 * c, v);
         if (row_live) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
-                const int sl = CONTIG ? 2 * c + (i >> 4) : (i & 15);
-                const uint32_t pos = CONTIG ? (uint32_t)(i & 15) : (uint32_t)(2 * c + (i >> 4));
+                const int sl = CONTIG ? 4 * c + (i >> 3) : (i & 15);
+                const uint32_t pos = CONTIG ? (uint32_t)(i & 7) : (uint32_t)(2 * c + (i >> 4));
                 const float w = __uint_as_float((__float_as_uint(v[i]) & ~15u) | pos);
                 s2[sl] = fminf(s2[sl], fmaxf(s1[sl], w));
                 s1[sl] = fminf(s1[sl], w);
@@ -218,6 +253,16 @@ __device__ __forceinline__ void bt_row_pass(uint32_t taddr_row, bool row_live, f
         }
     }
 }
+
+// phase timing (DA_DEBUG): thread 0 accumulates clock deltas between phase marks
+#define BT_MARK(i)                                                   \
+    do {                                                             \
+        if (a.prof && tid == 0) {                                    \
+            const long long _t = clock64();                          \
+            prof_acc[i] += _t - prof_t;                              \
+            prof_t = _t;                                             \
+        }                                                            \
+    } while (0)
 
 struct BeamTcArgs {
     const float* X; long long n; long long ldx; int D;
@@ -233,9 +278,11 @@ struct BeamTcArgs {
     int nch;
     int qv;                // exact-recheck queue capacity per vector
     int* bad;              // [n] set to 1 when a vector overflowed its queue (host re-encodes it)
+    int xs_smem;           // 1: the group's vectors are staged in shared memory as float64
+    unsigned long long* prof;  // [12] per-phase clock sums (debug) or null
 };
 
-__global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
+__global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int A_EL = BT_ROWS * BT_BK, B_EL = BT_N * BT_BK;
     float* Abuf = reinterpret_cast<float*>(smem);        // [NST][hi,lo][A_EL]
@@ -249,14 +296,18 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
     double* vlim = reinterpret_cast<double*>(p); p += sizeof(double) * V;               // [V]
     double* xnorm = reinterpret_cast<double*>(p); p += sizeof(double) * V;              // [V]
     p = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
-    float* slist = reinterpret_cast<float*>(p); p += sizeof(float) * BT_S * BT_ROWS;   // [rows][S] slice minima
+    float* slist = reinterpret_cast<float*>(p); p += sizeof(float) * 2 * BT_S * BT_ROWS;   // [rows][2S] slice minima
     int* rarg = reinterpret_cast<int*>(p); p += sizeof(int) * BT_ROWS;                  // (parent, k) per child
     int* qflat = reinterpret_cast<int*>(p); p += sizeof(int) * V * QV;                  // [V][QV]
     int* qcnt = reinterpret_cast<int*>(p); p += sizeof(int) * V;                        // [V]
     int* sel = reinterpret_cast<int*>(p); p += sizeof(int) * BT_ROWS;                   // selected entry per child slot
     int* vbad = reinterpret_cast<int*>(p); p += sizeof(int) * V;                       // [V] overflow flags
     float* erow = reinterpret_cast<float*>(p); p += sizeof(float) * BT_ROWS;           // per-row bound E_l
-    uint8_t* codes = p;                                                                 // [2][rows][M] (K <= 256)
+    uint8_t* codes = p; p += 2 * BT_ROWS * M;                                           // [2][rows][M] (K <= 256)
+    p = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+    int* qoff = reinterpret_cast<int*>(p); p += sizeof(int) * (V + 1);                 // queue prefix offsets
+    p = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+    double* xs = reinterpret_cast<double*>(p);                                          // [V][D] when xs_smem
     __shared__ uint64_t full_bar[BT_NST], empty_bar[BT_NST], acc_bar;
     __shared__ uint32_t tmem_sh;
 
@@ -287,14 +338,18 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tmem_sh;
-    const uint32_t taddr_row = tmem + ((uint32_t)(warp * 32) << 16);
+    const int half = tid >> 7;                       // column half of this thread's row
+    const uint32_t taddr_row = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(half * 128);
     double cmax_all = 0.0;
     for (int j = 0; j < M; ++j) cmax_all = fmax(cmax_all, a.cmax[2 * j]);
     const double steps = 3.0 * nch * (BT_BK / 8) + 7.0;   // fp32 accumulations per TMEM value (+ slack)
-    // slices: 16 contiguous 16-column blocks when K fills the row, else column mod 16
+    // slices: contiguous 8-column blocks when K fills the row, else column mod 16
     const bool contig = K > 128;
 
+    long long prof_acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long prof_t = clock64();
     long long q = 0;        // k-chunks streamed (ring phases persist across groups)
+    int bpre = 0;           // chunks of the coming stage whose codeword copy already started (tid 0)
     uint32_t acc_phase = 0;
     unsigned long long n_exact = 0;
     const long long ngroups = (a.n + V - 1) / V;
@@ -323,6 +378,11 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
         vbad[tid] = 0;
     }
     for (int r = tid; r < BT_ROWS; r += BT_T) score[r] = 0.0;
+    if (a.xs_smem)
+        for (int e = tid; e < V * D; e += BT_T) {
+            const int v = e / D, d = e % D;
+            xs[e] = v0 + v < a.n ? (double)a.X[(v0 + v) * a.ldx + d] : 0.0;
+        }
 
     int cur = 0, live = 1;
     for (int m = 0; m < M; ++m) {
@@ -331,23 +391,34 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
         // residual images written by threads (generic proxy) are read by bulk copies (async proxy)
         asm volatile("fence.proxy.async.global;" ::: "memory");
         __syncthreads();
+        BT_MARK(0);
         // ---- GEMM: TMEM[row][k] = ||c_k||^2 - 2 r_row . c_k  (3xTF32, fp32 accumulate)
         if (tid == 0) {
             const float* Ag = img + (size_t)cur * nch * 2 * A_EL;
             const float* Bm = a.Bg + (size_t)m * nch * 2 * B_EL;
             constexpr uint32_t bytes_a = 2 * A_EL * sizeof(float), bytes_b = 2 * B_EL * sizeof(float);
-            auto issue = [&](int ch) {
-                const long long qq = q + ch;
+            // slot for chunk ch of a stage starting at q0: wait until its previous MMAs
+            // retired, announce A+B bytes, start the codeword (B) copy
+            auto issue_b = [&](long long q0, const float* Bsrc, int ch) {
+                const long long qq = q0 + ch;
                 const int st = (int)(qq % BT_NST);
                 const long long lap = qq / BT_NST;
                 if (lap >= 1) bt_wait(&empty_bar[st], (uint32_t)((lap - 1) & 1));
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bt_smem_u32(&full_bar[st])),
                              "r"(bytes_a + bytes_b)
                              : "memory");
-                bt_bulk(Abuf + st * 2 * A_EL, Ag + (size_t)ch * 2 * A_EL, bytes_a, &full_bar[st]);
-                bt_bulk(Bbuf + st * 2 * B_EL, Bm + (size_t)ch * 2 * B_EL, bytes_b, &full_bar[st]);
+                bt_bulk(Bbuf + st * 2 * B_EL, Bsrc + (size_t)ch * 2 * B_EL, bytes_b, &full_bar[st]);
             };
-            for (int ch = 0; ch < std::min(BT_NST - 1, nch); ++ch) issue(ch);
+            auto issue_a = [&](int ch) {
+                const int st = (int)((q + ch) % BT_NST);
+                bt_bulk(Abuf + st * 2 * A_EL, Ag + (size_t)ch * 2 * A_EL, bytes_a, &full_bar[st]);
+            };
+            const int first = std::min(BT_NST - 1, nch);
+            // the first chunks' codeword copies were started at the end of the previous stage
+            for (int ch = 0; ch < first; ++ch) {
+                if (ch >= bpre) issue_b(q, Bm, ch);
+                issue_a(ch);
+            }
             for (int ch = 0; ch < nch; ++ch) {
                 const long long qq = q + ch;
                 const int st = (int)(qq % BT_NST);
@@ -371,17 +442,31 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
                                      bt_smem_u32(&acc_bar))
                                  : "memory");
                 // refill the slot of the previous chunk (its MMAs were issued before this one's)
-                if (ch + BT_NST - 1 < nch) issue(ch + BT_NST - 1);
+                if (ch + BT_NST - 1 < nch) {
+                    issue_b(q, Bm, ch + BT_NST - 1);
+                    issue_a(ch + BT_NST - 1);
+                }
+            }
+            // start the next stage's first codeword copies now (they do not depend on
+            // the epilogue); only when a next stage exists on this CTA
+            bpre = 0;
+            const bool more = BT_PREFETCH && ((m + 1 < M) || (grp + gridDim.x < ngroups));
+            if (more) {
+                const float* Bn = a.Bg + (size_t)((m + 1) % M) * nch * 2 * B_EL;
+                for (int ch = 0; ch < first; ++ch) issue_b(q + nch, Bn, ch);
+                bpre = first;
             }
         }
+        __syncwarp();   // warp 0 reconverges before the warp-collective TMEM loads
         q += nch;
         bt_wait(&acc_bar, acc_phase);
+        BT_MARK(1);
         acc_phase ^= 1;
         asm volatile("tcgen05.fence::after_thread_sync;");
 
         // ---- row pass: per 16-column slice the smallest / second smallest value
         // (column index in the 4 low mantissa bits), branch-free
-        const int r = tid;
+        const int r = tid & (BT_ROWS - 1);
         const int rv = r / cap, rl = r % cap;
         const bool row_live = rv < V && rl < live && (v0 + rv) < a.n && !vbad[rv];
         const float s32 = row_live ? (float)score[cur * BT_ROWS + r] : 0.f;
@@ -390,21 +475,36 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
         for (int i = 0; i < BT_S; ++i) { s1[i] = INF; s2v[i] = INF; }
         if (contig) bt_row_pass<true>(taddr_row, row_live, s1, s2v);
         else bt_row_pass<false>(taddr_row, row_live, s1, s2v);
+        {
+            // this half row's slice minima, sorted ascending (bitonic network), as one
+            // list of the vector's 2*live lists: slist[(r * 2 + half) * S + i]
+            float srt[BT_S];
 #pragma unroll
-        for (int i = 0; i < BT_S; i += 4) {
-            float4 t4;
-            t4.x = row_live ? s32 + s1[i] : INF;
-            t4.y = row_live ? s32 + s1[i + 1] : INF;
-            t4.z = row_live ? s32 + s1[i + 2] : INF;
-            t4.w = row_live ? s32 + s1[i + 3] : INF;
-            *reinterpret_cast<float4*>(slist + r * BT_S + i) = t4;   // [row][slice]
+            for (int i = 0; i < BT_S; ++i) srt[i] = row_live ? s32 + s1[i] : INF;
+#pragma unroll
+            for (int k2 = 2; k2 <= BT_S; k2 <<= 1) {
+#pragma unroll
+                for (int j = k2 >> 1; j > 0; j >>= 1) {
+#pragma unroll
+                    for (int i = 0; i < BT_S; ++i) {
+                        const int l = i ^ j;
+                        if (l > i) {
+                            const float lo = fminf(srt[i], srt[l]), hi = fmaxf(srt[i], srt[l]);
+                            if ((i & k2) == 0) { srt[i] = lo; srt[l] = hi; } else { srt[i] = hi; srt[l] = lo; }
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < BT_S; i += 4)
+                *reinterpret_cast<float4*>(slist + (r * 2 + half) * BT_S + i) = make_float4(srt[i], srt[i + 1], srt[i + 2], srt[i + 3]);
         }
         // rigorous |w' - v| for this row (v = the exact float64 score):
         //   3xTF32 (B rounding, lo*lo dropped): 2^-21 sum|a||b|; fp32 accumulation
         //   (steps * 2^-22 of the running sum); residual drift dlt (fp32 difference
         //   u24 + hi/lo truncation 2^-22 per stage); embedded index (16 ulp) and the
         //   fp32 score arithmetic; doubled for safety
-        if (row_live) {
+        if (row_live && half == 0) {
             const double xx = xnorm[rv] * xnorm[rv];
             const double sl = score[cur * BT_ROWS + r];
             const double rn = sqrt(fmax(sl + xx, 0.0) * (1.0 + 1e-9)) + 1e-30;
@@ -414,55 +514,66 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
             const double E = 2.0 * ((2.0 * u22 + steps * u22) * mag + 2.0 * dlt * cm +
                                     (u19 + 2.0 * u24) * (fabs(sl) + mag)) + 1e-30;
             erow[r] = (float)(E * (1.0 + 1e-6));
-        } else {
+        } else if (half == 0) {
             erow[r] = 0.f;
         }
         if (tid < V) qcnt[tid] = 0;
         __syncthreads();
+        BT_MARK(2);
         // ---- per vector (warp each): tau' = width-th smallest slice minimum
         for (int vv = warp; vv < V; vv += BT_T / 32) {
             if (v0 + vv >= a.n || vbad[vv]) continue;
             float thr = INF;
-            const int items = live * BT_S;
-            if (width < tot_ll && items >= width) {
-                // the vector's live rows are contiguous in slist: items e = row * S + slice
-                float* it0 = slist + vv * cap * BT_S;
-                if (items <= 32 * 8) {
-                    float it[8];
+            const int nl = 2 * live;    // sorted lists of the vector (two per live row)
+            if (width < tot_ll && nl * BT_S >= width) {
+                const float* L0 = slist + (size_t)vv * cap * 2 * BT_S;
+                if (nl <= 32) {
+                    // one sorted list per lane, held in registers; the winner shifts its list
+                    float it[BT_S];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) it[j] = lane + 32 * j < items ? it0[lane + 32 * j] : INF;
+                    for (int i = 0; i < BT_S; i += 4) {
+                        float4 t4 = make_float4(INF, INF, INF, INF);
+                        if (lane < nl) t4 = *reinterpret_cast<const float4*>(L0 + lane * BT_S + i);
+                        it[i] = t4.x; it[i + 1] = t4.y; it[i + 2] = t4.z; it[i + 3] = t4.w;
+                    }
                     for (int step = 0; step < width; ++step) {
-                        float best = it[0];
+                        const unsigned mk = bt_key(it[0]);
+                        const unsigned key = __reduce_min_sync(0xffffffffu, mk);
+                        const unsigned own = __ballot_sync(0xffffffffu, mk == key);
+                        const bool adv = lane == __ffs(own) - 1;
 #pragma unroll
-                        for (int j = 1; j < 8; ++j) best = fminf(best, it[j]);
-                        const unsigned key = __reduce_min_sync(0xffffffffu, bt_key(best));
-                        thr = bt_unkey(key);
-                        const unsigned own = __ballot_sync(0xffffffffu, bt_key(best) == key);
-                        bool rm = lane == __ffs(own) - 1;
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const bool h = rm && it[j] == best;
-                            it[j] = h ? INF : it[j];
-                            rm = rm && !h;
-                        }
+                        for (int i = 0; i < BT_S - 1; ++i) it[i] = adv ? it[i + 1] : it[i];
+                        it[BT_S - 1] = adv ? INF : it[BT_S - 1];
+                        if (step == width - 1) thr = bt_unkey(key);
                     }
                 } else {
-                    float best = INF;
-                    int bpos = -1;
-                    for (int e = lane; e < items; e += 32)
-                        if (it0[e] < best) { best = it0[e]; bpos = e; }
+                    // lane j merges lists j, j+32, ...: head pointers in registers
+                    int ptr[BT_ROWS * 2 / 32];
+                    float head[BT_ROWS * 2 / 32];
+#pragma unroll
+                    for (int j = 0; j < BT_ROWS * 2 / 32; ++j) {
+                        ptr[j] = 0;
+                        head[j] = lane + 32 * j < nl ? L0[(lane + 32 * j) * BT_S] : INF;
+                    }
+                    const int nj = (nl + 31) / 32;
                     for (int step = 0; step < width; ++step) {
+                        float best = head[0];
+#pragma unroll
+                        for (int j = 1; j < BT_ROWS * 2 / 32; ++j)
+                            if (j < nj) best = fminf(best, head[j]);
                         const unsigned key = __reduce_min_sync(0xffffffffu, bt_key(best));
                         thr = bt_unkey(key);
                         const unsigned own = __ballot_sync(0xffffffffu, bt_key(best) == key);
-                        if (lane == __ffs(own) - 1 && bpos >= 0) {
-                            it0[bpos] = INF;
-                            best = INF;
-                            bpos = -1;
-                            for (int e = lane; e < items; e += 32)
-                                if (it0[e] < best) { best = it0[e]; bpos = e; }
+                        bool adv = lane == __ffs(own) - 1;
+#pragma unroll
+                        for (int j = 0; j < BT_ROWS * 2 / 32; ++j) {
+                            const bool hit = adv && j < nj && head[j] == best;
+                            adv = adv && !hit;
+                            const int pj = ptr[j] + (hit ? 1 : 0);
+                            const float nx = (hit && pj < BT_S) ? L0[(lane + 32 * j) * BT_S + pj] : INF;
+                            ptr[j] = pj;
+                            head[j] = hit ? nx : head[j];
                         }
-                        __syncwarp();
                     }
                 }
             }
@@ -474,6 +585,7 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
             if (lane == 0) vlim[vv] = (double)thr + (double)emax;
         }
         __syncthreads();
+        BT_MARK(3);
         // ---- queue: slice minima under the limit; slices with two or more rescan
         {
             const double lim = row_live ? vlim[rv] + (double)erow[r] : -1.0;
@@ -487,7 +599,7 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
                             flag |= 1u << i;
                         } else {
                             const int e = (int)(__float_as_uint(s1[i]) & 15u);
-                            const int k = contig ? 16 * i + e : 16 * e + i;
+                            const int k = 128 * half + (contig ? 8 * i + e : 16 * e + i);
                             if (k < K) {
                                 const int slot = atomicAdd(&qcnt[rv], 1);
                                 if (slot < QV) qflat[rv * QV + slot] = rl * K + k;
@@ -497,17 +609,17 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
                 }
             }
 #pragma unroll
-            for (int c = 0; c < BT_N / 32; ++c) {
-                // contiguous slices 2c, 2c+1 live in chunk c; interleaved slices in every chunk < K
-                const uint32_t fc = contig ? (flag >> (2 * c)) & 3u : (32 * c < K ? flag : 0u);
+            for (int c = 0; c < 4; ++c) {
+                // contiguous slices 4c..4c+3 live in chunk c; interleaved slices in every chunk < K
+                const uint32_t fc = contig ? (flag >> (4 * c)) & 15u : (128 * half + 32 * c < K ? flag : 0u);
                 if (__any_sync(0xffffffffu, fc != 0)) {
                     float v[32];
                     bt_ld32(taddr_row + 32 * c, v);
                     if (fc) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i) {
-                            const int k = 32 * c + i;
-                            const uint32_t bit = contig ? (fc >> (i >> 4)) & 1u : (fc >> (i & 15)) & 1u;
+                            const int k = 128 * half + 32 * c + i;
+                            const uint32_t bit = contig ? (fc >> (i >> 3)) & 1u : (fc >> (i & 15)) & 1u;
                             if (bit && k < K && s32 + v[i] <= limf) {
                                 const int slot = atomicAdd(&qcnt[rv], 1);
                                 if (slot < QV) qflat[rv * QV + slot] = rl * K + k;
@@ -519,6 +631,7 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncthreads();
+        BT_MARK(4);
         // a queue that overflowed, or that holds fewer than width entries (cannot
         // happen with a valid bound; kept as a guard), sends the vector to the exact path
         if (tid < V && v0 + tid < a.n && !vbad[tid] && (qcnt[tid] > QV || qcnt[tid] < width)) {
@@ -526,27 +639,49 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
             a.bad[v0 + tid] = 1;
         }
         __syncthreads();
-        // ---- exact float64 value of every queued candidate (round robin over threads)
+        BT_MARK(5);
+        // ---- exact float64 value of every queued candidate (compacted work list)
+        if (tid == 0) {
+            int o = 0;
+            for (int vv = 0; vv < V; ++vv) {
+                qoff[vv] = o;
+                o += (v0 + vv < a.n && !vbad[vv]) ? qcnt[vv] : 0;
+            }
+            qoff[V] = o;
+        }
+        __syncthreads();
+        BT_MARK(6);
         {
             const uint8_t* pcodes = codes + cur * BT_ROWS * M;
-            int total_q = 0;
-            for (int vv = 0; vv < V; ++vv) total_q += vbad[vv] ? 0 : qcnt[vv];
-            for (int idx = tid; idx < V * QV; idx += BT_T) {
-                const int vv = idx / QV, slot = idx % QV;
-                if (v0 + vv >= a.n || vbad[vv] || slot >= qcnt[vv]) continue;
+            const int total_q = qoff[V];
+            for (int e = tid; e < total_q; e += BT_T) {
+                int vv = 0;
+                while (qoff[vv + 1] <= e) ++vv;
+                const int idx = vv * QV + (e - qoff[vv]);
                 const int flat = qflat[idx];
                 const int l = flat / K, k = flat % K;
                 const long long gv = v0 + vv;
-                const double dot = bt_exact_dot(a.X + gv * a.ldx, a.cw + ((long long)m * K + k) * D, D, xv4);
+                const uint8_t* pcv = pcodes + (vv * cap + l) * M;
+                // cross-table terms first (independent loads), summed in order below
+                double pc[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    pc[j] = j < m ? a.P[(((long long)j * M + m) * K + pcv[j]) * K + k] : 0.0;
+                const float* crow = a.cw + ((long long)m * K + k) * D;
+                const double dot = a.xs_smem ? bt_exact_dot_s(xs + vv * D, crow, D)
+                                             : bt_exact_dot(a.X + gv * a.ldx, crow, D, xv4);
                 const double t = dsub(a.sq[m * K + k], dmul(2.0, dot));
                 double cross = 0.0;
-                const uint8_t* pcv = pcodes + (vv * cap + l) * M;
-                for (int j = 0; j < m; ++j) cross = dadd(cross, a.P[(((long long)j * M + m) * K + pcv[j]) * K + k]);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (j < m) cross = dadd(cross, pc[j]);
+                for (int j = 8; j < m; ++j) cross = dadd(cross, a.P[(((long long)j * M + m) * K + pcv[j]) * K + k]);
                 qval[idx] = dadd(dadd(score[cur * BT_ROWS + vv * cap + l], t), dmul(2.0, cross));
             }
             n_exact += (tid == 0) ? (unsigned long long)total_q : 0ULL;
         }
         __syncthreads();
+        BT_MARK(7);
         // ---- exact top-width per vector by (value, flat) rank
         for (int idx = tid; idx < V * QV; idx += BT_T) {
             const int vv = idx / QV, slot = idx % QV;
@@ -559,11 +694,12 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
             if (rank < width) sel[vv * cap + rank] = idx;
         }
         __syncthreads();
+        BT_MARK(8);
         // ---- children in flat order (thread per child row)
         {
             const int vv = r / cap, slotv = r % cap;
             const int nxt = cur ^ 1;
-            if (vv < V && slotv < width && v0 + vv < a.n && !vbad[vv]) {
+            if (half == 0 && vv < V && slotv < width && v0 + vv < a.n && !vbad[vv]) {
                 const int idx = sel[vv * cap + slotv];
                 const int f = qflat[idx];
                 int pos = 0;
@@ -578,6 +714,7 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
             }
         }
         __syncthreads();
+        BT_MARK(9);
         // ---- child residual images r = (hi + lo)_parent - c_m(k), split again
         // (fp32; the bound covers both roundings); column D stays 1
         if (m + 1 < M) {
@@ -590,14 +727,15 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
                 float* dst = img + (size_t)nxt * nch * 2 * A_EL;
                 const float* cwr = a.cw + ((long long)m * K + kk) * D;
                 const int pr = vv * cap + parent;
+                // the two threads of a row split the k-chunks
 #pragma unroll 4
-                for (int ch = 0; ch < nch; ++ch) {
+                for (int ch = half; ch < nch; ch += 2) {
 #pragma unroll
                     for (int c4 = 0; c4 < BT_BK / 4; ++c4) {
                         const int k = ch * BT_BK + 4 * c4;
                         const uint32_t po = bt_off(pr, 4 * c4) >> 2;
-                        const float4 h4 = *reinterpret_cast<const float4*>(src + (size_t)ch * 2 * A_EL + po);
-                        const float4 l4 = *reinterpret_cast<const float4*>(src + (size_t)ch * 2 * A_EL + A_EL + po);
+                        const float4 h4 = __ldcg(reinterpret_cast<const float4*>(src + (size_t)ch * 2 * A_EL + po));
+                        const float4 l4 = __ldcg(reinterpret_cast<const float4*>(src + (size_t)ch * 2 * A_EL + A_EL + po));
                         float c[4];
                         if (xv4 && k + 3 < D) {
                             const float4 t = __ldg(reinterpret_cast<const float4*>(cwr + k));
@@ -613,6 +751,7 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
             }
         }
         __syncthreads();
+        BT_MARK(10);
         cur ^= 1;
         live = width;
     }
@@ -649,6 +788,8 @@ __global__ void __launch_bounds__(BT_T, 2) beam_tc_kernel(BeamTcArgs a) {
     __syncthreads();
     }  // groups
     if (a.stats && tid == 0) atomicAdd(a.stats, n_exact);
+    if (a.prof && tid == 0)
+        for (int i = 0; i < 12; ++i) atomicAdd(a.prof + i, (unsigned long long)prof_acc[i]);
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (warp == 0) {
@@ -703,25 +844,31 @@ __global__ void list_bad_kernel(const int* __restrict__ bad, long long n, int* _
         if (bad[i]) idx[atomicAdd(cnt, 1)] = (int)i;
 }
 
-// Returns 1 (without launching) when the shape is outside the tensor-core encoder.
+// Returns kNotApplicable (without launching) when the shape is outside the
+// tensor-core encoder; CUDA failures are returned as their (positive) status.
 int launch_encode_tc(const float* X, long long n, long long ldx, int D, const float* cw, int M, int K, int L,
                      const double* sq, const double* P, void* codes_out, int code_bytes, long long ldcodes,
                      double* err_out, unsigned long long* stats, cudaStream_t s) {
-    if (K > BT_N || K < 1) return 1;
+    if (K > BT_N || K < 1) return kNotApplicable;
     long long capll = 1;
     for (int m = 0; m < M && capll < L; ++m) capll *= K;
     const int cap = (int)std::min((long long)L, capll);
-    if (cap > BT_ROWS || n <= 0) return n <= 0 ? 0 : 1;
+    if (cap > BT_ROWS || n <= 0) return n <= 0 ? 0 : kNotApplicable;
     const int V = BT_ROWS / cap;
     const int nch = (D + 1 + BT_BK - 1) / BT_BK;   // + the norm column
     // a single first-stage row cannot cover beams wider than 16: then all K go to the exact pass
-    const int qv = cap > BT_S ? std::max(3 * cap + 8, K) : 3 * cap + 8;
+    const int qv = cap > 2 * BT_S ? std::max(3 * cap + 8, K) : 3 * cap + 8;
     size_t smem = sizeof(float) * (BT_NST * 2 * BT_ROWS * BT_BK + BT_NST * 2 * BT_N * BT_BK);
     smem += sizeof(double) * (2 * BT_ROWS + (size_t)V * qv + 2 * V);
-    smem += 16 + sizeof(float) * (size_t)BT_S * BT_ROWS + sizeof(int) * BT_ROWS + 2 * BT_ROWS * (size_t)M;
+    smem += 16 + sizeof(float) * 2 * (size_t)BT_S * BT_ROWS + sizeof(int) * BT_ROWS + 2 * BT_ROWS * (size_t)M;
     smem += sizeof(int) * ((size_t)V * qv + V + BT_ROWS) + sizeof(int) * V +
             sizeof(float) * BT_ROWS;
-    if (smem > 227 * 1024) return 1;
+    smem += 32 + sizeof(int) * (V + 1);   // alignment + qoff
+    // stage the vectors as float64 when D fits one BLAS k-block and two CTAs still fit per SM
+    int xs_smem = 0;
+    const size_t xs_bytes = sizeof(double) * (size_t)V * D;
+    if (D <= 384 && smem + xs_bytes <= 200 * 1024) { xs_smem = 1; smem += xs_bytes; }
+    if (smem > 227 * 1024) return kNotApplicable;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -734,7 +881,8 @@ int launch_encode_tc(const float* X, long long n, long long ldx, int D, const fl
     cudaFuncAttributes fa{};
     DA_CUDA(cudaFuncGetAttributes(&fa, beam_tc_kernel));
     DA_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
-    if (2 * (smem + fa.sharedSizeBytes + 1024) <= (size_t)smem_sm) per_sm = 2;
+    const int regs_cta = ((fa.numRegs + 7) & ~7) * BT_T;
+    if (2 * (smem + fa.sharedSizeBytes + 1024) <= (size_t)smem_sm && 2 * regs_cta <= 65536) per_sm = 2;
     const int grid = (int)std::min<long long>(ngroups, (long long)sms * per_sm);
     // scratch
     size_t off = 0;
@@ -763,7 +911,14 @@ int launch_encode_tc(const float* X, long long n, long long ldx, int D, const fl
     a.X = X; a.n = n; a.ldx = ldx; a.D = D; a.cw = cw; a.M = M; a.K = K; a.L = L; a.cap = cap;
     a.sq = sq; a.P = P; a.Bg = Bg; a.cmax = cmax; a.img = (float*)(base + o_rb);
     a.codes_out = codes_out; a.code_bytes = code_bytes; a.ldcodes = ldcodes; a.err_out = err_out; a.stats = stats;
-    a.nch = nch; a.qv = qv; a.bad = bad;
+    a.nch = nch; a.qv = qv; a.bad = bad; a.xs_smem = xs_smem;
+    unsigned long long* dprof = nullptr;
+    const bool dbg = getenv("DA_DEBUG") != nullptr;
+    if (dbg) {
+        DA_CUDA(cudaMallocAsync((void**)&dprof, sizeof(unsigned long long) * 12, s));
+        DA_CUDA(cudaMemsetAsync(dprof, 0, sizeof(unsigned long long) * 12, s));
+        a.prof = dprof;
+    }
     {
         ProfScope ps1("encode_beam_tc", s);
         beam_tc_kernel<<<grid, BT_T, smem, s>>>(a);
@@ -777,7 +932,18 @@ int launch_encode_tc(const float* X, long long n, long long ldx, int D, const fl
     int h_cnt = 0;
     DA_CUDA(cudaMemcpyAsync(&h_cnt, cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
     DA_CUDA(cudaStreamSynchronize(s));
-    if (getenv("DA_DEBUG")) fprintf(stderr, "[da] encode_tc: n=%lld V=%d cap=%d grid=%d per_sm=%d smem=%zu overflowed=%d\n", n, V, cap, grid, per_sm, smem, h_cnt);
+    if (dbg) {
+        fprintf(stderr, "[da] encode_tc: n=%lld V=%d cap=%d grid=%d per_sm=%d smem=%zu overflowed=%d\n", n, V, cap, grid, per_sm, smem, h_cnt);
+        unsigned long long hp[12];
+        DA_CUDA(cudaMemcpy(hp, dprof, sizeof(hp), cudaMemcpyDeviceToHost));
+        unsigned long long tot = 0;
+        for (int i = 0; i < 11; ++i) tot += hp[i];
+        const char* names[11] = {"init/sync", "gemm", "rowpass", "select", "queue", "ovf", "qoff", "recheck", "rank", "child", "update"};
+        fprintf(stderr, "[da] encode_tc phases (%% of CTA clocks):");
+        for (int i = 0; i < 11; ++i) fprintf(stderr, " %s %.1f", names[i], tot ? 100.0 * hp[i] / tot : 0.0);
+        fprintf(stderr, "\n");
+        cudaFree(dprof);
+    }
     if (h_cnt > 0) {
         float* xg = nullptr;
         void* cg = nullptr;
