@@ -44,9 +44,17 @@ namespace da {
 namespace {
 constexpr int BT_ROWS = 128;
 constexpr int BT_N = 256;
-constexpr int BT_BK = 8;
-constexpr int BT_NST = 6;  // shared-memory ring depth (k-chunks in flight)
-constexpr int BT_T = 256;   // two threads per row: column halves
+#ifndef BT_THREADS
+#define BT_THREADS 256
+#endif
+constexpr int BT_T = BT_THREADS;     // 128: one thread per row; 256: two (column halves)
+constexpr int BT_H = BT_T / 128;     // threads per row
+constexpr int BT_CPT = 8 / BT_H;     // 32-column TMEM chunks per thread
+constexpr int BT_SW = 2 * BT_CPT;    // contiguous slice width (16 slices per thread)
+constexpr int BT_COLS = 256 / BT_H;  // columns per thread
+constexpr int BT_BK = BT_H == 1 ? 8 : 16;
+constexpr int BT_NST = 3;  // shared-memory ring depth (k-chunks in flight)
+
 #ifndef BT_PREFETCH
 #define BT_PREFETCH 1
 #endif
@@ -238,14 +246,14 @@ __device__ __forceinline__ float bt_unkey(unsigned k) {
 template <bool CONTIG>
 __device__ __forceinline__ void bt_row_pass(uint32_t taddr_row, bool row_live, float* s1, float* s2) {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < BT_CPT; ++c) {
         float v[32];
         bt_ld32(taddr_row + 32 * c, v);
         if (row_live) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
-                const int sl = CONTIG ? 4 * c + (i >> 3) : (i & 15);
-                const uint32_t pos = CONTIG ? (uint32_t)(i & 7) : (uint32_t)(2 * c + (i >> 4));
+                const int sl = CONTIG ? c * (32 / BT_SW) + i / BT_SW : (i & 15);
+                const uint32_t pos = CONTIG ? (uint32_t)(i % BT_SW) : (uint32_t)(2 * c + (i >> 4));
                 const float w = __uint_as_float((__float_as_uint(v[i]) & ~15u) | pos);
                 s2[sl] = fminf(s2[sl], fmaxf(s1[sl], w));
                 s1[sl] = fminf(s1[sl], w);
@@ -282,7 +290,7 @@ struct BeamTcArgs {
     unsigned long long* prof;  // [12] per-phase clock sums (debug) or null
 };
 
-__global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
+__global__ void __launch_bounds__(BT_T, BT_H == 1 ? 2 : 1) beam_tc_kernel(BeamTcArgs a) {
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int A_EL = BT_ROWS * BT_BK, B_EL = BT_N * BT_BK;
     float* Abuf = reinterpret_cast<float*>(smem);        // [NST][hi,lo][A_EL]
@@ -296,7 +304,7 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
     double* vlim = reinterpret_cast<double*>(p); p += sizeof(double) * V;               // [V]
     double* xnorm = reinterpret_cast<double*>(p); p += sizeof(double) * V;              // [V]
     p = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
-    float* slist = reinterpret_cast<float*>(p); p += sizeof(float) * 2 * BT_S * BT_ROWS;   // [rows][2S] slice minima
+    float* slist = reinterpret_cast<float*>(p); p += sizeof(float) * BT_H * BT_S * BT_ROWS;   // [rows][H*S] slice minima
     int* rarg = reinterpret_cast<int*>(p); p += sizeof(int) * BT_ROWS;                  // (parent, k) per child
     int* qflat = reinterpret_cast<int*>(p); p += sizeof(int) * V * QV;                  // [V][QV]
     int* qcnt = reinterpret_cast<int*>(p); p += sizeof(int) * V;                        // [V]
@@ -338,8 +346,8 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tmem_sh;
-    const int half = tid >> 7;                       // column half of this thread's row
-    const uint32_t taddr_row = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(half * 128);
+    const int half = tid >> 7;                       // column part of this thread's row (BT_H == 2)
+    const uint32_t taddr_row = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(half * BT_COLS);
     double cmax_all = 0.0;
     for (int j = 0; j < M; ++j) cmax_all = fmax(cmax_all, a.cmax[2 * j]);
     const double steps = 3.0 * nch * (BT_BK / 8) + 7.0;   // fp32 accumulations per TMEM value (+ slack)
@@ -349,7 +357,7 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
     long long prof_acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     long long prof_t = clock64();
     long long q = 0;        // k-chunks streamed (ring phases persist across groups)
-    int bpre = 0;           // chunks of the coming stage whose codeword copy already started (tid 0)
+    int bpre = 0;           // chunks of the coming stage whose codeword copy already started (tid 32)
     uint32_t acc_phase = 0;
     unsigned long long n_exact = 0;
     const long long ngroups = (a.n + V - 1) / V;
@@ -393,7 +401,9 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
         __syncthreads();
         BT_MARK(0);
         // ---- GEMM: TMEM[row][k] = ||c_k||^2 - 2 r_row . c_k  (3xTF32, fp32 accumulate)
-        if (tid == 0) {
+        // warp-specialised: thread 32 streams operand chunks into the ring (running up
+        // to NST chunks ahead), thread 0 issues the MMAs as chunks land
+        if (tid == 32) {
             const float* Ag = img + (size_t)cur * nch * 2 * A_EL;
             const float* Bm = a.Bg + (size_t)m * nch * 2 * B_EL;
             constexpr uint32_t bytes_a = 2 * A_EL * sizeof(float), bytes_b = 2 * B_EL * sizeof(float);
@@ -409,16 +419,22 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
                              : "memory");
                 bt_bulk(Bbuf + st * 2 * B_EL, Bsrc + (size_t)ch * 2 * B_EL, bytes_b, &full_bar[st]);
             };
-            auto issue_a = [&](int ch) {
+            for (int ch = 0; ch < nch; ++ch) {
+                if (ch >= bpre) issue_b(q, Bm, ch);   // the first chunks' B copies may already be in flight
                 const int st = (int)((q + ch) % BT_NST);
                 bt_bulk(Abuf + st * 2 * A_EL, Ag + (size_t)ch * 2 * A_EL, bytes_a, &full_bar[st]);
-            };
-            const int first = std::min(BT_NST - 1, nch);
-            // the first chunks' codeword copies were started at the end of the previous stage
-            for (int ch = 0; ch < first; ++ch) {
-                if (ch >= bpre) issue_b(q, Bm, ch);
-                issue_a(ch);
             }
+            // start the next stage's first codeword copies now (they do not depend on
+            // the epilogue); only when a next stage exists on this CTA
+            bpre = 0;
+            if (BT_PREFETCH && ((m + 1 < M) || (grp + gridDim.x < ngroups))) {
+                const float* Bn = a.Bg + (size_t)((m + 1) % M) * nch * 2 * B_EL;
+                const int first = BT_NST < nch ? BT_NST : nch;
+                for (int ch = 0; ch < first; ++ch) issue_b(q + nch, Bn, ch);
+                bpre = first;
+            }
+        }
+        if (tid == 0) {
             for (int ch = 0; ch < nch; ++ch) {
                 const long long qq = q + ch;
                 const int st = (int)(qq % BT_NST);
@@ -441,23 +457,9 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
                     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                                      bt_smem_u32(&acc_bar))
                                  : "memory");
-                // refill the slot of the previous chunk (its MMAs were issued before this one's)
-                if (ch + BT_NST - 1 < nch) {
-                    issue_b(q, Bm, ch + BT_NST - 1);
-                    issue_a(ch + BT_NST - 1);
-                }
-            }
-            // start the next stage's first codeword copies now (they do not depend on
-            // the epilogue); only when a next stage exists on this CTA
-            bpre = 0;
-            const bool more = BT_PREFETCH && ((m + 1 < M) || (grp + gridDim.x < ngroups));
-            if (more) {
-                const float* Bn = a.Bg + (size_t)((m + 1) % M) * nch * 2 * B_EL;
-                for (int ch = 0; ch < first; ++ch) issue_b(q + nch, Bn, ch);
-                bpre = first;
             }
         }
-        __syncwarp();   // warp 0 reconverges before the warp-collective TMEM loads
+        __syncwarp();   // warps 0/1 reconverge before the warp-collective TMEM loads
         q += nch;
         bt_wait(&acc_bar, acc_phase);
         BT_MARK(1);
@@ -497,7 +499,7 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
             }
 #pragma unroll
             for (int i = 0; i < BT_S; i += 4)
-                *reinterpret_cast<float4*>(slist + (r * 2 + half) * BT_S + i) = make_float4(srt[i], srt[i + 1], srt[i + 2], srt[i + 3]);
+                *reinterpret_cast<float4*>(slist + (r * BT_H + half) * BT_S + i) = make_float4(srt[i], srt[i + 1], srt[i + 2], srt[i + 3]);
         }
         // rigorous |w' - v| for this row (v = the exact float64 score):
         //   3xTF32 (B rounding, lo*lo dropped): 2^-21 sum|a||b|; fp32 accumulation
@@ -524,9 +526,9 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
         for (int vv = warp; vv < V; vv += BT_T / 32) {
             if (v0 + vv >= a.n || vbad[vv]) continue;
             float thr = INF;
-            const int nl = 2 * live;    // sorted lists of the vector (two per live row)
+            const int nl = BT_H * live;    // sorted lists of the vector (BT_H per live row)
             if (width < tot_ll && nl * BT_S >= width) {
-                const float* L0 = slist + (size_t)vv * cap * 2 * BT_S;
+                const float* L0 = slist + (size_t)vv * cap * BT_H * BT_S;
                 if (nl <= 32) {
                     // one sorted list per lane, held in registers; the winner shifts its list
                     float it[BT_S];
@@ -548,10 +550,10 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
                     }
                 } else {
                     // lane j merges lists j, j+32, ...: head pointers in registers
-                    int ptr[BT_ROWS * 2 / 32];
-                    float head[BT_ROWS * 2 / 32];
+                    int ptr[BT_ROWS * BT_H / 32];
+                    float head[BT_ROWS * BT_H / 32];
 #pragma unroll
-                    for (int j = 0; j < BT_ROWS * 2 / 32; ++j) {
+                    for (int j = 0; j < BT_ROWS * BT_H / 32; ++j) {
                         ptr[j] = 0;
                         head[j] = lane + 32 * j < nl ? L0[(lane + 32 * j) * BT_S] : INF;
                     }
@@ -559,14 +561,14 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
                     for (int step = 0; step < width; ++step) {
                         float best = head[0];
 #pragma unroll
-                        for (int j = 1; j < BT_ROWS * 2 / 32; ++j)
+                        for (int j = 1; j < BT_ROWS * BT_H / 32; ++j)
                             if (j < nj) best = fminf(best, head[j]);
                         const unsigned key = __reduce_min_sync(0xffffffffu, bt_key(best));
                         thr = bt_unkey(key);
                         const unsigned own = __ballot_sync(0xffffffffu, bt_key(best) == key);
                         bool adv = lane == __ffs(own) - 1;
 #pragma unroll
-                        for (int j = 0; j < BT_ROWS * 2 / 32; ++j) {
+                        for (int j = 0; j < BT_ROWS * BT_H / 32; ++j) {
                             const bool hit = adv && j < nj && head[j] == best;
                             adv = adv && !hit;
                             const int pj = ptr[j] + (hit ? 1 : 0);
@@ -599,7 +601,7 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
                             flag |= 1u << i;
                         } else {
                             const int e = (int)(__float_as_uint(s1[i]) & 15u);
-                            const int k = 128 * half + (contig ? 8 * i + e : 16 * e + i);
+                            const int k = BT_COLS * half + (contig ? BT_SW * i + e : 16 * e + i);
                             if (k < K) {
                                 const int slot = atomicAdd(&qcnt[rv], 1);
                                 if (slot < QV) qflat[rv * QV + slot] = rl * K + k;
@@ -609,17 +611,18 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
                 }
             }
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < BT_CPT; ++c) {
                 // contiguous slices 4c..4c+3 live in chunk c; interleaved slices in every chunk < K
-                const uint32_t fc = contig ? (flag >> (4 * c)) & 15u : (128 * half + 32 * c < K ? flag : 0u);
+                const uint32_t fc = contig ? (flag >> (c * (32 / BT_SW))) & ((1u << (32 / BT_SW)) - 1u)
+                                          : (BT_COLS * half + 32 * c < K ? flag : 0u);
                 if (__any_sync(0xffffffffu, fc != 0)) {
                     float v[32];
                     bt_ld32(taddr_row + 32 * c, v);
                     if (fc) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i) {
-                            const int k = 128 * half + 32 * c + i;
-                            const uint32_t bit = contig ? (fc >> (i >> 3)) & 1u : (fc >> (i & 15)) & 1u;
+                            const int k = BT_COLS * half + 32 * c + i;
+                            const uint32_t bit = contig ? (fc >> (i / BT_SW)) & 1u : (fc >> (i & 15)) & 1u;
                             if (bit && k < K && s32 + v[i] <= limf) {
                                 const int slot = atomicAdd(&qcnt[rv], 1);
                                 if (slot < QV) qflat[rv * QV + slot] = rl * K + k;
@@ -723,28 +726,35 @@ __global__ void __launch_bounds__(BT_T, 1) beam_tc_kernel(BeamTcArgs a) {
             if (vv < V && slotv < width && v0 + vv < a.n && !vbad[vv]) {
                 const int pk = rarg[r];
                 const int parent = pk >> 16, kk = pk & 0xFFFF;
-                const float* src = img + (size_t)cur * nch * 2 * A_EL;
-                float* dst = img + (size_t)nxt * nch * 2 * A_EL;
-                const float* cwr = a.cw + ((long long)m * K + kk) * D;
+                // parent and child images are different buffers: no aliasing, so the
+                // loads of later chunks may be issued ahead of earlier stores
+                const float* __restrict__ src = img + (size_t)cur * nch * 2 * A_EL;
+                float* __restrict__ dst = img + (size_t)nxt * nch * 2 * A_EL;
+                const float* __restrict__ cwr = a.cw + ((long long)m * K + kk) * D;
                 const int pr = vv * cap + parent;
-                // the two threads of a row split the k-chunks
-#pragma unroll 4
-                for (int ch = half; ch < nch; ch += 2) {
+                // the BT_H threads of a row split the k-chunks
+#pragma unroll 2
+                for (int ch = half; ch < nch; ch += BT_H) {
+                    float4 hb[BT_BK / 4], lb[BT_BK / 4], cb[BT_BK / 4];
 #pragma unroll
                     for (int c4 = 0; c4 < BT_BK / 4; ++c4) {
                         const int k = ch * BT_BK + 4 * c4;
                         const uint32_t po = bt_off(pr, 4 * c4) >> 2;
-                        const float4 h4 = __ldcg(reinterpret_cast<const float4*>(src + (size_t)ch * 2 * A_EL + po));
-                        const float4 l4 = __ldcg(reinterpret_cast<const float4*>(src + (size_t)ch * 2 * A_EL + A_EL + po));
-                        float c[4];
+                        hb[c4] = *reinterpret_cast<const float4*>(src + (size_t)ch * 2 * A_EL + po);
+                        lb[c4] = *reinterpret_cast<const float4*>(src + (size_t)ch * 2 * A_EL + A_EL + po);
                         if (xv4 && k + 3 < D) {
-                            const float4 t = __ldg(reinterpret_cast<const float4*>(cwr + k));
-                            c[0] = t.x; c[1] = t.y; c[2] = t.z; c[3] = t.w;
+                            cb[c4] = __ldg(reinterpret_cast<const float4*>(cwr + k));
                         } else {
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) c[u] = k + u < D ? cwr[k + u] : 0.f;
+                            cb[c4].x = k + 0 < D ? cwr[k + 0] : 0.f;
+                            cb[c4].y = k + 1 < D ? cwr[k + 1] : 0.f;
+                            cb[c4].z = k + 2 < D ? cwr[k + 2] : 0.f;
+                            cb[c4].w = k + 3 < D ? cwr[k + 3] : 0.f;
                         }
-                        float x4[4] = {(h4.x + l4.x) - c[0], (h4.y + l4.y) - c[1], (h4.z + l4.z) - c[2], (h4.w + l4.w) - c[3]};
+                    }
+#pragma unroll
+                    for (int c4 = 0; c4 < BT_BK / 4; ++c4) {
+                        const float4 hh = hb[c4], ll = lb[c4], cc = cb[c4];
+                        float x4[4] = {(hh.x + ll.x) - cc.x, (hh.y + ll.y) - cc.y, (hh.z + ll.z) - cc.z, (hh.w + ll.w) - cc.w};
                         bt_store_split(dst + (size_t)ch * 2 * A_EL, bt_off(r, 4 * c4) >> 2, x4);
                     }
                 }
@@ -857,10 +867,10 @@ int launch_encode_tc(const float* X, long long n, long long ldx, int D, const fl
     const int V = BT_ROWS / cap;
     const int nch = (D + 1 + BT_BK - 1) / BT_BK;   // + the norm column
     // a single first-stage row cannot cover beams wider than 16: then all K go to the exact pass
-    const int qv = cap > 2 * BT_S ? std::max(3 * cap + 8, K) : 3 * cap + 8;
+    const int qv = cap > BT_H * BT_S ? std::max(3 * cap + 8, K) : 3 * cap + 8;
     size_t smem = sizeof(float) * (BT_NST * 2 * BT_ROWS * BT_BK + BT_NST * 2 * BT_N * BT_BK);
     smem += sizeof(double) * (2 * BT_ROWS + (size_t)V * qv + 2 * V);
-    smem += 16 + sizeof(float) * 2 * (size_t)BT_S * BT_ROWS + sizeof(int) * BT_ROWS + 2 * BT_ROWS * (size_t)M;
+    smem += 16 + sizeof(float) * BT_H * (size_t)BT_S * BT_ROWS + sizeof(int) * BT_ROWS + 2 * BT_ROWS * (size_t)M;
     smem += sizeof(int) * ((size_t)V * qv + V + BT_ROWS) + sizeof(int) * V +
             sizeof(float) * BT_ROWS;
     smem += 32 + sizeof(int) * (V + 1);   // alignment + qoff
