@@ -42,18 +42,22 @@
 namespace da {
 
 namespace {
-constexpr int BT_ROWS = 128;
-constexpr int BT_N = 256;
+#ifndef BT_BIG
+#define BT_BIG 0
+#endif
 #ifndef BT_THREADS
 #define BT_THREADS 256
 #endif
-constexpr int BT_T = BT_THREADS;     // 128: one thread per row; 256: two (column halves)
-constexpr int BT_H = BT_T / 128;     // threads per row
+constexpr int BT_ROWS = BT_BIG ? 256 : 128;   // rows (vector beams) per CTA
+constexpr int BT_RB = BT_ROWS / 128;          // 128-row MMA blocks, one TMEM accumulator each
+constexpr int BT_N = 256;
+constexpr int BT_T = BT_THREADS;
+constexpr int BT_H = BT_T / BT_ROWS;          // threads per row (1, or 2 = column halves)
 constexpr int BT_CPT = 8 / BT_H;     // 32-column TMEM chunks per thread
 constexpr int BT_SW = 2 * BT_CPT;    // contiguous slice width (16 slices per thread)
 constexpr int BT_COLS = 256 / BT_H;  // columns per thread
-constexpr int BT_BK = BT_H == 1 ? 8 : 16;
-constexpr int BT_NST = 3;  // shared-memory ring depth (k-chunks in flight)
+constexpr int BT_BK = BT_H == 1 ? 8 : 16;   // k per ring chunk
+constexpr int BT_NST = BT_RB == 2 ? 4 : 3;  // shared-memory ring depth (k-chunks in flight)
 
 #ifndef BT_PREFETCH
 #define BT_PREFETCH 1
@@ -290,7 +294,7 @@ struct BeamTcArgs {
     unsigned long long* prof;  // [12] per-phase clock sums (debug) or null
 };
 
-__global__ void __launch_bounds__(BT_T, BT_H == 1 ? 2 : 1) beam_tc_kernel(BeamTcArgs a) {
+__global__ void __launch_bounds__(BT_T, (BT_H == 1 && BT_RB == 1) ? 2 : 1) beam_tc_kernel(BeamTcArgs a) {
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int A_EL = BT_ROWS * BT_BK, B_EL = BT_N * BT_BK;
     float* Abuf = reinterpret_cast<float*>(smem);        // [NST][hi,lo][A_EL]
@@ -325,13 +329,13 @@ __global__ void __launch_bounds__(BT_T, BT_H == 1 ? 2 : 1) beam_tc_kernel(BeamTc
     float* img = a.img + (size_t)blockIdx.x * 2 * nch * 2 * A_EL;
     const double u24 = 5.9604644775390625e-08, u22 = 2.384185791015625e-07, u19 = 1.9073486328125e-06;
     const float INF = __int_as_float(0x7f800000);
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BT_N >> 3) << 17) | ((uint32_t)(BT_ROWS >> 4) << 24);
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BT_N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     const bool xv4 = ((D & 3) == 0) && ((a.ldx & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) &&
                      ((reinterpret_cast<uintptr_t>(a.cw) & 15) == 0);
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(bt_smem_u32(&tmem_sh)),
-                     "r"(BT_N));
+                     "r"(BT_N * BT_RB));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
@@ -346,8 +350,11 @@ __global__ void __launch_bounds__(BT_T, BT_H == 1 ? 2 : 1) beam_tc_kernel(BeamTc
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tmem_sh;
-    const int half = tid >> 7;                       // column part of this thread's row (BT_H == 2)
-    const uint32_t taddr_row = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(half * BT_COLS);
+    // TMEM: warp w reads lanes 32*(w%4)..; w / 4 selects the column half (BT_H == 2)
+    // or the 128-row block's accumulator (BT_RB == 2)
+    const int half = BT_H == 2 ? tid >> 7 : 0;
+    const int blk = BT_RB == 2 ? tid >> 7 : 0;
+    const uint32_t taddr_row = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(half * BT_COLS + blk * BT_N);
     double cmax_all = 0.0;
     for (int j = 0; j < M; ++j) cmax_all = fmax(cmax_all, a.cmax[2 * j]);
     const double steps = 3.0 * nch * (BT_BK / 8) + 7.0;   // fp32 accumulations per TMEM value (+ slack)
@@ -443,12 +450,18 @@ __global__ void __launch_bounds__(BT_T, BT_H == 1 ? 2 : 1) beam_tc_kernel(BeamTc
                 const uint32_t ah = bt_smem_u32(Abuf + st * 2 * A_EL), al = ah + A_EL * 4;
                 const uint32_t bh = bt_smem_u32(Bbuf + st * 2 * B_EL), bl = bh + B_EL * 4;
 #pragma unroll
-                for (int s2 = 0; s2 < BT_BK / 8; ++s2) {
-                    const uint32_t off = (uint32_t)s2 * 256;
-                    const uint32_t acc0 = (ch > 0 || s2 > 0) ? 1u : 0u;
-                    bt_mma(tmem, bt_desc(ah + off), bt_desc(bh + off), idesc, acc0);
-                    bt_mma(tmem, bt_desc(ah + off), bt_desc(bl + off), idesc, 1u);
-                    bt_mma(tmem, bt_desc(al + off), bt_desc(bh + off), idesc, 1u);
+                for (int b = 0; b < BT_RB; ++b) {
+                    // row block b: A rows 128b.. (contiguous in the image), accumulator columns 256b..
+                    const uint32_t ab = (uint32_t)b * 128 * BT_BK * 4;
+                    const uint32_t tb = tmem + (uint32_t)b * BT_N;
+#pragma unroll
+                    for (int s2 = 0; s2 < BT_BK / 8; ++s2) {
+                        const uint32_t off = (uint32_t)s2 * 256;
+                        const uint32_t acc0 = (ch > 0 || s2 > 0) ? 1u : 0u;
+                        bt_mma(tb, bt_desc(ah + ab + off), bt_desc(bh + off), idesc, acc0);
+                        bt_mma(tb, bt_desc(ah + ab + off), bt_desc(bl + off), idesc, 1u);
+                        bt_mma(tb, bt_desc(al + ab + off), bt_desc(bh + off), idesc, 1u);
+                    }
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                                  bt_smem_u32(&empty_bar[st]))
@@ -636,23 +649,24 @@ __global__ void __launch_bounds__(BT_T, BT_H == 1 ? 2 : 1) beam_tc_kernel(BeamTc
         __syncthreads();
         BT_MARK(4);
         // a queue that overflowed, or that holds fewer than width entries (cannot
-        // happen with a valid bound; kept as a guard), sends the vector to the exact path
-        if (tid < V && v0 + tid < a.n && !vbad[tid] && (qcnt[tid] > QV || qcnt[tid] < width)) {
-            vbad[tid] = 1;
-            a.bad[v0 + tid] = 1;
-        }
-        __syncthreads();
-        BT_MARK(5);
-        // ---- exact float64 value of every queued candidate (compacted work list)
+        // happen with a valid bound; kept as a guard), sends the vector to the exact
+        // path; the kept queues are compacted into one work list (thread 0)
         if (tid == 0) {
             int o = 0;
             for (int vv = 0; vv < V; ++vv) {
                 qoff[vv] = o;
-                o += (v0 + vv < a.n && !vbad[vv]) ? qcnt[vv] : 0;
+                if (v0 + vv >= a.n || vbad[vv]) continue;
+                if (qcnt[vv] > QV || qcnt[vv] < width) {
+                    vbad[vv] = 1;
+                    a.bad[v0 + vv] = 1;
+                    continue;
+                }
+                o += qcnt[vv];
             }
             qoff[V] = o;
         }
         __syncthreads();
+        BT_MARK(5);
         BT_MARK(6);
         {
             const uint8_t* pcodes = codes + cur * BT_ROWS * M;
@@ -804,7 +818,7 @@ __global__ void __launch_bounds__(BT_T, BT_H == 1 ? 2 : 1) beam_tc_kernel(BeamTc
     __syncthreads();
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BT_N));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BT_N * BT_RB));
     }
 }
 
