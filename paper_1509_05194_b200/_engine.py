@@ -406,6 +406,93 @@ def encode(X: torch.Tensor, cw: torch.Tensor, sq: torch.Tensor, Pt: torch.Tensor
     return codes, err
 
 
+_PINNED: list = []
+
+
+def _pinned_slots(nslot: int, elems: int) -> list:
+    """Reusable page-locked float32 staging buffers (allocation is slow; keep them)."""
+    global _PINNED
+    if len(_PINNED) < nslot or _PINNED[0].numel() < elems:
+        _PINNED = [torch.empty(max(elems, _PINNED[0].numel() if _PINNED else 0), dtype=torch.float32,
+                               pin_memory=True) for _ in range(nslot)]
+    return _PINNED[:nslot]
+
+
+def encode_host(X_np: np.ndarray, cw: torch.Tensor, sq: torch.Tensor, Pt: torch.Tensor, L: int,
+                out_dtype=I32, chunk: int = 131072, name: str = "data") -> torch.Tensor:
+    """Beam-encode a host float32 array, streamed: a worker thread copies row chunks
+    into pinned slots while the device uploads the previous chunk (copy stream) and
+    encodes the one before (compute stream).  Non-finite input raises ValueError
+    (checked on the device).  Returns the device codes (n, M)."""
+    import threading
+
+    n, D = X_np.shape
+    M = cw.shape[0]
+    dev = device()
+    codes = torch.empty((n, M), dtype=out_dtype, device=dev)
+    if n == 0:
+        return codes
+    chunk = max(1, min(chunk, n))
+    nslot = 3
+    pinned = _pinned_slots(nslot, chunk * D)
+    pinned = [p_[: chunk * D].view(chunk, D) for p_ in pinned]
+    dbuf = [torch.empty((chunk, D), dtype=torch.float32, device=dev) for _ in range(2)]
+    starts = list(range(0, n, chunk))
+    filled = [threading.Semaphore(0) for _ in range(nslot)]
+    free = [threading.Semaphore(1) for _ in range(nslot)]
+    errors = []
+
+    def producer():
+        try:
+            for i, r0 in enumerate(starts):
+                s = i % nslot
+                free[s].acquire()
+                rows = min(chunk, n - r0)
+                np.copyto(pinned[s][:rows].numpy(), X_np[r0:r0 + rows])
+                filled[s].release()
+        except BaseException as e:  # surfaced on the caller's thread
+            errors.append(e)
+            for f in filled:
+                f.release()
+
+    th = threading.Thread(target=producer, daemon=True)
+    th.start()
+    comp = torch.cuda.current_stream()
+    cstream = torch.cuda.Stream()
+    ok = torch.ones((), dtype=torch.bool, device=dev)
+    comp_done = [None, None]
+    try:
+        for i, r0 in enumerate(starts):
+            s, b = i % nslot, i % 2
+            rows = min(chunk, n - r0)
+            filled[s].acquire()
+            if errors:
+                raise errors[0]
+            with torch.cuda.stream(cstream):
+                if comp_done[b] is not None:
+                    cstream.wait_event(comp_done[b])        # device buffer b is free again
+                dbuf[b][:rows].copy_(pinned[s][:rows], non_blocking=True)
+                up = torch.cuda.Event()
+                up.record(cstream)
+            comp.wait_event(up)
+            x = dbuf[b][:rows]
+            ok &= torch.isfinite(x).all()
+            native.da_encode(P(x), 1, rows, x.stride(0), D, P(cw), M, cw.shape[1], int(L), P(sq), P(Pt),
+                             P(codes[r0:]), code_bytes(codes), codes.stride(0), None, stream())
+            ev = torch.cuda.Event()
+            ev.record(comp)
+            comp_done[b] = ev
+            up.synchronize()                                 # pinned slot s has been read
+            free[s].release()
+    finally:
+        th.join()
+    if errors:
+        raise errors[0]
+    if not bool(ok.item()):
+        raise ValueError(f"{name} contains non-finite values")
+    return codes
+
+
 def assign_config(mode: int, counter: torch.Tensor | None = None) -> None:
     """0 = tcgen05 3xTF32 filter with exact float64 recheck (default, K <= 256),
     1 = plain float64 kernel.  `counter` accumulates rechecked (row, codeword) pairs."""

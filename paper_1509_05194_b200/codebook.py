@@ -329,7 +329,7 @@ def encode_dataset(codebook: Codebook, data, beam_width: int = 10, n_jobs: int =
     """Beam-encode every vector; byte-identical for any n_jobs (ignored on the GPU)."""
     if beam_width < 1:
         raise ValueError("beam_width must be >= 1")
-    X = check_vectors(data, name="data", allow_empty=True)
+    X = check_vectors(data, name="data", allow_empty=True, finite=False)
     if X.shape[0] and X.shape[1] != codebook.dim:
         raise ValueError(f"data d={X.shape[1]} does not match codebook dim {codebook.dim}")
     if X.shape[0] == 0:
@@ -340,8 +340,8 @@ def encode_dataset(codebook: Codebook, data, beam_width: int = 10, n_jobs: int =
     _raw_kernel(2)
     cw, sq = _codebook_dev(codebook)
     Pt, _ = _cross_dev(cross)
-    codes, _ = E.encode(E.to_dev(X), cw, sq, Pt, beam_width, out_dtype=_torch_code_dtype(codebook.k_count),
-                        with_err=False)
+    # host rows stream through pinned buffers: upload, finiteness check and encode overlap
+    codes = E.encode_host(X, cw, sq, Pt, beam_width, out_dtype=_torch_code_dtype(codebook.k_count))
     return EncodedDataset(codes=codes.cpu().numpy(), k_count=codebook.k_count,
                           codebook_hash=codebook.content_hash())
 

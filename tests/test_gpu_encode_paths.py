@@ -76,3 +76,24 @@ def test_config_b_like_and_recheck_rate():
         # candidates per vector: sum over stages of live*K; the filter must cut most of them
         total = X.shape[0] * sum(min(L, 256 ** m) * 256 for m in range(1, 9))
         assert rechecked < 0.05 * total, (rechecked, total)
+
+
+def test_streamed_host_encode_matches_device_encode():
+    rng = np.random.default_rng(11)
+    book = da.Codebook(codewords=rng.standard_normal((4, 16, 12)).astype(np.float32), order=np.arange(4))
+    X = rng.standard_normal((2500, 12)).astype(np.float32)
+    cross = cb.cross_products(book)
+    cw, sq = cb._codebook_dev(book)
+    Pt, _ = cross.device()
+    ref, _ = E.encode(E.to_dev(X), cw, sq, Pt, 5, with_err=False)
+    for chunk in (1000, 2500, 4096):
+        got = E.encode_host(X, cw, sq, Pt, 5, chunk=chunk)
+        np.testing.assert_array_equal(got.cpu().numpy(), ref.cpu().numpy())
+    enc = da.encode_dataset(book, X, beam_width=5, cross=cross)
+    np.testing.assert_array_equal(enc.codes.astype(np.int64), ref.cpu().numpy().astype(np.int64))
+    bad = X.copy()
+    bad[1700, 3] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        E.encode_host(bad, cw, sq, Pt, 5, chunk=1000)
+    with pytest.raises(ValueError, match="non-finite"):
+        da.encode_dataset(book, bad, beam_width=5, cross=cross)

@@ -1,0 +1,16 @@
+#!/bin/bash
+# Bench + reference arm + ncu evidence for profiles/ (run on the GPU box from the repo root).
+set -u
+mkdir -p gpurun_out
+python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
+# launch list of the timed encode kernels (cold-cache, serialised: shares only)
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"encode|beam|sgemm|gemm_kernel|bound_prep" -c 60 --csv \
+    --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-anneal --no-cpu > gpurun_out/ncu_launch.log 2>&1; echo "launch rc=$?"
+# full capture of the dominant kernel (L=10 gather filter) and of the tcgen05 filter at L=1
+ncu --set full --clock-control none --import-source on -k regex:beam_fast -c 1 -o gpurun_out/prof_beam_fast \
+    python tools/prof_tc.py 2 10 > gpurun_out/ncu_bf.log 2>&1; echo "full bf rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:sgemm_table -c 1 -o gpurun_out/prof_sgemm \
+    python tools/prof_tc.py 2 10 > gpurun_out/ncu_sg.log 2>&1; echo "full sgemm rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:beam_tc -c 1 -o gpurun_out/prof_beam_tc_L1 \
+    python tools/prof_tc.py 3 1 > gpurun_out/ncu_tc.log 2>&1; echo "full tc rc=$?"
