@@ -148,6 +148,18 @@ int da_adc_scan(const void* codes, int code_bytes, int64_t ldc, const double* pa
                 int64_t ncand, int64_t nq, const double* lut, const double* qsq, int M, int K, int r, int64_t* ids,
                 double* dists, void* stream);
 
+/* Packed candidate records for the scan (one-byte codes, M <= 8): records is n x 16 bytes,
+ * codes in bytes 0..7 and the row's pair sum (float64) in bytes 8..15, so one random
+ * candidate reads one 32-byte sector.  Built once per encoded set.
+ * replaces the (codes, code_pair_sums) inputs of exhaustive_adc_search  codebook.py:388-429 */
+int da_adc_pack(const void* codes, int code_bytes, int64_t n, int64_t ldc, const double* pair, int M,
+                void* records, void* stream);
+
+/* da_adc_scan over packed records (same results, same tie rule).
+ * replaces exhaustive_adc_search / A-Tree candidate re-ranking  codebook.py:399-429 */
+int da_adc_scan_packed(const void* records, const int64_t* cand, int64_t ncand, int64_t nq, const double* lut,
+                       const double* qsq, int M, int K, int r, int64_t* ids, double* dists, void* stream);
+
 /* numpy pairwise sum (divide=0) or mean (divide=1) of a float64 vector, result on device.
  * replaces errs.mean() / .mean() of per-vector errors   clustering.py:187, annealing.py:176 */
 int da_np_sum(const double* a, int64_t n, int divide, double* out, void* stream);

@@ -534,6 +534,27 @@ def adc_scan(codes: torch.Tensor, pair: torch.Tensor, lut: torch.Tensor, qsq: to
     return ids, dists
 
 
+def adc_pack(codes: torch.Tensor, pair: torch.Tensor) -> torch.Tensor | None:
+    """(n, 16) uint8 packed records (codes + pair sum), or None when the codes do not
+    fit (more than 8 dictionaries or codes wider than one byte)."""
+    n, M = codes.shape
+    if codes.dtype != torch.uint8 or M > 8:
+        return None
+    rec = torch.empty((n, 16), dtype=torch.uint8, device=codes.device)
+    native.da_adc_pack(P(codes), 1, n, codes.stride(0), P(pair), M, P(rec), stream())
+    return rec
+
+
+def adc_scan_packed(rec: torch.Tensor, lut: torch.Tensor, qsq: torch.Tensor, r: int,
+                    cand: torch.Tensor | None = None):
+    nq, M, K = lut.shape
+    ncand = cand.shape[1] if cand is not None else rec.shape[0]
+    ids = torch.empty((nq, r), dtype=I64, device=lut.device)
+    dists = torch.empty((nq, r), dtype=F64, device=lut.device)
+    native.da_adc_scan_packed(P(rec), P(cand), ncand, nq, P(lut), P(qsq), M, K, int(r), P(ids), P(dists), stream())
+    return ids, dists
+
+
 # ---------------------------------------------------------------------------
 # DA training on device (annq/annealing.py:115-262)
 

@@ -392,6 +392,27 @@ def _search_inputs(codebook, encoded, cross, pair_sums):
     return codes_d, pair_d
 
 
+def _scan(codebook, encoded, cross, pair_sums, lut, qsq, r, cand=None):
+    """Top-r ADC scan: packed 16-byte records (codes + pair sum, one sector per
+    random candidate) when the codes fit, else the generic kernel."""
+    packed = None
+    cache = getattr(encoded, "__dict__", {}).get("_packed_cache")
+    dev = E.device()
+    if pair_sums is None and cache is not None and cache[0] is encoded.codes and cache[1] is cross and cache[2] == dev:
+        packed = cache[3]
+    if packed is None:
+        codes_d, pair_d = _search_inputs(codebook, encoded, cross, pair_sums)
+        packed = E.adc_pack(codes_d, pair_d)
+        if packed is None:
+            return E.adc_scan(codes_d, pair_d, lut, qsq, r, cand=cand)
+        if pair_sums is None and cross is not None:
+            try:
+                encoded.__dict__["_packed_cache"] = (encoded.codes, cross, dev, packed)
+            except (AttributeError, TypeError):
+                pass
+    return E.adc_scan_packed(packed, lut, qsq, r, cand=cand)
+
+
 def exhaustive_adc_search(codebook: Codebook, encoded: EncodedDataset, q, r: int, cross=None,
                           pair_sums: np.ndarray | None = None):
     """Exact top-r under adc_distance, ties by lower position -> (ids int64, dists f64)."""
@@ -414,9 +435,8 @@ def exhaustive_adc_search_batch(codebook: Codebook, encoded: EncodedDataset, Q, 
         raise ValueError("queries contain non-finite values")
     _raw_kernel()
     cw, sq = _codebook_dev(codebook)
-    codes_d, pair_d = _search_inputs(codebook, encoded, cross, pair_sums)
     lut, qsq = E.adc_lut(E.to_dev(Q), cw, sq)
-    ids, dists = E.adc_scan(codes_d, pair_d, lut, qsq, r)
+    ids, dists = _scan(codebook, encoded, cross, pair_sums, lut, qsq, r)
     ids = ids.cpu().numpy()
     if encoded.id_map is not None:
         ids = encoded.id_map[ids]
@@ -439,9 +459,8 @@ def adc_rerank(codebook: Codebook, encoded: EncodedDataset, Q, candidates, r: in
     if cand.size and (cand.min() < 0 or cand.max() >= encoded.n):
         raise ValueError("candidate ids outside the encoded set")
     cw, sq = _codebook_dev(codebook)
-    codes_d, pair_d = _search_inputs(codebook, encoded, cross, pair_sums)
     lut, qsq = E.adc_lut(E.to_dev(Q), cw, sq)
-    ids, dists = E.adc_scan(codes_d, pair_d, lut, qsq, r, cand=E.to_dev(cand))
+    ids, dists = _scan(codebook, encoded, cross, pair_sums, lut, qsq, r, cand=E.to_dev(cand))
     ids = ids.cpu().numpy()
     if encoded.id_map is not None:
         ids = encoded.id_map[ids]

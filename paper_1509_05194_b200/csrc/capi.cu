@@ -347,6 +347,19 @@ int da_adc_scan(const void* codes, int code_bytes, int64_t ldc, const double* pa
                            (long long*)ids, dists, STREAM(stream));
 }
 
+int da_adc_pack(const void* codes, int code_bytes, int64_t n, int64_t ldc, const double* pair, int M,
+                void* records, void* stream) {
+    if (code_bytes != 1 || M < 1 || M > 8) return fail_arg("adc_pack: needs one-byte codes and M <= 8 (M=%d)", M);
+    if (n < 0 || ldc < M) return fail_arg("adc_pack: bad shape");
+    return launch_adc_pack(codes, n, ldc, pair, M, records, STREAM(stream));
+}
+
+int da_adc_scan_packed(const void* records, const int64_t* cand, int64_t ncand, int64_t nq, const double* lut,
+                       const double* qsq, int M, int K, int r, int64_t* ids, double* dists, void* stream) {
+    return launch_adc_scan_packed(records, (const long long*)cand, ncand, nq, lut, qsq, M, K, r, (long long*)ids,
+                                  dists, STREAM(stream));
+}
+
 int da_np_sum(const double* a, int64_t n, int divide, double* out, void* stream) {
     return launch_np_sum(a, n, divide, out, STREAM(stream));
 }

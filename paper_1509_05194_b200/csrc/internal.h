@@ -61,6 +61,11 @@ int launch_einsum_sq(const float* cw, long long rows, int D, double* out, cudaSt
 int launch_pair_sums(const void* codes, int code_bytes, long long n, long long ldc, const double* P, int M, int K,
                      double* out, cudaStream_t s);
 int launch_qsq(const double* Q, long long nq, int D, double* out, cudaStream_t s);
+int launch_adc_pack(const void* codes, long long n, long long ldc, const double* pair, int M, void* records,
+                    cudaStream_t s);
+int launch_adc_scan_packed(const void* records, const long long* cand, long long ncand, long long nq,
+                           const double* lut, const double* qsq, int M, int K, int r, long long* ids_out,
+                           double* d_out, cudaStream_t s);
 int launch_adc_scan(const void* codes, int code_bytes, long long ldc, const double* pair, const long long* cand,
                     long long ncand, long long nq, const double* lut, const double* qsq, int M, int K, int r,
                     long long* ids_out, double* d_out, cudaStream_t s);

@@ -318,6 +318,146 @@ __global__ void adc_scan_kernel(const TC* __restrict__ codes, long long ldc, con
     }
 }
 
+// Packed candidate records (M <= 8 one-byte codes): record[row] = 16 bytes,
+// codes in bytes 0..7, the row's pair sum (float64) in bytes 8..15, so one
+// random candidate costs one 32-byte sector plus its 8-byte id.
+__global__ void adc_pack_kernel(const uint8_t* __restrict__ codes, long long n, long long ldc,
+                                const double* __restrict__ pair, int M, uint4* __restrict__ rec) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        uint32_t w[2] = {0u, 0u};
+        for (int m = 0; m < M; ++m) w[m >> 2] |= (uint32_t)codes[i * ldc + m] << (8 * (m & 3));
+        const unsigned long long pb = __double_as_longlong(pair[i]);
+        rec[i] = make_uint4(w[0], w[1], (uint32_t)pb, (uint32_t)(pb >> 32));
+    }
+}
+
+int launch_adc_pack(const void* codes, long long n, long long ldc, const double* pair, int M, void* records,
+                    cudaStream_t s) {
+    if (n <= 0) return 0;
+    adc_pack_kernel<<<grid_for(n, 256), 256, 0, s>>>((const uint8_t*)codes, n, ldc, pair, M, (uint4*)records);
+    DA_CHECK_LAUNCH("adc_pack_kernel");
+    return 0;
+}
+
+// Same scan over packed records; every lane scores ADC_U candidates per step so
+// their id and record loads are in flight together.
+constexpr int ADC_U = 4;
+
+__device__ __forceinline__ double adc_rec_dist(uint4 rc, const double* slut, int M, int K, double shift) {
+    double dist = dsub(__hiloint2double((int)rc.w, (int)rc.z), shift);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        if (m < M) {
+            const uint32_t word = m < 4 ? rc.x : rc.y;
+            dist = dadd(dist, slut[m * K + (int)((word >> (8 * (m & 3))) & 0xFFu)]);
+        }
+    }
+    return dist;
+}
+
+__global__ void adc_scan_packed_kernel(const uint4* __restrict__ rec, const long long* __restrict__ cand,
+                                       long long ncand, const double* __restrict__ lut,
+                                       const double* __restrict__ qsq, int M, int K, int r,
+                                       long long* __restrict__ ids_out, double* __restrict__ d_out) {
+    extern __shared__ __align__(16) char smem[];
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const long long q = blockIdx.x;
+    double* slut = (double*)smem;
+    const int MK = M * K;
+    for (int i = threadIdx.x; i < MK; i += blockDim.x) slut[i] = lut[q * MK + i];
+    double* lv_base = slut + MK;
+    long long* lp_base = (long long*)(lv_base + (size_t)nw * r);
+    __syncthreads();
+    TopList L{lv_base + (size_t)wid * r, lp_base + (size_t)wid * r};
+    int cnt = 0;
+    const double shift = dmul((double)(M - 1), qsq[q]);
+    const long long* qc = cand ? cand + q * ncand : nullptr;
+    for (long long b = (long long)wid * 32 * ADC_U; b < ncand; b += (long long)nw * 32 * ADC_U) {
+        long long pp[ADC_U], row[ADC_U];
+        uint4 rc[ADC_U];
+#pragma unroll
+        for (int u = 0; u < ADC_U; ++u) {
+            pp[u] = b + u * 32 + lane;
+            row[u] = pp[u] < ncand ? (qc ? __ldg(qc + pp[u]) : pp[u]) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < ADC_U; ++u) rc[u] = row[u] >= 0 ? __ldg(rec + row[u]) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < ADC_U; ++u) {
+            const bool valid = row[u] >= 0;
+            const double dist = valid ? adc_rec_dist(rc[u], slut, M, K, shift) : 0.0;
+            const long long p = pp[u];
+            auto accept = [&](double a, long long pa) -> bool {
+                if (cnt < r) return true;
+                return lex_less(a, pa, L.v[r - 1], L.p[r - 1]);
+            };
+            unsigned mask = __ballot_sync(FULL, valid && accept(dist, p));
+            while (mask) {
+                const int src = __ffs(mask) - 1;
+                const double cv = __shfl_sync(FULL, dist, src);
+                const long long cp = __shfl_sync(FULL, p, src);
+                warp_insert(L, cnt, r, cv, cp);
+                mask &= ~(1u << src);
+                mask &= __ballot_sync(FULL, valid && accept(dist, p));
+            }
+        }
+    }
+    __shared__ int cnts[32];
+    if (lane == 0) cnts[wid] = cnt;
+    __syncthreads();
+    if (wid == 0) {
+        for (int w = 1; w < nw; ++w) {
+            TopList O{lv_base + (size_t)w * r, lp_base + (size_t)w * r};
+            const int oc = cnts[w];
+            for (int b2 = 0; b2 < oc; b2 += 32) {
+                const int i = b2 + lane;
+                const bool valid = i < oc;
+                double cv = valid ? O.v[i] : 0.0;
+                long long cp = valid ? O.p[i] : 0;
+                auto accept = [&](double a, long long pa) -> bool {
+                    if (cnt < r) return true;
+                    return lex_less(a, pa, L.v[r - 1], L.p[r - 1]);
+                };
+                unsigned mask = __ballot_sync(FULL, valid && accept(cv, cp));
+                while (mask) {
+                    const int src = __ffs(mask) - 1;
+                    const double v = __shfl_sync(FULL, cv, src);
+                    const long long pp2 = __shfl_sync(FULL, cp, src);
+                    warp_insert(L, cnt, r, v, pp2);
+                    mask &= ~(1u << src);
+                    mask &= __ballot_sync(FULL, valid && accept(cv, cp));
+                }
+            }
+        }
+        for (int i = lane; i < cnt; i += 32) {
+            const long long p = L.p[i];
+            ids_out[q * r + i] = qc ? qc[p] : p;
+            d_out[q * r + i] = L.v[i];
+        }
+    }
+}
+
+int launch_adc_scan_packed(const void* records, const long long* cand, long long ncand, long long nq,
+                           const double* lut, const double* qsq, int M, int K, int r, long long* ids_out,
+                           double* d_out, cudaStream_t s) {
+    if (nq <= 0) return 0;
+    if (M < 1 || M > 8 || K > 256) return fail_arg("adc_scan_packed: needs M <= 8 one-byte codes (M=%d K=%d)", M, K);
+    if (r < 1 || r > ncand) return fail_arg("r=%d must be in [1, %lld]", r, ncand);
+    const size_t lut_b = sizeof(double) * (size_t)M * K;
+    int warps = 8;
+    while (warps > 1 && lut_b + (size_t)warps * r * 16 > 200 * 1024) warps >>= 1;
+    const size_t smem = lut_b + (size_t)warps * r * 16;
+    if (smem > 220 * 1024) return fail_arg("adc_scan: r=%d with M*K=%d exceeds shared memory", r, M * K);
+    ProfScope ps("adc_scan_packed", s);
+    if (smem > 48 * 1024)
+        DA_CUDA(cudaFuncSetAttribute(adc_scan_packed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    adc_scan_packed_kernel<<<(unsigned)nq, warps * 32, smem, s>>>((const uint4*)records, cand, ncand, lut, qsq, M, K,
+                                                                 r, ids_out, d_out);
+    DA_CHECK_LAUNCH("adc_scan_packed_kernel");
+    return 0;
+}
+
 int launch_adc_scan(const void* codes, int code_bytes, long long ldc, const double* pair, const long long* cand,
                     long long ncand, long long nq, const double* lut, const double* qsq, int M, int K, int r,
                     long long* ids_out, double* d_out, cudaStream_t s) {
