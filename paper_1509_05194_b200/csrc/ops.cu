@@ -343,6 +343,15 @@ int launch_adc_pack(const void* codes, long long n, long long ldc, const double*
 // their id and record loads are in flight together.
 constexpr int ADC_U = 4;
 
+// one random 16-byte record: no L1 allocation, smallest L2 prefetch granule
+__device__ __forceinline__ uint4 adc_ld_rec(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
 __device__ __forceinline__ double adc_rec_dist(uint4 rc, const double* slut, int M, int K, double shift) {
     double dist = dsub(__hiloint2double((int)rc.w, (int)rc.z), shift);
 #pragma unroll
@@ -382,7 +391,7 @@ __global__ void adc_scan_packed_kernel(const uint4* __restrict__ rec, const long
             row[u] = pp[u] < ncand ? (qc ? __ldg(qc + pp[u]) : pp[u]) : -1;
         }
 #pragma unroll
-        for (int u = 0; u < ADC_U; ++u) rc[u] = row[u] >= 0 ? __ldg(rec + row[u]) : make_uint4(0, 0, 0, 0);
+        for (int u = 0; u < ADC_U; ++u) rc[u] = row[u] >= 0 ? adc_ld_rec(rec + row[u]) : make_uint4(0, 0, 0, 0);
 #pragma unroll
         for (int u = 0; u < ADC_U; ++u) {
             const bool valid = row[u] >= 0;
