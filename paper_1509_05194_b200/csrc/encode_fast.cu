@@ -194,7 +194,8 @@ __device__ inline FastSmem carve_fast(char* p, int cap, int M, int K, int D) {
 }
 
 // exact x.c (reference order: FMA chain over d, OpenBLAS k-blocks above 384)
-__device__ __forceinline__ double exact_dot(const double* __restrict__ x64, const double* __restrict__ c, int D) {
+__device__ __forceinline__ double exact_dot(const double* __restrict__ x64, const double* __restrict__ c, int D,
+                                            const float* __restrict__ c32 = nullptr) {
     double tot = 0.0;
     bool first = true;
     int d = 0;
@@ -202,7 +203,22 @@ __device__ __forceinline__ double exact_dot(const double* __restrict__ x64, cons
         const int len = (int)blas_block_len(D - d);
         double acc = 0.0;
         const int e = d + len;
-        // loads run ahead of the (strictly sequential) FMA chain
+        // loads run ahead of the (strictly sequential) FMA chain: 16 codeword values
+        // per batch, fp32 in memory (exact in float64) so a batch is 4 vector loads
+        if (c32) {
+            for (; d + 32 <= e; d += 32) {
+                float4 cv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) cv[u] = __ldg(reinterpret_cast<const float4*>(c32 + d) + u);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    acc = __fma_rn(x64[d + 4 * u + 0], (double)cv[u].x, acc);
+                    acc = __fma_rn(x64[d + 4 * u + 1], (double)cv[u].y, acc);
+                    acc = __fma_rn(x64[d + 4 * u + 2], (double)cv[u].z, acc);
+                    acc = __fma_rn(x64[d + 4 * u + 3], (double)cv[u].w, acc);
+                }
+            }
+        }
         for (; d + 8 <= e; d += 8) {
             double cv[8];
             double xv[8];
@@ -233,6 +249,8 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
     const long long v = (long long)blockIdx.x * nwarps + wid;
     if (v >= n) return;
     FastSmem S = carve_fast(smem_raw + (size_t)wid * fast_smem_bytes(cap, M, K, D), cap, M, K, D);
+    // 16-byte aligned fp32 codeword rows (D % 4 == 0): vector loads in the exact dot
+    const bool c32ok = (D & 3) == 0 && ((reinterpret_cast<uintptr_t>(cw) & 15) == 0);
     const float* trow = tab32 + v * (long long)M * K;
     const TX* xr = X + v * ldx;
     // x in float64 (exact widening) and ||x||
@@ -421,7 +439,8 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
         __syncwarp();
         auto exact_value = [&](int flat) -> double {
             const int l = flat / K, k = flat % K;
-            const double xc = exact_dot(S.x64, cw64 + ((long long)m * K + k) * D, D);
+            const double xc = exact_dot(S.x64, cw64 + ((long long)m * K + k) * D, D,
+                                        c32ok ? cw + ((long long)m * K + k) * D : nullptr);
             const double t = dsub(sq[m * K + k], dmul(2.0, xc));
             double cross = 0.0;
             for (int j = 0; j < m; ++j) cross = dadd(cross, P[(((long long)j * M + m) * K + pc[l * M + j]) * K + k]);
