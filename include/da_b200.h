@@ -122,7 +122,7 @@ int da_encode(const void* X, int x_f32, int64_t n, int64_t ldx, int D, const flo
               void* stream);
 
 /* Encoder selection (all modes return identical codes/errors):
- *   0 (default) = by beam width: 3 for L <= 6 or L >= 16, else 2 (measured crossover on
+ *   0 (default) = by beam width: 3 for L <= 4 or L >= 24, else 2 (measured crossover on
  *       B200, config B); 1 = plain float64 score tables;
  *   2 = fp32 score table + fp32 cross-table gathers as a filter with a rigorous
  *       error bound, exact float64 recheck of the candidates that can still make the beam;

@@ -371,9 +371,11 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
                                        fminf(fminf(vv[4], vv[5]), fminf(vv[6], vv[7])));
                     if (bmin < m2) {
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            if (vv[q] < m1) { m2 = m1; m1 = vv[q]; i1 = l * K + kof(kb, q); }
-                            else if (vv[q] < m2) m2 = vv[q];
+                        for (int q = 0; q < 8; ++q) {   // branch-free two-smallest + first argmin
+                            const float w = vv[q];
+                            i1 = w < m1 ? l * K + kof(kb, q) : i1;
+                            m2 = fminf(m2, fmaxf(m1, w));
+                            m1 = fminf(m1, w);
                         }
                     }
                 }
