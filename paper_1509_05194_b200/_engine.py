@@ -187,11 +187,34 @@ def lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, c
     iters = 0
     counts = torch.empty(K, dtype=I32, device=dev)
     sums = torch.empty((K, D), dtype=F64, device=dev) if comm is not None else None
-    for _ in range(max_iters):
-        if comm is None:
+    if comm is None:
+        # one host sync per iteration: the assign runs speculatively on the updated
+        # centroids and is redone (after the host reseed) only when a cluster emptied
+        flags = torch.zeros(2, dtype=torch.int64, device=dev)   # [changed rows, empty clusters]
+        for _ in range(max_iters):
             native.da_group_sums(P(Xr), n, Xr.stride(0), D, P(labels), K, 0, P(C), C.stride(0), P(counts),
                                  stream())
-            counts_h = counts.cpu().numpy()
+            flags.zero_()
+            flags[1:2].copy_((counts == 0).sum().view(1))
+            new_labels, errs_new = assign(Xr, active, C, prev=labels, changed=flags[0:1], xx=xx)
+            fh = flags.cpu().numpy()
+            if fh[1]:
+                empty = np.flatnonzero(counts.cpu().numpy() == 0)
+                _reseed_single(Xr, errs, empty, C)
+                flags.zero_()
+                new_labels, errs_new = assign(Xr, active, C, prev=labels, changed=flags[0:1], xx=xx)
+                fh = flags.cpu().numpy()
+            errs = errs_new
+            iters += 1
+            trace_d[iters:iters + 1] = np_mean(errs, comm)
+            labels = new_labels
+            if int(fh[0]) == 0:
+                break
+        trace = trace_d[: iters + 1].cpu().tolist()
+        return C, labels, trace
+    for _ in range(max_iters):
+        if comm is None:
+            raise AssertionError("unreachable")
         else:
             if n:
                 native.da_group_sums(P(Xr), n, Xr.stride(0), D, P(labels), K, 1, P(sums), sums.stride(0),
