@@ -191,9 +191,15 @@ def lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, c
         # one host sync per iteration: the assign runs speculatively on the updated
         # centroids and is redone (after the host reseed) only when a cluster emptied
         flags = torch.zeros(2, dtype=torch.int64, device=dev)   # [changed rows, empty clusters]
+        # Only the active prefix feeds the assignments, so the iterations average the
+        # active columns; the remaining columns are averaged once at the end over the
+        # labels of the last update (per-column sums: identical bits).  Reseeds write
+        # whole rows, as in the reference.
+        gs_labels = None
         for _ in range(max_iters):
-            native.da_group_sums(P(Xr), n, Xr.stride(0), D, P(labels), K, 0, P(C), C.stride(0), P(counts),
+            native.da_group_sums(P(Xr), n, Xr.stride(0), active, P(labels), K, 0, P(C), C.stride(0), P(counts),
                                  stream())
+            gs_labels = labels
             flags.zero_()
             flags[1:2].copy_((counts == 0).sum().view(1))
             new_labels, errs_new = assign(Xr, active, C, prev=labels, changed=flags[0:1], xx=xx)
@@ -210,6 +216,9 @@ def lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, c
             labels = new_labels
             if int(fh[0]) == 0:
                 break
+        if gs_labels is not None and active < D:
+            native.da_group_sums(P(Xr), n, Xr.stride(0), D, P(gs_labels), K, 0, P(C), C.stride(0), P(counts),
+                                 stream())
         trace = trace_d[: iters + 1].cpu().tolist()
         return C, labels, trace
     for _ in range(max_iters):
