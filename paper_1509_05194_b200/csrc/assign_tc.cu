@@ -14,6 +14,8 @@
 // split) in the canonical K-major no-swizzle UMMA layout; one elected thread
 // issues the MMAs and commits them to an mbarrier.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 
 #include "common.cuh"
@@ -116,7 +118,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 template <typename TX>
 __device__ __forceinline__ double fma_chain(const TX* __restrict__ xr, const double* __restrict__ cr, int k, int e,
                                             double acc) {
-    // loads are issued 8 ahead of the (strictly sequential) FMA chain
+    // loads are issued 24 ahead of the (strictly sequential) FMA chain
+    for (; k + 24 <= e; k += 24) {
+        double xv[24], cv[24];
+#pragma unroll
+        for (int u = 0; u < 24; ++u) { xv[u] = (double)xr[k + u]; cv[u] = cr[k + u]; }
+#pragma unroll
+        for (int u = 0; u < 24; ++u) acc = __fma_rn(xv[u], cv[u], acc);
+    }
     for (; k + 8 <= e; k += 8) {
         double xv[8], cv[8];
 #pragma unroll
@@ -188,12 +197,23 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // the tensor cores work on tile i.
 constexpr int TC_T2 = 256;
 
+__device__ unsigned long long g_at_prof[8];
+#define AT_MARK(i)                                                   \
+    do {                                                             \
+        if (tid == 0) {                                              \
+            const long long _t = clock64();                          \
+            at_acc[i] += _t - at_t;                                  \
+            at_t = _t;                                               \
+        }                                                            \
+    } while (0)
+
 template <typename TX>
 __global__ void __launch_bounds__(TC_T2, 1) assign_tc_kernel(
     const TX* __restrict__ X, long long n, long long ldx, int d, const double* __restrict__ C, long long ldc, int K,
     const double* __restrict__ cc, const double* __restrict__ xx_in, const float* __restrict__ Bg,
     int32_t* __restrict__ labels, double* __restrict__ d2_out, const int32_t* __restrict__ prev,
-    unsigned long long* __restrict__ changed, unsigned long long* __restrict__ stats) {
+    unsigned long long* __restrict__ changed, unsigned long long* __restrict__ stats,
+    int* __restrict__ ovf_rows, int* __restrict__ ovf_cnt) {
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int A_ELEMS = TC_M * TC_BK, B_ELEMS = TC_NMAX * TC_BK;
     float* Abuf = reinterpret_cast<float*>(smem);                    // [2 stages][hi, lo][A_ELEMS]
@@ -251,6 +271,8 @@ __global__ void __launch_bounds__(TC_T2, 1) assign_tc_kernel(
         bulk_g2s(Bbuf, Bg, (uint32_t)(2 * B_ELEMS * sizeof(float)), &full_bar[0]);
     }
 
+    long long at_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // phase clocks (thread 0, DA_DEBUG)
+    long long at_t = clock64();
     const int erow = tid & (TC_M - 1);   // TMEM lane / tile row owned in the epilogue
     const int ehalf = tid >> 7;          // 0: codewords [0,128), 1: [128,256)
     auto epilogue = [&](long long tile, int accb) {
@@ -280,6 +302,7 @@ __global__ void __launch_bounds__(TC_T2, 1) assign_tc_kernel(
         }
         wmin_h[ehalf * TC_M + erow] = (double)wminf;
         __syncthreads();
+        AT_MARK(3);
         const double wmin = fmin(wmin_h[erow], wmin_h[TC_M + erow]);
         const double ub = fmax(xx + wmin + E, 0.0);
         // candidate k iff max(xx + w'_k - E, 0) <= ub  <=>  w'_k <= ub - xx + E (ub >= 0)
@@ -303,6 +326,7 @@ __global__ void __launch_bounds__(TC_T2, 1) assign_tc_kernel(
         ncand[ehalf * TC_M + erow] = nc;
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncthreads();
+        AT_MARK(4);
         if (ehalf != 0 || !valid) return;
         double best = __longlong_as_double(0x7ff0000000000000ULL);
         int bk = 0x7fffffff;
@@ -315,18 +339,34 @@ __global__ void __launch_bounds__(TC_T2, 1) assign_tc_kernel(
         };
         const int n0 = ncand[erow], n1 = ncand[TC_M + erow];
         const bool overflow = n0 > TC_CMAX || n1 > TC_CMAX;
-        if (!overflow) {
-            for (int i = 0; i < n0; ++i) consider(cand[erow * TC_CMAX + i]);
-            for (int i = 0; i < n1; ++i) consider(cand[(TC_M + erow) * TC_CMAX + i]);
-        } else {
-            for (int k = 0; k < K; ++k) consider(k);
+        if (overflow) {
+            // too many near-ties for this thread: a warp-parallel exact scan over all K
+            // runs after the kernel (assign_overflow_kernel) instead of stalling the CTA
+            ovf_rows[atomicAdd(ovf_cnt, 1)] = (int)r;
+            if (stats) atomicAdd(stats, (unsigned long long)K);
+            return;
         }
+        for (int i = 0; i < n0; ++i) consider(cand[erow * TC_CMAX + i]);
+        for (int i = 0; i < n1; ++i) consider(cand[(TC_M + erow) * TC_CMAX + i]);
         labels[r] = bk;
         d2_out[r] = best;
-        if (stats) atomicAdd(stats, (unsigned long long)(overflow ? K : n0 + n1));
+        if (stats) atomicAdd(stats, (unsigned long long)(n0 + n1));
         if (changed != nullptr && prev != nullptr && prev[r] != bk) atomicAdd(changed, 1ULL);
     };
 
+    double xv_next[16];
+    auto load_chunk = [&](long long tl, int chn) {
+        const long long rb = tl * TC_M;
+#pragma unroll
+        for (int it2 = 0; it2 < 16; ++it2) {
+            const int rg = it2 >> 3, kg = it2 & 7;
+            const int rr = warp * (TC_M / 8) + rg * 8 + (lane >> 2);
+            const int gk = chn * TC_BK + kg * 4 + (lane & 3);
+            const long long r = rb + rr;
+            xv_next[it2] = (tl < ntiles && r < n && gk < d) ? (double)X[r * ldx + gk] : 0.0;
+        }
+    };
+    if ((long long)blockIdx.x < ntiles) load_chunk(blockIdx.x, 0);
     long long q = 0;  // (tile, chunk) steps issued by this CTA
     long long it = 0; // tiles issued by this CTA
     long long prev_tile = -1;
@@ -346,15 +386,18 @@ __global__ void __launch_bounds__(TC_T2, 1) assign_tc_kernel(
             // stage 16 rows per warp as 8x4 blocks: lane -> (row 8-group row L/4,
             // k = 4-group + L%4).  Each block is one 8x16-B core matrix in shared
             // memory (all 32 banks once) and 8 full 32-B sectors in global memory.
+            // The values were loaded one step earlier (xv_next) so the loads overlap
+            // the previous barrier, MMA issue and epilogue.
             const int k0 = ch * TC_BK;
             double xv[16];
 #pragma unroll
-            for (int it2 = 0; it2 < 16; ++it2) {
-                const int rg = it2 >> 3, kg = it2 & 7;
-                const int rr = warp * (TC_M / 8) + rg * 8 + (lane >> 2);
-                const int gk = k0 + kg * 4 + (lane & 3);
-                const long long r = row0 + rr;
-                xv[it2] = (r < n && gk < d) ? (double)X[r * ldx + gk] : 0.0;
+            for (int it2 = 0; it2 < 16; ++it2) xv[it2] = xv_next[it2];
+            {
+                // prefetch the next (tile, chunk) step of this CTA
+                long long ntile = tile;
+                int nchunk = ch + 1;
+                if (nchunk == nch) { nchunk = 0; ntile = tile + gridDim.x; }
+                load_chunk(ntile, nchunk);
             }
 #pragma unroll
             for (int it2 = 0; it2 < 16; ++it2) {
@@ -368,6 +411,7 @@ __global__ void __launch_bounds__(TC_T2, 1) assign_tc_kernel(
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();
+            AT_MARK(0);
             if (tid == 0) {
                 if (!b_resident) mbar_wait(&full_bar[st], (uint32_t)((q >> 1) & 1));
                 else if (q == 0) mbar_wait(&full_bar[0], 0);
@@ -386,12 +430,15 @@ __global__ void __launch_bounds__(TC_T2, 1) assign_tc_kernel(
                 mma_commit(&empty_bar[st]);
                 if (ch == nch - 1) mma_commit(&acc_bar[accb]);
             }
+            AT_MARK(1);
         }
         if (prev_tile >= 0) {
             const int pb = (int)((it - 1) & 1);
             mbar_wait(&acc_bar[pb], (uint32_t)(((it - 1) >> 1) & 1));
+            AT_MARK(2);
             asm volatile("tcgen05.fence::after_thread_sync;");
             epilogue(prev_tile, pb);
+            AT_MARK(5);
         }
         prev_tile = tile;
     }
@@ -401,11 +448,53 @@ __global__ void __launch_bounds__(TC_T2, 1) assign_tc_kernel(
         asm volatile("tcgen05.fence::after_thread_sync;");
         epilogue(prev_tile, pb);
     }
+    if (tid == 0)
+        for (int i = 0; i < 8; ++i) atomicAdd(&g_at_prof[i], (unsigned long long)at_acc[i]);
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TC_NMAX));
+    }
+}
+
+// Rows whose candidate lists overflowed: one warp per row, lanes split the K
+// codewords (each an exact BLAS-ordered dot), lexicographic (d2, k) warp minimum.
+template <typename TX>
+__global__ void assign_overflow_kernel(const TX* __restrict__ X, long long ldx, int d, const double* __restrict__ C,
+                                       long long ldc, int K, const double* __restrict__ cc,
+                                       const double* __restrict__ xx_in, const int* __restrict__ rows,
+                                       const int* __restrict__ cnt, int32_t* __restrict__ labels,
+                                       double* __restrict__ d2_out, const int32_t* __restrict__ prev,
+                                       unsigned long long* __restrict__ changed) {
+    const int lane = threadIdx.x & 31;
+    const int nrows = *cnt;
+    const bool blk = d > (int)BLAS_Q;
+    for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nrows;
+         w += ((long long)gridDim.x * blockDim.x) >> 5) {
+        const long long r = rows[w];
+        const TX* xr = X + r * ldx;
+        const double xx = xx_in ? xx_in[r]
+                                : np_pw_sum([&](long long i) { double t = (double)xr[i]; return dmul(t, t); }, 0, d);
+        double best = __longlong_as_double(0x7ff0000000000000ULL);
+        int bk = 0x7fffffff;
+        for (int k = lane; k < K; k += 32) {
+            const double* crow = C + (long long)k * ldc;
+            const double xc = blk ? exact_xc<TX, true>(xr, crow, d) : exact_xc<TX, false>(xr, crow, d);
+            double dv = dadd(dsub(xx, dmul(2.0, xc)), cc[k]);
+            if (dv < 0.0) dv = 0.0;
+            if (lex_less(dv, k, best, bk)) { best = dv; bk = k; }
+        }
+        for (int off = 16; off >= 1; off >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+            const int ok = __shfl_xor_sync(0xffffffffu, bk, off);
+            if (lex_less(ob, ok, best, bk)) { best = ob; bk = ok; }
+        }
+        if (lane == 0) {
+            labels[r] = bk;
+            d2_out[r] = best;
+            if (changed != nullptr && prev != nullptr && prev[r] != bk) atomicAdd(changed, 1ULL);
+        }
     }
 }
 
@@ -416,8 +505,13 @@ int launch_assign_tc(const void* X, int x_is_f32, long long n, long long ldx, in
     if (K > TC_NMAX || K < 1 || d < 1) return 1;
     if (n <= 0) return 0;
     const int nch = (d + TC_BK - 1) / TC_BK;
-    float* Bg = (float*)scratch(9, sizeof(float) * (size_t)nch * 2 * TC_NMAX * TC_BK, s);
-    if (!Bg) return fail_cuda(cudaErrorMemoryAllocation, "assign_tc scratch");
+    const size_t bg_bytes = (sizeof(float) * (size_t)nch * 2 * TC_NMAX * TC_BK + 255) & ~size_t(255);
+    char* base = (char*)scratch(9, bg_bytes + sizeof(int) * ((size_t)n + 64), s);
+    if (!base) return fail_cuda(cudaErrorMemoryAllocation, "assign_tc scratch");
+    float* Bg = (float*)base;
+    int* ovf_cnt = (int*)(base + bg_bytes);
+    int* ovf_rows = ovf_cnt + 64;
+    DA_CUDA(cudaMemsetAsync(ovf_cnt, 0, sizeof(int), s));
     ProfScope ps(d <= 8 ? "assign_tc_d<=8" : d <= 32 ? "assign_tc_d<=32" : d <= 128 ? "assign_tc_d<=128" : "assign_tc_d>128",
                  s);
     cw_tf32_prep_kernel<<<grid_for((long long)nch * TC_NMAX * TC_BK, 256, 4096), 256, 0, s>>>(C, ldc, K, d, nch, Bg);
@@ -434,14 +528,35 @@ int launch_assign_tc(const void* X, int x_is_f32, long long n, long long ldx, in
         auto kf = assign_tc_kernel<float>;
         DA_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         kf<<<grid, TC_T2, smem, s>>>((const float*)X, n, ldx, d, C, ldc, K, cc, xx, Bg, labels, d2, prev, changed,
-                                     stats);
+                                     stats, ovf_rows, ovf_cnt);
+        DA_CHECK_LAUNCH("assign_tc_kernel");
+        assign_overflow_kernel<float><<<sms, 256, 0, s>>>((const float*)X, ldx, d, C, ldc, K, cc, xx, ovf_rows, ovf_cnt,
+                                                          labels, d2, prev, changed);
     } else {
         auto kf = assign_tc_kernel<double>;
         DA_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         kf<<<grid, TC_T2, smem, s>>>((const double*)X, n, ldx, d, C, ldc, K, cc, xx, Bg, labels, d2, prev, changed,
-                                     stats);
+                                     stats, ovf_rows, ovf_cnt);
+        DA_CHECK_LAUNCH("assign_tc_kernel");
+        assign_overflow_kernel<double><<<sms, 256, 0, s>>>((const double*)X, ldx, d, C, ldc, K, cc, xx, ovf_rows,
+                                                           ovf_cnt, labels, d2, prev, changed);
     }
-    DA_CHECK_LAUNCH("assign_tc_kernel");
+    DA_CHECK_LAUNCH("assign_overflow_kernel");
+    if (getenv("DA_DEBUG")) {
+        unsigned long long hp[8];
+        cudaStreamSynchronize(s);
+        cudaMemcpyFromSymbol(hp, g_at_prof, sizeof(hp));
+        unsigned long long tot = 0;
+        for (int i = 0; i < 6; ++i) tot += hp[i];
+        const char* nm[6] = {"stage", "mma_issue", "acc_wait", "pass1", "pass2", "recheck"};
+        fprintf(stderr, "[da] assign_tc d=%d phases:", d);
+        for (int i = 0; i < 6; ++i) fprintf(stderr, " %s %.1f%%", nm[i], tot ? 100.0 * hp[i] / tot : 0.0);
+        int hc = 0;
+        cudaMemcpy(&hc, ovf_cnt, sizeof(int), cudaMemcpyDeviceToHost);
+        fprintf(stderr, " overflow_rows %d\n", hc);
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_at_prof, z, sizeof(z));
+    }
     return 0;
 }
 
