@@ -384,6 +384,20 @@ def main():
                 "algorithmic": f"{tab_b + M} B per vector (score table read + codes write)"}
     roof["peak_source"] = "MEASURED_PEAKS.json (HBM) / profiles/peaks_r01.jsonl (FFMA, DFMA: measured on this pool)"
     roof["share_of_step"] = tot_ms / ms_local
+    # DRAM traffic of this kernel per launch, from the committed ncu --set full capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")) as f:
+            tr = json.load(f).get(name)
+        if tr:
+            roof["traffic"] = tr["bytes_per_vector"] * rows_per_launch
+            roof["traffic_source"] = "profiles/ncu_traffic_r01.json: " + tr["capture"]
+    except (OSError, ValueError, KeyError):
+        pass
+    # the whole encode step against BASELINE's compute roofline (2*M*K*D flop per vector)
+    step_tflops = 2.0 * M * K * D * value / world / 1e12
+    roof["encode_step_compute"] = {"achieved": step_tflops, "peak": pk["fp32_ffma_tflops"], "unit": "TFLOP/s",
+                                   "frac": step_tflops / pk["fp32_ffma_tflops"],
+                                   "note": "2*M*K*D flop per vector at the step rate vs measured FP32 FFMA peak"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
