@@ -234,6 +234,15 @@ __device__ __forceinline__ double exact_dot(const double* __restrict__ x64, cons
     return tot;
 }
 
+// float <-> unsigned key with the same order (for redux.sync.min)
+__device__ __forceinline__ unsigned fkey(float f) {
+    const unsigned b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float funkey(unsigned k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
 template <typename TX>
 __global__ void __launch_bounds__(256) beam_fast_kernel(
     const TX* __restrict__ X, long long n, long long ldx, int D, const float* __restrict__ cw, int M, int K, int L,
@@ -251,6 +260,10 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
     FastSmem S = carve_fast(smem_raw + (size_t)wid * fast_smem_bytes(cap, M, K, D), cap, M, K, D);
     // 16-byte aligned fp32 codeword rows (D % 4 == 0): vector loads in the exact dot
     const bool c32ok = (D & 3) == 0 && ((reinterpret_cast<uintptr_t>(cw) & 15) == 0);
+    // power-of-two shapes index with shifts instead of integer division
+    const int nkb = (K + 31) / 32;
+    const int nkb_sh = (nkb & (nkb - 1)) == 0 ? __ffs(nkb) - 1 : -1;
+    const int k_sh = (K & (K - 1)) == 0 ? __ffs(K) - 1 : -1;
     const float* trow = tab32 + v * (long long)M * K;
     const TX* xr = X + v * ldx;
     // x in float64 (exact widening) and ||x||
@@ -388,20 +401,19 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
         if (width >= total) {
             thr = __int_as_float(0x7f800000);
         } else if (width <= 64) {
-            const float a = m1, b = m2;
-            int r0 = 0, r1 = 0;
-            for (int s2 = 0; s2 < 32; ++s2) {
-                const float o0 = __shfl_sync(FULL, a, s2), o1 = __shfl_sync(FULL, b, s2);
-                r0 += (o0 < a) || (o0 == a && s2 < lane);
-                r0 += (o1 < a);
-                r1 += (o0 < b) || (o0 == b);
-                r1 += (o1 < b) || (o1 == b && s2 < lane);
+            // multiway merge of the lanes' sorted pairs (m1 <= m2): each step takes the
+            // warp minimum (redux.sync on order-preserving keys); the owner shifts
+            float h0 = m1, h1 = m2;
+            unsigned key = 0u;
+            for (int step = 0; step < width; ++step) {
+                const unsigned mk = fkey(h0);
+                key = __reduce_min_sync(FULL, mk);
+                const unsigned own = __ballot_sync(FULL, mk == key);
+                const bool adv = lane == __ffs(own) - 1;
+                h0 = adv ? h1 : h0;
+                h1 = adv ? __int_as_float(0x7f800000) : h1;
             }
-            float t0 = (r0 == width - 1) ? a : -__int_as_float(0x7f800000);
-            float t1 = (r1 == width - 1) ? b : -__int_as_float(0x7f800000);
-            float t = fmaxf(t0, t1);
-            for (int off = 16; off >= 1; off >>= 1) t = fmaxf(t, __shfl_xor_sync(FULL, t, off));
-            thr = t;
+            thr = funkey(key);
         } else {
             thr = __int_as_float(0x7f800000);  // wide beams: recheck everything
         }
@@ -420,14 +432,14 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
             if (slot < QCAP) S.queue[33 + slot] = i1;
         }
         unsigned flagged = __ballot_sync(FULL, multi);
-        const int per_lane = live * ((K + 31) / 32);
+        const int per_lane = live * nkb;
         while (flagged) {
             const int f = __ffs(flagged) - 1;
             flagged &= flagged - 1;
             for (int t = lane; t < per_lane; t += 32) {
                 // t enumerates (l, kb, q) of lane f's candidates
-                const int l = t / ((K + 31) / 32);
-                const int rem = t % ((K + 31) / 32);
+                const int l = nkb_sh >= 0 ? t >> nkb_sh : t / nkb;
+                const int rem = t - l * nkb;
                 const int kb = (rem >> 3) * 256, q = rem & 7;
                 const int k = vec ? kb + (q >> 2) * 128 + 4 * f + (q & 3) : kb + 32 * q + f;
                 if (k < K && S.vbuf[l * K + k] <= limf) {
@@ -440,7 +452,8 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
         const int nqueued = *qcount;
         __syncwarp();
         auto exact_value = [&](int flat) -> double {
-            const int l = flat / K, k = flat % K;
+            const int l = k_sh >= 0 ? flat >> k_sh : flat / K;
+            const int k = flat - l * K;
             const double xc = exact_dot(S.x64, cw64 + ((long long)m * K + k) * D, D,
                                         c32ok ? cw + ((long long)m * K + k) * D : nullptr);
             const double t = dsub(sq[m * K + k], dmul(2.0, xc));
@@ -536,7 +549,7 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
                 const int fi = S.lf[i];
                 int rank = 0;
                 for (int j = 0; j < width; ++j) rank += (S.lf[j] < fi);
-                const int parent = fi / K, kk = fi % K;
+                const int parent = k_sh >= 0 ? fi >> k_sh : fi / K, kk = fi - parent * K;
                 for (int j = 0; j < m; ++j) nc[rank * M + j] = pc[parent * M + j];
                 nc[rank * M + m] = kk;
                 ns[rank] = S.lv[i];
