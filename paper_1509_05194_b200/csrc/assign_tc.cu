@@ -354,65 +354,60 @@ __global__ void __launch_bounds__(TC_T2, 1) assign_tc_kernel(
         if (changed != nullptr && prev != nullptr && prev[r] != bk) atomicAdd(changed, 1ULL);
     };
 
-    double xv_next[16];
-    auto load_chunk = [&](long long tl, int chn) {
-        const long long rb = tl * TC_M;
-#pragma unroll
-        for (int it2 = 0; it2 < 16; ++it2) {
-            const int rg = it2 >> 3, kg = it2 & 7;
-            const int rr = warp * (TC_M / 8) + rg * 8 + (lane >> 2);
-            const int gk = chn * TC_BK + kg * 4 + (lane & 3);
-            const long long r = rb + rr;
-            xv_next[it2] = (tl < ntiles && r < n && gk < d) ? (double)X[r * ldx + gk] : 0.0;
-        }
-    };
-    if ((long long)blockIdx.x < ntiles) load_chunk(blockIdx.x, 0);
+    // Warp roles: warps 4-7 stage the row tiles and issue the MMAs (thread 128);
+    // warps 0-3 do the exact rechecks of the previous tile meanwhile.  Both halves
+    // run the two epilogue passes together.
+    const bool stager = warp >= 4;
     long long q = 0;  // (tile, chunk) steps issued by this CTA
     long long it = 0; // tiles issued by this CTA
     long long prev_tile = -1;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int accb = (int)(it & 1);
         const long long row0 = tile * TC_M;
+        if (!stager) {
+            q += nch;
+        } else {
         for (int ch = 0; ch < nch; ++ch, ++q) {
             const int st = (int)(q & 1);
             if (q >= 2) mbar_wait(&empty_bar[st], (uint32_t)(((q >> 1) - 1) & 1));
             float* Ah = Abuf + st * 2 * A_ELEMS;
             float* Al = Ah + A_ELEMS;
             float* Bs = b_resident ? Bbuf : Bbuf + st * 2 * B_ELEMS;
-            if (!b_resident && tid == 0) {
+            if (!b_resident && tid == 128) {
                 mbar_arrive_expect_tx(&full_bar[st], (uint32_t)(2 * B_ELEMS * sizeof(float)));
                 bulk_g2s(Bs, Bg + (size_t)ch * 2 * B_ELEMS, (uint32_t)(2 * B_ELEMS * sizeof(float)), &full_bar[st]);
             }
-            // stage 16 rows per warp as 8x4 blocks: lane -> (row 8-group row L/4,
+            // stage 32 rows per warp as 8x4 blocks: lane -> (row 8-group row L/4,
             // k = 4-group + L%4).  Each block is one 8x16-B core matrix in shared
             // memory (all 32 banks once) and 8 full 32-B sectors in global memory.
-            // The values were loaded one step earlier (xv_next) so the loads overlap
-            // the previous barrier, MMA issue and epilogue.
             const int k0 = ch * TC_BK;
-            double xv[16];
+            const int w4 = warp - 4;
 #pragma unroll
-            for (int it2 = 0; it2 < 16; ++it2) xv[it2] = xv_next[it2];
-            {
-                // prefetch the next (tile, chunk) step of this CTA
-                long long ntile = tile;
-                int nchunk = ch + 1;
-                if (nchunk == nch) { nchunk = 0; ntile = tile + gridDim.x; }
-                load_chunk(ntile, nchunk);
-            }
+            for (int half2 = 0; half2 < 2; ++half2) {
+                double xv[16];
 #pragma unroll
-            for (int it2 = 0; it2 < 16; ++it2) {
-                const int rg = it2 >> 3, kg = it2 & 7;
-                const int rr = warp * (TC_M / 8) + rg * 8 + (lane >> 2);
-                const float h = to_tf32((float)xv[it2]);
-                const float l = to_tf32((float)(xv[it2] - (double)h));
-                const uint32_t o = kmajor_off(rr, kg * 4 + (lane & 3)) >> 2;
-                Ah[o] = h;
-                Al[o] = l;
+                for (int it2 = 0; it2 < 16; ++it2) {
+                    const int rg = 2 * half2 + (it2 >> 3), kg = it2 & 7;
+                    const int rr = w4 * 32 + rg * 8 + (lane >> 2);
+                    const int gk = k0 + kg * 4 + (lane & 3);
+                    const long long r = row0 + rr;
+                    xv[it2] = (r < n && gk < d) ? (double)X[r * ldx + gk] : 0.0;
+                }
+#pragma unroll
+                for (int it2 = 0; it2 < 16; ++it2) {
+                    const int rg = 2 * half2 + (it2 >> 3), kg = it2 & 7;
+                    const int rr = w4 * 32 + rg * 8 + (lane >> 2);
+                    const float h = to_tf32((float)xv[it2]);
+                    const float l = to_tf32((float)(xv[it2] - (double)h));
+                    const uint32_t o = kmajor_off(rr, kg * 4 + (lane & 3)) >> 2;
+                    Ah[o] = h;
+                    Al[o] = l;
+                }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncthreads();
+            asm volatile("bar.sync 1, 128;" ::: "memory");   // the four staging warps
             AT_MARK(0);
-            if (tid == 0) {
+            if (tid == 128) {
                 if (!b_resident) mbar_wait(&full_bar[st], (uint32_t)((q >> 1) & 1));
                 else if (q == 0) mbar_wait(&full_bar[0], 0);
                 asm volatile("tcgen05.fence::after_thread_sync;");
@@ -430,7 +425,9 @@ __global__ void __launch_bounds__(TC_T2, 1) assign_tc_kernel(
                 mma_commit(&empty_bar[st]);
                 if (ch == nch - 1) mma_commit(&acc_bar[accb]);
             }
+            __syncwarp();
             AT_MARK(1);
+        }
         }
         if (prev_tile >= 0) {
             const int pb = (int)((it - 1) & 1);
