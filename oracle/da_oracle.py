@@ -390,3 +390,89 @@ def beam_min_gap(cw64: np.ndarray, P: np.ndarray, X64: np.ndarray, L: int) -> np
     if score.shape[1] > 1:
         boundary(score, 1)
     return gap
+
+
+# ---------------------------------------------------------------------------
+# A-Tree traversal (atree.py:336-475; compiled form _traverse.py:52-255)
+
+
+def _keep_first_smallest(vals: np.ndarray, count: int) -> np.ndarray:
+    """Mask of the `count` smallest; among values equal to the count-th
+    smallest the earliest positions win (_traverse.py:26-48)."""
+    n = vals.size
+    if n <= count:
+        return np.ones(n, dtype=bool)
+    kth = np.partition(vals, count - 1)[count - 1]
+    keep = vals < kth
+    need = count - int(keep.sum())
+    eq = np.flatnonzero(vals == kth)[:need]
+    keep[eq] = True
+    return keep
+
+
+def atree_traverse(ts, q_sq, tree, budgets, r):
+    """Per-query layered search -> (ids, dists, nodes_visited, table_lookups,
+    per_layer).  `ts` = adc values - ||q||^2 (M, K); `tree` has the ATree
+    arrays (atree.py:91-117).  Distances accumulate as in the compiled kernel:
+    internal steps (d + ts) + 2 eps, suffix steps d + (ts + 2 eps)."""
+    M = ts.shape[0]
+    code, eps = tree.code, tree.eps.astype(np.float64)
+    s_code, s_eps = tree.suffix_code, tree.suffix_eps.astype(np.float64)
+    visited = lookups = 0
+    per_layer = []
+    nodes = np.arange(tree.n_root_children, dtype=np.int64)
+    nd = np.array([(q_sq + ts[0, code[v]]) + 2.0 * eps[v] for v in nodes])
+    internal = np.empty(0, dtype=np.int64)
+    idist = np.empty(0)
+    leaves = np.empty(0, dtype=np.int64)
+    lpos = np.empty(0, dtype=np.int64)
+    ldist = np.empty(0)
+    for layer in range(M):
+        if layer > 0:
+            if internal.size == 0 and leaves.size <= int(np.min(budgets[layer:])):
+                rem = M - layer
+                for j in range(leaves.size):
+                    acc = ldist[j]
+                    for t in range(rem):
+                        acc += ts[layer + t, s_code[lpos[j] + t]] + 2.0 * s_eps[lpos[j] + t]
+                    ldist[j] = acc
+                lookups += leaves.size * rem
+                per_layer += [leaves.size] * rem
+                break
+            nn, dd = [], []
+            for v, pdv in zip(internal, idist):
+                for c in range(tree.child_lo[v], tree.child_hi[v]):
+                    nn.append(c)
+                    dd.append((pdv + ts[layer, code[c]]) + 2.0 * eps[c])
+            nodes = np.array(nn, dtype=np.int64)
+            nd = np.array(dd)
+            for j in range(leaves.size):
+                p = lpos[j]
+                ldist[j] += ts[layer, s_code[p]] + 2.0 * s_eps[p]
+            lpos = lpos + 1
+            lookups += leaves.size
+        visited += nodes.size
+        lookups += nodes.size
+        b = int(budgets[layer])
+        size = nodes.size + leaves.size
+        per_layer.append(min(size, b))
+        if size > b:
+            keep = _keep_first_smallest(np.concatenate([nd, ldist]), b)
+            kn, kl = keep[:nodes.size], keep[nodes.size:]
+            nodes, nd = nodes[kn], nd[kn]
+            leaves, lpos, ldist = leaves[kl], lpos[kl], ldist[kl]
+        is_leaf = tree.leaf_ref[nodes] >= 0
+        enter = tree.leaf_ref[nodes[is_leaf]]
+        leaves = np.concatenate([enter, leaves])
+        lpos = np.concatenate([tree.suffix_lo[enter], lpos])
+        ldist = np.concatenate([nd[is_leaf], ldist])
+        internal, idist = nodes[~is_leaf], nd[~is_leaf]
+    out_ids, out_d = [], []
+    for j, lf in enumerate(leaves):
+        for p in range(tree.ids_lo[lf], tree.ids_hi[lf]):
+            out_ids.append(tree.leaf_ids[p])
+            out_d.append(ldist[j])
+    out_ids = np.array(out_ids, dtype=np.int64)
+    out_d = np.array(out_d)
+    order = np.lexsort((out_ids, out_d))[:r]
+    return out_ids[order], out_d[order], visited, lookups, per_layer
