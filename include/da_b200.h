@@ -148,6 +148,20 @@ int da_adc_scan(const void* codes, int code_bytes, int64_t ldc, const double* pa
                 int64_t ncand, int64_t nq, const double* lut, const double* qsq, int M, int K, int r, int64_t* ids,
                 double* dists, void* stream);
 
+/* A-Tree search (one CTA per query): layered walk with per-layer budgets, boundary ties
+ * kept in enumeration order, early suffix resolution, r best (distance, id) per query.
+ * lut/qsq from da_adc_lut (device); tree arrays as in the reference's ATree (device);
+ * budgets: M positive int64 on the HOST.  Outputs (device): ids (nq, r) padded with -1,
+ * dists (nq, r) padded with NaN, counts (nq), stats (nq, 2 + M) = nodes_visited,
+ * table_lookups, per-layer sizes.
+ * replaces atree_search / _traverse.traverse      atree.py:336-475, _traverse.py:52-255 */
+int da_atree_search(const double* lut, const double* qsq, int64_t nq, int M, int K, const int32_t* code,
+                    const float* eps, const int64_t* child_lo, const int64_t* child_hi, const int64_t* leaf_ref,
+                    const int64_t* suffix_lo, const int32_t* suffix_code, const float* suffix_eps,
+                    const int64_t* ids_lo, const int64_t* ids_hi, const int64_t* leaf_ids, int64_t n_nodes,
+                    int64_t n_leaves, int64_t n_root, int64_t max_children, const int64_t* budgets, int r,
+                    int64_t* ids, double* dists, int64_t* counts, int64_t* stats, void* stream);
+
 /* Packed candidate records for the scan (one-byte codes, M <= 8): records is n x 16 bytes,
  * codes in bytes 0..7 and the row's pair sum (float64) in bytes 8..15, so one random
  * candidate reads one 32-byte sector.  Built once per encoded set.

@@ -279,18 +279,24 @@ def atree_search_batch(tree, codebook, Q, params: SearchParams):
                 np.zeros((nq, 2 + M), dtype=np.int64))
     cw, sq = _codebook_dev(codebook)
     lut, qsq = E.adc_lut(E.to_dev(Q), cw, sq)
+    return _search_tables(tree, lut, qsq, budgets, r)
+
+
+def _search_tables(tree, lut: torch.Tensor, qsq: torch.Tensor, budgets: np.ndarray, r: int):
+    """Traversal on given device tables lut (nq, M, K) and qsq (nq,)."""
+    nq, M = lut.shape[0], tree.m_count
     t = _tree_dev(tree)
     dev = lut.device
-    b_d = E.to_dev(np.ascontiguousarray(budgets, dtype=np.int64))
+    b_h = np.ascontiguousarray(budgets, dtype=np.int64)
     ids = torch.empty((nq, r), dtype=torch.int64, device=dev)
     dists = torch.empty((nq, r), dtype=torch.float64, device=dev)
     cnt = torch.empty(nq, dtype=torch.int64, device=dev)
     stats = torch.empty((nq, 2 + M), dtype=torch.int64, device=dev)
-    native.da_atree_search(P(lut), P(qsq), nq, M, codebook.k_count,
+    native.da_atree_search(P(lut), P(qsq), nq, M, lut.shape[2],
                            P(t["code"]), P(t["eps"]), P(t["child_lo"]), P(t["child_hi"]), P(t["leaf_ref"]),
                            P(t["suffix_lo"]), P(t["suffix_code"]), P(t["suffix_eps"]), P(t["ids_lo"]),
                            P(t["ids_hi"]), P(t["leaf_ids"]), tree.node_count, tree.leaf_count,
-                           int(tree.n_root_children), t["max_children"], P(b_d), r,
+                           int(tree.n_root_children), t["max_children"], b_h.ctypes.data, r,
                            P(ids), P(dists), P(cnt), P(stats), E.stream())
     return ids.cpu().numpy(), dists.cpu().numpy(), cnt.cpu().numpy(), stats.cpu().numpy()
 

@@ -360,6 +360,23 @@ int da_adc_scan_packed(const void* records, const int64_t* cand, int64_t ncand, 
                                   dists, STREAM(stream));
 }
 
+int da_atree_search(const double* lut, const double* qsq, int64_t nq, int M, int K, const int32_t* code,
+                    const float* eps, const int64_t* child_lo, const int64_t* child_hi, const int64_t* leaf_ref,
+                    const int64_t* suffix_lo, const int32_t* suffix_code, const float* suffix_eps,
+                    const int64_t* ids_lo, const int64_t* ids_hi, const int64_t* leaf_ids, int64_t n_nodes,
+                    int64_t n_leaves, int64_t n_root, int64_t max_children, const int64_t* budgets, int r,
+                    int64_t* ids, double* dists, int64_t* counts, int64_t* stats, void* stream) {
+    if (M < 1 || K < 1 || r < 1) return fail_arg("atree_search: bad shape M=%d K=%d r=%d", M, K, r);
+    for (int m = 0; m < M; ++m)
+        if (budgets[m] < 1) return fail_arg("atree_search: budgets must be positive");
+    if (n_nodes <= 0 || n_root <= 0) return fail_arg("atree_search: empty tree");
+    return launch_atree_search(lut, qsq, nq, M, K, code, eps, (const long long*)child_lo, (const long long*)child_hi,
+                               (const long long*)leaf_ref, (const long long*)suffix_lo, suffix_code, suffix_eps,
+                               (const long long*)ids_lo, (const long long*)ids_hi, (const long long*)leaf_ids,
+                               n_nodes, n_leaves, n_root, max_children, (const long long*)budgets, r,
+                               (long long*)ids, dists, (long long*)counts, (long long*)stats, STREAM(stream));
+}
+
 int da_np_sum(const double* a, int64_t n, int divide, double* out, void* stream) {
     return launch_np_sum(a, n, divide, out, STREAM(stream));
 }

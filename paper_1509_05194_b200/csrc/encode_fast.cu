@@ -290,8 +290,11 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
         double smax = 0.0;
         for (int l = lane; l < live; l += 32) smax = fmax(smax, fabs(ps[l]));
         for (int off = 16; off >= 1; off >>= 1) smax = fmax(smax, __shfl_xor_sync(FULL, smax, off));
+        // sum of the cross-table maxima (a bound, so any order): one load per lane
         double cb = 0.0;
-        for (int j = 0; j < m; ++j) cb += pabs[j * M + m];
+        for (int j = lane; j < m; j += 32) cb += pabs[j * M + m];
+        for (int off = 16; off >= 1; off >>= 1) cb += __shfl_xor_sync(FULL, cb, off);
+        cb *= 1.0 + 1e-12;
         const double cm = cmax[m];
         const double tmax = cm * cm + 2.0 * xnorm * cm;
         const double e_t = (2.0 * D + 8.0) * u * (xnorm * cm + cm * cm);

@@ -61,6 +61,13 @@ int launch_einsum_sq(const float* cw, long long rows, int D, double* out, cudaSt
 int launch_pair_sums(const void* codes, int code_bytes, long long n, long long ldc, const double* P, int M, int K,
                      double* out, cudaStream_t s);
 int launch_qsq(const double* Q, long long nq, int D, double* out, cudaStream_t s);
+int launch_atree_search(const double* lut, const double* qsq, long long nq, int M, int K, const int32_t* code,
+                        const float* eps, const long long* child_lo, const long long* child_hi,
+                        const long long* leaf_ref, const long long* suffix_lo, const int32_t* suffix_code,
+                        const float* suffix_eps, const long long* ids_lo, const long long* ids_hi,
+                        const long long* leaf_ids, long long n_nodes, long long n_leaves, long long n_root,
+                        long long max_children, const long long* budgets_host, int r, long long* ids_out,
+                        double* d_out, long long* cnt_out, long long* stats_out, cudaStream_t s);
 int launch_adc_pack(const void* codes, long long n, long long ldc, const double* pair, int M, void* records,
                     cudaStream_t s);
 int launch_adc_scan_packed(const void* records, const long long* cand, long long ncand, long long nq,
