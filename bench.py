@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--no-anneal", action="store_true", help="skip the full anneal-pass timing")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--no-adc", action="store_true", help="skip the config-E ADC scan timing")
+    ap.add_argument("--no-atree", action="store_true", help="skip the A-Tree build + search timing")
     ap.add_argument("--adc-n", type=int, default=1_000_000_000, help="encoded vectors for the ADC scan")
     return ap.parse_args()
 
@@ -352,6 +353,31 @@ def main():
                                             "profiles/README.md"}}
         del rec_e, cand_e, lut_e, Qe
 
+    # --- A-Tree: host build over this GPU's L=10 codes, GPU batched search
+    atree = None
+    if not args.no_atree:
+        from paper_1509_05194_b200 import atree as AT
+
+        book_t = da.Codebook(codewords=cw.cpu().numpy(), order=np.arange(M))
+        cross_t = da.cross_products(book_t)
+        codes_t = encode_once(L)
+        enc_t = da.EncodedDataset(codes=codes_t.cpu().numpy(), k_count=K, codebook_hash=book_t.content_hash())
+        t0 = time.perf_counter()
+        tree = AT.build_atree(enc_t, book_t, cross_t)
+        build_s = time.perf_counter() - t0
+        Qa = rank_data(7 + rank, 10_000).astype(np.float64)
+        params = AT.SearchParams(l0=8, ls=2.0, r=10)
+        AT.atree_search_batch(tree, book_t, Qa[:100], params)
+        barrier()
+        t0 = time.perf_counter()
+        _, _, _, st = AT.atree_search_batch(tree, book_t, Qa, params)
+        torch.cuda.synchronize()
+        search_s = time.perf_counter() - t0
+        atree = {"workload": f"{n} codes per GPU, 10,000 queries, SearchParams(l0=8, ls=2, r=10)",
+                 "build_s_host": build_s, "nodes": tree.node_count, "search_ms": search_s * 1e3,
+                 "queries_per_s": 10_000 / search_s, "mean_nodes_visited": float(st[:, 0].mean())}
+        del tree
+
     # --- roofline of the dominant kernel in the timed region
     pk = peaks()
     kernels = {k: {"launches": c, "ms_per_launch": round(t / max(c, 1), 4), "share": round(t / ms_local, 4)}
@@ -420,6 +446,7 @@ def main():
             "exact_recheck_fraction": recheck_frac,
             "anneal_pass": anneal,
             "adc_scan": adc,
+            "atree_search": atree,
             "roofline": roof,
             "kernels": kernels,
             "cpu_baseline": cpu,

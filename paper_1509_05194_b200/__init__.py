@@ -53,6 +53,7 @@ from .codebook import (
     write_codebook,
     write_encoded,
 )
+from .atree import ATree, SearchParams, SearchStats, atree_search, atree_search_batch, build_atree, node_distance
 from .validation import FormatError
 
 __version__ = "0.1.0"
@@ -67,10 +68,11 @@ _PATCH_TABLE = {
                        "improved_kmeans"],
     "annq.estimators": ["train_from_scratch", "train_online"],
     "annq.cli": ["train_from_scratch", "train_online"],
-    "annq.atree": ["adc_table"],
+    "annq.atree": ["adc_table", "build_atree", "atree_search"],
     "annq": ["cross_products", "encode_multipath", "encode_dataset", "adc_table", "exhaustive_adc_search",
              "reconstruct", "distortion", "pca_fit", "lloyd_kmeans", "improved_kmeans", "quantization_error",
-             "heat_up", "cool_down", "da_sweep", "train_from_scratch", "train_online", "rvq_train"],
+             "heat_up", "cool_down", "da_sweep", "train_from_scratch", "train_online", "rvq_train",
+             "build_atree", "atree_search"],
 }
 
 
@@ -85,11 +87,12 @@ def install(annq_module=None):
     import sys
 
     from . import annealing as _an
+    from . import atree as _at
     from . import clustering as _cl
     from . import codebook as _cbm
 
     ours = {}
-    for mod in (_cbm, _cl, _an):
+    for mod in (_cbm, _cl, _an, _at):
         for name in dir(mod):
             if not name.startswith("_"):
                 ours.setdefault(name, getattr(mod, name))
