@@ -162,6 +162,13 @@ int da_atree_search(const double* lut, const double* qsq, int64_t nq, int M, int
                     int64_t n_leaves, int64_t n_root, int64_t max_children, const int64_t* budgets, int r,
                     int64_t* ids, double* dists, int64_t* counts, int64_t* stats, void* stream);
 
+/* Exact squared-L2 top-r neighbours (ground truth): d2 = max((||q||^2 - 2 q.x) + ||x||^2, 0)
+ * with the dot in OpenBLAS dgemm order, ties to the lower id.  base (n x D, f32 or f64, row
+ * stride ldb), base_sq (n) and qsq (nq) pairwise row norms, Q (nq x D) float64; device.
+ * replaces brute_force_knn / _knn_block        data.py:167-215 */
+int da_knn(const void* base, int base_f32, int64_t n, int64_t ldb, int D, const double* base_sq, const double* Q,
+           int64_t nq, const double* qsq, int r, int64_t* ids, double* dists, void* stream);
+
 /* Packed candidate records for the scan (one-byte codes, M <= 8): records is n x 16 bytes,
  * codes in bytes 0..7 and the row's pair sum (float64) in bytes 8..15, so one random
  * candidate reads one 32-byte sector.  Built once per encoded set.

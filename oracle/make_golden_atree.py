@@ -1,4 +1,5 @@
-"""Generate tests/golden/atree.npz by running the REFERENCE A-Tree (build + search).
+"""Generate tests/golden/atree.npz (A-Tree build + search) and tests/golden/knn.npz
+(brute_force_knn) by running the REFERENCE.
 
 Build container only (imports /root/reference/pkg/src):
 
@@ -110,5 +111,23 @@ def main():
     print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KiB)")
 
 
+def knn_fixture():
+    """brute_force_knn on a small base with duplicate rows (exact ties)."""
+    rng = np.random.default_rng(21)
+    base = annq.generate_synthetic(2000, 16, clusters=20, spread=0.2, seed=21)
+    base[100:110] = base[5]
+    queries = np.vstack([rng.standard_normal((30, 16)).astype(np.float32), base[[5, 7]]])
+    out = {"base": base, "queries": queries}
+    for r in (1, 10, 37):
+        gt = annq.brute_force_knn(base, queries, r)
+        out[f"r{r}_ids"] = gt.ids
+        out[f"r{r}_dists"] = gt.distances
+    path = os.path.join(OUT, "knn.npz")
+    np.savez_compressed(path, **out)
+    print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KiB)")
+
+
 if __name__ == "__main__":
-    main()
+    if not os.environ.get("KNN_ONLY"):
+        main()
+    knn_fixture()

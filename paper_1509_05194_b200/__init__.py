@@ -54,6 +54,7 @@ from .codebook import (
     write_encoded,
 )
 from .atree import ATree, SearchParams, SearchStats, atree_search, atree_search_batch, build_atree, node_distance
+from .groundtruth import GroundTruth, brute_force_knn
 from .validation import FormatError
 
 __version__ = "0.1.0"
@@ -69,10 +70,11 @@ _PATCH_TABLE = {
     "annq.estimators": ["train_from_scratch", "train_online"],
     "annq.cli": ["train_from_scratch", "train_online"],
     "annq.atree": ["adc_table", "build_atree", "atree_search"],
+    "annq.data": ["brute_force_knn"],
     "annq": ["cross_products", "encode_multipath", "encode_dataset", "adc_table", "exhaustive_adc_search",
              "reconstruct", "distortion", "pca_fit", "lloyd_kmeans", "improved_kmeans", "quantization_error",
              "heat_up", "cool_down", "da_sweep", "train_from_scratch", "train_online", "rvq_train",
-             "build_atree", "atree_search"],
+             "build_atree", "atree_search", "brute_force_knn"],
 }
 
 
@@ -90,9 +92,10 @@ def install(annq_module=None):
     from . import atree as _at
     from . import clustering as _cl
     from . import codebook as _cbm
+    from . import groundtruth as _gt
 
     ours = {}
-    for mod in (_cbm, _cl, _an, _at):
+    for mod in (_cbm, _cl, _an, _at, _gt):
         for name in dir(mod):
             if not name.startswith("_"):
                 ours.setdefault(name, getattr(mod, name))

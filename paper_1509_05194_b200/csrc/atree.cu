@@ -401,3 +401,79 @@ int launch_atree_search(const double* lut, const double* qsq, long long nq, int 
 }
 
 }  // namespace da
+
+namespace da {
+
+// ---------------------------------------------------------------------------
+// Exact k-NN ground truth (data.py:167-215): one CTA per query row of a float64
+// distance block d2 (rows x n, produced by the ordered GEMM), top-r by
+// (distance, lower id): radix-select the r-th distance, keep everything below
+// it plus the lowest ids equal to it, then place each kept pair by its rank.
+__global__ void __launch_bounds__(AT_T) topr_rows_kernel(const double* __restrict__ d2, long long rows, long long n,
+                                                         int r, long long* __restrict__ ids_out,
+                                                         double* __restrict__ d_out, long long* __restrict__ scratch) {
+    __shared__ int s_w[32];
+    __shared__ unsigned long long hist[256];
+    __shared__ unsigned long long s_b[4];
+    const int tid = threadIdx.x;
+    long long* kid = scratch + (long long)blockIdx.x * r;
+    for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
+        const double* drow = d2 + row * n;
+        auto key = [&](long long i) { return at_key(drow[i]); };
+        const unsigned long long kth = at_select(n, (unsigned long long)(r - 1), key, [](long long) { return 1ULL; },
+                                                 hist, s_b);
+        long long strict = 0;
+        for (long long b0 = 0; b0 < n; b0 += AT_T) {
+            const long long i = b0 + tid;
+            int tot;
+            at_block_scan(i < n && key(i) < kth ? 1 : 0, s_w, &tot);
+            strict += tot;
+        }
+        const long long need = r - strict;
+        long long eq_seen = 0, w = 0;
+        for (long long b0 = 0; b0 < n; b0 += AT_T) {
+            const long long i = b0 + tid;
+            const unsigned long long kk = i < n ? key(i) : ~0ULL;
+            const int is_eq = (i < n && kk == kth) ? 1 : 0;
+            int teq;
+            const int eb = at_block_scan(is_eq, s_w, &teq);
+            const bool keep = i < n && (kk < kth || (is_eq && eq_seen + eb < need));
+            int tk;
+            const int pk = at_block_scan(keep ? 1 : 0, s_w, &tk);
+            if (keep) kid[w + pk] = i;
+            eq_seen += teq;
+            w += tk;
+        }
+        __syncthreads();
+        for (int t = tid; t < r; t += AT_T) {
+            const long long it = kid[t];
+            const double dv = drow[it];
+            int rank = 0;
+            for (int u = 0; u < r; ++u) {
+                const long long iu = kid[u];
+                const double du = drow[iu];
+                rank += (du < dv) || (du == dv && iu < it);
+            }
+            ids_out[row * r + rank] = it;
+            d_out[row * r + rank] = dv;
+        }
+        __syncthreads();
+    }
+}
+
+int launch_topr_rows(const double* d2, long long rows, long long n, int r, long long* ids_out, double* d_out,
+                     cudaStream_t s) {
+    if (rows <= 0) return 0;
+    if (r < 1 || r > n) return fail_arg("knn: r=%d must be in [1, %lld]", r, n);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = (int)std::min<long long>(rows, (long long)sms * 4);
+    long long* scr = (long long*)scratch(12, sizeof(long long) * (size_t)grid * r, s);
+    if (!scr) return fail_cuda(cudaErrorMemoryAllocation, "knn scratch");
+    topr_rows_kernel<<<grid, AT_T, 0, s>>>(d2, rows, n, r, ids_out, d_out, scr);
+    DA_CHECK_LAUNCH("topr_rows_kernel");
+    return 0;
+}
+
+}  // namespace da

@@ -377,6 +377,34 @@ int da_atree_search(const double* lut, const double* qsq, int64_t nq, int M, int
                                (long long*)ids, dists, (long long*)counts, (long long*)stats, STREAM(stream));
 }
 
+int da_knn(const void* base, int base_f32, int64_t n, int64_t ldb, int D, const double* base_sq, const double* Q,
+           int64_t nq, const double* qsq, int r, int64_t* ids, double* dists, void* stream) {
+    if (n < 1 || nq < 0 || D < 1 || ldb < D) return fail_arg("knn: bad shape n=%lld nq=%lld D=%d", (long long)n,
+                                                             (long long)nq, D);
+    if (r < 1 || r > n) return fail_arg("r=%d must be in [1, %lld]", r, (long long)n);
+    cudaStream_t s = STREAM(stream);
+    ProfScope ps("knn", s);
+    // distance blocks of <= 2^27 entries (1 GB): rows of max(0, (||q||^2 - 2 q.x) + ||x||^2)
+    // with the dot in OpenBLAS dgemm order, then the per-row top-r
+    const long long block = std::max(1LL, std::min((long long)nq, (1LL << 27) / n));
+    double* d2 = (double*)scratch(13, sizeof(double) * (size_t)(block * n), s);
+    if (!d2) return fail_cuda(cudaErrorMemoryAllocation, "knn distance block");
+    for (long long q0 = 0; q0 < nq; q0 += block) {
+        const long long rows = std::min(block, (long long)nq - q0);
+        GemmArgs g{};
+        g.A = Q + q0 * D; g.a_f32 = 0; g.sai = D; g.sak = 1;
+        g.B = base; g.b_f32 = base_f32; g.sbk = 1; g.sbj = ldb;
+        g.C = d2; g.sci = n; g.scj = 1;
+        g.M = rows; g.N = n; g.K = D; g.nb2 = 1; g.ksplit = 1; g.kchunk = D;
+        g.epi = 3; g.evec = base_sq; g.ivec = qsq + q0;
+        int rc = launch_gemm(g, 1, s);
+        if (rc) return rc;
+        rc = launch_topr_rows(d2, rows, n, r, (long long*)ids + q0 * r, dists + q0 * r, s);
+        if (rc) return rc;
+    }
+    return 0;
+}
+
 int da_np_sum(const double* a, int64_t n, int divide, double* out, void* stream) {
     return launch_np_sum(a, n, divide, out, STREAM(stream));
 }

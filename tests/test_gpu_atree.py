@@ -87,3 +87,16 @@ def test_unbounded_budgets_match_exhaustive_adc(gold):
     np.testing.assert_array_equal(ids, eids)
     # tree distances carry float32 epsilons (atree.py:150-155): the reference allows 1e-3
     np.testing.assert_allclose(d, ed, rtol=1e-3, atol=1e-8)
+
+
+def test_brute_force_knn_matches_reference():
+    import conftest
+    from paper_1509_05194_b200.groundtruth import brute_force_knn
+
+    g = conftest.load_golden("knn.npz")
+    for r in (1, 10, 37):
+        gt = brute_force_knn(g["base"], g["queries"], r)
+        np.testing.assert_array_equal(gt.ids, g[f"r{r}_ids"])
+        np.testing.assert_array_equal(gt.distances, g[f"r{r}_dists"])
+    with pytest.raises(ValueError):
+        brute_force_knn(g["base"], g["queries"][:, :3], 5)

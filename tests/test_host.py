@@ -139,7 +139,7 @@ class TestSynthetic:
 
 def test_install_patches_every_binding_site(monkeypatch):
     names = {"annq": {}, "annq.codebook": {}, "annq.clustering": {}, "annq.annealing": {},
-             "annq.estimators": {}, "annq.cli": {}, "annq.atree": {}}
+             "annq.estimators": {}, "annq.cli": {}, "annq.atree": {}, "annq.data": {}}
     for modname in names:
         mod = types.ModuleType(modname)
         for n in da._PATCH_TABLE.get(modname, []):
