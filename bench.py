@@ -373,9 +373,18 @@ def main():
         _, _, _, st = AT.atree_search_batch(tree, book_t, Qa, params)
         torch.cuda.synchronize()
         search_s = time.perf_counter() - t0
+        ids_t, _, _, st = AT.atree_search_batch(tree, book_t, Qa[:1000], params)
+        # recall@10 against the exact neighbours (GPU brute force)
+        from paper_1509_05194_b200.groundtruth import brute_force_knn
+
+        t0 = time.perf_counter()
+        gt = brute_force_knn(X_h, Qa[:1000].astype(np.float32), 10)
+        gt_s = time.perf_counter() - t0
+        recall = float(np.mean([len(set(a_) & set(b_)) / 10.0 for a_, b_ in zip(ids_t, gt.ids)]))
         atree = {"workload": f"{n} codes per GPU, 10,000 queries, SearchParams(l0=8, ls=2, r=10)",
                  "build_s_host": build_s, "nodes": tree.node_count, "search_ms": search_s * 1e3,
-                 "queries_per_s": 10_000 / search_s, "mean_nodes_visited": float(st[:, 0].mean())}
+                 "queries_per_s": 10_000 / search_s, "mean_nodes_visited": float(st[:, 0].mean()),
+                 "recall_at_10": recall, "ground_truth_ms_1000_queries": gt_s * 1e3}
         del tree
 
     # --- roofline of the dominant kernel in the timed region
