@@ -122,10 +122,11 @@ int da_encode(const void* X, int x_f32, int64_t n, int64_t ldx, int D, const flo
               void* stream);
 
 /* Encoder selection (all modes return identical codes/errors):
- *   0 (default) = by beam width: 3 for L <= 4 or L >= 24, else 2 (measured crossover on
+ *   0 (default) = by beam width: 3 for L <= 2 or L >= 24, else 2 (measured crossover on
  *       B200, config B); 1 = plain float64 score tables;
- *   2 = fp32 score table + fp32 cross-table gathers as a filter with a rigorous
- *       error bound, exact float64 recheck of the candidates that can still make the beam;
+ *   2 = fp32 score table (3xTF32 on tcgen05; FFMA when the shape does not fit) + fp32
+ *       cross-table gathers as a filter with a rigorous error bound, exact float64
+ *       recheck of the candidates that can still make the beam;
  *   3 = tcgen05 filter: per stage one 3xTF32 GEMM of the beams' residuals against the
  *       dictionary (score = s + ||c||^2 - 2 r.c), same bound + exact recheck.
  * recheck_counter (device, optional) accumulates the number of exactly rechecked candidates. */

@@ -17,6 +17,8 @@
 //      exact (value, flat index) top-width selection.
 // Beam scores are always the exact float64 values, so codes and errors equal
 // the reference's; only the amount of float64 work changes.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -249,7 +251,7 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
     int cap, const float* __restrict__ tab32, const double* __restrict__ sq, const double* __restrict__ P,
     const float* __restrict__ P32, const double* __restrict__ cmax, const double* __restrict__ pabs,
     const double* __restrict__ cw64, void* codes_out,
-    int code_bytes, long long ldcodes, double* __restrict__ err_out, unsigned long long* __restrict__ stats) {
+    int code_bytes, long long ldcodes, double* __restrict__ err_out, unsigned long long* __restrict__ stats, int tab_tc) {
     extern __shared__ __align__(16) char smem_raw[];
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -297,7 +299,12 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
         cb *= 1.0 + 1e-12;
         const double cm = cmax[m];
         const double tmax = cm * cm + 2.0 * xnorm * cm;
-        const double e_t = (2.0 * D + 8.0) * u * (xnorm * cm + cm * cm);
+        // table error: fp32 FFMA dot (D roundings) or 3xTF32 tensor-core dot
+        // (2^-21 representation + 2^-22 per accumulation step, 6 steps per 16 of D+1,
+        // on |sq| + 2|x.c|), doubled for the -2 factor and the norm entry
+        const double e_t = tab_tc ? (2.0 * (6.0 * ((D + 16) / 16) + 7.0) * 2.384185791015625e-07 +
+                                     9.5367431640625e-07 + 2.0 * u) * (2.0 * xnorm * cm + cm * cm)
+                                  : (2.0 * D + 8.0) * u * (xnorm * cm + cm * cm);
         const double e_cross = (m + 2.0) * u * cb;
         const double E = 2.0 * (e_t + 2.0 * e_cross + 4.0 * u * (smax + tmax + 2.0 * cb) + u * smax) + 1e-300;
 
@@ -639,15 +646,19 @@ int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int
     const int N = M * K;
     for (long long c0 = 0; c0 < n; c0 += chunk) {
         const long long cn = std::min(chunk, n - c0);
-        {
+        int tab_tc = 0;
+        if (!x_f32) return fail_arg("encode_fast: float32 input only");
+        if (getenv("DA_TABLE_FFMA") == nullptr) {
+            ProfScope ps("encode_table_tc", s);
+            const int rc = launch_table_tc((const float*)X + c0 * ldx, cn, ldx, D, cw, sq, M, K, tab, N, s);
+            if (rc == 0) tab_tc = 1;
+            else if (rc != kNotApplicable) return rc;
+        }
+        if (!tab_tc) {
             ProfScope ps("encode_table_sgemm", s);
-            if (x_f32) {
-                dim3 grid((N + SG_BN - 1) / SG_BN, (unsigned)((cn + SG_BM - 1) / SG_BM));
-                sgemm_table_kernel<<<grid, SG_T, 0, s>>>((const float*)X + c0 * ldx, cn, ldx, cw, N, D, sq32, tab, N);
-                DA_CHECK_LAUNCH("sgemm_table_kernel");
-            } else {
-                return fail_arg("encode_fast: float32 input only");
-            }
+            dim3 grid((N + SG_BN - 1) / SG_BN, (unsigned)((cn + SG_BM - 1) / SG_BM));
+            sgemm_table_kernel<<<grid, SG_T, 0, s>>>((const float*)X + c0 * ldx, cn, ldx, cw, N, D, sq32, tab, N);
+            DA_CHECK_LAUNCH("sgemm_table_kernel");
         }
         ProfScope ps2("encode_beam_fast", s);
         const unsigned grid = (unsigned)((cn + warps - 1) / warps);
@@ -655,7 +666,7 @@ int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int
         double* eout = err_out ? err_out + c0 : nullptr;
         beam_fast_kernel<float><<<grid, warps * 32, smem, s>>>((const float*)X + c0 * ldx, cn, ldx, D, cw, M, K, L,
                                                                cap, tab, sq, P, P32, cmax, pabs, cw64, cout, code_bytes,
-                                                               ldcodes, eout, stats);
+                                                               ldcodes, eout, stats, tab_tc);
         DA_CHECK_LAUNCH("beam_fast_kernel");
     }
     return 0;

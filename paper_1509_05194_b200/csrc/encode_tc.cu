@@ -995,3 +995,167 @@ int launch_encode_tc(const float* X, long long n, long long ldx, int D, const fl
 }
 
 }  // namespace da
+
+namespace da {
+
+// ---------------------------------------------------------------------------
+// Score table on the tensor cores: T[v][m*K + k] = ||c_mk||^2 - 2 x_v . c_mk (fp32,
+// 3xTF32 on tcgen05; the gather filter's input, encode_fast.cu).  One persistent
+// CTA per SM; per 128-row tile the [x, 1] rows are split into tf32 hi/lo once and
+// stay in shared memory for all M dictionaries; codeword chunks stream through a
+// 2-slot ring by bulk copy; two TMEM accumulators let dictionary m+1's MMAs run
+// while the threads store dictionary m's 128 x 256 block.
+__global__ void __launch_bounds__(256, 1) table_tc_kernel(const float* __restrict__ X, long long n, long long ldx,
+                                                           int D, int M, int K, int nch, const float* __restrict__ Bg,
+                                                           float* __restrict__ T, long long ldt) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    constexpr int A_EL = BT_ROWS * BT_BK, B_EL = BT_N * BT_BK;
+    float* Aimg = reinterpret_cast<float*>(smem);             // [nch][hi,lo][A_EL]
+    float* Bbuf = Aimg + (size_t)nch * 2 * A_EL;               // [2][hi,lo][B_EL]
+    __shared__ uint64_t full_bar[2], empty_bar[2], acc_bar[2];
+    __shared__ uint32_t tmem_sh;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(bt_smem_u32(&tmem_sh)),
+                     "r"(2 * BT_N));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < 2; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&full_bar[i])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&empty_bar[i])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&acc_bar[i])));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_sh;
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BT_N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const int row = tid & 127, half = tid >> 7;
+    const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(half * 128);
+    long long q = 0;            // B chunks streamed (ring phases)
+    long long nacc = 0;         // accumulator uses (acc_bar phases)
+    const long long ntiles = (n + 127) / 128;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long r0 = tile * 128;
+        // [x, 1, 0...] rows -> tf32 hi/lo images (all chunks), one 4-wide group per step
+        for (int e = tid; e < 128 * nch * (BT_BK / 4); e += 256) {
+            const int rr = e / (nch * (BT_BK / 4)), rem = e % (nch * (BT_BK / 4));
+            const int ch = rem / (BT_BK / 4), c4 = rem % (BT_BK / 4);
+            const long long gr = r0 + rr;
+            const int k = ch * BT_BK + 4 * c4;
+            float x4[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int kk = k + u;
+                x4[u] = kk < D ? (gr < n ? X[gr * ldx + kk] : 0.f) : (kk == D ? 1.f : 0.f);
+            }
+            bt_store_split(Aimg + (size_t)ch * 2 * A_EL, bt_off(rr, 4 * c4) >> 2, x4);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        for (int m = 0; m <= M; ++m) {
+            if (m < M && tid == 0) {
+                // dictionary m into accumulator (nacc & 1)
+                const int b = (int)(nacc & 1);
+                const uint32_t dacc = tmem + (uint32_t)(b * BT_N);
+                constexpr uint32_t bytes_b = 2 * B_EL * sizeof(float);
+                auto issue = [&](int ch) {
+                    const long long qq = q + ch;
+                    const int st = (int)(qq & 1);
+                    if (qq >= 2) bt_wait(&empty_bar[st], (uint32_t)(((qq >> 1) - 1) & 1));
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bt_smem_u32(&full_bar[st])),
+                                 "r"(bytes_b)
+                                 : "memory");
+                    bt_bulk(Bbuf + st * 2 * B_EL, Bg + ((size_t)m * nch + ch) * 2 * B_EL, bytes_b, &full_bar[st]);
+                };
+                issue(0);
+                for (int ch = 0; ch < nch; ++ch) {
+                    if (ch + 1 < nch) issue(ch + 1);
+                    const long long qq = q + ch;
+                    const int st = (int)(qq & 1);
+                    bt_wait(&full_bar[st], (uint32_t)((qq >> 1) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t ah = bt_smem_u32(Aimg + (size_t)ch * 2 * A_EL), al = ah + A_EL * 4;
+                    const uint32_t bh = bt_smem_u32(Bbuf + st * 2 * B_EL), bl = bh + B_EL * 4;
+#pragma unroll
+                    for (int s2 = 0; s2 < BT_BK / 8; ++s2) {
+                        const uint32_t off = (uint32_t)s2 * 256;
+                        const uint32_t acc0 = (ch > 0 || s2 > 0) ? 1u : 0u;
+                        bt_mma(dacc, bt_desc(ah + off), bt_desc(bh + off), idesc, acc0);
+                        bt_mma(dacc, bt_desc(ah + off), bt_desc(bl + off), idesc, 1u);
+                        bt_mma(dacc, bt_desc(al + off), bt_desc(bh + off), idesc, 1u);
+                    }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                     bt_smem_u32(&empty_bar[st]))
+                                 : "memory");
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 bt_smem_u32(&acc_bar[b]))
+                             : "memory");
+            }
+            __syncwarp();
+            if (m < M) { q += nch; }
+            // store dictionary m-1 (previous accumulator) while dictionary m multiplies
+            if (m > 0) {
+                const long long u = nacc - 1;
+                const int b = (int)(u & 1);
+                bt_wait(&acc_bar[b], (uint32_t)((u >> 1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const long long gr = r0 + row;
+                float* trow = T + gr * ldt + (long long)(m - 1) * K + half * 128;
+#pragma unroll 1
+                for (int c0 = 0; c0 < 128; c0 += 32) {
+                    float v[32];
+                    bt_ld32(taddr + (uint32_t)(b * BT_N) + c0, v);
+                    if (gr < n) {
+                        if ((K & 3) == 0 && half * 128 + c0 + 32 <= K) {
+#pragma unroll
+                            for (int i = 0; i < 32; i += 4)
+                                __stcs(reinterpret_cast<float4*>(trow + c0 + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 32; ++i)
+                                if (half * 128 + c0 + i < K) trow[c0 + i] = v[i];
+                        }
+                    }
+                }
+            }
+            if (m < M) ++nacc;
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncthreads();   // accumulator of m-1 drained before it is reused by m+1
+            asm volatile("tcgen05.fence::after_thread_sync;");
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BT_N));
+    }
+}
+
+// Returns kNotApplicable when the shape does not fit (K > 256 or the row tile's
+// operand image exceeds shared memory); the caller then uses the FFMA table.
+int launch_table_tc(const float* X, long long n, long long ldx, int D, const float* cw, const double* sq, int M, int K,
+                    float* T, long long ldt, cudaStream_t s) {
+    if (K > BT_N || K < 1 || n <= 0) return n <= 0 ? 0 : kNotApplicable;
+    const int nch = (D + 1 + BT_BK - 1) / BT_BK;
+    const size_t smem = sizeof(float) * ((size_t)nch * 2 * BT_ROWS * BT_BK + 2 * 2 * (size_t)BT_N * BT_BK);
+    if (smem > 220 * 1024) return kNotApplicable;
+    float* Bg = (float*)scratch(14, sizeof(float) * (size_t)M * nch * 2 * BT_N * BT_BK, s);
+    if (!Bg) return fail_cuda(cudaErrorMemoryAllocation, "table_tc scratch");
+    cb_tf32_prep_kernel<<<grid_for((long long)M * nch * BT_N * BT_BK, 256, 4096), 256, 0, s>>>(cw, sq, M, K, D, nch, Bg);
+    DA_CHECK_LAUNCH("cb_tf32_prep_kernel(table)");
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = (int)std::min<long long>((n + 127) / 128, sms);
+    DA_CUDA(cudaFuncSetAttribute(table_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    table_tc_kernel<<<grid, 256, smem, s>>>(X, n, ldx, D, M, K, nch, Bg, T, ldt);
+    DA_CHECK_LAUNCH("table_tc_kernel");
+    return 0;
+}
+
+}  // namespace da

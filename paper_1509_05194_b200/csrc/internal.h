@@ -92,6 +92,8 @@ int launch_assign_tc(const void* X, int x_is_f32, long long n, long long ldx, in
 int set_assign_config(int mode, unsigned long long* stats);
 // launcher result meaning "this path does not take the shape" (caller falls through)
 constexpr int kNotApplicable = 1 << 30;
+int launch_table_tc(const float* X, long long n, long long ldx, int D, const float* cw, const double* sq, int M, int K,
+                    float* T, long long ldt, cudaStream_t s);
 int launch_encode_tc(const float* X, long long n, long long ldx, int D, const float* cw, int M, int K, int L,
                      const double* sq, const double* P, void* codes_out, int code_bytes, long long ldcodes,
                      double* err_out, unsigned long long* stats, cudaStream_t s);
