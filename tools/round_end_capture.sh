@@ -5,7 +5,7 @@ mkdir -p gpurun_out
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
 # launch list of the timed encode kernels (cold-cache, serialised: shares only)
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"encode|beam|sgemm|gemm_kernel|bound_prep" -c 60 --csv \
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"beam_fast|table_tc|sgemm_table|bound_prep|cb_tf32_prep" -c 60 --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-anneal --no-cpu > gpurun_out/ncu_launch.log 2>&1; echo "launch rc=$?"
 # full capture of the dominant kernel (L=10 gather filter) and of the tcgen05 filter at L=1
 ncu --set full --clock-control none --import-source on -k regex:beam_fast -c 1 -o gpurun_out/prof_beam_fast \
