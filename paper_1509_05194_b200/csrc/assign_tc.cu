@@ -118,7 +118,36 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 template <typename TX>
 __device__ __forceinline__ double fma_chain(const TX* __restrict__ xr, const double* __restrict__ cr, int k, int e,
                                             double acc) {
-    // loads are issued 24 ahead of the (strictly sequential) FMA chain
+    // loads are issued 24 ahead of the (strictly sequential) FMA chain; 16-byte
+    // loads when both rows are float64 and 16-byte aligned at k
+    if (sizeof(TX) == 8 && ((reinterpret_cast<uintptr_t>(xr + k) | reinterpret_cast<uintptr_t>(cr + k)) & 15) == 0) {
+        for (; k + 24 <= e; k += 24) {
+            double2 xv[12], cv[12];
+#pragma unroll
+            for (int u = 0; u < 12; ++u) {
+                xv[u] = *reinterpret_cast<const double2*>(reinterpret_cast<const double*>(xr) + k + 2 * u);
+                cv[u] = *reinterpret_cast<const double2*>(cr + k + 2 * u);
+            }
+#pragma unroll
+            for (int u = 0; u < 12; ++u) {
+                acc = __fma_rn(xv[u].x, cv[u].x, acc);
+                acc = __fma_rn(xv[u].y, cv[u].y, acc);
+            }
+        }
+        for (; k + 8 <= e; k += 8) {
+            double2 xv[4], cv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                xv[u] = *reinterpret_cast<const double2*>(reinterpret_cast<const double*>(xr) + k + 2 * u);
+                cv[u] = *reinterpret_cast<const double2*>(cr + k + 2 * u);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                acc = __fma_rn(xv[u].x, cv[u].x, acc);
+                acc = __fma_rn(xv[u].y, cv[u].y, acc);
+            }
+        }
+    }
     for (; k + 24 <= e; k += 24) {
         double xv[24], cv[24];
 #pragma unroll
