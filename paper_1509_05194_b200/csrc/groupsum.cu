@@ -289,6 +289,74 @@ __global__ void __launch_bounds__(256, 2) leaf_sum_kernel(const double* __restri
         if (cols[q] < D) leaf_sums[leaf * D + cols[q]] = res[q];
 }
 
+// Narrow rows (D <= 32): a warp serves 32 / ceil(D/2) leaves at once, each lane
+// owning two columns of one leaf (one 16-B load per row), same per-column order.
+__global__ void __launch_bounds__(256) leaf_sum_narrow_kernel(const double* __restrict__ X, long long ldx, int D,
+                                                              const int32_t* __restrict__ order,
+                                                              const int4* __restrict__ leaves,
+                                                              const int32_t* __restrict__ n_leaves_total,
+                                                              double* __restrict__ leaf_sums) {
+    const int lane = threadIdx.x & 31;
+    const int lpl = (D + 1) >> 1;              // lanes per leaf
+    const int per_warp = 32 / lpl;
+    const long long warp_id = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int g = lane / lpl, c = lane % lpl;
+    const long long leaf = warp_id * per_warp + g;
+    if (g >= per_warp || leaf >= (long long)(*n_leaves_total)) return;
+    const int4 L = leaves[leaf];
+    const int start = L.y, n = L.z;
+    const int c0 = 2 * c, c1 = 2 * c + 1;
+    const bool vec = ((ldx & 1) == 0) && (c1 < D);
+    auto load_row = [&](long long r, double* out2) {
+        const double* p = X + r * ldx;
+        if (vec) {
+            const double2 a = *reinterpret_cast<const double2*>(p + c0);
+            out2[0] = a.x; out2[1] = a.y;
+        } else {
+            out2[0] = c0 < D ? p[c0] : 0.0;
+            out2[1] = c1 < D ? p[c1] : 0.0;
+        }
+    };
+    double res[2];
+    if (n < 8) {
+        res[0] = res[1] = 0.0;
+        for (int i = 0; i < n; ++i) {
+            double v[2];
+            load_row(order[start + i], v);
+            res[0] = dadd(res[0], v[0]);
+            res[1] = dadd(res[1], v[1]);
+        }
+    } else {
+        double acc[8][2];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) load_row(order[start + j], acc[j]);
+        int i = 8;
+        const int stop = n - (n % 8);
+        for (; i < stop; i += 8) {
+            double v[8][2];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) load_row(order[start + i + j], v[j]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                acc[j][0] = dadd(acc[j][0], v[j][0]);
+                acc[j][1] = dadd(acc[j][1], v[j][1]);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+            res[q] = dadd(dadd(dadd(acc[0][q], acc[1][q]), dadd(acc[2][q], acc[3][q])),
+                          dadd(dadd(acc[4][q], acc[5][q]), dadd(acc[6][q], acc[7][q])));
+        for (; i < n; ++i) {
+            double v[2];
+            load_row(order[start + i], v);
+            res[0] = dadd(res[0], v[0]);
+            res[1] = dadd(res[1], v[1]);
+        }
+    }
+    if (c0 < D) leaf_sums[leaf * D + c0] = res[0];
+    if (c1 < D) leaf_sums[leaf * D + c1] = res[1];
+}
+
 // One warp per (codeword, column chunk): fold leaves up the recursion tree,
 // prepend the first row, divide by the count.  mode 0 = write means into the
 // filled rows of C (empties untouched); mode 1 = write raw sums (all rows).
@@ -425,9 +493,16 @@ int launch_group_sums(const double* X, long long n, long long ldx, int D, const 
     {
         long long tasks = max_leaves * n_chunks;
         ProfScope ps3("group_sums_leaf", s);
-        leaf_sum_kernel<<<grid_for(tasks, 8, 1LL << 31), 256, 0, s>>>(X, ldx, D, order, leaves, total + 1,
-                                                                      n_chunks, lsum);
-        DA_CHECK_LAUNCH("leaf_sum_kernel");
+        if (D <= 32) {
+            const long long per_warp = 32 / ((D + 1) / 2);
+            leaf_sum_narrow_kernel<<<grid_for((max_leaves + per_warp - 1) / per_warp, 8, 1LL << 31), 256, 0, s>>>(
+                X, ldx, D, order, leaves, total + 1, lsum);
+            DA_CHECK_LAUNCH("leaf_sum_narrow_kernel");
+        } else {
+            leaf_sum_kernel<<<grid_for(tasks, 8, 1LL << 31), 256, 0, s>>>(X, ldx, D, order, leaves, total + 1,
+                                                                          n_chunks, lsum);
+            DA_CHECK_LAUNCH("leaf_sum_kernel");
+        }
     }
     {
         long long tasks = (long long)K * n_chunks;
