@@ -161,6 +161,65 @@ __global__ void stable_scatter_kernel(const int32_t* __restrict__ labels, long l
     }
 }
 
+// Same stable scatter with four warps per tile: warp w takes rows
+// [lo + 256w, lo + 256w + 256); per-warp label counts (shared memory) turn the
+// tile cursor into per-warp cursors, so the rows still land in row order.
+constexpr int GS_SW = 4;
+__global__ void __launch_bounds__(32 * GS_SW) stable_scatter4_kernel(const int32_t* __restrict__ labels, long long n,
+                                                                    int K, int T, const int32_t* __restrict__ cursor,
+                                                                    int32_t* __restrict__ order) {
+    extern __shared__ int32_t wc[];   // [GS_SW][K]
+    const int t = blockIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long lo = (long long)t * GS_TILE + (long long)w * (GS_TILE / GS_SW);
+    const long long hi = min(n, lo + GS_TILE / GS_SW);
+    const unsigned lt_mask = (1u << lane) - 1u;
+    for (int k = threadIdx.x; k < GS_SW * K; k += blockDim.x) wc[k] = 0;
+    __syncthreads();
+    int* my = wc + w * K;
+    for (long long base = lo; base < hi; base += 32) {
+        const long long r = base + lane;
+        const bool valid = r < hi;
+        const unsigned active = __ballot_sync(0xffffffffu, valid);
+        if (valid) {
+            const int lab = labels[r];
+            const unsigned peers = __match_any_sync(active, lab);
+            if (lane == __ffs(peers) - 1) my[lab] += __popc(peers);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+        int c = cursor[(long long)k * T + t];
+#pragma unroll
+        for (int q = 0; q < GS_SW; ++q) {
+            const int v = wc[q * K + k];
+            wc[q * K + k] = c;
+            c += v;
+        }
+    }
+    __syncthreads();
+    int lab_next = (lo + lane < hi) ? labels[lo + lane] : 0;
+    for (long long base = lo; base < hi; base += 32) {
+        const long long r = base + lane;
+        const bool valid = r < hi;
+        const int lab = lab_next;
+        lab_next = (r + 32 < hi) ? labels[r + 32] : 0;
+        const unsigned active = __ballot_sync(0xffffffffu, valid);
+        if (valid) {
+            const unsigned peers = __match_any_sync(active, lab);
+            const int leader = __ffs(peers) - 1;
+            const int rank = __popc(peers & lt_mask);
+            int b = 0;
+            if (lane == leader) b = my[lab];
+            b = __shfl_sync(peers, b, leader);
+            order[b + rank] = (int32_t)r;
+            if (lane == leader) my[lab] = b + __popc(peers);
+        }
+        __syncwarp();
+    }
+}
+
 // ---- pairwise recursion bookkeeping ----------------------------------------
 
 __device__ long long pw_leaf_count(long long m) {
@@ -482,8 +541,13 @@ int launch_group_sums(const double* X, long long n, long long ldx, int D, const 
     DA_CHECK_LAUNCH("exclusive_scan_kernel(counts)");
     add_seg_start_kernel<<<grid_for(KT, 256, 1LL << 31), 256, 0, s>>>(hist, K, T, seg);
     DA_CHECK_LAUNCH("add_seg_start_kernel");
-    stable_scatter_kernel<<<T, 32, sh, s>>>(labels, n, K, T, hist, order);
-    DA_CHECK_LAUNCH("stable_scatter_kernel");
+    if ((size_t)GS_SW * K * sizeof(int32_t) <= 48 * 1024) {
+        stable_scatter4_kernel<<<T, 32 * GS_SW, sizeof(int32_t) * GS_SW * K, s>>>(labels, n, K, T, hist, order);
+        DA_CHECK_LAUNCH("stable_scatter4_kernel");
+    } else {
+        stable_scatter_kernel<<<T, 32, sh, s>>>(labels, n, K, T, hist, order);
+        DA_CHECK_LAUNCH("stable_scatter_kernel");
+    }
     leaf_count_kernel<<<grid_for(K, 256), 256, 0, s>>>(counts, K, nleaf);
     DA_CHECK_LAUNCH("leaf_count_kernel");
     exclusive_scan_kernel<<<1, 1024, 0, s>>>(nleaf, K, total + 1);
