@@ -189,7 +189,7 @@ __global__ void col_partial_kernel(const T* __restrict__ X, long long n, long lo
 // chain.  A block owns 8 columns: all 256 threads stream row chunks into shared
 // memory (double-buffered, coalesced 8-column segments) while 8 threads of warp
 // 0 run the chains out of shared memory.
-constexpr int CM_COLS = 8, CM_ROWS = 256, CM_T = 256;
+constexpr int CM_COLS = 1, CM_ROWS = 2048, CM_T = 256;
 
 template <typename T>
 __global__ void __launch_bounds__(CM_T) col_mean_seq_kernel(const T* __restrict__ X, long long n, long long ld, int D,
