@@ -10,6 +10,8 @@
 // k staged through shared memory in chunks of 16.  The argmin is fused into
 // the epilogue of every codeword tile; a running (value, index) minimum per
 // row is kept in registers and reduced across the 16 column lanes at the end.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -197,10 +199,116 @@ int set_assign_config(int mode, unsigned long long* stats) {
     return 0;
 }
 
+// Small active widths (d <= 16): every candidate exactly, no filter.  Thread per
+// row, the row in registers, the codebook (K x d float64) and its norms in shared
+// memory (broadcast reads); four codewords' FMA chains interleave for ILP.  Same
+// value per candidate as the reference ((xx - 2 x.c) + cc, dot as one FMA chain
+// from 0, clipped at 0) and the same first-index minimum.
+constexpr int AS_SMALL_D = 16;
+constexpr int AS_SMALL_R = 2;   // rows per thread (each codeword load feeds both)
+template <typename TX>
+__global__ void __launch_bounds__(256) assign_small_kernel(const TX* __restrict__ X, long long n, long long ldx, int d,
+                                                           const double* __restrict__ C, long long ldc, int K,
+                                                           const double* __restrict__ cc,
+                                                           const double* __restrict__ xx_in,
+                                                           int32_t* __restrict__ labels, double* __restrict__ d2,
+                                                           const int32_t* __restrict__ prev,
+                                                           unsigned long long* __restrict__ changed) {
+    extern __shared__ double sC[];   // [K][dp] (dp = d rounded up to even, zero padded), then cc[K]
+    const int dp = (d + 1) & ~1;
+    double* scc = sC + (size_t)K * dp;
+    for (int i = threadIdx.x; i < K * dp; i += blockDim.x) {
+        const int k = i / dp, j = i % dp;
+        sC[i] = j < d ? C[(long long)k * ldc + j] : 0.0;
+    }
+    for (int k = threadIdx.x; k < K; k += blockDim.x) scc[k] = cc[k];
+    __syncthreads();
+    const long long r0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * AS_SMALL_R;
+    double x[AS_SMALL_R][AS_SMALL_D], xx[AS_SMALL_R], best[AS_SMALL_R];
+    int bk[AS_SMALL_R];
+#pragma unroll
+    for (int t = 0; t < AS_SMALL_R; ++t) {
+        const long long r = r0 + t;
+        const TX* xr = X + (r < n ? r : 0) * ldx;
+#pragma unroll
+        for (int j = 0; j < AS_SMALL_D; ++j) x[t][j] = (j < d && r < n) ? (double)xr[j] : 0.0;
+        xx[t] = r < n ? (xx_in ? xx_in[r]
+                               : np_pw_sum([&](long long i) { double v = (double)xr[i]; return dmul(v, v); }, 0, d))
+                      : 0.0;
+        best[t] = __longlong_as_double(0x7ff0000000000000ULL);
+        bk[t] = 0x7fffffff;
+    }
+    for (int k0 = 0; k0 < K; k0 += 4) {
+        double a[AS_SMALL_R][4];
+#pragma unroll
+        for (int t = 0; t < AS_SMALL_R; ++t)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[t][u] = 0.0;
+#pragma unroll
+        for (int j = 0; j < AS_SMALL_D; j += 2) {
+            if (j < d) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (k0 + u < K) {
+                        const double2 c2 = *reinterpret_cast<const double2*>(sC + (size_t)(k0 + u) * dp + j);
+#pragma unroll
+                        for (int t = 0; t < AS_SMALL_R; ++t) {
+                            a[t][u] = __fma_rn(x[t][j], c2.x, a[t][u]);
+                            if (j + 1 < d) a[t][u] = __fma_rn(x[t][j + 1], c2.y, a[t][u]);
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int k = k0 + u;
+            if (k < K) {
+#pragma unroll
+                for (int t = 0; t < AS_SMALL_R; ++t) {
+                    double dv = dadd(dsub(xx[t], dmul(2.0, a[t][u])), scc[k]);
+                    if (dv < 0.0) dv = 0.0;
+                    if (dv < best[t]) { best[t] = dv; bk[t] = k; }   // k ascending: first index wins ties
+                }
+            }
+        }
+    }
+    unsigned nchg = 0;
+#pragma unroll
+    for (int t = 0; t < AS_SMALL_R; ++t) {
+        const long long r = r0 + t;
+        if (r < n) {
+            labels[r] = bk[t];
+            d2[r] = best[t];
+            if (changed != nullptr && prev != nullptr && prev[r] != bk[t]) ++nchg;
+        }
+    }
+    if (changed != nullptr && prev != nullptr) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) nchg += __shfl_xor_sync(0xffffffffu, nchg, o);
+        if ((threadIdx.x & 31) == 0 && nchg) atomicAdd(changed, (unsigned long long)nchg);
+    }
+}
+
 int launch_assign(const void* X, int x_is_f32, long long n, long long ldx, int d, const double* C,
                   long long ldc, int K, const double* cc, const double* xx, int32_t* labels, double* d2,
                   const int32_t* prev, unsigned long long* changed, cudaStream_t s) {
     if (n <= 0) return 0;
+    // measured crossover against the tensor-core filter on B200: d <= 3
+    static const int small_max = getenv("DA_ASSIGN_SMALL_D") ? atoi(getenv("DA_ASSIGN_SMALL_D")) : 3;
+    if (g_assign_mode == 0 && d <= small_max && K <= 4096) {
+        ProfScope ps("assign_small_d<=16", s);
+        const size_t smem = sizeof(double) * ((size_t)K * ((d + 1) & ~1) + K);
+        const unsigned g = grid_for((n + AS_SMALL_R - 1) / AS_SMALL_R, 256, 1LL << 31);
+        if (x_is_f32)
+            assign_small_kernel<float><<<g, 256, smem, s>>>((const float*)X, n, ldx, d, C, ldc, K, cc, xx, labels, d2,
+                                                            prev, changed);
+        else
+            assign_small_kernel<double><<<g, 256, smem, s>>>((const double*)X, n, ldx, d, C, ldc, K, cc, xx, labels,
+                                                             d2, prev, changed);
+        DA_CHECK_LAUNCH("assign_small_kernel");
+        return 0;
+    }
     if (g_assign_mode == 0) {
         int rc = launch_assign_tc(X, x_is_f32, n, ldx, d, C, ldc, K, cc, xx, labels, d2, prev, changed, g_assign_stats, s);
         if (rc <= 0) return rc;

@@ -52,3 +52,34 @@ def test_float32_rows_and_large_values():
     (lt, dt), (lp, dp), _ = both(X, 128, C)
     np.testing.assert_array_equal(lt, lp)
     np.testing.assert_array_equal(dt, dp)
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 5, 16])
+def test_small_width_exact_kernel_matches_plain(d):
+    """The direct float64 kernel for small active widths equals the plain kernel."""
+    import os
+    import subprocess
+    import sys
+
+    code = f"""
+import numpy as np, torch, sys
+sys.path.insert(0, {repr(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))})
+from paper_1509_05194_b200 import _engine as E
+g = torch.Generator(device="cuda").manual_seed({d})
+X = torch.randn((20000, 24), dtype=torch.float64, device="cuda", generator=g) * 3
+C = X[torch.randint(0, 20000, (256,), device="cuda", generator=g)].clone()
+C[7] = C[3]
+prev = torch.randint(0, 256, (20000,), dtype=torch.int32, device="cuda", generator=g)
+outs = []
+for mode in (0, 1):
+    E.assign_config(mode)
+    ch = torch.zeros(1, dtype=torch.int64, device="cuda")
+    lab, d2 = E.assign(X, {d}, C, prev=prev, changed=ch)
+    outs.append((lab.cpu().numpy(), d2.cpu().numpy(), int(ch.item())))
+E.assign_config(0)
+assert (outs[0][0] == outs[1][0]).all() and (outs[0][1] == outs[1][1]).all() and outs[0][2] == outs[1][2]
+print("ok")
+"""
+    env = dict(os.environ, DA_ASSIGN_SMALL_D="16")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
