@@ -341,14 +341,24 @@ int launch_adc_pack(const void* codes, long long n, long long ldc, const double*
 
 // Same scan over packed records; every lane scores ADC_U candidates per step so
 // their id and record loads are in flight together.
-constexpr int ADC_U = 4;
+#ifndef DA_ADC_U
+#define DA_ADC_U 4
+#endif
+constexpr int ADC_U = DA_ADC_U;
 
-// one random 16-byte record: no L1 allocation, smallest L2 prefetch granule
+// one random 16-byte record: no L1 allocation; HINT 1 adds the L2::64B prefetch
+// granule, HINT 0 leaves the fetch size to the device limit
+template <int HINT>
 __device__ __forceinline__ uint4 adc_ld_rec(const uint4* p) {
     uint4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p));
+    if (HINT)
+        asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "l"(p));
+    else
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "l"(p));
     return v;
 }
 
@@ -364,11 +374,23 @@ __device__ __forceinline__ double adc_rec_dist(uint4 rc, const double* slut, int
     return dist;
 }
 
+// order-preserving 64-bit key of a non-NaN double (for the shared threshold)
+__device__ __forceinline__ unsigned long long dkey(double d) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+    return (b & 0x8000000000000000ULL) ? ~b : (b | 0x8000000000000000ULL);
+}
+
+// Candidates stream through a two-deep software pipeline: the ids of step i+1
+// are in flight while the records of step i are scored.  The warps of a CTA
+// share one threshold (the smallest r-th distance of any warp's full list): a
+// candidate above it cannot be in the query's top r, so it is never inserted.
+template <int HINT>
 __global__ void adc_scan_packed_kernel(const uint4* __restrict__ rec, const long long* __restrict__ cand,
                                        long long ncand, const double* __restrict__ lut,
                                        const double* __restrict__ qsq, int M, int K, int r,
                                        long long* __restrict__ ids_out, double* __restrict__ d_out) {
     extern __shared__ __align__(16) char smem[];
+    __shared__ unsigned long long s_thr;
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const long long q = blockIdx.x;
@@ -377,27 +399,36 @@ __global__ void adc_scan_packed_kernel(const uint4* __restrict__ rec, const long
     for (int i = threadIdx.x; i < MK; i += blockDim.x) slut[i] = lut[q * MK + i];
     double* lv_base = slut + MK;
     long long* lp_base = (long long*)(lv_base + (size_t)nw * r);
+    if (threadIdx.x == 0) s_thr = ~0ULL;
     __syncthreads();
     TopList L{lv_base + (size_t)wid * r, lp_base + (size_t)wid * r};
     int cnt = 0;
     const double shift = dmul((double)(M - 1), qsq[q]);
     const long long* qc = cand ? cand + q * ncand : nullptr;
-    for (long long b = (long long)wid * 32 * ADC_U; b < ncand; b += (long long)nw * 32 * ADC_U) {
-        long long pp[ADC_U], row[ADC_U];
-        uint4 rc[ADC_U];
+    const long long stride = (long long)nw * 32 * ADC_U;
+    auto load_rows = [&](long long b, long long* row) {
 #pragma unroll
         for (int u = 0; u < ADC_U; ++u) {
-            pp[u] = b + u * 32 + lane;
-            row[u] = pp[u] < ncand ? (qc ? __ldg(qc + pp[u]) : pp[u]) : -1;
+            const long long p = b + u * 32 + lane;
+            row[u] = p < ncand ? (qc ? __ldg(qc + p) : p) : -1;
         }
+    };
+    long long row[ADC_U], nrow[ADC_U];
+    long long b = (long long)wid * 32 * ADC_U;
+    load_rows(b, row);
+    for (; b < ncand; b += stride) {
+        uint4 rc[ADC_U];
 #pragma unroll
-        for (int u = 0; u < ADC_U; ++u) rc[u] = row[u] >= 0 ? adc_ld_rec(rec + row[u]) : make_uint4(0, 0, 0, 0);
+        for (int u = 0; u < ADC_U; ++u) rc[u] = row[u] >= 0 ? adc_ld_rec<HINT>(rec + row[u]) : make_uint4(0, 0, 0, 0);
+        load_rows(b + stride, nrow);
+        const unsigned long long thr = *(volatile unsigned long long*)&s_thr;
 #pragma unroll
         for (int u = 0; u < ADC_U; ++u) {
             const bool valid = row[u] >= 0;
             const double dist = valid ? adc_rec_dist(rc[u], slut, M, K, shift) : 0.0;
-            const long long p = pp[u];
+            const long long p = b + u * 32 + lane;
             auto accept = [&](double a, long long pa) -> bool {
+                if (dkey(a) > thr) return false;
                 if (cnt < r) return true;
                 return lex_less(a, pa, L.v[r - 1], L.p[r - 1]);
             };
@@ -411,6 +442,9 @@ __global__ void adc_scan_packed_kernel(const uint4* __restrict__ rec, const long
                 mask &= __ballot_sync(FULL, valid && accept(dist, p));
             }
         }
+        if (cnt == r && lane == 0) atomicMin(&s_thr, dkey(L.v[r - 1]));
+#pragma unroll
+        for (int u = 0; u < ADC_U; ++u) row[u] = nrow[u];
     }
     __shared__ int cnts[32];
     if (lane == 0) cnts[wid] = cnt;
@@ -458,11 +492,15 @@ int launch_adc_scan_packed(const void* records, const long long* cand, long long
     while (warps > 1 && lut_b + (size_t)warps * r * 16 > 200 * 1024) warps >>= 1;
     const size_t smem = lut_b + (size_t)warps * r * 16;
     if (smem > 220 * 1024) return fail_arg("adc_scan: r=%d with M*K=%d exceeds shared memory", r, M * K);
+    // DA_ADC_HINT=0 drops the L2::64B qualifier (measured: 128 B of DRAM per
+    // record instead of 64; cudaLimitMaxL2FetchGranularity has no effect)
+    const char* eh = getenv("DA_ADC_HINT");
+    const int hint = eh ? atoi(eh) : 1;
+    auto kf = hint ? adc_scan_packed_kernel<1> : adc_scan_packed_kernel<0>;
     ProfScope ps("adc_scan_packed", s);
     if (smem > 48 * 1024)
-        DA_CUDA(cudaFuncSetAttribute(adc_scan_packed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    adc_scan_packed_kernel<<<(unsigned)nq, warps * 32, smem, s>>>((const uint4*)records, cand, ncand, lut, qsq, M, K,
-                                                                 r, ids_out, d_out);
+        DA_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kf<<<(unsigned)nq, warps * 32, smem, s>>>((const uint4*)records, cand, ncand, lut, qsq, M, K, r, ids_out, d_out);
     DA_CHECK_LAUNCH("adc_scan_packed_kernel");
     return 0;
 }
