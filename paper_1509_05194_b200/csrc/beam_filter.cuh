@@ -1,0 +1,106 @@
+// Pieces of the fp32 gather-filter beam encoder (encode_fast.cu): per-warp
+// shared-memory carving, the exact float64 dot in the reference's BLAS order,
+// and order-preserving float keys for redux.sync.
+#pragma once
+#include "common.cuh"
+
+namespace da {
+
+constexpr int QCAP = 224;  // per-warp recheck queue
+
+// The double-buffered beam state is addressed as base + cur * stride (a
+// two-element pointer array indexed by the stage parity would live in local
+// memory and turn every shared access into a generic one).
+struct FastSmem {
+    int32_t* codes;  // [2][cap*M]
+    double* score;   // [2][cap]
+    double* lv;
+    int32_t* lf;
+    double* x64;     // [D]
+    float* vbuf;     // [cap*K] approximate values; reused as D doubles for the error
+    int32_t* queue;  // [33 + QCAP]: [32] = count, [33..] = queued flat indices
+    long long* roff; // [cap*M] cross-table row offsets of the current stage
+};
+
+__host__ __device__ inline size_t fast_vbuf_bytes(int cap, int K, int D) {
+    size_t a = sizeof(float) * (size_t)cap * K, b = sizeof(double) * (size_t)D;
+    size_t c = (sizeof(double) + sizeof(int)) * (size_t)QCAP;  // exact (value, flat) of queued candidates
+    size_t m = a > b ? a : b;
+    m = m > c ? m : c;
+    return (m + 15) & ~size_t(15);
+}
+
+__host__ __device__ inline size_t fast_smem_bytes(int cap, int M, int K, int D) {
+    size_t b = sizeof(double) * (3 * (size_t)cap + D) + sizeof(long long) * (size_t)cap * M;
+    b = (b + 15) & ~size_t(15);
+    b += fast_vbuf_bytes(cap, K, D);
+    b += sizeof(int32_t) * (2 * (size_t)cap * M + cap + 33 + QCAP);
+    return (b + 15) & ~size_t(15);
+}
+
+__device__ inline FastSmem carve_fast(char* p, int cap, int M, int K, int D) {
+    FastSmem s;
+    char* p0 = p;
+    s.x64 = (double*)p; p += sizeof(double) * D;  // first: 16-byte aligned for double2 reads
+    s.score = (double*)p; p += 2 * sizeof(double) * cap;
+    s.lv = (double*)p; p += sizeof(double) * cap;
+    s.roff = (long long*)p; p += sizeof(long long) * cap * M;
+    p = p0 + (((size_t)(p - p0) + 15) & ~size_t(15));
+    s.vbuf = (float*)p; p += fast_vbuf_bytes(cap, K, D);
+    s.codes = (int32_t*)p; p += 2 * sizeof(int32_t) * cap * M;
+    s.lf = (int32_t*)p; p += sizeof(int32_t) * cap;
+    s.queue = (int32_t*)p;
+    return s;
+}
+
+// exact x.c (reference order: FMA chain over d, OpenBLAS k-blocks above 384)
+__device__ __forceinline__ double exact_dot(const double* __restrict__ x64, const double* __restrict__ c, int D,
+                                            const float* __restrict__ c32 = nullptr) {
+    double tot = 0.0;
+    bool first = true;
+    int d = 0;
+    while (d < D) {
+        const int len = (int)blas_block_len(D - d);
+        double acc = 0.0;
+        const int e = d + len;
+        // loads run ahead of the (strictly sequential) FMA chain: 16 codeword values
+        // per batch, fp32 in memory (exact in float64) so a batch is 4 vector loads
+        if (c32) {
+            for (; d + 32 <= e; d += 32) {
+                float4 cv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) cv[u] = __ldg(reinterpret_cast<const float4*>(c32 + d) + u);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    acc = __fma_rn(x64[d + 4 * u + 0], (double)cv[u].x, acc);
+                    acc = __fma_rn(x64[d + 4 * u + 1], (double)cv[u].y, acc);
+                    acc = __fma_rn(x64[d + 4 * u + 2], (double)cv[u].z, acc);
+                    acc = __fma_rn(x64[d + 4 * u + 3], (double)cv[u].w, acc);
+                }
+            }
+        }
+        for (; d + 8 <= e; d += 8) {
+            double cv[8];
+            double xv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) { cv[u] = __ldg(c + d + u); xv[u] = x64[d + u]; }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = __fma_rn(xv[u], cv[u], acc);
+        }
+        for (; d < e; ++d) acc = __fma_rn(x64[d], c[d], acc);
+        tot = first ? acc : dadd(tot, acc);
+        first = false;
+    }
+    return tot;
+}
+
+// float <-> unsigned key with the same order (for redux.sync.min)
+__device__ __forceinline__ unsigned fkey(float f) {
+    const unsigned b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float funkey(unsigned k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+}  // namespace da

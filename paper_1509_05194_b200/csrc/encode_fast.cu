@@ -18,9 +18,11 @@
 // Beam scores are always the exact float64 values, so codes and errors equal
 // the reference's; only the amount of float64 work changes.
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "internal.h"
+#include "beam_filter.cuh"
 
 namespace da {
 
@@ -28,7 +30,6 @@ namespace da {
 // SGEMM for the approximate score table: T[i, j] = sq32[j] - 2 * sum_k X[i,k] C[j,k]
 namespace {
 constexpr int SG_BM = 128, SG_BN = 128, SG_BK = 8, SG_T = 256;
-constexpr int QCAP = 224;  // per-warp recheck queue
 }
 
 __global__ void __launch_bounds__(SG_T) sgemm_table_kernel(const float* __restrict__ X, long long n, long long ldx,
@@ -149,102 +150,6 @@ __global__ void bound_prep_kernel(const float* __restrict__ cw, const double* __
     }
 }
 
-// ---------------------------------------------------------------------------
-
-struct FastSmem {
-    int32_t* codes[2];
-    double* score[2];
-    double* lv;
-    int32_t* lf;
-    double* x64;     // [D]
-    float* vbuf;     // [cap*K] approximate values; reused as D doubles for the error
-    int32_t* queue;  // [33 + QCAP]: [32] = count, [33..] = queued flat indices
-    long long* roff; // [cap*M] cross-table row offsets of the current stage
-};
-
-__host__ __device__ inline size_t fast_vbuf_bytes(int cap, int K, int D) {
-    size_t a = sizeof(float) * (size_t)cap * K, b = sizeof(double) * (size_t)D;
-    size_t c = (sizeof(double) + sizeof(int)) * (size_t)QCAP;  // exact (value, flat) of queued candidates
-    size_t m = a > b ? a : b;
-    m = m > c ? m : c;
-    return (m + 15) & ~size_t(15);
-}
-
-__host__ __device__ inline size_t fast_smem_bytes(int cap, int M, int K, int D) {
-    size_t b = sizeof(double) * (3 * (size_t)cap + D) + sizeof(long long) * (size_t)cap * M;
-    b = (b + 15) & ~size_t(15);
-    b += fast_vbuf_bytes(cap, K, D);
-    b += sizeof(int32_t) * (2 * (size_t)cap * M + cap + 33 + QCAP);
-    return (b + 15) & ~size_t(15);
-}
-
-__device__ inline FastSmem carve_fast(char* p, int cap, int M, int K, int D) {
-    FastSmem s;
-    char* p0 = p;
-    s.score[0] = (double*)p; p += sizeof(double) * cap;
-    s.score[1] = (double*)p; p += sizeof(double) * cap;
-    s.lv = (double*)p; p += sizeof(double) * cap;
-    s.x64 = (double*)p; p += sizeof(double) * D;
-    s.roff = (long long*)p; p += sizeof(long long) * cap * M;
-    p = p0 + (((size_t)(p - p0) + 15) & ~size_t(15));
-    s.vbuf = (float*)p; p += fast_vbuf_bytes(cap, K, D);
-    s.codes[0] = (int32_t*)p; p += sizeof(int32_t) * cap * M;
-    s.codes[1] = (int32_t*)p; p += sizeof(int32_t) * cap * M;
-    s.lf = (int32_t*)p; p += sizeof(int32_t) * cap;
-    s.queue = (int32_t*)p;
-    return s;
-}
-
-// exact x.c (reference order: FMA chain over d, OpenBLAS k-blocks above 384)
-__device__ __forceinline__ double exact_dot(const double* __restrict__ x64, const double* __restrict__ c, int D,
-                                            const float* __restrict__ c32 = nullptr) {
-    double tot = 0.0;
-    bool first = true;
-    int d = 0;
-    while (d < D) {
-        const int len = (int)blas_block_len(D - d);
-        double acc = 0.0;
-        const int e = d + len;
-        // loads run ahead of the (strictly sequential) FMA chain: 16 codeword values
-        // per batch, fp32 in memory (exact in float64) so a batch is 4 vector loads
-        if (c32) {
-            for (; d + 32 <= e; d += 32) {
-                float4 cv[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) cv[u] = __ldg(reinterpret_cast<const float4*>(c32 + d) + u);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    acc = __fma_rn(x64[d + 4 * u + 0], (double)cv[u].x, acc);
-                    acc = __fma_rn(x64[d + 4 * u + 1], (double)cv[u].y, acc);
-                    acc = __fma_rn(x64[d + 4 * u + 2], (double)cv[u].z, acc);
-                    acc = __fma_rn(x64[d + 4 * u + 3], (double)cv[u].w, acc);
-                }
-            }
-        }
-        for (; d + 8 <= e; d += 8) {
-            double cv[8];
-            double xv[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) { cv[u] = __ldg(c + d + u); xv[u] = x64[d + u]; }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) acc = __fma_rn(xv[u], cv[u], acc);
-        }
-        for (; d < e; ++d) acc = __fma_rn(x64[d], c[d], acc);
-        tot = first ? acc : dadd(tot, acc);
-        first = false;
-    }
-    return tot;
-}
-
-// float <-> unsigned key with the same order (for redux.sync.min)
-__device__ __forceinline__ unsigned fkey(float f) {
-    const unsigned b = __float_as_uint(f);
-    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-}
-__device__ __forceinline__ float funkey(unsigned k) {
-    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
-}
-
 template <typename TX>
 __global__ void __launch_bounds__(256) beam_fast_kernel(
     const TX* __restrict__ X, long long n, long long ldx, int D, const float* __restrict__ cw, int M, int K, int L,
@@ -261,10 +166,10 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
     if (v >= n) return;
     FastSmem S = carve_fast(smem_raw + (size_t)wid * fast_smem_bytes(cap, M, K, D), cap, M, K, D);
     // 16-byte aligned fp32 codeword rows (D % 4 == 0): vector loads in the exact dot
-    const bool c32ok = (D & 3) == 0 && ((reinterpret_cast<uintptr_t>(cw) & 15) == 0);
-    // power-of-two shapes index with shifts instead of integer division
     const int nkb = (K + 31) / 32;
     const int nkb_sh = (nkb & (nkb - 1)) == 0 ? __ffs(nkb) - 1 : -1;
+    const bool c32ok = (D & 3) == 0 && ((reinterpret_cast<uintptr_t>(cw) & 15) == 0);
+    // power-of-two shapes index with shifts instead of integer division
     const int k_sh = (K & (K - 1)) == 0 ? __ffs(K) - 1 : -1;
     const float* trow = tab32 + v * (long long)M * K;
     const TX* xr = X + v * ldx;
@@ -277,7 +182,7 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
     }
     for (int off = 16; off >= 1; off >>= 1) xx_part += __shfl_xor_sync(FULL, xx_part, off);
     const double xnorm = sqrt(xx_part) * (1.0 + 1e-12);
-    if (lane == 0) S.score[0][0] = 0.0;
+    if (lane == 0) S.score[0] = 0.0;
     __syncwarp();
     const double u = 5.9604644775390625e-08;  // 2^-24
     unsigned long long n_exact = 0;
@@ -286,8 +191,8 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
     for (int m = 0; m < M; ++m) {
         const int total = live * K;
         const int width = min(L, total);
-        const int32_t* pc = S.codes[cur];
-        const double* ps = S.score[cur];
+        const int32_t* pc = S.codes + cur * cap * M;
+        const double* ps = S.score + cur * cap;
         // ---- rigorous bound of |v' - v| for this stage
         double smax = 0.0;
         for (int l = lane; l < live; l += 32) smax = fmax(smax, fabs(ps[l]));
@@ -336,20 +241,47 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
                     tk[q] = (k < K) ? trow[m * K + k] : 0.f;
                 }
             }
-            for (int l0 = 0; l0 < live; l0 += 4) {
-                float acc[4][8];
+            // A group of G consecutive beams (flat-index order = lexicographic order
+            // of the code prefixes) shares its first gl codes, so the rows j < gl
+            // are gathered once and the running sum is copied to every beam; the
+            // additions stay in j order, so each value is bit-identical to a
+            // per-beam gather.  A tail group has exactly live - l0 beams.
+            auto group = [&](auto Gc, int l0) {
+                constexpr int G = decltype(Gc)::value;
+                const int last = l0 + G - 1;
+                const bool same = lane < m && pc[l0 * M + lane] == pc[last * M + lane];
+                const unsigned neq = ~__ballot_sync(FULL, same);
+                const int gl = neq ? min(m, __ffs(neq) - 1) : min(m, 32);
+                float acc[G][8];
+                {
+                    float sh[8];
 #pragma unroll
-                for (int g = 0; g < 4; ++g)
+                    for (int q = 0; q < 8; ++q) sh[q] = 0.f;
+                    for (int j = 0; j < gl; ++j) {
+                        const float* rp = P32 + S.roff[l0 * M + j] + kb;
+                        if (vec) {
+                            const float4 a = __ldg(reinterpret_cast<const float4*>(rp + 4 * lane));
+                            const float4 b = __ldg(reinterpret_cast<const float4*>(rp + 128 + 4 * lane));
+                            sh[0] += a.x; sh[1] += a.y; sh[2] += a.z; sh[3] += a.w;
+                            sh[4] += b.x; sh[5] += b.y; sh[6] += b.z; sh[7] += b.w;
+                        } else {
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) acc[g][q] = 0.f;
-                for (int j = 0; j < m; ++j) {
-                    const float* rp[4];
+                            for (int q = 0; q < 8; ++q) sh[q] += (kof(kb, q) < K) ? __ldg(rp + 32 * q + lane) : 0.f;
+                        }
+                    }
 #pragma unroll
-                    for (int g = 0; g < 4; ++g) rp[g] = P32 + S.roff[min(l0 + g, live - 1) * M + j] + kb;
-                    float vals[4][8];
+                    for (int g = 0; g < G; ++g)
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) acc[g][q] = sh[q];
+                }
+                for (int j = gl; j < m; ++j) {
+                    const float* rp[G];
+#pragma unroll
+                    for (int g = 0; g < G; ++g) rp[g] = P32 + S.roff[(l0 + g) * M + j] + kb;
+                    float vals[G][8];
                     if (vec) {
 #pragma unroll
-                        for (int g = 0; g < 4; ++g) {
+                        for (int g = 0; g < G; ++g) {
                             const float4 a = __ldg(reinterpret_cast<const float4*>(rp[g] + 4 * lane));
                             const float4 b = __ldg(reinterpret_cast<const float4*>(rp[g] + 128 + 4 * lane));
                             vals[g][0] = a.x; vals[g][1] = a.y; vals[g][2] = a.z; vals[g][3] = a.w;
@@ -357,20 +289,19 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
                         }
                     } else {
 #pragma unroll
-                        for (int g = 0; g < 4; ++g)
+                        for (int g = 0; g < G; ++g)
 #pragma unroll
                             for (int q = 0; q < 8; ++q)
                                 vals[g][q] = (kof(kb, q) < K) ? __ldg(rp[g] + 32 * q + lane) : 0.f;
                     }
 #pragma unroll
-                    for (int g = 0; g < 4; ++g)
+                    for (int g = 0; g < G; ++g)
 #pragma unroll
                         for (int q = 0; q < 8; ++q) acc[g][q] += vals[g][q];
                 }
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
+                for (int g = 0; g < G; ++g) {
                     const int l = l0 + g;
-                    if (l >= live) break;
                     const float sl = (float)ps[l];
                     float vv[8];
 #pragma unroll
@@ -402,6 +333,14 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
                         }
                     }
                 }
+            };
+            int l0 = 0;
+            for (; l0 + 4 <= live; l0 += 4) group(std::integral_constant<int, 4>{}, l0);
+            switch (live - l0) {
+                case 3: group(std::integral_constant<int, 3>{}, l0); break;
+                case 2: group(std::integral_constant<int, 2>{}, l0); break;
+                case 1: group(std::integral_constant<int, 1>{}, l0); break;
+                default: break;
             }
         }
         __syncwarp();
@@ -551,8 +490,8 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
 
         // ---- next beam in flat (lexicographic) order
         const int nxt = cur ^ 1;
-        int32_t* nc = S.codes[nxt];
-        double* ns = S.score[nxt];
+        int32_t* nc = S.codes + nxt * cap * M;
+        double* ns = S.score + nxt * cap;
         for (int b = 0; b < width; b += 32) {
             int i = b + lane;
             if (i < width) {
@@ -573,7 +512,7 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
     double bv = __longlong_as_double(0x7ff0000000000000ULL);
     int bi = 0x7fffffff;
     for (int i = lane; i < live; i += 32) {
-        double s = S.score[cur][i];
+        double s = S.score[cur * cap + i];
         if (lex_less(s, i, bv, bi)) { bv = s; bi = i; }
     }
     for (int off = 16; off >= 1; off >>= 1) {
@@ -581,7 +520,7 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
         int oi = __shfl_xor_sync(FULL, bi, off);
         if (lex_less(ov, oi, bv, bi)) { bv = ov; bi = oi; }
     }
-    const int32_t* best = S.codes[cur] + (long long)bi * M;
+    const int32_t* best = S.codes + cur * cap * M + (long long)bi * M;
     for (int j = lane; j < M; j += 32) {
         int c = best[j];
         if (code_bytes == 1) ((uint8_t*)codes_out)[v * ldcodes + j] = (uint8_t)c;
@@ -660,10 +599,10 @@ int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int
             sgemm_table_kernel<<<grid, SG_T, 0, s>>>((const float*)X + c0 * ldx, cn, ldx, cw, N, D, sq32, tab, N);
             DA_CHECK_LAUNCH("sgemm_table_kernel");
         }
-        ProfScope ps2("encode_beam_fast", s);
-        const unsigned grid = (unsigned)((cn + warps - 1) / warps);
         void* cout = (char*)codes_out + (size_t)c0 * ldcodes * code_bytes;
         double* eout = err_out ? err_out + c0 : nullptr;
+        ProfScope ps2("encode_beam_fast", s);
+        const unsigned grid = (unsigned)((cn + warps - 1) / warps);
         beam_fast_kernel<float><<<grid, warps * 32, smem, s>>>((const float*)X + c0 * ldx, cn, ldx, D, cw, M, K, L,
                                                                cap, tab, sq, P, P32, cmax, pabs, cw64, cout, code_bytes,
                                                                ldcodes, eout, stats, tab_tc);
