@@ -177,6 +177,13 @@ int da_knn(const void* base, int base_f32, int64_t n, int64_t ldb, int D, const 
 int da_adc_pack(const void* codes, int code_bytes, int64_t n, int64_t ldc, const double* pair, int M,
                 void* records, void* stream);
 
+/* Unpack n raw texmex records (4-byte dimension header + d values; kind 0 =
+ * fvecs float32, kind 1 = bvecs uint8), uploaded as they lie in the file, into
+ * (n, d) float32 rows (leading dim ldo).  Non-finite fvecs values add to *bad.
+ * replaces the payload decoding of read_fvecs / read_bvecs  data.py:94-127 */
+int da_unpack_vecs(const void* raw, int64_t n, int d, int kind, float* out, int64_t ldo, unsigned long long* bad,
+                   void* stream);
+
 /* da_adc_scan over packed records (same results, same tie rule).
  * replaces exhaustive_adc_search / A-Tree candidate re-ranking  codebook.py:399-429 */
 int da_adc_scan_packed(const void* records, const int64_t* cand, int64_t ncand, int64_t nq, const double* lut,

@@ -34,6 +34,7 @@ from .codebook import (
     Codebook,
     CrossProductTable,
     EncodedDataset,
+    EncodedWriter,
     adc_distance,
     adc_rerank,
     adc_table,
@@ -55,6 +56,7 @@ from .codebook import (
 )
 from .atree import ATree, SearchParams, SearchStats, atree_search, atree_search_batch, build_atree, node_distance
 from .groundtruth import GroundTruth, brute_force_knn
+from .data import VecsFile, encode_vecs, read_bvecs, read_fvecs, read_ivecs, write_fvecs, write_ivecs
 from .validation import FormatError
 
 __version__ = "0.1.0"

@@ -441,24 +441,24 @@ def encode(X: torch.Tensor, cw: torch.Tensor, sq: torch.Tensor, Pt: torch.Tensor
 _PINNED: list = []
 
 
-def _pinned_slots(nslot: int, elems: int) -> list:
-    """Reusable page-locked float32 staging buffers (allocation is slow; keep them)."""
+def _pinned_slots(nslot: int, nbytes: int) -> list:
+    """Reusable page-locked byte staging buffers (allocation is slow; keep them)."""
     global _PINNED
-    if len(_PINNED) < nslot or _PINNED[0].numel() < elems:
-        _PINNED = [torch.empty(max(elems, _PINNED[0].numel() if _PINNED else 0), dtype=torch.float32,
-                               pin_memory=True) for _ in range(nslot)]
+    if len(_PINNED) < nslot or _PINNED[0].numel() < nbytes:
+        size = max(nbytes, _PINNED[0].numel() if _PINNED else 0)
+        _PINNED = [torch.empty(size, dtype=torch.uint8, pin_memory=True) for _ in range(nslot)]
     return _PINNED[:nslot]
 
 
-def encode_host(X_np: np.ndarray, cw: torch.Tensor, sq: torch.Tensor, Pt: torch.Tensor, L: int,
-                out_dtype=I32, chunk: int = 131072, name: str = "data") -> torch.Tensor:
-    """Beam-encode a host float32 array, streamed: a worker thread copies row chunks
-    into pinned slots while the device uploads the previous chunk (copy stream) and
-    encodes the one before (compute stream).  Non-finite input raises ValueError
-    (checked on the device).  Returns the device codes (n, M)."""
+def _encode_stream(n: int, D: int, row_bytes: int, fill, to_rows, cw: torch.Tensor, sq: torch.Tensor,
+                   Pt: torch.Tensor, L: int, out_dtype, chunk: int) -> torch.Tensor:
+    """Streamed beam encode of n host rows.  A worker thread runs fill(slot, r0, rows)
+    to copy the raw bytes of rows [r0, r0+rows) into a pinned byte slot; the copy
+    stream uploads a slot while the compute stream turns the previous upload into
+    float32 rows (to_rows(raw_dev, rows, out_f32)) and encodes them.  Three pinned
+    slots, two device buffers.  Returns the device codes (n, M)."""
     import threading
 
-    n, D = X_np.shape
     M = cw.shape[0]
     dev = device()
     codes = torch.empty((n, M), dtype=out_dtype, device=dev)
@@ -466,9 +466,9 @@ def encode_host(X_np: np.ndarray, cw: torch.Tensor, sq: torch.Tensor, Pt: torch.
         return codes
     chunk = max(1, min(chunk, n))
     nslot = 3
-    pinned = _pinned_slots(nslot, chunk * D)
-    pinned = [p_[: chunk * D].view(chunk, D) for p_ in pinned]
-    dbuf = [torch.empty((chunk, D), dtype=torch.float32, device=dev) for _ in range(2)]
+    pinned = [p_[: chunk * row_bytes] for p_ in _pinned_slots(nslot, chunk * row_bytes)]
+    draw = [torch.empty(chunk * row_bytes, dtype=torch.uint8, device=dev) for _ in range(2)]
+    drows = [torch.empty((chunk, D), dtype=torch.float32, device=dev) for _ in range(2)]
     starts = list(range(0, n, chunk))
     filled = [threading.Semaphore(0) for _ in range(nslot)]
     free = [threading.Semaphore(1) for _ in range(nslot)]
@@ -479,8 +479,7 @@ def encode_host(X_np: np.ndarray, cw: torch.Tensor, sq: torch.Tensor, Pt: torch.
             for i, r0 in enumerate(starts):
                 s = i % nslot
                 free[s].acquire()
-                rows = min(chunk, n - r0)
-                np.copyto(pinned[s][:rows].numpy(), X_np[r0:r0 + rows])
+                fill(pinned[s], r0, min(chunk, n - r0))
                 filled[s].release()
         except BaseException as e:  # surfaced on the caller's thread
             errors.append(e)
@@ -491,7 +490,6 @@ def encode_host(X_np: np.ndarray, cw: torch.Tensor, sq: torch.Tensor, Pt: torch.
     th.start()
     comp = torch.cuda.current_stream()
     cstream = torch.cuda.Stream()
-    ok = torch.ones((), dtype=torch.bool, device=dev)
     comp_done = [None, None]
     try:
         for i, r0 in enumerate(starts):
@@ -502,13 +500,12 @@ def encode_host(X_np: np.ndarray, cw: torch.Tensor, sq: torch.Tensor, Pt: torch.
                 raise errors[0]
             with torch.cuda.stream(cstream):
                 if comp_done[b] is not None:
-                    cstream.wait_event(comp_done[b])        # device buffer b is free again
-                dbuf[b][:rows].copy_(pinned[s][:rows], non_blocking=True)
+                    cstream.wait_event(comp_done[b])        # device buffers b are free again
+                draw[b][: rows * row_bytes].copy_(pinned[s][: rows * row_bytes], non_blocking=True)
                 up = torch.cuda.Event()
                 up.record(cstream)
             comp.wait_event(up)
-            x = dbuf[b][:rows]
-            ok &= torch.isfinite(x).all()
+            x = to_rows(draw[b][: rows * row_bytes], rows, drows[b])
             native.da_encode(P(x), 1, rows, x.stride(0), D, P(cw), M, cw.shape[1], int(L), P(sq), P(Pt),
                              P(codes[r0:]), code_bytes(codes), codes.stride(0), None, stream())
             ev = torch.cuda.Event()
@@ -520,9 +517,45 @@ def encode_host(X_np: np.ndarray, cw: torch.Tensor, sq: torch.Tensor, Pt: torch.
         th.join()
     if errors:
         raise errors[0]
-    if not bool(ok.item()):
+    return codes
+
+
+def encode_host(X_np: np.ndarray, cw: torch.Tensor, sq: torch.Tensor, Pt: torch.Tensor, L: int,
+                out_dtype=I32, chunk: int = 131072, name: str = "data") -> torch.Tensor:
+    """Beam-encode a host float32 array through _encode_stream.  Non-finite input
+    raises ValueError (checked on the device).  Returns the device codes (n, M)."""
+    n, D = X_np.shape
+    ok = torch.ones((), dtype=torch.bool, device=device())
+
+    def fill(slot, r0, rows):
+        np.copyto(slot[: rows * D * 4].view(torch.float32).numpy().reshape(rows, D), X_np[r0:r0 + rows])
+
+    def to_rows(raw, rows, buf):
+        x = raw.view(torch.float32).view(rows, D)
+        ok.logical_and_(torch.isfinite(x).all())
+        return x
+
+    codes = _encode_stream(n, D, 4 * D, fill, to_rows, cw, sq, Pt, L, out_dtype, chunk)
+    if n and not bool(ok.item()):
         raise ValueError(f"{name} contains non-finite values")
     return codes
+
+
+def encode_records(fill, n: int, D: int, kind: int, cw: torch.Tensor, sq: torch.Tensor, Pt: torch.Tensor,
+                   L: int, out_dtype=I32, chunk: int = 1 << 18) -> tuple[torch.Tensor, int]:
+    """Beam-encode n texmex records (kind 0 = fvecs, 1 = bvecs) streamed as raw
+    file bytes: fill(slot, r0, rows) copies the records; the device unpacks them
+    (da_unpack_vecs).  Returns (device codes, count of non-finite payload values)."""
+    rec = 4 + D * (1 if kind else 4)
+    bad = torch.zeros(1, dtype=torch.int64, device=device())
+
+    def to_rows(raw, rows, buf):
+        x = buf[:rows]
+        native.da_unpack_vecs(P(raw), rows, D, kind, P(x), x.stride(0), P(bad), stream())
+        return x
+
+    codes = _encode_stream(n, D, rec, fill, to_rows, cw, sq, Pt, L, out_dtype, chunk)
+    return codes, int(bad.item())
 
 
 def assign_config(mode: int, counter: torch.Tensor | None = None) -> None:

@@ -42,6 +42,7 @@ _SIGNATURES = {
     "da_adc_lut": [_P, _L, _I, _P, _I, _I, _P, _P, _P, _P],
     "da_adc_scan": [_P, _I, _L, _P, _P, _L, _L, _P, _P, _I, _I, _I, _P, _P, _P],
     "da_adc_pack": [_P, _I, _L, _L, _P, _I, _P, _P],
+    "da_unpack_vecs": [_P, _L, _I, _I, _P, _L, _P, _P],
     "da_knn": [_P, _I, _L, _L, _I, _P, _P, _L, _P, _I, _P, _P, _P],
     "da_atree_search": [_P, _P, _L, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _L, _L, _L, _L, _P, _I,
                         _P, _P, _P, _P, _P],

@@ -18,6 +18,7 @@ Reference map (annq/codebook.py):
 from __future__ import annotations
 
 import hashlib
+import os
 import struct
 import weakref
 from dataclasses import dataclass
@@ -32,6 +33,7 @@ __all__ = [
     "Codebook",
     "CrossProductTable",
     "EncodedDataset",
+    "EncodedWriter",
     "AdcTable",
     "reconstruct",
     "distortion",
@@ -508,7 +510,79 @@ def write_encoded(path, encoded: EncodedDataset) -> None:
         f.write(np.ascontiguousarray(encoded.codes, dtype=f"<u{width}").tobytes())
 
 
-def read_encoded(path) -> EncodedDataset:
+_ENCODED_HEADER = 4 + struct.calcsize("<IQIIB")
+
+
+class EncodedWriter:
+    """HCLE file written chunk by chunk (same bytes as write_encoded of the whole
+    set): header first, then codes in row order.  For code sets that never sit
+    in host memory at once (1e9 rows = 8 GB of uint8 codes)."""
+
+    def __init__(self, path, n: int, m_count: int, k_count: int):
+        self.path, self.n, self.m_count, self.k_count = path, int(n), int(m_count), int(k_count)
+        self.width = 1 if k_count <= 256 else 2
+        self.rows = 0
+        self._f = open(path, "wb")
+        self._f.write(ENCODED_MAGIC)
+        self._f.write(struct.pack("<IQIIB", FORMAT_VERSION, self.n, self.m_count, self.k_count, self.width))
+
+    def write(self, codes) -> None:
+        codes = np.asarray(codes)
+        if codes.ndim != 2 or codes.shape[1] != self.m_count:
+            raise ValueError(f"codes chunk must be (rows, {self.m_count}), got {codes.shape}")
+        if self.rows + codes.shape[0] > self.n:
+            raise ValueError(f"{self.path}: more than the declared {self.n} rows")
+        self._f.write(np.ascontiguousarray(codes, dtype=f"<u{self.width}").tobytes())
+        self.rows += codes.shape[0]
+
+    def close(self) -> None:
+        if self._f is None:
+            return
+        self._f.close()
+        self._f = None
+        if self.rows != self.n:
+            raise ValueError(f"{self.path}: {self.rows} rows written, header declares {self.n}")
+
+    def abort(self) -> None:
+        if self._f is not None:
+            self._f.close()
+            self._f = None
+        os.remove(self.path)
+
+    def codes_map(self) -> np.ndarray:
+        """Read-only memory map of the written codes (n, M)."""
+        if self.n == 0:
+            return np.empty((0, self.m_count), dtype=f"<u{self.width}")
+        return np.memmap(self.path, dtype=f"<u{self.width}", mode="r", offset=_ENCODED_HEADER,
+                         shape=(self.n, self.m_count))
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, et, ev, tb):
+        if et is None:
+            self.close()
+        else:
+            self.abort()
+
+
+def read_encoded(path, mmap: bool = False) -> EncodedDataset:
+    """mmap=True maps the codes read-only instead of reading them (large sets)."""
+    if mmap:
+        with open(path, "rb") as f:
+            magic = f.read(4)
+            if magic != ENCODED_MAGIC:
+                raise FormatError(f"{path}: bad magic {magic!r}, expected {ENCODED_MAGIC!r}", exit_code=2)
+            version, n, M, K, width = struct.unpack("<IQIIB", _read_exact(f, 21, path, "header"))
+        if version != FORMAT_VERSION:
+            raise FormatError(f"{path}: unsupported format version {version}")
+        if width not in (1, 2):
+            raise FormatError(f"{path}: invalid code width {width}")
+        if os.path.getsize(path) < _ENCODED_HEADER + width * n * M:
+            raise FormatError(f"{path}: truncated while reading codes")
+        codes = (np.memmap(path, dtype=f"<u{width}", mode="r", offset=_ENCODED_HEADER, shape=(n, M)) if n * M
+                 else np.empty((n, M), dtype=f"<u{width}"))
+        return EncodedDataset(codes=codes, k_count=K)
     with open(path, "rb") as f:
         magic = f.read(4)
         if magic != ENCODED_MAGIC:

@@ -347,6 +347,13 @@ int da_adc_scan(const void* codes, int code_bytes, int64_t ldc, const double* pa
                            (long long*)ids, dists, STREAM(stream));
 }
 
+int da_unpack_vecs(const void* raw, int64_t n, int d, int kind, float* out, int64_t ldo, unsigned long long* bad,
+                   void* stream) {
+    if (n < 0 || d < 1 || (kind != 0 && kind != 1) || ldo < d)
+        return fail_arg("unpack_vecs: bad arguments n=%lld d=%d kind=%d", (long long)n, d, kind);
+    return launch_unpack_vecs(raw, n, d, kind, out, ldo, bad, STREAM(stream));
+}
+
 int da_adc_pack(const void* codes, int code_bytes, int64_t n, int64_t ldc, const double* pair, int M,
                 void* records, void* stream) {
     if (code_bytes != 1 || M < 1 || M > 8) return fail_arg("adc_pack: needs one-byte codes and M <= 8 (M=%d)", M);

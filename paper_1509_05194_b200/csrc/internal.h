@@ -70,6 +70,8 @@ int launch_atree_search(const double* lut, const double* qsq, long long nq, int 
                         double* d_out, long long* cnt_out, long long* stats_out, cudaStream_t s);
 int launch_topr_rows(const double* d2, long long rows, long long n, int r, long long* ids_out, double* d_out,
                      cudaStream_t s);
+int launch_unpack_vecs(const void* raw, long long n, int d, int kind, float* out, long long ldo,
+                       unsigned long long* bad, cudaStream_t s);
 int launch_adc_pack(const void* codes, long long n, long long ldc, const double* pair, int M, void* records,
                     cudaStream_t s);
 int launch_adc_scan_packed(const void* records, const long long* cand, long long ncand, long long nq,

@@ -318,6 +318,45 @@ __global__ void adc_scan_kernel(const TC* __restrict__ codes, long long ldc, con
     }
 }
 
+// texmex record streams (data.py:50-142): rows of a 4-byte dimension header then
+// d payload values (kind 0 = fvecs: float32, kind 1 = bvecs: uint8).  The raw
+// records of a chunk are uploaded as they lie in the file and unpacked here into
+// (n, d) float32 rows (bytes widen exactly); non-finite fvecs values are counted
+// into *bad (the caller raises).  One thread per 4 payload values.
+__global__ void unpack_vecs_kernel(const uint8_t* __restrict__ raw, long long n, int d, int kind,
+                                   float* __restrict__ out, long long ldo, unsigned long long* __restrict__ bad) {
+    const long long rec = 4 + (long long)d * (kind ? 1 : 4);
+    const int qpr = (d + 3) / 4;  // quads per row
+    unsigned nbad = 0;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n * qpr;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long i = t / qpr;
+        const int j0 = (int)(t - i * qpr) * 4;
+        const uint8_t* r = raw + i * rec + 4;
+        float* o = out + i * ldo;
+        if (kind) {
+            for (int j = j0; j < min(d, j0 + 4); ++j) o[j] = (float)r[j];
+        } else {
+            const float* rf = reinterpret_cast<const float*>(r);
+            for (int j = j0; j < min(d, j0 + 4); ++j) {
+                const float v = __ldg(rf + j);
+                nbad += isfinite(v) ? 0u : 1u;
+                o[j] = v;
+            }
+        }
+    }
+    if (bad && nbad) atomicAdd(bad, (unsigned long long)nbad);
+}
+
+int launch_unpack_vecs(const void* raw, long long n, int d, int kind, float* out, long long ldo,
+                       unsigned long long* bad, cudaStream_t s) {
+    if (n <= 0) return 0;
+    const long long work = n * ((d + 3) / 4);
+    unpack_vecs_kernel<<<grid_for(work, 256), 256, 0, s>>>((const uint8_t*)raw, n, d, kind, out, ldo, bad);
+    DA_CHECK_LAUNCH("unpack_vecs_kernel");
+    return 0;
+}
+
 // Packed candidate records (M <= 8 one-byte codes): record[row] = 16 bytes,
 // codes in bytes 0..7, the row's pair sum (float64) in bytes 8..15, so one
 // random candidate costs one 32-byte sector plus its 8-byte id.
