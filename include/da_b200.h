@@ -53,6 +53,17 @@ int da_assign(const void* X, int x_f32, int64_t n, int64_t ldx, int d, const dou
               const double* cc, const double* xx, int32_t* labels, double* d2, const int32_t* prev,
               unsigned long long* changed, void* stream);
 
+/* Bytes of the tf32 hi/lo row image da_assign_bind_image builds for (n, d). */
+int64_t da_assign_image_bytes(int64_t n, int d);
+
+/* Build the tf32 hi/lo image of the first d columns of X (n rows, leading dim
+ * ldx) into the caller's buffer `image` (da_assign_image_bytes) and bind it:
+ * every following da_assign on exactly (X, n, ldx, d) reads the image instead
+ * of re-splitting the rows.  X = NULL unbinds.  The caller keeps X and image
+ * unchanged while bound (one Lloyd call: the rotated rows are fixed).
+ * part of lloyd_kmeans' per-stage setup  clustering.py:165-203 */
+int da_assign_bind_image(const void* X, int x_f32, int64_t n, int64_t ldx, int d, float* image, void* stream);
+
 /* Assign selection: mode 0 (default) = tcgen05 3xTF32 distance tiles in TMEM +
  * rigorous bound + exact float64 recheck (K <= 256; same labels/d2 as mode 1);
  * mode 1 = plain float64 FMA kernel.  candidate_counter (device, optional)

@@ -20,7 +20,7 @@ import ctypes
 import numpy as np
 import torch
 
-from ._native import native
+from ._native import load_library as native_lib, native
 
 F32, F64, I32, I64 = torch.float32, torch.float64, torch.int32, torch.int64
 
@@ -122,6 +122,32 @@ def assign(X: torch.Tensor, d: int, C: torch.Tensor, cc: torch.Tensor | None = N
     return labels, d2
 
 
+class assign_image:
+    """Context manager binding the tf32 row image of X[:, :d] for the assigns of
+    one Lloyd call (da_assign_bind_image); the buffer is reused across calls."""
+
+    _buf = None
+
+    def __init__(self, X: torch.Tensor, d: int):
+        self.X, self.d = X, d
+
+    def __enter__(self):
+        n = self.X.shape[0]
+        nbytes = int(native_lib().da_assign_image_bytes(n, self.d)) if n else 0
+        if nbytes:
+            buf = assign_image._buf
+            if buf is None or buf.numel() < nbytes or buf.device != self.X.device:
+                assign_image._buf = buf = None
+                buf = torch.empty(nbytes, dtype=torch.uint8, device=self.X.device)
+                assign_image._buf = buf
+            native.da_assign_bind_image(P(self.X), is_f32(self.X), n, self.X.stride(0), self.d, P(buf), stream())
+        return self
+
+    def __exit__(self, *exc):
+        native.da_assign_bind_image(None, 0, 0, 0, 0, None, stream())
+        return False
+
+
 # ---------------------------------------------------------------------------
 # Lloyd k-means with an active prefix (annq/clustering.py:165-203)
 
@@ -175,6 +201,11 @@ def _sharded_update(sums, counts, C, comm):
 
 def lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, comm=None):
     """Returns (C f64 (K,D), labels int32 (n,), trace list[float])."""
+    with assign_image(Xr, active):
+        return _lloyd(Xr, C_init, active, max_iters, comm)
+
+
+def _lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, comm=None):
     n, D = Xr.shape
     K = C_init.shape[0]
     C = C_init.clone().contiguous()

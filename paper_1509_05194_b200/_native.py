@@ -52,13 +52,14 @@ _SIGNATURES = {
     "da_set_column": [_P, _L, _I, _I, _P, _P],
     "da_encode_config": [_I, _P],
     "da_assign_config": [_I, _P],
+    "da_assign_bind_image": [_P, _I, _L, _L, _I, _P, _P],
     "da_release_scratch": [],
     "da_prof_enable": [_I],
     "da_prof_collect": [ctypes.c_char_p, _I],
     "da_version": [],
 }
 
-EXPORTED = tuple(_SIGNATURES) + ("da_last_error", "da_launch_count")
+EXPORTED = tuple(_SIGNATURES) + ("da_last_error", "da_launch_count", "da_assign_image_bytes")
 
 
 def launch_count() -> int:
@@ -100,6 +101,8 @@ def load_library(path: str = LIB_PATH):
             fn.restype = ctypes.c_int
         lib.da_launch_count.argtypes = []
         lib.da_launch_count.restype = ctypes.c_longlong
+        lib.da_assign_image_bytes.argtypes = [_L, _I]
+        lib.da_assign_image_bytes.restype = ctypes.c_int64
         lib.da_last_error.argtypes = []
         lib.da_last_error.restype = ctypes.c_char_p
         _lib = lib

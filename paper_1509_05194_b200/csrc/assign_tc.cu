@@ -10,9 +10,10 @@
 //   3. those candidates are recomputed in float64 exactly like the reference
 //      ((||x||^2 - 2 x.c) + ||c||^2 with BLAS-ordered FMA dot, clip at 0) and the
 //      lexicographic (d2, k) minimum is written.
-// Operands are staged to shared memory by the CTA's threads (f64 -> tf32 hi/lo
-// split) in the canonical K-major no-swizzle UMMA layout; one elected thread
-// issues the MMAs and commits them to an mbarrier.
+// Both operands are pre-split f64 -> tf32 hi/lo into the canonical K-major
+// no-swizzle UMMA layout (x_tf32_prep_kernel, cw_tf32_prep_kernel) and fetched
+// with bulk copies by a producer warp, which also issues the MMAs; the exact
+// rechecks run in a separate kernel with coalesced row staging.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -27,7 +28,6 @@ namespace {
 constexpr int TC_M = 128;     // rows per CTA (= TMEM lanes)
 constexpr int TC_NMAX = 256;  // codewords per MMA (TMEM columns)
 constexpr int TC_BK = 32;     // tf32 elements of K staged per round (4 MMA k-steps)
-constexpr int TC_THREADS = 128;
 constexpr int TC_CMAX = 8;    // candidates kept per row before falling back to a full exact scan
 }  // namespace
 
@@ -217,14 +217,55 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  : "memory");
 }
 
-// Persistent, software-pipelined kernel: one CTA (8 warps) per SM walks row
-// tiles.  Per (tile, k-chunk) step the warps stage 16 rows each as tf32 hi/lo
-// (coalesced 256-B row segments) while a bulk copy brings the matching codeword
-// chunk (kept resident when d <= 32), and thread 0 issues 3 x (<= 4)
-// tcgen05.mma into one of two TMEM accumulators (2 x 256 columns).  The epilogue
-// of tile i-1 (two threads per row, one per half of the codewords) runs while
-// the tensor cores work on tile i.
-constexpr int TC_T2 = 256;
+// Rows (n x d, float32 or float64) -> per-(tile, chunk) tf32 hi/lo images in the
+// exact shared-memory layout the MMA reads (128 rows x 32 k, zero padded), so the
+// assign kernel fetches each chunk with one bulk copy.  Built once per Lloyd call
+// (the rotated rows do not change between iterations) or per unbound assign.
+template <typename TX>
+__global__ void x_tf32_prep_kernel(const TX* __restrict__ X, long long n, long long ldx, int d, int nch,
+                                   float* __restrict__ out) {
+    // one thread per (row, 4-k group); consecutive threads take the 8 rows of one
+    // core matrix, so each group of 8 writes 128 contiguous bytes per image and
+    // reads 8 full 32-B row segments
+    constexpr int A_ELEMS = TC_M * TC_BK, KG = TC_BK / 4;
+    const long long ntiles = (n + TC_M - 1) / TC_M;
+    const long long total = ntiles * nch * (A_ELEMS / 4);
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        const long long blk = e / (A_ELEMS / 4);       // (tile, chunk)
+        const int rem = (int)(e - blk * (A_ELEMS / 4));
+        const int rl = rem & 7, kg = (rem >> 3) % KG, r8 = (rem >> 3) / KG;
+        const int r = r8 * 8 + rl;
+        const long long tile = blk / nch;
+        const int ch = (int)(blk - tile * nch);
+        const long long gr = tile * TC_M + r;
+        const int gk0 = ch * TC_BK + kg * 4;
+        float h[4], l[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            h[u] = 0.f;
+            l[u] = 0.f;
+            if (gr < n && gk0 + u < d) {
+                const double v = (double)X[gr * ldx + gk0 + u];
+                h[u] = to_tf32((float)v);
+                l[u] = to_tf32((float)(v - (double)h[u]));
+            }
+        }
+        float* base = out + blk * 2 * A_ELEMS;
+        const uint32_t o = kmajor_off(r, kg * 4) >> 2;
+        *reinterpret_cast<float4*>(base + o) = make_float4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<float4*>(base + A_ELEMS + o) = make_float4(l[0], l[1], l[2], l[3]);
+    }
+}
+
+// Persistent warp-specialised kernel: one CTA per SM walks 128-row tiles.
+// Warp 8 (one lane) is the producer: per (tile, 32-k chunk) it bulk-copies the
+// row image and the codeword image (kept resident when d <= 32) into a 2-stage
+// ring and issues 3 x (<= 4) tcgen05.mma into one of two TMEM accumulators.
+// Warps 0-7 run the epilogue of each finished tile (two threads per row, one
+// per half of the codewords): window, candidate list to global memory.  The
+// exact float64 rechecks follow in assign_recheck_kernel.
+constexpr int TC_T2 = 256;        // epilogue threads
+constexpr int TC_TP = TC_T2 + 32; // + producer warp
 
 __device__ unsigned long long g_at_prof[8];
 #define AT_MARK(i)                                                   \
@@ -236,13 +277,17 @@ __device__ unsigned long long g_at_prof[8];
         }                                                            \
     } while (0)
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 2, 256;" ::: "memory"); }
+
 template <typename TX>
-__global__ void __launch_bounds__(TC_T2, 1) assign_tc_kernel(
-    const TX* __restrict__ X, long long n, long long ldx, int d, const double* __restrict__ C, long long ldc, int K,
-    const double* __restrict__ cc, const double* __restrict__ xx_in, const float* __restrict__ Bg,
-    int32_t* __restrict__ labels, double* __restrict__ d2_out, const int32_t* __restrict__ prev,
-    unsigned long long* __restrict__ changed, unsigned long long* __restrict__ stats,
-    int* __restrict__ ovf_rows, int* __restrict__ ovf_cnt) {
+__global__ void __launch_bounds__(TC_TP, 1) assign_tc_kernel(
+    const TX* __restrict__ X, long long n, long long ldx, int d, int K, const double* __restrict__ cc,
+    const double* __restrict__ xx_in, const float* __restrict__ Ag, const float* __restrict__ Bg,
+    unsigned long long* __restrict__ stats, int* __restrict__ ovf_rows, int* __restrict__ ovf_cnt,
+    uint8_t* __restrict__ gcand, uint8_t* __restrict__ gcnt) {
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int A_ELEMS = TC_M * TC_BK, B_ELEMS = TC_NMAX * TC_BK;
     float* Abuf = reinterpret_cast<float*>(smem);                    // [2 stages][hi, lo][A_ELEMS]
@@ -252,7 +297,7 @@ __global__ void __launch_bounds__(TC_T2, 1) assign_tc_kernel(
     double* wmin_h = reinterpret_cast<double*>(ccf + TC_NMAX);        // [2][TC_M]
     int* cand = reinterpret_cast<int*>(wmin_h + 2 * TC_M);            // [2][TC_M][TC_CMAX]
     int* ncand = cand + 2 * TC_M * TC_CMAX;                           // [2][TC_M]
-    __shared__ uint64_t full_bar[2], empty_bar[2], acc_bar[2];
+    __shared__ uint64_t full_bar[2], empty_bar[2], acc_full[2], acc_empty[2], b_bar;
     __shared__ uint32_t tmem_base_sh;
     __shared__ double red[8];
 
@@ -272,210 +317,167 @@ __global__ void __launch_bounds__(TC_T2, 1) assign_tc_kernel(
         for (int i = 0; i < 2; ++i) {
             mbar_init(&full_bar[i], 1);
             mbar_init(&empty_bar[i], 1);
-            mbar_init(&acc_bar[i], 1);
+            mbar_init(&acc_full[i], 1);
+            mbar_init(&acc_empty[i], 1);
         }
+        mbar_init(&b_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     double cm = 0.0;
-    for (int k = tid; k < TC_NMAX; k += TC_T2) {
-        const double v = k < K ? cc[k] : 0.0;
-        ccs[k] = v;
-        ccf[k] = k < K ? (float)v : __int_as_float(0x7f800000);
-        cm = fmax(cm, v);
+    if (tid < TC_T2) {
+        for (int k = tid; k < TC_NMAX; k += TC_T2) {
+            const double v = k < K ? cc[k] : 0.0;
+            ccs[k] = v;
+            ccf[k] = k < K ? (float)v : __int_as_float(0x7f800000);
+            cm = fmax(cm, v);
+        }
+        for (int off = 16; off >= 1; off >>= 1) cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, off));
+        if (lane == 0) red[warp] = cm;
     }
-    for (int off = 16; off >= 1; off >>= 1) cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, off));
-    if (lane == 0) red[warp] = cm;
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tmem_base_sh;
-    double ccmax = 0.0;
-    for (int w = 0; w < 8; ++w) ccmax = fmax(ccmax, red[w]);
-    const double sc = sqrt(ccmax);
-    const uint32_t idesc = make_idesc_tf32(TC_M, N);
-    const double u22 = 2.384185791015625e-07;  // 2^-22
-    const bool blk = d > (int)BLAS_Q;
-    if (b_resident && tid == 0) {  // the whole (single-chunk) codebook once
-        mbar_arrive_expect_tx(&full_bar[0], (uint32_t)(2 * B_ELEMS * sizeof(float)));
-        bulk_g2s(Bbuf, Bg, (uint32_t)(2 * B_ELEMS * sizeof(float)), &full_bar[0]);
-    }
 
-    long long at_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // phase clocks (thread 0, DA_DEBUG)
-    long long at_t = clock64();
-    const int erow = tid & (TC_M - 1);   // TMEM lane / tile row owned in the epilogue
-    const int ehalf = tid >> 7;          // 0: codewords [0,128), 1: [128,256)
-    auto epilogue = [&](long long tile, int accb) {
-        const long long r = tile * TC_M + erow;
-        const bool valid = r < n;
-        const TX* xr = X + (valid ? r : 0) * ldx;
-        double xx = 0.0;
-        if (valid) {
-            if (xx_in) xx = xx_in[r];
-            else xx = np_pw_sum([&](long long i) { double t = (double)xr[i]; return dmul(t, t); }, 0, d);
-        }
-        const double sx = sqrt(xx);
-        // bound on |w' - (cc - 2 x.c)| for w' = fmaf(-2, dot', (float)cc): 3xTF32 + fp32
-        // accumulation of the dot, fp32 rounding of cc and of the fma, float64
-        // rounding of the window arithmetic
-        const double E = 2.0 * (4.0 * d + 16.0) * u22 * sx * sc * (1.0 + 1e-9) +
-                         2.384185791015625e-07 * (ccmax + 2.0 * sx * sc) +
-                         8.8817841970012523e-16 * (xx + ccmax + 2.0 * sx * sc) + 1e-300;
-        const int cbeg = ehalf * 128, cend = min(N, cbeg + 128);
-        const uint32_t taddr = tmem + (uint32_t)(accb * TC_NMAX) + ((uint32_t)((warp & 3) * 32) << 16);
-        float v[32];
-        float wminf = __int_as_float(0x7f800000);
-        for (int c0 = cbeg; c0 < cend; c0 += 32) {
-            tmem_ld32(taddr + c0, v);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) wminf = fminf(wminf, fmaf(-2.f, v[i], ccf[c0 + i]));
-        }
-        wmin_h[ehalf * TC_M + erow] = (double)wminf;
-        __syncthreads();
-        AT_MARK(3);
-        const double wmin = fmin(wmin_h[erow], wmin_h[TC_M + erow]);
-        const double ub = fmax(xx + wmin + E, 0.0);
-        // candidate k iff max(xx + w'_k - E, 0) <= ub  <=>  w'_k <= ub - xx + E (ub >= 0)
-        const double tlim = ub - xx + E;
-        const float tf = (tlim >= 3.0e38) ? __int_as_float(0x7f800000)
-                                          : __fadd_ru((float)tlim, fabsf((float)tlim) * 1e-6f + 1e-30f);
-        int nc = 0;
-        int* my = cand + (ehalf * TC_M + erow) * TC_CMAX;
-        for (int c0 = cbeg; c0 < cend; c0 += 32) {
-            tmem_ld32(taddr + c0, v);
-            uint32_t hit = 0;  // branch-free test, then walk the (rare) set bits
-#pragma unroll
-            for (int i = 0; i < 32; ++i) hit |= (uint32_t)(fmaf(-2.f, v[i], ccf[c0 + i]) <= tf) << i;
-            while (hit) {
-                const int i = __ffs(hit) - 1;
-                hit &= hit - 1;
-                if (nc < TC_CMAX) my[nc] = c0 + i;
-                ++nc;
+    if (warp == 8) {
+        // ---------------- producer: bulk copies + MMA issue (one lane)
+        if (lane == 0) {
+            const uint32_t idesc = make_idesc_tf32(TC_M, N);
+            if (b_resident) {
+                mbar_arrive_expect_tx(&b_bar, (uint32_t)(2 * B_ELEMS * sizeof(float)));
+                bulk_g2s(Bbuf, Bg, (uint32_t)(2 * B_ELEMS * sizeof(float)), &b_bar);
+                mbar_wait(&b_bar, 0);
             }
-        }
-        ncand[ehalf * TC_M + erow] = nc;
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncthreads();
-        AT_MARK(4);
-        if (ehalf != 0 || !valid) return;
-        double best = __longlong_as_double(0x7ff0000000000000ULL);
-        int bk = 0x7fffffff;
-        auto consider = [&](int k) {
-            const double* crow = C + (long long)k * ldc;
-            const double xc = blk ? exact_xc<TX, true>(xr, crow, d) : exact_xc<TX, false>(xr, crow, d);
-            double dv = dadd(dsub(xx, dmul(2.0, xc)), ccs[k]);
-            if (dv < 0.0) dv = 0.0;
-            if (lex_less(dv, k, best, bk)) { best = dv; bk = k; }
-        };
-        const int n0 = ncand[erow], n1 = ncand[TC_M + erow];
-        const bool overflow = n0 > TC_CMAX || n1 > TC_CMAX;
-        if (overflow) {
-            // too many near-ties for this thread: a warp-parallel exact scan over all K
-            // runs after the kernel (assign_overflow_kernel) instead of stalling the CTA
-            ovf_rows[atomicAdd(ovf_cnt, 1)] = (int)r;
-            if (stats) atomicAdd(stats, (unsigned long long)K);
-            return;
-        }
-        for (int i = 0; i < n0; ++i) consider(cand[erow * TC_CMAX + i]);
-        for (int i = 0; i < n1; ++i) consider(cand[(TC_M + erow) * TC_CMAX + i]);
-        labels[r] = bk;
-        d2_out[r] = best;
-        if (stats) atomicAdd(stats, (unsigned long long)(n0 + n1));
-        if (changed != nullptr && prev != nullptr && prev[r] != bk) atomicAdd(changed, 1ULL);
-    };
-
-    // Warp roles: warps 4-7 stage the row tiles and issue the MMAs (thread 128);
-    // warps 0-3 do the exact rechecks of the previous tile meanwhile.  Both halves
-    // run the two epilogue passes together.
-    const bool stager = warp >= 4;
-    long long q = 0;  // (tile, chunk) steps issued by this CTA
-    long long it = 0; // tiles issued by this CTA
-    long long prev_tile = -1;
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int accb = (int)(it & 1);
-        const long long row0 = tile * TC_M;
-        if (!stager) {
-            q += nch;
-        } else {
-        for (int ch = 0; ch < nch; ++ch, ++q) {
-            const int st = (int)(q & 1);
-            if (q >= 2) mbar_wait(&empty_bar[st], (uint32_t)(((q >> 1) - 1) & 1));
-            float* Ah = Abuf + st * 2 * A_ELEMS;
-            float* Al = Ah + A_ELEMS;
-            float* Bs = b_resident ? Bbuf : Bbuf + st * 2 * B_ELEMS;
-            if (!b_resident && tid == 128) {
-                mbar_arrive_expect_tx(&full_bar[st], (uint32_t)(2 * B_ELEMS * sizeof(float)));
-                bulk_g2s(Bs, Bg + (size_t)ch * 2 * B_ELEMS, (uint32_t)(2 * B_ELEMS * sizeof(float)), &full_bar[st]);
-            }
-            // stage 32 rows per warp as 8x4 blocks: lane -> (row 8-group row L/4,
-            // k = 4-group + L%4).  Each block is one 8x16-B core matrix in shared
-            // memory (all 32 banks once) and 8 full 32-B sectors in global memory.
-            const int k0 = ch * TC_BK;
-            const int w4 = warp - 4;
-#pragma unroll
-            for (int half2 = 0; half2 < 2; ++half2) {
-                double xv[16];
-#pragma unroll
-                for (int it2 = 0; it2 < 16; ++it2) {
-                    const int rg = 2 * half2 + (it2 >> 3), kg = it2 & 7;
-                    const int rr = w4 * 32 + rg * 8 + (lane >> 2);
-                    const int gk = k0 + kg * 4 + (lane & 3);
-                    const long long r = row0 + rr;
-                    xv[it2] = (r < n && gk < d) ? (double)X[r * ldx + gk] : 0.0;
-                }
-#pragma unroll
-                for (int it2 = 0; it2 < 16; ++it2) {
-                    const int rg = 2 * half2 + (it2 >> 3), kg = it2 & 7;
-                    const int rr = w4 * 32 + rg * 8 + (lane >> 2);
-                    const float h = to_tf32((float)xv[it2]);
-                    const float l = to_tf32((float)(xv[it2] - (double)h));
-                    const uint32_t o = kmajor_off(rr, kg * 4 + (lane & 3)) >> 2;
-                    Ah[o] = h;
-                    Al[o] = l;
+            long long q = 0, it = 0;
+            for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+                const int accb = (int)(it & 1);
+                if (it >= 2) mbar_wait(&acc_empty[accb], (uint32_t)(((it - 2) >> 1) & 1));
+                for (int ch = 0; ch < nch; ++ch, ++q) {
+                    const int st = (int)(q & 1);
+                    if (q >= 2) mbar_wait(&empty_bar[st], (uint32_t)(((q >> 1) - 1) & 1));
+                    float* Ah = Abuf + st * 2 * A_ELEMS;
+                    float* Bs = b_resident ? Bbuf : Bbuf + st * 2 * B_ELEMS;
+                    const uint32_t abytes = (uint32_t)(2 * A_ELEMS * sizeof(float));
+                    const uint32_t bbytes = b_resident ? 0u : (uint32_t)(2 * B_ELEMS * sizeof(float));
+                    mbar_arrive_expect_tx(&full_bar[st], abytes + bbytes);
+                    bulk_g2s(Ah, Ag + ((size_t)tile * nch + ch) * 2 * A_ELEMS, abytes, &full_bar[st]);
+                    if (!b_resident) bulk_g2s(Bs, Bg + (size_t)ch * 2 * B_ELEMS, bbytes, &full_bar[st]);
+                    mbar_wait(&full_bar[st], (uint32_t)((q >> 1) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t sa_hi = smem_u32(Ah), sa_lo = smem_u32(Ah + A_ELEMS);
+                    const uint32_t sb_hi = smem_u32(Bs), sb_lo = smem_u32(Bs + B_ELEMS);
+                    const uint32_t dacc = tmem + (uint32_t)(accb * TC_NMAX);
+                    const int ks = min(TC_BK / 8, (d - ch * TC_BK + 7) / 8);
+                    for (int s2 = 0; s2 < ks; ++s2) {
+                        const uint32_t off = (uint32_t)s2 * 256;
+                        const uint32_t acc0 = (ch > 0 || s2 > 0) ? 1u : 0u;
+                        mma_tf32(dacc, make_desc(sa_hi + off), make_desc(sb_hi + off), idesc, acc0);
+                        mma_tf32(dacc, make_desc(sa_hi + off), make_desc(sb_lo + off), idesc, 1u);
+                        mma_tf32(dacc, make_desc(sa_lo + off), make_desc(sb_hi + off), idesc, 1u);
+                    }
+                    mma_commit(&empty_bar[st]);
+                    if (ch == nch - 1) mma_commit(&acc_full[accb]);
                 }
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            asm volatile("bar.sync 1, 128;" ::: "memory");   // the four staging warps
-            AT_MARK(0);
-            if (tid == 128) {
-                if (!b_resident) mbar_wait(&full_bar[st], (uint32_t)((q >> 1) & 1));
-                else if (q == 0) mbar_wait(&full_bar[0], 0);
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t sa_hi = smem_u32(Ah), sa_lo = smem_u32(Al);
-                const uint32_t sb_hi = smem_u32(Bs), sb_lo = smem_u32(Bs + B_ELEMS);
-                const uint32_t dacc = tmem + (uint32_t)(accb * TC_NMAX);
-                const int ks = min(TC_BK / 8, (d - k0 + 7) / 8);
-                for (int s2 = 0; s2 < ks; ++s2) {
-                    const uint32_t off = (uint32_t)s2 * 256;
-                    const uint32_t acc0 = (ch > 0 || s2 > 0) ? 1u : 0u;
-                    mma_tf32(dacc, make_desc(sa_hi + off), make_desc(sb_hi + off), idesc, acc0);
-                    mma_tf32(dacc, make_desc(sa_hi + off), make_desc(sb_lo + off), idesc, 1u);
-                    mma_tf32(dacc, make_desc(sa_lo + off), make_desc(sb_hi + off), idesc, 1u);
+        }
+        __syncwarp();
+    } else {
+        // ---------------- epilogue warps
+        double ccmax = 0.0;
+        for (int w = 0; w < 8; ++w) ccmax = fmax(ccmax, red[w]);
+        const double sc = sqrt(ccmax);
+        const double u22 = 2.384185791015625e-07;  // 2^-22
+        long long at_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // phase clocks (thread 0, DA_DEBUG)
+        long long at_t = clock64();
+        const int erow = tid & (TC_M - 1);   // TMEM lane / tile row owned in the epilogue
+        const int ehalf = tid >> 7;          // 0: codewords [0,128), 1: [128,256)
+        long long it = 0;
+        for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const int accb = (int)(it & 1);
+            const long long r = tile * TC_M + erow;
+            const bool valid = r < n;
+            double xx = 0.0;
+            if (valid) {
+                if (xx_in) xx = xx_in[r];
+                else {
+                    const TX* xr = X + r * ldx;
+                    xx = np_pw_sum([&](long long i) { double t = (double)xr[i]; return dmul(t, t); }, 0, d);
                 }
-                mma_commit(&empty_bar[st]);
-                if (ch == nch - 1) mma_commit(&acc_bar[accb]);
             }
-            __syncwarp();
-            AT_MARK(1);
-        }
-        }
-        if (prev_tile >= 0) {
-            const int pb = (int)((it - 1) & 1);
-            mbar_wait(&acc_bar[pb], (uint32_t)(((it - 1) >> 1) & 1));
-            AT_MARK(2);
+            const double sx = sqrt(xx);
+            // bound on |w' - (cc - 2 x.c)| for w' = fmaf(-2, dot', (float)cc): 3xTF32 + fp32
+            // accumulation of the dot, fp32 rounding of cc and of the fma, float64
+            // rounding of the window arithmetic
+            const double E = 2.0 * (4.0 * d + 16.0) * u22 * sx * sc * (1.0 + 1e-9) +
+                             2.384185791015625e-07 * (ccmax + 2.0 * sx * sc) +
+                             8.8817841970012523e-16 * (xx + ccmax + 2.0 * sx * sc) + 1e-300;
+            mbar_wait(&acc_full[accb], (uint32_t)((it >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
-            epilogue(prev_tile, pb);
+            AT_MARK(2);
+            const int cbeg = ehalf * 128, cend = min(N, cbeg + 128);
+            const uint32_t taddr = tmem + (uint32_t)(accb * TC_NMAX) + ((uint32_t)((warp & 3) * 32) << 16);
+            float v[32];
+            float wminf = __int_as_float(0x7f800000);
+            for (int c0 = cbeg; c0 < cend; c0 += 32) {
+                tmem_ld32(taddr + c0, v);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) wminf = fminf(wminf, fmaf(-2.f, v[i], ccf[c0 + i]));
+            }
+            wmin_h[ehalf * TC_M + erow] = (double)wminf;
+            epi_sync();
+            AT_MARK(3);
+            const double wmin = fmin(wmin_h[erow], wmin_h[TC_M + erow]);
+            const double ub = fmax(xx + wmin + E, 0.0);
+            // candidate k iff max(xx + w'_k - E, 0) <= ub  <=>  w'_k <= ub - xx + E (ub >= 0)
+            const double tlim = ub - xx + E;
+            const float tf = (tlim >= 3.0e38) ? __int_as_float(0x7f800000)
+                                              : __fadd_ru((float)tlim, fabsf((float)tlim) * 1e-6f + 1e-30f);
+            int nc = 0;
+            int* my = cand + (ehalf * TC_M + erow) * TC_CMAX;
+            for (int c0 = cbeg; c0 < cend; c0 += 32) {
+                tmem_ld32(taddr + c0, v);
+                uint32_t hit = 0;  // branch-free test, then walk the (rare) set bits
+#pragma unroll
+                for (int i = 0; i < 32; ++i) hit |= (uint32_t)(fmaf(-2.f, v[i], ccf[c0 + i]) <= tf) << i;
+                while (hit) {
+                    const int i = __ffs(hit) - 1;
+                    hit &= hit - 1;
+                    if (nc < TC_CMAX) my[nc] = c0 + i;
+                    ++nc;
+                }
+            }
+            ncand[ehalf * TC_M + erow] = nc;
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            epi_sync();
+            if (tid == 0) mbar_arrive(&acc_empty[accb]);   // TMEM buffer free for tile it + 2
+            AT_MARK(4);
+            if (ehalf == 0 && valid) {
+                // the row's candidates (both halves, ascending k) go to global memory; the
+                // exact float64 rechecks run in assign_recheck_kernel with coalesced rows
+                const int n0 = ncand[erow], n1 = ncand[TC_M + erow];
+                if (n0 + n1 > TC_CMAX) {
+                    // too many near-ties for this row: a warp-parallel exact scan over
+                    // all K runs after the kernel (assign_overflow_kernel)
+                    ovf_rows[atomicAdd(ovf_cnt, 1)] = (int)r;
+                    gcnt[r] = 0xFF;
+                    if (stats) atomicAdd(stats, (unsigned long long)K);
+                } else {
+                    uint32_t w2[2] = {0u, 0u};
+                    for (int i = 0; i < n0; ++i) w2[i >> 2] |= (uint32_t)cand[erow * TC_CMAX + i] << (8 * (i & 3));
+                    for (int i = 0; i < n1; ++i) {
+                        const int j = n0 + i;
+                        w2[j >> 2] |= (uint32_t)cand[(TC_M + erow) * TC_CMAX + i] << (8 * (j & 3));
+                    }
+                    *reinterpret_cast<uint2*>(gcand + r * 8) = make_uint2(w2[0], w2[1]);
+                    gcnt[r] = (uint8_t)(n0 + n1);
+                }
+            }
+            epi_sync();   // cand / ncand / wmin_h are rewritten by the next tile
             AT_MARK(5);
         }
-        prev_tile = tile;
+        if (tid == 0)
+            for (int i = 0; i < 8; ++i) atomicAdd(&g_at_prof[i], (unsigned long long)at_acc[i]);
     }
-    if (prev_tile >= 0) {
-        const int pb = (int)((it - 1) & 1);
-        mbar_wait(&acc_bar[pb], (uint32_t)(((it - 1) >> 1) & 1));
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        epilogue(prev_tile, pb);
-    }
-    if (tid == 0)
-        for (int i = 0; i < 8; ++i) atomicAdd(&g_at_prof[i], (unsigned long long)at_acc[i]);
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (warp == 0) {
@@ -524,6 +526,203 @@ __global__ void assign_overflow_kernel(const TX* __restrict__ X, long long ldx, 
     }
 }
 
+// Exact float64 rechecks of the tensor-core candidates.  One warp per 32
+// consecutive rows (lane = row).  The rows' x values and each round's candidate
+// codeword rows are staged through shared memory 32 columns at a time with
+// coalesced 256-B row reads, then every lane runs its own BLAS-ordered FMA chain
+// from a padded (conflict-free) row.  Same value per candidate as assign.cu:
+// ((xx - 2 x.c) + cc) clipped at 0, lexicographic (d2, k) minimum.
+constexpr int RC_WARPS = 1;
+
+// 4- or 8-byte global -> shared copy that bypasses the registers (LDGSTS)
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* sdst, const void* gsrc) {
+    if (BYTES == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <typename TX>
+__global__ void __launch_bounds__(32 * RC_WARPS) assign_recheck_kernel(
+    const TX* __restrict__ X, long long n, long long ldx, int d, const double* __restrict__ C, long long ldc,
+    const double* __restrict__ cc, const double* __restrict__ xx_in, const uint8_t* __restrict__ gcand,
+    const uint8_t* __restrict__ gcnt, int32_t* __restrict__ labels, double* __restrict__ d2_out,
+    const int32_t* __restrict__ prev, unsigned long long* __restrict__ changed, unsigned long long* __restrict__ stats) {
+    __shared__ TX sx[RC_WARPS][2][32][33];   // the rows' 32-column chunk, double-buffered
+    __shared__ double sc[RC_WARPS][32][33];  // one candidate round's codeword rows
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const bool blk = d > (int)BLAS_Q;
+    unsigned long long nstat = 0, nchg = 0;
+    for (long long r0 = ((long long)blockIdx.x * RC_WARPS + w) * 32; r0 < n; r0 += (long long)gridDim.x * RC_WARPS * 32) {
+        const long long r = r0 + lane;
+        const int rows = (int)min(32LL, n - r0);
+        int cnt = r < n ? gcnt[r] : 0;
+        if (cnt > TC_CMAX) cnt = 0;   // overflow row: assign_overflow_kernel owns it
+        uint2 cw2 = make_uint2(0u, 0u);
+        if (cnt) cw2 = *reinterpret_cast<const uint2*>(gcand + r * 8);
+        int maxc = cnt;
+        for (int o = 16; o > 0; o >>= 1) maxc = max(maxc, __shfl_xor_sync(FULL, maxc, o));
+        double acc[TC_CMAX], tot[TC_CMAX];
+#pragma unroll
+        for (int j = 0; j < TC_CMAX; ++j) { acc[j] = 0.0; tot[j] = 0.0; }
+        // chunks: 32-column pieces that never straddle a BLAS k-block; [bs, be) is
+        // the block holding column kc (one block of d columns when d <= BLAS_Q)
+        auto block_of = [&](int kc, int& bs, int& be) {
+            bs = 0;
+            be = d;
+            if (blk) {
+                while (true) {
+                    be = bs + (int)blas_block_len(d - bs);
+                    if (kc < be) break;
+                    bs = be;
+                }
+            }
+        };
+        auto chunk_end = [&](int kc) -> int {
+            int bs, be;
+            block_of(kc, bs, be);
+            return min(be, kc + 32);
+        };
+        auto stage_x = [&](int kc, int wd, int buf) {
+            if (lane < wd)
+                for (int rr = 0; rr < rows; ++rr)
+                    cp_async<sizeof(TX)>(&sx[w][buf][rr][lane], X + (r0 + rr) * ldx + kc + lane);
+            cp_async_commit();
+        };
+        __syncwarp();
+        int kc = 0, ce = chunk_end(0), buf = 0;
+        stage_x(0, ce, 0);
+        while (kc < d) {
+            const int wd = ce - kc;
+            const int nkc = ce, nce = ce < d ? chunk_end(ce) : d;
+#pragma unroll
+            for (int j = 0; j < TC_CMAX; ++j) {
+                if (j < maxc) {
+                    const int kj = (int)(((j < 4 ? cw2.x : cw2.y) >> (8 * (j & 3))) & 0xFFu);
+                    const bool has = j < cnt;
+                    const unsigned hm = __ballot_sync(FULL, has);
+                    __syncwarp();
+                    for (int rr = 0; rr < rows; ++rr) {
+                        const int krr = __shfl_sync(FULL, kj, rr);
+                        if (((hm >> rr) & 1u) && lane < wd) cp_async<8>(&sc[w][rr][lane], C + (long long)krr * ldc + kc + lane);
+                    }
+                    cp_async_commit();
+                    if (j == 0 && nkc < d) {
+                        stage_x(nkc, nce - nkc, buf ^ 1);   // next chunk's rows in flight meanwhile
+                        cp_async_wait_group<1>();
+                    } else {
+                        cp_async_wait_group<0>();
+                    }
+                    __syncwarp();
+                    if (has) {
+                        double a = acc[j];
+                        for (int t = 0; t < wd; ++t) a = __fma_rn((double)sx[w][buf][lane][t], sc[w][lane][t], a);
+                        acc[j] = a;
+                    }
+                }
+            }
+            if (maxc == 0 && nkc < d) {
+                __syncwarp();
+                stage_x(nkc, nce - nkc, buf ^ 1);
+            }
+            int bs, be;
+            block_of(kc, bs, be);
+            if (ce == be) {   // end of a BLAS block: fold its chain into the total
+#pragma unroll
+                for (int j = 0; j < TC_CMAX; ++j) {
+                    tot[j] = bs == 0 ? acc[j] : dadd(tot[j], acc[j]);
+                    acc[j] = 0.0;
+                }
+            }
+            kc = nkc;
+            ce = nce;
+            buf ^= 1;
+        }
+        cp_async_wait_group<0>();
+        if (cnt) {
+            double xx;
+            if (xx_in) {
+                xx = xx_in[r];
+            } else {
+                const TX* xr = X + r * ldx;
+                xx = np_pw_sum([&](long long i) { double t = (double)xr[i]; return dmul(t, t); }, 0, d);
+            }
+            double best = __longlong_as_double(0x7ff0000000000000ULL);
+            int bk = 0x7fffffff;
+#pragma unroll
+            for (int j = 0; j < TC_CMAX; ++j) {
+                if (j < cnt) {
+                    const int kj = (int)(((j < 4 ? cw2.x : cw2.y) >> (8 * (j & 3))) & 0xFFu);
+                    double dv = dadd(dsub(xx, dmul(2.0, tot[j])), cc[kj]);
+                    if (dv < 0.0) dv = 0.0;
+                    if (lex_less(dv, kj, best, bk)) { best = dv; bk = kj; }
+                }
+            }
+            labels[r] = bk;
+            d2_out[r] = best;
+            nstat += cnt;
+            if (prev != nullptr && prev[r] != bk) ++nchg;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        nstat += __shfl_xor_sync(FULL, nstat, o);
+        nchg += __shfl_xor_sync(FULL, nchg, o);
+    }
+    if (lane == 0) {
+        if (stats && nstat) atomicAdd(stats, nstat);
+        if (changed != nullptr && prev != nullptr && nchg) atomicAdd(changed, nchg);
+    }
+}
+
+// Row image bound by the host for the duration of one Lloyd call (the rotated
+// rows are fixed while the centroids move): assigns on exactly this (X, n, ldx,
+// d) read it instead of rebuilding it.
+static struct {
+    const void* X = nullptr;
+    long long n = 0, ldx = 0;
+    int d = 0;
+    const float* img = nullptr;
+} g_img;
+
+size_t assign_image_bytes(long long n, int d) {
+    const long long ntiles = (n + TC_M - 1) / TC_M;
+    const int nch = (d + TC_BK - 1) / TC_BK;
+    return sizeof(float) * (size_t)ntiles * nch * 2 * TC_M * TC_BK;
+}
+
+static void build_image(const void* X, int x_is_f32, long long n, long long ldx, int d, float* img, cudaStream_t s) {
+    const int nch = (d + TC_BK - 1) / TC_BK;
+    const long long total = ((n + TC_M - 1) / TC_M) * nch * TC_M * TC_BK / 4;
+    if (x_is_f32)
+        x_tf32_prep_kernel<float><<<grid_for(total, 256), 256, 0, s>>>((const float*)X, n, ldx, d, nch, img);
+    else
+        x_tf32_prep_kernel<double><<<grid_for(total, 256), 256, 0, s>>>((const double*)X, n, ldx, d, nch, img);
+}
+
+int assign_bind_image(const void* X, int x_is_f32, long long n, long long ldx, int d, float* img, cudaStream_t s) {
+    g_img.X = nullptr;
+    g_img.img = nullptr;
+    if (X == nullptr || img == nullptr || n <= 0 || d < 1) return 0;   // unbind
+    {
+        ProfScope ps("assign_image", s);
+        build_image(X, x_is_f32, n, ldx, d, img, s);
+    }
+    DA_CHECK_LAUNCH("x_tf32_prep_kernel");
+    g_img.X = X;
+    g_img.n = n;
+    g_img.ldx = ldx;
+    g_img.d = d;
+    g_img.img = img;
+    return 0;
+}
+
 // Returns 1 (without launching) when the shape is outside the tensor-core path.
 int launch_assign_tc(const void* X, int x_is_f32, long long n, long long ldx, int d, const double* C, long long ldc,
                      int K, const double* cc, const double* xx, int32_t* labels, double* d2, const int32_t* prev,
@@ -531,15 +730,26 @@ int launch_assign_tc(const void* X, int x_is_f32, long long n, long long ldx, in
     if (K > TC_NMAX || K < 1 || d < 1) return 1;
     if (n <= 0) return 0;
     const int nch = (d + TC_BK - 1) / TC_BK;
+    const bool bound = g_img.img != nullptr && g_img.X == X && g_img.n == n && g_img.ldx == ldx && g_img.d == d;
     const size_t bg_bytes = (sizeof(float) * (size_t)nch * 2 * TC_NMAX * TC_BK + 255) & ~size_t(255);
-    char* base = (char*)scratch(9, bg_bytes + sizeof(int) * ((size_t)n + 64), s);
+    const size_t ovf_bytes = (sizeof(int) * ((size_t)n + 64) + 255) & ~size_t(255);
+    const size_t cand_bytes = (9 * (size_t)n + 255) & ~size_t(255);
+    const size_t img_bytes = bound ? 0 : assign_image_bytes(n, d);
+    char* base = (char*)scratch(9, bg_bytes + ovf_bytes + cand_bytes + img_bytes, s);
     if (!base) return fail_cuda(cudaErrorMemoryAllocation, "assign_tc scratch");
     float* Bg = (float*)base;
     int* ovf_cnt = (int*)(base + bg_bytes);
     int* ovf_rows = ovf_cnt + 64;
+    uint8_t* gcand = (uint8_t*)(base + bg_bytes + ovf_bytes);   // [n][8] candidate codewords
+    uint8_t* gcnt = gcand + 8 * (size_t)n;                        // [n] counts (0xFF = overflow)
+    const float* Ag = bound ? g_img.img : (const float*)(base + bg_bytes + ovf_bytes + cand_bytes);
     DA_CUDA(cudaMemsetAsync(ovf_cnt, 0, sizeof(int), s));
     ProfScope ps(d <= 8 ? "assign_tc_d<=8" : d <= 32 ? "assign_tc_d<=32" : d <= 128 ? "assign_tc_d<=128" : "assign_tc_d>128",
                  s);
+    if (!bound) {
+        build_image(X, x_is_f32, n, ldx, d, (float*)Ag, s);
+        DA_CHECK_LAUNCH("x_tf32_prep_kernel");
+    }
     cw_tf32_prep_kernel<<<grid_for((long long)nch * TC_NMAX * TC_BK, 256, 4096), 256, 0, s>>>(C, ldc, K, d, nch, Bg);
     DA_CHECK_LAUNCH("cw_tf32_prep_kernel");
     const size_t smem = sizeof(float) * (2 * 2 * TC_M * TC_BK + 2 * 2 * TC_NMAX * TC_BK) + sizeof(double) * TC_NMAX +
@@ -550,20 +760,27 @@ int launch_assign_tc(const void* X, int x_is_f32, long long n, long long ldx, in
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const long long ntiles = (n + TC_M - 1) / TC_M;
     const unsigned grid = (unsigned)std::min<long long>(ntiles, sms);
+    const unsigned rgrid = grid_for((n + 31) / 32, RC_WARPS, 1LL << 31);
     if (x_is_f32) {
         auto kf = assign_tc_kernel<float>;
         DA_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kf<<<grid, TC_T2, smem, s>>>((const float*)X, n, ldx, d, C, ldc, K, cc, xx, Bg, labels, d2, prev, changed,
-                                     stats, ovf_rows, ovf_cnt);
+        kf<<<grid, TC_TP, smem, s>>>((const float*)X, n, ldx, d, K, cc, xx, Ag, Bg, stats, ovf_rows, ovf_cnt, gcand,
+                                     gcnt);
         DA_CHECK_LAUNCH("assign_tc_kernel");
+        assign_recheck_kernel<float><<<rgrid, 32 * RC_WARPS, 0, s>>>((const float*)X, n, ldx, d, C, ldc, cc, xx, gcand,
+                                                                     gcnt, labels, d2, prev, changed, stats);
+        DA_CHECK_LAUNCH("assign_recheck_kernel");
         assign_overflow_kernel<float><<<sms, 256, 0, s>>>((const float*)X, ldx, d, C, ldc, K, cc, xx, ovf_rows, ovf_cnt,
                                                           labels, d2, prev, changed);
     } else {
         auto kf = assign_tc_kernel<double>;
         DA_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kf<<<grid, TC_T2, smem, s>>>((const double*)X, n, ldx, d, C, ldc, K, cc, xx, Bg, labels, d2, prev, changed,
-                                     stats, ovf_rows, ovf_cnt);
+        kf<<<grid, TC_TP, smem, s>>>((const double*)X, n, ldx, d, K, cc, xx, Ag, Bg, stats, ovf_rows, ovf_cnt, gcand,
+                                     gcnt);
         DA_CHECK_LAUNCH("assign_tc_kernel");
+        assign_recheck_kernel<double><<<rgrid, 32 * RC_WARPS, 0, s>>>((const double*)X, n, ldx, d, C, ldc, cc, xx,
+                                                                      gcand, gcnt, labels, d2, prev, changed, stats);
+        DA_CHECK_LAUNCH("assign_recheck_kernel");
         assign_overflow_kernel<double><<<sms, 256, 0, s>>>((const double*)X, ldx, d, C, ldc, K, cc, xx, ovf_rows,
                                                            ovf_cnt, labels, d2, prev, changed);
     }
@@ -573,10 +790,10 @@ int launch_assign_tc(const void* X, int x_is_f32, long long n, long long ldx, in
         cudaStreamSynchronize(s);
         cudaMemcpyFromSymbol(hp, g_at_prof, sizeof(hp));
         unsigned long long tot = 0;
-        for (int i = 0; i < 6; ++i) tot += hp[i];
-        const char* nm[6] = {"stage", "mma_issue", "acc_wait", "pass1", "pass2", "recheck"};
-        fprintf(stderr, "[da] assign_tc d=%d phases:", d);
-        for (int i = 0; i < 6; ++i) fprintf(stderr, " %s %.1f%%", nm[i], tot ? 100.0 * hp[i] / tot : 0.0);
+        for (int i = 2; i < 6; ++i) tot += hp[i];
+        const char* nm[6] = {"", "", "acc_wait", "pass1", "pass2", "cand_write"};
+        fprintf(stderr, "[da] assign_tc d=%d epilogue thread phases:", d);
+        for (int i = 2; i < 6; ++i) fprintf(stderr, " %s %.1f%%", nm[i], tot ? 100.0 * hp[i] / tot : 0.0);
         int hc = 0;
         cudaMemcpy(&hc, ovf_cnt, sizeof(int), cudaMemcpyDeviceToHost);
         fprintf(stderr, " overflow_rows %d\n", hc);

@@ -92,6 +92,17 @@ int da_encode_config(int mode, unsigned long long* recheck_counter) {
     return 0;
 }
 
+int64_t da_assign_image_bytes(int64_t n, int d) {
+    if (n < 0 || d < 1) return 0;
+    return (int64_t)assign_image_bytes(n, d);
+}
+
+int da_assign_bind_image(const void* X, int x_f32, int64_t n, int64_t ldx, int d, float* image, void* stream) {
+    if (X != nullptr && image != nullptr && (n < 0 || d < 1 || ldx < d))
+        return fail_arg("assign_bind_image: bad shape n=%lld d=%d ldx=%lld", (long long)n, d, (long long)ldx);
+    return assign_bind_image(X, x_f32, n, ldx, d, image, STREAM(stream));
+}
+
 int da_assign_config(int mode, unsigned long long* candidate_counter) {
     if (mode != 0 && mode != 1) return fail_arg("assign mode must be 0 (auto) or 1 (plain float64)");
     return set_assign_config(mode, candidate_counter);

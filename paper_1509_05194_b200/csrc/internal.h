@@ -92,6 +92,8 @@ int launch_assign_tc(const void* X, int x_is_f32, long long n, long long ldx, in
                      int K, const double* cc, const double* xx, int32_t* labels, double* d2, const int32_t* prev,
                      unsigned long long* changed, unsigned long long* stats, cudaStream_t s);
 int set_assign_config(int mode, unsigned long long* stats);
+size_t assign_image_bytes(long long n, int d);
+int assign_bind_image(const void* X, int x_is_f32, long long n, long long ldx, int d, float* img, cudaStream_t s);
 // launcher result meaning "this path does not take the shape" (caller falls through)
 constexpr int kNotApplicable = 1 << 30;
 int launch_table_tc(const float* X, long long n, long long ldx, int D, const float* cw, const double* sq, int M, int K,

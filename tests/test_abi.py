@@ -23,7 +23,7 @@ def declared():
 def test_header_lists_the_hot_path():
     names = declared()
     for must in ("da_assign", "da_group_sums", "da_heat_up", "da_pca_cov", "da_rotate", "da_cross_products",
-                 "da_encode", "da_pair_sums", "da_adc_lut", "da_adc_scan", "da_adc_pack", "da_unpack_vecs",
+                 "da_encode", "da_pair_sums", "da_adc_lut", "da_adc_scan", "da_adc_pack", "da_unpack_vecs", "da_assign_bind_image", "da_assign_image_bytes",
                  "da_adc_scan_packed", "da_atree_search", "da_knn", "da_last_error"):
         assert must in names
 
