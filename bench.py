@@ -373,7 +373,7 @@ def main():
         build_s = time.perf_counter() - t0
         Qa = rank_data(7 + rank, 10_000).astype(np.float64)
         params = AT.SearchParams(l0=8, ls=2.0, r=10)
-        AT.atree_search_batch(tree, book_t, Qa[:100], params)
+        AT.atree_search_batch(tree, book_t, Qa, params)   # warm-up sizes the per-CTA scratch
         barrier()
         t0 = time.perf_counter()
         _, _, _, st = AT.atree_search_batch(tree, book_t, Qa, params)

@@ -25,7 +25,7 @@ Q = bench.rank_data(7, nq).astype(np.float64)
 out = {"n": n, "nq": nq, "build_s": t_build, "nodes": tree.node_count, "leaves": tree.leaf_count}
 for l0 in (8, 32):
     params = AT.SearchParams(l0=l0, ls=2.0, r=10)
-    AT.atree_search_batch(tree, book, Q[:100], params)
+    AT.atree_search_batch(tree, book, Q, params)   # warm-up sizes the per-CTA scratch
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     ids, d, cnt, st = AT.atree_search_batch(tree, book, Q, params)
