@@ -22,23 +22,25 @@ struct FastSmem {
     long long* roff; // [cap*M] cross-table row offsets of the current stage
 };
 
-__host__ __device__ inline size_t fast_vbuf_bytes(int cap, int K, int D) {
-    size_t a = sizeof(float) * (size_t)cap * K, b = sizeof(double) * (size_t)D;
+// lean: no per-candidate value buffer (rescans recompute), only the exact-phase
+// (value, flat) arrays and the float64 error staging share the region
+__host__ __device__ inline size_t fast_vbuf_bytes(int cap, int K, int D, bool lean = false) {
+    size_t a = lean ? 0 : sizeof(float) * (size_t)cap * K, b = sizeof(double) * (size_t)D;
     size_t c = (sizeof(double) + sizeof(int)) * (size_t)QCAP;  // exact (value, flat) of queued candidates
     size_t m = a > b ? a : b;
     m = m > c ? m : c;
     return (m + 15) & ~size_t(15);
 }
 
-__host__ __device__ inline size_t fast_smem_bytes(int cap, int M, int K, int D) {
+__host__ __device__ inline size_t fast_smem_bytes(int cap, int M, int K, int D, bool lean = false) {
     size_t b = sizeof(double) * (3 * (size_t)cap + D) + sizeof(long long) * (size_t)cap * M;
     b = (b + 15) & ~size_t(15);
-    b += fast_vbuf_bytes(cap, K, D);
+    b += fast_vbuf_bytes(cap, K, D, lean);
     b += sizeof(int32_t) * (2 * (size_t)cap * M + cap + 33 + QCAP);
     return (b + 15) & ~size_t(15);
 }
 
-__device__ inline FastSmem carve_fast(char* p, int cap, int M, int K, int D) {
+__device__ inline FastSmem carve_fast(char* p, int cap, int M, int K, int D, bool lean = false) {
     FastSmem s;
     char* p0 = p;
     s.x64 = (double*)p; p += sizeof(double) * D;  // first: 16-byte aligned for double2 reads
@@ -46,7 +48,7 @@ __device__ inline FastSmem carve_fast(char* p, int cap, int M, int K, int D) {
     s.lv = (double*)p; p += sizeof(double) * cap;
     s.roff = (long long*)p; p += sizeof(long long) * cap * M;
     p = p0 + (((size_t)(p - p0) + 15) & ~size_t(15));
-    s.vbuf = (float*)p; p += fast_vbuf_bytes(cap, K, D);
+    s.vbuf = (float*)p; p += fast_vbuf_bytes(cap, K, D, lean);
     s.codes = (int32_t*)p; p += 2 * sizeof(int32_t) * cap * M;
     s.lf = (int32_t*)p; p += sizeof(int32_t) * cap;
     s.queue = (int32_t*)p;

@@ -150,8 +150,93 @@ __global__ void bound_prep_kernel(const float* __restrict__ cw, const double* __
     }
 }
 
-template <typename TX>
-__global__ void __launch_bounds__(256) beam_fast_kernel(
+// LEAN: no shared-memory copy of the candidate values (the few lanes that hold
+// two or more candidates under the limit recompute theirs), groups of two beams:
+// ~5 KB of shared memory and <= 80 registers per warp, so 24 warps fit an SM
+// instead of 16.  Same values, same codes.
+#ifndef DA_LEAN_MINB
+#define DA_LEAN_MINB 3
+#endif
+#ifndef DA_LEAN_G
+#define DA_LEAN_G 2
+#endif
+// Exact float64 value of candidate `flat` of stage m, in the reference's order
+// (BLAS-ordered x.c, einsum ||c||^2, sequential cross sum).  Out of line: it is
+// called from the queue pass and from the overflow path, and the kernel's hot
+// loops must stay within the instruction cache.
+template <bool INL>
+__device__ __forceinline__ double beam_exact_value_t(const double* __restrict__ x64, const double* __restrict__ cw64,
+                                                const float* __restrict__ cw32, int D, const double* __restrict__ sq,
+                                                const double* __restrict__ P, const int32_t* __restrict__ pc,
+                                                const double* __restrict__ ps, int M, int K, int m, int flat, int k_sh) {
+    const int l = k_sh >= 0 ? flat >> k_sh : flat / K;
+    const int k = flat - l * K;
+    const double xc = exact_dot(x64, cw64 + ((long long)m * K + k) * D, D, cw32 ? cw32 + ((long long)m * K + k) * D : nullptr);
+    const double t = dsub(sq[m * K + k], dmul(2.0, xc));
+    double cross = 0.0;
+    for (int j = 0; j < m; ++j) cross = dadd(cross, P[(((long long)j * M + m) * K + pc[l * M + j]) * K + k]);
+    return dadd(dadd(ps[l], t), dmul(2.0, cross));
+}
+__device__ __noinline__ double beam_exact_value(const double* __restrict__ x64, const double* __restrict__ cw64,
+                                                const float* __restrict__ cw32, int D, const double* __restrict__ sq,
+                                                const double* __restrict__ P, const int32_t* __restrict__ pc,
+                                                const double* __restrict__ ps, int M, int K, int m, int flat, int k_sh) {
+    return beam_exact_value_t<false>(x64, cw64, cw32, D, sq, P, pc, ps, M, K, m, flat, k_sh);
+}
+
+// Rare path: more near-boundary candidates than the queue holds -> exact
+// streaming selection over every candidate of the stage (warp-collective).
+__device__ __noinline__ void beam_overflow_select(FastSmem S, int total, int width, const double* __restrict__ x64,
+                                                  const double* __restrict__ cw64, const float* __restrict__ cw32,
+                                                  int D, const double* __restrict__ sq, const double* __restrict__ P,
+                                                  const int32_t* __restrict__ pc, const double* __restrict__ ps, int M,
+                                                  int K, int m, int k_sh, unsigned long long& n_exact) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    int cnt = 0;
+    auto accept = [&](double a, int fa) -> bool {
+        if (cnt < width) return true;
+        return lex_less(a, fa, S.lv[width - 1], S.lf[width - 1]);
+    };
+    for (int b = 0; b < total; b += 32) {
+        const int flat = b + lane;
+        const bool has = flat < total;
+        const double val = has ? beam_exact_value(x64, cw64, cw32, D, sq, P, pc, ps, M, K, m, flat, k_sh) : 0.0;
+        n_exact += has ? 1 : 0;
+        unsigned mask = __ballot_sync(FULL, has && accept(val, flat));
+        while (mask) {
+            const int src = __ffs(mask) - 1;
+            const double cv = __shfl_sync(FULL, val, src);
+            const int cf = __shfl_sync(FULL, flat, src);
+            int pos = 0;
+            for (int bb = 0; bb < cnt; bb += 32) {
+                int i = bb + lane;
+                bool lt = (i < cnt) && lex_less(S.lv[i], S.lf[i], cv, cf);
+                pos += __popc(__ballot_sync(FULL, lt));
+            }
+            const int endp = min(cnt, width - 1);
+            for (int bb = endp - 1; bb >= pos; bb -= 32) {
+                int i = bb - lane;
+                bool act = i >= pos;
+                double tv = 0.0;
+                int tf = 0;
+                if (act) { tv = S.lv[i]; tf = S.lf[i]; }
+                __syncwarp();
+                if (act) { S.lv[i + 1] = tv; S.lf[i + 1] = tf; }
+                __syncwarp();
+            }
+            if (lane == 0) { S.lv[pos] = cv; S.lf[pos] = cf; }
+            __syncwarp();
+            cnt = min(cnt + 1, width);
+            mask &= ~(1u << src);
+            mask &= __ballot_sync(FULL, has && accept(val, flat));
+        }
+    }
+    __syncwarp();
+}
+
+template <typename TX, bool LEAN, bool VEC>
+__global__ void __launch_bounds__(256, LEAN ? DA_LEAN_MINB : 2) beam_fast_kernel(
     const TX* __restrict__ X, long long n, long long ldx, int D, const float* __restrict__ cw, int M, int K, int L,
     int cap, const float* __restrict__ tab32, const double* __restrict__ sq, const double* __restrict__ P,
     const float* __restrict__ P32, const double* __restrict__ cmax, const double* __restrict__ pabs,
@@ -164,7 +249,7 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
     const int nwarps = blockDim.x >> 5;
     const long long v = (long long)blockIdx.x * nwarps + wid;
     if (v >= n) return;
-    FastSmem S = carve_fast(smem_raw + (size_t)wid * fast_smem_bytes(cap, M, K, D), cap, M, K, D);
+    FastSmem S = carve_fast(smem_raw + (size_t)wid * fast_smem_bytes(cap, M, K, D, LEAN), cap, M, K, D, LEAN);
     // 16-byte aligned fp32 codeword rows (D % 4 == 0): vector loads in the exact dot
     const int nkb = (K + 31) / 32;
     const int nkb_sh = (nkb & (nkb - 1)) == 0 ? __ffs(nkb) - 1 : -1;
@@ -222,7 +307,7 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
         // (and the index of the smallest).  With K % 256 == 0 a lane owns
         // k = kb + 4*lane + {0..3} and kb + 128 + 4*lane + {0..3} (16-B gathers),
         // otherwise k = kb + 32q + lane.  Four beams are processed together.
-        const bool vec = (K & 255) == 0;
+        const bool vec = VEC;   // K % 256 == 0: 16-byte gathers (compile-time, keeps the code small)
         auto kof = [&](int kb, int q) -> int {
             return vec ? kb + (q >> 2) * 128 + 4 * lane + (q & 3) : kb + 32 * q + lane;
         };
@@ -306,7 +391,7 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
                     float vv[8];
 #pragma unroll
                     for (int q = 0; q < 8; ++q) vv[q] = (sl + tk[q]) + 2.f * acc[g][q];
-                    if (vec) {
+                    if (vec && !LEAN) {
                         *reinterpret_cast<float4*>(S.vbuf + l * K + kb + 4 * lane) = make_float4(vv[0], vv[1], vv[2], vv[3]);
                         *reinterpret_cast<float4*>(S.vbuf + l * K + kb + 128 + 4 * lane) =
                             make_float4(vv[4], vv[5], vv[6], vv[7]);
@@ -315,8 +400,11 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
                             const int k = kof(kb, q);
-                            if (k < K) S.vbuf[l * K + k] = vv[q];
-                            else vv[q] = __int_as_float(0x7f800000);
+                            if (k < K) {
+                                if (!LEAN) S.vbuf[l * K + k] = vv[q];
+                            } else {
+                                vv[q] = __int_as_float(0x7f800000);
+                            }
                         }
                     }
                     // batch minimum first; the per-candidate update only runs when the
@@ -335,12 +423,17 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
                 }
             };
             int l0 = 0;
-            for (; l0 + 4 <= live; l0 += 4) group(std::integral_constant<int, 4>{}, l0);
-            switch (live - l0) {
-                case 3: group(std::integral_constant<int, 3>{}, l0); break;
-                case 2: group(std::integral_constant<int, 2>{}, l0); break;
-                case 1: group(std::integral_constant<int, 1>{}, l0); break;
-                default: break;
+            if (LEAN && DA_LEAN_G == 2) {
+                for (; l0 + 2 <= live; l0 += 2) group(std::integral_constant<int, 2>{}, l0);
+                if (l0 < live) group(std::integral_constant<int, 1>{}, l0);
+            } else {
+                for (; l0 + 4 <= live; l0 += 4) group(std::integral_constant<int, 4>{}, l0);
+                switch (live - l0) {
+                    case 3: group(std::integral_constant<int, 3>{}, l0); break;
+                    case 2: group(std::integral_constant<int, 2>{}, l0); break;
+                    case 1: group(std::integral_constant<int, 1>{}, l0); break;
+                    default: break;
+                }
             }
         }
         __syncwarp();
@@ -381,6 +474,47 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
             if (slot < QCAP) S.queue[33 + slot] = i1;
         }
         unsigned flagged = __ballot_sync(FULL, multi);
+        if (LEAN) {
+            // lanes holding two or more candidates under the limit: the warp recomputes
+            // their values (same gathers, same addition order as pass A), one item per
+            // (flagged lane, beam, 256-column block)
+            const int nflag = __popc(flagged);
+            const int nkb256 = (K + 255) / 256;
+            const int per_f = live * nkb256;
+            for (int t = lane; t < nflag * per_f; t += 32) {
+                const int fi = t / per_f, rem = t - fi * per_f;
+                unsigned fm = flagged;
+                for (int i = 0; i < fi; ++i) fm &= fm - 1;
+                const int f = __ffs(fm) - 1;
+                const int l = rem / nkb256, kb = (rem - l * nkb256) * 256;
+                auto kf = [&](int q) -> int { return vec ? kb + (q >> 2) * 128 + 4 * f + (q & 3) : kb + 32 * q + f; };
+                float acc[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+                for (int j = 0; j < m; ++j) {
+                    const float* rp = P32 + S.roff[l * M + j];
+                    if (vec) {
+                        const float4 a = __ldg(reinterpret_cast<const float4*>(rp + kb + 4 * f));
+                        const float4 b = __ldg(reinterpret_cast<const float4*>(rp + kb + 128 + 4 * f));
+                        acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+                        acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) acc[q] += (kf(q) < K) ? __ldg(rp + kf(q)) : 0.f;
+                    }
+                }
+                const float sl = (float)ps[l];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int k = kf(q);
+                    if (k < K && (sl + trow[m * K + k]) + 2.f * acc[q] <= limf) {
+                        const int slot = atomicAdd(qcount, 1);
+                        if (slot < QCAP) S.queue[33 + slot] = l * K + k;
+                    }
+                }
+            }
+            flagged = 0;
+        }
         const int per_lane = live * nkb;
         while (flagged) {
             const int f = __ffs(flagged) - 1;
@@ -400,15 +534,9 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
         __syncwarp();
         const int nqueued = *qcount;
         __syncwarp();
+        const float* cw32 = c32ok ? cw : nullptr;
         auto exact_value = [&](int flat) -> double {
-            const int l = k_sh >= 0 ? flat >> k_sh : flat / K;
-            const int k = flat - l * K;
-            const double xc = exact_dot(S.x64, cw64 + ((long long)m * K + k) * D, D,
-                                        c32ok ? cw + ((long long)m * K + k) * D : nullptr);
-            const double t = dsub(sq[m * K + k], dmul(2.0, xc));
-            double cross = 0.0;
-            for (int j = 0; j < m; ++j) cross = dadd(cross, P[(((long long)j * M + m) * K + pc[l * M + j]) * K + k]);
-            return dadd(dadd(ps[l], t), dmul(2.0, cross));
+            return beam_exact_value_t<true>(S.x64, cw64, cw32, D, sq, P, pc, ps, M, K, m, flat, k_sh);
         };
         int cnt = 0;
         if (nqueued <= QCAP) {
@@ -446,46 +574,7 @@ __global__ void __launch_bounds__(256) beam_fast_kernel(
             cnt = width;
             __syncwarp();
         } else {
-            // rare: too many near-boundary candidates -> exact streaming selection over all
-            auto accept = [&](double a, int fa) -> bool {
-                if (cnt < width) return true;
-                return lex_less(a, fa, S.lv[width - 1], S.lf[width - 1]);
-            };
-            for (int b = 0; b < total; b += 32) {
-                const int flat = b + lane;
-                const bool has = flat < total;
-                const double val = has ? exact_value(flat) : 0.0;
-                n_exact += has ? 1 : 0;
-                unsigned mask = __ballot_sync(FULL, has && accept(val, flat));
-                while (mask) {
-                    const int src = __ffs(mask) - 1;
-                    const double cv = __shfl_sync(FULL, val, src);
-                    const int cf = __shfl_sync(FULL, flat, src);
-                    int pos = 0;
-                    for (int bb = 0; bb < cnt; bb += 32) {
-                        int i = bb + lane;
-                        bool lt = (i < cnt) && lex_less(S.lv[i], S.lf[i], cv, cf);
-                        pos += __popc(__ballot_sync(FULL, lt));
-                    }
-                    const int endp = min(cnt, width - 1);
-                    for (int bb = endp - 1; bb >= pos; bb -= 32) {
-                        int i = bb - lane;
-                        bool act = i >= pos;
-                        double tv = 0.0;
-                        int tf = 0;
-                        if (act) { tv = S.lv[i]; tf = S.lf[i]; }
-                        __syncwarp();
-                        if (act) { S.lv[i + 1] = tv; S.lf[i + 1] = tf; }
-                        __syncwarp();
-                    }
-                    if (lane == 0) { S.lv[pos] = cv; S.lf[pos] = cf; }
-                    __syncwarp();
-                    cnt = min(cnt + 1, width);
-                    mask &= ~(1u << src);
-                    mask &= __ballot_sync(FULL, has && accept(val, flat));
-                }
-            }
-            __syncwarp();
+            beam_overflow_select(S, total, width, S.x64, cw64, cw32, D, sq, P, pc, ps, M, K, m, k_sh, n_exact);
         }
 
         // ---- next beam in flat (lexicographic) order
@@ -553,7 +642,12 @@ int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int
     long long capll = 1;
     for (int m = 0; m < M && capll < L; ++m) capll *= K;
     const int cap = (int)std::min((long long)L, capll);
-    const size_t per_warp = fast_smem_bytes(cap, M, K, D);
+    // measured on B200 (config B, 1M vectors): the value-buffer kernel wins for
+    // narrow beams (L=4: 33.6 vs 36.4 ms), the lean one from L=8 up (L=10: 58.8 vs
+    // 59.7, L=16: 100.9 vs 129.5).  DA_BEAM_VBUF=0/1 forces either (A/B runs).
+    const char* ev = getenv("DA_BEAM_VBUF");
+    const bool lean = ev ? atoi(ev) == 0 : L >= 8;
+    const size_t per_warp = fast_smem_bytes(cap, M, K, D, lean);
     int warps = 8;
     while (warps > 1 && per_warp * warps > 200 * 1024) warps >>= 1;
     if (per_warp * warps > 220 * 1024) return 1;  // caller falls back to the plain encoder
@@ -575,7 +669,10 @@ int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int
     bound_prep_kernel<<<M * M, 256, 0, s>>>(cw, P, M, K, D, sq, P32, sq32, cmax, pabs, cw64);
     DA_CHECK_LAUNCH("bound_prep_kernel");
 
-    auto kf = x_f32 ? (const void*)beam_fast_kernel<float> : (const void*)beam_fast_kernel<double>;
+    if (!x_f32) return fail_arg("encode_fast: float32 input only");
+    const bool vec = (K & 255) == 0;
+    auto kf = lean ? (vec ? (const void*)beam_fast_kernel<float, true, true> : (const void*)beam_fast_kernel<float, true, false>)
+                   : (vec ? (const void*)beam_fast_kernel<float, false, true> : (const void*)beam_fast_kernel<float, false, false>);
     if (smem > 48 * 1024) DA_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const long long row_bytes = (long long)M * K * sizeof(float);
     long long chunk = std::max(1024LL, (1LL << 30) / row_bytes);
@@ -603,9 +700,11 @@ int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int
         double* eout = err_out ? err_out + c0 : nullptr;
         ProfScope ps2("encode_beam_fast", s);
         const unsigned grid = (unsigned)((cn + warps - 1) / warps);
-        beam_fast_kernel<float><<<grid, warps * 32, smem, s>>>((const float*)X + c0 * ldx, cn, ldx, D, cw, M, K, L,
-                                                               cap, tab, sq, P, P32, cmax, pabs, cw64, cout, code_bytes,
-                                                               ldcodes, eout, stats, tab_tc);
+        auto* kfn = (void (*)(const float*, long long, long long, int, const float*, int, int, int, int, const float*,
+                              const double*, const double*, const float*, const double*, const double*, const double*,
+                              void*, int, long long, double*, unsigned long long*, int))kf;
+        kfn<<<grid, warps * 32, smem, s>>>((const float*)X + c0 * ldx, cn, ldx, D, cw, M, K, L, cap, tab, sq, P, P32,
+                                           cmax, pabs, cw64, cout, code_bytes, ldcodes, eout, stats, tab_tc);
         DA_CHECK_LAUNCH("beam_fast_kernel");
     }
     return 0;
