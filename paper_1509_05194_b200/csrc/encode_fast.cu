@@ -160,6 +160,15 @@ __global__ void bound_prep_kernel(const float* __restrict__ cw, const double* __
 #ifndef DA_LEAN_G
 #define DA_LEAN_G 2
 #endif
+// cbm[m] = (1 + 1e-12) * sum_{j<m} max|P[j,m]|: the cross-term bound of stage m
+__global__ void cb_prep_kernel(const double* __restrict__ pabs, int M, double* __restrict__ cbm) {
+    for (int m = threadIdx.x; m < M; m += blockDim.x) {
+        double c = 0.0;
+        for (int j = 0; j < m; ++j) c += pabs[j * M + m];
+        cbm[m] = c * (1.0 + 1e-12);
+    }
+}
+
 // Exact float64 value of candidate `flat` of stage m, in the reference's order
 // (BLAS-ordered x.c, einsum ||c||^2, sequential cross sum).  Out of line: it is
 // called from the queue pass and from the overflow path, and the kernel's hot
@@ -174,6 +183,7 @@ __device__ __forceinline__ double beam_exact_value_t(const double* __restrict__ 
     const double xc = exact_dot(x64, cw64 + ((long long)m * K + k) * D, D, cw32 ? cw32 + ((long long)m * K + k) * D : nullptr);
     const double t = dsub(sq[m * K + k], dmul(2.0, xc));
     double cross = 0.0;
+#pragma unroll 4
     for (int j = 0; j < m; ++j) cross = dadd(cross, P[(((long long)j * M + m) * K + pc[l * M + j]) * K + k]);
     return dadd(dadd(ps[l], t), dmul(2.0, cross));
 }
@@ -239,7 +249,7 @@ template <typename TX, bool LEAN, bool VEC>
 __global__ void __launch_bounds__(256, LEAN ? DA_LEAN_MINB : 2) beam_fast_kernel(
     const TX* __restrict__ X, long long n, long long ldx, int D, const float* __restrict__ cw, int M, int K, int L,
     int cap, const float* __restrict__ tab32, const double* __restrict__ sq, const double* __restrict__ P,
-    const float* __restrict__ P32, const double* __restrict__ cmax, const double* __restrict__ pabs,
+    const float* __restrict__ P32, const double* __restrict__ cmax, const double* __restrict__ cbm,
     const double* __restrict__ cw64, void* codes_out,
     int code_bytes, long long ldcodes, double* __restrict__ err_out, unsigned long long* __restrict__ stats, int tab_tc) {
     extern __shared__ __align__(16) char smem_raw[];
@@ -279,14 +289,11 @@ __global__ void __launch_bounds__(256, LEAN ? DA_LEAN_MINB : 2) beam_fast_kernel
         const int32_t* pc = S.codes + cur * cap * M;
         const double* ps = S.score + cur * cap;
         // ---- rigorous bound of |v' - v| for this stage
-        double smax = 0.0;
-        for (int l = lane; l < live; l += 32) smax = fmax(smax, fabs(ps[l]));
+        double smax = lane < live ? fabs(ps[lane]) : 0.0;   // straight-line for live <= 32
+        for (int l = lane + 32; l < live; l += 32) smax = fmax(smax, fabs(ps[l]));
         for (int off = 16; off >= 1; off >>= 1) smax = fmax(smax, __shfl_xor_sync(FULL, smax, off));
-        // sum of the cross-table maxima (a bound, so any order): one load per lane
-        double cb = 0.0;
-        for (int j = lane; j < m; j += 32) cb += pabs[j * M + m];
-        for (int off = 16; off >= 1; off >>= 1) cb += __shfl_xor_sync(FULL, cb, off);
-        cb *= 1.0 + 1e-12;
+        // sum of the cross-table maxima over j < m (cb_prep_kernel, once per call)
+        const double cb = cbm[m];
         const double cm = cmax[m];
         const double tmax = cm * cm + 2.0 * xnorm * cm;
         // table error: fp32 FFMA dot (D roundings) or 3xTF32 tensor-core dot
@@ -567,6 +574,7 @@ __global__ void __launch_bounds__(256, LEAN ? DA_LEAN_MINB : 2) beam_fast_kernel
                 const int i = b + lane;
                 if (i < nqueued) {
                     int rank = 0;
+#pragma unroll 4
                     for (int j = 0; j < nqueued; ++j) rank += lex_less(ev[j], ef[j], qv[t], qf[t]);
                     if (rank < width) { S.lv[rank] = qv[t]; S.lf[rank] = qf[t]; }
                 }
@@ -586,8 +594,10 @@ __global__ void __launch_bounds__(256, LEAN ? DA_LEAN_MINB : 2) beam_fast_kernel
             if (i < width) {
                 const int fi = S.lf[i];
                 int rank = 0;
+#pragma unroll 4
                 for (int j = 0; j < width; ++j) rank += (S.lf[j] < fi);
                 const int parent = k_sh >= 0 ? fi >> k_sh : fi / K, kk = fi - parent * K;
+#pragma unroll 4
                 for (int j = 0; j < m; ++j) nc[rank * M + j] = pc[parent * M + j];
                 nc[rank * M + m] = kk;
                 ns[rank] = S.lv[i];
@@ -658,6 +668,7 @@ int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
     const size_t o_p32 = take(sizeof(float) * pe), o_sq32 = take(sizeof(float) * M * K);
     const size_t o_cmax = take(sizeof(double) * M), o_pabs = take(sizeof(double) * M * M);
+    const size_t o_cbm = take(sizeof(double) * M);
     const size_t o_cw64 = take(sizeof(double) * (size_t)M * K * D);
     char* base = (char*)scratch(7, off, s);
     if (!base) return fail_cuda(cudaErrorMemoryAllocation, "encode_fast scratch");
@@ -665,9 +676,12 @@ int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int
     float* sq32 = (float*)(base + o_sq32);
     double* cmax = (double*)(base + o_cmax);
     double* pabs = (double*)(base + o_pabs);
+    double* cbm = (double*)(base + o_cbm);
     double* cw64 = (double*)(base + o_cw64);
     bound_prep_kernel<<<M * M, 256, 0, s>>>(cw, P, M, K, D, sq, P32, sq32, cmax, pabs, cw64);
     DA_CHECK_LAUNCH("bound_prep_kernel");
+    cb_prep_kernel<<<1, 32, 0, s>>>(pabs, M, cbm);
+    DA_CHECK_LAUNCH("cb_prep_kernel");
 
     if (!x_f32) return fail_arg("encode_fast: float32 input only");
     const bool vec = (K & 255) == 0;
@@ -704,7 +718,7 @@ int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int
                               const double*, const double*, const float*, const double*, const double*, const double*,
                               void*, int, long long, double*, unsigned long long*, int))kf;
         kfn<<<grid, warps * 32, smem, s>>>((const float*)X + c0 * ldx, cn, ldx, D, cw, M, K, L, cap, tab, sq, P, P32,
-                                           cmax, pabs, cw64, cout, code_bytes, ldcodes, eout, stats, tab_tc);
+                                           cmax, cbm, cw64, cout, code_bytes, ldcodes, eout, stats, tab_tc);
         DA_CHECK_LAUNCH("beam_fast_kernel");
     }
     return 0;
