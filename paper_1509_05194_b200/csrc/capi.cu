@@ -313,8 +313,8 @@ int da_encode(const void* X, int x_f32, int64_t n, int64_t ldx, int D, const flo
     if (code_bytes != 1 && code_bytes != 2 && code_bytes != 4) return fail_arg("code_bytes must be 1, 2 or 4");
     if (M < 1 || K < 1 || D < 1) return fail_arg("encode: bad codebook shape");
     // auto (0): the tcgen05 filter where it measured faster on B200 (config B, 1M
-    // vectors: L <= 2 and L >= 24), the fp32 gather filter in between
-    const bool tc_auto = g_encode_mode == 0 && (L <= 2 || L >= 24);
+    // vectors: L = 1 only since the lean gather kernel), the fp32 gather filter otherwise
+    const bool tc_auto = g_encode_mode == 0 && L <= 1;
     if (x_f32 && (g_encode_mode == 3 || tc_auto)) {
         int rc = launch_encode_tc((const float*)X, n, ldx, D, cw, M, K, L, sq, P, codes, code_bytes, ldcodes, err,
                                   g_encode_stats, STREAM(stream));
