@@ -551,32 +551,27 @@ __global__ void __launch_bounds__(256, LEAN ? DA_LEAN_MINB : 2) beam_fast_kernel
             // (value, flat) rank; queue entries are distinct
             double* ev = reinterpret_cast<double*>(S.vbuf);
             int* ef = reinterpret_cast<int*>(ev + QCAP);
-            int qf[QCAP / 32 + 1];
-            double qv[QCAP / 32 + 1];
-            int nmine = 0;
+            // exact values straight into shared memory (no per-lane arrays: they
+            // would live in local memory)
             for (int b = 0; b < nqueued; b += 32) {
                 const int i = b + lane;
                 if (i < nqueued) {
                     const int flat = S.queue[33 + i];
-                    qf[nmine] = flat;
-                    qv[nmine] = exact_value(flat);
-                    ++nmine;
+                    ev[i] = exact_value(flat);
+                    ef[i] = flat;
+                    ++n_exact;
                 }
             }
-            n_exact += nmine;
             __syncwarp();
-            for (int b = 0, t = 0; b < nqueued; b += 32, ++t) {
-                const int i = b + lane;
-                if (i < nqueued) { ev[i] = qv[t]; ef[i] = qf[t]; }
-            }
-            __syncwarp();
-            for (int b = 0, t = 0; b < nqueued; b += 32, ++t) {
+            for (int b = 0; b < nqueued; b += 32) {
                 const int i = b + lane;
                 if (i < nqueued) {
+                    const double mv = ev[i];
+                    const int mf = ef[i];
                     int rank = 0;
 #pragma unroll 4
-                    for (int j = 0; j < nqueued; ++j) rank += lex_less(ev[j], ef[j], qv[t], qf[t]);
-                    if (rank < width) { S.lv[rank] = qv[t]; S.lf[rank] = qf[t]; }
+                    for (int j = 0; j < nqueued; ++j) rank += lex_less(ev[j], ef[j], mv, mf);
+                    if (rank < width) { S.lv[rank] = mv; S.lf[rank] = mf; }
                 }
             }
             cnt = width;
