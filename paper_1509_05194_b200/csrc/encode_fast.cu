@@ -511,12 +511,27 @@ __global__ void __launch_bounds__(256, LEAN ? DA_LEAN_MINB : 2) beam_fast_kernel
                     }
                 }
                 const float sl = (float)ps[l];
+                if (vec) {
+                    const float4 ta = *reinterpret_cast<const float4*>(trow + m * K + kb + 4 * f);
+                    const float4 tb = *reinterpret_cast<const float4*>(trow + m * K + kb + 128 + 4 * f);
+                    const float tk8[8] = {ta.x, ta.y, ta.z, ta.w, tb.x, tb.y, tb.z, tb.w};
+                    unsigned hit = 0;
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int k = kf(q);
-                    if (k < K && (sl + trow[m * K + k]) + 2.f * acc[q] <= limf) {
+                    for (int q = 0; q < 8; ++q) hit |= (unsigned)((sl + tk8[q]) + 2.f * acc[q] <= limf) << q;
+                    while (hit) {
+                        const int q = __ffs(hit) - 1;
+                        hit &= hit - 1;
                         const int slot = atomicAdd(qcount, 1);
-                        if (slot < QCAP) S.queue[33 + slot] = l * K + k;
+                        if (slot < QCAP) S.queue[33 + slot] = l * K + kf(q);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int k = kf(q);
+                        if (k < K && (sl + trow[m * K + k]) + 2.f * acc[q] <= limf) {
+                            const int slot = atomicAdd(qcount, 1);
+                            if (slot < QCAP) S.queue[33 + slot] = l * K + k;
+                        }
                     }
                 }
             }
