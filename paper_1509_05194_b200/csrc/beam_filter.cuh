@@ -96,6 +96,33 @@ __device__ __forceinline__ double exact_dot(const double* __restrict__ x64, cons
     return tot;
 }
 
+// Packed fp32 pair add (FADD2, sm_100): each lane's result is rounded exactly
+// like two scalar adds.
+__device__ __forceinline__ void add2(float& a0, float& a1, float b0, float b1) {
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%0, %1};\n\t"
+        "mov.b64 rb, {%2, %3};\n\t"
+        "add.rn.f32x2 rd, ra, rb;\n\t"
+        "mov.b64 {%0, %1}, rd;\n\t}"
+        : "+f"(a0), "+f"(a1)
+        : "f"(b0), "f"(b1));
+}
+
+// (s + t) + 2 * a for a pair, packed (FADD2 + FFMA2).  2 * a is exact, so the
+// fused form rounds exactly like the separate multiply and add.
+__device__ __forceinline__ void cand2(float& v0, float& v1, float s, float t0, float t1, float a0, float a1) {
+    asm("{\n\t.reg .b64 rs, rt, ra, r2, rd;\n\t"
+        "mov.b64 rs, {%2, %2};\n\t"
+        "mov.b64 rt, {%3, %4};\n\t"
+        "mov.b64 ra, {%5, %6};\n\t"
+        "mov.b64 r2, {%7, %7};\n\t"
+        "add.rn.f32x2 rs, rs, rt;\n\t"
+        "fma.rn.f32x2 rd, ra, r2, rs;\n\t"
+        "mov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(v0), "=f"(v1)
+        : "f"(s), "f"(t0), "f"(t1), "f"(a0), "f"(a1), "f"(2.0f));
+}
+
 // float <-> unsigned key with the same order (for redux.sync.min)
 __device__ __forceinline__ unsigned fkey(float f) {
     const unsigned b = __float_as_uint(f);

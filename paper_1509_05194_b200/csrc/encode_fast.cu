@@ -354,8 +354,8 @@ __global__ void __launch_bounds__(256, LEAN ? DA_LEAN_MINB : 2) beam_fast_kernel
                         if (vec) {
                             const float4 a = __ldg(reinterpret_cast<const float4*>(rp + 4 * lane));
                             const float4 b = __ldg(reinterpret_cast<const float4*>(rp + 128 + 4 * lane));
-                            sh[0] += a.x; sh[1] += a.y; sh[2] += a.z; sh[3] += a.w;
-                            sh[4] += b.x; sh[5] += b.y; sh[6] += b.z; sh[7] += b.w;
+                            add2(sh[0], sh[1], a.x, a.y); add2(sh[2], sh[3], a.z, a.w);
+                            add2(sh[4], sh[5], b.x, b.y); add2(sh[6], sh[7], b.z, b.w);
                         } else {
 #pragma unroll
                             for (int q = 0; q < 8; ++q) sh[q] += (kof(kb, q) < K) ? __ldg(rp + 32 * q + lane) : 0.f;
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(256, LEAN ? DA_LEAN_MINB : 2) beam_fast_kernel
 #pragma unroll
                     for (int g = 0; g < G; ++g)
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) acc[g][q] += vals[g][q];
+                        for (int q = 0; q < 8; q += 2) add2(acc[g][q], acc[g][q + 1], vals[g][q], vals[g][q + 1]);
                 }
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(256, LEAN ? DA_LEAN_MINB : 2) beam_fast_kernel
                     const float sl = (float)ps[l];
                     float vv[8];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) vv[q] = (sl + tk[q]) + 2.f * acc[g][q];
+                    for (int q = 0; q < 8; q += 2) cand2(vv[q], vv[q + 1], sl, tk[q], tk[q + 1], acc[g][q], acc[g][q + 1]);
                     if (vec && !LEAN) {
                         *reinterpret_cast<float4*>(S.vbuf + l * K + kb + 4 * lane) = make_float4(vv[0], vv[1], vv[2], vv[3]);
                         *reinterpret_cast<float4*>(S.vbuf + l * K + kb + 128 + 4 * lane) =
@@ -503,8 +503,8 @@ __global__ void __launch_bounds__(256, LEAN ? DA_LEAN_MINB : 2) beam_fast_kernel
                     if (vec) {
                         const float4 a = __ldg(reinterpret_cast<const float4*>(rp + kb + 4 * f));
                         const float4 b = __ldg(reinterpret_cast<const float4*>(rp + kb + 128 + 4 * f));
-                        acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
-                        acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+                        add2(acc[0], acc[1], a.x, a.y); add2(acc[2], acc[3], a.z, a.w);
+                        add2(acc[4], acc[5], b.x, b.y); add2(acc[6], acc[7], b.z, b.w);
                     } else {
 #pragma unroll
                         for (int q = 0; q < 8; ++q) acc[q] += (kf(q) < K) ? __ldg(rp + kf(q)) : 0.f;
