@@ -199,6 +199,16 @@ def _sharded_update(sums, counts, C, comm):
     return counts_h
 
 
+_FLAGS_H: list = []
+
+
+def _pinned_flags() -> list:
+    """Two page-locked int64[2] flag buffers for the Lloyd loop (kept: pinning is slow)."""
+    if not _FLAGS_H:
+        _FLAGS_H.extend(torch.zeros(2, dtype=torch.int64, pin_memory=True) for _ in range(2))
+    return _FLAGS_H
+
+
 def lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, comm=None):
     """Returns (C f64 (K,D), labels int32 (n,), trace list[float])."""
     with assign_image(Xr, active):
@@ -219,34 +229,60 @@ def _lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, 
     counts = torch.empty(K, dtype=I32, device=dev)
     sums = torch.empty((K, D), dtype=F64, device=dev) if comm is not None else None
     if comm is None:
-        # one host sync per iteration: the assign runs speculatively on the updated
-        # centroids and is redone (after the host reseed) only when a cluster emptied
-        flags = torch.zeros(2, dtype=torch.int64, device=dev)   # [changed rows, empty clusters]
         # Only the active prefix feeds the assignments, so the iterations average the
         # active columns; the remaining columns are averaged once at the end over the
         # labels of the last update (per-column sums: identical bits).  Reseeds write
         # whole rows, as in the reference.
+        #
+        # Iteration i+1 is launched before the host looks at iteration i's flags
+        # (rows changed, clusters emptied), so the device never idles on the
+        # per-iteration sync.  It runs in the other of two centroid buffers and is
+        # dropped when iteration i converged or emptied a cluster (the reseed
+        # changes C_i, so i+1 is recomputed); accepted results are the
+        # reference's, step for step.
+        slots = [(C, torch.empty(K, dtype=I32, device=dev), torch.zeros(2, dtype=torch.int64, device=dev)),
+                 (torch.empty_like(C), torch.empty(K, dtype=I32, device=dev),
+                  torch.zeros(2, dtype=torch.int64, device=dev))]
+        flags_h = _pinned_flags()
+        done_ev = [torch.cuda.Event(), torch.cuda.Event()]
+
+        def launch(C_prev, labels_prev, slot):
+            Cn, cn, fl = slots[slot]
+            if Cn is not C_prev:
+                Cn.copy_(C_prev)                     # empty clusters keep their previous rows
+            native.da_group_sums(P(Xr), n, Xr.stride(0), active, P(labels_prev), K, 0, P(Cn), Cn.stride(0),
+                                 P(cn), stream())
+            fl.zero_()
+            fl[1:2].copy_((cn == 0).sum().view(1))
+            nl, ne = assign(Xr, active, Cn, prev=labels_prev, changed=fl[0:1], xx=xx)
+            flags_h[slot].copy_(fl, non_blocking=True)
+            done_ev[slot].record()
+            return [slot, labels_prev, nl, ne]
+
         gs_labels = None
-        for _ in range(max_iters):
-            native.da_group_sums(P(Xr), n, Xr.stride(0), active, P(labels), K, 0, P(C), C.stride(0), P(counts),
-                                 stream())
-            gs_labels = labels
-            flags.zero_()
-            flags[1:2].copy_((counts == 0).sum().view(1))
-            new_labels, errs_new = assign(Xr, active, C, prev=labels, changed=flags[0:1], xx=xx)
-            fh = flags.cpu().numpy()
+        cur = launch(C, labels, 0) if max_iters > 0 else None
+        while cur is not None:
+            slot, labels_prev, new_labels, errs_new = cur
+            Cn, cn, fl = slots[slot]
+            spec = launch(Cn, new_labels, slot ^ 1) if iters + 1 < max_iters else None
+            done_ev[slot].synchronize()
+            fh = flags_h[slot].numpy().copy()
             if fh[1]:
-                empty = np.flatnonzero(counts.cpu().numpy() == 0)
-                _reseed_single(Xr, errs, empty, C)
-                flags.zero_()
-                new_labels, errs_new = assign(Xr, active, C, prev=labels, changed=flags[0:1], xx=xx)
-                fh = flags.cpu().numpy()
+                spec = None                          # computed from pre-reseed centroids
+                empty = np.flatnonzero(cn.cpu().numpy() == 0)
+                _reseed_single(Xr, errs, empty, Cn)
+                fl.zero_()
+                new_labels, errs_new = assign(Xr, active, Cn, prev=labels_prev, changed=fl[0:1], xx=xx)
+                fh = fl.cpu().numpy()
+            C = Cn
+            gs_labels = labels_prev
             errs = errs_new
             iters += 1
             trace_d[iters:iters + 1] = np_mean(errs, comm)
             labels = new_labels
-            if int(fh[0]) == 0:
+            if int(fh[0]) == 0 or iters >= max_iters:
                 break
+            cur = spec if spec is not None else launch(C, labels, slot ^ 1)
         if gs_labels is not None and active < D:
             native.da_group_sums(P(Xr), n, Xr.stride(0), D, P(gs_labels), K, 0, P(C), C.stride(0), P(counts),
                                  stream())
