@@ -312,9 +312,10 @@ int da_encode(const void* X, int x_f32, int64_t n, int64_t ldx, int D, const flo
     if (L < 1) return fail_arg("beam_width must be >= 1");
     if (code_bytes != 1 && code_bytes != 2 && code_bytes != 4) return fail_arg("code_bytes must be 1, 2 or 4");
     if (M < 1 || K < 1 || D < 1) return fail_arg("encode: bad codebook shape");
-    // auto (0): the tcgen05 filter where it measured faster on B200 (config B, 1M
-    // vectors: L = 1 only since the lean gather kernel), the fp32 gather filter otherwise
-    const bool tc_auto = g_encode_mode == 0 && L <= 1;
+    // auto (0): the fp32 gather filter, which measured faster than the tcgen05
+    // residual-GEMM filter at every beam width on B200 once the two-vector and lean
+    // kernels landed (config B, 1M vectors, L=1: 17.5 vs 20.1 ms); mode 3 forces it
+    const bool tc_auto = false;
     if (x_f32 && (g_encode_mode == 3 || tc_auto)) {
         int rc = launch_encode_tc((const float*)X, n, ldx, D, cw, M, K, L, sq, P, codes, code_bytes, ldcodes, err,
                                   g_encode_stats, STREAM(stream));

@@ -722,6 +722,18 @@ int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int
         }
         void* cout = (char*)codes_out + (size_t)c0 * ldcodes * code_bytes;
         double* eout = err_out ? err_out + c0 : nullptr;
+        // two vectors per warp wins for narrow beams (B200, config B, 1M vectors: L=2
+        // 21.5 vs 27.4 ms, L=6 32.1 vs 37.7), the one-vector lean kernel from L = 8
+        // (L=8 39.0 vs 40.1, L=10 47.0 vs 54.3).  DA_BEAM_PAIR=0/1 forces it off/on.
+        const char* epair = getenv("DA_BEAM_PAIR");
+        const bool pair = epair ? atoi(epair) != 0 : L <= 7;
+        if (pair) {
+            ProfScope ps3("encode_beam_pair", s);
+            const int rc = launch_beam_pair((const float*)X + c0 * ldx, cn, ldx, D, cw, M, K, L, cap, tab, sq, P, P32,
+                                            cmax, cbm, cw64, cout, code_bytes, ldcodes, eout, stats, tab_tc, s);
+            if (rc == 0) continue;
+            if (rc != kNotApplicable) return rc;
+        }
         ProfScope ps2("encode_beam_fast", s);
         const unsigned grid = (unsigned)((cn + warps - 1) / warps);
         auto* kfn = (void (*)(const float*, long long, long long, int, const float*, int, int, int, int, const float*,

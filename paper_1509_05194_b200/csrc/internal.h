@@ -88,6 +88,10 @@ int launch_select_better(long long n, int M, const int32_t* beam_codes, const do
 int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int D, const float* cw, int M, int K,
                        int L, const double* sq, const double* P, void* codes_out, int code_bytes, long long ldcodes,
                        double* err_out, unsigned long long* stats, cudaStream_t s);
+int launch_beam_pair(const float* X, long long n, long long ldx, int D, const float* cw, int M, int K, int L, int cap,
+                     const float* tab, const double* sq, const double* P, const float* P32, const double* cmax,
+                     const double* cbm, const double* cw64, void* codes_out, int code_bytes, long long ldcodes,
+                     double* err_out, unsigned long long* stats, int tab_tc, cudaStream_t s);
 int launch_assign_tc(const void* X, int x_is_f32, long long n, long long ldx, int d, const double* C, long long ldc,
                      int K, const double* cc, const double* xx, int32_t* labels, double* d2, const int32_t* prev,
                      unsigned long long* changed, unsigned long long* stats, cudaStream_t s);
