@@ -10,8 +10,8 @@
 // idle (~15 rechecks and 10 beams per stage at L = 10).
 //
 // Lane mapping: h = lane / 16 selects the vector, hl = lane % 16.  In the
-// gather pass a lane owns 16 of the 256 columns, walked in two 128-column
-// passes: k = p*128 + {0, 64} + 4*hl + {0..3}.
+// gather pass a lane owns 16 of the 256 columns: k = {0, 64, 128, 192} +
+// 4*hl + {0..3} (four 16-byte gathers per cross-table row).
 #include <cstdlib>
 
 #include "beam_filter.cuh"
@@ -205,17 +205,17 @@ __global__ void __launch_bounds__(256, DA_PAIR_MINB) beam_pair_kernel(
             S.roff[l * M + j] = (((long long)j * M + m) * K + pc[l * M + j]) * K;
         }
         __syncwarp();
-        // ---- pass A: both halves walk the same (group, level) structure
+        // ---- pass A: both halves walk the same (group, level) structure; a lane
+        // owns 16 columns k = {0, 64, 128, 192} + 4*hl + {0..3}
         float m1 = __int_as_float(0x7f800000), m2 = m1;
         int i1 = -1;
-#pragma unroll 1
-        for (int p = 0; p < 2; ++p) {
-            const int cbase = p * 128 + 4 * hl;      // + {0, 64} + {0..3}
-            float tk[8];
-            {
-                const float4 a = *reinterpret_cast<const float4*>(trow + m * K + cbase);
-                const float4 b = *reinterpret_cast<const float4*>(trow + m * K + cbase + 64);
-                tk[0] = a.x; tk[1] = a.y; tk[2] = a.z; tk[3] = a.w; tk[4] = b.x; tk[5] = b.y; tk[6] = b.z; tk[7] = b.w;
+        {
+            const int cbase = 4 * hl;
+            float tk[16];
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+                const float4 a = *reinterpret_cast<const float4*>(trow + m * K + cbase + 64 * c4);
+                tk[4 * c4] = a.x; tk[4 * c4 + 1] = a.y; tk[4 * c4 + 2] = a.z; tk[4 * c4 + 3] = a.w;
             }
             auto group = [&](auto Gc, int l0) {
                 constexpr int G = decltype(Gc)::value;
@@ -227,49 +227,54 @@ __global__ void __launch_bounds__(256, DA_PAIR_MINB) beam_pair_kernel(
                 const int glA = nA ? min(m, __ffs(nA) - 1) : min(m, 16);
                 const int glB = nB ? min(m, __ffs(nB) - 1) : min(m, 16);
                 const int gl = min(glA, glB);
-                float acc[G][8];
+                float acc[G][16];
                 {
-                    float sh[8];
+                    float sh[16];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) sh[q] = 0.f;
+                    for (int q = 0; q < 16; ++q) sh[q] = 0.f;
                     for (int j = 0; j < gl; ++j) {
                         const float* rp = P32 + S.roff[l0 * M + j] + cbase;
-                        const float4 a = __ldg(reinterpret_cast<const float4*>(rp));
-                        const float4 b = __ldg(reinterpret_cast<const float4*>(rp + 64));
-                        add2(sh[0], sh[1], a.x, a.y); add2(sh[2], sh[3], a.z, a.w);
-                        add2(sh[4], sh[5], b.x, b.y); add2(sh[6], sh[7], b.z, b.w);
+#pragma unroll
+                        for (int c4 = 0; c4 < 4; ++c4) {
+                            const float4 a = __ldg(reinterpret_cast<const float4*>(rp + 64 * c4));
+                            add2(sh[4 * c4], sh[4 * c4 + 1], a.x, a.y);
+                            add2(sh[4 * c4 + 2], sh[4 * c4 + 3], a.z, a.w);
+                        }
                     }
 #pragma unroll
                     for (int g = 0; g < G; ++g)
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) acc[g][q] = sh[q];
+                        for (int q = 0; q < 16; ++q) acc[g][q] = sh[q];
                 }
                 for (int j = gl; j < m; ++j) {
-                    float4 va[G], vb2[G];
+                    float4 va[G][4];
 #pragma unroll
                     for (int g = 0; g < G; ++g) {
                         const float* rp = P32 + S.roff[(l0 + g) * M + j] + cbase;
-                        va[g] = __ldg(reinterpret_cast<const float4*>(rp));
-                        vb2[g] = __ldg(reinterpret_cast<const float4*>(rp + 64));
+#pragma unroll
+                        for (int c4 = 0; c4 < 4; ++c4) va[g][c4] = __ldg(reinterpret_cast<const float4*>(rp + 64 * c4));
                     }
 #pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        add2(acc[g][0], acc[g][1], va[g].x, va[g].y); add2(acc[g][2], acc[g][3], va[g].z, va[g].w);
-                        add2(acc[g][4], acc[g][5], vb2[g].x, vb2[g].y); add2(acc[g][6], acc[g][7], vb2[g].z, vb2[g].w);
-                    }
+                    for (int g = 0; g < G; ++g)
+#pragma unroll
+                        for (int c4 = 0; c4 < 4; ++c4) {
+                            add2(acc[g][4 * c4], acc[g][4 * c4 + 1], va[g][c4].x, va[g][c4].y);
+                            add2(acc[g][4 * c4 + 2], acc[g][4 * c4 + 3], va[g][c4].z, va[g][c4].w);
+                        }
                 }
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
                     const int l = l0 + g;
                     const float sl = (float)ps[l];
-                    float vv[8];
+                    float vv[16];
 #pragma unroll
-                    for (int q = 0; q < 8; q += 2) cand2(vv[q], vv[q + 1], sl, tk[q], tk[q + 1], acc[g][q], acc[g][q + 1]);
-                    const float bmin = fminf(fminf(fminf(vv[0], vv[1]), fminf(vv[2], vv[3])),
-                                             fminf(fminf(vv[4], vv[5]), fminf(vv[6], vv[7])));
+                    for (int q = 0; q < 16; q += 2) cand2(vv[q], vv[q + 1], sl, tk[q], tk[q + 1], acc[g][q], acc[g][q + 1]);
+                    float bmin = vv[0];
+#pragma unroll
+                    for (int q = 1; q < 16; ++q) bmin = fminf(bmin, vv[q]);
                     if (bmin < m2) {
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) {
+                        for (int q = 0; q < 16; ++q) {
                             const float w = vv[q];
                             i1 = w < m1 ? l * K + cbase + (q >> 2) * 64 + (q & 3) : i1;
                             m2 = fminf(m2, fmaxf(m1, w));
@@ -317,10 +322,10 @@ __global__ void __launch_bounds__(256, DA_PAIR_MINB) beam_pair_kernel(
         const unsigned flagged = __ballot_sync(FULL, multi);
         const float limA = __shfl_sync(FULL, limf, 0), limB = __shfl_sync(FULL, limf, 16);
         if (flagged) {
-            const int per_f = live * 2;      // (beam, pass) items per flagged lane
+            const int per_f = live;          // one item per (flagged lane, beam)
             const int items = __popc(flagged) * per_f;
             for (int t = lane; t < items; t += 32) {
-                const int fi = t / per_f, rem = t - fi * per_f;
+                const int fi = t / per_f, l = t - fi * per_f;
                 const int f = __fns(flagged, 0, fi + 1);   // lane that owns these columns
                 const int fh = f >> 4, fhl = f & 15;
                 const PairSmem T = fh ? SB : SA;
@@ -328,28 +333,30 @@ __global__ void __launch_bounds__(256, DA_PAIR_MINB) beam_pair_kernel(
                 const long long vf = v0 + fh < n ? v0 + fh : v0;
                 const float* ttrow = tab32 + vf * (long long)M * K;
                 const float tlim = fh ? limB : limA;
-                const int l = rem >> 1, p = rem & 1;
-                const int cbase = p * 128 + 4 * fhl;
-                float acc[8];
+                const int cbase = 4 * fhl;
+                float acc[16];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+                for (int q = 0; q < 16; ++q) acc[q] = 0.f;
                 for (int j = 0; j < m; ++j) {
                     const float* rp = P32 + T.roff[l * M + j] + cbase;
-                    const float4 a = __ldg(reinterpret_cast<const float4*>(rp));
-                    const float4 b = __ldg(reinterpret_cast<const float4*>(rp + 64));
-                    add2(acc[0], acc[1], a.x, a.y); add2(acc[2], acc[3], a.z, a.w);
-                    add2(acc[4], acc[5], b.x, b.y); add2(acc[6], acc[7], b.z, b.w);
-                }
-                const float4 ta = *reinterpret_cast<const float4*>(ttrow + m * K + cbase);
-                const float4 tb = *reinterpret_cast<const float4*>(ttrow + m * K + cbase + 64);
-                const float tk8[8] = {ta.x, ta.y, ta.z, ta.w, tb.x, tb.y, tb.z, tb.w};
-                const float sl = (float)tps[l];
-                float vv[8];
 #pragma unroll
-                for (int q = 0; q < 8; q += 2) cand2(vv[q], vv[q + 1], sl, tk8[q], tk8[q + 1], acc[q], acc[q + 1]);
+                    for (int c4 = 0; c4 < 4; ++c4) {
+                        const float4 a = __ldg(reinterpret_cast<const float4*>(rp + 64 * c4));
+                        add2(acc[4 * c4], acc[4 * c4 + 1], a.x, a.y);
+                        add2(acc[4 * c4 + 2], acc[4 * c4 + 3], a.z, a.w);
+                    }
+                }
+                const float sl = (float)tps[l];
                 unsigned hit = 0;
 #pragma unroll
-                for (int q = 0; q < 8; ++q) hit |= (unsigned)(vv[q] <= tlim) << q;
+                for (int c4 = 0; c4 < 4; ++c4) {
+                    const float4 ta = *reinterpret_cast<const float4*>(ttrow + m * K + cbase + 64 * c4);
+                    float vv[4];
+                    cand2(vv[0], vv[1], sl, ta.x, ta.y, acc[4 * c4], acc[4 * c4 + 1]);
+                    cand2(vv[2], vv[3], sl, ta.z, ta.w, acc[4 * c4 + 2], acc[4 * c4 + 3]);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) hit |= (unsigned)(vv[q] <= tlim) << (4 * c4 + q);
+                }
                 while (hit) {
                     const int q = __ffs(hit) - 1;
                     hit &= hit - 1;
