@@ -587,6 +587,27 @@ def _encode_stream(n: int, D: int, row_bytes: int, fill, to_rows, cw: torch.Tens
     return codes
 
 
+_COPY_POOL = None
+
+
+def _parallel_copy(dst: np.ndarray, src: np.ndarray, parts: int = 4) -> None:
+    """Row-split host copy on a small thread pool (numpy releases the GIL): one
+    thread's memcpy into pinned memory is slower than the device encodes."""
+    global _COPY_POOL
+    rows = src.shape[0]
+    if rows < 4096 or parts <= 1:
+        np.copyto(dst, src)
+        return
+    if _COPY_POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _COPY_POOL = ThreadPoolExecutor(max_workers=parts, thread_name_prefix="da-copy")
+    step = (rows + parts - 1) // parts
+    futs = [_COPY_POOL.submit(np.copyto, dst[i:i + step], src[i:i + step]) for i in range(0, rows, step)]
+    for f in futs:
+        f.result()
+
+
 def encode_host(X_np: np.ndarray, cw: torch.Tensor, sq: torch.Tensor, Pt: torch.Tensor, L: int,
                 out_dtype=I32, chunk: int = 131072, name: str = "data") -> torch.Tensor:
     """Beam-encode a host float32 array through _encode_stream.  Non-finite input
@@ -595,7 +616,8 @@ def encode_host(X_np: np.ndarray, cw: torch.Tensor, sq: torch.Tensor, Pt: torch.
     ok = torch.ones((), dtype=torch.bool, device=device())
 
     def fill(slot, r0, rows):
-        np.copyto(slot[: rows * D * 4].view(torch.float32).numpy().reshape(rows, D), X_np[r0:r0 + rows])
+        dst = slot[: rows * D * 4].view(torch.float32).numpy().reshape(rows, D)
+        _parallel_copy(dst, X_np[r0:r0 + rows])
 
     def to_rows(raw, rows, buf):
         x = raw.view(torch.float32).view(rows, D)
