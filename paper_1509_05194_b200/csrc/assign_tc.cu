@@ -537,7 +537,9 @@ constexpr int RC_WARPS = 1;
 // 4- or 8-byte global -> shared copy that bypasses the registers (LDGSTS)
 template <int BYTES>
 __device__ __forceinline__ void cp_async(void* sdst, const void* gsrc) {
-    if (BYTES == 8)
+    if (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+    else if (BYTES == 8)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
     else
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
@@ -554,8 +556,10 @@ __global__ void __launch_bounds__(32 * RC_WARPS) assign_recheck_kernel(
     const double* __restrict__ cc, const double* __restrict__ xx_in, const uint8_t* __restrict__ gcand,
     const uint8_t* __restrict__ gcnt, int32_t* __restrict__ labels, double* __restrict__ d2_out,
     const int32_t* __restrict__ prev, unsigned long long* __restrict__ changed, unsigned long long* __restrict__ stats) {
-    __shared__ TX sx[RC_WARPS][2][32][33];   // the rows' 32-column chunk, double-buffered
-    __shared__ double sc[RC_WARPS][32][33];  // one candidate round's codeword rows
+    // row stride 34 (272 B): 16-byte aligned for the paired copies, and a quarter
+    // warp's 16-byte reads of its 8 rows hit 8 disjoint bank groups
+    __shared__ __align__(16) TX sx[RC_WARPS][2][32][34];   // the rows' 32-column chunk, double-buffered
+    __shared__ __align__(16) double sc[RC_WARPS][32][34];  // one candidate round's codeword rows
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const bool blk = d > (int)BLAS_Q;
@@ -590,10 +594,21 @@ __global__ void __launch_bounds__(32 * RC_WARPS) assign_recheck_kernel(
             block_of(kc, bs, be);
             return min(be, kc + 32);
         };
+        // float64 rows with even strides: 16-byte copies, two rows per instruction
+        const bool wide = sizeof(TX) == 8 && ((ldx | ldc) & 1) == 0 &&
+                          ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(C)) & 15) == 0;
+        const int pc2 = lane & 15, rsub = lane >> 4;
         auto stage_x = [&](int kc, int wd, int buf) {
-            if (lane < wd)
+            if (wide && (wd & 1) == 0) {
+                if (2 * pc2 < wd)
+                    for (int i = 0; i < 16; ++i) {
+                        const int rr = 2 * i + rsub;
+                        if (rr < rows) cp_async<16>(&sx[w][buf][rr][2 * pc2], X + (r0 + rr) * ldx + kc + 2 * pc2);
+                    }
+            } else if (lane < wd) {
                 for (int rr = 0; rr < rows; ++rr)
                     cp_async<sizeof(TX)>(&sx[w][buf][rr][lane], X + (r0 + rr) * ldx + kc + lane);
+            }
             cp_async_commit();
         };
         __syncwarp();
@@ -608,10 +623,20 @@ __global__ void __launch_bounds__(32 * RC_WARPS) assign_recheck_kernel(
                     const int kj = (int)(((j < 4 ? cw2.x : cw2.y) >> (8 * (j & 3))) & 0xFFu);
                     const bool has = j < cnt;
                     const unsigned hm = __ballot_sync(FULL, has);
+                    const bool wchunk = wide && (wd & 1) == 0;
                     __syncwarp();
-                    for (int rr = 0; rr < rows; ++rr) {
-                        const int krr = __shfl_sync(FULL, kj, rr);
-                        if (((hm >> rr) & 1u) && lane < wd) cp_async<8>(&sc[w][rr][lane], C + (long long)krr * ldc + kc + lane);
+                    if (wchunk) {
+                        for (int i = 0; i < 16; ++i) {
+                            const int rr = 2 * i + rsub;
+                            const int krr = __shfl_sync(FULL, kj, rr);
+                            if (((hm >> rr) & 1u) && 2 * pc2 < wd)
+                                cp_async<16>(&sc[w][rr][2 * pc2], C + (long long)krr * ldc + kc + 2 * pc2);
+                        }
+                    } else {
+                        for (int rr = 0; rr < rows; ++rr) {
+                            const int krr = __shfl_sync(FULL, kj, rr);
+                            if (((hm >> rr) & 1u) && lane < wd) cp_async<8>(&sc[w][rr][lane], C + (long long)krr * ldc + kc + lane);
+                        }
                     }
                     cp_async_commit();
                     if (j == 0 && nkc < d) {
@@ -623,7 +648,16 @@ __global__ void __launch_bounds__(32 * RC_WARPS) assign_recheck_kernel(
                     __syncwarp();
                     if (has) {
                         double a = acc[j];
-                        for (int t = 0; t < wd; ++t) a = __fma_rn((double)sx[w][buf][lane][t], sc[w][lane][t], a);
+                        if (wchunk) {
+                            for (int t = 0; t < wd; t += 2) {
+                                const double2 xv = *reinterpret_cast<const double2*>(&sx[w][buf][lane][t]);
+                                const double2 cv = *reinterpret_cast<const double2*>(&sc[w][lane][t]);
+                                a = __fma_rn(xv.x, cv.x, a);
+                                a = __fma_rn(xv.y, cv.y, a);
+                            }
+                        } else {
+                            for (int t = 0; t < wd; ++t) a = __fma_rn((double)sx[w][buf][lane][t], sc[w][lane][t], a);
+                        }
                         acc[j] = a;
                     }
                 }
