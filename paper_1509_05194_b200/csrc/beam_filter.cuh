@@ -123,6 +123,19 @@ __device__ __forceinline__ void cand2(float& v0, float& v1, float s, float t0, f
         : "f"(s), "f"(t0), "f"(t1), "f"(a0), "f"(a1), "f"(2.0f));
 }
 
+// One streamed 16-byte read (the score table row, read once per stage): L2
+// evict-first, so it does not push the cross tables out of L2.
+__device__ __forceinline__ float4 ld_stream_f4(const float* p) {
+    float4 v;
+    asm volatile(
+        "{\n\t.reg .b64 pol;\n\t"
+        "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+        "ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], pol;\n\t}"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+        : "l"(p));
+    return v;
+}
+
 // float <-> unsigned key with the same order (for redux.sync.min)
 __device__ __forceinline__ unsigned fkey(float f) {
     const unsigned b = __float_as_uint(f);

@@ -323,8 +323,8 @@ __global__ void __launch_bounds__(256, LEAN ? DA_LEAN_MINB : 2) beam_fast_kernel
         for (int kb = 0; kb < K; kb += 256) {
             float tk[8];
             if (vec) {
-                const float4 a = *reinterpret_cast<const float4*>(trow + m * K + kb + 4 * lane);
-                const float4 b = *reinterpret_cast<const float4*>(trow + m * K + kb + 128 + 4 * lane);
+                const float4 a = ld_stream_f4(trow + m * K + kb + 4 * lane);
+                const float4 b = ld_stream_f4(trow + m * K + kb + 128 + 4 * lane);
                 tk[0] = a.x; tk[1] = a.y; tk[2] = a.z; tk[3] = a.w; tk[4] = b.x; tk[5] = b.y; tk[6] = b.z; tk[7] = b.w;
             } else {
 #pragma unroll

@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(256, DA_PAIR_MINB) beam_pair_kernel(
             float tk[16];
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4) {
-                const float4 a = *reinterpret_cast<const float4*>(trow + m * K + cbase + 64 * c4);
+                const float4 a = ld_stream_f4(trow + m * K + cbase + 64 * c4);
                 tk[4 * c4] = a.x; tk[4 * c4 + 1] = a.y; tk[4 * c4 + 2] = a.z; tk[4 * c4 + 3] = a.w;
             }
             auto group = [&](auto Gc, int l0) {
