@@ -106,9 +106,14 @@ class ATree:
 def _eps_of(products, U_rows: np.ndarray, depth: int) -> np.ndarray:
     """epsilon = sum_{i<depth} c_i . c_depth over code rows, accumulated from 0
     in i order in float64, stored as float32 (atree.py:150-155)."""
-    acc = np.zeros(U_rows.shape[0])
+    return _eps_cols(products, [U_rows[:, i] for i in range(depth + 1)], depth)
+
+
+def _eps_cols(products, cols, depth: int) -> np.ndarray:
+    """_eps_of on per-depth code columns (1-D arrays, cols[i] = codes at depth i)."""
+    acc = np.zeros(cols[depth].shape[0])
     for i in range(depth):
-        acc = acc + products[i, depth][U_rows[:, i], U_rows[:, depth]]
+        acc = acc + products[i, depth][cols[i], cols[depth]]
     return acc.astype(np.float32)
 
 
@@ -132,7 +137,15 @@ def build_atree(encoded, codebook, cross=None) -> ATree:
     ids = np.arange(n, dtype=i64) if encoded.id_map is None else np.asarray(encoded.id_map, dtype=i64)
     codes = np.asarray(encoded.codes).astype(i64)
     # rows in lexicographic code order (stable), then distinct full codes
-    order = np.lexsort([codes[:, m] for m in range(M - 1, -1, -1)])
+    bits = max(1, int(codebook.k_count - 1).bit_length())
+    if bits * M <= 64:
+        # one packed key (code 0 most significant): a single stable radix sort
+        key = np.zeros(n, dtype=np.uint64)
+        for m in range(M):
+            key = (key << np.uint64(bits)) | codes[:, m].astype(np.uint64)
+        order = np.argsort(key, kind="stable")
+    else:
+        order = np.lexsort([codes[:, m] for m in range(M - 1, -1, -1)])
     S = codes[order]
     ids_sorted = ids[order]
     first = np.ones(n, dtype=bool)
@@ -181,10 +194,12 @@ def build_atree(encoded, codebook, cross=None) -> ATree:
     leaf_ref = np.full(total, -1, dtype=i64)
     leaf_row, leaf_depth = [], []
     n_leaf = 0
+    Uc = np.ascontiguousarray(U.T)          # code columns: 1-D gathers below
     for m, lv in enumerate(levels):
         rows, base = lv["rows"], int(bases[m])
-        code_a[base:base + rows.size] = U[rows, m]
-        eps_a[base:base + rows.size] = _eps_of(products, U[rows], m)
+        cols = [Uc[i][rows] for i in range(m + 1)]
+        code_a[base:base + rows.size] = cols[m]
+        eps_a[base:base + rows.size] = _eps_cols(products, cols, m)
         if m > 0 and rows.size:
             # parent of each node = the position of its depth-(m-1) prefix among the
             # previous level's nodes; children are contiguous in code order
@@ -212,21 +227,27 @@ def build_atree(encoded, codebook, cross=None) -> ATree:
     suffix_hi = suffix_lo + slen
     suffix_code = np.empty(int(slen.sum()), dtype=i32)
     suffix_eps = np.empty(int(slen.sum()), dtype=f32)
+    Lc = [Uc[i][leaf_row] for i in range(M)]   # code columns of the leaves' rows
     for t in range(1, M):
         sel = np.flatnonzero(leaf_depth < t)
         if sel.size:
             at = suffix_lo[sel] + (t - 1 - leaf_depth[sel])
-            urows = U[leaf_row[sel]]
-            suffix_code[at] = urows[:, t]
-            suffix_eps[at] = _eps_of(products, urows, t)
+            cols = [Lc[i][sel] for i in range(t + 1)]
+            suffix_code[at] = cols[t]
+            suffix_eps[at] = _eps_cols(products, cols, t)
 
     # vector ids of each leaf, ascending
     cnt = gend[leaf_row] - gstart[leaf_row]
     ids_lo = np.concatenate([[0], np.cumsum(cnt)[:-1]]).astype(i64)
     ids_hi = ids_lo + cnt
-    leaf_ids = np.empty(int(cnt.sum()), dtype=i64)
-    for j in range(leaf_row.size):
-        leaf_ids[ids_lo[j]:ids_hi[j]] = np.sort(ids_sorted[gstart[leaf_row[j]]:gend[leaf_row[j]]])
+    if encoded.id_map is None:
+        ids_g = ids_sorted            # the stable sort kept row order inside each group
+    else:
+        gid = np.cumsum(first) - 1    # ids ascending inside each group: sort by (group, id)
+        ids_g = ids_sorted[np.lexsort((ids_sorted, gid))]
+    total_ids = int(cnt.sum())
+    pos = np.repeat(gstart[leaf_row] - ids_lo, cnt) + np.arange(total_ids, dtype=i64)
+    leaf_ids = ids_g[pos]
     return ATree(h, M, codebook.k_count, int(counts[0]), code_a, eps_a, child_lo, child_hi, leaf_ref,
                  suffix_lo, suffix_hi, suffix_code, suffix_eps, ids_lo, ids_hi, leaf_ids)
 
