@@ -419,7 +419,7 @@ def main():
     else:
         # beam selection: streams the fp32 score table (M*K*4 B per vector) and the
         # cross-term tables out of L2; algorithmic HBM bytes = table + codes
-        tab_b = M * K * (4 if "fast" in name else 8)
+        tab_b = M * K * (4 if ("fast" in name or "pair" in name) else 8)
         achieved = rows_per_launch * (tab_b + M) / (per_launch_ms / 1e3) / 1e9
         roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": pk.get("hbm_gbs", 6550.4),
                 "unit": "GB/s", "frac": achieved / pk.get("hbm_gbs", 6550.4), "traffic": None,
