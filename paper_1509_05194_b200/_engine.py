@@ -84,6 +84,13 @@ def scalar(t: torch.Tensor) -> float:
 # reductions in numpy order
 
 
+def true_div(t: torch.Tensor, d) -> torch.Tensor:
+    """t / d as an IEEE division (numpy's true_divide).  torch turns a division
+    by a Python scalar into a multiply by its reciprocal, which can differ in
+    the last bit, so the divisor is passed as a tensor."""
+    return t / torch.full_like(t, float(d))
+
+
 def np_mean(a: torch.Tensor, comm=None) -> torch.Tensor:
     """Device scalar equal to numpy's a.mean() (pairwise) on one GPU.
 
@@ -99,7 +106,7 @@ def np_mean(a: torch.Tensor, comm=None) -> torch.Tensor:
     else:
         out.zero_()
     comm.allreduce_(out)
-    return out / float(comm.total(n))
+    return true_div(out, comm.total(n))
 
 
 def row_sqnorms(A: torch.Tensor, d: int) -> torch.Tensor:
@@ -186,17 +193,15 @@ def _reseed_sharded(Xr, errs, empty_idx, C, comm):
     C[torch.from_numpy(np.asarray(empty_idx, dtype=np.int64)).to(C.device)] = all_rows[pick]
 
 
-def _sharded_update(sums, counts, C, comm):
-    """Allreduce per-shard (K, D) sums and K counts; C[filled] = sums / counts.
-    Returns the global counts (numpy int64)."""
-    cnt = counts.to(F64)
-    comm.allreduce_(sums)
-    comm.allreduce_(cnt)
-    counts_h = cnt.cpu().numpy().astype(np.int64)
-    filled = torch.from_numpy(np.flatnonzero(counts_h > 0)).to(C.device)
-    if filled.numel():
-        C[filled] = sums[filled] / cnt[filled].unsqueeze(1)
-    return counts_h
+def _sharded_update(red, K, d, C, comm):
+    """red = [local (K, d) sums | local K counts] in one f64 buffer: one
+    allreduce, then C[filled, :d] = sums / counts (the division of
+    clustering.py:161); empty clusters keep their rows for the reseed.
+    Returns the number of empty clusters as a device scalar."""
+    comm.allreduce_(red)
+    sums, cnt = red[: K * d].view(K, d), red[K * d:]
+    C[:, :d] = torch.where(cnt.unsqueeze(1) > 0, sums / cnt.unsqueeze(1), C[:, :d])
+    return (cnt == 0).sum()
 
 
 _FLAGS_H: list = []
@@ -220,14 +225,12 @@ def _lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, 
     K = C_init.shape[0]
     C = C_init.clone().contiguous()
     dev = Xr.device
-    changed = torch.zeros(1, dtype=torch.int64, device=dev)
     trace_d = torch.empty(max_iters + 1, dtype=F64, device=dev)
     xx = row_sqnorms(Xr, active) if n else None  # fixed for the whole stage
     labels, errs = assign(Xr, active, C, xx=xx)
     trace_d[0:1] = np_mean(errs, comm)
     iters = 0
     counts = torch.empty(K, dtype=I32, device=dev)
-    sums = torch.empty((K, D), dtype=F64, device=dev) if comm is not None else None
     if comm is None:
         # Only the active prefix feeds the assignments, so the iterations average the
         # active columns; the remaining columns are averaged once at the end over the
@@ -288,33 +291,105 @@ def _lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, 
                                  stream())
         trace = trace_d[: iters + 1].cpu().tolist()
         return C, labels, trace
-    for _ in range(max_iters):
-        if comm is None:
-            raise AssertionError("unreachable")
+    return _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm)
+
+
+_FLAGS_SH: list = []
+
+
+def _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm):
+    """The Lloyd loop over row shards (clustering.py:165-203, statistics allreduced).
+
+    Same restructuring as the one-GPU loop: the iterations sum only the active
+    prefix and the remaining columns are summed once at the end; iteration i+1
+    is launched before the host reads iteration i's flags.  Per iteration there
+    are two collectives -- one allreduce of [active sums | counts] and one of
+    [rows changed | error sum] -- and no blocking host sync on the critical
+    path.  Every decision the host takes (converged, reseed) is a function of
+    allreduced values, so all ranks launch the same collective sequence.
+    """
+    n, D = Xr.shape
+    K = C.shape[0]
+    dev = Xr.device
+    da = active
+    ntot = float(comm.total(n))
+    if not _FLAGS_SH:
+        _FLAGS_SH.extend(torch.zeros(3, dtype=F64, pin_memory=True) for _ in range(2))
+    flags_h = _FLAGS_SH
+
+    def new_slot(Cbuf):
+        return (Cbuf, torch.empty(K * da + K, dtype=F64, device=dev), torch.empty(K, dtype=I32, device=dev),
+                torch.zeros(1, dtype=torch.int64, device=dev), torch.zeros(3, dtype=F64, device=dev),
+                torch.cuda.Event())
+
+    slots = [new_slot(C), new_slot(torch.empty_like(C))]
+
+    def stats_(slot, ne):
+        """fl[1:3] = global [rows changed, error sum] of the assign that wrote ne."""
+        _, _, _, chg, fl, _ = slots[slot]
+        if n:
+            native.da_np_sum(P(ne), n, 0, P(fl[2:3]), stream())
         else:
-            if n:
-                native.da_group_sums(P(Xr), n, Xr.stride(0), D, P(labels), K, 1, P(sums), sums.stride(0),
-                                     P(counts), stream())
-            else:
-                sums.zero_()
-                counts.zero_()
-            counts_h = _sharded_update(sums, counts, C, comm)
-        empty = np.flatnonzero(counts_h == 0)
-        if empty.size:
-            if comm is None:
-                _reseed_single(Xr, errs, empty, C)
-            else:
-                _reseed_sharded(Xr, errs, empty, C, comm)
-        changed.zero_()
-        new_labels, errs = assign(Xr, active, C, prev=labels, changed=changed, xx=xx)
+            fl[2:3].zero_()
+        fl[1:2].copy_(chg)
+        comm.allreduce_(fl[1:3])
+
+    def launch(C_prev, labels_prev, slot):
+        Cn, red, cn, chg, fl, ev = slots[slot]
+        sums = red[: K * da].view(K, da)
+        if n:
+            native.da_group_sums(P(Xr), n, Xr.stride(0), da, P(labels_prev), K, 1, P(sums), da, P(cn), stream())
+        else:
+            red.zero_()
+            cn.zero_()
+        red[K * da:].copy_(cn)
+        if Cn is not C_prev:
+            Cn.copy_(C_prev)                         # empty clusters keep their previous rows
+        fl[0:1].copy_(_sharded_update(red, K, da, Cn, comm).view(1))
+        chg.zero_()
+        nl, ne = assign(Xr, active, Cn, prev=labels_prev, changed=chg, xx=xx)
+        stats_(slot, ne)
+        flags_h[slot].copy_(fl, non_blocking=True)
+        ev.record()
+        return [slot, labels_prev, nl, ne]
+
+    iters = 0
+    gs_labels = None
+    cur = launch(C, labels, 0) if max_iters > 0 else None
+    while cur is not None:
+        slot, labels_prev, new_labels, errs_new = cur
+        Cn, red, cn, chg, fl, ev = slots[slot]
+        spec = launch(Cn, new_labels, slot ^ 1) if iters + 1 < max_iters else None
+        ev.synchronize()
+        fh = flags_h[slot].numpy().copy()
+        if fh[0]:
+            spec = None                              # computed from pre-reseed centroids
+            empty = np.flatnonzero(red[K * da:].cpu().numpy() == 0)
+            _reseed_sharded(Xr, errs, empty, Cn, comm)
+            chg.zero_()
+            new_labels, errs_new = assign(Xr, active, Cn, prev=labels_prev, changed=chg, xx=xx)
+            stats_(slot, errs_new)
+            fh[1:3] = fl[1:3].cpu().numpy()
+        C = Cn
+        gs_labels = labels_prev
+        errs = errs_new
         iters += 1
-        trace_d[iters:iters + 1] = np_mean(errs, comm)
-        if comm is not None:
-            comm.allreduce_(changed)
-        stable = int(changed.item()) == 0
+        trace_d[iters] = fh[2] / ntot
         labels = new_labels
-        if stable:
+        if int(fh[1]) == 0 or iters >= max_iters:
             break
+        cur = spec if spec is not None else launch(C, labels, slot ^ 1)
+    if gs_labels is not None and active < D:
+        full = torch.empty(K * D + K, dtype=F64, device=dev)
+        sums, cnt = full[: K * D].view(K, D), full[K * D:]
+        counts = torch.empty(K, dtype=I32, device=dev)
+        if n:
+            native.da_group_sums(P(Xr), n, Xr.stride(0), D, P(gs_labels), K, 1, P(sums), D, P(counts), stream())
+        else:
+            full.zero_()
+            counts.zero_()
+        cnt.copy_(counts)
+        _sharded_update(full, K, D, C, comm)
     trace = trace_d[: iters + 1].cpu().tolist()
     return C, labels, trace
 
@@ -349,6 +424,8 @@ def pca(X: torch.Tensor, comm=None):
     the D x D eigendecomposition runs in LAPACK on the host, like the reference.
     """
     n_local, D = X.shape
+    if comm is not None and comm.world == 1:
+        comm = None  # one shard: the allreduces are identities, keep the one-GPU rounding
     n = comm.total(n_local) if comm is not None else n_local
     if n < 2:
         raise ValueError(f"PCA needs at least 2 vectors, got {n}")
@@ -362,7 +439,7 @@ def pca(X: torch.Tensor, comm=None):
         else:
             mean.zero_()
         comm.allreduce_(mean)
-        mean /= float(n)
+        mean = true_div(mean, n)
     if n > D:
         cov = torch.empty((D, D), dtype=F64, device=X.device)
         if comm is None:
@@ -374,7 +451,7 @@ def pca(X: torch.Tensor, comm=None):
             else:
                 cov.zero_()
             comm.allreduce_(cov)
-            cov /= float(n - 1)
+            cov = true_div(cov, n - 1)
         cov_h = cov.cpu().numpy()
         w, V = np.linalg.eigh(cov_h)
         order = np.argsort(w, kind="stable")[::-1]

@@ -69,7 +69,10 @@ def _update_case(rank, world):
     np.add.at(sums, lab[sl], X[sl])
     counts = np.bincount(lab[sl], minlength=K).astype(np.int32)
     C = torch.full((K, X.shape[1]), -3.0, dtype=torch.float64)
-    cnt = E._sharded_update(torch.from_numpy(sums), torch.from_numpy(counts), C, comm)
+    red = torch.from_numpy(np.concatenate([sums.ravel(), counts.astype(np.float64)]))
+    n_empty = int(E._sharded_update(red, K, X.shape[1], C, comm))
+    cnt = red[K * X.shape[1]:].numpy().astype(np.int64)
+    assert n_empty == int((cnt == 0).sum())
     return cnt.tolist(), C.numpy().tolist(), comm.row_offset, comm.total(sl.stop - sl.start)
 
 

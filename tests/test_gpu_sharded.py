@@ -76,3 +76,62 @@ def test_two_shards_on_one_gpu():
     single = rep.distortions()
     # same algorithm, different float64 summation order across shards
     assert abs(d0[-1] - single[-1]) <= 0.02 * single[-1], (d0[-1], single[-1])
+
+
+@pytest.fixture(scope="module")
+def gloo1():
+    """A one-process gloo group for the world-1 equivalence tests."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    yield
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("K,active,seed", [(8, 3, 0), (64, 5, 1), (200, 2, 2)])
+def test_sharded_lloyd_world1_equals_single(gloo1, K, active, seed):
+    """One shard: the pipelined sharded Lloyd loop (two collectives per
+    iteration, active-prefix sums, speculative next iteration, reseeds) must
+    give the one-GPU loop's centroids, labels and trace bit for bit.  K=200 on
+    clustered data empties clusters, so the reseed path runs."""
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import cases
+    from paper_1509_05194_b200 import _engine as E
+    from paper_1509_05194_b200 import distributed as D
+
+    X = cases.mixture(3000, 9, 6, 0.05, 40 + seed).astype(np.float64)
+    rng = np.random.default_rng(seed)
+    C0 = X[rng.choice(len(X), K, replace=False)].copy()
+    Xd, Cd = E.to_dev(X), E.to_dev(C0)
+    comm = D.Comm().bind_rows(len(X))
+    C1, l1, t1 = E.lloyd(Xd, Cd, active, 30, None)
+    C2, l2, t2 = E.lloyd(Xd, Cd, active, 30, comm)
+    assert torch.equal(C1, C2)
+    assert torch.equal(l1, l2)
+    assert t1 == t2
+
+
+def test_sharded_sweep_world1_equals_single(gloo1):
+    """A full da_sweep through the sharded engine on one shard (PCA, staged
+    Lloyd, beam re-encode) equals the one-GPU sweep bit for bit."""
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import cases
+    import paper_1509_05194_b200 as da
+    from paper_1509_05194_b200 import _engine as E
+    from paper_1509_05194_b200 import distributed as D
+
+    c = cases.train_case()
+    X = E.to_dev(c["X"])
+    cfg = da.TrainConfig(**{**c["config"], "sweeps": 0})
+    cw, codes = E.growth_pass(X, cfg)
+    Pt, sq = E.cross_full(cw)
+    st1 = [cw.clone(), codes.clone(), Pt.clone(), sq.clone()]
+    st2 = [cw.clone(), codes.clone(), Pt.clone(), sq.clone()]
+    cfg1 = da.TrainConfig(**{**c["config"], "sweeps": 1, "rel_tol": 0.0})
+    E.da_sweep(X, *st1, cfg1)
+    D.da_sweep_sharded(X, *st2, cfg1, D.Comm())
+    for a, b in zip(st1, st2):
+        assert torch.equal(a, b)

@@ -1,0 +1,54 @@
+"""Time one anneal pass through the row-sharded (NCCL) engine against the
+single-GPU engine on the same config-B data, and check that at world 1 they
+give the same dictionaries and codes.
+
+usage: python -m torch.distributed.run --nproc-per-node 1 --master-addr 127.0.0.1 \
+           --master-port 29511 tools/bench_anneal_sharded.py [n]
+"""
+import os, sys, time, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import torch.distributed as dist
+import paper_1509_05194_b200 as da
+from paper_1509_05194_b200 import _engine as E, distributed as DD
+import bench
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
+rank = int(os.environ.get("RANK", "0"))
+torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+dist.init_process_group("nccl")
+X = E.to_dev(bench.rank_data(rank, n))
+cfg0 = da.TrainConfig(m_count=8, k_count=256, beam_width=10, sweeps=0, rel_tol=0.0)
+cw, _ = E.growth_pass(X[:100_000].contiguous(), cfg0)
+Pt, sq = E.cross_full(cw)
+codes, _ = E.encode(X, cw, E.einsum_sq(cw), Pt, 10, out_dtype=torch.int32, with_err=False)
+cfg1 = da.TrainConfig(m_count=8, k_count=256, beam_width=10, sweeps=1, rel_tol=0.0)
+comm = DD.Comm()
+
+
+def run(sharded):
+    state = [cw.clone(), codes.clone(), Pt.clone(), sq.clone()]
+    rep = da.TrainReport(config=cfg1)
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    if sharded:
+        DD.da_sweep_sharded(X, *state, cfg1, comm, report=rep)
+    else:
+        E.da_sweep(X, *state, cfg1, report=rep)
+    torch.cuda.synchronize()
+    return time.perf_counter() - t0, state, rep
+
+
+run(True)  # warm-up (scratch growth, NCCL setup)
+ts, ss, rs = run(True)
+t1, s1, r1 = run(False)
+same_cw = bool(torch.equal(ss[0], s1[0]))
+same_codes = bool(torch.equal(ss[1], s1[1]))
+if rank == 0:
+    print(json.dumps({"n": n, "world": dist.get_world_size(), "sharded_s": ts, "single_s": t1,
+                      "same_codewords": same_cw, "same_codes": same_codes,
+                      "sharded_per_dict": [round(s.seconds, 3) for s in rs.steps],
+                      "single_per_dict": [round(s.seconds, 3) for s in r1.steps],
+                      "distortion": [rs.steps[-1].distortion, r1.steps[-1].distortion]}))
+dist.destroy_process_group()

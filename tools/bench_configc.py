@@ -3,7 +3,7 @@ import os, sys, time, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_1509_05194_b200 as da
-from paper_1509_05194_b200 import _engine as E, synthetic
+from paper_1509_05194_b200 import _engine as E, synthetic, _native
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 200_000
 X_h = synthetic.config_c(n=n) if "n" in synthetic.config_c.__code__.co_varnames else synthetic.config_c(n)
 X = E.to_dev(np.ascontiguousarray(X_h, dtype=np.float32))
@@ -17,4 +17,8 @@ for L in (1, 10):
     E.encode(X, cw, sq, Pt, L, out_dtype=torch.uint8, with_err=False); torch.cuda.synchronize()
     t0 = time.perf_counter(); E.encode(X, cw, sq, Pt, L, out_dtype=torch.uint8, with_err=False); torch.cuda.synchronize()
     out[f"L={L} vectors/s"] = n / (time.perf_counter() - t0)
+    _native.prof_enable(True)
+    E.encode(X, cw, sq, Pt, L, out_dtype=torch.uint8, with_err=False); torch.cuda.synchronize()
+    _native.prof_enable(False)
+    out[f"L={L} kernels_ms"] = {k: round(v[1], 3) for k, v in _native.prof_collect().items()}
 print(json.dumps(out))
