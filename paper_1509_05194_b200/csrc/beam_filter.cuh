@@ -55,9 +55,12 @@ __device__ inline FastSmem carve_fast(char* p, int cap, int M, int K, int D, boo
     return s;
 }
 
-// exact x.c (reference order: FMA chain over d, OpenBLAS k-blocks above 384)
+// exact x.c (reference order: FMA chain over d, OpenBLAS k-blocks above 384).
+// Bound by the codeword-row load latency (32 values in flight per lane), not by
+// the FMA chain: interleaving the independent k-block chains with fewer loads in
+// flight per chain measured 2x slower at D=960.
 __device__ __forceinline__ double exact_dot(const double* __restrict__ x64, const double* __restrict__ c, int D,
-                                            const float* __restrict__ c32 = nullptr) {
+                                                const float* __restrict__ c32 = nullptr) {
     double tot = 0.0;
     bool first = true;
     int d = 0;
@@ -98,6 +101,22 @@ __device__ __forceinline__ double exact_dot(const double* __restrict__ x64, cons
 
 // Packed fp32 pair add (FADD2, sm_100): each lane's result is rounded exactly
 // like two scalar adds.
+// Rigorous bound of |t' - t| for one fp32 score-table entry t' = sq32 - 2 x.c,
+// by how the table was computed (`tab`):
+//   0  FFMA dot accumulated sequentially over D (D roundings);
+//   1  3xTF32 tensor-core dot (2^-21 representation + 2^-22 per accumulation
+//      step, 6 steps per 16 of D+1);
+//   c >= 8  FFMA dot in chunks of c terms whose partials are added sequentially
+//      (c + ceil(D/c) roundings: gamma_c + gamma_{D/c} <= gamma_{c + D/c}).
+// The -2 factor and the norm entry double the dot bound (+8 roundings of slack).
+__device__ __forceinline__ double table_err(int tab, int D, double u, double xnorm, double cm) {
+    if (tab == 1)
+        return (2.0 * (6.0 * ((D + 16) / 16) + 7.0) * 2.384185791015625e-07 + 9.5367431640625e-07 + 2.0 * u) *
+               (2.0 * xnorm * cm + cm * cm);
+    const double steps = tab == 0 ? (double)D : (double)(tab + (D + tab - 1) / tab);
+    return (2.0 * steps + 8.0) * u * (xnorm * cm + cm * cm);
+}
+
 __device__ __forceinline__ void add2(float& a0, float& a1, float b0, float b1) {
     asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
         "mov.b64 ra, {%0, %1};\n\t"

@@ -17,6 +17,7 @@
 //      exact (value, flat index) top-width selection.
 // Beam scores are always the exact float64 values, so codes and errors equal
 // the reference's; only the amount of float64 work changes.
+#include <cmath>
 #include <cstdlib>
 #include <type_traits>
 
@@ -30,23 +31,45 @@ namespace da {
 // SGEMM for the approximate score table: T[i, j] = sq32[j] - 2 * sum_k X[i,k] C[j,k]
 namespace {
 constexpr int SG_BM = 128, SG_BN = 128, SG_BK = 8, SG_T = 256;
+
+// FFMA table chunk length: ~sqrt(D) rounded to a multiple of SG_BK (minimises
+// chunk + D/chunk), or 0 (one sequential chain).  DA_SGEMM_CHUNK
+// overrides it (0 = sequential) for A/B runs.
+// Chunking costs registers (one CTA per SM: the D=960 table takes 155 instead
+// of 124 ms per 1M vectors) and pays only where the rechecks it saves are many:
+// wide beams (L=10, D=960: beam 248 -> 191 ms; L=1 loses).
+int sgemm_chunk(int D, int L) {
+    if (const char* e = getenv("DA_SGEMM_CHUNK")) {
+        const int c = atoi(e);
+        return c <= 0 ? 0 : ((c + SG_BK - 1) / SG_BK) * SG_BK;
+    }
+    if (D < 256 || L < 8) return 0;
+    int c = (int)(sqrt((double)D) / SG_BK + 0.5) * SG_BK;
+    return c < SG_BK ? SG_BK : c;
+}
 }
 
+// chunk == 0: one sequential FFMA chain over D per entry.  chunk >= 8 (a multiple
+// of SG_BK): the chain restarts every `chunk` terms and the partials are added
+// into a second accumulator, so the rounding error grows with chunk + D/chunk
+// instead of D (table_err in beam_filter.cuh); at D=960 that is 62 roundings
+// instead of 960, and the exact-recheck queue shrinks with the bound.
+template <bool CHUNKED>
 __global__ void __launch_bounds__(SG_T) sgemm_table_kernel(const float* __restrict__ X, long long n, long long ldx,
                                                            const float* __restrict__ Cw, int N, int D,
                                                            const float* __restrict__ sq32, float* __restrict__ T,
-                                                           long long ldt) {
+                                                           long long ldt, int chunk) {
     __shared__ __align__(16) float As[2][SG_BK][SG_BM];
     __shared__ __align__(16) float Bs[2][SG_BK][SG_BN];
     const int tid = threadIdx.x;
     const int tx = tid & 15, ty = tid >> 4;
     const long long i0 = (long long)blockIdx.y * SG_BM;
     const int j0 = blockIdx.x * SG_BN;
-    float acc[8][8];
+    float acc[8][8], tot[8][8];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+        for (int j = 0; j < 8; ++j) acc[i][j] = tot[i][j] = 0.f;
     // each thread loads 4 A elements and 4 B elements per k-tile
     const int lr = tid >> 1;          // row within tile (0..127)
     const int lk = (tid & 1) * 4;     // k offset 0 or 4
@@ -88,6 +111,15 @@ __global__ void __launch_bounds__(SG_T) sgemm_table_kernel(const float* __restri
 #pragma unroll
                 for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
         }
+        if (CHUNKED && (!more || (k0 + SG_BK) % chunk == 0)) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    tot[i][j] += acc[i][j];
+                    acc[i][j] = 0.f;
+                }
+        }
         if (more) {
             store(buf ^ 1);
             __syncthreads();
@@ -101,7 +133,7 @@ __global__ void __launch_bounds__(SG_T) sgemm_table_kernel(const float* __restri
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             int gc = j0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
-            if (gc < N) T[gr * ldt + gc] = sq32[gc] - 2.f * acc[i][j];
+            if (gc < N) T[gr * ldt + gc] = sq32[gc] - 2.f * (CHUNKED ? tot[i][j] : acc[i][j]);
         }
     }
 }
@@ -296,12 +328,8 @@ __global__ void __launch_bounds__(256, LEAN ? DA_LEAN_MINB : 2) beam_fast_kernel
         const double cb = cbm[m];
         const double cm = cmax[m];
         const double tmax = cm * cm + 2.0 * xnorm * cm;
-        // table error: fp32 FFMA dot (D roundings) or 3xTF32 tensor-core dot
-        // (2^-21 representation + 2^-22 per accumulation step, 6 steps per 16 of D+1,
-        // on |sq| + 2|x.c|), doubled for the -2 factor and the norm entry
-        const double e_t = tab_tc ? (2.0 * (6.0 * ((D + 16) / 16) + 7.0) * 2.384185791015625e-07 +
-                                     9.5367431640625e-07 + 2.0 * u) * (2.0 * xnorm * cm + cm * cm)
-                                  : (2.0 * D + 8.0) * u * (xnorm * cm + cm * cm);
+        // table error by how the table was computed (beam_filter.cuh: table_err)
+        const double e_t = table_err(tab_tc, D, u, xnorm, cm);
         const double e_cross = (m + 2.0) * u * cb;
         const double E = 2.0 * (e_t + 2.0 * e_cross + 4.0 * u * (smax + tmax + 2.0 * cb) + u * smax) + 1e-300;
 
@@ -717,7 +745,15 @@ int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int
         if (!tab_tc) {
             ProfScope ps("encode_table_sgemm", s);
             dim3 grid((N + SG_BN - 1) / SG_BN, (unsigned)((cn + SG_BM - 1) / SG_BM));
-            sgemm_table_kernel<<<grid, SG_T, 0, s>>>((const float*)X + c0 * ldx, cn, ldx, cw, N, D, sq32, tab, N);
+            const int ck = sgemm_chunk(D, L);
+            if (ck) {
+                sgemm_table_kernel<true><<<grid, SG_T, 0, s>>>((const float*)X + c0 * ldx, cn, ldx, cw, N, D, sq32,
+                                                               tab, N, ck);
+                tab_tc = ck;
+            } else {
+                sgemm_table_kernel<false><<<grid, SG_T, 0, s>>>((const float*)X + c0 * ldx, cn, ldx, cw, N, D, sq32,
+                                                                tab, N, 0);
+            }
             DA_CHECK_LAUNCH("sgemm_table_kernel");
         }
         void* cout = (char*)codes_out + (size_t)c0 * ldcodes * code_bytes;

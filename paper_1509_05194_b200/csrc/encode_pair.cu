@@ -194,9 +194,7 @@ __global__ void __launch_bounds__(256, DA_PAIR_MINB) beam_pair_kernel(
         const double cb = cbm[m];
         const double cm = cmax[m];
         const double tmax = cm * cm + 2.0 * xnorm * cm;
-        const double e_t = tab_tc ? (2.0 * (6.0 * ((D + 16) / 16) + 7.0) * 2.384185791015625e-07 +
-                                     9.5367431640625e-07 + 2.0 * u) * (2.0 * xnorm * cm + cm * cm)
-                                  : (2.0 * D + 8.0) * u * (xnorm * cm + cm * cm);
+        const double e_t = table_err(tab_tc, D, u, xnorm, cm);
         const double e_cross = (m + 2.0) * u * cb;
         const double E = 2.0 * (e_t + 2.0 * e_cross + 4.0 * u * (smax + tmax + 2.0 * cb) + u * smax) + 1e-300;
 

@@ -17,8 +17,14 @@ for L in (1, 10):
     E.encode(X, cw, sq, Pt, L, out_dtype=torch.uint8, with_err=False); torch.cuda.synchronize()
     t0 = time.perf_counter(); E.encode(X, cw, sq, Pt, L, out_dtype=torch.uint8, with_err=False); torch.cuda.synchronize()
     out[f"L={L} vectors/s"] = n / (time.perf_counter() - t0)
+    rc = torch.zeros(1, dtype=torch.int64, device="cuda")
+    E.encode_config(0, rc)
     _native.prof_enable(True)
-    E.encode(X, cw, sq, Pt, L, out_dtype=torch.uint8, with_err=False); torch.cuda.synchronize()
+    codes_L = E.encode(X, cw, sq, Pt, L, out_dtype=torch.uint8, with_err=False)[0]; torch.cuda.synchronize()
     _native.prof_enable(False)
+    E.encode_config(0)
+    M, K = cw.shape[0], cw.shape[1]
+    out[f"L={L} recheck_fraction"] = float(rc.item()) / (n * sum(min(L, K ** m) * K for m in range(M)))
+    out[f"L={L} codes_sha"] = __import__("hashlib").sha256(codes_L.cpu().numpy().tobytes()).hexdigest()[:16]
     out[f"L={L} kernels_ms"] = {k: round(v[1], 3) for k, v in _native.prof_collect().items()}
 print(json.dumps(out))
