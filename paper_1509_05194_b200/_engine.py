@@ -116,14 +116,17 @@ def row_sqnorms(A: torch.Tensor, d: int) -> torch.Tensor:
 
 
 def assign(X: torch.Tensor, d: int, C: torch.Tensor, cc: torch.Tensor | None = None,
-           prev: torch.Tensor | None = None, changed: torch.Tensor | None = None, xx: torch.Tensor | None = None):
+           prev: torch.Tensor | None = None, changed: torch.Tensor | None = None, xx: torch.Tensor | None = None,
+           want_d2: bool = True):
     """annq/clustering.py:139-148 on the first d columns; labels int32, d2 f64.
-    `xx` = row_sqnorms(X, d) may be passed to reuse it across Lloyd iterations."""
+    `xx` = row_sqnorms(X, d) may be passed to reuse it across Lloyd iterations.
+    want_d2=False returns (labels, None): rows whose nearest codeword the
+    tensor-core filter decides alone skip the float64 recheck."""
     n, K = X.shape[0], C.shape[0]
     if cc is None:
         cc = row_sqnorms(C, d)
     labels = torch.empty(n, dtype=I32, device=X.device)
-    d2 = torch.empty(n, dtype=F64, device=X.device)
+    d2 = torch.empty(n, dtype=F64, device=X.device) if want_d2 else None
     native.da_assign(P(X), is_f32(X), n, X.stride(0), d, P(C), C.stride(0), K, P(cc), P(xx), P(labels), P(d2),
                      P(prev), P(changed), stream())
     return labels, d2
@@ -214,21 +217,29 @@ def _pinned_flags() -> list:
     return _FLAGS_H
 
 
-def lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, comm=None):
-    """Returns (C f64 (K,D), labels int32 (n,), trace list[float])."""
+def lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, comm=None, want_trace: bool = True):
+    """Returns (C f64 (K,D), labels int32 (n,), trace list[float]).
+
+    want_trace=False (the cool-down inside DA, whose traces nobody reads): the
+    trace is not computed (returned empty) and the assigns write labels only.
+    The per-row errors are then needed only by an empty-cluster reseed
+    (clustering.py:195, ~1% of updates); they are recomputed there against a
+    snapshot of the centroids they belong to.  Centroids and labels are the
+    same bits either way."""
     with assign_image(Xr, active):
-        return _lloyd(Xr, C_init, active, max_iters, comm)
+        return _lloyd(Xr, C_init, active, max_iters, comm, not want_trace)
 
 
-def _lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, comm=None):
+def _lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, comm=None, lazy=False):
     n, D = Xr.shape
     K = C_init.shape[0]
     C = C_init.clone().contiguous()
     dev = Xr.device
     trace_d = torch.empty(max_iters + 1, dtype=F64, device=dev)
     xx = row_sqnorms(Xr, active) if n else None  # fixed for the whole stage
-    labels, errs = assign(Xr, active, C, xx=xx)
-    trace_d[0:1] = np_mean(errs, comm)
+    labels, errs = assign(Xr, active, C, xx=xx, want_d2=not lazy)
+    if not lazy:
+        trace_d[0:1] = np_mean(errs, comm)
     iters = 0
     counts = torch.empty(K, dtype=I32, device=dev)
     if comm is None:
@@ -248,16 +259,19 @@ def _lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, 
                   torch.zeros(2, dtype=torch.int64, device=dev))]
         flags_h = _pinned_flags()
         done_ev = [torch.cuda.Event(), torch.cuda.Event()]
+        snaps = [torch.empty_like(C), torch.empty_like(C)] if lazy else None
 
         def launch(C_prev, labels_prev, slot):
             Cn, cn, fl = slots[slot]
+            if lazy:
+                snaps[slot].copy_(C_prev)            # the centroids the previous assign measured against
             if Cn is not C_prev:
                 Cn.copy_(C_prev)                     # empty clusters keep their previous rows
             native.da_group_sums(P(Xr), n, Xr.stride(0), active, P(labels_prev), K, 0, P(Cn), Cn.stride(0),
                                  P(cn), stream())
             fl.zero_()
             fl[1:2].copy_((cn == 0).sum().view(1))
-            nl, ne = assign(Xr, active, Cn, prev=labels_prev, changed=fl[0:1], xx=xx)
+            nl, ne = assign(Xr, active, Cn, prev=labels_prev, changed=fl[0:1], xx=xx, want_d2=not lazy)
             flags_h[slot].copy_(fl, non_blocking=True)
             done_ev[slot].record()
             return [slot, labels_prev, nl, ne]
@@ -273,15 +287,19 @@ def _lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, 
             if fh[1]:
                 spec = None                          # computed from pre-reseed centroids
                 empty = np.flatnonzero(cn.cpu().numpy() == 0)
+                if lazy:
+                    errs = assign(Xr, active, snaps[slot], xx=xx)[1]
                 _reseed_single(Xr, errs, empty, Cn)
                 fl.zero_()
-                new_labels, errs_new = assign(Xr, active, Cn, prev=labels_prev, changed=fl[0:1], xx=xx)
+                new_labels, errs_new = assign(Xr, active, Cn, prev=labels_prev, changed=fl[0:1], xx=xx,
+                                              want_d2=not lazy)
                 fh = fl.cpu().numpy()
             C = Cn
             gs_labels = labels_prev
             errs = errs_new
             iters += 1
-            trace_d[iters:iters + 1] = np_mean(errs, comm)
+            if not lazy:
+                trace_d[iters:iters + 1] = np_mean(errs, comm)
             labels = new_labels
             if int(fh[0]) == 0 or iters >= max_iters:
                 break
@@ -289,15 +307,15 @@ def _lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, 
         if gs_labels is not None and active < D:
             native.da_group_sums(P(Xr), n, Xr.stride(0), D, P(gs_labels), K, 0, P(C), C.stride(0), P(counts),
                                  stream())
-        trace = trace_d[: iters + 1].cpu().tolist()
+        trace = [] if lazy else trace_d[: iters + 1].cpu().tolist()
         return C, labels, trace
-    return _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm)
+    return _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm, lazy)
 
 
 _FLAGS_SH: list = []
 
 
-def _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm):
+def _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm, lazy=False):
     """The Lloyd loop over row shards (clustering.py:165-203, statistics allreduced).
 
     Same restructuring as the one-GPU loop: the iterations sum only the active
@@ -323,11 +341,13 @@ def _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm):
                 torch.cuda.Event())
 
     slots = [new_slot(C), new_slot(torch.empty_like(C))]
+    snaps = [torch.empty_like(C), torch.empty_like(C)] if lazy else None
 
     def stats_(slot, ne):
-        """fl[1:3] = global [rows changed, error sum] of the assign that wrote ne."""
+        """fl[1:3] = global [rows changed, error sum] of the assign that wrote ne
+        (error sum 0 when the trace is not wanted)."""
         _, _, _, chg, fl, _ = slots[slot]
-        if n:
+        if n and ne is not None:
             native.da_np_sum(P(ne), n, 0, P(fl[2:3]), stream())
         else:
             fl[2:3].zero_()
@@ -336,6 +356,8 @@ def _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm):
 
     def launch(C_prev, labels_prev, slot):
         Cn, red, cn, chg, fl, ev = slots[slot]
+        if lazy:
+            snaps[slot].copy_(C_prev)
         sums = red[: K * da].view(K, da)
         if n:
             native.da_group_sums(P(Xr), n, Xr.stride(0), da, P(labels_prev), K, 1, P(sums), da, P(cn), stream())
@@ -347,7 +369,7 @@ def _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm):
             Cn.copy_(C_prev)                         # empty clusters keep their previous rows
         fl[0:1].copy_(_sharded_update(red, K, da, Cn, comm).view(1))
         chg.zero_()
-        nl, ne = assign(Xr, active, Cn, prev=labels_prev, changed=chg, xx=xx)
+        nl, ne = assign(Xr, active, Cn, prev=labels_prev, changed=chg, xx=xx, want_d2=not lazy)
         stats_(slot, ne)
         flags_h[slot].copy_(fl, non_blocking=True)
         ev.record()
@@ -365,9 +387,11 @@ def _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm):
         if fh[0]:
             spec = None                              # computed from pre-reseed centroids
             empty = np.flatnonzero(red[K * da:].cpu().numpy() == 0)
+            if lazy:
+                errs = assign(Xr, active, snaps[slot], xx=xx)[1] if n else errs
             _reseed_sharded(Xr, errs, empty, Cn, comm)
             chg.zero_()
-            new_labels, errs_new = assign(Xr, active, Cn, prev=labels_prev, changed=chg, xx=xx)
+            new_labels, errs_new = assign(Xr, active, Cn, prev=labels_prev, changed=chg, xx=xx, want_d2=not lazy)
             stats_(slot, errs_new)
             fh[1:3] = fl[1:3].cpu().numpy()
         C = Cn
@@ -390,7 +414,7 @@ def _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm):
             counts.zero_()
         cnt.copy_(counts)
         _sharded_update(full, K, D, C, comm)
-    trace = trace_d[: iters + 1].cpu().tolist()
+    trace = [] if lazy else trace_d[: iters + 1].cpu().tolist()
     return C, labels, trace
 
 
@@ -492,8 +516,9 @@ def rotate(X: torch.Tensor, R: torch.Tensor, mean: torch.Tensor, inverse: bool =
     return out
 
 
-def improved_kmeans(X: torch.Tensor, C0: torch.Tensor, schedule, max_iters: int, comm=None):
-    """Staged k-means in PCA space.  Returns (points f64, labels int32, trace)."""
+def improved_kmeans(X: torch.Tensor, C0: torch.Tensor, schedule, max_iters: int, comm=None, want_trace=True):
+    """Staged k-means in PCA space.  Returns (points f64, labels int32, trace);
+    the trace is the last stage's (empty when want_trace is False)."""
     D = X.shape[1]
     if schedule[-1] != D:
         raise ValueError(f"schedule must end at d={D}, got {schedule}")
@@ -502,7 +527,7 @@ def improved_kmeans(X: torch.Tensor, C0: torch.Tensor, schedule, max_iters: int,
     Cr = rotate(C0, R, mean)
     trace = []
     for dims in schedule:
-        Cr, _, trace = lloyd(Xr, Cr, dims, max_iters, comm)
+        Cr, _, trace = lloyd(Xr, Cr, dims, max_iters, comm, want_trace=want_trace and dims == schedule[-1])
     del Xr
     C = rotate(Cr, R, mean, inverse=True)
     final_labels, final_errs = assign(X, D, C)
@@ -819,7 +844,7 @@ def cool_down(inter: torch.Tensor, C0_f32: torch.Tensor, config, comm=None):
     schedule = dimension_schedule(D, config.schedule_stages)
     n_total = comm.total(inter.shape[0]) if comm is not None else inter.shape[0]
     check_k(n_total, C0_f32.shape[0])
-    pts, labels, _ = improved_kmeans(inter, C0_f32.to(F64), schedule, config.kmeans_iters, comm)
+    pts, labels, _ = improved_kmeans(inter, C0_f32.to(F64), schedule, config.kmeans_iters, comm, want_trace=False)
     return pts.to(F32), labels
 
 

@@ -157,7 +157,7 @@ assign_kernel(const TX* __restrict__ X, long long n, long long ldx, int d,
         long long r = row0 + ty * AS_TM + i;
         if (tx == 0 && r < n) {
             labels[r] = ix;
-            d2_out[r] = v;
+            if (d2_out) d2_out[r] = v;
             if (prev != nullptr && prev[r] != ix) ++local_changed;
         }
     }
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(256) assign_small_kernel(const TX* __restrict_
         const long long r = r0 + t;
         if (r < n) {
             labels[r] = bk[t];
-            d2[r] = best[t];
+            if (d2) d2[r] = best[t];
             if (changed != nullptr && prev != nullptr && prev[r] != bk[t]) ++nchg;
         }
     }

@@ -520,7 +520,7 @@ __global__ void assign_overflow_kernel(const TX* __restrict__ X, long long ldx, 
         }
         if (lane == 0) {
             labels[r] = bk;
-            d2_out[r] = best;
+            if (d2_out) d2_out[r] = best;
             if (changed != nullptr && prev != nullptr && prev[r] != bk) atomicAdd(changed, 1ULL);
         }
     }
@@ -571,8 +571,17 @@ __global__ void __launch_bounds__(32 * RC_WARPS) assign_recheck_kernel(
         if (cnt > TC_CMAX) cnt = 0;   // overflow row: assign_overflow_kernel owns it
         uint2 cw2 = make_uint2(0u, 0u);
         if (cnt) cw2 = *reinterpret_cast<const uint2*>(gcand + r * 8);
+        if (d2_out == nullptr && cnt == 1) {
+            // labels only: a single candidate is the nearest codeword, no float64 work
+            const int k0 = (int)(cw2.x & 0xFFu);
+            labels[r] = k0;
+            if (prev != nullptr && prev[r] != k0) ++nchg;
+            cnt = 0;
+        }
         int maxc = cnt;
         for (int o = 16; o > 0; o >>= 1) maxc = max(maxc, __shfl_xor_sync(FULL, maxc, o));
+        if (maxc == 0) continue;   // warp-uniform: no row of this group needs a recheck
+        const unsigned need = __ballot_sync(FULL, cnt > 0);
         double acc[TC_CMAX], tot[TC_CMAX];
 #pragma unroll
         for (int j = 0; j < TC_CMAX; ++j) { acc[j] = 0.0; tot[j] = 0.0; }
@@ -603,11 +612,12 @@ __global__ void __launch_bounds__(32 * RC_WARPS) assign_recheck_kernel(
                 if (2 * pc2 < wd)
                     for (int i = 0; i < 16; ++i) {
                         const int rr = 2 * i + rsub;
-                        if (rr < rows) cp_async<16>(&sx[w][buf][rr][2 * pc2], X + (r0 + rr) * ldx + kc + 2 * pc2);
+                        if (rr < rows && ((need >> rr) & 1u))
+                            cp_async<16>(&sx[w][buf][rr][2 * pc2], X + (r0 + rr) * ldx + kc + 2 * pc2);
                     }
             } else if (lane < wd) {
                 for (int rr = 0; rr < rows; ++rr)
-                    cp_async<sizeof(TX)>(&sx[w][buf][rr][lane], X + (r0 + rr) * ldx + kc + lane);
+                    if ((need >> rr) & 1u) cp_async<sizeof(TX)>(&sx[w][buf][rr][lane], X + (r0 + rr) * ldx + kc + lane);
             }
             cp_async_commit();
         };
@@ -662,10 +672,6 @@ __global__ void __launch_bounds__(32 * RC_WARPS) assign_recheck_kernel(
                     }
                 }
             }
-            if (maxc == 0 && nkc < d) {
-                __syncwarp();
-                stage_x(nkc, nce - nkc, buf ^ 1);
-            }
             int bs, be;
             block_of(kc, bs, be);
             if (ce == be) {   // end of a BLAS block: fold its chain into the total
@@ -700,7 +706,7 @@ __global__ void __launch_bounds__(32 * RC_WARPS) assign_recheck_kernel(
                 }
             }
             labels[r] = bk;
-            d2_out[r] = best;
+            if (d2_out) d2_out[r] = best;
             nstat += cnt;
             if (prev != nullptr && prev[r] != bk) ++nchg;
         }

@@ -83,3 +83,40 @@ print("ok")
     env = dict(os.environ, DA_ASSIGN_SMALL_D="16")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("n,D,d,K", [(1000, 32, 17, 256), (777, 128, 128, 256), (5000, 128, 49, 200),
+                                     (300, 960, 484, 64), (600, 16, 16, 43), (2000, 12, 2, 8)])
+def test_labels_only_mode(n, D, d, K):
+    """want_d2=False (single-candidate rows skip the float64 recheck) gives the
+    same labels and changed count as the full assign."""
+    rng = np.random.default_rng(n + d + K + 1)
+    X = rng.standard_normal((n, D)) * rng.uniform(0.1, 10, D)
+    C = X[rng.integers(0, n, K)] + 0.01 * rng.standard_normal((K, D))
+    C[1] = C[0]  # an exact tie: the lower index must win in both modes
+    Xd, Cd = E.to_dev(X), E.to_dev(C)
+    prev = torch.from_numpy(rng.integers(0, K, n).astype(np.int32)).cuda()
+    c1 = torch.zeros(1, dtype=torch.int64, device="cuda")
+    c2 = torch.zeros(1, dtype=torch.int64, device="cuda")
+    l1, d1 = E.assign(Xd, d, Cd, prev=prev, changed=c1)
+    l2, d2 = E.assign(Xd, d, Cd, prev=prev, changed=c2, want_d2=False)
+    assert d2 is None
+    assert torch.equal(l1, l2)
+    assert int(c1.item()) == int(c2.item())
+
+
+@pytest.mark.parametrize("K,active,seed", [(256, 6, 0), (256, 40, 1), (64, 128, 2)])
+def test_lloyd_without_trace_same_bits(K, active, seed):
+    """lloyd(want_trace=False) (labels-only assigns, errors recomputed from a
+    centroid snapshot at each reseed) equals the traced loop bit for bit.
+    K=256 on a 12-component mixture empties clusters, so reseeds run."""
+    rng = np.random.default_rng(seed)
+    centres = rng.uniform(0, 50, (12, 128))
+    X = centres[rng.integers(0, 12, 20000)] + rng.standard_normal((20000, 128))
+    C0 = X[rng.choice(len(X), K, replace=False)] + 0.5 * rng.standard_normal((K, 128))
+    Xd, Cd = E.to_dev(X), E.to_dev(C0)
+    C1, l1, t1 = E.lloyd(Xd, Cd, active, 30)
+    C2, l2, t2 = E.lloyd(Xd, Cd, active, 30, want_trace=False)
+    assert t2 == [] and len(t1) >= 2
+    assert torch.equal(C1, C2)
+    assert torch.equal(l1, l2)

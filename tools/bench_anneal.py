@@ -17,7 +17,7 @@ calls = {"lloyd": 0, "iters": 0}
 orig = E.lloyd
 def lloyd_count(*a, **k):
     C, lab, tr = orig(*a, **k)
-    calls["lloyd"] += 1; calls["iters"] += len(tr) - 1
+    calls["lloyd"] += 1; calls["iters"] += max(len(tr) - 1, 0)  # traces are empty inside DA (labels-only Lloyd)
     return C, lab, tr
 E.lloyd = lloyd_count
 cfg1 = da.TrainConfig(m_count=8, k_count=256, beam_width=10, sweeps=1, rel_tol=0.0)
