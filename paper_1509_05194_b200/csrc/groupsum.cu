@@ -222,56 +222,132 @@ __global__ void __launch_bounds__(32 * GS_SW) stable_scatter4_kernel(const int32
 
 // ---- pairwise recursion bookkeeping ----------------------------------------
 
-__device__ long long pw_leaf_count(long long m) {
-    if (m <= 0) return 0;
-    if (m <= 128) return 1;
-    // iterative: count leaves of the recursion
-    long long st[64];
-    int sp = 0;
-    long long c = 0;
-    st[sp++] = m;
-    while (sp) {
-        long long x = st[--sp];
-        if (x <= 128) { ++c; continue; }
-        long long n2 = x / 2; n2 -= n2 % 8;
-        st[sp++] = x - n2;
-        st[sp++] = n2;
+// The walks below keep their recursion stacks in shared memory (one column per
+// thread, conflict-free): in local memory every push and pop was an L1/L2
+// round trip, and these kernels are latency chains (13-55 us per call before).
+// Depth: the right child of x is at most x/2 + 8, so x < 2^31 reaches a leaf
+// (<= 128) within 25 levels.
+constexpr int GS_DMAX = 32;
+constexpr int GS_RING = 8;       // leaves in flight per seg_finish warp
+
+// 8-byte global -> shared copy (LDGSTS), for the seg_finish leaf ring
+__device__ __forceinline__ void gs_cp8(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
+                 "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void gs_cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void gs_cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+constexpr int GS_WALK_T = 128;   // threads per block of the per-codeword walks
+
+__global__ void __launch_bounds__(GS_WALK_T) leaf_count_kernel(const int32_t* __restrict__ counts, int K,
+                                                                int32_t* __restrict__ nleaf) {
+    __shared__ int st[GS_DMAX][GS_WALK_T];
+    const int t = threadIdx.x;
+    const int k = blockIdx.x * GS_WALK_T + t;
+    if (k >= K) return;
+    const int c = counts[k];
+    const int m = c >= 2 ? c - 1 : 0;
+    int leaves = 0;
+    if (m > 0) {
+        int sp = 0;
+        st[sp++][t] = m;
+        while (sp) {
+            const int x = st[--sp][t];
+            if (x <= 128) { ++leaves; continue; }
+            int n2 = x / 2; n2 -= n2 % 8;
+            st[sp++][t] = x - n2;
+            st[sp++][t] = n2;
+        }
     }
-    return c;
+    nleaf[k] = leaves;
 }
 
-__global__ void leaf_count_kernel(const int32_t* __restrict__ counts, int K, int32_t* __restrict__ nleaf) {
-    int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= K) return;
-    int c = counts[k];
-    nleaf[k] = (int32_t)pw_leaf_count(c >= 2 ? c - 1 : 0);
+// leaf_count + exclusive scan + leaf_enum in one single-block launch (K <= 512,
+// one thread per codeword): count the leaves of pairwise(rest), block scan,
+// then enumerate them in left-to-right order.  The second walk needs no offset
+// stack: leaves come out contiguous, so a leaf starts where the previous ended.
+constexpr int GS_PLAN_MAXK = 512;
+__global__ void __launch_bounds__(GS_PLAN_MAXK) leaf_plan_kernel(const int32_t* __restrict__ counts,
+                                                                  const int32_t* __restrict__ seg_start, int K,
+                                                                  int32_t* __restrict__ leaf_base,
+                                                                  int32_t* __restrict__ total_leaves,
+                                                                  int4* __restrict__ leaves) {
+    extern __shared__ int gs_plan_sh[];
+    const int T = blockDim.x;
+    int* scan = gs_plan_sh;   // [T]
+    int* st = scan + T;       // [GS_DMAX][T]
+    const int t = threadIdx.x;
+    const int c = t < K ? counts[t] : 0;
+    const int m = c >= 2 ? c - 1 : 0;
+    int nl = 0;
+    if (m > 0) {
+        int sp = 0;
+        st[(sp++) * T + t] = m;
+        while (sp) {
+            const int x = st[(--sp) * T + t];
+            if (x <= 128) { ++nl; continue; }
+            int n2 = x / 2; n2 -= n2 % 8;
+            st[(sp++) * T + t] = x - n2;
+            st[(sp++) * T + t] = n2;
+        }
+    }
+    scan[t] = nl;
+    __syncthreads();
+    for (int off = 1; off < T; off <<= 1) {
+        const int v = t >= off ? scan[t - off] : 0;
+        __syncthreads();
+        scan[t] += v;
+        __syncthreads();
+    }
+    const int excl = scan[t] - nl;
+    if (t < K) leaf_base[t] = excl;
+    if (t == T - 1) *total_leaves = scan[t];
+    if (m > 0) {
+        int out = excl, lo = 0, sp = 0;
+        const int rest0 = seg_start[t] + 1;
+        st[(sp++) * T + t] = m;
+        while (sp) {
+            const int x = st[(--sp) * T + t];
+            if (x <= 128) {
+                leaves[out++] = make_int4(t, rest0 + lo, x, 0);
+                lo += x;
+                continue;
+            }
+            int n2 = x / 2; n2 -= n2 % 8;
+            st[(sp++) * T + t] = x - n2;   // right first, so the left subtree is emitted first
+            st[(sp++) * T + t] = n2;
+        }
+    }
 }
 
 // Per codeword: enumerate the leaves of pairwise(rest) in left-to-right order.
-__global__ void leaf_enum_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ seg_start,
-                                 const int32_t* __restrict__ leaf_base, int K,
-                                 int4* __restrict__ leaves) {
-    int k = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(GS_WALK_T) leaf_enum_kernel(const int32_t* __restrict__ counts,
+                                                               const int32_t* __restrict__ seg_start,
+                                                               const int32_t* __restrict__ leaf_base, int K,
+                                                               int4* __restrict__ leaves) {
+    __shared__ int st_lo[GS_DMAX][GS_WALK_T];
+    __shared__ int st_n[GS_DMAX][GS_WALK_T];
+    const int t = threadIdx.x;
+    const int k = blockIdx.x * GS_WALK_T + t;
     if (k >= K) return;
-    int c = counts[k];
+    const int c = counts[k];
     if (c < 2) return;
-    long long m = c - 1;
     int out = leaf_base[k];
     const int rest0 = seg_start[k] + 1;
-    long long st_lo[64], st_n[64];
     int sp = 0;
-    st_lo[sp] = 0; st_n[sp] = m; ++sp;
+    st_lo[sp][t] = 0; st_n[sp][t] = c - 1; ++sp;
     while (sp) {
         --sp;
-        long long lo = st_lo[sp], x = st_n[sp];
+        const int lo = st_lo[sp][t], x = st_n[sp][t];
         if (x <= 128) {
-            leaves[out++] = make_int4(k, rest0 + (int)lo, (int)x, 0);
+            leaves[out++] = make_int4(k, rest0 + lo, x, 0);
             continue;
         }
-        long long n2 = x / 2; n2 -= n2 % 8;
+        int n2 = x / 2; n2 -= n2 % 8;
         // push right first so the left leaf is emitted first
-        st_lo[sp] = lo + n2; st_n[sp] = x - n2; ++sp;
-        st_lo[sp] = lo; st_n[sp] = n2; ++sp;
+        st_lo[sp][t] = lo + n2; st_n[sp][t] = x - n2; ++sp;
+        st_lo[sp][t] = lo; st_n[sp][t] = n2; ++sp;
     }
 }
 
@@ -416,16 +492,28 @@ __global__ void __launch_bounds__(256) leaf_sum_narrow_kernel(const double* __re
     if (c1 < D) leaf_sums[leaf * D + c1] = res[1];
 }
 
-// One warp per (codeword, column chunk): fold leaves up the recursion tree,
-// prepend the first row, divide by the count.  mode 0 = write means into the
-// filled rows of C (empties untouched); mode 1 = write raw sums (all rows).
-__global__ void seg_finish_kernel(const double* __restrict__ X, long long ldx, int D,
-                                  const int32_t* __restrict__ order, const int32_t* __restrict__ counts,
-                                  const int32_t* __restrict__ seg_start, const int32_t* __restrict__ leaf_base,
-                                  const double* __restrict__ leaf_sums, int K, int n_chunks, int mode,
-                                  double* __restrict__ out, long long ldo) {
+// One warp (one block) per (codeword, column chunk): fold leaves up the
+// recursion tree, prepend the first row, divide by the count.  mode 0 = write
+// means into the filled rows of C (empties untouched); mode 1 = write raw sums
+// (all rows).  The walk's shape (sizes, states) is warp-uniform and lives in
+// shared memory, written by lane 0; each lane's pending left sums live in its
+// own shared column.  Leaves are consumed in order, so their sums stream
+// through a GS_RING-deep cp.async ring (each lane copies and reads only its
+// own columns: no warp barrier needed for the ring).
+__global__ void __launch_bounds__(32) seg_finish_kernel(const double* __restrict__ X, long long ldx, int D,
+                                                        const int32_t* __restrict__ order,
+                                                        const int32_t* __restrict__ counts,
+                                                        const int32_t* __restrict__ seg_start,
+                                                        const int32_t* __restrict__ leaf_base,
+                                                        const int32_t* __restrict__ n_leaves_total,
+                                                        const double* __restrict__ leaf_sums, int K, int n_chunks,
+                                                        int mode, double* __restrict__ out, long long ldo) {
+    __shared__ int s_n[GS_DMAX + 1];
+    __shared__ int s_state[GS_DMAX + 1];
+    __shared__ double s_left[GS_DMAX][4][32];
+    __shared__ double s_ring[GS_RING][4][32];
     const int lane = threadIdx.x & 31;
-    const long long task = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const long long task = blockIdx.x;
     if (task >= (long long)K * n_chunks) return;
     const int k = (int)(task / n_chunks);
     const int chunk = (int)(task % n_chunks);
@@ -447,47 +535,71 @@ __global__ void seg_finish_kernel(const double* __restrict__ X, long long ldx, i
         tot[q] = (col < D) ? X[first * ldx + col] : 0.0;
     }
     if (c >= 2) {
-        const long long m = c - 1;
-        // post-order walk; all lanes follow the same shape
-        long long st_n[64];
-        int st_state[64];
-        double st_left[64][4];
-        int sp = 0;
-        st_n[0] = m; st_state[0] = 0;
-        long long leaf = leaf_base[k];
-        double ret[4] = {0.0, 0.0, 0.0, 0.0};
-        while (sp >= 0) {
-            long long x = st_n[sp];
-            if (x <= 128) {
+        const long long lf0 = leaf_base[k];
+        const long long nk = (k + 1 < K ? (long long)leaf_base[k + 1] : (long long)*n_leaves_total) - lf0;
+        auto issue = [&](long long j) {
+            if (j < nk) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    int col = chunk * GS_COLS + lane + 32 * q;
-                    ret[q] = (col < D) ? leaf_sums[leaf * D + col] : 0.0;
+                    const int col = chunk * GS_COLS + lane + 32 * q;
+                    if (col < D) gs_cp8(&s_ring[j % GS_RING][q][lane], leaf_sums + (lf0 + j) * D + col);
                 }
+            }
+            gs_cp_commit();   // one group per leaf, empty past the end: the wait count stays uniform
+        };
+#pragma unroll
+        for (int j = 0; j < GS_RING; ++j) issue(j);
+        long long leaf = 0;
+        // post-order walk; all lanes follow the same shape
+        int sp = 0;
+        if (lane == 0) { s_n[0] = c - 1; s_state[0] = 0; }
+        __syncwarp();
+        double ret[4] = {0.0, 0.0, 0.0, 0.0};
+        while (sp >= 0) {
+            const int x = s_n[sp];
+            if (x <= 128) {
+                gs_cp_wait<GS_RING - 1>();
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int col = chunk * GS_COLS + lane + 32 * q;
+                    ret[q] = col < D ? s_ring[leaf % GS_RING][q][lane] : 0.0;
+                }
+                issue(leaf + GS_RING);
                 ++leaf;
                 --sp;
                 while (sp >= 0) {
-                    if (st_state[sp] == 1) {
+                    if (s_state[sp] == 1) {
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) st_left[sp][q] = ret[q];
-                        st_state[sp] = 2;
-                        long long n2 = st_n[sp] / 2; n2 -= n2 % 8;
+                        for (int q = 0; q < 4; ++q) s_left[sp][q][lane] = ret[q];
+                        __syncwarp();
+                        if (lane == 0) {
+                            int n2 = s_n[sp] / 2; n2 -= n2 % 8;
+                            s_state[sp] = 2;
+                            s_n[sp + 1] = s_n[sp] - n2;
+                            s_state[sp + 1] = 0;
+                        }
+                        __syncwarp();
                         ++sp;
-                        st_n[sp] = st_n[sp - 1] - n2; st_state[sp] = 0;
                         break;
                     } else {
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) ret[q] = dadd(st_left[sp][q], ret[q]);
+                        for (int q = 0; q < 4; ++q) ret[q] = dadd(s_left[sp][q][lane], ret[q]);
                         --sp;
                     }
                 }
                 continue;
             }
-            long long n2 = x / 2; n2 -= n2 % 8;
-            st_state[sp] = 1;
+            __syncwarp();
+            if (lane == 0) {
+                int n2 = x / 2; n2 -= n2 % 8;
+                s_state[sp] = 1;
+                s_n[sp + 1] = n2;
+                s_state[sp + 1] = 0;
+            }
+            __syncwarp();
             ++sp;
-            st_n[sp] = n2; st_state[sp] = 0;
         }
+        gs_cp_wait<0>();
 #pragma unroll
         for (int q = 0; q < 4; ++q) tot[q] = dadd(tot[q], ret[q]);
     }
@@ -548,12 +660,22 @@ int launch_group_sums(const double* X, long long n, long long ldx, int D, const 
         stable_scatter_kernel<<<T, 32, sh, s>>>(labels, n, K, T, hist, order);
         DA_CHECK_LAUNCH("stable_scatter_kernel");
     }
-    leaf_count_kernel<<<grid_for(K, 256), 256, 0, s>>>(counts, K, nleaf);
-    DA_CHECK_LAUNCH("leaf_count_kernel");
-    exclusive_scan_kernel<<<1, 1024, 0, s>>>(nleaf, K, total + 1);
-    DA_CHECK_LAUNCH("exclusive_scan_kernel(leaves)");
-    leaf_enum_kernel<<<grid_for(K, 128), 128, 0, s>>>(counts, seg, nleaf, K, leaves);
-    DA_CHECK_LAUNCH("leaf_enum_kernel");
+    if (K <= GS_PLAN_MAXK) {
+        int T = 32;
+        while (T < K) T <<= 1;
+        const size_t psh = sizeof(int) * (size_t)T * (GS_DMAX + 1);
+        if (psh > 48 * 1024)
+            DA_CUDA(cudaFuncSetAttribute(leaf_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psh));
+        leaf_plan_kernel<<<1, T, psh, s>>>(counts, seg, K, nleaf, total + 1, leaves);
+        DA_CHECK_LAUNCH("leaf_plan_kernel");
+    } else {
+        leaf_count_kernel<<<grid_for(K, GS_WALK_T), GS_WALK_T, 0, s>>>(counts, K, nleaf);
+        DA_CHECK_LAUNCH("leaf_count_kernel");
+        exclusive_scan_kernel<<<1, 1024, 0, s>>>(nleaf, K, total + 1);
+        DA_CHECK_LAUNCH("exclusive_scan_kernel(leaves)");
+        leaf_enum_kernel<<<grid_for(K, GS_WALK_T), GS_WALK_T, 0, s>>>(counts, seg, nleaf, K, leaves);
+        DA_CHECK_LAUNCH("leaf_enum_kernel");
+    }
     {
         long long tasks = max_leaves * n_chunks;
         ProfScope ps3("group_sums_leaf", s);
@@ -570,8 +692,8 @@ int launch_group_sums(const double* X, long long n, long long ldx, int D, const 
     }
     {
         long long tasks = (long long)K * n_chunks;
-        seg_finish_kernel<<<grid_for(tasks, 4), 128, 0, s>>>(X, ldx, D, order, counts, seg, nleaf, lsum, K,
-                                                            n_chunks, mode, out, ldo);
+        seg_finish_kernel<<<(unsigned)tasks, 32, 0, s>>>(X, ldx, D, order, counts, seg, nleaf, total + 1, lsum, K,
+                                                         n_chunks, mode, out, ldo);
         DA_CHECK_LAUNCH("seg_finish_kernel");
     }
     return 0;

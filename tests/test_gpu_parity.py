@@ -13,6 +13,7 @@ dgemv/ddot, whose order is not emulated) are held to 1e-12 relative."""
 
 import numpy as np
 import pytest
+import torch
 
 import cases
 import paper_1509_05194_b200 as da
@@ -281,3 +282,27 @@ def test_config_c_subsample(golden):
                               Xe[bad].astype(np.float64), 10)
         assert (gaps < 1e-6).all(), (bad, gaps)
     np.testing.assert_array_equal(enc.codes, g["enc_codes"])
+
+
+@pytest.mark.parametrize("n,k,D", [(50000, 300, 5), (40000, 700, 3), (3000, 512, 130), (200000, 4, 2)])
+def test_group_means_many_labels_and_big_segments(n, k, D):
+    """Group means against the oracle's reduceat restatement for label counts
+    on both sides of the one-block leaf plan (K <= 512 fused, larger K three
+    kernels) and for segments deep in the pairwise recursion (n/k = 50000)."""
+    from oracle import da_oracle as O
+
+    rng = np.random.default_rng(n + k)
+    X = rng.standard_normal((n, D)) * 10.0 ** rng.uniform(-2, 2, (n, D))
+    lab = rng.integers(0, k, n)
+    lab[lab == 3] = 2  # an empty label
+    Xd = E.to_dev(X)
+    labd = E.to_dev(lab.astype(np.int32))
+    out = torch.full((k, D), -7.0, dtype=torch.float64, device="cuda")
+    counts = torch.empty(k, dtype=torch.int32, device="cuda")
+    E.native.da_group_sums(E.P(Xd), n, Xd.stride(0), D, E.P(labd), k, 0, E.P(out), D, E.P(counts), E.stream())
+    means, cnt = O.segment_means(X, lab, k)
+    np.testing.assert_array_equal(counts.cpu().numpy(), cnt)
+    got = out.cpu().numpy()
+    filled = cnt > 0
+    np.testing.assert_array_equal(got[filled], means[filled])
+    assert (got[~filled] == -7.0).all()
