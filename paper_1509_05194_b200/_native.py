@@ -12,7 +12,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libda_b200.so")
+# DA_LIB_PATH: load another in-tree build of the same library (A/B timing runs)
+LIB_PATH = os.environ.get("DA_LIB_PATH") or os.path.join(_HERE, "libda_b200.so")
 
 _lock = threading.Lock()
 _lib = None

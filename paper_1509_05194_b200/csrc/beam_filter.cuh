@@ -103,18 +103,17 @@ __device__ __forceinline__ double exact_dot(const double* __restrict__ x64, cons
 // like two scalar adds.
 // Rigorous bound of |t' - t| for one fp32 score-table entry t' = sq32 - 2 x.c,
 // by how the table was computed (`tab`):
-//   0  FFMA dot accumulated sequentially over D (D roundings);
-//   1  3xTF32 tensor-core dot (2^-21 representation + 2^-22 per accumulation
-//      step, 6 steps per 16 of D+1);
-//   c >= 8  FFMA dot in chunks of c terms whose partials are added sequentially
-//      (c + ceil(D/c) roundings: gamma_c + gamma_{D/c} <= gamma_{c + D/c}).
+//   0   FFMA dot accumulated sequentially over D (D roundings);
+//   1   3xTF32 tensor-core dot (2^-21 representation + 2^-22 per accumulation
+//       step, 6 steps per 16 of D+1);
+//   -s  FFMA dot in chunks whose partials are added sequentially, s = chunk +
+//       ceil(D/chunk) roundings (gamma_c + gamma_{D/c} <= gamma_{c + D/c}),
+//       computed on the host: the kernels only select, no division.
 // The -2 factor and the norm entry double the dot bound (+8 roundings of slack).
 __device__ __forceinline__ double table_err(int tab, int D, double u, double xnorm, double cm) {
-    if (tab == 1)
-        return (2.0 * (6.0 * ((D + 16) / 16) + 7.0) * 2.384185791015625e-07 + 9.5367431640625e-07 + 2.0 * u) *
-               (2.0 * xnorm * cm + cm * cm);
-    const double steps = tab == 0 ? (double)D : (double)(tab + (D + tab - 1) / tab);
-    return (2.0 * steps + 8.0) * u * (xnorm * cm + cm * cm);
+    return tab == 1 ? (2.0 * (6.0 * ((D + 16) / 16) + 7.0) * 2.384185791015625e-07 + 9.5367431640625e-07 + 2.0 * u) *
+                          (2.0 * xnorm * cm + cm * cm)
+                    : (2.0 * (tab < 0 ? (double)(-tab) : (double)D) + 8.0) * u * (xnorm * cm + cm * cm);
 }
 
 __device__ __forceinline__ void add2(float& a0, float& a1, float b0, float b1) {

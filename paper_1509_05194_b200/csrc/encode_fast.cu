@@ -749,7 +749,7 @@ int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int
             if (ck) {
                 sgemm_table_kernel<true><<<grid, SG_T, 0, s>>>((const float*)X + c0 * ldx, cn, ldx, cw, N, D, sq32,
                                                                tab, N, ck);
-                tab_tc = ck;
+                tab_tc = -(ck + (D + ck - 1) / ck);   // rounding steps (table_err)
             } else {
                 sgemm_table_kernel<false><<<grid, SG_T, 0, s>>>((const float*)X + c0 * ldx, cn, ldx, cw, N, D, sq32,
                                                                 tab, N, 0);
