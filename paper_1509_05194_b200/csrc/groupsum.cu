@@ -16,6 +16,8 @@
 //   3. one warp per (codeword, column chunk) folds the leaf sums back up the
 //      same recursion, adds the first row, and divides by the count.
 // The result is deterministic (no float atomics) and equal to the reference.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -424,72 +426,83 @@ __global__ void __launch_bounds__(256, 2) leaf_sum_kernel(const double* __restri
         if (cols[q] < D) leaf_sums[leaf * D + cols[q]] = res[q];
 }
 
-// Narrow rows (D <= 32): a warp serves 32 / ceil(D/2) leaves at once, each lane
-// owning two columns of one leaf (one 16-B load per row), same per-column order.
+// Rows up to D = 128 (DA_GS_NARROW_MAX; wider rows use leaf_sum_kernel): one
+// warp per (leaf, 8-column chunk).  The leaf rule's
+// 8 interleaved accumulators are independent chains, so each gets its own
+// lane: lane = 4*j + p owns accumulator j (rows j, j+8, ... of the leaf) for
+// the column pair p.  A lane first loads its <= 16 row ids, then its <= 16
+// rows (all independent: the whole leaf is in flight at once instead of one
+// 8-row batch per round trip), then runs its chain in row order.  Lane j = 0
+// gathers the 8 accumulators with shuffles, combines them in numpy's
+// ((a0+a1)+(a2+a3))+((a4+a5)+(a6+a7)) order and adds the n % 8 tail rows in
+// sequence: the same per-column operations as the one-lane-per-leaf loop.
+constexpr int GS_NARROW_ROWS = 16;   // rows per accumulator chain of a <= 128-row leaf
 __global__ void __launch_bounds__(256) leaf_sum_narrow_kernel(const double* __restrict__ X, long long ldx, int D,
                                                               const int32_t* __restrict__ order,
                                                               const int4* __restrict__ leaves,
                                                               const int32_t* __restrict__ n_leaves_total,
                                                               double* __restrict__ leaf_sums) {
     const int lane = threadIdx.x & 31;
-    const int lpl = (D + 1) >> 1;              // lanes per leaf
-    const int per_warp = 32 / lpl;
-    const long long warp_id = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int g = lane / lpl, c = lane % lpl;
-    const long long leaf = warp_id * per_warp + g;
-    if (g >= per_warp || leaf >= (long long)(*n_leaves_total)) return;
+    const int n_chunks = (D + 7) >> 3;
+    const long long task = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (task >= (long long)(*n_leaves_total) * n_chunks) return;
+    const long long leaf = task / n_chunks;
+    const int chunk = (int)(task - leaf * n_chunks);
+    const int j = lane >> 2, p = lane & 3;
+    const int c0 = chunk * 8 + 2 * p, c1 = c0 + 1;
     const int4 L = leaves[leaf];
     const int start = L.y, n = L.z;
-    const int c0 = 2 * c, c1 = 2 * c + 1;
     const bool vec = ((ldx & 1) == 0) && (c1 < D);
-    auto load_row = [&](long long r, double* out2) {
-        const double* p = X + r * ldx;
+    auto load_row = [&](long long r, double& v0, double& v1) {
+        const double* q = X + r * ldx;
         if (vec) {
-            const double2 a = *reinterpret_cast<const double2*>(p + c0);
-            out2[0] = a.x; out2[1] = a.y;
+            const double2 a = *reinterpret_cast<const double2*>(q + c0);
+            v0 = a.x; v1 = a.y;
         } else {
-            out2[0] = c0 < D ? p[c0] : 0.0;
-            out2[1] = c1 < D ? p[c1] : 0.0;
+            v0 = c0 < D ? q[c0] : 0.0;
+            v1 = c1 < D ? q[c1] : 0.0;
         }
     };
-    double res[2];
-    if (n < 8) {
-        res[0] = res[1] = 0.0;
-        for (int i = 0; i < n; ++i) {
-            double v[2];
-            load_row(order[start + i], v);
-            res[0] = dadd(res[0], v[0]);
-            res[1] = dadd(res[1], v[1]);
+    double r0 = 0.0, r1 = 0.0;
+    const int stop = n >= 8 ? n - (n % 8) : 0;
+    if (n >= 8) {
+        const int cnt = (stop - j + 7) >> 3;   // rows j, j+8, ... < stop (>= 1)
+        int ids[GS_NARROW_ROWS];
+#pragma unroll
+        for (int t = 0; t < GS_NARROW_ROWS; ++t) ids[t] = t < cnt ? order[start + j + 8 * t] : 0;
+        double v0[GS_NARROW_ROWS], v1[GS_NARROW_ROWS];
+#pragma unroll
+        for (int t = 0; t < GS_NARROW_ROWS; ++t) {
+            if (t < cnt) load_row(ids[t], v0[t], v1[t]);
+            else v0[t] = v1[t] = 0.0;
         }
-    } else {
-        double acc[8][2];
+        double a0 = v0[0], a1 = v1[0];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) load_row(order[start + j], acc[j]);
-        int i = 8;
-        const int stop = n - (n % 8);
-        for (; i < stop; i += 8) {
-            double v[8][2];
+        for (int t = 1; t < GS_NARROW_ROWS; ++t)
+            if (t < cnt) { a0 = dadd(a0, v0[t]); a1 = dadd(a1, v1[t]); }
+        double g0[8], g1[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) load_row(order[start + i + j], v[j]);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                acc[j][0] = dadd(acc[j][0], v[j][0]);
-                acc[j][1] = dadd(acc[j][1], v[j][1]);
-            }
+        for (int q = 0; q < 8; ++q) {
+            g0[q] = __shfl_sync(0xffffffffu, a0, 4 * q + p);
+            g1[q] = __shfl_sync(0xffffffffu, a1, 4 * q + p);
         }
-#pragma unroll
-        for (int q = 0; q < 2; ++q)
-            res[q] = dadd(dadd(dadd(acc[0][q], acc[1][q]), dadd(acc[2][q], acc[3][q])),
-                          dadd(dadd(acc[4][q], acc[5][q]), dadd(acc[6][q], acc[7][q])));
-        for (; i < n; ++i) {
-            double v[2];
-            load_row(order[start + i], v);
-            res[0] = dadd(res[0], v[0]);
-            res[1] = dadd(res[1], v[1]);
-        }
+        r0 = dadd(dadd(dadd(g0[0], g0[1]), dadd(g0[2], g0[3])), dadd(dadd(g0[4], g0[5]), dadd(g0[6], g0[7])));
+        r1 = dadd(dadd(dadd(g1[0], g1[1]), dadd(g1[2], g1[3])), dadd(dadd(g1[4], g1[5]), dadd(g1[6], g1[7])));
     }
-    if (c0 < D) leaf_sums[leaf * D + c0] = res[0];
-    if (c1 < D) leaf_sums[leaf * D + c1] = res[1];
+    if (j != 0) return;
+    // tail (n % 8 rows, or the whole leaf when n < 8): sequential, loads first
+    const int tn = n - stop;
+    double w0[8], w1[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        if (t < tn) load_row(order[start + stop + t], w0[t], w1[t]);
+        else w0[t] = w1[t] = 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+        if (t < tn) { r0 = dadd(r0, w0[t]); r1 = dadd(r1, w1[t]); }
+    if (c0 < D) leaf_sums[leaf * D + c0] = r0;
+    if (c1 < D) leaf_sums[leaf * D + c1] = r1;
 }
 
 // One warp (one block) per (codeword, column chunk): fold leaves up the
@@ -679,10 +692,11 @@ int launch_group_sums(const double* X, long long n, long long ldx, int D, const 
     {
         long long tasks = max_leaves * n_chunks;
         ProfScope ps3("group_sums_leaf", s);
-        if (D <= 32) {
-            const long long per_warp = 32 / ((D + 1) / 2);
-            leaf_sum_narrow_kernel<<<grid_for((max_leaves + per_warp - 1) / per_warp, 8, 1LL << 31), 256, 0, s>>>(
-                X, ldx, D, order, leaves, total + 1, lsum);
+        static const int narrow_max = getenv("DA_GS_NARROW_MAX") ? atoi(getenv("DA_GS_NARROW_MAX")) : 128;
+        if (D <= narrow_max) {
+            const long long ntask = max_leaves * ((D + 7) / 8);
+            leaf_sum_narrow_kernel<<<grid_for(ntask, 8, 1LL << 31), 256, 0, s>>>(X, ldx, D, order, leaves, total + 1,
+                                                                                 lsum);
             DA_CHECK_LAUNCH("leaf_sum_narrow_kernel");
         } else {
             leaf_sum_kernel<<<grid_for(tasks, 8, 1LL << 31), 256, 0, s>>>(X, ldx, D, order, leaves, total + 1,
