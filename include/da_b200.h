@@ -48,7 +48,10 @@ int da_row_sqnorms(const void* A, int a_f32, int64_t rows, int64_t lda, int d, d
 /* Nearest codeword over the active prefix d with first-min ties; d2 clipped at 0.
  * replaces _assign                              clustering.py:139-148
  * xx optional: precomputed ||x||^2 over the prefix (da_row_sqnorms), reused across Lloyd iterations.
- * prev/changed optional: counts rows whose label differs from prev (clustering.py:199). */
+ * prev/changed optional: counts rows whose label differs from prev (clustering.py:199).
+ * d2 optional: NULL = labels only (the Lloyd loop inside DA, whose objective trace
+ * nobody reads); rows whose nearest codeword the tensor-core bound decides alone
+ * then skip the float64 recheck.  Labels and changed are the same either way. */
 int da_assign(const void* X, int x_f32, int64_t n, int64_t ldx, int d, const double* C, int64_t ldc, int K,
               const double* cc, const double* xx, int32_t* labels, double* d2, const int32_t* prev,
               unsigned long long* changed, void* stream);
