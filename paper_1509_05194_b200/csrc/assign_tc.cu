@@ -392,17 +392,23 @@ __global__ void __launch_bounds__(TC_TP, 1) assign_tc_kernel(
         const int erow = tid & (TC_M - 1);   // TMEM lane / tile row owned in the epilogue
         const int ehalf = tid >> 7;          // 0: codewords [0,128), 1: [128,256)
         long long it = 0;
+        // the row norm of the next tile is loaded one tile ahead: waiting on it at the
+        // top of every tile was the epilogue's largest stall
+        double xx_next = 0.0;
+        if (xx_in && (long long)blockIdx.x * TC_M + erow < n) xx_next = xx_in[(long long)blockIdx.x * TC_M + erow];
         for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
             const int accb = (int)(it & 1);
             const long long r = tile * TC_M + erow;
             const bool valid = r < n;
             double xx = 0.0;
-            if (valid) {
-                if (xx_in) xx = xx_in[r];
-                else {
-                    const TX* xr = X + r * ldx;
-                    xx = np_pw_sum([&](long long i) { double t = (double)xr[i]; return dmul(t, t); }, 0, d);
-                }
+            if (xx_in) {
+                xx = valid ? xx_next : 0.0;
+                const long long rn = r + (long long)gridDim.x * TC_M;
+                if (rn < n) xx_next = xx_in[rn];
+            }
+            if (valid && !xx_in) {
+                const TX* xr = X + r * ldx;
+                xx = np_pw_sum([&](long long i) { double t = (double)xr[i]; return dmul(t, t); }, 0, d);
             }
             const double sx = sqrt(xx);
             // bound on |w' - (cc - 2 x.c)| for w' = fmaf(-2, dot', (float)cc): 3xTF32 + fp32
