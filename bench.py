@@ -325,6 +325,37 @@ def main():
                   "per_dictionary_s": [round(s.seconds, 4) for s in rep.steps],
                   "distortion_after": rep.steps[-1].distortion,
                   "kernels_ms": {k: round(v[1], 3) for k, v in aprof.items()}}
+        # the Lloyd update's HBM-bound kernel at full width: leaf sums of 1M float64
+        # rows (d=128) gathered through a label order, live CUDA-event time on the
+        # launching stream (ProfScope), algorithmic N*(8*d + 4) bytes per call
+        Xr = X.to(torch.float64)
+        lab = torch.randint(0, K, (n,), dtype=torch.int32, device="cuda",
+                            generator=torch.Generator(device="cuda").manual_seed(5))
+        Cg = torch.empty((K, D), dtype=torch.float64, device="cuda")
+        cg = torch.empty(K, dtype=torch.int32, device="cuda")
+
+        def group_sums():
+            E.native.da_group_sums(E.P(Xr), n, Xr.stride(0), D, E.P(lab), K, 0, E.P(Cg), D, E.P(cg), E.stream())
+
+        for _ in range(3):
+            group_sums()
+        _native.prof_collect()
+        _native.prof_enable(True)
+        for _ in range(10):
+            group_sums()
+        torch.cuda.synchronize()
+        _native.prof_enable(False)
+        gprof = _native.prof_collect()
+        leaf_ms = gprof["group_sums_leaf"][1] / gprof["group_sums_leaf"][0]
+        upd_bytes = n * (8 * D + 4)
+        hbm = float(peaks().get("hbm_gbs", 6550.4))
+        anneal["update_roofline"] = {
+            "kernel": "leaf_sum_narrow_kernel (Lloyd update, d=128)", "bound": "hbm",
+            "achieved": upd_bytes / (leaf_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+            "frac": upd_bytes / (leaf_ms * 1e-3) / 1e9 / hbm,
+            "ms_per_call": leaf_ms, "whole_update_ms": gprof["group_sums"][1] / gprof["group_sums"][0],
+            "algorithmic": "N*(8*d + 4) B per update (float64 rows + int32 label)"}
+        del Xr
 
     # --- ADC candidate scan, config E shape: 10,000 queries x 100,000 uniform random
     # candidate ids over N_E encoded vectors (random codes stand in for the encoded
