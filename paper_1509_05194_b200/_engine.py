@@ -388,7 +388,7 @@ def _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm, la
             spec = None                              # computed from pre-reseed centroids
             empty = np.flatnonzero(red[K * da:].cpu().numpy() == 0)
             if lazy:
-                errs = assign(Xr, active, snaps[slot], xx=xx)[1] if n else errs
+                errs = assign(Xr, active, snaps[slot], xx=xx)[1] if n else torch.empty(0, dtype=F64, device=dev)
             _reseed_sharded(Xr, errs, empty, Cn, comm)
             chg.zero_()
             new_labels, errs_new = assign(Xr, active, Cn, prev=labels_prev, changed=chg, xx=xx, want_d2=not lazy)
