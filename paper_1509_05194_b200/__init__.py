@@ -113,4 +113,13 @@ def install(annq_module=None):
             if hasattr(mod, name) and name in ours:
                 setattr(mod, name, ours[name])
                 patched.append((modname, name))
+    # One counter dict for both packages: the patched entry points count their
+    # raw-dimension kernels into the reference's DEBUG_COUNTERS, which its tests
+    # read and reset (annq/codebook.py:53-55, 177-178; tests/test_codebook.py:236-243).
+    ref_cb = sys.modules.get("annq.codebook")
+    counters = getattr(ref_cb, "DEBUG_COUNTERS", None) if ref_cb is not None else None
+    if isinstance(counters, dict):
+        counters.setdefault("raw_dim_kernel_calls", 0)
+        _cbm.DEBUG_COUNTERS = counters
+        patched.append(("paper_1509_05194_b200.codebook", "DEBUG_COUNTERS"))
     return patched

@@ -649,12 +649,15 @@ def _encode_stream(n: int, D: int, row_bytes: int, fill, to_rows, cw: torch.Tens
     filled = [threading.Semaphore(0) for _ in range(nslot)]
     free = [threading.Semaphore(1) for _ in range(nslot)]
     errors = []
+    stop = threading.Event()
 
     def producer():
         try:
             for i, r0 in enumerate(starts):
                 s = i % nslot
                 free[s].acquire()
+                if stop.is_set():                    # the consumer failed: stop filling
+                    return
                 fill(pinned[s], r0, sizes[i])
                 filled[s].release()
         except BaseException as e:  # surfaced on the caller's thread
@@ -689,6 +692,12 @@ def _encode_stream(n: int, D: int, row_bytes: int, fill, to_rows, cw: torch.Tens
             comp_done[b] = ev
             up.synchronize()                                 # pinned slot s has been read
             free[s].release()
+    except BaseException:
+        # wake the producer wherever it waits so the join below cannot hang
+        stop.set()
+        for f in free:
+            f.release()
+        raise
     finally:
         th.join()
     if errors:

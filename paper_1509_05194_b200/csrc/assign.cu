@@ -300,6 +300,13 @@ int launch_assign(const void* X, int x_is_f32, long long n, long long ldx, int d
         ProfScope ps("assign_small_d<=16", s);
         const size_t smem = sizeof(double) * ((size_t)K * ((d + 1) & ~1) + K);
         const unsigned g = grid_for((n + AS_SMALL_R - 1) / AS_SMALL_R, 256, 1LL << 31);
+        if (smem > 48 * 1024) {
+            // K up to 4096 at d = 3 needs up to 160 KB of codebook in shared memory
+            DA_CUDA(cudaFuncSetAttribute(assign_small_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+            DA_CUDA(cudaFuncSetAttribute(assign_small_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+        }
         if (x_is_f32)
             assign_small_kernel<float><<<g, 256, smem, s>>>((const float*)X, n, ldx, d, C, ldc, K, cc, xx, labels, d2,
                                                             prev, changed);

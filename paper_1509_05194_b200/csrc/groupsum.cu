@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(256) leaf_sum_narrow_kernel(const double* __re
     const int c0 = chunk * 8 + 2 * p, c1 = c0 + 1;
     const int4 L = leaves[leaf];
     const int start = L.y, n = L.z;
-    const bool vec = ((ldx & 1) == 0) && (c1 < D);
+    const bool vec = ((ldx & 1) == 0) && (c1 < D) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
     auto load_row = [&](long long r, double& v0, double& v1) {
         const double* q = X + r * ldx;
         if (vec) {

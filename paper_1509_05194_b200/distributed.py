@@ -35,7 +35,7 @@ class Comm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
-        self._sizes = {}
+        self._bound = None
         self.row_offset = 0
 
     @property
@@ -60,18 +60,25 @@ class Comm:
         return out.to(t.device) if t.is_cuda else out
 
     def sizes(self, n_local: int) -> list:
-        if n_local not in self._sizes:
-            dev = "cpu" if self._host_staged else "cuda"
-            t = torch.tensor([n_local], dtype=torch.int64, device=dev)
-            self._sizes[n_local] = [int(x) for x in self.allgather(t).cpu().tolist()]
-        return self._sizes[n_local]
+        """Every rank's shard size.  The allgather runs unless bind_rows() already
+        recorded the sizes for this n_local; bind_rows is itself collective, so
+        whether a call communicates is decided identically on every rank."""
+        if self._bound is not None and self._bound[0] == n_local:
+            return self._bound[1]
+        dev = "cpu" if self._host_staged else "cuda"
+        t = torch.tensor([n_local], dtype=torch.int64, device=dev)
+        return [int(x) for x in self.allgather(t).cpu().tolist()]
 
     def total(self, n_local: int) -> int:
         return int(sum(self.sizes(n_local)))
 
     def bind_rows(self, n_local: int) -> "Comm":
-        """Record this shard's first global row id (shards are rank-ordered)."""
+        """Collective: record every shard's size and this shard's first global
+        row id (shards are rank-ordered).  Later sizes()/total() calls with the
+        same n_local read the record instead of communicating."""
+        self._bound = None
         s = self.sizes(n_local)
+        self._bound = (n_local, s)
         self.row_offset = int(sum(s[: self.rank]))
         return self
 

@@ -2,6 +2,7 @@
 content hashes, file formats, synthetic generators and the drop-in patcher."""
 
 import hashlib
+import os
 import struct
 import sys
 import types
@@ -150,3 +151,45 @@ def test_install_patches_every_binding_site(monkeypatch):
         for a in attrs:
             assert (modname, a) in patched
             assert getattr(sys.modules[modname], a).__module__.startswith("paper_1509_05194_b200")
+
+
+def _real_reference():
+    """The unmodified reference installed untracked under baseline/_ref
+    (oracle/ship_reference.sh); None when it is not there."""
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "annq")):
+        return None
+    return ref
+
+
+def test_install_against_the_real_reference(monkeypatch):
+    """install() on the real annq: every by-name binding site points at this
+    package and the raw-kernel counters are one dict (test_codebook.py:236-243)."""
+    ref = _real_reference()
+    if ref is None:
+        pytest.skip("baseline/_ref not installed (oracle/ship_reference.sh)")
+    for k in [k for k in sys.modules if k == "annq" or k.startswith("annq.")]:
+        monkeypatch.delitem(sys.modules, k)
+    monkeypatch.syspath_prepend(ref)
+    import importlib
+
+    annq = importlib.import_module("annq")
+    saved = {m: dict(vars(sys.modules[m])) for m in list(sys.modules) if m == "annq" or m.startswith("annq.")}
+    from paper_1509_05194_b200 import codebook as ours_cb
+
+    old_counters = ours_cb.DEBUG_COUNTERS
+    try:
+        patched = da.install()
+        assert ("annq.annealing", "improved_kmeans") in patched
+        assert ("annq.atree", "adc_table") in patched
+        assert annq.encode_dataset is da.encode_dataset
+        import annq.codebook as rcb
+
+        assert ours_cb.DEBUG_COUNTERS is rcb.DEBUG_COUNTERS
+        rcb.DEBUG_COUNTERS["raw_dim_kernel_calls"] = 0
+        ours_cb._raw_kernel(2)
+        assert rcb.DEBUG_COUNTERS["raw_dim_kernel_calls"] == 2
+    finally:
+        ours_cb.DEBUG_COUNTERS = old_counters
+        for m, d in saved.items():
+            vars(sys.modules[m]).update(d)
