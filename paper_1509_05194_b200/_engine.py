@@ -217,6 +217,11 @@ def _pinned_flags() -> list:
     return _FLAGS_H
 
 
+# When a list, every Lloyd call appends (active width, rows, K, iterations):
+# the per-stage iteration counts I_{m,s} of SURVEY 8(d)'s anneal-pass FLOP formula.
+LLOYD_LOG: list | None = None
+
+
 def lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, comm=None, want_trace: bool = True):
     """Returns (C f64 (K,D), labels int32 (n,), trace list[float]).
 
@@ -308,6 +313,8 @@ def _lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, 
             native.da_group_sums(P(Xr), n, Xr.stride(0), D, P(gs_labels), K, 0, P(C), C.stride(0), P(counts),
                                  stream())
         trace = [] if lazy else trace_d[: iters + 1].cpu().tolist()
+        if LLOYD_LOG is not None:
+            LLOYD_LOG.append((active, n, K, iters))
         return C, labels, trace
     return _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm, lazy)
 
@@ -415,6 +422,8 @@ def _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm, la
         cnt.copy_(counts)
         _sharded_update(full, K, D, C, comm)
     trace = [] if lazy else trace_d[: iters + 1].cpu().tolist()
+    if LLOYD_LOG is not None:
+        LLOYD_LOG.append((active, n, K, iters))
     return C, labels, trace
 
 
