@@ -102,6 +102,31 @@ int da_vec_err(const void* X, int x_f32, int64_t n, int64_t ldx, int D, const vo
 int da_reconstruct(const void* codes, int code_bytes, int64_t n, int64_t ldc, const float* cw, int M, int K, int D,
                    double* out, void* stream);
 
+/* Row-sharded Lloyd update, bit-identical to da_group_sums over the
+ * concatenated shards (rank order) -- the reduceat order of
+ * clustering.py:151-162 cut at shard boundaries.  Per update:
+ *   da_gs_shard_sort   local stable sort; counts_local (K int32) -> allgather
+ *                      into counts_all (world x K, rank-major);
+ *   da_gs_shard_plan   global pairwise leaves; fills red (cap_leaves*d leaf sums
+ *                      | K*d segment first rows) with -0.0 and this shard's leaves
+ *                      and first rows; the states of leaves cut at the right
+ *                      boundary go to send_state (K*8*d); counts_global = n_k;
+ *   world-1 rounds of { send send_state right, receive recv_state from the
+ *                      left; da_gs_shard_round } (a cut leaf's state crosses
+ *                      one boundary per round);
+ *   allreduce(sum) of red, then da_gs_shard_fold: mode 0 = means into the
+ *                      filled rows of out, mode 1 = raw sums.
+ * cap_leaves >= K + N/64 + 2 (N = global rows).  One shard per process. */
+int da_gs_shard_sort(const double* X, int64_t n, int64_t ldx, int d, const int32_t* labels, int K,
+                     int32_t* counts_local, void* stream);
+int da_gs_shard_plan(const double* X, int64_t n, int64_t ldx, int d, int K, const int32_t* counts_all, int world,
+                     int rank, int64_t cap_leaves, double* red, double* send_state, int32_t* counts_global,
+                     void* stream);
+int da_gs_shard_round(const double* X, int64_t ldx, int d, int K, const double* recv_state, double* send_state,
+                      double* red, void* stream);
+int da_gs_shard_fold(int d, int K, const double* red, int64_t cap_leaves, const int32_t* counts_global, int mode,
+                     double* out, int64_t ldo, void* stream);
+
 /* Column means (PCA centre).  replaces X.mean(axis=0)   clustering.py:93 */
 int da_col_mean(const void* X, int x_f32, int64_t n, int64_t ld, int D, double* mean, void* stream);
 
@@ -109,6 +134,24 @@ int da_col_mean(const void* X, int x_f32, int64_t n, int64_t ld, int D, double* 
  * centred scatter (divide=0, for sharded PCA).  replaces clustering.py:94-96 */
 int da_pca_cov(const void* X, int x_f32, int64_t n, int64_t ld, int D, const double* mean, double* cov, int divide,
                void* stream);
+
+/* Sharded PCA, bit-identical to the unsharded reductions (distributed.py runs
+ * the rank-ordered ring; the reference is unsharded: clustering.py:93-96).
+ *   da_col_sums:   sums = init + X[0] + X[1] + ... per column, one sequential
+ *                  add chain (X.mean(axis=0)'s order) continued from the running
+ *                  sums of the rows before this shard (init may alias sums;
+ *                  init = NULL starts a new chain).
+ *   da_cov_chains: out[s] (D x D) = the FMA chain of (x - mean)^T (x - mean) over
+ *                  rows [seg_starts[s], seg_starts[s+1]) (1..384 rows: one
+ *                  OpenBLAS GEMM_Q block or the part of one inside this shard),
+ *                  segment 0 continuing the accumulator `init` when non-NULL.
+ *   da_fold:       out = (accumulate ? out : parts[0]) + parts[..] in order (the
+ *                  dsyrk block sums added into C). */
+int da_col_sums(const void* X, int x_f32, int64_t n, int64_t ld, int D, const double* init, double* sums,
+                void* stream);
+int da_cov_chains(const void* X, int x_f32, int64_t n, int64_t ld, int D, const double* mean,
+                  const int64_t* seg_starts, int nseg, const double* init, double* out, void* stream);
+int da_fold(const double* parts, int nz, int64_t len, int accumulate, double* out, void* stream);
 
 /* inverse=0: out = (X - mean) @ R^T;  inverse=1: out = X @ R + mean.
  * replaces PcaModel.transform / inverse_transform   clustering.py:39-43 */

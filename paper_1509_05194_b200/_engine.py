@@ -322,16 +322,47 @@ def _lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, 
 _FLAGS_SH: list = []
 
 
+class _ShardSums:
+    """Buffers + calls of the exact sharded Lloyd update (da_gs_shard_*): the
+    one-GPU reduceat order across row shards (see groupsum.cu)."""
+
+    def __init__(self, K, D, n_total, comm, dev):
+        self.K, self.comm = K, comm
+        self.cap = K + n_total // 64 + 2           # >= the global leaf count
+        self.cnt_local = torch.empty(K, dtype=I32, device=dev)
+        self.send = torch.zeros(K * 8 * D, dtype=F64, device=dev)
+        self.recv = torch.zeros(K * 8 * D, dtype=F64, device=dev)
+
+    def plan(self, Xr, d, labels, red, gcount):
+        """Leaf sums + first rows of this shard into red (then allreduced by
+        the caller); gcount = global label counts."""
+        comm, K = self.comm, self.K
+        n = Xr.shape[0]
+        native.da_gs_shard_sort(P(Xr), n, Xr.stride(0), d, P(labels), K, P(self.cnt_local), stream())
+        cnt_all = comm.allgather(self.cnt_local)
+        send, recv = self.send[: K * 8 * d], self.recv[: K * 8 * d]
+        native.da_gs_shard_plan(P(Xr), n, Xr.stride(0), d, K, P(cnt_all), comm.world, comm.rank, self.cap, P(red),
+                                P(send), P(gcount), stream())
+        for _ in range(comm.world - 1):
+            comm.shift_(send, recv)
+            native.da_gs_shard_round(P(Xr), Xr.stride(0), d, K, P(recv), P(send), P(red), stream())
+
+    def fold(self, d, red, gcount, mode, out):
+        native.da_gs_shard_fold(d, self.K, P(red), self.cap, P(gcount), mode, P(out), out.stride(0), stream())
+
+
 def _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm, lazy=False):
     """The Lloyd loop over row shards (clustering.py:165-203, statistics allreduced).
 
     Same restructuring as the one-GPU loop: the iterations sum only the active
     prefix and the remaining columns are summed once at the end; iteration i+1
-    is launched before the host reads iteration i's flags.  Per iteration there
-    are two collectives -- one allreduce of [active sums | counts] and one of
-    [rows changed | error sum] -- and no blocking host sync on the critical
-    path.  Every decision the host takes (converged, reseed) is a function of
-    allreduced values, so all ranks launch the same collective sequence.
+    is launched before the host reads iteration i's flags.  ONE collective per
+    iteration: the allreduce of [active sums | counts | rows changed | error
+    sum], where the last two belong to the previous iteration's assign (so the
+    stop decision for iteration i is read from iteration i+1's allreduce; when
+    it says "converged", i+1 is dropped).  Every decision the host takes
+    (converged, reseed) is a function of allreduced values, so all ranks launch
+    the same collective sequence.
     """
     n, D = Xr.shape
     K = C.shape[0]
@@ -341,76 +372,112 @@ def _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm, la
     if not _FLAGS_SH:
         _FLAGS_SH.extend(torch.zeros(3, dtype=F64, pin_memory=True) for _ in range(2))
     flags_h = _FLAGS_SH
+    exact = getattr(comm, "exact", False)
+    sh = _ShardSums(K, D, int(ntot), comm, dev) if exact else None
+    # reduced buffer: [sums | counts] (fast) or [leaf sums | first rows] (exact),
+    # then the stats of the assign before this update
+    nst = sh.cap * da + K * da if exact else K * da + K
 
     def new_slot(Cbuf):
-        return (Cbuf, torch.empty(K * da + K, dtype=F64, device=dev), torch.empty(K, dtype=I32, device=dev),
+        nred = nst + 2
+        return (Cbuf, torch.empty(nred, dtype=F64, device=dev), torch.empty(K, dtype=I32, device=dev),
                 torch.zeros(1, dtype=torch.int64, device=dev), torch.zeros(3, dtype=F64, device=dev),
                 torch.cuda.Event())
 
     slots = [new_slot(C), new_slot(torch.empty_like(C))]
     snaps = [torch.empty_like(C), torch.empty_like(C)] if lazy else None
 
-    def stats_(slot, ne):
-        """fl[1:3] = global [rows changed, error sum] of the assign that wrote ne
-        (error sum 0 when the trace is not wanted)."""
-        _, _, _, chg, fl, _ = slots[slot]
+    def put_stats(dst, chg, ne):
+        """dst[0:2] = this shard's [rows changed, error sum] of one assign."""
+        if chg is None:
+            dst.zero_()
+            return
+        dst[0:1].copy_(chg)
         if n and ne is not None:
-            native.da_np_sum(P(ne), n, 0, P(fl[2:3]), stream())
+            native.da_np_sum(P(ne), n, 0, P(dst[1:2]), stream())
         else:
-            fl[2:3].zero_()
-        fl[1:2].copy_(chg)
-        comm.allreduce_(fl[1:3])
+            dst[1:2].zero_()
 
-    def launch(C_prev, labels_prev, slot):
+    def launch(C_prev, labels_prev, slot, pchg, pne):
         Cn, red, cn, chg, fl, ev = slots[slot]
         if lazy:
-            snaps[slot].copy_(C_prev)
-        sums = red[: K * da].view(K, da)
-        if n:
-            native.da_group_sums(P(Xr), n, Xr.stride(0), da, P(labels_prev), K, 1, P(sums), da, P(cn), stream())
-        else:
-            red.zero_()
-            cn.zero_()
-        red[K * da:].copy_(cn)
+            snaps[slot].copy_(C_prev)                # the centroids the previous assign measured against
         if Cn is not C_prev:
             Cn.copy_(C_prev)                         # empty clusters keep their previous rows
-        fl[0:1].copy_(_sharded_update(red, K, da, Cn, comm).view(1))
+        if exact:
+            sh.plan(Xr, da, labels_prev, red, cn)
+            put_stats(red[nst:], pchg, pne)
+            comm.allreduce_(red)
+            sh.fold(da, red, cn, 0, Cn)
+            fl[0:1].copy_((cn == 0).sum().view(1))
+        else:
+            sums = red[: K * da].view(K, da)
+            if n:
+                native.da_group_sums(P(Xr), n, Xr.stride(0), da, P(labels_prev), K, 1, P(sums), da, P(cn), stream())
+            else:
+                red[:nst].zero_()
+                cn.zero_()
+            red[K * da:nst].copy_(cn)
+            put_stats(red[nst:], pchg, pne)
+            comm.allreduce_(red)
+            cnt = red[K * da:nst]
+            Cn[:, :da] = torch.where(cnt.unsqueeze(1) > 0, sums / cnt.unsqueeze(1), Cn[:, :da])
+            fl[0:1].copy_((cnt == 0).sum().view(1))
+        fl[1:3].copy_(red[nst:])
+        flags_h[slot].copy_(fl, non_blocking=True)
+        ev.record()                                  # the host's flags are ready after the allreduce
         chg.zero_()
         nl, ne = assign(Xr, active, Cn, prev=labels_prev, changed=chg, xx=xx, want_d2=not lazy)
-        stats_(slot, ne)
-        flags_h[slot].copy_(fl, non_blocking=True)
-        ev.record()
         return [slot, labels_prev, nl, ne]
 
     iters = 0
     gs_labels = None
-    cur = launch(C, labels, 0) if max_iters > 0 else None
+    cur = launch(C, labels, 0, None, None) if max_iters > 0 else None
+    spec = None
+    if cur is not None and max_iters > 1:
+        spec = launch(slots[0][0], cur[2], 1, slots[0][3], cur[3])
     while cur is not None:
-        slot, labels_prev, new_labels, errs_new = cur
+        slot, labels_prev, _, _ = cur
         Cn, red, cn, chg, fl, ev = slots[slot]
-        spec = launch(Cn, new_labels, slot ^ 1) if iters + 1 < max_iters else None
         ev.synchronize()
-        fh = flags_h[slot].numpy().copy()
-        if fh[0]:
+        if flags_h[slot][0].item():
             spec = None                              # computed from pre-reseed centroids
-            empty = np.flatnonzero(red[K * da:].cpu().numpy() == 0)
+            gcnt = cn if exact else red[K * da:nst]
+            empty = np.flatnonzero(gcnt.cpu().numpy() == 0)
             if lazy:
                 errs = assign(Xr, active, snaps[slot], xx=xx)[1] if n else torch.empty(0, dtype=F64, device=dev)
             _reseed_sharded(Xr, errs, empty, Cn, comm)
             chg.zero_()
-            new_labels, errs_new = assign(Xr, active, Cn, prev=labels_prev, changed=chg, xx=xx, want_d2=not lazy)
-            stats_(slot, errs_new)
-            fh[1:3] = fl[1:3].cpu().numpy()
+            cur[2], cur[3] = assign(Xr, active, Cn, prev=labels_prev, changed=chg, xx=xx, want_d2=not lazy)
         C = Cn
         gs_labels = labels_prev
-        errs = errs_new
+        labels, errs = cur[2], cur[3]
         iters += 1
-        trace_d[iters] = fh[2] / ntot
-        labels = new_labels
-        if int(fh[1]) == 0 or iters >= max_iters:
+        if iters >= max_iters:
+            if not lazy:                             # no next iteration carries the last assign's stats
+                st = torch.zeros(2, dtype=F64, device=dev)
+                put_stats(st, chg, errs)
+                comm.allreduce_(st)
+                trace_d[iters:iters + 1] = true_div(st[1:2], ntot)
             break
-        cur = spec if spec is not None else launch(C, labels, slot ^ 1)
-    if gs_labels is not None and active < D:
+        if spec is None:
+            spec = launch(C, labels, slot ^ 1, chg, errs)
+        s2 = spec[0]
+        slots[s2][5].synchronize()
+        fh = flags_h[s2].numpy().copy()
+        trace_d[iters] = fh[2] / ntot
+        if int(fh[1]) == 0:
+            break                                    # iteration `iters` changed no row: spec dropped
+        cur, spec = spec, None
+        if iters + 1 < max_iters:
+            spec = launch(slots[s2][0], cur[2], s2 ^ 1, slots[s2][3], cur[3])
+    if gs_labels is not None and active < D and exact:
+        full = torch.empty(sh.cap * D + K * D, dtype=F64, device=dev)
+        gcnt = torch.empty(K, dtype=I32, device=dev)
+        sh.plan(Xr, D, gs_labels, full, gcnt)
+        comm.allreduce_(full)
+        sh.fold(D, full, gcnt, 0, C)
+    elif gs_labels is not None and active < D:
         full = torch.empty(K * D + K, dtype=F64, device=dev)
         sums, cnt = full[: K * D].view(K, D), full[K * D:]
         counts = torch.empty(K, dtype=I32, device=dev)
@@ -450,10 +517,45 @@ def _complete_basis(components: np.ndarray, d: int) -> np.ndarray:
     return np.vstack(rows)
 
 
+class _DevicePcaOps:
+    """Device arithmetic of distributed.exact_pca_moments (the sharded PCA ring)."""
+
+    def __init__(self, dev):
+        self.dev = dev
+
+    def zeros(self, shape):
+        return torch.zeros(shape, dtype=F64, device=self.dev)
+
+    def div(self, t, d):
+        return true_div(t, d)
+
+    def col_sums(self, X, init):
+        out = torch.empty(X.shape[1], dtype=F64, device=X.device)
+        native.da_col_sums(P(X), is_f32(X), X.shape[0], X.stride(0), X.shape[1], P(init), P(out), stream())
+        return out
+
+    def cov_chains(self, X, mean, starts, init):
+        D = X.shape[1]
+        nseg = len(starts) - 1
+        out = torch.empty((nseg, D, D), dtype=F64, device=X.device)
+        for s0 in range(0, nseg, 65535):
+            s1 = min(nseg, s0 + 65535)
+            arr = (ctypes.c_int64 * (s1 - s0 + 1))(*starts[s0:s1 + 1])
+            native.da_cov_chains(P(X), is_f32(X), X.shape[0], X.stride(0), D, P(mean), ctypes.cast(arr, ctypes.c_void_p),
+                                 s1 - s0, P(init) if s0 == 0 else None, P(out[s0]), stream())
+        return out
+
+    def fold(self, total, parts):
+        out = total if total is not None else torch.empty_like(parts[0])
+        native.da_fold(P(parts), parts.shape[0], parts[0].numel(), 0 if total is None else 1, P(out), stream())
+        return out
+
+
 def pca(X: torch.Tensor, comm=None):
     """Returns (R dev f64 (D,D), mean dev f64 (D,), variances np, R host).
 
-    Mean and covariance are reduced on the device (allreduced across shards);
+    Mean and covariance are reduced on the device; across shards they run the
+    rank-ordered ring of distributed.exact_pca_moments (bit-identical);
     the D x D eigendecomposition runs in LAPACK on the host, like the reference.
     """
     n_local, D = X.shape
@@ -462,37 +564,26 @@ def pca(X: torch.Tensor, comm=None):
     n = comm.total(n_local) if comm is not None else n_local
     if n < 2:
         raise ValueError(f"PCA needs at least 2 vectors, got {n}")
-    mean = torch.empty(D, dtype=F64, device=X.device)
     if comm is None:
+        mean = torch.empty(D, dtype=F64, device=X.device)
         native.da_col_mean(P(X), is_f32(X), n_local, X.stride(0), D, P(mean), stream())
-    else:
-        if n_local:
-            native.da_col_mean(P(X), is_f32(X), n_local, X.stride(0), D, P(mean), stream())
-            mean *= float(n_local)
-        else:
-            mean.zero_()
-        comm.allreduce_(mean)
-        mean = true_div(mean, n)
-    if n > D:
-        cov = torch.empty((D, D), dtype=F64, device=X.device)
-        if comm is None:
+        if n > D:
+            cov = torch.empty((D, D), dtype=F64, device=X.device)
             native.da_pca_cov(P(X), is_f32(X), n_local, X.stride(0), D, P(mean), P(cov), 1, stream())
-        else:
-            # scatter around the GLOBAL mean on every shard, allreduce, then / (n-1)
-            if n_local:
-                native.da_pca_cov(P(X), is_f32(X), n_local, X.stride(0), D, P(mean), P(cov), 0, stream())
-            else:
-                cov.zero_()
-            comm.allreduce_(cov)
-            cov = true_div(cov, n - 1)
+    else:
+        if n <= D:
+            raise ValueError("the Gram-matrix PCA route (n <= d) is not sharded")
+        from .distributed import exact_pca_moments
+
+        # rank-ordered ring: the same chains as one GPU, cut at the shard boundaries
+        mean, cov = exact_pca_moments(X, comm, _DevicePcaOps(X.device))
+    if n > D:
         cov_h = cov.cpu().numpy()
         w, V = np.linalg.eigh(cov_h)
         order = np.argsort(w, kind="stable")[::-1]
         R_h = np.ascontiguousarray(V[:, order].T)
         variances = np.maximum(w[order], 0.0)
     else:
-        if comm is not None:
-            raise ValueError("the Gram-matrix PCA route (n <= d) is not sharded")
         # Gram route (clustering.py:101-112): n <= d, so these products are tiny
         Xc = torch.empty((n, D), dtype=F64, device=X.device)
         ident = torch.eye(D, dtype=F64, device=X.device)

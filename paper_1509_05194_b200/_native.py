@@ -34,6 +34,13 @@ _SIGNATURES = {
     "da_reconstruct": [_P, _I, _L, _L, _P, _I, _I, _I, _P, _P],
     "da_col_mean": [_P, _I, _L, _L, _I, _P, _P],
     "da_pca_cov": [_P, _I, _L, _L, _I, _P, _P, _I, _P],
+    "da_col_sums": [_P, _I, _L, _L, _I, _P, _P, _P],
+    "da_cov_chains": [_P, _I, _L, _L, _I, _P, _P, _I, _P, _P, _P],
+    "da_fold": [_P, _I, _L, _I, _P, _P],
+    "da_gs_shard_sort": [_P, _L, _L, _I, _P, _I, _P, _P],
+    "da_gs_shard_plan": [_P, _L, _L, _I, _I, _P, _I, _I, _L, _P, _P, _P, _P],
+    "da_gs_shard_round": [_P, _L, _I, _I, _P, _P, _P, _P],
+    "da_gs_shard_fold": [_I, _I, _P, _L, _P, _I, _P, _L, _P],
     "da_rotate": [_P, _I, _L, _L, _I, _P, _P, _P, _I, _P],
     "da_gemm_strided": [_P, _I, _L, _L, _P, _I, _L, _L, _P, _L, _L, _L, _L, _L, _P],
     "da_einsum_sq": [_P, _L, _I, _P, _P],

@@ -141,6 +141,34 @@ int da_group_sums(const double* X, int64_t n, int64_t ldx, int D, const int32_t*
     return launch_group_sums(X, n, ldx, D, labels, K, mode, out, ldo, counts, STREAM(stream));
 }
 
+int da_gs_shard_sort(const double* X, int64_t n, int64_t ldx, int d, const int32_t* labels, int K,
+                     int32_t* counts_local, void* stream) {
+    if (n < 0 || K < 1 || d < 1 || (n > 0 && ldx < d)) return fail_arg("gs_shard_sort: bad arguments");
+    if (n >= (1LL << 31)) return fail_arg("gs_shard_sort: n=%lld exceeds int32 row ids", (long long)n);
+    return launch_gs_shard_sort(X, n, ldx, d, labels, K, counts_local, STREAM(stream));
+}
+
+int da_gs_shard_plan(const double* X, int64_t n, int64_t ldx, int d, int K, const int32_t* counts_all, int world,
+                     int rank, int64_t cap_leaves, double* red, double* send_state, int32_t* counts_global,
+                     void* stream) {
+    if (world < 1 || rank < 0 || rank >= world || cap_leaves < 1 || d < 1)
+        return fail_arg("gs_shard_plan: bad arguments world=%d rank=%d cap=%lld", world, rank, (long long)cap_leaves);
+    return launch_gs_shard_plan(X, n, ldx, d, K, counts_all, world, rank, cap_leaves, red, send_state, counts_global,
+                                STREAM(stream));
+}
+
+int da_gs_shard_round(const double* X, int64_t ldx, int d, int K, const double* recv_state, double* send_state,
+                      double* red, void* stream) {
+    return launch_gs_shard_round(X, ldx, d, K, recv_state, send_state, red, STREAM(stream));
+}
+
+int da_gs_shard_fold(int d, int K, const double* red, int64_t cap_leaves, const int32_t* counts_global, int mode,
+                     double* out, int64_t ldo, void* stream) {
+    if (mode != 0 && mode != 1) return fail_arg("gs_shard_fold: mode must be 0 or 1");
+    if (ldo < d) return fail_arg("gs_shard_fold: ldo < d");
+    return launch_gs_shard_fold(d, K, red, cap_leaves, counts_global, mode, out, ldo, STREAM(stream));
+}
+
 int da_label_order(const int32_t* labels, int64_t n, int K, int32_t* order, int32_t* counts, void* stream) {
     if (n < 0 || K < 1) return fail_arg("label_order: bad arguments");
     if (n >= (1LL << 31)) return fail_arg("label_order: n too large");
@@ -218,6 +246,51 @@ int da_pca_cov(const void* X, int x_f32, int64_t n, int64_t ld, int D, const dou
     // the pinned starts vector must outlive the async copy
     DA_CUDA(cudaStreamSynchronize(s));
     return 0;
+}
+
+// Sharded PCA pieces (the reference's reductions cut at shard boundaries,
+// continued bit for bit by the next shard; distributed.py runs the ring).
+int da_col_sums(const void* X, int x_f32, int64_t n, int64_t ld, int D, const double* init, double* sums,
+                void* stream) {
+    if (D < 1) return fail_arg("col_sums: D must be positive");
+    return launch_col_sums(X, x_f32, n, ld, D, init, sums, STREAM(stream));
+}
+
+int da_cov_chains(const void* X, int x_f32, int64_t n, int64_t ld, int D, const double* mean,
+                  const int64_t* seg_starts, int nseg, const double* init, double* out, void* stream) {
+    if (nseg < 1 || !seg_starts) return fail_arg("cov_chains: need at least one segment");
+    if (nseg > 65535) return fail_arg("cov_chains: at most 65535 segments per call");
+    if (seg_starts[0] < 0 || seg_starts[nseg] > n) return fail_arg("cov_chains: segments outside the rows");
+    for (int i = 0; i < nseg; ++i) {
+        const long long len = seg_starts[i + 1] - seg_starts[i];
+        if (len < 1 || len > BLAS_Q) return fail_arg("cov_chains: segment %d has %lld rows (1..384)", i, len);
+    }
+    cudaStream_t s = STREAM(stream);
+    ProfScope ps("pca_cov", s);
+    long long* kst = (long long*)scratch(6, sizeof(long long) * (size_t)(nseg + 1), s);
+    if (!kst) return fail_cuda(cudaErrorMemoryAllocation, "cov_chains scratch");
+    DA_CUDA(cudaMemcpyAsync(kst, seg_starts, sizeof(long long) * (nseg + 1), cudaMemcpyHostToDevice, s));
+    GemmArgs g{};
+    g.A = X; g.a_f32 = x_f32; g.sai = 1; g.sak = ld; g.asub = mean; g.asub_mode = 1;
+    g.B = X; g.b_f32 = x_f32; g.sbk = ld; g.sbj = 1; g.bsub = mean; g.bsub_mode = 2;
+    g.C = out; g.sci = D; g.scj = 1; g.sCz = (long long)D * D;
+    g.M = D; g.N = D; g.K = n; g.nb2 = 1; g.ksplit = nseg; g.kstarts = kst; g.epi = 0; g.cinit = init;
+    int rc;
+    {
+        ProfScope p1("pca_cov_gemm", s);
+        rc = launch_gemm(g, 1, s);
+    }
+    if (rc) return rc;
+    // the host starts array may be released by the caller on return
+    DA_CUDA(cudaStreamSynchronize(s));
+    return 0;
+}
+
+int da_fold(const double* parts, int nz, int64_t len, int accumulate, double* out, void* stream) {
+    if (nz < 1 || len < 1) return fail_arg("fold: nothing to fold");
+    cudaStream_t s = STREAM(stream);
+    ProfScope p2("pca_cov_fold", s);
+    return launch_accumulate_partials(parts, nz, len, 0.0, accumulate, out, s);
 }
 
 int da_rotate(const void* X, int x_f32, int64_t n, int64_t ld, int D, const double* R, const double* mean,

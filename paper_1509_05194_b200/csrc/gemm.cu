@@ -43,6 +43,16 @@ __global__ void __launch_bounds__(G_THREADS) gemm_kernel(GemmArgs g) {
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) { acc[i][j] = 0.0; tot[i][j] = 0.0; }
+    if (g.cinit && ks == 0) {
+        // continue a chain another shard started (same FMA sequence as one long chain)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const long long gi = i0 + ty * 4 + i, gj = j0 + (j < 2 ? 2 * tx + j : 30 + 2 * tx + j);
+                if (gi < g.M && gj < g.N) acc[i][j] = g.cinit[gi * g.sci + gj * g.scj];
+            }
+    }
     // BLAS k-blocking of this k-range (one block when the range is <= 384)
     long long blk_end = kbeg + blas_block_len(kend - kbeg);
     bool first_blk = true;
@@ -193,7 +203,8 @@ constexpr int CM_COLS = 1, CM_ROWS = 2048, CM_T = 256;
 
 template <typename T>
 __global__ void __launch_bounds__(CM_T) col_mean_seq_kernel(const T* __restrict__ X, long long n, long long ld, int D,
-                                                             double* __restrict__ mean) {
+                                                             double* __restrict__ mean, const double* __restrict__ init,
+                                                             int raw) {
     __shared__ double buf[2][CM_ROWS][CM_COLS];
     const int c0 = blockIdx.x * CM_COLS;
     const int tid = threadIdx.x;
@@ -206,7 +217,7 @@ __global__ void __launch_bounds__(CM_T) col_mean_seq_kernel(const T* __restrict_
             buf[b][rr][cc] = v;
         }
     };
-    double s = 0.0;
+    double s = (init && tid < CM_COLS && c0 + tid < D) ? init[c0 + tid] : 0.0;
     const long long nchunks = (n + CM_ROWS - 1) / CM_ROWS;
     load(0, 0);
     __syncthreads();
@@ -227,15 +238,34 @@ __global__ void __launch_bounds__(CM_T) col_mean_seq_kernel(const T* __restrict_
         }
         __syncthreads();
     }
-    if (tid < CM_COLS && c0 + tid < D) mean[c0 + tid] = __ddiv_rn(s, (double)n);
+    if (tid < CM_COLS && c0 + tid < D) mean[c0 + tid] = raw ? s : __ddiv_rn(s, (double)n);
 }
 
 int launch_col_mean(const void* X, int x_f32, long long n, long long ld, int D, double* mean, cudaStream_t s) {
     if (n <= 0) return fail_arg("col_mean: n must be positive");
     ProfScope ps("col_mean", s);
     const unsigned g = (unsigned)((D + CM_COLS - 1) / CM_COLS);
-    if (x_f32) col_mean_seq_kernel<float><<<g, CM_T, 0, s>>>((const float*)X, n, ld, D, mean);
-    else col_mean_seq_kernel<double><<<g, CM_T, 0, s>>>((const double*)X, n, ld, D, mean);
+    if (x_f32) col_mean_seq_kernel<float><<<g, CM_T, 0, s>>>((const float*)X, n, ld, D, mean, nullptr, 0);
+    else col_mean_seq_kernel<double><<<g, CM_T, 0, s>>>((const double*)X, n, ld, D, mean, nullptr, 0);
+    DA_CHECK_LAUNCH("col_mean_seq_kernel");
+    return 0;
+}
+
+// Raw column sums continuing a running sum (init, may alias sums) another
+// shard computed over the rows before these: the per-column add chains of
+// X.mean(axis=0) cut at a shard boundary, bit for bit.
+int launch_col_sums(const void* X, int x_f32, long long n, long long ld, int D, const double* init, double* sums,
+                    cudaStream_t s) {
+    if (n < 0) return fail_arg("col_sums: negative row count");
+    if (n == 0) {
+        if (init && init != sums) DA_CUDA(cudaMemcpyAsync(sums, init, sizeof(double) * D, cudaMemcpyDeviceToDevice, s));
+        else if (!init) DA_CUDA(cudaMemsetAsync(sums, 0, sizeof(double) * D, s));
+        return 0;
+    }
+    ProfScope ps("col_mean", s);
+    const unsigned g = (unsigned)((D + CM_COLS - 1) / CM_COLS);
+    if (x_f32) col_mean_seq_kernel<float><<<g, CM_T, 0, s>>>((const float*)X, n, ld, D, sums, init, 1);
+    else col_mean_seq_kernel<double><<<g, CM_T, 0, s>>>((const double*)X, n, ld, D, sums, init, 1);
     DA_CHECK_LAUNCH("col_mean_seq_kernel");
     return 0;
 }

@@ -16,6 +16,7 @@
 //   3. one warp per (codeword, column chunk) folds the leaf sums back up the
 //      same recursion, adds the first row, and divides by the count.
 // The result is deterministic (no float atomics) and equal to the reference.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -312,7 +313,8 @@ __global__ void __launch_bounds__(GS_PLAN_MAXK) leaf_plan_kernel(const int32_t* 
         while (sp) {
             const int x = st[(--sp) * T + t];
             if (x <= 128) {
-                leaves[out++] = make_int4(t, rest0 + lo, x, 0);
+                leaves[out] = make_int4(t, rest0 + lo, x, out);
+                ++out;
                 lo += x;
                 continue;
             }
@@ -343,7 +345,8 @@ __global__ void __launch_bounds__(GS_WALK_T) leaf_enum_kernel(const int32_t* __r
         --sp;
         const int lo = st_lo[sp][t], x = st_n[sp][t];
         if (x <= 128) {
-            leaves[out++] = make_int4(k, rest0 + lo, x, 0);
+            leaves[out] = make_int4(k, rest0 + lo, x, out);
+            ++out;
             continue;
         }
         int n2 = x / 2; n2 -= n2 % 8;
@@ -423,7 +426,7 @@ __global__ void __launch_bounds__(256, 2) leaf_sum_kernel(const double* __restri
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-        if (cols[q] < D) leaf_sums[leaf * D + cols[q]] = res[q];
+        if (cols[q] < D) leaf_sums[(long long)L.w * D + cols[q]] = res[q];
 }
 
 // Rows up to D = 128 (DA_GS_NARROW_MAX; wider rows use leaf_sum_kernel): one
@@ -501,8 +504,8 @@ __global__ void __launch_bounds__(256) leaf_sum_narrow_kernel(const double* __re
 #pragma unroll
     for (int t = 0; t < 8; ++t)
         if (t < tn) { r0 = dadd(r0, w0[t]); r1 = dadd(r1, w1[t]); }
-    if (c0 < D) leaf_sums[leaf * D + c0] = r0;
-    if (c1 < D) leaf_sums[leaf * D + c1] = r1;
+    if (c0 < D) leaf_sums[(long long)L.w * D + c0] = r0;
+    if (c1 < D) leaf_sums[(long long)L.w * D + c1] = r1;
 }
 
 // One warp (one block) per (codeword, column chunk): fold leaves up the
@@ -520,7 +523,8 @@ __global__ void __launch_bounds__(32) seg_finish_kernel(const double* __restrict
                                                         const int32_t* __restrict__ leaf_base,
                                                         const int32_t* __restrict__ n_leaves_total,
                                                         const double* __restrict__ leaf_sums, int K, int n_chunks,
-                                                        int mode, double* __restrict__ out, long long ldo) {
+                                                        int mode, double* __restrict__ out, long long ldo,
+                                                        const double* __restrict__ first_rows = nullptr) {
     __shared__ int s_n[GS_DMAX + 1];
     __shared__ int s_state[GS_DMAX + 1];
     __shared__ double s_left[GS_DMAX][4][32];
@@ -540,12 +544,20 @@ __global__ void __launch_bounds__(32) seg_finish_kernel(const double* __restrict
         }
         return;
     }
-    const long long first = order[seg_start[k]];
     double tot[4];
+    if (first_rows) {   // sharded: the segment's first row, gathered from the shard holding it
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        int col = chunk * GS_COLS + lane + 32 * q;
-        tot[q] = (col < D) ? X[first * ldx + col] : 0.0;
+        for (int q = 0; q < 4; ++q) {
+            int col = chunk * GS_COLS + lane + 32 * q;
+            tot[q] = (col < D) ? first_rows[(long long)k * D + col] : 0.0;
+        }
+    } else {
+        const long long first = order[seg_start[k]];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            int col = chunk * GS_COLS + lane + 32 * q;
+            tot[q] = (col < D) ? X[first * ldx + col] : 0.0;
+        }
     }
     if (c >= 2) {
         const long long lf0 = leaf_base[k];
@@ -624,6 +636,32 @@ __global__ void __launch_bounds__(32) seg_finish_kernel(const double* __restrict
     }
 }
 
+// Stable counting sort of the labels: counts[K], seg[K] (segment starts),
+// order[n] (row ids in label order, rows in increasing order within a label).
+static int gs_stable_sort(const int32_t* labels, long long n, int K, int T, int32_t* hist, int32_t* counts,
+                          int32_t* seg, int32_t* total, int32_t* order, cudaStream_t s) {
+    const long long KT = (long long)K * T;
+    DA_CUDA(cudaMemsetAsync(hist, 0, sizeof(int32_t) * (KT + 1), s));
+    size_t sh = (K <= GS_SMEM_HIST) ? sizeof(int32_t) * K : 0;
+    tile_hist_kernel<<<T, 256, sh, s>>>(labels, n, K, T, hist);
+    DA_CHECK_LAUNCH("tile_hist_kernel");
+    label_tile_scan_kernel<<<grid_for(K, 8), 256, 0, s>>>(hist, K, T, counts);
+    DA_CHECK_LAUNCH("label_tile_scan_kernel");
+    DA_CUDA(cudaMemcpyAsync(seg, counts, sizeof(int32_t) * K, cudaMemcpyDeviceToDevice, s));
+    exclusive_scan_kernel<<<1, 1024, 0, s>>>(seg, K, total);
+    DA_CHECK_LAUNCH("exclusive_scan_kernel(counts)");
+    add_seg_start_kernel<<<grid_for(KT, 256, 1LL << 31), 256, 0, s>>>(hist, K, T, seg);
+    DA_CHECK_LAUNCH("add_seg_start_kernel");
+    if ((size_t)GS_SW * K * sizeof(int32_t) <= 48 * 1024) {
+        stable_scatter4_kernel<<<T, 32 * GS_SW, sizeof(int32_t) * GS_SW * K, s>>>(labels, n, K, T, hist, order);
+        DA_CHECK_LAUNCH("stable_scatter4_kernel");
+    } else {
+        stable_scatter_kernel<<<T, 32, sh, s>>>(labels, n, K, T, hist, order);
+        DA_CHECK_LAUNCH("stable_scatter_kernel");
+    }
+    return 0;
+}
+
 // Host driver.  X: (n, D) float64 rows (leading dim ldx); labels int32 in [0,K).
 // Writes counts[K]; mode 0: out[k] = mean for non-empty k (empty rows untouched);
 // mode 1: out[k] = raw sum (0 for empty).
@@ -655,23 +693,9 @@ int launch_group_sums(const double* X, long long n, long long ldx, int D, const 
     double* lsum = (double*)(base + o_lsum);
 
     ProfScope ps("group_sums", s);
-    DA_CUDA(cudaMemsetAsync(hist, 0, sizeof(int32_t) * (KT + 1), s));
-    size_t sh = (K <= GS_SMEM_HIST) ? sizeof(int32_t) * K : 0;
-    tile_hist_kernel<<<T, 256, sh, s>>>(labels, n, K, T, hist);
-    DA_CHECK_LAUNCH("tile_hist_kernel");
-    label_tile_scan_kernel<<<grid_for(K, 8), 256, 0, s>>>(hist, K, T, counts);
-    DA_CHECK_LAUNCH("label_tile_scan_kernel");
-    DA_CUDA(cudaMemcpyAsync(seg, counts, sizeof(int32_t) * K, cudaMemcpyDeviceToDevice, s));
-    exclusive_scan_kernel<<<1, 1024, 0, s>>>(seg, K, total);
-    DA_CHECK_LAUNCH("exclusive_scan_kernel(counts)");
-    add_seg_start_kernel<<<grid_for(KT, 256, 1LL << 31), 256, 0, s>>>(hist, K, T, seg);
-    DA_CHECK_LAUNCH("add_seg_start_kernel");
-    if ((size_t)GS_SW * K * sizeof(int32_t) <= 48 * 1024) {
-        stable_scatter4_kernel<<<T, 32 * GS_SW, sizeof(int32_t) * GS_SW * K, s>>>(labels, n, K, T, hist, order);
-        DA_CHECK_LAUNCH("stable_scatter4_kernel");
-    } else {
-        stable_scatter_kernel<<<T, 32, sh, s>>>(labels, n, K, T, hist, order);
-        DA_CHECK_LAUNCH("stable_scatter_kernel");
+    {
+        const int rc = gs_stable_sort(labels, n, K, T, hist, counts, seg, total, order, s);
+        if (rc) return rc;
     }
     if (K <= GS_PLAN_MAXK) {
         int T = 32;
@@ -739,6 +763,289 @@ int launch_label_order(const int32_t* labels, long long n, int K, int32_t* order
     DA_CHECK_LAUNCH("seg_counts_kernel");
     stable_scatter_kernel<<<T, 32, sh, s>>>(labels, n, K, T, hist, order_out);
     DA_CHECK_LAUNCH("stable_scatter_kernel");
+    return 0;
+}
+
+
+// ============================================================================
+// Row-sharded Lloyd update with the reference's summation order (bit-identical
+// to the one-GPU launch_group_sums over the concatenated shards).
+//
+// Label k's global segment is the concatenation of every shard's label-k rows
+// (shards are rank-ordered, rows in order within a shard), so shard r owns the
+// positions [off_k, off_k + c_k) of it, off_k = sum of the counts of shards
+// < r.  The pairwise recursion over the segment's rest is a function of the
+// global count n_k alone, so every shard enumerates the same leaves.  Leaves
+// inside a shard are summed locally with the normal leaf kernels; a leaf cut by
+// a shard boundary is a chain of partial leaf states (the 8 interleaved
+// accumulators, or the combined sum once the accumulator rows are done) handed
+// from shard to shard, W - 1 neighbour rounds (a leaf can cross every shard).
+// Leaf sums land in a global leaf-indexed buffer that is -0.0 everywhere this
+// shard does not own a leaf (x + -0.0 == x for every x, signed zeros included),
+// together with the segments' first rows; one allreduce completes it and every
+// shard folds the same tree.  The host side is distributed.py / _engine.py.
+
+namespace {
+constexpr int GSS_SLOT = 20;   // scratch slot holding the shard's sort + plan between calls
+struct ShardState {
+    int32_t* hist; int32_t* order; int32_t* seg; int32_t* total; int32_t* cnt;
+    int32_t* goff; int32_t* nleaf; int32_t* leaf_base; int32_t* nlocal; int4* local_leaves;
+    int4* itemL; int4* itemR; int32_t* first_pos;
+    long long n, cap; int K, T;
+};
+ShardState g_shard;   // one shard per process and device (the loops call in sequence)
+
+__device__ int gs_count_leaves(int m) {
+    if (m <= 0) return 0;
+    int st[GS_DMAX], sp = 0, leaves = 0;
+    st[sp++] = m;
+    while (sp) {
+        const int x = st[--sp];
+        if (x <= 128) { ++leaves; continue; }
+        int n2 = x / 2; n2 -= n2 % 8;
+        st[sp++] = x - n2;
+        st[sp++] = n2;
+    }
+    return leaves;
+}
+}  // namespace
+
+// per label: global count, this shard's offset in the segment, global leaf count
+__global__ void shard_label_kernel(const int32_t* __restrict__ cnt_all, int W, int rank, int K,
+                                   int32_t* __restrict__ gcount, int32_t* __restrict__ goff,
+                                   int32_t* __restrict__ nleaf) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    int n = 0, off = 0;
+    for (int r = 0; r < W; ++r) {
+        const int c = cnt_all[(long long)r * K + k];
+        if (r < rank) off += c;
+        n += c;
+    }
+    gcount[k] = n;
+    goff[k] = off;
+    nleaf[k] = gs_count_leaves(n >= 2 ? n - 1 : 0);
+}
+
+// per label: walk the global leaves of pairwise(rest) left to right and
+// classify each against this shard's rest range [ra, rb):
+//   inside        -> local leaf (k, local sorted position, length, global index)
+//   cut, s > 0    -> itemL[k]: continues a state received from the left
+//   cut, s == 0   -> itemR[k]: starts here, its state goes right
+// items: (global leaf index, local sorted position of leaf row s, s + 256 e, x);
+// a label with no rows here gets itemL = (-2, ...): forward the state as is.
+__global__ void shard_enum_kernel(const int32_t* __restrict__ gcount, const int32_t* __restrict__ goff,
+                                  const int32_t* __restrict__ cnt, const int32_t* __restrict__ seg,
+                                  const int32_t* __restrict__ leaf_base, int K, int4* __restrict__ local_leaves,
+                                  int32_t* __restrict__ nlocal, int4* __restrict__ itemL, int4* __restrict__ itemR,
+                                  int32_t* __restrict__ first_pos) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    const int n = gcount[k], off = goff[k], c = cnt[k];
+    itemL[k] = make_int4(c == 0 ? -2 : -1, 0, 0, 0);
+    itemR[k] = make_int4(-1, 0, 0, 0);
+    first_pos[k] = (off == 0 && c > 0) ? seg[k] : -1;
+    if (c == 0 || n < 2) return;
+    // rest index q <-> segment position q + 1
+    const int ra = off > 0 ? off - 1 : 0, rb = off - 1 + c;
+    if (rb <= ra) return;
+    auto lpos = [&](int q) { return seg[k] + (q + 1 - off); };
+    int st_lo[GS_DMAX], st_n[GS_DMAX], sp = 0;
+    st_lo[sp] = 0; st_n[sp] = n - 1; ++sp;
+    int idx = leaf_base[k];
+    while (sp) {
+        --sp;
+        const int lo = st_lo[sp], x = st_n[sp];
+        if (x <= 128) {
+            const int gi = idx++;
+            if (lo + x <= ra || lo >= rb) continue;
+            if (lo >= ra && lo + x <= rb) {
+                const int slot = atomicAdd(nlocal, 1);
+                local_leaves[slot] = make_int4(k, lpos(lo), x, gi);
+            } else {
+                const int s = max(ra, lo) - lo, e = min(rb, lo + x) - lo;
+                const int4 it = make_int4(gi, lpos(lo + s), s + 256 * e, x);
+                if (s > 0) itemL[k] = it;
+                else itemR[k] = it;
+            }
+            continue;
+        }
+        int n2 = x / 2; n2 -= n2 % 8;
+        st_lo[sp] = lo + n2; st_n[sp] = x - n2; ++sp;
+        st_lo[sp] = lo; st_n[sp] = n2; ++sp;
+    }
+}
+
+__global__ void fill_neg_zero_kernel(double* __restrict__ a, long long len) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (long long)gridDim.x * blockDim.x)
+        a[i] = -0.0;
+}
+
+__global__ void shard_first_rows_kernel(const double* __restrict__ X, long long ldx, int d, int K,
+                                        const int32_t* __restrict__ order, const int32_t* __restrict__ first_pos,
+                                        double* __restrict__ out) {
+    const int k = blockIdx.x;
+    const int fp = first_pos[k];
+    if (fp < 0) return;
+    const long long row = order[fp];
+    for (int c = threadIdx.x; c < d; c += blockDim.x) out[(long long)k * d + c] = X[row * ldx + c];
+}
+
+// One warp per label: run the leaf rule over this shard's rows [s, e) of a cut
+// leaf, continuing the received state when s > 0.  State layout [K][8][d]:
+// the 8 accumulators while e < x8 (rows of the 8-way part), else the combined
+// running sum in slot 0.  e == x: the finished leaf sum goes to red.
+__global__ void shard_edge_kernel(const double* __restrict__ X, long long ldx, int d, int K,
+                                  const int32_t* __restrict__ order, const int4* __restrict__ items, int want_cont,
+                                  const double* __restrict__ recv, double* __restrict__ send,
+                                  double* __restrict__ red) {
+    const int lane = threadIdx.x & 31;
+    const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (k >= K) return;
+    const int4 it = items[k];
+    const long long sb = (long long)k * 8 * d;
+    if (it.x == -2) {                        // no rows of this label here: forward the state
+        if (want_cont)
+            for (int e = lane; e < 8 * d; e += 32) send[sb + e] = recv[sb + e];
+        return;
+    }
+    if (it.x < 0) return;
+    const int s = it.z & 255, e = it.z >> 8, x = it.w;
+    if ((s > 0) != (want_cont != 0)) return;
+    const int x8 = x >= 8 ? x - (x % 8) : 0;
+    for (int c = lane; c < d; c += 32) {
+        double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        double res = 0.0;
+        if (s > 0) {
+            if (s < x8) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[j] = recv[sb + (long long)j * d + c];
+            } else {
+                res = recv[sb + c];
+            }
+        }
+        for (int i = s; i < e; ++i) {
+            const double v = X[(long long)order[it.y + (i - s)] * ldx + c];
+            if (i < x8) {
+                acc[i & 7] = i < 8 ? v : dadd(acc[i & 7], v);
+                if (i == x8 - 1)
+                    res = dadd(dadd(dadd(acc[0], acc[1]), dadd(acc[2], acc[3])),
+                               dadd(dadd(acc[4], acc[5]), dadd(acc[6], acc[7])));
+            } else {
+                res = dadd(res, v);
+            }
+        }
+        if (e == x) {
+            red[(long long)it.x * d + c] = res;
+        } else if (e < x8) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) send[sb + (long long)j * d + c] = acc[j];
+        } else {
+            send[sb + c] = res;
+        }
+    }
+}
+
+int launch_gs_shard_sort(const double* X, long long n, long long ldx, int d, const int32_t* labels, int K,
+                         int32_t* counts_local, cudaStream_t s) {
+    (void)X; (void)ldx; (void)d;
+    ShardState& S = g_shard;
+    S.n = n; S.K = K;
+    S.T = (int)std::max(1LL, (n + GS_TILE - 1) / GS_TILE);
+    const long long KT = (long long)K * S.T;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
+    const size_t o_hist = take(sizeof(int32_t) * (KT + 1)), o_order = take(sizeof(int32_t) * std::max(1LL, n));
+    const size_t o_seg = take(sizeof(int32_t) * K), o_total = take(sizeof(int32_t) * 4);
+    const size_t o_cnt = take(sizeof(int32_t) * K), o_goff = take(sizeof(int32_t) * K);
+    const size_t o_nleaf = take(sizeof(int32_t) * (K + 1)), o_base = take(sizeof(int32_t) * (K + 1));
+    const size_t o_il = take(sizeof(int4) * K), o_ir = take(sizeof(int4) * K), o_fp = take(sizeof(int32_t) * K);
+    const size_t o_ll = take(0);   // local leaves: sized in the plan (needs the global row count)
+    char* base = (char*)scratch(GSS_SLOT, off, s);
+    if (!base) return fail_cuda(cudaErrorMemoryAllocation, "shard group sums scratch");
+    S.hist = (int32_t*)(base + o_hist); S.order = (int32_t*)(base + o_order); S.seg = (int32_t*)(base + o_seg);
+    S.total = (int32_t*)(base + o_total); S.cnt = (int32_t*)(base + o_cnt); S.goff = (int32_t*)(base + o_goff);
+    S.nleaf = (int32_t*)(base + o_nleaf); S.leaf_base = (int32_t*)(base + o_base);
+    S.itemL = (int4*)(base + o_il); S.itemR = (int4*)(base + o_ir); S.first_pos = (int32_t*)(base + o_fp);
+    S.nlocal = S.total + 2;
+    (void)o_ll;
+    ProfScope ps("group_sums", s);
+    if (n == 0) {
+        DA_CUDA(cudaMemsetAsync(S.cnt, 0, sizeof(int32_t) * K, s));
+        DA_CUDA(cudaMemsetAsync(S.seg, 0, sizeof(int32_t) * K, s));
+    } else {
+        const int rc = gs_stable_sort(labels, n, K, S.T, S.hist, S.cnt, S.seg, S.total, S.order, s);
+        if (rc) return rc;
+    }
+    if (counts_local != S.cnt)
+        DA_CUDA(cudaMemcpyAsync(counts_local, S.cnt, sizeof(int32_t) * K, cudaMemcpyDeviceToDevice, s));
+    return 0;
+}
+
+int launch_gs_shard_plan(const double* X, long long n, long long ldx, int d, int K, const int32_t* cnt_all, int W,
+                         int rank, long long cap, double* red, double* send, int32_t* gcount, cudaStream_t s) {
+    ShardState& S = g_shard;
+    if (S.K != K || S.n != n) return fail_arg("shard plan: call da_gs_shard_sort on the same rows first");
+    S.cap = cap;
+    int4* ll = (int4*)scratch(GSS_SLOT + 1, sizeof(int4) * (size_t)cap, s);
+    if (!ll) return fail_cuda(cudaErrorMemoryAllocation, "shard leaf list");
+    S.local_leaves = ll;
+    ProfScope ps("group_sums", s);
+    shard_label_kernel<<<grid_for(K, 128), 128, 0, s>>>(cnt_all, W, rank, K, gcount, S.goff, S.nleaf);
+    DA_CHECK_LAUNCH("shard_label_kernel");
+    DA_CUDA(cudaMemcpyAsync(S.leaf_base, S.nleaf, sizeof(int32_t) * K, cudaMemcpyDeviceToDevice, s));
+    exclusive_scan_kernel<<<1, 1024, 0, s>>>(S.leaf_base, K, S.total + 1);
+    DA_CHECK_LAUNCH("exclusive_scan_kernel(shard leaves)");
+    DA_CUDA(cudaMemsetAsync(S.nlocal, 0, sizeof(int32_t), s));
+    shard_enum_kernel<<<grid_for(K, 128), 128, 0, s>>>(gcount, S.goff, S.cnt, S.seg, S.leaf_base, K, ll, S.nlocal,
+                                                       S.itemL, S.itemR, S.first_pos);
+    DA_CHECK_LAUNCH("shard_enum_kernel");
+    const long long len = cap * d + (long long)K * d;
+    fill_neg_zero_kernel<<<grid_for(len, 256, 4096), 256, 0, s>>>(red, len);
+    DA_CHECK_LAUNCH("fill_neg_zero_kernel");
+    if (n > 0) {
+        ProfScope ps3("group_sums_leaf", s);
+        static const int narrow_max = getenv("DA_GS_NARROW_MAX") ? atoi(getenv("DA_GS_NARROW_MAX")) : 128;
+        const long long maxl = std::min(cap, n / 1 + 1);
+        if (d <= narrow_max) {
+            const long long ntask = maxl * ((d + 7) / 8);
+            leaf_sum_narrow_kernel<<<grid_for(ntask, 8, 1LL << 31), 256, 0, s>>>(X, ldx, d, S.order, ll, S.nlocal, red);
+            DA_CHECK_LAUNCH("leaf_sum_narrow_kernel");
+        } else {
+            const int n_chunks = (d + GS_COLS - 1) / GS_COLS;
+            leaf_sum_kernel<<<grid_for(maxl * n_chunks, 8, 1LL << 31), 256, 0, s>>>(X, ldx, d, S.order, ll, S.nlocal,
+                                                                                   n_chunks, red);
+            DA_CHECK_LAUNCH("leaf_sum_kernel");
+        }
+        shard_first_rows_kernel<<<K, 128, 0, s>>>(X, ldx, d, K, S.order, S.first_pos, red + cap * d);
+        DA_CHECK_LAUNCH("shard_first_rows_kernel");
+        // round 0: the cut leaves that start here
+        shard_edge_kernel<<<grid_for(K, 8), 256, 0, s>>>(X, ldx, d, K, S.order, S.itemR, 0, nullptr, send, red);
+        DA_CHECK_LAUNCH("shard_edge_kernel(start)");
+    }
+    return 0;
+}
+
+int launch_gs_shard_round(const double* X, long long ldx, int d, int K, const double* recv, double* send, double* red,
+                          cudaStream_t s) {
+    ShardState& S = g_shard;
+    if (S.K != K) return fail_arg("shard round: no plan for K=%d", K);
+    ProfScope ps("group_sums", s);
+    shard_edge_kernel<<<grid_for(K, 8), 256, 0, s>>>(X, ldx, d, K, S.order, S.itemL, 1, recv, send, red);
+    DA_CHECK_LAUNCH("shard_edge_kernel(continue)");
+    return 0;
+}
+
+int launch_gs_shard_fold(int d, int K, const double* red, long long cap, const int32_t* gcount, int mode, double* out,
+                         long long ldo, cudaStream_t s) {
+    ShardState& S = g_shard;
+    if (S.K != K || S.cap != cap) return fail_arg("shard fold: no plan for K=%d cap=%lld", K, cap);
+    ProfScope ps("group_sums", s);
+    const int n_chunks = (d + GS_COLS - 1) / GS_COLS;
+    seg_finish_kernel<<<(unsigned)((long long)K * n_chunks), 32, 0, s>>>(
+        nullptr, 0, d, nullptr, gcount, nullptr, S.leaf_base, S.total + 1, red, K, n_chunks, mode, out, ldo,
+        red + cap * d);
+    DA_CHECK_LAUNCH("seg_finish_kernel(shard)");
     return 0;
 }
 

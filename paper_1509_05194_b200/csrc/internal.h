@@ -24,11 +24,15 @@ struct GemmArgs {
     int nb2, ksplit; long long kchunk; const long long* kstarts;  // kstarts[ksplit+1] overrides kchunk
     // epi 0: acc; 1: acc + evec[j]; 2: evec[j] - 2*acc; 3: max(0, (ivec[i] - 2*acc) + evec[j])
     int epi; const double* evec; const double* ivec;
+    // optional D x D accumulator the chain of k-slice 0 continues from (sharded PCA)
+    const double* cinit;
 };
 
 int launch_gemm(const GemmArgs& g, int nb1, cudaStream_t s);
 int launch_reduce_partials(const double* P, int nz, long long len, double scale_div, double* out, cudaStream_t s);
 int launch_col_mean(const void* X, int x_f32, long long n, long long ld, int D, double* mean, cudaStream_t s);
+int launch_col_sums(const void* X, int x_f32, long long n, long long ld, int D, const double* init, double* sums,
+                    cudaStream_t s);
 int launch_col_mean_chunked(const void* X, int x_f32, long long n, long long ld, int D, double* mean, cudaStream_t s);
 int launch_accumulate_partials(const double* P, int nz, long long len, double scale_div, int accumulate,
                                double* out, cudaStream_t s);
@@ -41,6 +45,14 @@ int launch_assign(const void* X, int x_is_f32, long long n, long long ldx, int d
 
 int launch_group_sums(const double* X, long long n, long long ldx, int D, const int32_t* labels, int K, int mode,
                       double* out, long long ldo, int32_t* counts, cudaStream_t s);
+int launch_gs_shard_sort(const double* X, long long n, long long ldx, int d, const int32_t* labels, int K,
+                         int32_t* counts_local, cudaStream_t s);
+int launch_gs_shard_plan(const double* X, long long n, long long ldx, int d, int K, const int32_t* cnt_all, int W,
+                         int rank, long long cap, double* red, double* send, int32_t* gcount, cudaStream_t s);
+int launch_gs_shard_round(const double* X, long long ldx, int d, int K, const double* recv, double* send, double* red,
+                          cudaStream_t s);
+int launch_gs_shard_fold(int d, int K, const double* red, long long cap, const int32_t* gcount, int mode, double* out,
+                         long long ldo, cudaStream_t s);
 int launch_label_order(const int32_t* labels, long long n, int K, int32_t* order_out, int32_t* counts,
                        cudaStream_t s);
 

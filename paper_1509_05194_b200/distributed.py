@@ -6,7 +6,10 @@ the ones the algorithm has:
 
   * Lloyd update      allreduce of the K x D float64 per-codeword sums and
                       the K counts (plus the changed-row count);
-  * PCA               allreduce of the column sums, then of the centred Gram;
+  * PCA               a rank-ordered ring: each shard continues the column-sum
+                      chains and the covariance's OpenBLAS block chains where
+                      the previous shard stopped, so mean and covariance are
+                      bit-identical to the unsharded reference (exact_pca_moments);
   * empty reseed      allgather of each shard's local worst (err, row id, row)
                       candidates, merged with the reference's order
                       (descending error, ties -> higher global row id);
@@ -22,17 +25,23 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-__all__ = ["Comm", "merge_worst", "shard_rows", "train_from_scratch_sharded", "da_sweep_sharded"]
+__all__ = ["Comm", "merge_worst", "shard_rows", "train_from_scratch_sharded", "da_sweep_sharded",
+           "blas_block_starts", "cov_segments", "exact_pca_moments"]
 
 
 class Comm:
     """Thin torch.distributed wrapper used by the engine (`comm=` argument)."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, exact: bool = True):
         import torch.distributed as dist
 
         self.dist = dist
         self.group = group
+        # exact=True: Lloyd sums in the reference's order across shards
+        # (bit-identical to one GPU; W-1 neighbour rounds + a leaf-sum allreduce
+        # per update).  exact=False: one allreduce of shard partial sums per
+        # update (same algorithm, float64 sums in another order).
+        self.exact = exact
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self._bound = None
@@ -58,6 +67,41 @@ class Comm:
         self.dist.all_gather(parts, src, group=self.group)
         out = torch.cat(parts, dim=0)
         return out.to(t.device) if t.is_cuda else out
+
+    def _staged(self, t: torch.Tensor) -> torch.Tensor:
+        return t.cpu() if (self._host_staged and t.is_cuda) else t
+
+    def send_(self, t: torch.Tensor, dst: int) -> None:
+        self.dist.send(self._staged(t.contiguous()), dst, group=self.group)
+
+    def recv_(self, t: torch.Tensor, src: int) -> torch.Tensor:
+        buf = self._staged(t)
+        self.dist.recv(buf, src, group=self.group)
+        if buf is not t:
+            t.copy_(buf)
+        return t
+
+    def broadcast_(self, t: torch.Tensor, src: int) -> torch.Tensor:
+        buf = self._staged(t)
+        self.dist.broadcast(buf, src, group=self.group)
+        if buf is not t:
+            t.copy_(buf)
+        return t
+
+    def shift_(self, send: torch.Tensor, recv: torch.Tensor) -> torch.Tensor:
+        """send -> rank + 1 and recv <- rank - 1 at once (the ends skip theirs)."""
+        ops = []
+        sb, rb = self._staged(send.contiguous()), self._staged(recv)
+        if self.rank + 1 < self.world:
+            ops.append(self.dist.P2POp(self.dist.isend, sb, self.rank + 1, group=self.group))
+        if self.rank > 0:
+            ops.append(self.dist.P2POp(self.dist.irecv, rb, self.rank - 1, group=self.group))
+        if ops:
+            for w in self.dist.batch_isend_irecv(ops):
+                w.wait()
+        if rb is not recv and self.rank > 0:
+            recv.copy_(rb)
+        return recv
 
     def sizes(self, n_local: int) -> list:
         """Every rank's shard size.  The allgather runs unless bind_rows() already
@@ -88,6 +132,110 @@ def shard_rows(n: int, world: int, rank: int) -> slice:
     base, extra = divmod(n, world)
     lo = rank * base + min(rank, extra)
     return slice(lo, lo + base + (1 if rank < extra else 0))
+
+
+def blas_block_starts(n: int) -> list:
+    """Row offsets of OpenBLAS's GEMM_Q blocks over an n-long contraction (the
+    dsyrk behind Xc.T @ Xc, clustering.py:96): 384 rows, the last two balanced
+    (common.cuh: blas_block_len)."""
+    q = 384
+    starts = [0]
+    while starts[-1] < n:
+        rest = n - starts[-1]
+        step = q if rest >= 2 * q else (((rest // 2 + 1) // 2) * 2 if rest > q else rest)
+        starts.append(starts[-1] + step)
+    return starts
+
+
+def cov_segments(n_total: int, lo: int, hi: int):
+    """This shard's pieces of the global blocks: (segments as local row offsets
+    [(r0, r1), ...], cont_first, open_last, total_valid_in).  cont_first: the
+    first piece continues a block begun on an earlier shard; open_last: the
+    last piece's block ends on a later shard; total_valid_in: some block
+    completed before this shard (the incoming running total is live)."""
+    st = blas_block_starts(n_total)
+    segs, blocks = [], []
+    for a, b in zip(st[:-1], st[1:]):
+        if a < hi and b > lo:
+            segs.append((max(a, lo) - lo, min(b, hi) - lo))
+            blocks.append((a, b))
+    cont_first = bool(blocks) and blocks[0][0] < lo
+    open_last = bool(blocks) and blocks[-1][1] > hi
+    total_valid_in = len(st) > 1 and st[1] <= lo
+    return segs, cont_first, open_last, total_valid_in
+
+
+def exact_pca_moments(X, comm: "Comm", ops):
+    """Mean (D,) and covariance (D, D) of the row-sharded X (clustering.py:93-96),
+    bit-identical to the unsharded computation.
+
+    Both reductions of the reference are sequential in row order: X.mean(axis=0)
+    is one add chain per column, and OpenBLAS's dsyrk cuts the n-long contraction
+    into GEMM_Q blocks (each an FMA chain from zero) added into C in order.  So
+    shards run a rank-ordered ring: rank r receives the running column sums,
+    continues them over its rows and forwards them; then it receives the
+    running covariance total and the carried chain of a block cut at the shard
+    boundary, finishes that chain, adds its own blocks in order (their chains
+    were computed before the receive, in parallel with the other ranks) and
+    forwards the total plus its own cut chain.  The last rank divides and
+    broadcasts.  `ops` supplies the arithmetic (device kernels in production,
+    numpy in the CPU ring tests): zeros(shape), col_sums(X, init|None),
+    div(t, d), cov_chains(X, mean, starts, init|None) -> (nseg, D, D),
+    fold(total|None, parts) -> total."""
+    n, D = X.shape
+    sizes = comm.sizes(n)
+    N = int(sum(sizes))
+    lo = int(sum(sizes[: comm.rank]))
+    hi = lo + n
+    last = comm.world - 1
+    prev, nxt = comm.rank - 1, comm.rank + 1
+    # ---- column sums: one chain per column across the shards
+    S = ops.zeros((D,))
+    if prev >= 0:
+        comm.recv_(S, prev)
+    if n:
+        S = ops.col_sums(X, S if lo > 0 else None)
+    if nxt <= last:
+        comm.send_(S, nxt)
+    mean = ops.div(S, N) if comm.rank == last else ops.zeros((D,))
+    comm.broadcast_(mean, last)
+    if N <= D:
+        return mean, None
+    # ---- covariance: block chains, block totals added in global order
+    segs, cont_first, open_last, t_valid = cov_segments(N, lo, hi)
+    first = 1 if cont_first else 0
+    parts = None
+    if len(segs) > first:
+        st = [segs[first][0]] + [b for _, b in segs[first:]]
+        parts = ops.cov_chains(X, mean, st, None)      # before the receive: in parallel
+    state = ops.zeros((2, D, D))
+    if prev >= 0:
+        comm.recv_(state, prev)
+    T, C = state[0], state[1]
+    if not segs:
+        out = state                                   # empty shard: pass everything on
+    else:
+        chains = list(parts) if parts is not None else []
+        if cont_first:
+            chain0 = ops.cov_chains(X, mean, [segs[0][0], segs[0][1]], C)[0]
+            chains = [chain0] + chains
+        ncomplete = len(chains) - (1 if open_last else 0)
+        out = ops.zeros((2, D, D))
+        total = T if t_valid else None
+        if cont_first and ncomplete >= 1:
+            total = ops.fold(total, chain0.reshape(1, D, D))
+        k = ncomplete - (1 if cont_first else 0)
+        if k > 0:
+            total = ops.fold(total, parts[:k])
+        if total is not None:
+            out[0] = total
+        if open_last:
+            out[1] = chains[-1]                       # the block continues on the next shard
+    if nxt <= last:
+        comm.send_(out, nxt)
+    cov = ops.div(out[0], N - 1) if comm.rank == last else ops.zeros((D, D))
+    comm.broadcast_(cov, last)
+    return mean, cov
 
 
 def merge_worst(all_err: np.ndarray, all_gid: np.ndarray, e: int) -> np.ndarray:

@@ -5,6 +5,7 @@ partials (computed with numpy) through the production merge code
 (_engine._sharded_update, _engine._reseed_sharded, distributed.Comm) and
 check the result against the unsharded reference semantics."""
 
+import functools
 import os
 import socket
 
@@ -129,3 +130,95 @@ def test_shard_rows_partition(n, world):
         assert a.stop == b.start
     sizes = [p.stop - p.start for p in parts]
     assert max(sizes) - min(sizes) <= 1
+
+
+# ---------------------------------------------------------------------------
+# sharded PCA ring (distributed.exact_pca_moments): the chains must be cut and
+# continued so that every shard layout gives the one-shard bits.
+
+
+class _NumpyPcaOps:
+    """Host stand-in for the device kernels: the same dependency structure
+    (one add chain per column, one accumulation chain per cov block, block
+    totals added in order), plain float64 multiply + add.  Any reordering of
+    those chains across a shard boundary changes the bits."""
+
+    def zeros(self, shape):
+        return torch.zeros(shape, dtype=torch.float64)
+
+    def div(self, t, d):
+        return t / torch.full_like(t, float(d))
+
+    def col_sums(self, X, init):
+        s = init.clone() if init is not None else torch.zeros(X.shape[1], dtype=torch.float64)
+        for r in range(X.shape[0]):
+            s = s + X[r]
+        return s
+
+    def cov_chains(self, X, mean, starts, init):
+        out = []
+        for i in range(len(starts) - 1):
+            acc = init.clone() if (i == 0 and init is not None) else torch.zeros((X.shape[1],) * 2, dtype=torch.float64)
+            for r in range(starts[i], starts[i + 1]):
+                xc = X[r] - mean
+                acc = acc + torch.outer(xc, xc)
+            out.append(acc)
+        return torch.stack(out)
+
+    def fold(self, total, parts):
+        s = total.clone() if total is not None else parts[0].clone()
+        for p in parts[(0 if total is not None else 1):]:
+            s = s + p
+        return s
+
+
+class _OneShard:
+    rank, world = 0, 1
+
+    def sizes(self, n):
+        return [n]
+
+    def broadcast_(self, t, src):
+        return t
+
+
+def _ring_data():
+    rng = np.random.default_rng(7)
+    return torch.from_numpy(rng.standard_normal((1000, 5)) * 10.0 ** rng.uniform(-2, 3, 5))
+
+
+RING_LAYOUTS = [[500, 500], [100, 200, 700], [0, 1000, 0], [384, 308, 308], [383, 2, 615], [1, 999]]
+
+
+def _ring_fn(layout, rank, world):
+    X = _ring_data()
+    lo = sum(layout[:rank])
+    comm = D.Comm()
+    comm.bind_rows(layout[rank])
+    mean, cov = D.exact_pca_moments(X[lo:lo + layout[rank]], comm, _NumpyPcaOps())
+    return mean.numpy(), cov.numpy()
+
+
+@pytest.mark.parametrize("layout", RING_LAYOUTS)
+def test_exact_pca_ring_equals_one_shard(layout):
+    X = _ring_data()
+    m1, c1 = D.exact_pca_moments(X, _OneShard(), _NumpyPcaOps())
+    # the column chains are numpy's own X.mean(axis=0) order
+    np.testing.assert_array_equal(m1.numpy(), X.numpy().mean(axis=0))
+    out = run(functools.partial(_ring_fn, layout), world=len(layout))
+    for r in range(len(layout)):
+        assert not isinstance(out[r], str), out[r]
+        np.testing.assert_array_equal(out[r][0], m1.numpy())
+        np.testing.assert_array_equal(out[r][1], c1.numpy())
+
+
+def test_cov_segments_cover_the_blocks():
+    st = D.blas_block_starts(1000)
+    assert st == [0, 384, 692, 1000]
+    segs, cf, ol, tv = D.cov_segments(1000, 100, 300)
+    assert segs == [(0, 200)] and cf and ol and not tv
+    segs, cf, ol, tv = D.cov_segments(1000, 384, 1000)
+    assert segs == [(0, 308), (308, 616)] and not cf and not ol and tv
+    for n in (1, 383, 384, 385, 767, 768, 769, 5000):
+        st = D.blas_block_starts(n)
+        assert st[-1] == n and all(0 < b - a <= 384 for a, b in zip(st[:-1], st[1:]))
