@@ -127,6 +127,35 @@ int da_gs_shard_round(const double* X, int64_t ldx, int d, int K, const double* 
 int da_gs_shard_fold(int d, int K, const double* red, int64_t cap_leaves, const int32_t* counts_global, int mode,
                      double* out, int64_t ldo, void* stream);
 
+/* One Lloyd iteration in one call (clustering.py:185-202, one GPU): C_out =
+ * C_prev (snap = C_prev too when non-NULL), C_out[k, :d] = reduceat-order mean
+ * of the rows labelled k by labels_prev (empty clusters keep C_prev's row),
+ * counts (K), then the assign of X[:, :d] against C_out into labels_out
+ * (d2_out optional: NULL = labels-only) counting rows whose label changed.
+ * flags_dev (2 uint64) = [rows changed, #empty clusters], copied to the pinned
+ * flags_host and followed by cudaEventRecord(event) when those are non-NULL.
+ * xx = row_sqnorms(X, d) of the rows (reused across iterations). */
+int da_lloyd_step(const double* X, int64_t n, int64_t ldx, int d, int K, const double* C_prev, double* C_out,
+                  int64_t ldc, double* snap, const int32_t* labels_prev, int32_t* labels_out, double* d2_out,
+                  const double* xx, int32_t* counts, unsigned long long* flags_dev, void* flags_host, void* event,
+                  void* stream);
+
+/* Sharded Lloyd iteration around the collective:
+ *   da_lloyd_prepare: C_out = C_prev (and snap), stats[0:2] = [*changed_prev, 0]
+ *                     (the previous assign's stats ride this update's allreduce);
+ *   da_lloyd_finish:  after the allreduce.  fast=1: red = [sums K*d | counts K |
+ *                     ..], C[k, :d] = sums / counts where counts > 0; fast=0: the
+ *                     means are already in C (da_gs_shard_fold) and counts are
+ *                     the global counts.  flags_dev (3 f64) = [#empty, stats[0],
+ *                     stats[1]] -> flags_host + event, *changed = 0, then (if
+ *                     labels_out) the assign of X against C like da_lloyd_step. */
+int da_lloyd_prepare(const double* C_prev, double* C_out, double* snap, int64_t elems,
+                     const unsigned long long* changed_prev, double* stats, void* stream);
+int da_lloyd_finish(int fast, const double* red, const int32_t* counts, int K, int d, double* C, int64_t ldc,
+                    const double* stats, double* flags_dev, void* flags_host, void* event, const double* X,
+                    int64_t n, int64_t ldx, const double* xx, const int32_t* labels_prev, int32_t* labels_out,
+                    double* d2_out, unsigned long long* changed, void* stream);
+
 /* Column means (PCA centre).  replaces X.mean(axis=0)   clustering.py:93 */
 int da_col_mean(const void* X, int x_f32, int64_t n, int64_t ld, int D, double* mean, void* stream);
 

@@ -266,19 +266,17 @@ def _lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, 
         done_ev = [torch.cuda.Event(), torch.cuda.Event()]
         snaps = [torch.empty_like(C), torch.empty_like(C)] if lazy else None
 
+        for ev in done_ev:
+            ev.record()                              # creates the event handles da_lloyd_step records into
+
         def launch(C_prev, labels_prev, slot):
             Cn, cn, fl = slots[slot]
-            if lazy:
-                snaps[slot].copy_(C_prev)            # the centroids the previous assign measured against
-            if Cn is not C_prev:
-                Cn.copy_(C_prev)                     # empty clusters keep their previous rows
-            native.da_group_sums(P(Xr), n, Xr.stride(0), active, P(labels_prev), K, 0, P(Cn), Cn.stride(0),
-                                 P(cn), stream())
-            fl.zero_()
-            fl[1:2].copy_((cn == 0).sum().view(1))
-            nl, ne = assign(Xr, active, Cn, prev=labels_prev, changed=fl[0:1], xx=xx, want_d2=not lazy)
-            flags_h[slot].copy_(fl, non_blocking=True)
-            done_ev[slot].record()
+            nl = torch.empty(n, dtype=I32, device=dev)
+            ne = None if lazy else torch.empty(n, dtype=F64, device=dev)
+            # group means, #empty, assign, flags -> pinned host, event: one call
+            native.da_lloyd_step(P(Xr), n, Xr.stride(0), active, K, P(C_prev), P(Cn), Cn.stride(0),
+                                 P(snaps[slot]) if lazy else None, P(labels_prev), P(nl), P(ne), P(xx), P(cn), P(fl),
+                                 P(flags_h[slot]), ctypes.c_void_p(done_ev[slot].cuda_event), stream())
             return [slot, labels_prev, nl, ne]
 
         gs_labels = None
@@ -398,36 +396,33 @@ def _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm, la
         else:
             dst[1:2].zero_()
 
+    for sl in slots:
+        sl[5].record()                               # creates the event handles da_lloyd_finish records into
+
     def launch(C_prev, labels_prev, slot, pchg, pne):
         Cn, red, cn, chg, fl, ev = slots[slot]
-        if lazy:
-            snaps[slot].copy_(C_prev)                # the centroids the previous assign measured against
-        if Cn is not C_prev:
-            Cn.copy_(C_prev)                         # empty clusters keep their previous rows
+        # C_out = C_prev (+ snapshot for a lazy reseed), previous assign's stats -> red[nst:]
+        native.da_lloyd_prepare(P(C_prev), P(Cn), P(snaps[slot]) if lazy else None, C.numel(), P(pchg),
+                                P(red[nst:]), stream())
+        if pne is not None and n:
+            native.da_np_sum(P(pne), n, 0, P(red[nst + 1:nst + 2]), stream())
         if exact:
             sh.plan(Xr, da, labels_prev, red, cn)
-            put_stats(red[nst:], pchg, pne)
-            comm.allreduce_(red)
-            sh.fold(da, red, cn, 0, Cn)
-            fl[0:1].copy_((cn == 0).sum().view(1))
         else:
-            sums = red[: K * da].view(K, da)
             if n:
-                native.da_group_sums(P(Xr), n, Xr.stride(0), da, P(labels_prev), K, 1, P(sums), da, P(cn), stream())
+                native.da_group_sums(P(Xr), n, Xr.stride(0), da, P(labels_prev), K, 1, P(red), da, P(cn), stream())
+                red[K * da:nst].copy_(cn)
             else:
                 red[:nst].zero_()
-                cn.zero_()
-            red[K * da:nst].copy_(cn)
-            put_stats(red[nst:], pchg, pne)
-            comm.allreduce_(red)
-            cnt = red[K * da:nst]
-            Cn[:, :da] = torch.where(cnt.unsqueeze(1) > 0, sums / cnt.unsqueeze(1), Cn[:, :da])
-            fl[0:1].copy_((cnt == 0).sum().view(1))
-        fl[1:3].copy_(red[nst:])
-        flags_h[slot].copy_(fl, non_blocking=True)
-        ev.record()                                  # the host's flags are ready after the allreduce
-        chg.zero_()
-        nl, ne = assign(Xr, active, Cn, prev=labels_prev, changed=chg, xx=xx, want_d2=not lazy)
+        comm.allreduce_(red)
+        if exact:
+            sh.fold(da, red, cn, 0, Cn)
+        nl = torch.empty(n, dtype=I32, device=dev)
+        ne = None if lazy else torch.empty(n, dtype=F64, device=dev)
+        # means (fast mode), flags -> pinned host + event, then the assign
+        native.da_lloyd_finish(0 if exact else 1, P(red), P(cn), K, da, P(Cn), Cn.stride(0), P(red[nst:]), P(fl),
+                               P(flags_h[slot]), ctypes.c_void_p(ev.cuda_event), P(Xr), n, Xr.stride(0), P(xx),
+                               P(labels_prev), P(nl) if n else None, P(ne), P(chg), stream())
         return [slot, labels_prev, nl, ne]
 
     iters = 0
