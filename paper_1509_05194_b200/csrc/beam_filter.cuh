@@ -59,7 +59,7 @@ __device__ inline FastSmem carve_fast(char* p, int cap, int M, int K, int D, boo
 // Bound by the codeword-row load latency (32 values in flight per lane), not by
 // the FMA chain: interleaving the independent k-block chains with fewer loads in
 // flight per chain measured 2x slower at D=960.
-__device__ __forceinline__ double exact_dot(const double* __restrict__ x64, const double* __restrict__ c, int D,
+static __device__ __noinline__ double exact_dot_general(const double* __restrict__ x64, const double* __restrict__ c, int D,
                                                 const float* __restrict__ c32 = nullptr) {
     double tot = 0.0;
     bool first = true;
@@ -70,6 +70,22 @@ __device__ __forceinline__ double exact_dot(const double* __restrict__ x64, cons
         const int e = d + len;
         // loads run ahead of the (strictly sequential) FMA chain: 16 codeword values
         // per batch, fp32 in memory (exact in float64) so a batch is 4 vector loads
+#ifdef DA_DOT64
+        // float64 rows read as pairs (no F2F conversions; 2x the bytes)
+        if (c32) {
+            for (; d + 16 <= e; d += 16) {
+                double2 cv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) cv[u] = __ldg(reinterpret_cast<const double2*>(c + d) + u);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const double2 xv = *reinterpret_cast<const double2*>(x64 + d + 2 * u);
+                    acc = __fma_rn(xv.x, cv[u].x, acc);
+                    acc = __fma_rn(xv.y, cv[u].y, acc);
+                }
+            }
+        }
+#else
         if (c32) {
             for (; d + 32 <= e; d += 32) {
                 float4 cv[8];
@@ -84,6 +100,7 @@ __device__ __forceinline__ double exact_dot(const double* __restrict__ x64, cons
                 }
             }
         }
+#endif
         for (; d + 8 <= e; d += 8) {
             double cv[8];
             double xv[8];
@@ -97,6 +114,31 @@ __device__ __forceinline__ double exact_dot(const double* __restrict__ x64, cons
         first = false;
     }
     return tot;
+}
+
+// Hot path of exact_dot for the common shape (D % 32 == 0, D <= 384: one BLAS
+// block, 16-byte aligned fp32 rows): a rolled loop of 32-value batches keeps
+// the kernels' hot code small (the beam kernels are instruction-fetch bound
+// when their stage loop exceeds the instruction cache); anything else goes out
+// of line.  Same FMA sequence either way.
+__device__ __forceinline__ double exact_dot(const double* __restrict__ x64, const double* __restrict__ c, int D,
+                                            const float* __restrict__ c32 = nullptr) {
+    if (c32 == nullptr || (D & 31) != 0 || D > 384) return exact_dot_general(x64, c, D, c32);
+    double acc = 0.0;
+#pragma unroll 1
+    for (int d = 0; d < D; d += 32) {
+        float4 cv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) cv[u] = __ldg(reinterpret_cast<const float4*>(c32 + d) + u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            acc = __fma_rn(x64[d + 4 * u + 0], (double)cv[u].x, acc);
+            acc = __fma_rn(x64[d + 4 * u + 1], (double)cv[u].y, acc);
+            acc = __fma_rn(x64[d + 4 * u + 2], (double)cv[u].z, acc);
+            acc = __fma_rn(x64[d + 4 * u + 3], (double)cv[u].w, acc);
+        }
+    }
+    return acc;
 }
 
 // Packed fp32 pair add (FADD2, sm_100): each lane's result is rounded exactly

@@ -209,14 +209,20 @@ template <bool INL>
 __device__ __forceinline__ double beam_exact_value_t(const double* __restrict__ x64, const double* __restrict__ cw64,
                                                 const float* __restrict__ cw32, int D, const double* __restrict__ sq,
                                                 const double* __restrict__ P, const int32_t* __restrict__ pc,
-                                                const double* __restrict__ ps, int M, int K, int m, int flat, int k_sh) {
+                                                const double* __restrict__ ps, int M, int K, int m, int flat, int k_sh,
+                                                const long long* __restrict__ roff = nullptr) {
     const int l = k_sh >= 0 ? flat >> k_sh : flat / K;
     const int k = flat - l * K;
     const double xc = exact_dot(x64, cw64 + ((long long)m * K + k) * D, D, cw32 ? cw32 + ((long long)m * K + k) * D : nullptr);
     const double t = dsub(sq[m * K + k], dmul(2.0, xc));
     double cross = 0.0;
-#pragma unroll 4
-    for (int j = 0; j < m; ++j) cross = dadd(cross, P[(((long long)j * M + m) * K + pc[l * M + j]) * K + k]);
+    if (roff) {   // this stage's row offsets (same layout as the float table)
+#pragma unroll 1
+        for (int j = 0; j < m; ++j) cross = dadd(cross, P[roff[l * M + j] + k]);
+    } else {
+#pragma unroll 1
+        for (int j = 0; j < m; ++j) cross = dadd(cross, P[(((long long)j * M + m) * K + pc[l * M + j]) * K + k]);
+    }
     return dadd(dadd(ps[l], t), dmul(2.0, cross));
 }
 __device__ __noinline__ double beam_exact_value(const double* __restrict__ x64, const double* __restrict__ cw64,
@@ -277,6 +283,23 @@ __device__ __noinline__ void beam_overflow_select(FastSmem S, int total, int wid
     __syncwarp();
 }
 
+// Exact error of the chosen code (reconstruction in m order, numpy pairwise
+// over d; diff^2 staged in dd).  Out of line: once per vector, off the hot path.
+__device__ __noinline__ void beam_final_error(const double* __restrict__ x64, double* __restrict__ dd,
+                                              const float* __restrict__ cw, const int32_t* __restrict__ best, int M,
+                                              int K, int D, double* __restrict__ err) {
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    for (int d = lane; d < D; d += 32) {
+        double r = 0.0;
+        for (int j = 0; j < M; ++j) r = dadd(r, (double)cw[((long long)j * K + best[j]) * D + d]);
+        double df = dsub(x64[d], r);
+        dd[d] = dmul(df, df);
+    }
+    __syncwarp();
+    if (lane == 0) *err = np_pw_sum([&](long long i) { return dd[i]; }, 0, D);
+}
+
 template <typename TX, bool LEAN, bool VEC>
 __global__ void __launch_bounds__(256, LEAN ? DA_LEAN_MINB : 2) beam_fast_kernel(
     const TX* __restrict__ X, long long n, long long ldx, int D, const float* __restrict__ cw, int M, int K, int L,
@@ -302,6 +325,7 @@ __global__ void __launch_bounds__(256, LEAN ? DA_LEAN_MINB : 2) beam_fast_kernel
     const TX* xr = X + v * ldx;
     // x in float64 (exact widening) and ||x||
     double xx_part = 0.0;
+#pragma unroll 1
     for (int d = lane; d < D; d += 32) {
         double t = (double)xr[d];
         S.x64[d] = t;
@@ -314,6 +338,15 @@ __global__ void __launch_bounds__(256, LEAN ? DA_LEAN_MINB : 2) beam_fast_kernel
     const double u = 5.9604644775390625e-08;  // 2^-24
     unsigned long long n_exact = 0;
 
+    // the score-independent part of every stage's bound, lane m holding stage m's
+    double a_stage = 0.0;
+    for (int mm = lane; mm < M; mm += 32) {
+        const double cb = cbm[mm], cm = cmax[mm];
+        const double tmax = cm * cm + 2.0 * xnorm * cm;
+        const double a = 2.0 * (table_err(tab_tc, D, u, xnorm, cm) + 2.0 * ((mm + 2.0) * u * cb) +
+                                4.0 * u * (tmax + 2.0 * cb));
+        if (mm == lane) a_stage = a;
+    }
     int cur = 0, live = 1;
     for (int m = 0; m < M; ++m) {
         const int total = live * K;
@@ -321,17 +354,18 @@ __global__ void __launch_bounds__(256, LEAN ? DA_LEAN_MINB : 2) beam_fast_kernel
         const int32_t* pc = S.codes + cur * cap * M;
         const double* ps = S.score + cur * cap;
         // ---- rigorous bound of |v' - v| for this stage
-        double smax = lane < live ? fabs(ps[lane]) : 0.0;   // straight-line for live <= 32
-        for (int l = lane + 32; l < live; l += 32) smax = fmax(smax, fabs(ps[l]));
-        for (int off = 16; off >= 1; off >>= 1) smax = fmax(smax, __shfl_xor_sync(FULL, smax, off));
-        // sum of the cross-table maxima over j < m (cb_prep_kernel, once per call)
-        const double cb = cbm[m];
-        const double cm = cmax[m];
-        const double tmax = cm * cm + 2.0 * xnorm * cm;
-        // table error by how the table was computed (beam_filter.cuh: table_err)
-        const double e_t = table_err(tab_tc, D, u, xnorm, cm);
-        const double e_cross = (m + 2.0) * u * cb;
-        const double E = 2.0 * (e_t + 2.0 * e_cross + 4.0 * u * (smax + tmax + 2.0 * cb) + u * smax) + 1e-300;
+        // max |score| rounded up to float (non-negative floats order like their bits)
+        unsigned sbits = lane < live ? __float_as_uint(__double2float_ru(fabs(ps[lane]))) : 0u;
+#pragma unroll 1
+        for (int l = lane + 32; l < live; l += 32) sbits = max(sbits, __float_as_uint(__double2float_ru(fabs(ps[l]))));
+        const double smax = (double)__uint_as_float(__reduce_max_sync(FULL, sbits));
+        double a_m = __shfl_sync(FULL, a_stage, m & 31);
+        if (M > 32) {   // more stages than lanes: this stage's constant directly
+            const double cb = cbm[m], cm = cmax[m];
+            a_m = 2.0 * (table_err(tab_tc, D, u, xnorm, cm) + 2.0 * ((m + 2.0) * u * cb) +
+                         4.0 * u * (cm * cm + 2.0 * xnorm * cm + 2.0 * cb));
+        }
+        const double E = a_m + 10.0 * u * smax + 1e-300;
 
         for (int e = lane; e < live * m; e += 32) {
             const int l = e / m, j = e % m;
@@ -586,7 +620,7 @@ __global__ void __launch_bounds__(256, LEAN ? DA_LEAN_MINB : 2) beam_fast_kernel
         __syncwarp();
         const float* cw32 = c32ok ? cw : nullptr;
         auto exact_value = [&](int flat) -> double {
-            return beam_exact_value_t<true>(S.x64, cw64, cw32, D, sq, P, pc, ps, M, K, m, flat, k_sh);
+            return beam_exact_value_t<true>(S.x64, cw64, cw32, D, sq, P, pc, ps, M, K, m, flat, k_sh, S.roff);
         };
         int cnt = 0;
         if (nqueued <= QCAP) {
@@ -658,6 +692,7 @@ __global__ void __launch_bounds__(256, LEAN ? DA_LEAN_MINB : 2) beam_fast_kernel
         if (lex_less(ov, oi, bv, bi)) { bv = ov; bi = oi; }
     }
     const int32_t* best = S.codes + cur * cap * M + (long long)bi * M;
+#pragma unroll 1
     for (int j = lane; j < M; j += 32) {
         int c = best[j];
         if (code_bytes == 1) ((uint8_t*)codes_out)[v * ldcodes + j] = (uint8_t)c;
@@ -668,19 +703,7 @@ __global__ void __launch_bounds__(256, LEAN ? DA_LEAN_MINB : 2) beam_fast_kernel
         for (int off = 16; off >= 1; off >>= 1) n_exact += __shfl_xor_sync(FULL, n_exact, off);
         if (lane == 0) atomicAdd(stats, n_exact);
     }
-    if (err_out) {
-        // exact error, numpy pairwise over d; diff^2 staged in vbuf (as doubles)
-        double* dd = reinterpret_cast<double*>(S.vbuf);
-        __syncwarp();
-        for (int d = lane; d < D; d += 32) {
-            double r = 0.0;
-            for (int j = 0; j < M; ++j) r = dadd(r, (double)cw[((long long)j * K + best[j]) * D + d]);
-            double df = dsub(S.x64[d], r);
-            dd[d] = dmul(df, df);
-        }
-        __syncwarp();
-        if (lane == 0) err_out[v] = np_pw_sum([&](long long i) { return dd[i]; }, 0, D);
-    }
+    if (err_out) beam_final_error(S.x64, reinterpret_cast<double*>(S.vbuf), cw, best, M, K, D, err_out + v);
 }
 
 int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int D, const float* cw, int M, int K,
