@@ -751,6 +751,7 @@ int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int
     if (smem > 48 * 1024) DA_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const long long row_bytes = (long long)M * K * sizeof(float);
     long long chunk = std::max(1024LL, (1LL << 30) / row_bytes);
+    if (const char* e = getenv("DA_ENC_CHUNK")) chunk = std::max(256LL, atoll(e));   // A/B runs
     chunk = std::min(chunk, n);
     float* tab = (float*)scratch(8, (size_t)(chunk * row_bytes), s);
     if (!tab) return fail_cuda(cudaErrorMemoryAllocation, "encode_fast table scratch");
@@ -784,6 +785,13 @@ int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int
         // two vectors per warp wins for narrow beams (B200, config B, 1M vectors: L=2
         // 21.5 vs 27.4 ms, L=6 32.1 vs 37.7), the one-vector lean kernel from L = 8
         // (L=8 39.0 vs 40.1, L=10 47.0 vs 54.3).  DA_BEAM_PAIR=0/1 forces it off/on.
+        if (L == 1) {   // greedy: one live beam, lazily exact scores (encode_greedy.cu)
+            ProfScope ps4("encode_greedy", s);
+            const int rc = launch_greedy((const float*)X + c0 * ldx, cn, ldx, D, cw, M, K, tab, sq, P, P32, cmax, cbm,
+                                         cw64, cout, code_bytes, ldcodes, eout, stats, tab_tc, s);
+            if (rc == 0) continue;
+            if (rc != kNotApplicable) return rc;
+        }
         const char* epair = getenv("DA_BEAM_PAIR");
         const bool pair = epair ? atoi(epair) != 0 : L <= 7;
         if (pair) {

@@ -112,6 +112,10 @@ size_t assign_image_bytes(long long n, int d);
 int assign_bind_image(const void* X, int x_is_f32, long long n, long long ldx, int d, float* img, cudaStream_t s);
 // launcher result meaning "this path does not take the shape" (caller falls through)
 constexpr int kNotApplicable = 1 << 30;
+int launch_greedy(const float* X, long long n, long long ldx, int D, const float* cw, int M, int K, const float* tab,
+                  const double* sq, const double* P, const float* P32, const double* cmax, const double* cbm,
+                  const double* cw64, void* codes_out, int code_bytes, long long ldcodes, double* err_out,
+                  unsigned long long* stats, int tab_tc, cudaStream_t s);
 int launch_table_tc(const float* X, long long n, long long ldx, int D, const float* cw, const double* sq, int M, int K,
                     float* T, long long ldt, cudaStream_t s);
 int launch_encode_tc(const float* X, long long n, long long ldx, int D, const float* cw, int M, int K, int L,
