@@ -26,6 +26,7 @@ import numpy as np
 import torch
 
 __all__ = ["Comm", "merge_worst", "shard_rows", "train_from_scratch_sharded", "da_sweep_sharded",
+           "train_online_sharded", "ChunkFeeder", "train_online_stream",
            "blas_block_starts", "cov_segments", "exact_pca_moments"]
 
 
@@ -270,3 +271,87 @@ def da_sweep_sharded(X_local, cw, codes, Pt, sq, config, comm: Comm, sweep_index
 
     comm.bind_rows(X_local.shape[0])
     E.da_sweep(X_local, cw, codes, Pt, sq, config, sweep_index=sweep_index, report=report, comm=comm)
+
+
+def train_online_sharded(cw: torch.Tensor, X_local: torch.Tensor, config, comm: Comm, report=None):
+    """annealing.py:248-262 over row shards (config D: each GPU holds 1/world of
+    the batch): encode this shard's rows with the current codebook, then
+    config.sweeps annealing passes with the exact shard reductions.  Every rank
+    returns the same new codebook (float32 (M, K, D) on the device) -- the
+    codebook the one-GPU train_online returns for the whole batch."""
+    from . import _engine as E
+    from .annealing import TrainReport
+
+    comm.bind_rows(X_local.shape[0])
+    report = report if report is not None else TrainReport(config=config)
+    cw = cw.clone()
+    Pt, sq = E.cross_full(cw)
+    codes, _ = E.encode(X_local, cw, sq, Pt, config.beam_width, out_dtype=torch.int32, with_err=False)
+    E.sweep_until_converged(X_local, cw, codes, config, report, comm=comm)
+    return cw, report
+
+
+class ChunkFeeder:
+    """Host chunks (this rank's rows, numpy uint8 or float32) -> device float32,
+    uploaded through page-locked buffers on a side stream one chunk ahead: while
+    chunk c trains, chunk c+1 is copied into pinned memory (a worker thread) and
+    sent to the device asynchronously (config D's pinned async copies).  uint8
+    rows travel as bytes (128 B per config-D row) and widen on the device."""
+
+    def __init__(self, chunks, device=None):
+        import threading
+
+        self.chunks = list(chunks)
+        self.dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.side = torch.cuda.Stream(device=self.dev)
+        self._threading = threading
+
+    def _stage(self, i):
+        a = np.ascontiguousarray(self.chunks[i])
+        dt = torch.uint8 if a.dtype == np.uint8 else torch.float32
+        if a.dtype not in (np.uint8, np.float32):
+            a = a.astype(np.float32)
+        pin = torch.empty(a.shape, dtype=dt, pin_memory=True)
+        pin.numpy()[...] = a
+        dev = torch.empty(a.shape, dtype=dt, device=self.dev)
+        with torch.cuda.stream(self.side):
+            dev.copy_(pin, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self.side)
+        return pin, dev, ev
+
+    def __iter__(self):
+        if not self.chunks:
+            return
+        nxt = self._stage(0)
+        for i in range(len(self.chunks)):
+            pin, dev, ev = nxt
+            holder = {}
+            th = None
+            if i + 1 < len(self.chunks):
+                # next chunk: host copy into pinned memory + async upload, off the critical path
+                th = self._threading.Thread(target=lambda: holder.setdefault("v", self._stage(i + 1)))
+                th.start()
+            main = torch.cuda.current_stream(self.dev)
+            main.wait_event(ev)
+            dev.record_stream(main)                   # read on the main stream: no early reuse
+            X = dev.float() if dev.dtype == torch.uint8 else dev
+            yield X
+            if th is not None:
+                th.join()
+                nxt = holder["v"]
+            del pin
+
+
+def train_online_stream(cw: torch.Tensor, chunks, config, comm: Comm, checkpoint=None):
+    """Online DA over a stream of chunks (config D): this rank's slice of each
+    chunk is uploaded one chunk ahead (ChunkFeeder) and trained with
+    train_online_sharded.  checkpoint(c, cw) is called after every chunk (rank 0
+    writes an HCLB checkpoint in tools/bench_online.py).  Returns (cw, reports)."""
+    reports = []
+    for c, X in enumerate(ChunkFeeder(chunks)):
+        cw, rep = train_online_sharded(cw, X, config, comm)
+        reports.append(rep)
+        if checkpoint is not None:
+            checkpoint(c, cw)
+    return cw, reports

@@ -289,3 +289,61 @@ def test_exact_sharded_lloyd_equals_one_gpu(layout):
                 assert len(out[0][i][2]) == len(t1)
                 np.testing.assert_allclose(out[0][i][2], t1, rtol=1e-13)
             i += 1
+
+
+def _online_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        import paper_1509_05194_b200 as da
+        from paper_1509_05194_b200 import codebook as cb
+        from paper_1509_05194_b200 import distributed as D
+        from paper_1509_05194_b200 import synthetic
+
+        chunks = [synthetic.mixture_b_chunk(3, c, n=3000).astype(np.uint8) for c in range(3)]
+        cfg0 = da.TrainConfig(m_count=4, k_count=32, beam_width=4, sweeps=0, rel_tol=0.0)
+        book, _, _ = da.train_from_scratch(chunks[0].astype(np.float32), cfg0)
+        cw0, _ = cb._codebook_dev(book)
+        cfg = da.TrainConfig(m_count=4, k_count=32, beam_width=4, sweeps=1, rel_tol=0.0)
+        mine = [ch[D.shard_rows(len(ch), world, rank)] for ch in chunks[1:]]
+        cw, reps = D.train_online_stream(cw0, mine, cfg, D.Comm())
+        q.put((rank, (cw.cpu().numpy(), [r.distortions() for r in reps])))
+    except Exception:
+        import traceback
+
+        q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_online_stream_sharded_equals_one_gpu(world):
+    """Config-D style online DA: uint8 chunks, each rank streaming its slice
+    through pinned async uploads (ChunkFeeder) into train_online_sharded; the
+    codebook after every chunk equals the one-GPU train_online on the whole chunk."""
+    import paper_1509_05194_b200 as da
+    from paper_1509_05194_b200 import synthetic
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_online_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=600) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(world):
+        assert not isinstance(out[r], str), out[r]
+        np.testing.assert_array_equal(out[r][0], out[0][0])
+    chunks = [synthetic.mixture_b_chunk(3, c, n=3000).astype(np.uint8) for c in range(3)]
+    cfg0 = da.TrainConfig(m_count=4, k_count=32, beam_width=4, sweeps=0, rel_tol=0.0)
+    book, _, _ = da.train_from_scratch(chunks[0].astype(np.float32), cfg0)
+    cfg = da.TrainConfig(m_count=4, k_count=32, beam_width=4, sweeps=1, rel_tol=0.0)
+    for c in chunks[1:]:
+        book, rep = da.train_online(book, c.astype(np.float32), cfg)
+    np.testing.assert_array_equal(out[0][0], book.codewords)
+    np.testing.assert_allclose(out[0][1][-1], rep.distortions(), rtol=1e-12)

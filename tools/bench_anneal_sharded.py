@@ -6,6 +6,7 @@ usage: python -m torch.distributed.run --nproc-per-node 1 --master-addr 127.0.0.
            --master-port 29511 tools/bench_anneal_sharded.py [n]
 """
 import os, sys, time, json
+os.environ.setdefault("DA_SHARD_LOOP", "1")   # time the shard loop even at world 1
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import torch.distributed as dist
