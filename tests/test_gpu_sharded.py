@@ -83,10 +83,11 @@ def test_two_shards_on_one_gpu():
 @pytest.fixture(scope="module")
 def gloo1():
     """A one-process gloo group for the world-1 equivalence tests."""
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), DA_SHARD_LOOP="1")
     dist.init_process_group("gloo", rank=0, world_size=1)
     yield
     dist.destroy_process_group()
+    os.environ.pop("DA_SHARD_LOOP", None)
 
 
 @pytest.mark.parametrize("K,active,seed", [(8, 3, 0), (64, 5, 1), (200, 2, 2)])
