@@ -4,8 +4,9 @@ Same data structure and public API as the reference (`annq/atree.py`):
 
 * `build_atree(encoded, codebook, cross)` -> `ATree` (flat arrays; node ids
   level by level in code order, children contiguous, leaf-suffix compression;
-  `atree.py:158-324`).  Built on the host: it is a one-off sort-and-scan over
-  the codes, not part of the per-query hot path.
+  `atree.py:158-324`).  Built on the GPU: stable radix passes of the library's
+  counting sort put the codes in lexicographic order, device scans find the
+  prefix boundaries, epsilons come from the device cross tables.
 * `atree_search(tree, codebook, q, params)` -> (ids, distances, SearchStats)
   (`atree.py:336-475`, `_traverse.py:52-255`) and the batched
   `atree_search_batch(tree, codebook, Q, params)`.  One CTA per query walks the
@@ -103,23 +104,40 @@ class ATree:
         return self.leaf_ids.shape[0]
 
 
-def _eps_of(products, U_rows: np.ndarray, depth: int) -> np.ndarray:
-    """epsilon = sum_{i<depth} c_i . c_depth over code rows, accumulated from 0
-    in i order in float64, stored as float32 (atree.py:150-155)."""
-    return _eps_cols(products, [U_rows[:, i] for i in range(depth + 1)], depth)
-
-
-def _eps_cols(products, cols, depth: int) -> np.ndarray:
-    """_eps_of on per-depth code columns (1-D arrays, cols[i] = codes at depth i)."""
-    acc = np.zeros(cols[depth].shape[0])
+def _eps_cols(Pt: torch.Tensor, cols, depth: int) -> torch.Tensor:
+    """epsilon = sum_{i<depth} c_i . c_depth over per-depth code columns, accumulated
+    from 0 in i order in float64 (the reference's order, atree.py:150-155), as
+    float32.  Pt: device cross tables (M, M, K, K)."""
+    acc = torch.zeros(cols[depth].shape[0], dtype=torch.float64, device=Pt.device)
     for i in range(depth):
-        acc = acc + products[i, depth][cols[i], cols[depth]]
-    return acc.astype(np.float32)
+        acc = acc + Pt[i, depth][cols[i], cols[depth]]
+    return acc.to(torch.float32)
+
+
+def _lex_order(codes: torch.Tensor, K: int) -> torch.Tensor:
+    """Stable lexicographic order of the code rows (code 0 most significant): LSD
+    radix passes of the library's stable counting sort (da_label_order), one per
+    code column from the last to the first."""
+    n, M = codes.shape
+    order = torch.arange(n, dtype=torch.int64, device=codes.device)
+    o = torch.empty(n, dtype=torch.int32, device=codes.device)
+    cnt = torch.empty(K, dtype=torch.int32, device=codes.device)
+    for m in range(M - 1, -1, -1):
+        lab = codes[order, m].to(torch.int32).contiguous()
+        native.da_label_order(P(lab), n, K, P(o), P(cnt), E.stream())
+        order = order[o.long()]
+    return order
 
 
 def build_atree(encoded, codebook, cross=None) -> ATree:
-    """Prefix tree with leaf-suffix compression, identical arrays to atree.py:158-324."""
-    from .codebook import cross_products
+    """Prefix tree with leaf-suffix compression, built on the GPU: identical
+    arrays to the reference's build (atree.py:158-324).  Rows are put in
+    lexicographic code order by stable radix passes (da_label_order), distinct
+    codes and per-depth prefix boundaries come from device scans, and node
+    epsilons are gathered from the device cross tables in the reference's
+    addition order.  oracle/atree_build.py holds the host restatement the tests
+    compare against."""
+    from .codebook import _cross_dev, cross_products
 
     h = codebook.content_hash()
     if encoded.codebook_hash is not None and encoded.codebook_hash != h:
@@ -128,128 +146,123 @@ def build_atree(encoded, codebook, cross=None) -> ATree:
         raise ValueError("encoded shape does not match the codebook")
     if cross is None:
         cross = cross_products(codebook)
-    M, n = codebook.m_count, encoded.n
+    M, n, K = codebook.m_count, encoded.n, codebook.k_count
     i64, i32, f32 = np.int64, np.int32, np.float32
     if n == 0:
         e = np.empty(0, dtype=i64)
-        return ATree(h, M, codebook.k_count, 0, np.empty(0, i32), np.empty(0, f32), e, e, e, e, e,
+        return ATree(h, M, K, 0, np.empty(0, i32), np.empty(0, f32), e, e, e, e, e,
                      np.empty(0, i32), np.empty(0, f32), e, e, e)
-    ids = np.arange(n, dtype=i64) if encoded.id_map is None else np.asarray(encoded.id_map, dtype=i64)
-    codes = np.asarray(encoded.codes).astype(i64)
-    # rows in lexicographic code order (stable), then distinct full codes
-    bits = max(1, int(codebook.k_count - 1).bit_length())
-    if bits * M <= 64:
-        # one packed key (code 0 most significant): a single stable radix sort
-        key = np.zeros(n, dtype=np.uint64)
-        for m in range(M):
-            key = (key << np.uint64(bits)) | codes[:, m].astype(np.uint64)
-        order = np.argsort(key, kind="stable")
-    else:
-        order = np.lexsort([codes[:, m] for m in range(M - 1, -1, -1)])
+    E.require_cuda()
+    dev = E.device()
+    Pt = _cross_dev(cross)[0] if hasattr(cross, "sq_norms") else E.to_dev(
+        np.ascontiguousarray(cross.products, dtype=np.float64))
+    T = torch
+    codes = T.from_numpy(np.ascontiguousarray(encoded.codes).astype(i64)).to(dev)
+    ids = (T.arange(n, dtype=T.int64, device=dev) if encoded.id_map is None
+           else T.from_numpy(np.asarray(encoded.id_map, dtype=i64)).to(dev))
+    order = _lex_order(codes, K)
     S = codes[order]
     ids_sorted = ids[order]
-    first = np.ones(n, dtype=bool)
+    first = T.ones(n, dtype=T.bool, device=dev)
     if n > 1:
-        first[1:] = np.any(S[1:] != S[:-1], axis=1)
+        first[1:] = (S[1:] != S[:-1]).any(dim=1)
     U = S[first]
     g = U.shape[0]
-    gstart = np.flatnonzero(first)
-    gend = np.append(gstart[1:], n)
+    gstart = T.nonzero(first).flatten()
+    gend = T.cat([gstart[1:], T.tensor([n], dtype=T.int64, device=dev)])
     # differs[m, i]: prefix U[i, :m+1] differs from U[i-1, :m+1] (row 0 starts one)
-    differs = np.ones((M, g), dtype=bool)
+    differs = T.ones((M, g), dtype=T.bool, device=dev)
     if g > 1:
-        running = np.zeros(g - 1, dtype=bool)
-        for m in range(M):
-            running |= U[1:, m] != U[:-1, m]
-            differs[m, 1:] = running
-    products = cross.products
+        neq = (U[1:] != U[:-1]).to(T.int32)
+        differs[:, 1:] = neq.cummax(dim=1).values.T.bool()
+    prefix_id = [T.cumsum(differs[m].to(T.int64), 0) - 1 for m in range(M)]
 
-    # level by level: a depth-m prefix is a node iff its parent node is internal;
-    # it is a leaf iff exactly one distinct code lies under it
     levels = []
-    parent_internal = None   # per depth-(m-1) prefix index: parent node is internal (materialised)
+    parent_internal = None
     for m in range(M):
-        starts = np.flatnonzero(differs[m])
-        width = np.append(starts[1:], g) - starts
-        if m == 0:
-            exists = np.ones(starts.size, dtype=bool)
-        else:
-            prev_prefix_of_row = np.cumsum(differs[m - 1]) - 1
-            exists = parent_internal[prev_prefix_of_row[starts]]
+        starts = T.nonzero(differs[m]).flatten()
+        width = T.cat([starts[1:], T.tensor([g], dtype=T.int64, device=dev)]) - starts
+        exists = (T.ones(starts.numel(), dtype=T.bool, device=dev) if m == 0
+                  else parent_internal[prefix_id[m - 1][starts]])
         leaf = width == 1
         rows = starts[exists]
         levels.append({"rows": rows, "leaf": leaf[exists],
-                       "parent_prefix": (np.cumsum(differs[m - 1]) - 1)[rows] if m else None})
-        # internal & existing, per depth-m prefix (for the next level)
+                       "parent_prefix": prefix_id[m - 1][rows] if m else None})
         parent_internal = exists & ~leaf
 
-    # global ids: level m occupies [base_m, base_m + count_m)
-    counts = [lv["rows"].size for lv in levels]
+    counts = [int(lv["rows"].numel()) for lv in levels]
     bases = np.concatenate([[0], np.cumsum(counts)]).astype(i64)
     total = int(bases[-1])
-    code_a = np.empty(total, dtype=i32)
-    eps_a = np.empty(total, dtype=f32)
-    child_lo = np.zeros(total, dtype=i64)
-    child_hi = np.zeros(total, dtype=i64)
-    leaf_ref = np.full(total, -1, dtype=i64)
+    code_a = T.empty(total, dtype=T.int32, device=dev)
+    eps_a = T.empty(total, dtype=T.float32, device=dev)
+    child_lo = T.zeros(total, dtype=T.int64, device=dev)
+    child_hi = T.zeros(total, dtype=T.int64, device=dev)
+    leaf_ref = T.full((total,), -1, dtype=T.int64, device=dev)
     leaf_row, leaf_depth = [], []
     n_leaf = 0
-    Uc = np.ascontiguousarray(U.T)          # code columns: 1-D gathers below
+    Uc = U.T.contiguous()
     for m, lv in enumerate(levels):
         rows, base = lv["rows"], int(bases[m])
+        R = rows.numel()
         cols = [Uc[i][rows] for i in range(m + 1)]
-        code_a[base:base + rows.size] = cols[m]
-        eps_a[base:base + rows.size] = _eps_cols(products, cols, m)
-        if m > 0 and rows.size:
-            # parent of each node = the position of its depth-(m-1) prefix among the
-            # previous level's nodes; children are contiguous in code order
+        code_a[base:base + R] = cols[m].to(T.int32)
+        eps_a[base:base + R] = _eps_cols(Pt, cols, m)
+        if m > 0 and R:
             prev = levels[m - 1]
-            prev_prefix_ids = (np.cumsum(differs[m - 1]) - 1)[prev["rows"]]
-            slot = np.searchsorted(prev_prefix_ids, lv["parent_prefix"])
-            cnt = np.bincount(slot, minlength=prev["rows"].size)
-            off = np.concatenate([[0], np.cumsum(cnt)])
+            prev_prefix_ids = prefix_id[m - 1][prev["rows"]]
+            slot = T.searchsorted(prev_prefix_ids, lv["parent_prefix"])
+            cnt = T.bincount(slot, minlength=prev["rows"].numel())
+            off = T.cat([T.zeros(1, dtype=T.int64, device=dev), T.cumsum(cnt, 0)])
             pb = int(bases[m - 1])
-            child_lo[pb:pb + cnt.size] = base + off[:-1]
-            child_hi[pb:pb + cnt.size] = base + off[1:]
-        lf = np.flatnonzero(lv["leaf"])
-        leaf_ref[base + lf] = n_leaf + np.arange(lf.size)
-        n_leaf += lf.size
+            child_lo[pb:pb + cnt.numel()] = base + off[:-1]
+            child_hi[pb:pb + cnt.numel()] = base + off[1:]
+        lf = T.nonzero(lv["leaf"]).flatten()
+        leaf_ref[base + lf] = n_leaf + T.arange(lf.numel(), dtype=T.int64, device=dev)
+        n_leaf += lf.numel()
         leaf_row.append(rows[lf])
-        leaf_depth.append(np.full(lf.size, m, dtype=i64))
-    child_lo[leaf_ref >= 0] = 0
-    child_hi[leaf_ref >= 0] = 0
-    leaf_row = np.concatenate(leaf_row)
-    leaf_depth = np.concatenate(leaf_depth)
+        leaf_depth.append(T.full((lf.numel(),), m, dtype=T.int64, device=dev))
+    is_leaf = leaf_ref >= 0
+    child_lo[is_leaf] = 0
+    child_hi[is_leaf] = 0
+    leaf_row = T.cat(leaf_row)
+    leaf_depth = T.cat(leaf_depth)
 
     # compressed suffixes: depths depth+1 .. M-1 of the leaf's single code
     slen = (M - 1) - leaf_depth
-    suffix_lo = np.concatenate([[0], np.cumsum(slen)[:-1]]).astype(i64)
+    csl = T.cumsum(slen, 0)
+    suffix_lo = T.cat([T.zeros(1, dtype=T.int64, device=dev), csl[:-1]])
     suffix_hi = suffix_lo + slen
-    suffix_code = np.empty(int(slen.sum()), dtype=i32)
-    suffix_eps = np.empty(int(slen.sum()), dtype=f32)
-    Lc = [Uc[i][leaf_row] for i in range(M)]   # code columns of the leaves' rows
+    ns = int(csl[-1].item()) if csl.numel() else 0
+    suffix_code = T.empty(ns, dtype=T.int32, device=dev)
+    suffix_eps = T.empty(ns, dtype=T.float32, device=dev)
+    Lc = [Uc[i][leaf_row] for i in range(M)]
     for t in range(1, M):
-        sel = np.flatnonzero(leaf_depth < t)
-        if sel.size:
+        sel = T.nonzero(leaf_depth < t).flatten()
+        if sel.numel():
             at = suffix_lo[sel] + (t - 1 - leaf_depth[sel])
             cols = [Lc[i][sel] for i in range(t + 1)]
-            suffix_code[at] = cols[t]
-            suffix_eps[at] = _eps_cols(products, cols, t)
+            suffix_code[at] = cols[t].to(T.int32)
+            suffix_eps[at] = _eps_cols(Pt, cols, t)
 
     # vector ids of each leaf, ascending
     cnt = gend[leaf_row] - gstart[leaf_row]
-    ids_lo = np.concatenate([[0], np.cumsum(cnt)[:-1]]).astype(i64)
+    ccnt = T.cumsum(cnt, 0)
+    ids_lo = T.cat([T.zeros(1, dtype=T.int64, device=dev), ccnt[:-1]])
     ids_hi = ids_lo + cnt
     if encoded.id_map is None:
         ids_g = ids_sorted            # the stable sort kept row order inside each group
     else:
-        gid = np.cumsum(first) - 1    # ids ascending inside each group: sort by (group, id)
-        ids_g = ids_sorted[np.lexsort((ids_sorted, gid))]
-    total_ids = int(cnt.sum())
-    pos = np.repeat(gstart[leaf_row] - ids_lo, cnt) + np.arange(total_ids, dtype=i64)
+        gid = T.cumsum(first.to(T.int64), 0) - 1   # ids ascending inside each group
+        o1 = T.sort(ids_sorted, stable=True).indices
+        o2 = T.sort(gid[o1], stable=True).indices
+        ids_g = ids_sorted[o1[o2]]
+    total_ids = int(ccnt[-1].item()) if ccnt.numel() else 0
+    pos = T.repeat_interleave(gstart[leaf_row] - ids_lo, cnt) + T.arange(total_ids, dtype=T.int64, device=dev)
     leaf_ids = ids_g[pos]
-    return ATree(h, M, codebook.k_count, int(counts[0]), code_a, eps_a, child_lo, child_hi, leaf_ref,
-                 suffix_lo, suffix_hi, suffix_code, suffix_eps, ids_lo, ids_hi, leaf_ids)
+    host = lambda t: t.cpu().numpy()
+    return ATree(h, M, K, int(counts[0]), host(code_a), host(eps_a), host(child_lo), host(child_hi), host(leaf_ref),
+                 host(suffix_lo), host(suffix_hi), host(suffix_code), host(suffix_eps), host(ids_lo), host(ids_hi),
+                 host(leaf_ids))
 
 
 def node_distance(parent_dist: float, table, code: int, epsilon: float, layer: int, q_sq_norm: float) -> float:

@@ -737,7 +737,8 @@ int launch_group_sums(const double* X, long long n, long long ldx, int D, const 
     return 0;
 }
 
-// Stable argsort of labels only (used by tests and the reseed path).
+// Stable argsort of labels only (tests, the reseed path, the A-Tree build's
+// LSD radix passes): the same tile-scan counting sort as the Lloyd update.
 int launch_label_order(const int32_t* labels, long long n, int K, int32_t* order_out, int32_t* counts,
                        cudaStream_t s) {
     if (n <= 0) return 0;
@@ -750,20 +751,8 @@ int launch_label_order(const int32_t* labels, long long n, int K, int32_t* order
     size_t o_total = take(sizeof(int32_t) * 4);
     char* base = (char*)scratch(1, off, s);
     if (!base) return fail_cuda(cudaErrorMemoryAllocation, "label_order scratch");
-    int32_t* hist = (int32_t*)(base + o_hist);
-    int32_t* seg = (int32_t*)(base + o_seg);
-    int32_t* total = (int32_t*)(base + o_total);
-    DA_CUDA(cudaMemsetAsync(hist, 0, sizeof(int32_t) * (KT + 1), s));
-    size_t sh = (K <= GS_SMEM_HIST) ? sizeof(int32_t) * K : 0;
-    tile_hist_kernel<<<T, 256, sh, s>>>(labels, n, K, T, hist);
-    DA_CHECK_LAUNCH("tile_hist_kernel");
-    exclusive_scan_kernel<<<1, 1024, 0, s>>>(hist, KT, total);
-    DA_CHECK_LAUNCH("exclusive_scan_kernel");
-    seg_counts_kernel<<<grid_for(K, 256), 256, 0, s>>>(hist, K, T, n, seg, counts);
-    DA_CHECK_LAUNCH("seg_counts_kernel");
-    stable_scatter_kernel<<<T, 32, sh, s>>>(labels, n, K, T, hist, order_out);
-    DA_CHECK_LAUNCH("stable_scatter_kernel");
-    return 0;
+    return gs_stable_sort(labels, n, K, T, (int32_t*)(base + o_hist), counts, (int32_t*)(base + o_seg),
+                          (int32_t*)(base + o_total), order_out, s);
 }
 
 

@@ -1,4 +1,4 @@
-"""A-Tree on the host: the build reproduces the reference's tree arrays, and the
+"""A-Tree on the host: the oracle build (oracle/atree_build.py) reproduces the reference's tree arrays, and the
 oracle's traversal restatement reproduces the reference's search results
 (tests/golden/atree.npz, made by oracle/make_golden_atree.py)."""
 
@@ -10,6 +10,7 @@ import pytest
 import paper_1509_05194_b200 as da
 from paper_1509_05194_b200 import atree as AT
 from oracle import da_oracle as O
+from oracle.atree_build import build_atree_host
 
 
 @pytest.fixture(scope="module")
@@ -29,7 +30,7 @@ def _case(g, pre):
 @pytest.mark.parametrize("pre", ["small", "ties"])
 def test_build_matches_reference_tree(gold, pre):
     book, enc, cross = _case(gold, pre)
-    t = AT.build_atree(enc, book, cross)
+    t = build_atree_host(enc, book, cross)
     assert t.n_root_children == gold[f"{pre}_tree_meta"][0]
     for f in AT._TREE_FIELDS:
         np.testing.assert_array_equal(getattr(t, f), gold[f"{pre}_tree_{f}"], err_msg=f)
@@ -39,7 +40,7 @@ def test_build_matches_reference_tree(gold, pre):
 @pytest.mark.parametrize("pre", ["small", "ties"])
 def test_oracle_traversal_matches_reference(gold, pre):
     book, enc, cross = _case(gold, pre)
-    t = AT.build_atree(enc, book, cross)
+    t = build_atree_host(enc, book, cross)
     Q = gold[f"{pre}_queries"]
     M = book.m_count
     pi = 0

@@ -100,3 +100,40 @@ def test_brute_force_knn_matches_reference():
         np.testing.assert_array_equal(gt.distances, g[f"r{r}_dists"])
     with pytest.raises(ValueError):
         brute_force_knn(g["base"], g["queries"][:, :3], 5)
+
+
+@pytest.mark.parametrize("pre", ["small", "ties"])
+def test_device_build_matches_reference_tree(gold, pre):
+    """The GPU build (radix passes + device scans) gives the reference's arrays."""
+    book = da.Codebook(codewords=gold[f"{pre}_codewords"], order=gold[f"{pre}_order"])
+    enc = da.EncodedDataset(codes=gold[f"{pre}_codes"], k_count=book.k_count)
+    Pm, _ = O.cross_table(book.codewords)
+    t = AT.build_atree(enc, book, types.SimpleNamespace(products=Pm))
+    assert t.n_root_children == gold[f"{pre}_tree_meta"][0]
+    for f in AT._TREE_FIELDS:
+        np.testing.assert_array_equal(getattr(t, f), gold[f"{pre}_tree_{f}"], err_msg=f)
+        assert getattr(t, f).dtype == gold[f"{pre}_tree_{f}"].dtype, f
+
+
+@pytest.mark.parametrize("M,K,n,dup,idmap", [(4, 16, 20000, 0.3, False), (8, 256, 200000, 0.05, True),
+                                             (3, 5, 4000, 0.5, True), (1, 8, 100, 0.0, False)])
+def test_device_build_matches_host_build(M, K, n, dup, idmap):
+    """Device build == the oracle's host restatement on larger, duplicate-heavy
+    code sets, with and without an id_map (ids ascending inside each leaf)."""
+    from oracle.atree_build import build_atree_host
+
+    rng = np.random.default_rng(M * 1000 + K)
+    cw = rng.standard_normal((M, K, 6)).astype(np.float32)
+    book = da.Codebook(codewords=cw, order=np.arange(M))
+    base = rng.integers(0, K, (max(1, int(n * (1 - dup))), M))
+    codes = base[rng.integers(0, len(base), n)].astype(np.uint8 if K <= 256 else np.uint16)
+    id_map = rng.permutation(10 * n)[:n].astype(np.int64) if idmap else None
+    enc = da.EncodedDataset(codes=codes, k_count=K, id_map=id_map)
+    Pm, _ = O.cross_table(cw)
+    cross = types.SimpleNamespace(products=Pm)
+    a = AT.build_atree(enc, book, cross)
+    b = build_atree_host(enc, book, cross)
+    assert a.n_root_children == b.n_root_children
+    for f in AT._TREE_FIELDS:
+        np.testing.assert_array_equal(getattr(a, f), getattr(b, f), err_msg=f)
+        assert getattr(a, f).dtype == getattr(b, f).dtype, f
