@@ -36,14 +36,16 @@ constexpr int SG_BM = 128, SG_BN = 128, SG_BK = 8, SG_T = 256;
 // chunk + D/chunk), or 0 (one sequential chain).  DA_SGEMM_CHUNK
 // overrides it (0 = sequential) for A/B runs.
 // Chunking costs registers (one CTA per SM: the D=960 table takes 155 instead
-// of 124 ms per 1M vectors) and pays only where the rechecks it saves are many:
-// wide beams (L=10, D=960: beam 248 -> 191 ms; L=1 loses).
+// of 124 ms per 1M vectors) and pays where the rechecks it saves are many:
+// wide beams (L=10, D=960: beam 248 -> 191 ms) and the greedy L=1 kernel,
+// whose exact stages follow the band (D=960 per 200k: greedy 20 -> 6 ms,
+// table 25 -> 31 ms).
 int sgemm_chunk(int D, int L) {
     if (const char* e = getenv("DA_SGEMM_CHUNK")) {
         const int c = atoi(e);
         return c <= 0 ? 0 : ((c + SG_BK - 1) / SG_BK) * SG_BK;
     }
-    if (D < 256 || L < 8) return 0;
+    if (D < 256 || (L > 1 && L < 8)) return 0;   // L = 1: the greedy kernel's band is the bound
     int c = (int)(sqrt((double)D) / SG_BK + 0.5) * SG_BK;
     return c < SG_BK ? SG_BK : c;
 }
