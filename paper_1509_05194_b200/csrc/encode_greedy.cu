@@ -112,7 +112,10 @@ __device__ __noinline__ int greedy_exact(GreedySmem S, const float* __restrict__
 }
 
 // One warp per vector, K == 256 (lane owns k = 4 lane + {0..3} and 128 + 4 lane + {0..3}).
-__global__ void __launch_bounds__(32 * GR_WARPS) greedy_kernel(
+#ifndef DA_GR_MINB
+#define DA_GR_MINB 7   // 40 registers: 56 warps per SM hide the gathers (L=1 per 1M: 11.8 -> 9.1 ms)
+#endif
+__global__ void __launch_bounds__(32 * GR_WARPS, DA_GR_MINB) greedy_kernel(
     const float* __restrict__ X, long long n, long long ldx, int D, const float* __restrict__ cw, int M, int K,
     const float* __restrict__ tab32, const double* __restrict__ sq, const double* __restrict__ P,
     const float* __restrict__ P32, const double* __restrict__ cmax, const double* __restrict__ cbm,
