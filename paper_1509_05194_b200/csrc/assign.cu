@@ -10,6 +10,7 @@
 // k staged through shared memory in chunks of 16.  The argmin is fused into
 // the epilogue of every codeword tile; a running (value, index) minimum per
 // row is kept in registers and reduced across the 16 column lanes at the end.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -290,11 +291,233 @@ __global__ void __launch_bounds__(256) assign_small_kernel(const TX* __restrict_
     }
 }
 
+// Narrow active widths (d <= 16, K <= 4096): an fp32 filter with a rigorous
+// bound, then float64 only where the bound cannot decide.  Thread per row; the
+// codebook as fp32 rows (+ fp32 norms) in shared memory.  v'(k) = cc'_k - 2 x'.c'_k
+// approximates v(k) = cc_k - 2 x.c_k within E = (2d + 12) u S with
+// S = xx + 2 ||x|| max||c|| + max cc (float representation of x, c and cc, the
+// d-term fp32 dot, the final subtraction, and the reference's own float64
+// roundings, generously).  Codeword k can be the reference's choice only if
+// max(xx + v'_k - E, 0) <= max(xx + min v' + E, 0) (the clip at 0 makes ties);
+// when that holds for the minimum alone it is the label, otherwise the kept
+// candidates are evaluated exactly like assign_small_kernel and the first
+// minimum wins.  d2 (when asked for) is the exact value of the label.
+// packed fp32 pair FMA (FFMA2): d = a * b + c lane-wise
+__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\t"
+        "mov.b64 rb, {%4, %4};\n\t"
+        "mov.b64 rd, {%0, %1};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rd;\n\t"
+        "mov.b64 {%0, %1}, rd;\n\t}"
+        : "+f"(d0), "+f"(d1)
+        : "f"(a0), "f"(a1), "f"(b0));
+    (void)b1;
+}
+
+constexpr int AF_R = 2;   // rows per thread: one codeword load and one FFMA2 feed both
+template <typename TX, int DM>
+__global__ void __launch_bounds__(256) assign_ffma_kernel(const TX* __restrict__ X, long long n, long long ldx, int d,
+                                                          const double* __restrict__ C, long long ldc, int K,
+                                                          const double* __restrict__ cc,
+                                                          const double* __restrict__ xx_in,
+                                                          int32_t* __restrict__ labels, double* __restrict__ d2,
+                                                          const int32_t* __restrict__ prev,
+                                                          unsigned long long* __restrict__ changed,
+                                                          unsigned long long* __restrict__ stats,
+                                                          int* __restrict__ hard, int* __restrict__ nhard) {
+    extern __shared__ __align__(16) float sCf[];   // [K][DM] fp32 codewords (zero padded), then [K] fp32 norms
+    float* scc = sCf + (size_t)K * DM;
+    __shared__ float s_cmax, s_ccmax;
+    if (threadIdx.x == 0) { s_cmax = 0.f; s_ccmax = 0.f; }
+    __syncthreads();
+    float cm = 0.f, ccm = 0.f;
+    for (int i = threadIdx.x; i < K * DM; i += blockDim.x) {
+        const int k = i / DM, j = i - k * DM;
+        sCf[i] = j < d ? (float)C[(long long)k * ldc + j] : 0.f;
+    }
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+        scc[k] = (float)cc[k];
+        ccm = fmaxf(ccm, __double2float_ru(cc[k]));
+        cm = fmaxf(cm, __double2float_ru(sqrt(cc[k]) * (1.0 + 1e-12)));
+    }
+    atomicMax(reinterpret_cast<int*>(&s_cmax), __float_as_int(cm));   // non-negative floats order like ints
+    atomicMax(reinterpret_cast<int*>(&s_ccmax), __float_as_int(ccm));
+    __syncthreads();
+    // persistent blocks: the codebook is staged once per block, rows stream through
+    for (long long rbase = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * AF_R; rbase < n;
+         rbase += (long long)gridDim.x * blockDim.x * AF_R) {
+    float x[AF_R][DM];
+    double xxv[AF_R];
+    float m1[AF_R], m2[AF_R];
+    int k1[AF_R];
+#pragma unroll
+    for (int t = 0; t < AF_R; ++t) {
+        const long long r = rbase + t < n ? rbase + t : rbase;
+        const TX* xr = X + r * ldx;
+#pragma unroll
+        for (int j = 0; j < DM; ++j) x[t][j] = j < d ? (float)xr[j] : 0.f;
+        xxv[t] = xx_in ? xx_in[r] : np_pw_sum([&](long long i) { double v = (double)xr[i]; return dmul(v, v); }, 0, d);
+        m1[t] = m2[t] = __int_as_float(0x7f800000);
+        k1[t] = 0;
+    }
+    // pass 1: fp32 filter values of both rows, two smallest + argmin per row
+    for (int k = 0; k < K; ++k) {
+        const float* c = sCf + (size_t)k * DM;
+        float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+        for (int j = 0; j < DM; j += 4) {
+            const float4 c4 = *reinterpret_cast<const float4*>(c + j);
+            ffma2(a0, a1, x[0][j], x[1][j], c4.x, c4.x);
+            ffma2(a0, a1, x[0][j + 1], x[1][j + 1], c4.y, c4.y);
+            ffma2(a0, a1, x[0][j + 2], x[1][j + 2], c4.z, c4.z);
+            ffma2(a0, a1, x[0][j + 3], x[1][j + 3], c4.w, c4.w);
+        }
+        const float ck = scc[k];
+        const float v0 = fmaf(-2.f, a0, ck), v1 = fmaf(-2.f, a1, ck);
+        k1[0] = v0 < m1[0] ? k : k1[0]; m2[0] = fminf(m2[0], fmaxf(m1[0], v0)); m1[0] = fminf(m1[0], v0);
+        k1[1] = v1 < m1[1] ? k : k1[1]; m2[1] = fminf(m2[1], fmaxf(m1[1], v1)); m1[1] = fminf(m1[1], v1);
+    }
+    unsigned nchg = 0;
+    unsigned long long nx = 0;
+#pragma unroll
+    for (int t = 0; t < AF_R; ++t) {
+        const long long r = rbase + t;
+        if (r >= n) continue;
+        const TX* xr = X + r * ldx;
+        const double xx = xxv[t];
+        const double S = xx + 2.0 * sqrt(xx) * (1.0 + 1e-12) * (double)s_cmax + (double)s_ccmax;
+        const float E = __double2float_ru((2.0 * d + 12.0) * 5.9604644775390625e-08 * S);
+        const float xxf = (float)xx;
+        const float lim = fmaxf(__fadd_ru(__fadd_ru(xxf, m1[t]), E) * (1.f + 1e-6f) + 1e-30f, 0.f);
+        const bool alone = fmaxf(__fsub_rd(__fadd_rd(xxf, m2[t]), E) * (1.f - 1e-6f), 0.f) > lim;
+        auto exact = [&](int k) -> double {
+            const double* crow = C + (long long)k * ldc;
+            double a = 0.0;
+            for (int j = 0; j < d; ++j) a = __fma_rn((double)xr[j], crow[j], a);
+            const double v = dadd(dsub(xx, dmul(2.0, a)), cc[k]);
+            return v < 0.0 ? 0.0 : v;
+        };
+        if (!alone) {   // rare: decided by assign_ffma_hard_kernel (a warp per row, no divergence here)
+            hard[atomicAdd(nhard, 1)] = (int)r;
+            continue;
+        }
+        const int lab = k1[t];
+        double best = 0.0;
+        if (d2) { best = exact(lab); ++nx; }
+        labels[r] = lab;
+        if (d2) d2[r] = best;
+        if (prev != nullptr && prev[r] != lab) ++nchg;
+    }
+    // threads past the end leave the loop early: no warp-wide reduction, one atomic per changed thread
+    if (changed != nullptr && prev != nullptr && nchg) atomicAdd(changed, (unsigned long long)nchg);
+    if (stats && nx) atomicAdd(stats, nx);
+    }
+}
+
+// Rows the fp32 filter could not decide: one warp per row, lane l takes
+// codewords l, l+32, ...; every kept codeword is evaluated exactly and the
+// lexicographic (value, index) minimum is the reference's first minimum.
+template <typename TX>
+__global__ void __launch_bounds__(256) assign_ffma_hard_kernel(const TX* __restrict__ X, long long ldx, int d,
+                                                               const double* __restrict__ C, long long ldc, int K,
+                                                               const double* __restrict__ cc,
+                                                               const double* __restrict__ xx_in,
+                                                               int32_t* __restrict__ labels, double* __restrict__ d2,
+                                                               const int32_t* __restrict__ prev,
+                                                               unsigned long long* __restrict__ changed,
+                                                               unsigned long long* __restrict__ stats,
+                                                               const int* __restrict__ hard, const int* __restrict__ nhard) {
+    const int lane = threadIdx.x & 31;
+    const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int nw = gridDim.x * (blockDim.x >> 5);
+    double cmax = 0.0, ccmax = 0.0;
+    for (int k = lane; k < K; k += 32) { ccmax = fmax(ccmax, cc[k]); }
+    for (int o = 16; o > 0; o >>= 1) ccmax = fmax(ccmax, __shfl_xor_sync(0xffffffffu, ccmax, o));
+    cmax = sqrt(ccmax) * (1.0 + 1e-12);
+    for (int h = w; h < *nhard; h += nw) {
+        const long long r = hard[h];
+        const TX* xr = X + r * ldx;
+        const double xx = xx_in ? xx_in[r]
+                                : np_pw_sum([&](long long i) { double t = (double)xr[i]; return dmul(t, t); }, 0, d);
+        const double S = xx + 2.0 * sqrt(xx) * (1.0 + 1e-12) * cmax + ccmax;
+        const float E = __double2float_ru((2.0 * d + 12.0) * 5.9604644775390625e-08 * S);
+        const float xxf = (float)xx;
+        // same fp32 values as the filter (same operand roundings, same FMA order)
+        float vmin = __int_as_float(0x7f800000);
+        auto fval = [&](int k) -> float {
+            const double* crow = C + (long long)k * ldc;
+            float dot = 0.f;
+            for (int j = 0; j < d; ++j) dot = fmaf((float)xr[j], (float)crow[j], dot);
+            return fmaf(-2.f, dot, (float)cc[k]);
+        };
+        for (int k = lane; k < K; k += 32) vmin = fminf(vmin, fval(k));
+        for (int o = 16; o > 0; o >>= 1) vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+        const float lim = fmaxf(__fadd_ru(__fadd_ru(xxf, vmin), E) * (1.f + 1e-6f) + 1e-30f, 0.f);
+        double best = __longlong_as_double(0x7ff0000000000000ULL);
+        int lab = 0x7fffffff;
+        unsigned long long nx = 0;
+        for (int k = lane; k < K; k += 32) {
+            if (fmaxf(__fsub_rd(__fadd_rd(xxf, fval(k)), E) * (1.f - 1e-6f), 0.f) <= lim) {
+                const double* crow = C + (long long)k * ldc;
+                double a = 0.0;
+                for (int j = 0; j < d; ++j) a = __fma_rn((double)xr[j], crow[j], a);
+                double v = dadd(dsub(xx, dmul(2.0, a)), cc[k]);
+                if (v < 0.0) v = 0.0;
+                ++nx;
+                if (lex_less(v, k, best, lab)) { best = v; lab = k; }
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+            const int ok = __shfl_xor_sync(0xffffffffu, lab, o);
+            if (lex_less(ov, ok, best, lab)) { best = ov; lab = ok; }
+        }
+        for (int o = 16; o > 0; o >>= 1) nx += __shfl_xor_sync(0xffffffffu, nx, o);
+        if (lane == 0) {
+            labels[r] = lab;
+            if (d2) d2[r] = best;
+            if (changed != nullptr && prev != nullptr && prev[r] != lab) atomicAdd(changed, 1ULL);
+            if (stats && nx) atomicAdd(stats, nx);
+        }
+    }
+}
+
 int launch_assign(const void* X, int x_is_f32, long long n, long long ldx, int d, const double* C,
                   long long ldc, int K, const double* cc, const double* xx, int32_t* labels, double* d2,
                   const int32_t* prev, unsigned long long* changed, cudaStream_t s) {
     if (n <= 0) return 0;
-    // measured crossover against the tensor-core filter on B200: d <= 3
+    // fp32 filter for narrow prefixes (d <= 16), then the float64 kernels
+    static const int ffma_max = getenv("DA_ASSIGN_FFMA_D") ? atoi(getenv("DA_ASSIGN_FFMA_D")) : 8;   // B200, 1M rows: d=2 0.25 -> 0.14 ms, d=8 0.33 -> 0.25; the tcgen05 filter wins from d=12
+    if (g_assign_mode == 0 && d <= ffma_max && d <= 16 && K <= 4096) {
+        ProfScope ps("assign_ffma_d<=8", s);
+        const int dm = d <= 4 ? 4 : d <= 8 ? 8 : 16;
+        const size_t smem = sizeof(float) * ((size_t)K * dm + K);
+        int dev_ = 0, sms_ = 148;
+        cudaGetDevice(&dev_);
+        cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dev_);
+        const unsigned g = (unsigned)std::min<long long>((n + AF_R * 256 - 1) / (AF_R * 256), 4LL * sms_);
+        int* nhard = (int*)scratch(22, sizeof(int) * ((size_t)n + 64), s);
+        if (!nhard) return fail_cuda(cudaErrorMemoryAllocation, "assign_ffma scratch");
+        int* hard = nhard + 64;
+        DA_CUDA(cudaMemsetAsync(nhard, 0, sizeof(int), s));
+#define AF_LAUNCH(T, DMv)                                                                                            \
+    do {                                                                                                             \
+        if (smem > 48 * 1024)                                                                                        \
+            DA_CUDA(cudaFuncSetAttribute(assign_ffma_kernel<T, DMv>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                         (int)smem));                                                                \
+        assign_ffma_kernel<T, DMv><<<g, 256, smem, s>>>((const T*)X, n, ldx, d, C, ldc, K, cc, xx, labels, d2, prev, \
+                                                        changed, g_assign_stats, hard, nhard);                       \
+        DA_CHECK_LAUNCH("assign_ffma_kernel");                                                                       \
+        assign_ffma_hard_kernel<T><<<2 * sms_, 256, 0, s>>>((const T*)X, ldx, d, C, ldc, K, cc, xx, labels, d2, prev, \
+                                                           changed, g_assign_stats, hard, nhard);                    \
+    } while (0)
+        if (x_is_f32) { if (dm == 4) AF_LAUNCH(float, 4); else if (dm == 8) AF_LAUNCH(float, 8); else AF_LAUNCH(float, 16); }
+        else { if (dm == 4) AF_LAUNCH(double, 4); else if (dm == 8) AF_LAUNCH(double, 8); else AF_LAUNCH(double, 16); }
+#undef AF_LAUNCH
+        DA_CHECK_LAUNCH("assign_ffma_hard_kernel");
+        return 0;
+    }
     static const int small_max = getenv("DA_ASSIGN_SMALL_D") ? atoi(getenv("DA_ASSIGN_SMALL_D")) : 3;
     if (g_assign_mode == 0 && d <= small_max && K <= 4096) {
         ProfScope ps("assign_small_d<=16", s);
