@@ -336,6 +336,15 @@ def dry_run(args):
         dist.destroy_process_group()
 
 
+def _adc_traffic() -> float:
+    """DRAM bytes per ADC candidate from the committed ncu capture (72 B: the 64-B L2 granule + the id)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r02.json")) as f:
+            return float(json.load(f)["adc_scan_packed"]["bytes_per_candidate"])
+    except (OSError, KeyError, ValueError):
+        return float("nan")
+
+
 def anneal_flop(log, N, Dd, Mm, Kk):
     """sum_m [2ND^2 (Gram) + 2ND^2 (rotate) + sum_s (I+1) 2NKd_s
     + 2*2NKD (final/init assigns) + 2NMKD (encode)], I from the Lloyd log."""
@@ -471,7 +480,10 @@ def main():
     def compute_roof(name, flop, sec, extra=None):
         a = flop / sec / 1e12
         r = {"bound": "compute", "achieved": a, "unit": "TFLOP/s", "peak_ffma": ffma, "frac_ffma": a / ffma,
-             "peak_3xtf32": tf32_peak / 3.0, "frac_3xtf32": a / (tf32_peak / 3.0)}
+             "peak_3xtf32": tf32_peak / 3.0, "frac_3xtf32": a / (tf32_peak / 3.0),
+             # /2 when x is exact in tf32 (integer config-B rows): the score table then runs two
+             # tf32 MMAs per k step (table_tc_x_kernel), so this is the tensor-core roof of the encode table
+             "peak_2xtf32": tf32_peak / 2.0, "frac_2xtf32": a / (tf32_peak / 2.0)}
         if extra:
             r.update(extra)
         rooflines[name] = r
@@ -657,7 +669,9 @@ def main():
         rooflines["adc_scan"] = {"bound": "hbm", "kernel": "adc_scan_packed_kernel", "achieved": ach,
                                  "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": ach / pk["hbm_gbs"],
                                  "algorithmic": "40 B per candidate (8-B id + one 32-B sector of the 16-B record)",
-                                 "traffic_source": "profiles/ncu_adc_r02.txt (dram bytes per candidate)"}
+                                 "traffic": _adc_traffic() * ncand_tot,
+                                 "traffic_unit": "bytes per launch (DRAM read + write, ncu)",
+                                 "traffic_source": "profiles/ncu_traffic_r02.json: adc_scan_packed bytes per candidate"}
         del rec_e, cand_r, lut_e, Qe
 
     # --- A-Tree: GPU build over this GPU's L=10 codes, GPU batched search

@@ -11,7 +11,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"
 # full captures: L=10 beam kernel, tcgen05 score table, L=1 greedy kernel, ADC scan
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:beam_fast -c 1 -o gpurun_out/prof_beam_fast -f \
     python tools/prof_tc.py 2 10 > gpurun_out/ncu_bf.log 2>&1; echo "full bf rc=$?"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"table_tc|greedy" -c 2 -o gpurun_out/prof_l1 -f \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"table_tc_x|greedy" -c 2 -o gpurun_out/prof_l1 -f \
     python tools/prof_tc.py 2 1 > gpurun_out/ncu_l1.log 2>&1; echo "full l1 rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:adc_scan_packed -c 1 -o gpurun_out/prof_adc -f \
     python tools/bench_adc.py 100000000 2000 100000 > gpurun_out/ncu_adc.log 2>&1; echo "full adc rc=$?"
