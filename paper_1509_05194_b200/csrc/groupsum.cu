@@ -97,24 +97,68 @@ __global__ void seg_counts_kernel(const int32_t* __restrict__ offs, int K, int T
 }
 
 // One warp per label: exclusive scan of hist[k][0..T) in place; counts[k] = total.
-__global__ void label_tile_scan_kernel(int32_t* __restrict__ hist, int K, int T, int32_t* __restrict__ counts) {
+// The last block to finish (threadfence + counter) also writes the segment
+// starts seg = exclusive_scan(counts) and *total -- one launch instead of three.
+__global__ void label_tile_scan_kernel(int32_t* __restrict__ hist, int K, int T, int32_t* __restrict__ counts,
+                                       int32_t* __restrict__ seg, int32_t* __restrict__ total,
+                                       unsigned* __restrict__ done) {
     const int lane = threadIdx.x & 31;
     const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (k >= K) return;
-    int32_t* row = hist + (long long)k * T;
-    int carry = 0;
-    for (int b = 0; b < T; b += 32) {
-        const int t = b + lane;
-        const int v = t < T ? row[t] : 0;
-        int incl = v;
-        for (int off = 1; off < 32; off <<= 1) {
-            const int o = __shfl_up_sync(0xffffffffu, incl, off);
-            if (lane >= off) incl += o;
+    if (k < K) {
+        int32_t* row = hist + (long long)k * T;
+        int carry = 0;
+        for (int b = 0; b < T; b += 32) {
+            const int t = b + lane;
+            const int v = t < T ? row[t] : 0;
+            int incl = v;
+            for (int off = 1; off < 32; off <<= 1) {
+                const int o = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += o;
+            }
+            if (t < T) row[t] = carry + incl - v;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
         }
-        if (t < T) row[t] = carry + incl - v;
-        carry += __shfl_sync(0xffffffffu, incl, 31);
+        if (lane == 0) counts[k] = carry;
     }
-    if (lane == 0) counts[k] = carry;
+    if (seg == nullptr) return;
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // block-wide exclusive scan of the K counts (K / blockDim per thread, in order)
+    __shared__ int wsum[32];
+    const int nt = blockDim.x, per = (K + nt - 1) / nt;
+    const int lo = min(K, threadIdx.x * per), hi = min(K, lo + per);
+    int sum = 0;
+    for (int i = lo; i < hi; ++i) sum += __ldcg(counts + i);
+    int incl = sum;
+    for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+    }
+    if (lane == 31) wsum[threadIdx.x >> 5] = incl;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int w = threadIdx.x < (nt >> 5) ? wsum[threadIdx.x] : 0;
+        int wi = w;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int o = __shfl_up_sync(0xffffffffu, wi, off);
+            if (lane >= off) wi += o;
+        }
+        wsum[threadIdx.x] = wi - w;
+        if (threadIdx.x == 31) *total = wi;
+    }
+    __syncthreads();
+    int run = wsum[threadIdx.x >> 5] + incl - sum;
+    for (int i = lo; i < hi; ++i) {
+        const int v = __ldcg(counts + i);
+        seg[i] = run;
+        run += v;
+    }
+    if (threadIdx.x == 0) *done = 0u;   // ready for the next call on this stream
 }
 
 // hist[k][t] += seg_start[k] (turns within-label offsets into global cursors)
@@ -168,10 +212,25 @@ __global__ void stable_scatter_kernel(const int32_t* __restrict__ labels, long l
 // [lo + 256w, lo + 256w + 256); per-warp label counts (shared memory) turn the
 // tile cursor into per-warp cursors, so the rows still land in row order.
 constexpr int GS_SW = 4;
+// Lanes holding the same label (what __match_any_sync returns), built from one
+// ballot per label bit: ballots are single cheap instructions, while match.any
+// serialises over the distinct values of the warp (the stable scatter issued
+// 16 of them per warp per tile and was the slowest bookkeeping kernel).
+__device__ __forceinline__ unsigned gs_match(unsigned active, int lab, int nbits) {
+    unsigned peers = active;
+    for (int b = 0; b < nbits; ++b) {
+        const unsigned on = __ballot_sync(active, (lab >> b) & 1);
+        peers &= ((lab >> b) & 1) ? on : ~on;
+    }
+    return peers;
+}
+
 __global__ void __launch_bounds__(32 * GS_SW) stable_scatter4_kernel(const int32_t* __restrict__ labels, long long n,
                                                                     int K, int T, const int32_t* __restrict__ cursor,
-                                                                    int32_t* __restrict__ order) {
+                                                                    int32_t* __restrict__ order,
+                                                                    const int32_t* __restrict__ seg) {
     extern __shared__ int32_t wc[];   // [GS_SW][K]
+    const int nbits = 32 - __clz(max(K - 1, 1));
     const int t = blockIdx.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const long long lo = (long long)t * GS_TILE + (long long)w * (GS_TILE / GS_SW);
@@ -186,14 +245,14 @@ __global__ void __launch_bounds__(32 * GS_SW) stable_scatter4_kernel(const int32
         const unsigned active = __ballot_sync(0xffffffffu, valid);
         if (valid) {
             const int lab = labels[r];
-            const unsigned peers = __match_any_sync(active, lab);
+            const unsigned peers = gs_match(active, lab, nbits);
             if (lane == __ffs(peers) - 1) my[lab] += __popc(peers);
         }
         __syncwarp();
     }
     __syncthreads();
     for (int k = threadIdx.x; k < K; k += blockDim.x) {
-        int c = cursor[(long long)k * T + t];
+        int c = cursor[(long long)k * T + t] + (seg ? seg[k] : 0);
 #pragma unroll
         for (int q = 0; q < GS_SW; ++q) {
             const int v = wc[q * K + k];
@@ -210,7 +269,7 @@ __global__ void __launch_bounds__(32 * GS_SW) stable_scatter4_kernel(const int32
         lab_next = (r + 32 < hi) ? labels[r + 32] : 0;
         const unsigned active = __ballot_sync(0xffffffffu, valid);
         if (valid) {
-            const unsigned peers = __match_any_sync(active, lab);
+            const unsigned peers = gs_match(active, lab, nbits);
             const int leader = __ffs(peers) - 1;
             const int rank = __popc(peers & lt_mask);
             int b = 0;
@@ -641,11 +700,25 @@ __global__ void __launch_bounds__(32) seg_finish_kernel(const double* __restrict
 static int gs_stable_sort(const int32_t* labels, long long n, int K, int T, int32_t* hist, int32_t* counts,
                           int32_t* seg, int32_t* total, int32_t* order, cudaStream_t s) {
     const long long KT = (long long)K * T;
-    DA_CUDA(cudaMemsetAsync(hist, 0, sizeof(int32_t) * (KT + 1), s));
-    size_t sh = (K <= GS_SMEM_HIST) ? sizeof(int32_t) * K : 0;
+    const bool smem_hist = K <= GS_SMEM_HIST;   // tiles write their whole histogram column: no memset
+    const bool fast = (size_t)GS_SW * K * sizeof(int32_t) <= 48 * 1024 && K <= 1024;
+    if (!smem_hist) DA_CUDA(cudaMemsetAsync(hist, 0, sizeof(int32_t) * (KT + 1), s));
+    size_t sh = smem_hist ? sizeof(int32_t) * K : 0;
     tile_hist_kernel<<<T, 256, sh, s>>>(labels, n, K, T, hist);
     DA_CHECK_LAUNCH("tile_hist_kernel");
-    label_tile_scan_kernel<<<grid_for(K, 8), 256, 0, s>>>(hist, K, T, counts);
+    if (fast) {
+        // tile scan + segment starts in one launch; the scatter adds seg to the tile cursors
+        unsigned* done = (unsigned*)scratch(23, 256, s);
+        static thread_local void* zeroed = nullptr;   // the kernel leaves the counter at 0 for the next call
+        if (!done) return fail_cuda(cudaErrorMemoryAllocation, "label scan counter");
+        if (zeroed != done) { DA_CUDA(cudaMemsetAsync(done, 0, 256, s)); zeroed = done; }
+        label_tile_scan_kernel<<<grid_for(K, 8), 256, 0, s>>>(hist, K, T, counts, seg, total, done);
+        DA_CHECK_LAUNCH("label_tile_scan_kernel");
+        stable_scatter4_kernel<<<T, 32 * GS_SW, sizeof(int32_t) * GS_SW * K, s>>>(labels, n, K, T, hist, order, seg);
+        DA_CHECK_LAUNCH("stable_scatter4_kernel");
+        return 0;
+    }
+    label_tile_scan_kernel<<<grid_for(K, 8), 256, 0, s>>>(hist, K, T, counts, nullptr, nullptr, nullptr);
     DA_CHECK_LAUNCH("label_tile_scan_kernel");
     DA_CUDA(cudaMemcpyAsync(seg, counts, sizeof(int32_t) * K, cudaMemcpyDeviceToDevice, s));
     exclusive_scan_kernel<<<1, 1024, 0, s>>>(seg, K, total);
@@ -653,7 +726,8 @@ static int gs_stable_sort(const int32_t* labels, long long n, int K, int T, int3
     add_seg_start_kernel<<<grid_for(KT, 256, 1LL << 31), 256, 0, s>>>(hist, K, T, seg);
     DA_CHECK_LAUNCH("add_seg_start_kernel");
     if ((size_t)GS_SW * K * sizeof(int32_t) <= 48 * 1024) {
-        stable_scatter4_kernel<<<T, 32 * GS_SW, sizeof(int32_t) * GS_SW * K, s>>>(labels, n, K, T, hist, order);
+        stable_scatter4_kernel<<<T, 32 * GS_SW, sizeof(int32_t) * GS_SW * K, s>>>(labels, n, K, T, hist, order,
+                                                                                   nullptr);
         DA_CHECK_LAUNCH("stable_scatter4_kernel");
     } else {
         stable_scatter_kernel<<<T, 32, sh, s>>>(labels, n, K, T, hist, order);
