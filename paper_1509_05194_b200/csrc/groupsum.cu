@@ -107,16 +107,25 @@ __global__ void label_tile_scan_kernel(int32_t* __restrict__ hist, int K, int T,
     if (k < K) {
         int32_t* row = hist + (long long)k * T;
         int carry = 0;
-        for (int b = 0; b < T; b += 32) {
-            const int t = b + lane;
-            const int v = t < T ? row[t] : 0;
-            int incl = v;
-            for (int off = 1; off < 32; off <<= 1) {
-                const int o = __shfl_up_sync(0xffffffffu, incl, off);
-                if (lane >= off) incl += o;
+        // 16 chunks of 32 tiles in flight per batch (the loads were the latency chain)
+        for (int b0 = 0; b0 < T; b0 += 32 * 16) {
+            int v[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int t = b0 + 32 * q + lane;
+                v[q] = t < T ? row[t] : 0;
             }
-            if (t < T) row[t] = carry + incl - v;
-            carry += __shfl_sync(0xffffffffu, incl, 31);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int t = b0 + 32 * q + lane;
+                int incl = v[q];
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int o = __shfl_up_sync(0xffffffffu, incl, off);
+                    if (lane >= off) incl += o;
+                }
+                if (t < T) row[t] = carry + incl - v[q];
+                carry += __shfl_sync(0xffffffffu, incl, 31);
+            }
         }
         if (lane == 0) counts[k] = carry;
     }
