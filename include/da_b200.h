@@ -111,9 +111,12 @@ int da_reconstruct(const void* codes, int code_bytes, int64_t n, int64_t ldc, co
  *                      | K*d segment first rows) with -0.0 and this shard's leaves
  *                      and first rows; the states of leaves cut at the right
  *                      boundary go to send_state (K*8*d); counts_global = n_k;
- *   world-1 rounds of { send send_state right, receive recv_state from the
- *                      left; da_gs_shard_round } (a cut leaf's state crosses
- *                      one boundary per round);
+ *   `rounds` (<= world-1) rounds of { send send_state right, receive recv_state
+ *                      from the left; da_gs_shard_round } (a cut leaf's state
+ *                      crosses one boundary per round); the plan adds 1.0 to
+ *                      *overflow (when non-NULL) for every cut leaf that spans
+ *                      more than `rounds` boundaries -- the caller then redoes
+ *                      the update with world-1 rounds;
  *   allreduce(sum) of red, then da_gs_shard_fold: mode 0 = means into the
  *                      filled rows of out, mode 1 = raw sums.
  * cap_leaves >= K + N/64 + 2 (N = global rows).  One shard per process. */
@@ -121,7 +124,7 @@ int da_gs_shard_sort(const double* X, int64_t n, int64_t ldx, int d, const int32
                      int32_t* counts_local, void* stream);
 int da_gs_shard_plan(const double* X, int64_t n, int64_t ldx, int d, int K, const int32_t* counts_all, int world,
                      int rank, int64_t cap_leaves, double* red, double* send_state, int32_t* counts_global,
-                     void* stream);
+                     int rounds, double* overflow, void* stream);
 int da_gs_shard_round(const double* X, int64_t ldx, int d, int K, const double* recv_state, double* send_state,
                       double* red, void* stream);
 int da_gs_shard_fold(int d, int K, const double* red, int64_t cap_leaves, const int32_t* counts_global, int mode,
@@ -141,13 +144,13 @@ int da_lloyd_step(const double* X, int64_t n, int64_t ldx, int d, int K, const d
                   void* stream);
 
 /* Sharded Lloyd iteration around the collective:
- *   da_lloyd_prepare: C_out = C_prev (and snap), stats[0:2] = [*changed_prev, 0]
+ *   da_lloyd_prepare: C_out = C_prev (and snap), stats[0:3] = [*changed_prev, 0, 0]
  *                     (the previous assign's stats ride this update's allreduce);
  *   da_lloyd_finish:  after the allreduce.  fast=1: red = [sums K*d | counts K |
  *                     ..], C[k, :d] = sums / counts where counts > 0; fast=0: the
  *                     means are already in C (da_gs_shard_fold) and counts are
- *                     the global counts.  flags_dev (3 f64) = [#empty, stats[0],
- *                     stats[1]] -> flags_host + event, *changed = 0, then (if
+ *                     the global counts.  flags_dev (4 f64) = [#empty, stats[0],
+ *                     stats[1], stats[2]] -> flags_host + event, *changed = 0, then (if
  *                     labels_out) the assign of X against C like da_lloyd_step. */
 int da_lloyd_prepare(const double* C_prev, double* C_out, double* snap, int64_t elems,
                      const unsigned long long* changed_prev, double* stats, void* stream);

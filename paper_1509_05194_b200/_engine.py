@@ -334,17 +334,20 @@ class _ShardSums:
         self.send = torch.zeros(K * 8 * D, dtype=F64, device=dev)
         self.recv = torch.zeros(K * 8 * D, dtype=F64, device=dev)
 
-    def plan(self, Xr, d, labels, red, gcount):
+    def plan(self, Xr, d, labels, red, gcount, rounds=None, overflow=None):
         """Leaf sums + first rows of this shard into red (then allreduced by
-        the caller); gcount = global label counts."""
+        the caller); gcount = global label counts.  `rounds` neighbour
+        exchanges (default: all world-1); the plan adds to `overflow` for cut
+        leaves spanning more boundaries (the caller redoes the update)."""
         comm, K = self.comm, self.K
         n = Xr.shape[0]
         native.da_gs_shard_sort(P(Xr), n, Xr.stride(0), d, P(labels), K, P(self.cnt_local), stream())
         cnt_all = comm.allgather(self.cnt_local)
         send, recv = self.send[: K * 8 * d], self.recv[: K * 8 * d]
+        rounds = comm.world - 1 if rounds is None else min(rounds, comm.world - 1)
         native.da_gs_shard_plan(P(Xr), n, Xr.stride(0), d, K, P(cnt_all), comm.world, comm.rank, self.cap, P(red),
-                                P(send), P(gcount), stream())
-        for _ in range(comm.world - 1):
+                                P(send), P(gcount), rounds, P(overflow), stream())
+        for _ in range(rounds):
             comm.shift_(send, recv)
             native.da_gs_shard_round(P(Xr), Xr.stride(0), d, K, P(recv), P(send), P(red), stream())
 
@@ -371,8 +374,11 @@ def _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm, la
     da = active
     ntot = float(comm.total(n))
     if not _FLAGS_SH:
-        _FLAGS_SH.extend(torch.zeros(3, dtype=F64, pin_memory=True) for _ in range(2))
+        _FLAGS_SH.extend(torch.zeros(4, dtype=F64, pin_memory=True) for _ in range(2))
     flags_h = _FLAGS_SH
+    # neighbour rounds of the exact exchange: most cut leaves span one boundary;
+    # an update whose leaves need more is redone with world - 1 rounds (flag)
+    rounds = min(comm.world - 1, int(os.environ.get("DA_SHARD_ROUNDS", "2")))
     exact = getattr(comm, "exact", False)
     sh = _ShardSums(K, D, int(ntot), comm, dev) if exact else None
     # reduced buffer: [sums | counts] (fast) or [leaf sums | first rows] (exact),
@@ -380,13 +386,13 @@ def _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm, la
     nst = sh.cap * da + K * da if exact else K * da + K
 
     def new_slot(Cbuf):
-        nred = nst + 2
+        nred = nst + 3
         return (Cbuf, torch.empty(nred, dtype=F64, device=dev), torch.empty(K, dtype=I32, device=dev),
-                torch.zeros(1, dtype=torch.int64, device=dev), torch.zeros(3, dtype=F64, device=dev),
+                torch.zeros(1, dtype=torch.int64, device=dev), torch.zeros(4, dtype=F64, device=dev),
                 torch.cuda.Event())
 
     slots = [new_slot(C), new_slot(torch.empty_like(C))]
-    snaps = [torch.empty_like(C), torch.empty_like(C)] if lazy else None
+    snaps = [torch.empty_like(C), torch.empty_like(C)]   # C before each update: reseed errors, exchange redo
 
     def put_stats(dst, chg, ne):
         """dst[0:2] = this shard's [rows changed, error sum] of one assign."""
@@ -402,15 +408,15 @@ def _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm, la
     for sl in slots:
         sl[5].record()                               # creates the event handles da_lloyd_finish records into
 
-    def launch(C_prev, labels_prev, slot, pchg, pne):
+    def launch(C_prev, labels_prev, slot, pchg, pne, nrounds=None):
         Cn, red, cn, chg, fl, ev = slots[slot]
-        # C_out = C_prev (+ snapshot for a lazy reseed), previous assign's stats -> red[nst:]
-        native.da_lloyd_prepare(P(C_prev), P(Cn), P(snaps[slot]) if lazy else None, C.numel(), P(pchg),
-                                P(red[nst:]), stream())
+        # C_out = C_prev (+ snapshot), previous assign's stats -> red[nst:]
+        native.da_lloyd_prepare(P(C_prev), P(Cn), P(snaps[slot]) if C_prev is not snaps[slot] else None, C.numel(),
+                                P(pchg), P(red[nst:]), stream())
         if pne is not None and n:
             native.da_np_sum(P(pne), n, 0, P(red[nst + 1:nst + 2]), stream())
         if exact:
-            sh.plan(Xr, da, labels_prev, red, cn)
+            sh.plan(Xr, da, labels_prev, red, cn, rounds if nrounds is None else nrounds, red[nst + 2:nst + 3])
         else:
             if n:
                 native.da_group_sums(P(Xr), n, Xr.stride(0), da, P(labels_prev), K, 1, P(red), da, P(cn), stream())
@@ -438,6 +444,13 @@ def _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm, la
         slot, labels_prev, _, _ = cur
         Cn, red, cn, chg, fl, ev = slots[slot]
         ev.synchronize()
+        if flags_h[slot][3].item():
+            # a cut leaf spanned more shards than the exchange rounds: redo this update
+            if os.environ.get("DA_DEBUG"):
+                print(f"[da] shard exchange overflow at iteration {iters}: redo with {comm.world - 1} rounds", flush=True)
+            spec = None
+            cur = launch(snaps[slot], labels_prev, slot, None, None, comm.world - 1)
+            ev.synchronize()
         if flags_h[slot][0].item():
             spec = None                              # computed from pre-reseed centroids
             gcnt = cn if exact else red[K * da:nst]

@@ -41,7 +41,7 @@ _SIGNATURES = {
     "da_lloyd_prepare": [_P, _P, _P, _L, _P, _P, _P],
     "da_lloyd_finish": [_I, _P, _P, _I, _I, _P, _L, _P, _P, _P, _P, _P, _L, _L, _P, _P, _P, _P, _P, _P],
     "da_gs_shard_sort": [_P, _L, _L, _I, _P, _I, _P, _P],
-    "da_gs_shard_plan": [_P, _L, _L, _I, _I, _P, _I, _I, _L, _P, _P, _P, _P],
+    "da_gs_shard_plan": [_P, _L, _L, _I, _I, _P, _I, _I, _L, _P, _P, _P, _I, _P, _P],
     "da_gs_shard_round": [_P, _L, _I, _I, _P, _P, _P, _P],
     "da_gs_shard_fold": [_I, _I, _P, _L, _P, _I, _P, _L, _P],
     "da_rotate": [_P, _I, _L, _L, _I, _P, _P, _P, _I, _P],

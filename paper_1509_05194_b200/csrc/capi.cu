@@ -150,11 +150,11 @@ int da_gs_shard_sort(const double* X, int64_t n, int64_t ldx, int d, const int32
 
 int da_gs_shard_plan(const double* X, int64_t n, int64_t ldx, int d, int K, const int32_t* counts_all, int world,
                      int rank, int64_t cap_leaves, double* red, double* send_state, int32_t* counts_global,
-                     void* stream) {
+                     int rounds, double* overflow, void* stream) {
     if (world < 1 || rank < 0 || rank >= world || cap_leaves < 1 || d < 1)
         return fail_arg("gs_shard_plan: bad arguments world=%d rank=%d cap=%lld", world, rank, (long long)cap_leaves);
     return launch_gs_shard_plan(X, n, ldx, d, K, counts_all, world, rank, cap_leaves, red, send_state, counts_global,
-                                STREAM(stream));
+                                rounds, overflow, STREAM(stream));
 }
 
 int da_gs_shard_round(const double* X, int64_t ldx, int d, int K, const double* recv_state, double* send_state,

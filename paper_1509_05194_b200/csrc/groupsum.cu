@@ -910,7 +910,8 @@ __global__ void shard_enum_kernel(const int32_t* __restrict__ gcount, const int3
                                   const int32_t* __restrict__ cnt, const int32_t* __restrict__ seg,
                                   const int32_t* __restrict__ leaf_base, int K, int4* __restrict__ local_leaves,
                                   int32_t* __restrict__ nlocal, int4* __restrict__ itemL, int4* __restrict__ itemR,
-                                  int32_t* __restrict__ first_pos) {
+                                  int32_t* __restrict__ first_pos, const int32_t* __restrict__ cnt_all, int rank,
+                                  int rounds, double* __restrict__ overflow) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= K) return;
     const int n = gcount[k], off = goff[k], c = cnt[k];
@@ -937,8 +938,18 @@ __global__ void shard_enum_kernel(const int32_t* __restrict__ gcount, const int3
             } else {
                 const int s = max(ra, lo) - lo, e = min(rb, lo + x) - lo;
                 const int4 it = make_int4(gi, lpos(lo + s), s + 256 * e, x);
-                if (s > 0) itemL[k] = it;
-                else itemR[k] = it;
+                if (s > 0) {
+                    itemL[k] = it;
+                    // shards this leaf's state crosses before reaching us: more than `rounds`
+                    // neighbour exchanges -> the update is redone with world - 1 rounds
+                    if (overflow) {
+                        int r = rank, o = off;                  // segment position of our first row
+                        while (r > 0 && o > lo + 1) { --r; o -= cnt_all[(long long)r * K + k]; }
+                        if (rank - r > rounds) atomicAdd(overflow, 1.0);
+                    }
+                } else {
+                    itemR[k] = it;
+                }
             }
             continue;
         }
@@ -1055,7 +1066,8 @@ int launch_gs_shard_sort(const double* X, long long n, long long ldx, int d, con
 }
 
 int launch_gs_shard_plan(const double* X, long long n, long long ldx, int d, int K, const int32_t* cnt_all, int W,
-                         int rank, long long cap, double* red, double* send, int32_t* gcount, cudaStream_t s) {
+                         int rank, long long cap, double* red, double* send, int32_t* gcount, int rounds,
+                         double* overflow, cudaStream_t s) {
     ShardState& S = g_shard;
     if (S.K != K || S.n != n) return fail_arg("shard plan: call da_gs_shard_sort on the same rows first");
     S.cap = cap;
@@ -1070,7 +1082,7 @@ int launch_gs_shard_plan(const double* X, long long n, long long ldx, int d, int
     DA_CHECK_LAUNCH("exclusive_scan_kernel(shard leaves)");
     DA_CUDA(cudaMemsetAsync(S.nlocal, 0, sizeof(int32_t), s));
     shard_enum_kernel<<<grid_for(K, 128), 128, 0, s>>>(gcount, S.goff, S.cnt, S.seg, S.leaf_base, K, ll, S.nlocal,
-                                                       S.itemL, S.itemR, S.first_pos);
+                                                       S.itemL, S.itemR, S.first_pos, cnt_all, rank, rounds, overflow);
     DA_CHECK_LAUNCH("shard_enum_kernel");
     const long long len = cap * d + (long long)K * d;
     fill_neg_zero_kernel<<<grid_for(len, 256, 4096), 256, 0, s>>>(red, len);

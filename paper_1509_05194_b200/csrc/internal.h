@@ -48,7 +48,8 @@ int launch_group_sums(const double* X, long long n, long long ldx, int D, const 
 int launch_gs_shard_sort(const double* X, long long n, long long ldx, int d, const int32_t* labels, int K,
                          int32_t* counts_local, cudaStream_t s);
 int launch_gs_shard_plan(const double* X, long long n, long long ldx, int d, int K, const int32_t* cnt_all, int W,
-                         int rank, long long cap, double* red, double* send, int32_t* gcount, cudaStream_t s);
+                         int rank, long long cap, double* red, double* send, int32_t* gcount, int rounds,
+                         double* overflow, cudaStream_t s);
 int launch_gs_shard_round(const double* X, long long ldx, int d, int K, const double* recv, double* send, double* red,
                           cudaStream_t s);
 int launch_gs_shard_fold(int d, int K, const double* red, long long cap, const int32_t* gcount, int mode, double* out,

@@ -11,7 +11,7 @@
 //                     buffer's stats slot;
 //   da_lloyd_finish   shards, after the allreduce: means of the fast mode
 //                     (sums / counts, IEEE division, empties untouched), flags
-//                     [#empty, rows changed, error sum] -> pinned host + event,
+//                     [#empty, rows changed, error sum, exchange overflow] -> pinned host + event,
 //                     then the assign against the new centroids.
 #include <cuda_runtime.h>
 
@@ -37,10 +37,11 @@ __global__ void lloyd_empty_kernel(const int32_t* __restrict__ counts, int K, un
     }
 }
 
-// red stats slot <- [rows changed by the previous assign, 0]
+// red stats slot <- [rows changed by the previous assign, 0 (error sum), 0 (exchange overflow)]
 __global__ void lloyd_stats_kernel(const unsigned long long* __restrict__ changed, double* __restrict__ stats) {
     stats[0] = changed ? (double)*changed : 0.0;
     stats[1] = 0.0;
+    stats[2] = 0.0;
 }
 
 // fast sharded mode: red = [sums (K, d) | counts (K) | ...]: C[k, :d] = sums / counts where counts > 0
@@ -68,6 +69,7 @@ __global__ void lloyd_shard_flags_kernel(const int32_t* __restrict__ counts_i, c
         flags[0] = (double)tot;
         flags[1] = stats[0];
         flags[2] = stats[1];
+        flags[3] = stats[2];
         if (changed) *changed = 0ULL;
     }
 }
@@ -137,7 +139,7 @@ int da_lloyd_finish(int fast, const double* red, const int32_t* counts, int K, i
     lloyd_shard_flags_kernel<<<1, 256, 0, s>>>(fast ? nullptr : counts, fast ? red + (long long)K * d : nullptr, K,
                                                stats, flags_dev, changed);
     DA_CHECK_LAUNCH("lloyd_shard_flags_kernel");
-    if (flags_host) DA_CUDA(cudaMemcpyAsync(flags_host, flags_dev, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (flags_host) DA_CUDA(cudaMemcpyAsync(flags_host, flags_dev, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
     if (event) DA_CUDA(cudaEventRecord((cudaEvent_t)event, s));
     if (labels_out)
         return assign_against(X, n, ldx, d, K, C, ldc, xx, labels_prev, labels_out, d2_out, changed, s);

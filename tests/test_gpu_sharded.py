@@ -251,12 +251,18 @@ def _lloyd_worker(rank, world, port, layout, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("layout", [[1500, 1500], [5, 2990, 5], [1000, 0, 1200, 800], [2999, 1]])
-def test_exact_sharded_lloyd_equals_one_gpu(layout):
+@pytest.mark.parametrize("layout,rounds", [([1500, 1500], None), ([5, 2990, 5], None), ([1000, 0, 1200, 800], None),
+                                           ([2999, 1], None), ([5, 2990, 5], "1"), ([1000, 0, 1200, 800], "1")])
+def test_exact_sharded_lloyd_equals_one_gpu(layout, rounds, monkeypatch):
     """The exact sharded Lloyd update (da_gs_shard_*: leaf states handed across
     shard boundaries, W-1 neighbour rounds, one leaf-sum allreduce) gives the
     one-GPU centroids and labels bit for bit on every shard layout, including
-    tiny and empty shards (a leaf crossing several shards) and reseeds (K=200)."""
+    tiny and empty shards (a leaf crossing several shards) and reseeds (K=200).
+    rounds="1": one neighbour round per update, so leaves crossing two or more
+    boundaries trip the overflow flag and the update is redone with world-1
+    rounds -- same bits."""
+    if rounds is not None:
+        monkeypatch.setenv("DA_SHARD_ROUNDS", rounds)
     import sys
 
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
