@@ -348,20 +348,35 @@ __global__ void __launch_bounds__(TC_TP, 1) assign_tc_kernel(
                 bulk_g2s(Bbuf, Bg, (uint32_t)(2 * B_ELEMS * sizeof(float)), &b_bar);
                 mbar_wait(&b_bar, 0);
             }
+            // chunks are issued one ahead of the MMAs (the next chunk's copy overlaps
+            // this chunk's wait and MMAs; before, every chunk waited for its own
+            // freshly issued copy)
+            const uint32_t abytes = (uint32_t)(2 * A_ELEMS * sizeof(float));
+            const uint32_t bbytes = b_resident ? 0u : (uint32_t)(2 * B_ELEMS * sizeof(float));
+            long long iss_tile = blockIdx.x, iss_q = 0;
+            int iss_ch = 0;
+            auto issue_next = [&]() {
+                if (iss_tile >= ntiles) return;
+                const int st = (int)(iss_q & 1);
+                if (iss_q >= 2) mbar_wait(&empty_bar[st], (uint32_t)(((iss_q >> 1) - 1) & 1));
+                float* Ah = Abuf + st * 2 * A_ELEMS;
+                float* Bs = b_resident ? Bbuf : Bbuf + st * 2 * B_ELEMS;
+                mbar_arrive_expect_tx(&full_bar[st], abytes + bbytes);
+                bulk_g2s(Ah, Ag + ((size_t)iss_tile * nch + iss_ch) * 2 * A_ELEMS, abytes, &full_bar[st]);
+                if (!b_resident) bulk_g2s(Bs, Bg + (size_t)iss_ch * 2 * B_ELEMS, bbytes, &full_bar[st]);
+                ++iss_q;
+                if (++iss_ch == nch) { iss_ch = 0; iss_tile += gridDim.x; }
+            };
+            issue_next();
             long long q = 0, it = 0;
             for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
                 const int accb = (int)(it & 1);
                 if (it >= 2) mbar_wait(&acc_empty[accb], (uint32_t)(((it - 2) >> 1) & 1));
                 for (int ch = 0; ch < nch; ++ch, ++q) {
                     const int st = (int)(q & 1);
-                    if (q >= 2) mbar_wait(&empty_bar[st], (uint32_t)(((q >> 1) - 1) & 1));
+                    issue_next();                       // chunk q+1 (waits for its slot's MMAs of q-1)
                     float* Ah = Abuf + st * 2 * A_ELEMS;
                     float* Bs = b_resident ? Bbuf : Bbuf + st * 2 * B_ELEMS;
-                    const uint32_t abytes = (uint32_t)(2 * A_ELEMS * sizeof(float));
-                    const uint32_t bbytes = b_resident ? 0u : (uint32_t)(2 * B_ELEMS * sizeof(float));
-                    mbar_arrive_expect_tx(&full_bar[st], abytes + bbytes);
-                    bulk_g2s(Ah, Ag + ((size_t)tile * nch + ch) * 2 * A_ELEMS, abytes, &full_bar[st]);
-                    if (!b_resident) bulk_g2s(Bs, Bg + (size_t)ch * 2 * B_ELEMS, bbytes, &full_bar[st]);
                     mbar_wait(&full_bar[st], (uint32_t)((q >> 1) & 1));
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     const uint32_t sa_hi = smem_u32(Ah), sa_lo = smem_u32(Ah + A_ELEMS);
