@@ -604,6 +604,28 @@ def main():
                 "leaf_kernel_bytes_moved_frac": b64 / (leaf_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
                 "note": "rows are float64 for bit parity: the leaf kernel moves N*(8*D+4) B"}
             del Xr
+            # scaling projection: the pass over one rank's share at 8 GPUs
+            # (1/8 of the rows) on this GPU.  Its device time bounds T(8) from below
+            # (collective latency excluded), so T(1M) / T(1M/8) bounds the 8-GPU
+            # strong-scaling factor from above.
+            n8 = NA // 8
+            X8 = XA[:n8].contiguous()
+            cw8 = cw.clone()
+            codes8, _ = E.encode(X8, cw8, sq, Pt, L, out_dtype=torch.int32, with_err=False)
+            P8, s8 = E.cross_full(cw8)
+            E.da_sweep(X8, cw8.clone(), codes8.clone(), P8.clone(), s8.clone(), cfg1)   # warm-up
+            torch.cuda.synchronize()
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            b0.record(stream)
+            E.da_sweep(X8, cw8, codes8, P8, s8, cfg1)
+            b1.record(stream)
+            torch.cuda.synchronize()
+            t8 = b0.elapsed_time(b1) / 1e3
+            anneal["projection_8gpu"] = {
+                "rows_per_gpu": n8, "seconds_one_share": t8, "speedup_bound": anneal_s / t8,
+                "note": "anneal pass over 1/8 of the rows on one GPU: a lower bound of T(8) (no collective "
+                        "latency), so anneal_pass.seconds / seconds_one_share bounds the 8-GPU strong scaling"}
+            del X8, codes8, P8, s8
         del XA
 
     # --- ADC candidate scan, config E shape: 10,000 queries (sharded over the
