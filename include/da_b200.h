@@ -143,6 +143,14 @@ int da_lloyd_step(const double* X, int64_t n, int64_t ldx, int d, int K, const d
                   const double* xx, int32_t* counts, unsigned long long* flags_dev, void* flags_host, void* event,
                   void* stream);
 
+/* CUDA graphs for da_lloyd_step (default on; DA_LLOYD_GRAPHS=0 disables): an
+ * argument set is run eagerly once, captured the second time and replayed
+ * after that; any library scratch reallocation drops the captured graphs, and
+ * the per-kernel profiler bypasses them.  on = 0 disables and frees them. */
+int da_lloyd_graphs(int on);
+/* out[4] = iterations run eagerly, graphs captured, graph replays, failed captures */
+int da_lloyd_graph_stats(long long* out);
+
 /* Sharded Lloyd iteration around the collective:
  *   da_lloyd_prepare: C_out = C_prev (and snap), stats[0:3] = [*changed_prev, 0, 0]
  *                     (the previous assign's stats ride this update's allreduce);

@@ -236,16 +236,54 @@ def lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, c
         return _lloyd(Xr, C_init, active, max_iters, comm, not want_trace)
 
 
+def _arena(name: str, shape, dtype, dev) -> torch.Tensor:
+    """A persistent device buffer per (name, shape, dtype, device)."""
+    key = (name, tuple(shape), dtype, dev)
+    t = _ARENA.get(key)
+    if t is None:
+        t = _ARENA[key] = torch.empty(tuple(shape), dtype=dtype, device=dev)
+    return t
+
+
+_ARENA: dict = {}
+_EVENTS: dict = {}
+
+
+def _lloyd_events():
+    dev = torch.cuda.current_device()
+    if dev not in _EVENTS:
+        evs = [torch.cuda.Event(), torch.cuda.Event()]
+        for e in evs:
+            e.record()                                # creates the handles da_lloyd_step records into
+        _EVENTS[dev] = evs
+    return _EVENTS[dev]
+
+
 def _lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, comm=None, lazy=False):
     if comm is not None and comm.world == 1 and not os.environ.get("DA_SHARD_LOOP"):
         comm = None   # one shard: nothing to exchange (DA_SHARD_LOOP=1 keeps the shard loop, for timing it)
     n, D = Xr.shape
     K = C_init.shape[0]
-    C = C_init.clone().contiguous()
     dev = Xr.device
+    if comm is None:
+        C = _arena("lloyd_C0", C_init.shape, F64, dev)
+        C.copy_(C_init)
+    else:
+        C = C_init.clone().contiguous()
     trace_d = torch.empty(max_iters + 1, dtype=F64, device=dev)
-    xx = row_sqnorms(Xr, active) if n else None  # fixed for the whole stage
+    xx = None
+    if n:
+        xx = _arena("lloyd_xx", (n,), F64, dev) if comm is None else torch.empty(n, dtype=F64, device=dev)
+        native.da_row_sqnorms(P(Xr), is_f32(Xr), n, Xr.stride(0), active, P(xx), stream())   # fixed for the stage
     labels, errs = assign(Xr, active, C, xx=xx, want_d2=not lazy)
+    if comm is None and n:
+        lab2 = _arena("lloyd_lab2", (n,), I32, dev)   # the ring slot iteration 0 reads (labels_prev)
+        lab2.copy_(labels)
+        labels = lab2
+        if not lazy:
+            d22 = _arena("lloyd_d22", (n,), F64, dev)
+            d22.copy_(errs)
+            errs = d22
     if not lazy:
         trace_d[0:1] = np_mean(errs, comm)
     iters = 0
@@ -262,20 +300,28 @@ def _lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, 
         # dropped when iteration i converged or emptied a cluster (the reseed
         # changes C_i, so i+1 is recomputed); accepted results are the
         # reference's, step for step.
-        slots = [(C, torch.empty(K, dtype=I32, device=dev), torch.zeros(2, dtype=torch.int64, device=dev)),
-                 (torch.empty_like(C), torch.empty(K, dtype=I32, device=dev),
-                  torch.zeros(2, dtype=torch.int64, device=dev))]
+        # Persistent buffers (same addresses every call of this shape): the
+        # library replays a CUDA graph of an iteration whose arguments it has
+        # seen before (da_lloyd_step), so slots, label and error rings and the
+        # events are reused across Lloyd calls and dictionary steps.
+        slots = [(C, _arena("lloyd_cnt0", (K,), I32, dev), _arena("lloyd_fl0", (2,), torch.int64, dev)),
+                 (_arena("lloyd_C1", C.shape, F64, dev), _arena("lloyd_cnt1", (K,), I32, dev),
+                  _arena("lloyd_fl1", (2,), torch.int64, dev))]
         flags_h = _pinned_flags()
-        done_ev = [torch.cuda.Event(), torch.cuda.Event()]
-        snaps = [torch.empty_like(C), torch.empty_like(C)] if lazy else None
-
-        for ev in done_ev:
-            ev.record()                              # creates the event handles da_lloyd_step records into
+        done_ev = _lloyd_events()
+        snaps = [_arena("lloyd_snap0", C.shape, F64, dev), _arena("lloyd_snap1", C.shape, F64, dev)] if lazy else None
+        lab_ring = [_arena(f"lloyd_lab{i}", (n,), I32, dev) for i in range(3)]
+        d2_ring = None if lazy else [_arena(f"lloyd_d2{i}", (n,), F64, dev) for i in range(3)]
+        nlaunch = [0]
 
         def launch(C_prev, labels_prev, slot):
             Cn, cn, fl = slots[slot]
-            nl = torch.empty(n, dtype=I32, device=dev)
-            ne = None if lazy else torch.empty(n, dtype=F64, device=dev)
+            j = nlaunch[0]
+            nlaunch[0] += 1
+            nl = lab_ring[j % 3]
+            if nl is labels_prev:                    # a reseed re-assign broke the rotation
+                nl = lab_ring[(j + 1) % 3]
+            ne = None if lazy else d2_ring[j % 3]
             # group means, #empty, assign, flags -> pinned host, event: one call
             native.da_lloyd_step(P(Xr), n, Xr.stride(0), active, K, P(C_prev), P(Cn), Cn.stride(0),
                                  P(snaps[slot]) if lazy else None, P(labels_prev), P(nl), P(ne), P(xx), P(cn), P(fl),
@@ -316,7 +362,7 @@ def _lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, 
         trace = [] if lazy else trace_d[: iters + 1].cpu().tolist()
         if LLOYD_LOG is not None:
             LLOYD_LOG.append((active, n, K, iters))
-        return C, labels, trace
+        return C.clone(), labels.clone(), trace   # the loop's buffers are reused by the next call
     return _lloyd_sharded(Xr, C, labels, errs, xx, trace_d, active, max_iters, comm, lazy)
 
 

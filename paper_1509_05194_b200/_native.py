@@ -38,6 +38,8 @@ _SIGNATURES = {
     "da_cov_chains": [_P, _I, _L, _L, _I, _P, _P, _I, _P, _P, _P],
     "da_fold": [_P, _I, _L, _I, _P, _P],
     "da_lloyd_step": [_P, _L, _L, _I, _I, _P, _P, _L, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "da_lloyd_graphs": [_I],
+    "da_lloyd_graph_stats": [_P],
     "da_lloyd_prepare": [_P, _P, _P, _L, _P, _P, _P],
     "da_lloyd_finish": [_I, _P, _P, _I, _I, _P, _L, _P, _P, _P, _P, _P, _L, _L, _P, _P, _P, _P, _P, _P],
     "da_gs_shard_sort": [_P, _L, _L, _I, _P, _I, _P, _P],

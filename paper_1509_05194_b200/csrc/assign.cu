@@ -194,6 +194,8 @@ int launch_row_sqnorms(const void* A, int a_is_f32, long long rows, long long ld
 static int g_assign_mode = 0;  // 0: tensor-core filter + exact recheck when K <= 256; 1: plain float64
 static unsigned long long* g_assign_stats = nullptr;
 
+long long assign_config_key() { return (long long)(uintptr_t)g_assign_stats * 31 + g_assign_mode; }
+
 int set_assign_config(int mode, unsigned long long* stats) {
     g_assign_mode = mode;
     g_assign_stats = stats;
@@ -504,8 +506,7 @@ int launch_assign(const void* X, int x_is_f32, long long n, long long ldx, int d
 #define AF_LAUNCH(T, DMv)                                                                                            \
     do {                                                                                                             \
         if (smem > 48 * 1024)                                                                                        \
-            DA_CUDA(cudaFuncSetAttribute(assign_ffma_kernel<T, DMv>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                                         (int)smem));                                                                \
+            { const int rc_ = ensure_smem((const void*)assign_ffma_kernel<T, DMv>, (int)smem); if (rc_) return rc_; } \
         assign_ffma_kernel<T, DMv><<<g, 256, smem, s>>>((const T*)X, n, ldx, d, C, ldc, K, cc, xx, labels, d2, prev, \
                                                         changed, g_assign_stats, hard, nhard);                       \
         DA_CHECK_LAUNCH("assign_ffma_kernel");                                                                       \

@@ -752,6 +752,15 @@ static struct {
     const float* img = nullptr;
 } g_img;
 
+long long assign_config_key();
+// identity of the bound row image and of the assign configuration (lloyd.cu's graph keys)
+int assign_image_key(const void** img, long long* mode) {
+    *img = g_img.img;
+    *mode = (long long)(uintptr_t)g_img.X * 1315423911LL + (long long)g_img.d * 2654435761LL + g_img.n +
+            assign_config_key();
+    return 0;
+}
+
 size_t assign_image_bytes(long long n, int d) {
     const long long ntiles = (n + TC_M - 1) / TC_M;
     const int nch = (d + TC_BK - 1) / TC_BK;
@@ -824,7 +833,7 @@ int launch_assign_tc(const void* X, int x_is_f32, long long n, long long ldx, in
     const unsigned rgrid = grid_for((n + 31) / 32, RC_WARPS, 1LL << 31);
     if (x_is_f32) {
         auto kf = assign_tc_kernel<float>;
-        DA_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        { const int rc_ = ensure_smem((const void*)kf, (int)smem); if (rc_) return rc_; }
         kf<<<grid, TC_TP, smem, s>>>((const float*)X, n, ldx, d, K, cc, xx, Ag, Bg, stats, ovf_rows, ovf_cnt, gcand,
                                      gcnt);
         DA_CHECK_LAUNCH("assign_tc_kernel");
@@ -835,7 +844,7 @@ int launch_assign_tc(const void* X, int x_is_f32, long long n, long long ldx, in
                                                           labels, d2, prev, changed);
     } else {
         auto kf = assign_tc_kernel<double>;
-        DA_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        { const int rc_ = ensure_smem((const void*)kf, (int)smem); if (rc_) return rc_; }
         kf<<<grid, TC_TP, smem, s>>>((const double*)X, n, ldx, d, K, cc, xx, Ag, Bg, stats, ovf_rows, ovf_cnt, gcand,
                                      gcnt);
         DA_CHECK_LAUNCH("assign_tc_kernel");

@@ -26,6 +26,27 @@ static int g_encode_mode = 0;
 static unsigned long long* g_encode_stats = nullptr;  // device counter of exact rechecks
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, size):
+// repeated calls inside a CUDA-graph capture (lloyd.cu) invalidate it.
+int ensure_smem(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, int> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    int& cur = done[{dev, func}];
+    if (bytes <= cur) return 0;
+    const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
+    cur = bytes;
+    return 0;
+}
+
+void count_launches(long long k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+long long launch_total() { return g_launches.load(std::memory_order_relaxed); }
+// bumped whenever a scratch buffer is freed: captured CUDA graphs that point
+// into scratch memory are dropped (lloyd.cu)
+std::atomic<long long> g_scratch_gen{0};
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 
@@ -58,6 +79,7 @@ void* scratch(int slot, size_t bytes, cudaStream_t stream) {
         cudaFree(s.ptr);
         s.ptr = nullptr;
         s.bytes = 0;
+        g_scratch_gen.fetch_add(1);
     }
     size_t want = bytes < 256 ? 256 : bytes;
     want = want + want / 8;  // headroom so slightly larger calls do not reallocate
@@ -113,6 +135,7 @@ int da_release_scratch(void) {
     for (auto& kv : g_scratch)
         if (kv.second.ptr) cudaFree(kv.second.ptr);
     g_scratch.clear();
+    g_scratch_gen.fetch_add(1);
     return 0;
 }
 

@@ -33,6 +33,10 @@ int fail_cuda(cudaError_t e, const char* where);
 // Every kernel launch is followed by DA_CHECK_LAUNCH, which also counts it
 // (da_launch_count() reports the total; bench.py uses it for gpu_launches).
 void count_launch();
+void count_launches(long long k);
+long long launch_total();
+bool prof_enabled();
+int ensure_smem(const void* func, int bytes);
 
 #define DA_CHECK_LAUNCH(where)                                   \
     do {                                                         \

@@ -785,7 +785,7 @@ int launch_group_sums(const double* X, long long n, long long ldx, int D, const 
         while (T < K) T <<= 1;
         const size_t psh = sizeof(int) * (size_t)T * (GS_DMAX + 1);
         if (psh > 48 * 1024)
-            DA_CUDA(cudaFuncSetAttribute(leaf_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psh));
+            { const int rc_ = ensure_smem((const void*)leaf_plan_kernel, (int)psh); if (rc_) return rc_; }
         leaf_plan_kernel<<<1, T, psh, s>>>(counts, seg, K, nleaf, total + 1, leaves);
         DA_CHECK_LAUNCH("leaf_plan_kernel");
     } else {

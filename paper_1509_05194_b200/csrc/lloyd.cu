@@ -15,6 +15,13 @@
 //                     then the assign against the new centroids.
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
 #include "../../include/da_b200.h"
 #include "common.cuh"
 #include "internal.h"
@@ -85,19 +92,77 @@ static int assign_against(const double* X, long long n, long long ldx, int d, in
     return launch_assign(X, 0, n, ldx, d, C, ldc, K, cc, xx, labels, d2, prev, changed, s);
 }
 
+// ---------------------------------------------------------------------------
+// CUDA graphs of one Lloyd iteration.  A 1/8 shard's iteration is ~20 launches
+// of a few microseconds each; issued one by one the host falls behind the
+// device (29 % idle at 125k rows).  Every distinct argument set of
+// da_lloyd_step runs eagerly the first time (scratch warm-up), is captured the
+// second time and replayed from then on.  Graphs point into library scratch,
+// so any scratch reallocation drops them all (g_scratch_gen).  Off while the
+// per-kernel profiler runs (its events would be captured).
+extern std::atomic<long long> g_scratch_gen;
+int assign_image_key(const void** img, long long* mode);
+
+namespace {
+struct GKey {
+    uintptr_t v[20];
+    bool operator==(const GKey& o) const { return std::memcmp(v, o.v, sizeof(v)) == 0; }
+};
+struct GKeyHash {
+    size_t operator()(const GKey& k) const {
+        size_t h = 1469598103934665603ull;
+        for (uintptr_t x : k.v) { h ^= (size_t)x; h *= 1099511628211ull; }
+        return h;
+    }
+};
+struct GEntry {
+    cudaGraphExec_t exec = nullptr;
+    int seen = 0;
+    long long kernels = 0;
+    long long gen = -1;
+};
+std::unordered_map<GKey, GEntry, GKeyHash> g_graphs;
+long long g_gstat[4] = {0, 0, 0, 0};   // eager, captured, replayed, capture failures
+std::mutex g_graph_mu;
+int g_graph_mode = -1;   // -1: from DA_LLOYD_GRAPHS (default on)
+
+bool graphs_on() {
+    if (g_graph_mode < 0) {
+        const char* e = getenv("DA_LLOYD_GRAPHS");
+        g_graph_mode = e ? (atoi(e) != 0) : 1;
+    }
+    return g_graph_mode == 1 && !prof_enabled();
+}
+
+void drop_graphs_locked() {
+    for (auto& kv : g_graphs)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    g_graphs.clear();
+}
+}  // namespace
+
 }  // namespace da
 
 using namespace da;
 
 extern "C" {
 
-int da_lloyd_step(const double* X, int64_t n, int64_t ldx, int d, int K, const double* C_prev, double* C_out,
-                  int64_t ldc, double* snap, const int32_t* labels_prev, int32_t* labels_out, double* d2_out,
-                  const double* xx, int32_t* counts, unsigned long long* flags_dev, void* flags_host, void* event,
-                  void* stream) {
-    if (n < 1 || K < 1 || d < 1 || ldx < d || ldc < d || !counts || !flags_dev)
-        return fail_arg("lloyd_step: bad arguments n=%lld K=%d d=%d", (long long)n, K, d);
-    cudaStream_t s = (cudaStream_t)stream;
+int da_lloyd_graph_stats(long long* out) {
+    for (int i = 0; i < 4; ++i) out[i] = g_gstat[i];
+    return 0;
+}
+
+int da_lloyd_graphs(int on) {
+    std::lock_guard<std::mutex> g(g_graph_mu);
+    g_graph_mode = on ? 1 : 0;
+    if (!on) drop_graphs_locked();
+    return 0;
+}
+
+static int lloyd_step_body(const double* X, int64_t n, int64_t ldx, int d, int K, const double* C_prev, double* C_out,
+                           int64_t ldc, double* snap, const int32_t* labels_prev, int32_t* labels_out, double* d2_out,
+                           const double* xx, int32_t* counts, unsigned long long* flags_dev, void* flags_host,
+                           cudaStream_t s) {
     const size_t cbytes = sizeof(double) * (size_t)K * (size_t)ldc;
     if (snap) DA_CUDA(cudaMemcpyAsync(snap, C_prev, cbytes, cudaMemcpyDeviceToDevice, s));
     if (C_out != C_prev) DA_CUDA(cudaMemcpyAsync(C_out, C_prev, cbytes, cudaMemcpyDeviceToDevice, s));
@@ -109,6 +174,98 @@ int da_lloyd_step(const double* X, int64_t n, int64_t ldx, int d, int K, const d
     if (rc) return rc;
     if (flags_host)
         DA_CUDA(cudaMemcpyAsync(flags_host, flags_dev, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    return 0;
+}
+
+int da_lloyd_step(const double* X, int64_t n, int64_t ldx, int d, int K, const double* C_prev, double* C_out,
+                  int64_t ldc, double* snap, const int32_t* labels_prev, int32_t* labels_out, double* d2_out,
+                  const double* xx, int32_t* counts, unsigned long long* flags_dev, void* flags_host, void* event,
+                  void* stream) {
+    if (n < 1 || K < 1 || d < 1 || ldx < d || ldc < d || !counts || !flags_dev)
+        return fail_arg("lloyd_step: bad arguments n=%lld K=%d d=%d", (long long)n, K, d);
+    cudaStream_t s = (cudaStream_t)stream;
+    auto body = [&]() {
+        return lloyd_step_body(X, n, ldx, d, K, C_prev, C_out, ldc, snap, labels_prev, labels_out, d2_out, xx, counts,
+                               flags_dev, flags_host, s);
+    };
+    // captures are recorded on a private stream (the caller's may be the legacy
+    // default stream, which cannot capture); the graph is then launched on `s`
+    auto body_cap = [&](cudaStream_t cs) {
+        return lloyd_step_body(X, n, ldx, d, K, C_prev, C_out, ldc, snap, labels_prev, labels_out, d2_out, xx, counts,
+                               flags_dev, flags_host, cs);
+    };
+    int rc = 0;
+    if (graphs_on()) {
+        const void* img = nullptr;
+        long long amode = 0;
+        assign_image_key(&img, &amode);
+        GKey key{{(uintptr_t)X, (uintptr_t)n, (uintptr_t)ldx, (uintptr_t)d, (uintptr_t)K, (uintptr_t)C_prev,
+                  (uintptr_t)C_out, (uintptr_t)ldc, (uintptr_t)snap, (uintptr_t)labels_prev, (uintptr_t)labels_out,
+                  (uintptr_t)d2_out, (uintptr_t)xx, (uintptr_t)counts, (uintptr_t)flags_dev, (uintptr_t)flags_host,
+                  (uintptr_t)s, (uintptr_t)img, (uintptr_t)amode, 0}};
+        std::unique_lock<std::mutex> g(g_graph_mu);
+        const long long gen = g_scratch_gen.load();
+        GEntry& e = g_graphs[key];
+        if (e.gen != gen) {               // scratch moved since this graph was captured
+            if (e.exec) cudaGraphExecDestroy(e.exec);
+            e = GEntry{};
+            e.gen = gen;
+        }
+        if (e.exec) {
+            ++g_gstat[2];
+            DA_CUDA(cudaGraphLaunch(e.exec, s));
+            count_launches(e.kernels);
+        } else if (e.seen >= 1) {
+            if (g_graphs.size() > 4096) drop_graphs_locked();
+            GEntry& f = g_graphs[key];
+            f.gen = gen;
+            const long long k0 = launch_total();
+            cudaGraph_t graph = nullptr;
+            static thread_local cudaStream_t cap = nullptr;
+            if (!cap) cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking);
+            cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+            const cudaError_t be = cap ? cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal)
+                                       : cudaErrorStreamCaptureUnsupported;
+            int brc = 0;
+            cudaError_t ce = be;
+            if (be == cudaSuccess) {
+                brc = body_cap(cap);
+                ce = cudaStreamEndCapture(cap, &graph);
+            }
+            if (cap && cudaStreamIsCapturing(cap, &cst) == cudaSuccess && cst != cudaStreamCaptureStatusNone) {
+                cudaGraph_t g2 = nullptr;           // never leave the capture stream capturing
+                cudaStreamEndCapture(cap, &g2);
+                if (g2) cudaGraphDestroy(g2);
+                ce = cudaErrorStreamCaptureInvalidated;
+            }
+            if (brc == 0 && ce == cudaSuccess && graph && g_scratch_gen.load() == gen &&
+                cudaGraphInstantiate(&f.exec, graph, 0) == cudaSuccess) {
+                f.kernels = launch_total() - k0;
+                ++g_gstat[1];
+                cudaGraphDestroy(graph);
+                DA_CUDA(cudaGraphLaunch(f.exec, s));
+            } else {
+                // capture failed (or scratch moved inside it): run eagerly, never capture this key again
+                if (graph) cudaGraphDestroy(graph);
+                cudaGetLastError();
+                if (getenv("DA_DEBUG"))
+                    fprintf(stderr, "[da] lloyd graph capture failed (begin %d, body %d, end %d, d %d, n %lld, last %s): eager\n",
+                            (int)be, brc, (int)ce, d, (long long)n, da_last_error());
+                f.exec = nullptr;
+                f.seen = -1000000;
+                ++g_gstat[3];
+                rc = body();
+            }
+        } else {
+            ++e.seen;
+            ++g_gstat[0];
+            g.unlock();
+            rc = body();
+        }
+    } else {
+        rc = body();
+    }
+    if (rc) return rc;
     if (event) DA_CUDA(cudaEventRecord((cudaEvent_t)event, s));
     return 0;
 }

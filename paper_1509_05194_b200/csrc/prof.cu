@@ -18,6 +18,7 @@ struct ProfRec {
 };
 
 static bool g_prof_on = false;
+bool prof_enabled() { return g_prof_on; }
 static std::mutex g_prof_mu;
 static std::vector<ProfRec> g_recs;
 static std::vector<cudaEvent_t> g_free_events;
