@@ -222,3 +222,22 @@ def test_cov_segments_cover_the_blocks():
     for n in (1, 383, 384, 385, 767, 768, 769, 5000):
         st = D.blas_block_starts(n)
         assert st[-1] == n and all(0 < b - a <= 384 for a, b in zip(st[:-1], st[1:]))
+
+
+def _shift_fn(rank, world):
+    comm = D.Comm()
+    send = torch.full((5,), float(rank + 1), dtype=torch.float64)
+    recv = torch.full((5,), -1.0, dtype=torch.float64)
+    comm.shift_(send, recv)
+    return recv.numpy()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shift_passes_right(world):
+    """Comm.shift_: every rank sends to rank+1 and receives from rank-1 in one
+    batched exchange (the exact shard reductions' neighbour rounds); rank 0's
+    receive buffer is untouched."""
+    out = run(_shift_fn, world=world)
+    np.testing.assert_array_equal(out[0], np.full(5, -1.0))
+    for r in range(1, world):
+        np.testing.assert_array_equal(out[r], np.full(5, float(r)))
