@@ -433,11 +433,13 @@ __global__ void __launch_bounds__(256) assign_ffma_hard_kernel(const TX* __restr
     const int lane = threadIdx.x & 31;
     const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int nw = gridDim.x * (blockDim.x >> 5);
+    const int nh = *nhard;
+    if (w >= nh) return;                 // usually no or few undecided rows: most warps leave at once
     double cmax = 0.0, ccmax = 0.0;
     for (int k = lane; k < K; k += 32) { ccmax = fmax(ccmax, cc[k]); }
     for (int o = 16; o > 0; o >>= 1) ccmax = fmax(ccmax, __shfl_xor_sync(0xffffffffu, ccmax, o));
     cmax = sqrt(ccmax) * (1.0 + 1e-12);
-    for (int h = w; h < *nhard; h += nw) {
+    for (int h = w; h < nh; h += nw) {
         const long long r = hard[h];
         const TX* xr = X + r * ldx;
         const double xx = xx_in ? xx_in[r]
