@@ -143,6 +143,24 @@ int da_lloyd_step(const double* X, int64_t n, int64_t ldx, int d, int K, const d
                   const double* xx, int32_t* counts, unsigned long long* flags_dev, void* flags_host, void* event,
                   void* stream);
 
+/* Context: the devices, one library-owned non-blocking stream per
+ * device, and optionally an NCCL communicator for a row shard (NCCL is bound at
+ * run time from libnccl.so.2).  A stream argument of NULL in the da_ctx_*
+ * collectives means the context's stream of its first device.
+ *   da_nccl_unique_id: 128 bytes for ncclCommInitRank, made on one rank and
+ *                      shared with the others by the caller;
+ *   da_ctx_allreduce_f64 (in place, sum), da_ctx_allgather_i32, da_ctx_shift_f64
+ *                      (send to rank+1, receive from rank-1): the exchange steps
+ *                      of the sharded Lloyd update (da_gs_shard_*, da_lloyd_*). */
+int da_ctx_create(int n_devices, const int* device_ids, void** ctx);
+int da_ctx_stream(void* ctx, int i, void** stream);
+int da_nccl_unique_id(void* out128);
+int da_ctx_nccl_init(void* ctx, int rank, int world, const void* id128);
+int da_ctx_allreduce_f64(void* ctx, double* buf, int64_t count, void* stream);
+int da_ctx_allgather_i32(void* ctx, const int32_t* send, int32_t* recv, int64_t count, void* stream);
+int da_ctx_shift_f64(void* ctx, const double* send, double* recv, int64_t count, void* stream);
+int da_ctx_destroy(void* ctx);
+
 /* CUDA graphs for da_lloyd_step (default on; DA_LLOYD_GRAPHS=0 disables): an
  * argument set is run eagerly once, captured the second time and replayed
  * after that; any library scratch reallocation drops the captured graphs, and

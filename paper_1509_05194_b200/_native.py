@@ -39,6 +39,14 @@ _SIGNATURES = {
     "da_fold": [_P, _I, _L, _I, _P, _P],
     "da_lloyd_step": [_P, _L, _L, _I, _I, _P, _P, _L, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "da_lloyd_graphs": [_I],
+    "da_ctx_create": [_I, _P, _P],
+    "da_ctx_stream": [_P, _I, _P],
+    "da_nccl_unique_id": [_P],
+    "da_ctx_nccl_init": [_P, _I, _I, _P],
+    "da_ctx_allreduce_f64": [_P, _P, _L, _P],
+    "da_ctx_allgather_i32": [_P, _P, _P, _L, _P],
+    "da_ctx_shift_f64": [_P, _P, _P, _L, _P],
+    "da_ctx_destroy": [_P],
     "da_lloyd_graph_stats": [_P],
     "da_lloyd_prepare": [_P, _P, _P, _L, _P, _P, _P],
     "da_lloyd_finish": [_I, _P, _P, _I, _I, _P, _L, _P, _P, _P, _P, _P, _L, _L, _P, _P, _P, _P, _P, _P],

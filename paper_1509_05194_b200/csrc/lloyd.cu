@@ -141,6 +141,12 @@ void drop_graphs_locked() {
 }
 }  // namespace
 
+int drop_lloyd_graphs() {
+    std::lock_guard<std::mutex> g(g_graph_mu);
+    drop_graphs_locked();
+    return 0;
+}
+
 }  // namespace da
 
 using namespace da;
