@@ -72,7 +72,7 @@ static __device__ __noinline__ double exact_dot_general(const double* __restrict
         // per batch, fp32 in memory (exact in float64) so a batch is 4 vector loads
 #ifdef DA_DOT64
         // float64 rows read as pairs (no F2F conversions; 2x the bytes)
-        if (c32) {
+        if (c32 && (d & 1) == 0) {
             for (; d + 16 <= e; d += 16) {
                 double2 cv[8];
 #pragma unroll
@@ -86,7 +86,7 @@ static __device__ __noinline__ double exact_dot_general(const double* __restrict
             }
         }
 #else
-        if (c32) {
+        if (c32 && (d & 3) == 0) {   // a BLAS block may start off a 16-byte boundary (D = 500: blocks of 250)
             for (; d + 32 <= e; d += 32) {
                 float4 cv[8];
 #pragma unroll

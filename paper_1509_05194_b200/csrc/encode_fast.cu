@@ -764,7 +764,12 @@ int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int
         if (!x_f32) return fail_arg("encode_fast: float32 input only");
         if (getenv("DA_TABLE_FFMA") == nullptr) {
             ProfScope ps("encode_table_tc", s);
-            const int rc = launch_table_tc((const float*)X + c0 * ldx, cn, ldx, D, cw, sq, M, K, tab, N, s);
+            // D too wide for the resident tile image: the D-tiled tcgen05 table
+            // (looser bound than the chunked FFMA table) pays when the band is then
+            // narrowed by the greedy kernel's warp-wide fp32 dots, i.e. at L = 1
+            const char* est = getenv("DA_TABLE_STREAM");
+            const int stream_ok = est ? atoi(est) != 0 : L == 1;
+            const int rc = launch_table_tc((const float*)X + c0 * ldx, cn, ldx, D, cw, sq, M, K, tab, N, s, stream_ok);
             if (rc == 0) tab_tc = 1;
             else if (rc != kNotApplicable) return rc;
         }

@@ -111,6 +111,101 @@ __device__ __noinline__ int greedy_exact(GreedySmem S, const float* __restrict__
     return bk;
 }
 
+// Band narrowing (warp-collective, rare): the tensor-core table's bound grows
+// with D (6 accumulation steps per 16 columns), so at D = 960 the band often
+// holds a few candidates.  Their table entries are recomputed here as warp-wide
+// fp32 dots -- lane l runs one FMA chain over the columns 4l..4l+3 of every
+// 128-column block, then a 5-level shuffle tree: 4*ceil(D/128) + 5 roundings,
+// the bound of table_err(-steps) -- and the band is rebuilt around the smallest
+// recomputed value.  The winner of the wide band is in the narrow one (its
+// recomputed value is within the new bound of its exact one); a single survivor
+// is therefore the reference's choice, otherwise greedy_exact decides among the
+// survivors.  Returns this lane's surviving candidates (bit q as in `hits`).
+__device__ __noinline__ unsigned greedy_narrow(GreedySmem S, const float* __restrict__ xr, int D,
+                                               const float* __restrict__ cw32, const double* __restrict__ sq,
+                                               const double* __restrict__ cmax, const double* __restrict__ cbm, int K,
+                                               int m, unsigned hits, float a0, float a1, float a2_, float a3, float a4,
+                                               float a5, float a6, float a7, double xnorm, double e2) {
+    const float acc[8] = {a0, a1, a2_, a3, a4, a5, a6, a7};   // by value: the caller's sums stay in registers
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const float inf = __int_as_float(0x7f800000);
+    const bool v4 = (D & 3) == 0 && ((reinterpret_cast<uintptr_t>(cw32) & 15) == 0) &&
+                    ((reinterpret_cast<uintptr_t>(xr) & 15) == 0);
+    float v2[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v2[q] = inf;
+#pragma unroll 1
+    for (int q = 0; q < 8; ++q) {
+        const bool hit = (hits >> q) & 1u;
+        const unsigned hb = __ballot_sync(FULL, hit);
+        if (!hb) continue;
+        const int pos = __popc(hb & ((1u << lane) - 1u));
+        const int nc = __popc(hb);
+        __syncwarp();
+        if (hit) S.cand[pos] = (q >> 2) * 128 + 4 * lane + (q & 3);
+        __syncwarp();
+#pragma unroll 1
+        for (int c0 = 0; c0 < nc; c0 += 4) {
+            const float* cr[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                cr[i] = cw32 + ((long long)m * K + S.cand[min(c0 + i, nc - 1)]) * D;
+            float dot[4] = {0.f, 0.f, 0.f, 0.f};
+            if (v4) {
+#pragma unroll 1
+                for (int d = 4 * lane; d < D; d += 128) {
+                    const float4 x = __ldg(reinterpret_cast<const float4*>(xr + d));
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const float4 c = __ldg(reinterpret_cast<const float4*>(cr[i] + d));
+                        dot[i] = fmaf(x.x, c.x, dot[i]);
+                        dot[i] = fmaf(x.y, c.y, dot[i]);
+                        dot[i] = fmaf(x.z, c.z, dot[i]);
+                        dot[i] = fmaf(x.w, c.w, dot[i]);
+                    }
+                }
+            } else {
+#pragma unroll 1
+                for (int d0 = 4 * lane; d0 < D; d0 += 128) {
+                    for (int d = d0; d < min(d0 + 4, D); ++d) {
+                        const float x = xr[d];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) dot[i] = fmaf(x, cr[i][d], dot[i]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) dot[i] += __shfl_xor_sync(FULL, dot[i], off);
+            }
+            if (hit && pos >= c0 && pos < c0 + 4) {
+                const int i = pos - c0;
+                const float dsel = i == 0 ? dot[0] : (i == 1 ? dot[1] : (i == 2 ? dot[2] : dot[3]));
+                const int k = (q >> 2) * 128 + 4 * lane + (q & 3);
+                const float t2 = fmaf(-2.f, dsel, (float)sq[m * K + k]);
+                const float aq = acc[q];
+                v2[q] = fmaf(2.f, aq, t2);
+            }
+        }
+    }
+    const double u = 5.9604644775390625e-08;  // 2^-24
+    const double cb = cbm[m], cm = cmax[m];
+    const int steps = 4 * ((D + 127) / 128) + 5;
+    const double a2 = 2.0 * (table_err(-steps, D, u, xnorm, cm) + 2.0 * ((m + 2.0) * u * cb) +
+                             4.0 * u * (cm * cm + 2.0 * xnorm * cm + 2.0 * cb));
+    const double E = a2 + e2 + 1e-300;
+    float lm = fminf(fminf(fminf(v2[0], v2[1]), fminf(v2[2], v2[3])), fminf(fminf(v2[4], v2[5]), fminf(v2[6], v2[7])));
+    const float vmin = funkey(__reduce_min_sync(FULL, fkey(lm)));
+    const double lim = (double)vmin + 2.0 * E;
+    const float limf = (lim >= 3.0e38) ? inf : __fadd_ru((float)lim, fabsf((float)lim) * 1e-6f);
+    unsigned keep = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) keep |= (unsigned)(((hits >> q) & 1u) && v2[q] <= limf) << q;
+    return keep;
+}
+
 // One warp per vector, K == 256 (lane owns k = 4 lane + {0..3} and 128 + 4 lane + {0..3}).
 #ifndef DA_GR_MINB
 #define DA_GR_MINB 7   // 40 registers: 56 warps per SM hide the gathers (L=1 per 1M: 11.8 -> 9.1 ms)
@@ -120,7 +215,7 @@ __global__ void __launch_bounds__(32 * GR_WARPS, DA_GR_MINB) greedy_kernel(
     const float* __restrict__ tab32, const double* __restrict__ sq, const double* __restrict__ P,
     const float* __restrict__ P32, const double* __restrict__ cmax, const double* __restrict__ cbm,
     const double* __restrict__ cw64, void* codes_out, int code_bytes, long long ldcodes, double* __restrict__ err_out,
-    unsigned long long* __restrict__ stats, int tab_tc) {
+    unsigned long long* __restrict__ stats, int tab_tc, int narrow) {
     extern __shared__ __align__(16) char smem_raw[];
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -195,10 +290,17 @@ __global__ void __launch_bounds__(32 * GR_WARPS, DA_GR_MINB) greedy_kernel(
         unsigned hits = 0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) hits |= (unsigned)(vv[q] <= limf) << q;
-        const int cnt = __popc(hits);
-        const int first_q = __ffs(hits) - 1;
-        const int total = __reduce_add_sync(FULL, cnt);
+        int cnt = __popc(hits);
+        int first_q = __ffs(hits) - 1;
+        int total = __reduce_add_sync(FULL, cnt);
         int code;
+        if (total > 1 && narrow) {   // tensor-core table at wide D: tighten the band first
+            hits = greedy_narrow(S, xr, D, cw, sq, cmax, cbm, K, m, hits, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5],
+                                 acc[6], acc[7], xnorm, e2);
+            cnt = __popc(hits);
+            first_q = __ffs(hits) - 1;
+            total = __reduce_add_sync(FULL, cnt);
+        }
         if (total == 1) {
             const unsigned own = __ballot_sync(FULL, cnt != 0);
             const int src = __ffs(own) - 1;
@@ -251,8 +353,11 @@ int launch_greedy(const float* X, long long n, long long ldx, int D, const float
     if (smem > 48 * 1024)
         DA_CUDA(cudaFuncSetAttribute(greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const unsigned grid = (unsigned)((n + GR_WARPS - 1) / GR_WARPS);
+    // band narrowing pays where the tensor-core bound is loose (wide D); DA_GREEDY_NARROW=0/1 forces it
+    int narrow = tab_tc == 1 && D >= 256;
+    if (const char* e = getenv("DA_GREEDY_NARROW")) narrow = atoi(e) != 0;
     greedy_kernel<<<grid, 32 * GR_WARPS, smem, s>>>(X, n, ldx, D, cw, M, K, tab, sq, P, P32, cmax, cbm, cw64,
-                                                    codes_out, code_bytes, ldcodes, err_out, stats, tab_tc);
+                                                    codes_out, code_bytes, ldcodes, err_out, stats, tab_tc, narrow);
     DA_CHECK_LAUNCH("greedy_kernel");
     return 0;
 }

@@ -137,7 +137,7 @@ __device__ __forceinline__ double bt_exact_dot(const float* __restrict__ x, cons
     while (d < D) {
         const int e = d + (int)blas_block_len(D - d);
         double acc = 0.0;
-        if (v4) {
+        if (v4 && (d & 3) == 0) {   // a BLAS block may start off a 16-byte boundary
             for (; d + 8 <= e; d += 8) {
                 const float4 x0 = __ldg(reinterpret_cast<const float4*>(x + d));
                 const float4 x1 = __ldg(reinterpret_cast<const float4*>(x + d + 4));
@@ -1377,14 +1377,252 @@ __global__ void __launch_bounds__(TX_T, 1) table_tc_x_kernel(const float* __rest
     }
 }
 
-// Returns kNotApplicable when the shape does not fit (K > 256 or the row tile's
-// operand image exceeds shared memory); the caller then uses the FFMA table.
+// ---------------------------------------------------------------------------
+// D-tiled score table (D too wide for a resident row-tile image: config C,
+// D = 960).  A pre-pass writes the [x, 1, 0..] rows of every 128-row tile as
+// tf32 hi/lo images in the canonical K-major layout, one 16-KB block per
+// (tile, 16-wide k chunk); the table kernel then streams (A chunk, B chunk)
+// pairs through a shared-memory ring by bulk copy -- nothing is staged by
+// threads -- and accumulates the 3xTF32 product over all chunks in TMEM.
+// Warp roles: warp 8 loads, warp 9 issues the MMAs (so a slot refill never
+// delays the next chunk's MMAs), warps 0-7 drain accumulators into the table.
+// A work item is (row tile, group of dictionaries); the `msplit` items of a
+// tile run on neighbouring CTAs at the same time, so the tile's image is read
+// from HBM about once and from L2 after that (148 whole-tile images would not
+// fit L2 at D = 960).
+__global__ void a_tf32_img_kernel(const float* __restrict__ X, long long n, long long ldx, int D, int nch,
+                                  long long ntiles, float* __restrict__ out) {
+    constexpr int A_EL = BT_ROWS * BT_BK;
+    const bool v4 = (D & 3) == 0 && (ldx & 3) == 0 && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+    const long long total = ntiles * nch * (long long)(BT_ROWS * (BT_BK / 4));
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        // (tile, chunk, 8-row group, 4-wide k group, row in group): a warp writes 512
+        // contiguous bytes of each image and reads 64-byte row segments
+        const int r7 = (int)(e & 7), c4 = (int)((e >> 3) & (BT_BK / 4 - 1));
+        const long long rest = e / (8 * (BT_BK / 4));
+        const int r8 = (int)(rest % (BT_ROWS / 8));
+        const long long tc = rest / (BT_ROWS / 8);
+        const int ch = (int)(tc % nch);
+        const long long tile = tc / nch;
+        const int rr = r8 * 8 + r7;
+        const long long gr = tile * BT_ROWS + rr;
+        const int k = ch * BT_BK + 4 * c4;
+        float x4[4];
+        if (v4 && k + 3 < D) {
+            const float4 t = gr < n ? __ldg(reinterpret_cast<const float4*>(X + gr * ldx + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            x4[0] = t.x; x4[1] = t.y; x4[2] = t.z; x4[3] = t.w;
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int kk = k + u;
+                x4[u] = kk < D ? (gr < n ? X[gr * ldx + kk] : 0.f) : (kk == D ? 1.f : 0.f);
+            }
+        }
+        bt_store_split(out + (size_t)tc * 2 * A_EL, bt_off(rr, 4 * c4) >> 2, x4);
+    }
+}
+
+constexpr int TS_EPI = 256;            // epilogue threads (warps 0-7)
+constexpr int TS_T = TS_EPI + 64;      // + loader warp + MMA warp
+constexpr int TS_NS = 4;               // ring slots of one (A chunk, B chunk) pair: 48 KB each
+__global__ void __launch_bounds__(TS_T, 1) table_tc_stream_kernel(const float* __restrict__ Ag, long long n, int M, int K,
+                                                                 int nch, const float* __restrict__ Bg,
+                                                                 float* __restrict__ T, long long ldt, int msplit) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    constexpr int A_EL = BT_ROWS * BT_BK, B_EL = BT_N * BT_BK;
+    constexpr int SLOT = 2 * A_EL + 2 * B_EL;                  // floats per ring slot: A hi, A lo, B hi, B lo
+    float* ring = reinterpret_cast<float*>(smem);
+    float* Xpose = ring + (size_t)TS_NS * SLOT;                 // [8 warps][32 x 32] store transpose
+    __shared__ uint64_t full_bar[TS_NS], empty_bar[TS_NS], acc_full[2], acc_empty[2];
+    __shared__ uint32_t tmem_sh;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(bt_smem_u32(&tmem_sh)),
+                     "r"(2 * BT_N));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < TS_NS; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&full_bar[i])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&empty_bar[i])));
+        }
+        for (int i = 0; i < 2; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&acc_full[i])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bt_smem_u32(&acc_empty[i])), "r"(TS_EPI));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_sh;
+    const long long ntiles = (n + BT_ROWS - 1) / BT_ROWS;
+    const long long nitems = ntiles * msplit;
+    const int mper = (M + msplit - 1) / msplit;               // dictionaries per item
+    long long my_items = 0;
+    for (long long t = blockIdx.x; t < nitems; t += gridDim.x) ++my_items;
+
+    if (warp == TS_EPI / 32) {
+        // ---------------- loader: (A chunk, B chunk) pairs into the ring
+        if ((tid & 31) == 0) {
+            constexpr uint32_t bytes_a = 2 * A_EL * sizeof(float), bytes_b = 2 * B_EL * sizeof(float);
+            long long q = 0;
+            for (long long it = 0; it < my_items; ++it) {
+                const long long item = blockIdx.x + it * gridDim.x;
+                const long long tile = item / msplit;
+                const int m0 = (int)(item % msplit) * mper, m1 = min(M, m0 + mper);
+                for (int m = m0; m < m1; ++m) {
+                    for (int ch = 0; ch < nch; ++ch, ++q) {
+                        const int st = (int)(q % TS_NS);
+                        if (q >= TS_NS) bt_wait(&empty_bar[st], (uint32_t)(((q / TS_NS) - 1) & 1));
+                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                                         bt_smem_u32(&full_bar[st])),
+                                     "r"(bytes_a + bytes_b)
+                                     : "memory");
+                        float* slot = ring + (size_t)st * SLOT;
+                        bt_bulk(slot, Ag + ((size_t)tile * nch + ch) * 2 * A_EL, bytes_a, &full_bar[st]);
+                        bt_bulk(slot + 2 * A_EL, Bg + ((size_t)m * nch + ch) * 2 * B_EL, bytes_b, &full_bar[st]);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == TS_EPI / 32 + 1) {
+        // ---------------- MMA issuer
+        if ((tid & 31) == 0) {
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BT_N >> 3) << 17) |
+                                   ((uint32_t)(128 >> 4) << 24);
+            long long q = 0, nacc = 0;
+            for (long long it = 0; it < my_items; ++it) {
+                const long long item = blockIdx.x + it * gridDim.x;
+                const int m0 = (int)(item % msplit) * mper, m1 = min(M, m0 + mper);
+                for (int m = m0; m < m1; ++m, ++nacc) {
+                    const int b = (int)(nacc & 1);
+                    if (nacc >= 2) bt_wait(&acc_empty[b], (uint32_t)(((nacc >> 1) - 1) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t dacc = tmem + (uint32_t)(b * BT_N);
+                    for (int ch = 0; ch < nch; ++ch, ++q) {
+                        const int st = (int)(q % TS_NS);
+                        bt_wait(&full_bar[st], (uint32_t)((q / TS_NS) & 1));
+                        asm volatile("tcgen05.fence::after_thread_sync;");
+                        const uint32_t ah = bt_smem_u32(ring + (size_t)st * SLOT), al = ah + A_EL * 4;
+                        const uint32_t bh = ah + 2 * A_EL * 4, bl = bh + B_EL * 4;
+#pragma unroll
+                        for (int s2 = 0; s2 < BT_BK / 8; ++s2) {
+                            const uint32_t off = (uint32_t)s2 * 256;
+                            const uint32_t acc0 = (ch > 0 || s2 > 0) ? 1u : 0u;
+                            bt_mma(dacc, bt_desc(ah + off), bt_desc(bh + off), idesc, acc0);
+                            bt_mma(dacc, bt_desc(ah + off), bt_desc(bl + off), idesc, 1u);
+                            bt_mma(dacc, bt_desc(al + off), bt_desc(bh + off), idesc, 1u);
+                        }
+                        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                         bt_smem_u32(&empty_bar[st]))
+                                     : "memory");
+                    }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                     bt_smem_u32(&acc_full[b]))
+                                 : "memory");
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- epilogue: TMEM -> 32 x 32 transposes -> full 128-byte row segments
+        const int half = tid >> 7, lane = tid & 31;
+        const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(half * 128);
+        float* xp = Xpose + (size_t)warp * 1024;
+        long long nacc = 0;
+        for (long long it = 0; it < my_items; ++it) {
+            const long long item = blockIdx.x + it * gridDim.x;
+            const long long tile = item / msplit;
+            const int m0 = (int)(item % msplit) * mper, m1 = min(M, m0 + mper);
+            const long long wrow0 = tile * BT_ROWS + (warp & 3) * 32;
+            for (int m = m0; m < m1; ++m, ++nacc) {
+                const int b = (int)(nacc & 1);
+                bt_wait(&acc_full[b], (uint32_t)((nacc >> 1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+                for (int c0 = 0; c0 < 128; c0 += 32) {
+                    float v[32];
+                    bt_ld32(taddr + (uint32_t)(b * BT_N) + c0, v);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        *reinterpret_cast<float4*>(xp + lane * 32 + ((j ^ (lane & 7)) << 2)) =
+                            make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                    __syncwarp();
+                    const int cj = lane & 7, col = half * 128 + c0 + 4 * cj;
+#pragma unroll
+                    for (int rb = 0; rb < 32; rb += 4) {
+                        const int r = rb + (lane >> 3);
+                        const float4 w = *reinterpret_cast<const float4*>(xp + r * 32 + ((cj ^ (r & 7)) << 2));
+                        const long long g = wrow0 + r;
+                        if (g < n) {
+                            float* dst = T + g * ldt + (long long)m * K + col;
+                            if ((K & 3) == 0 && col + 3 < K) __stcs(reinterpret_cast<float4*>(dst), w);
+                            else {
+                                if (col < K) dst[0] = w.x;
+                                if (col + 1 < K) dst[1] = w.y;
+                                if (col + 2 < K) dst[2] = w.z;
+                                if (col + 3 < K) dst[3] = w.w;
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bt_smem_u32(&acc_empty[b])) : "memory");
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BT_N));
+    }
+}
+
+static int launch_table_tc_stream(const float* X, long long n, long long ldx, int D, const float* cw, const double* sq,
+                                  int M, int K, int nch, float* T, long long ldt, cudaStream_t s) {
+    constexpr size_t A_EL = (size_t)BT_ROWS * BT_BK, B_EL = (size_t)BT_N * BT_BK;
+    const long long ntiles = (n + BT_ROWS - 1) / BT_ROWS;
+    float* Bg = (float*)scratch(14, sizeof(float) * (size_t)M * nch * 2 * B_EL, s);
+    float* Ag = (float*)scratch(16, sizeof(float) * (size_t)ntiles * nch * 2 * A_EL, s);
+    if (!Bg || !Ag) return fail_cuda(cudaErrorMemoryAllocation, "table_tc_stream scratch");
+    cb_tf32_prep_kernel<<<grid_for((long long)M * nch * BT_N * BT_BK, 256, 4096), 256, 0, s>>>(cw, sq, M, K, D, nch, Bg);
+    DA_CHECK_LAUNCH("cb_tf32_prep_kernel(stream)");
+    a_tf32_img_kernel<<<grid_for(ntiles * nch * (long long)(BT_ROWS * (BT_BK / 4)), 256, 1 << 16), 256, 0, s>>>(
+        X, n, ldx, D, nch, ntiles, Ag);
+    DA_CHECK_LAUNCH("a_tf32_img_kernel");
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int msplit = M % 4 == 0 ? 4 : (M % 2 == 0 ? 2 : 1);
+    if (const char* e = getenv("DA_TABLE_MSPLIT")) msplit = std::max(1, std::min(M, atoi(e)));   // A/B runs
+    const size_t smem = sizeof(float) * ((size_t)TS_NS * (2 * A_EL + 2 * B_EL) + 8 * 1024);
+    static bool attr_set = false;
+    if (!attr_set) {
+        DA_CUDA(cudaFuncSetAttribute(table_tc_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set = true;
+    }
+    const int grid = (int)std::min<long long>(ntiles * msplit, sms);
+    table_tc_stream_kernel<<<grid, TS_T, smem, s>>>(Ag, n, M, K, nch, Bg, T, ldt, msplit);
+    DA_CHECK_LAUNCH("table_tc_stream_kernel");
+    return 0;
+}
+
+// Returns kNotApplicable when the shape does not fit (K > 256, or the row tile's
+// operand image exceeds shared memory and `stream_ok` is 0); the caller then
+// uses the FFMA table.
 int launch_table_tc(const float* X, long long n, long long ldx, int D, const float* cw, const double* sq, int M, int K,
-                    float* T, long long ldt, cudaStream_t s) {
+                    float* T, long long ldt, cudaStream_t s, int stream_ok) {
     if (K > BT_N || K < 1 || n <= 0) return n <= 0 ? 0 : kNotApplicable;
     const int nch = (D + 1 + BT_BK - 1) / BT_BK;
     const size_t smem = sizeof(float) * ((size_t)nch * 2 * BT_ROWS * BT_BK + 2 * 2 * (size_t)BT_N * BT_BK);
-    if (smem > 220 * 1024) return kNotApplicable;
+    if (smem > 220 * 1024) {
+        if (!stream_ok) return kNotApplicable;
+        return launch_table_tc_stream(X, n, ldx, D, cw, sq, M, K, nch, T, ldt, s);
+    }
     float* Bg = (float*)scratch(14, sizeof(float) * (size_t)M * nch * 2 * BT_N * BT_BK, s);
     if (!Bg) return fail_cuda(cudaErrorMemoryAllocation, "table_tc scratch");
     cb_tf32_prep_kernel<<<grid_for((long long)M * nch * BT_N * BT_BK, 256, 4096), 256, 0, s>>>(cw, sq, M, K, D, nch, Bg);

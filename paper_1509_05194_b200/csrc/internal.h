@@ -118,7 +118,7 @@ int launch_greedy(const float* X, long long n, long long ldx, int D, const float
                   const double* cw64, void* codes_out, int code_bytes, long long ldcodes, double* err_out,
                   unsigned long long* stats, int tab_tc, cudaStream_t s);
 int launch_table_tc(const float* X, long long n, long long ldx, int D, const float* cw, const double* sq, int M, int K,
-                    float* T, long long ldt, cudaStream_t s);
+                    float* T, long long ldt, cudaStream_t s, int stream_ok = 0);
 int launch_encode_tc(const float* X, long long n, long long ldx, int D, const float* cw, int M, int K, int L,
                      const double* sq, const double* P, void* codes_out, int code_bytes, long long ldcodes,
                      double* err_out, unsigned long long* stats, cudaStream_t s);

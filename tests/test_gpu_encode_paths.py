@@ -97,3 +97,39 @@ def test_streamed_host_encode_matches_device_encode():
         E.encode_host(bad, cw, sq, Pt, 5, chunk=1000)
     with pytest.raises(ValueError, match="non-finite"):
         da.encode_dataset(book, bad, beam_width=5, cross=cross)
+
+
+@pytest.mark.parametrize("M,D,n", [(8, 960, 1500), (3, 500, 300), (2, 256, 129)])
+def test_wide_rows_d_tiled_table(M, D, n, monkeypatch):
+    """D too wide for a resident tile image: the D-tiled tcgen05 table (streamed
+    tf32 images, looser bound, band narrowing at L = 1) against the plain float64
+    encoder -- default policy, forced on for every width, and forced off."""
+    rng = np.random.default_rng(D + M)
+    centers = rng.random((64, D)).astype(np.float32) * 0.3
+    X = np.clip(centers[rng.integers(0, 64, n)] + 0.05 * rng.standard_normal((n, D)), 0, 1).astype(np.float32)
+    cw = (rng.standard_normal((M, 256, D)) * (0.3 / np.arange(1, M + 1))[:, None, None]).astype(np.float32)
+    cw[0] = np.abs(cw[0])
+    book = da.Codebook(codewords=cw, order=np.arange(M))
+    cross = cb.cross_products(book)
+    cwd, sq = cb._codebook_dev(book)
+    Pt, _ = cross.device()
+    Xd = E.to_dev(X)
+    for L in (1, 10):
+        E.encode_config(1)
+        plain = E.encode(Xd, cwd, sq, Pt, L)
+        E.encode_config(0)
+        for force in (None, "1", "0"):
+            if force is None:
+                monkeypatch.delenv("DA_TABLE_STREAM", raising=False)
+            else:
+                monkeypatch.setenv("DA_TABLE_STREAM", force)
+            assert_same(E.encode(Xd, cwd, sq, Pt, L), plain)
+        monkeypatch.delenv("DA_TABLE_STREAM", raising=False)
+    # band narrowing on the resident-image table too (forced), and off at wide D
+    for val in ("1", "0"):
+        monkeypatch.setenv("DA_GREEDY_NARROW", val)
+        E.encode_config(1)
+        plain = E.encode(Xd, cwd, sq, Pt, 1)
+        E.encode_config(0)
+        assert_same(E.encode(Xd, cwd, sq, Pt, 1), plain)
+    monkeypatch.delenv("DA_GREEDY_NARROW", raising=False)
