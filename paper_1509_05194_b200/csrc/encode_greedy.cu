@@ -38,6 +38,40 @@ __host__ __device__ inline size_t greedy_smem_bytes(int M, int D) {
     return (b + 15) & ~size_t(15);
 }
 
+// x.c in the reference's order with the row read from global memory as fp32
+// (exact in float64): the wide-row path, where staging D doubles per warp would
+// cost the kernel its occupancy.  Same FMA sequence as exact_dot.
+__device__ __noinline__ double exact_dot_gx(const float* __restrict__ x, const float* __restrict__ c, int D, bool v4) {
+    double tot = 0.0;
+    bool first = true;
+    int d = 0;
+    while (d < D) {
+        const int e = d + (int)blas_block_len(D - d);
+        double acc = 0.0;
+        if (v4 && (d & 3) == 0) {
+            for (; d + 16 <= e; d += 16) {
+                float4 xv[4], cv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    xv[u] = __ldg(reinterpret_cast<const float4*>(x + d) + u);
+                    cv[u] = __ldg(reinterpret_cast<const float4*>(c + d) + u);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    acc = __fma_rn((double)xv[u].x, (double)cv[u].x, acc);
+                    acc = __fma_rn((double)xv[u].y, (double)cv[u].y, acc);
+                    acc = __fma_rn((double)xv[u].z, (double)cv[u].z, acc);
+                    acc = __fma_rn((double)xv[u].w, (double)cv[u].w, acc);
+                }
+            }
+        }
+        for (; d < e; ++d) acc = __fma_rn((double)x[d], (double)c[d], acc);
+        tot = first ? acc : dadd(tot, acc);
+        first = false;
+    }
+    return tot;
+}
+
 // Exact stage decision (warp-collective, rare): bring the exact score s from
 // stage *sv up to stage m, then the band candidates' exact values (V, k) and
 // their lexicographic minimum.  Out of line to keep the hot loop small.
@@ -47,20 +81,23 @@ __device__ __noinline__ int greedy_exact(GreedySmem S, const float* __restrict__
                                          double& s, int& sv, bool& staged, unsigned long long& n_exact) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    if (!staged) {
+    const bool gx = S.x64 == nullptr;   // wide rows: no float64 staging, x read from global
+    if (!staged && !gx) {
         for (int d = lane; d < D; d += 32) S.x64[d] = (double)xr[d];
         __syncwarp();
         staged = true;
     }
     const bool c32ok = (D & 3) == 0 && ((reinterpret_cast<uintptr_t>(cw32) & 15) == 0);
+    const bool gx4 = c32ok && ((reinterpret_cast<uintptr_t>(xr) & 15) == 0);
     // 1. exact scores of the stages decided without them: t64 of the chosen codes, one lane each
     while (sv < m) {
         const int nst = min(32, m - sv);
         double t = 0.0;
         if (lane < nst) {
             const int j = sv + lane, c = S.codes[j];
-            const double xc = exact_dot(S.x64, cw64 + ((long long)j * K + c) * D, D,
-                                        c32ok ? cw32 + ((long long)j * K + c) * D : nullptr);
+            const double xc = gx ? exact_dot_gx(xr, cw32 + ((long long)j * K + c) * D, D, gx4)
+                                 : exact_dot(S.x64, cw64 + ((long long)j * K + c) * D, D,
+                                             c32ok ? cw32 + ((long long)j * K + c) * D : nullptr);
             t = dsub(sq[j * K + c], dmul(2.0, xc));
         }
         n_exact += lane < nst ? 1 : 0;
@@ -89,8 +126,9 @@ __device__ __noinline__ int greedy_exact(GreedySmem S, const float* __restrict__
             const int nc = __popc(hb);
             if (lane < nc) {
                 const int k = S.cand[lane];
-                const double xc = exact_dot(S.x64, cw64 + ((long long)m * K + k) * D, D,
-                                            c32ok ? cw32 + ((long long)m * K + k) * D : nullptr);
+                const double xc = gx ? exact_dot_gx(xr, cw32 + ((long long)m * K + k) * D, D, gx4)
+                                     : exact_dot(S.x64, cw64 + ((long long)m * K + k) * D, D,
+                                                 c32ok ? cw32 + ((long long)m * K + k) * D : nullptr);
                 const double t = dsub(sq[m * K + k], dmul(2.0, xc));
                 double cross = 0.0;
                 for (int j = 0; j < m; ++j) cross = dadd(cross, P[(((long long)j * M + m) * K + S.codes[j]) * K + k]);
@@ -132,32 +170,40 @@ __device__ __noinline__ unsigned greedy_narrow(GreedySmem S, const float* __rest
     const float inf = __int_as_float(0x7f800000);
     const bool v4 = (D & 3) == 0 && ((reinterpret_cast<uintptr_t>(cw32) & 15) == 0) &&
                     ((reinterpret_cast<uintptr_t>(xr) & 15) == 0);
-    float v2[8];
+    // one list of all band candidates (k order within a lane, lanes in order)
+    const int cnt = __popc(hits);
+    int base = cnt;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v2[q] = inf;
+    for (int off = 1; off < 32; off <<= 1) {
+        const int t = __shfl_up_sync(FULL, base, off);
+        if (lane >= off) base += t;
+    }
+    const int total = __shfl_sync(FULL, base, 31);
+    base -= cnt;
+    if (total > 32) return hits;   // a very wide band: the exact pass takes it as it is
+    __syncwarp();
+    {
+        unsigned h = hits;
+        for (int i = 0; h; ++i, h &= h - 1) {
+            const int q = __ffs(h) - 1;
+            S.cand[base + i] = (q >> 2) * 128 + 4 * lane + (q & 3);
+        }
+    }
+    __syncwarp();
 #pragma unroll 1
-    for (int q = 0; q < 8; ++q) {
-        const bool hit = (hits >> q) & 1u;
-        const unsigned hb = __ballot_sync(FULL, hit);
-        if (!hb) continue;
-        const int pos = __popc(hb & ((1u << lane) - 1u));
-        const int nc = __popc(hb);
-        __syncwarp();
-        if (hit) S.cand[pos] = (q >> 2) * 128 + 4 * lane + (q & 3);
-        __syncwarp();
-#pragma unroll 1
-        for (int c0 = 0; c0 < nc; c0 += 4) {
-            const float* cr[4];
+    for (int c0 = 0; c0 < total; c0 += 4) {
+        const int nb = min(4, total - c0);   // warp-uniform
+        const float* cr[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-                cr[i] = cw32 + ((long long)m * K + S.cand[min(c0 + i, nc - 1)]) * D;
-            float dot[4] = {0.f, 0.f, 0.f, 0.f};
-            if (v4) {
-#pragma unroll 1
-                for (int d = 4 * lane; d < D; d += 128) {
-                    const float4 x = __ldg(reinterpret_cast<const float4*>(xr + d));
+        for (int i = 0; i < 4; ++i) cr[i] = cw32 + ((long long)m * K + S.cand[min(c0 + i, total - 1)]) * D;
+        float dot[4] = {0.f, 0.f, 0.f, 0.f};
+        if (v4) {
+#pragma unroll 2
+            for (int d = 4 * lane; d < D; d += 128) {
+                const float4 x = __ldg(reinterpret_cast<const float4*>(xr + d));
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
+                for (int i = 0; i < 4; ++i) {
+                    if (i < nb) {
                         const float4 c = __ldg(reinterpret_cast<const float4*>(cr[i] + d));
                         dot[i] = fmaf(x.x, c.x, dot[i]);
                         dot[i] = fmaf(x.y, c.y, dot[i]);
@@ -165,29 +211,42 @@ __device__ __noinline__ unsigned greedy_narrow(GreedySmem S, const float* __rest
                         dot[i] = fmaf(x.w, c.w, dot[i]);
                     }
                 }
-            } else {
+            }
+        } else {
 #pragma unroll 1
-                for (int d0 = 4 * lane; d0 < D; d0 += 128) {
-                    for (int d = d0; d < min(d0 + 4, D); ++d) {
-                        const float x = xr[d];
+            for (int d0 = 4 * lane; d0 < D; d0 += 128) {
+                for (int d = d0; d < min(d0 + 4, D); ++d) {
+                    const float x = xr[d];
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) dot[i] = fmaf(x, cr[i][d], dot[i]);
-                    }
+                    for (int i = 0; i < 4; ++i)
+                        if (i < nb) dot[i] = fmaf(x, cr[i][d], dot[i]);
                 }
             }
+        }
 #pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) {
+        for (int off = 16; off >= 1; off >>= 1) {
 #pragma unroll
-                for (int i = 0; i < 4; ++i) dot[i] += __shfl_xor_sync(FULL, dot[i], off);
-            }
-            if (hit && pos >= c0 && pos < c0 + 4) {
-                const int i = pos - c0;
-                const float dsel = i == 0 ? dot[0] : (i == 1 ? dot[1] : (i == 2 ? dot[2] : dot[3]));
-                const int k = (q >> 2) * 128 + 4 * lane + (q & 3);
-                const float t2 = fmaf(-2.f, dsel, (float)sq[m * K + k]);
-                const float aq = acc[q];
-                v2[q] = fmaf(2.f, aq, t2);
-            }
+            for (int i = 0; i < 4; ++i) dot[i] += __shfl_xor_sync(FULL, dot[i], off);
+        }
+        __syncwarp();   // every lane has read this batch's candidates: the slots now carry the dots
+        if (lane < nb) {
+            const float dsel = lane == 0 ? dot[0] : (lane == 1 ? dot[1] : (lane == 2 ? dot[2] : dot[3]));
+            S.cand[c0 + lane] = __float_as_int(dsel);
+        }
+    }
+    __syncwarp();
+    float v2[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v2[q] = inf;
+    {
+        unsigned h = hits;
+        for (int i = 0; h; ++i, h &= h - 1) {
+            const int q = __ffs(h) - 1;
+            const int k = (q >> 2) * 128 + 4 * lane + (q & 3);
+            const float t2 = fmaf(-2.f, __int_as_float(S.cand[base + i]), (float)sq[m * K + k]);
+            const float val = fmaf(2.f, acc[q], t2);
+#pragma unroll
+            for (int qq = 0; qq < 8; ++qq) v2[qq] = qq == q ? val : v2[qq];
         }
     }
     const double u = 5.9604644775390625e-08;  // 2^-24
@@ -210,31 +269,46 @@ __device__ __noinline__ unsigned greedy_narrow(GreedySmem S, const float* __rest
 #ifndef DA_GR_MINB
 #define DA_GR_MINB 7   // 40 registers: 56 warps per SM hide the gathers (L=1 per 1M: 11.8 -> 9.1 ms)
 #endif
+template <bool WIDE>   // WIDE: band narrowing + vector norm loads + optional staging (wide rows / forced)
 __global__ void __launch_bounds__(32 * GR_WARPS, DA_GR_MINB) greedy_kernel(
     const float* __restrict__ X, long long n, long long ldx, int D, const float* __restrict__ cw, int M, int K,
     const float* __restrict__ tab32, const double* __restrict__ sq, const double* __restrict__ P,
     const float* __restrict__ P32, const double* __restrict__ cmax, const double* __restrict__ cbm,
     const double* __restrict__ cw64, void* codes_out, int code_bytes, long long ldcodes, double* __restrict__ err_out,
-    unsigned long long* __restrict__ stats, int tab_tc, int narrow) {
+    unsigned long long* __restrict__ stats, int tab_tc, int narrow, int stage_d) {
     extern __shared__ __align__(16) char smem_raw[];
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const long long v = (long long)blockIdx.x * GR_WARPS + wid;
     if (v >= n) return;
-    char* p = smem_raw + (size_t)wid * greedy_smem_bytes(M, D);
+    // stage_d = D: room for the float64 row (staged when an exact stage needs it, and for
+    // the error); 0: wide rows without errors -- exact dots read x from global memory
+    const int sd = WIDE ? stage_d : D;   // the narrow-row instance always stages
+    char* p = smem_raw + (size_t)wid * greedy_smem_bytes(M, sd);
     GreedySmem S;
-    S.x64 = (double*)p;
-    S.codes = (int32_t*)(p + sizeof(double) * D);
+    S.x64 = (!WIDE || sd) ? (double*)p : nullptr;
+    S.codes = (int32_t*)(p + sizeof(double) * sd);
     S.cand = S.codes + M;
     const float* xr = X + v * ldx;
     const float* trow = tab32 + v * (long long)M * K;
-    // ||x|| (rounded up) for the bound; the float64 row is staged only if an exact stage needs it
+    // ||x|| (rounded up) for the bound: all of a lane's loads in flight at once
     double xx_part = 0.0;
+    if (WIDE && (D & 3) == 0 && (ldx & 3) == 0 && ((reinterpret_cast<uintptr_t>(X) & 15) == 0)) {
+#pragma unroll 4
+        for (int d = 4 * lane; d < D; d += 128) {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(xr + d));
+            xx_part = __fma_rn((double)t.x, (double)t.x, xx_part);
+            xx_part = __fma_rn((double)t.y, (double)t.y, xx_part);
+            xx_part = __fma_rn((double)t.z, (double)t.z, xx_part);
+            xx_part = __fma_rn((double)t.w, (double)t.w, xx_part);
+        }
+    } else {
 #pragma unroll 1
-    for (int d = lane; d < D; d += 32) {
-        const double t = (double)xr[d];
-        xx_part = __fma_rn(t, t, xx_part);
+        for (int d = lane; d < D; d += 32) {
+            const double t = (double)xr[d];
+            xx_part = __fma_rn(t, t, xx_part);
+        }
     }
     for (int off = 16; off >= 1; off >>= 1) xx_part += __shfl_xor_sync(FULL, xx_part, off);
     const double xnorm = sqrt(xx_part) * (1.0 + 1e-12);
@@ -294,7 +368,7 @@ __global__ void __launch_bounds__(32 * GR_WARPS, DA_GR_MINB) greedy_kernel(
         int first_q = __ffs(hits) - 1;
         int total = __reduce_add_sync(FULL, cnt);
         int code;
-        if (total > 1 && narrow) {   // tensor-core table at wide D: tighten the band first
+        if (WIDE && total > 1 && narrow) {   // tensor-core table at wide D: tighten the band first
             hits = greedy_narrow(S, xr, D, cw, sq, cmax, cbm, K, m, hits, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5],
                                  acc[6], acc[7], xnorm, e2);
             cnt = __popc(hits);
@@ -348,16 +422,20 @@ int launch_greedy(const float* X, long long n, long long ldx, int D, const float
     if (K != 256) return kNotApplicable;
     if (const char* e = getenv("DA_GREEDY"))
         if (atoi(e) == 0) return kNotApplicable;
-    const size_t smem = greedy_smem_bytes(M, D) * GR_WARPS;
+    // wide rows without errors: no float64 staging (7.7 KB per warp at D = 960 would leave 24 warps per SM)
+    const int stage_d = (err_out != nullptr || D <= 384) ? D : 0;
+    const size_t smem = greedy_smem_bytes(M, stage_d) * GR_WARPS;
     if (smem > 200 * 1024) return kNotApplicable;
-    if (smem > 48 * 1024)
-        DA_CUDA(cudaFuncSetAttribute(greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+
     const unsigned grid = (unsigned)((n + GR_WARPS - 1) / GR_WARPS);
     // band narrowing pays where the tensor-core bound is loose (wide D); DA_GREEDY_NARROW=0/1 forces it
     int narrow = tab_tc == 1 && D >= 256;
     if (const char* e = getenv("DA_GREEDY_NARROW")) narrow = atoi(e) != 0;
-    greedy_kernel<<<grid, 32 * GR_WARPS, smem, s>>>(X, n, ldx, D, cw, M, K, tab, sq, P, P32, cmax, cbm, cw64,
-                                                    codes_out, code_bytes, ldcodes, err_out, stats, tab_tc, narrow);
+    const bool wide = narrow || stage_d == 0;
+    auto kfn = wide ? greedy_kernel<true> : greedy_kernel<false>;
+    if (smem > 48 * 1024) DA_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kfn<<<grid, 32 * GR_WARPS, smem, s>>>(X, n, ldx, D, cw, M, K, tab, sq, P, P32, cmax, cbm, cw64, codes_out, code_bytes,
+                                          ldcodes, err_out, stats, tab_tc, narrow, stage_d);
     DA_CHECK_LAUNCH("greedy_kernel");
     return 0;
 }
