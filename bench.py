@@ -65,6 +65,8 @@ def parse():
                     help="also time the reference's da_sweep on this many rows (slow: ~66 s for 4096)")
     ap.add_argument("--no-adc", action="store_true", help="skip the config-E ADC scan timing")
     ap.add_argument("--no-atree", action="store_true", help="skip the A-Tree build + search timing")
+    ap.add_argument("--no-configc", action="store_true", help="skip the config-C (D=960) encode timing")
+    ap.add_argument("--configc-n", type=int, default=131_072, help="config-C vectors (D=960) for the L=1 encode")
     ap.add_argument("--adc-n", type=int, default=1_000_000_000, help="encoded vectors for the ADC scan")
     ap.add_argument("--dry-run", action="store_true",
                     help="launcher/collective plumbing only (gloo on CPU, no kernels): for CPU-box tests")
@@ -696,6 +698,57 @@ def main():
                                  "traffic_source": "profiles/ncu_traffic_r02.json: adc_scan_packed bytes per candidate"}
         del rec_e, cand_r, lut_e, Qe
 
+    # --- config C (D = 960): the D-tiled tcgen05 score table + greedy L=1 encode on a
+    # bounded sample (the 1M-vector config does not change per-vector cost: the encode
+    # runs in 131k-row chunks), and the L=10 encode (chunked FFMA table) for reference
+    configc = None
+    if not args.no_configc and rank == 0:
+        from paper_1509_05194_b200 import synthetic as SY
+
+        nc_ = args.configc_n
+        Dc = 960
+        Xc = E.to_dev(np.ascontiguousarray(SY.config_c(n=nc_), dtype=np.float32))
+        cwc, _ = E.growth_pass(Xc[:20_000].contiguous(), cfg0)
+        Pc, _ = E.cross_full(cwc)
+        sqc = E.einsum_sq(cwc)
+        cc_out = {"workload": f"config C: {nc_} vectors, D=960, M=8, K=256 (codebook: growth pass on 20,000 rows)"}
+        for Lw, reps in ((1, 3), (10, 1)):
+            E.encode(Xc, cwc, sqc, Pc, Lw, out_dtype=torch.uint8, with_err=False)
+            torch.cuda.synchronize()
+            _native.prof_collect()
+            _native.prof_enable(True)
+            c0e, c1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0e.record(stream)
+            for _ in range(reps):
+                E.encode(Xc, cwc, sqc, Pc, Lw, out_dtype=torch.uint8, with_err=False)
+            c1e.record(stream)
+            torch.cuda.synchronize()
+            _native.prof_enable(False)
+            cprof = _native.prof_collect()
+            c_ms = c0e.elapsed_time(c1e) / reps
+            cc_out[f"L{Lw}_vectors_per_s"] = nc_ / (c_ms / 1e3)
+            cc_out[f"L{Lw}_ms"] = c_ms
+            cc_out[f"L{Lw}_kernels_ms"] = {k: round(t / reps, 4) for k, (c, t) in cprof.items()}
+            if Lw == 1 and "encode_table_tc" in cprof:
+                t_tab = cprof["encode_table_tc"][1] / reps / 1e3
+                # issued tensor work: 3 tf32 MMAs per 8 columns over D+1 columns padded to 16
+                kpad = ((Dc + 1 + 15) // 16) * 16
+                issued = 3 * 2.0 * M * K * kpad * nc_
+                rooflines["configC_table_tc_stream"] = {
+                    "bound": "tensor", "kernel": "table_tc_stream_kernel (+ image and codeword preps)",
+                    "achieved": issued / t_tab / 1e12, "peak": tf32_peak, "unit": "TFLOP/s",
+                    "frac": issued / t_tab / 1e12 / tf32_peak,
+                    "algorithmic_tflops": 2.0 * M * K * Dc * nc_ / t_tab / 1e12,
+                    "frac_3xtf32": 2.0 * M * K * Dc * nc_ / t_tab / 1e12 / (tf32_peak / 3.0),
+                    "peak_nominal": 1125.0, "frac_nominal": issued / t_tab / 1e12 / 1125.0,
+                    "algorithmic": "2*M*K*D flop per vector (SURVEY 8d) against the 3xTF32 roof; `achieved` counts "
+                                   "the three tf32 MMAs issued per k step against the dense TF32 peak measured with "
+                                   "a cuBLAS TF32 GEMM in this run (a conservative denominator: this kernel can "
+                                   "exceed it; peak_nominal = half the nominal dense bf16 rate)",
+                    "ms": t_tab * 1e3}
+        configc = cc_out
+        del Xc, Pc
+
     # --- A-Tree: GPU build over this GPU's L=10 codes, GPU batched search
     atree = None
     if not args.no_atree:
@@ -798,6 +851,7 @@ def main():
             "anneal_pass": anneal,
             "adc_scan": adc,
             "atree_search": atree,
+            "config_c": configc,
             "roofline": roof,
             "rooflines": rooflines,
             "peaks": {"fp32_ffma_tflops": ffma, "tf32_dense_tflops_measured": tf32_peak,

@@ -306,3 +306,54 @@ def test_group_means_many_labels_and_big_segments(n, k, D):
     filled = cnt > 0
     np.testing.assert_array_equal(got[filled], means[filled])
     assert (got[~filled] == -7.0).all()
+
+
+def test_config_d_shape_online_chunks_against_oracle():
+    """Config D's shape at test size: uint8-stored config-B-mixture vectors (D=128),
+    M=8, K=32, streamed as chunks, one anneal pass per chunk -- codewords and
+    distortions of every chunk against the CPU oracle's train_online, bit for bit."""
+    from oracle import da_oracle as O
+    from paper_1509_05194_b200 import synthetic
+
+    X = synthetic.config_b(n=3 * 1200, seed=3, chunk=1200)
+    assert X.dtype == np.float32 and (X == np.round(X)).all() and X.min() >= 0 and X.max() <= 255
+    stored = X.astype(np.uint8)                       # config D stores uint8
+    cfg = da.TrainConfig(m_count=8, k_count=32, beam_width=10, sweeps=1, rel_tol=0.0)
+    book, _, _ = da.train_from_scratch(stored[:1200].astype(np.float32), cfg)
+    cw_o = book.codewords.copy()
+    for c in (1, 2):
+        chunk = stored[c * 1200:(c + 1) * 1200].astype(np.float32)
+        book, rep = da.train_online(book, chunk, cfg)
+        cw_o, steps = O.train_online(cw_o, chunk, L=10, sweeps=1, rel_tol=0.0)
+        np.testing.assert_array_equal(book.codewords, cw_o)
+        np.testing.assert_array_equal(rep.distortions(), np.array([s[2] for s in steps]))
+
+
+def test_config_e_shape_encode_and_candidate_adc_against_oracle():
+    """Config E's shape at test size: uint8 vectors encoded with fixed seeded fp32
+    dictionaries (M=8, K=256, D=128), then queries from the same mixture each
+    scoring its own uniform-random candidate id list, top-100 (adc_rerank) -- codes
+    bit-exact, ids exact, distances to 1e-12 against the CPU oracle."""
+    from oracle import da_oracle as O
+    from paper_1509_05194_b200 import synthetic
+
+    n, nq, ncand, r = 6000, 12, 2500, 100
+    X = synthetic.config_b(n=n, seed=4, chunk=n).astype(np.uint8).astype(np.float32)
+    rng = np.random.default_rng(4)
+    cw = (rng.standard_normal((8, 256, 128)) * (40.0 / (1 + np.arange(8)))[:, None, None]).astype(np.float32)
+    cw[0] += X[rng.integers(0, n, 256)]
+    book = book_of(cw)
+    cross = cb.cross_products(book)
+    enc = da.encode_dataset(book, X, beam_width=10, cross=cross)
+    P, _ = O.cross_table(cw)
+    np.testing.assert_array_equal(enc.codes[:400], O.encode_chunked(cw, P, X[:400], 10))
+    Q = synthetic.config_e_queries(nq=nq, seed=4).astype(np.float64)
+    cand = synthetic.config_e_candidates(nq, ncand=ncand, n_total=n, seed=4)
+    ids, dists = cb.adc_rerank(book, enc, Q, cand, r, cross=cross)
+    codes = enc.codes.astype(np.int64)
+    pair = O.pair_terms(P, codes)
+    for i in range(nq):
+        v, qq = O.adc_lut(cw, Q[i])
+        pos, dref = O.adc_topr(v, qq, codes[cand[i]], pair[cand[i]], r)
+        np.testing.assert_array_equal(ids[i], cand[i][pos])
+        rel_close(dists[i], dref, rtol=1e-12, atol=1e-9)
