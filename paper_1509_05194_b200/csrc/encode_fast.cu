@@ -768,7 +768,7 @@ int launch_encode_fast(const void* X, int x_f32, long long n, long long ldx, int
             // (looser bound than the chunked FFMA table) pays when the band is then
             // narrowed by the greedy kernel's warp-wide fp32 dots, i.e. at L = 1
             const char* est = getenv("DA_TABLE_STREAM");
-            const int stream_ok = est ? atoi(est) != 0 : L == 1;
+            const int stream_ok = est ? atoi(est) != 0 : (L == 1 && K == 256);   // K == 256: the greedy kernel's shape
             const int rc = launch_table_tc((const float*)X + c0 * ldx, cn, ldx, D, cw, sq, M, K, tab, N, s, stream_ok);
             if (rc == 0) tab_tc = 1;
             else if (rc != kNotApplicable) return rc;

@@ -15,7 +15,10 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:"tab
     python tools/prof_tc.py 2 1 > gpurun_out/ncu_l1.log 2>&1; echo "full l1 rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:adc_scan_packed -c 1 -o gpurun_out/prof_adc -f \
     python tools/bench_adc.py 100000000 2000 100000 > gpurun_out/ncu_adc.log 2>&1; echo "full adc rc=$?"
-for r in prof_beam_fast prof_l1 prof_adc; do
+# config C (D=960): D-tiled tcgen05 table + wide-row greedy kernel
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"greedy|table_tc_stream|a_tf32_img" -c 3 -o gpurun_out/prof_c -f \
+    python tools/prof_configc.py 1 > gpurun_out/ncu_c.log 2>&1; echo "full configC rc=$?"
+for r in prof_beam_fast prof_l1 prof_adc prof_c; do
   ncu -i gpurun_out/$r.ncu-rep --page raw --csv > gpurun_out/${r}_raw.csv 2>/dev/null
 done
 ncu -i gpurun_out/prof_beam_fast.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/bf_source.csv 2>/dev/null
