@@ -115,6 +115,28 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// packed fp32 pairs (sm_100 f32x2): one FMA-pipe instruction for two elements,
+// each rounded exactly like the scalar operation
+__device__ __forceinline__ void tc_fma2(float& d0, float& d1, float a, float b0, float b1, float c0, float c1) {
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %2};\n\t"
+        "mov.b64 rb, {%3, %4};\n\t"
+        "mov.b64 rc, {%5, %6};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\t"
+        "mov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d0), "=f"(d1)
+        : "f"(a), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+__device__ __forceinline__ void tc_add2(float& d0, float& d1, float a0, float a1, float b) {
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\t"
+        "mov.b64 rb, {%4, %4};\n\t"
+        "add.rn.f32x2 rd, ra, rb;\n\t"
+        "mov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d0), "=f"(d1)
+        : "f"(a0), "f"(a1), "f"(b));
+}
+
 template <typename TX>
 __device__ __forceinline__ double fma_chain(const TX* __restrict__ xr, const double* __restrict__ cr, int k, int e,
                                             double acc) {
@@ -281,6 +303,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 2, 256;" ::: "memory"); }
+// the two warps that own the same 32 rows (column halves): named barrier 3 + quadrant, 64 threads
+__device__ __forceinline__ void pair_sync(int quad) { asm volatile("bar.sync %0, 64;" ::"r"(3 + quad) : "memory"); }
 
 template <typename TX>
 __global__ void __launch_bounds__(TC_TP, 1) assign_tc_kernel(
@@ -294,9 +318,10 @@ __global__ void __launch_bounds__(TC_TP, 1) assign_tc_kernel(
     float* Bbuf = Abuf + 2 * 2 * A_ELEMS;                             // [2 stages][hi, lo][B_ELEMS]
     double* ccs = reinterpret_cast<double*>(Bbuf + 2 * 2 * B_ELEMS);  // [TC_NMAX]
     float* ccf = reinterpret_cast<float*>(ccs + TC_NMAX);            // [TC_NMAX], +inf beyond K
-    double* wmin_h = reinterpret_cast<double*>(ccf + TC_NMAX);        // [2][TC_M]
-    int* cand = reinterpret_cast<int*>(wmin_h + 2 * TC_M);            // [2][TC_M][TC_CMAX]
-    int* ncand = cand + 2 * TC_M * TC_CMAX;                           // [2][TC_M]
+    // per-tile exchange buffers, double-buffered by tile parity (no barrier between tiles)
+    double* wmin_h = reinterpret_cast<double*>(ccf + TC_NMAX);        // [2 tiles][2 halves][TC_M]
+    unsigned long long* cand64 = reinterpret_cast<unsigned long long*>(wmin_h + 4 * TC_M);   // [2][2][TC_M] packed lists
+    int* ncand = reinterpret_cast<int*>(cand64 + 4 * TC_M);           // [2][2][TC_M]
     __shared__ uint64_t full_bar[2], empty_bar[2], acc_full[2], acc_empty[2], b_bar;
     __shared__ uint32_t tmem_base_sh;
     __shared__ double red[8];
@@ -318,7 +343,7 @@ __global__ void __launch_bounds__(TC_TP, 1) assign_tc_kernel(
             mbar_init(&full_bar[i], 1);
             mbar_init(&empty_bar[i], 1);
             mbar_init(&acc_full[i], 1);
-            mbar_init(&acc_empty[i], 1);
+            mbar_init(&acc_empty[i], TC_T2 / 32);   // one arrival per epilogue warp
         }
         mbar_init(&b_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -439,43 +464,83 @@ __global__ void __launch_bounds__(TC_TP, 1) assign_tc_kernel(
             const uint32_t taddr = tmem + (uint32_t)(accb * TC_NMAX) + ((uint32_t)((warp & 3) * 32) << 16);
             float v[32];
             float wminf = __int_as_float(0x7f800000);
-            for (int c0 = cbeg; c0 < cend; c0 += 32) {
-                tmem_ld32(taddr + c0, v);
+            // Both passes are bound by instruction issue: the FMA and the ALU pipe each take one
+            // warp instruction per two clocks.  Packed f32x2 operations halve the FMA-pipe
+            // count (w' = cc - 2 v for two codewords per instruction); the minimum keeps its
+            // three-input ALU form.
+            {
+                // four independent minimum chains (two epilogue warps per scheduler cannot
+                // hide a 16-long dependent chain per load)
+                float wm1 = wminf, wm2 = wminf, wm3 = wminf;
+                for (int c0 = cbeg; c0 < cend; c0 += 32) {
+                    tmem_ld32(taddr + c0, v);
 #pragma unroll
-                for (int i = 0; i < 32; ++i) wminf = fminf(wminf, fmaf(-2.f, v[i], ccf[c0 + i]));
+                    for (int i = 0; i < 32; i += 8) {
+                        float w0, w1, w2, w3, w4, w5, w6, w7;
+                        tc_fma2(w0, w1, -2.f, v[i], v[i + 1], ccf[c0 + i], ccf[c0 + i + 1]);
+                        tc_fma2(w2, w3, -2.f, v[i + 2], v[i + 3], ccf[c0 + i + 2], ccf[c0 + i + 3]);
+                        tc_fma2(w4, w5, -2.f, v[i + 4], v[i + 5], ccf[c0 + i + 4], ccf[c0 + i + 5]);
+                        tc_fma2(w6, w7, -2.f, v[i + 6], v[i + 7], ccf[c0 + i + 6], ccf[c0 + i + 7]);
+                        wminf = fminf(fminf(wminf, w0), w1);
+                        wm1 = fminf(fminf(wm1, w2), w3);
+                        wm2 = fminf(fminf(wm2, w4), w5);
+                        wm3 = fminf(fminf(wm3, w6), w7);
+                    }
+                }
+                wminf = fminf(fminf(wminf, wm1), fminf(wm2, wm3));
             }
-            wmin_h[ehalf * TC_M + erow] = (double)wminf;
-            epi_sync();
+            double* wm = wmin_h + accb * 2 * TC_M;
+            wm[ehalf * TC_M + erow] = (double)wminf;
+            pair_sync(warp & 3);   // only the row's other half has to be there
             AT_MARK(3);
-            const double wmin = fmin(wmin_h[erow], wmin_h[TC_M + erow]);
+            const double wmin = fmin(wm[erow], wm[TC_M + erow]);
             const double ub = fmax(xx + wmin + E, 0.0);
             // candidate k iff max(xx + w'_k - E, 0) <= ub  <=>  w'_k <= ub - xx + E (ub >= 0)
             const double tlim = ub - xx + E;
             const float tf = (tlim >= 3.0e38) ? __int_as_float(0x7f800000)
                                               : __fadd_ru((float)tlim, fabsf((float)tlim) * 1e-6f + 1e-30f);
+            // -tf2 with tf2 just above tf (tf = +inf: every finite w' is a candidate, as before)
+            const float ntf2 = (tlim >= 3.0e38) ? -tf : -__fadd_ru(tf, fabsf(tf) * 1.1920929e-07f + 1e-37f);
             int nc = 0;
-            int* my = cand + (ehalf * TC_M + erow) * TC_CMAX;
+            unsigned long long pk = 0ULL;   // this half row's candidates, one byte each, ascending
             for (int c0 = cbeg; c0 < cend; c0 += 32) {
                 tmem_ld32(taddr + c0, v);
-                uint32_t hit = 0;  // branch-free test, then walk the (rare) set bits
+                // Branch-free test: e = w' - tf2 is negative for every w' <= tf (tf2 lies above
+                // tf; a difference of two distinct floats is never zero), and one funnel shift per
+                // element moves its sign bit into the mask (compare + select + add cost 2.5 ALU
+                // instructions per element before).  Column c0 + i ends at bit 31 - i.  Padding
+                // columns (w' = +inf) give +inf or NaN: sign clear.
+                uint32_t h4[4] = {0u, 0u, 0u, 0u};   // four independent shift chains of 8 columns each
 #pragma unroll
-                for (int i = 0; i < 32; ++i) hit |= (uint32_t)(fmaf(-2.f, v[i], ccf[c0 + i]) <= tf) << i;
+                for (int i = 0; i < 8; i += 2) {
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        float w0, w1, e0, e1;
+                        tc_fma2(w0, w1, -2.f, v[8 * g + i], v[8 * g + i + 1], ccf[c0 + 8 * g + i], ccf[c0 + 8 * g + i + 1]);
+                        tc_add2(e0, e1, w0, w1, ntf2);
+                        h4[g] = __funnelshift_l(__float_as_uint(e0), h4[g], 1);
+                        h4[g] = __funnelshift_l(__float_as_uint(e1), h4[g], 1);
+                    }
+                }
+                uint32_t hit = (h4[0] << 24) | (h4[1] << 16) | (h4[2] << 8) | h4[3];   // then walk the (rare) set bits, ascending column
                 while (hit) {
-                    const int i = __ffs(hit) - 1;
-                    hit &= hit - 1;
-                    if (nc < TC_CMAX) my[nc] = c0 + i;
+                    const int i = __clz(hit);
+                    hit &= ~(0x80000000u >> i);
+                    if (nc < TC_CMAX) pk |= (unsigned long long)(c0 + i) << (8 * nc);
                     ++nc;
                 }
             }
-            ncand[ehalf * TC_M + erow] = nc;
+            cand64[(accb * 2 + ehalf) * TC_M + erow] = pk;
+            ncand[(accb * 2 + ehalf) * TC_M + erow] = nc;
             asm volatile("tcgen05.fence::before_thread_sync;");
-            epi_sync();
-            if (tid == 0) mbar_arrive(&acc_empty[accb]);   // TMEM buffer free for tile it + 2
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[accb]);   // this warp is done with the TMEM buffer (free for tile it + 2 after all 8)
+            pair_sync(warp & 3);
             AT_MARK(4);
             if (ehalf == 0 && valid) {
                 // the row's candidates (both halves, ascending k) go to global memory; the
                 // exact float64 rechecks run in assign_recheck_kernel with coalesced rows
-                const int n0 = ncand[erow], n1 = ncand[TC_M + erow];
+                const int n0 = ncand[accb * 2 * TC_M + erow], n1 = ncand[(accb * 2 + 1) * TC_M + erow];
                 if (n0 + n1 > TC_CMAX) {
                     // too many near-ties for this row: a warp-parallel exact scan over
                     // all K runs after the kernel (assign_overflow_kernel)
@@ -483,18 +548,13 @@ __global__ void __launch_bounds__(TC_TP, 1) assign_tc_kernel(
                     gcnt[r] = 0xFF;
                     if (stats) atomicAdd(stats, (unsigned long long)K);
                 } else {
-                    uint32_t w2[2] = {0u, 0u};
-                    for (int i = 0; i < n0; ++i) w2[i >> 2] |= (uint32_t)cand[erow * TC_CMAX + i] << (8 * (i & 3));
-                    for (int i = 0; i < n1; ++i) {
-                        const int j = n0 + i;
-                        w2[j >> 2] |= (uint32_t)cand[(TC_M + erow) * TC_CMAX + i] << (8 * (j & 3));
-                    }
-                    *reinterpret_cast<uint2*>(gcand + r * 8) = make_uint2(w2[0], w2[1]);
+                    unsigned long long mg = cand64[accb * 2 * TC_M + erow];
+                    if (n1 > 0) mg |= cand64[(accb * 2 + 1) * TC_M + erow] << (8 * n0);   // n0 < 8 here
+                    *reinterpret_cast<uint2*>(gcand + r * 8) = make_uint2((uint32_t)mg, (uint32_t)(mg >> 32));
                     gcnt[r] = (uint8_t)(n0 + n1);
                 }
             }
-            epi_sync();   // cand / ncand / wmin_h are rewritten by the next tile
-            AT_MARK(5);
+            AT_MARK(5);   // no barrier here: the exchange buffers alternate with the tile parity
         }
         if (tid == 0)
             for (int i = 0; i < 8; ++i) atomicAdd(&g_at_prof[i], (unsigned long long)at_acc[i]);
@@ -824,7 +884,7 @@ int launch_assign_tc(const void* X, int x_is_f32, long long n, long long ldx, in
     DA_CHECK_LAUNCH("cw_tf32_prep_kernel");
     const size_t smem = sizeof(float) * (2 * 2 * TC_M * TC_BK + 2 * 2 * TC_NMAX * TC_BK) + sizeof(double) * TC_NMAX +
                         sizeof(float) * TC_NMAX +
-                        sizeof(double) * 2 * TC_M + sizeof(int) * (2 * TC_M * TC_CMAX + 2 * TC_M);
+                        sizeof(double) * 4 * TC_M + sizeof(unsigned long long) * 4 * TC_M + sizeof(int) * 4 * TC_M;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
