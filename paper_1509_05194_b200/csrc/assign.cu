@@ -492,7 +492,7 @@ int launch_assign(const void* X, int x_is_f32, long long n, long long ldx, int d
                   const int32_t* prev, unsigned long long* changed, cudaStream_t s) {
     if (n <= 0) return 0;
     // fp32 filter for narrow prefixes (d <= 16), then the float64 kernels
-    static const int ffma_max = getenv("DA_ASSIGN_FFMA_D") ? atoi(getenv("DA_ASSIGN_FFMA_D")) : 8;   // B200, 1M rows: d=2 0.25 -> 0.14 ms, d=8 0.33 -> 0.25; the tcgen05 filter wins from d=12
+    static const int ffma_max = getenv("DA_ASSIGN_FFMA_D") ? atoi(getenv("DA_ASSIGN_FFMA_D")) : 4;   // B200, 1M rows: d=2,3 0.14 ms; from d=5 the tcgen05 filter wins (0.18 vs 0.20 ms per call inside the anneal pass)
     if (g_assign_mode == 0 && d <= ffma_max && d <= 16 && K <= 4096) {
         ProfScope ps("assign_ffma_d<=8", s);
         const int dm = d <= 4 ? 4 : d <= 8 ? 8 : 16;

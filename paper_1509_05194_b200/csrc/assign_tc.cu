@@ -311,7 +311,11 @@ __global__ void __launch_bounds__(TC_TP, 1) assign_tc_kernel(
     const TX* __restrict__ X, long long n, long long ldx, int d, int K, const double* __restrict__ cc,
     const double* __restrict__ xx_in, const float* __restrict__ Ag, const float* __restrict__ Bg,
     unsigned long long* __restrict__ stats, int* __restrict__ ovf_rows, int* __restrict__ ovf_cnt,
-    uint8_t* __restrict__ gcand, uint8_t* __restrict__ gcnt) {
+    uint8_t* __restrict__ gcand, uint8_t* __restrict__ gcnt, int32_t* __restrict__ lo_labels,
+    const int32_t* __restrict__ lo_prev, unsigned long long* __restrict__ lo_changed, int* __restrict__ multi_rows) {
+    // lo_labels != nullptr: labels-only mode (the Lloyd loop inside DA).  A row with a single
+    // candidate gets its label here; rows with 2..8 candidates go to a compact list for
+    // assign_multi_kernel (ovf_cnt[1] counts them) -- no pass over all rows after this kernel.
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int A_ELEMS = TC_M * TC_BK, B_ELEMS = TC_NMAX * TC_BK;
     float* Abuf = reinterpret_cast<float*>(smem);                    // [2 stages][hi, lo][A_ELEMS]
@@ -432,6 +436,7 @@ __global__ void __launch_bounds__(TC_TP, 1) assign_tc_kernel(
         const int erow = tid & (TC_M - 1);   // TMEM lane / tile row owned in the epilogue
         const int ehalf = tid >> 7;          // 0: codewords [0,128), 1: [128,256)
         long long it = 0;
+        unsigned lo_nchg = 0;   // labels-only: rows of this thread whose label changed
         // the row norm of the next tile is loaded one tile ahead: waiting on it at the
         // top of every tile was the epilogue's largest stall
         double xx_next = 0.0;
@@ -550,11 +555,22 @@ __global__ void __launch_bounds__(TC_TP, 1) assign_tc_kernel(
                 } else {
                     unsigned long long mg = cand64[accb * 2 * TC_M + erow];
                     if (n1 > 0) mg |= cand64[(accb * 2 + 1) * TC_M + erow] << (8 * n0);   // n0 < 8 here
-                    *reinterpret_cast<uint2*>(gcand + r * 8) = make_uint2((uint32_t)mg, (uint32_t)(mg >> 32));
-                    gcnt[r] = (uint8_t)(n0 + n1);
+                    if (lo_labels != nullptr && n0 + n1 == 1) {
+                        const int k0 = (int)(mg & 0xFFu);
+                        lo_labels[r] = k0;
+                        if (lo_prev != nullptr && lo_prev[r] != k0) ++lo_nchg;
+                    } else {
+                        *reinterpret_cast<uint2*>(gcand + r * 8) = make_uint2((uint32_t)mg, (uint32_t)(mg >> 32));
+                        gcnt[r] = (uint8_t)(n0 + n1);
+                        if (lo_labels != nullptr) multi_rows[atomicAdd(ovf_cnt + 1, 1)] = (int)r;
+                    }
                 }
             }
             AT_MARK(5);   // no barrier here: the exchange buffers alternate with the tile parity
+        }
+        if (lo_changed != nullptr && lo_prev != nullptr) {
+            lo_nchg = __reduce_add_sync(0xffffffffu, lo_nchg);
+            if (lane == 0 && lo_nchg) atomicAdd(lo_changed, (unsigned long long)lo_nchg);
         }
         if (tid == 0)
             for (int i = 0; i < 8; ++i) atomicAdd(&g_at_prof[i], (unsigned long long)at_acc[i]);
@@ -802,6 +818,59 @@ __global__ void __launch_bounds__(32 * RC_WARPS) assign_recheck_kernel(
     }
 }
 
+// Labels-only mode: the rows that kept 2..8 candidates (a compact list written by
+// assign_tc_kernel).  One warp per row, lane j evaluates candidate j exactly (same
+// BLAS-ordered value as assign_recheck_kernel), first minimum by (value, index).
+template <typename TX>
+__global__ void __launch_bounds__(256) assign_multi_kernel(const TX* __restrict__ X, long long ldx, int d,
+                                                           const double* __restrict__ C, long long ldc,
+                                                           const double* __restrict__ cc,
+                                                           const double* __restrict__ xx_in,
+                                                           const uint8_t* __restrict__ gcand,
+                                                           const uint8_t* __restrict__ gcnt,
+                                                           const int* __restrict__ rows, const int* __restrict__ cnt_p,
+                                                           int32_t* __restrict__ labels,
+                                                           const int32_t* __restrict__ prev,
+                                                           unsigned long long* __restrict__ changed,
+                                                           unsigned long long* __restrict__ stats) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int nrows = *cnt_p;
+    const bool blk = d > (int)BLAS_Q;
+    unsigned long long nchg = 0, nstat = 0;
+    for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nrows;
+         w += ((long long)gridDim.x * blockDim.x) >> 5) {
+        const long long r = rows[w];
+        const int cnt = gcnt[r];
+        const TX* xr = X + r * ldx;
+        double dv = __longlong_as_double(0x7ff0000000000000ULL);
+        int kj = 0x7fffffff;
+        if (lane < cnt) {
+            kj = gcand[r * 8 + lane];
+            const double xx = xx_in ? xx_in[r]
+                                    : np_pw_sum([&](long long i) { double t = (double)xr[i]; return dmul(t, t); }, 0, d);
+            const double* crow = C + (long long)kj * ldc;
+            const double xc = blk ? exact_xc<TX, true>(xr, crow, d) : exact_xc<TX, false>(xr, crow, d);
+            dv = dadd(dsub(xx, dmul(2.0, xc)), cc[kj]);
+            if (dv < 0.0) dv = 0.0;
+        }
+        for (int off = 4; off >= 1; off >>= 1) {   // candidates live in lanes 0..7
+            const double ob = __shfl_xor_sync(FULL, dv, off);
+            const int ok = __shfl_xor_sync(FULL, kj, off);
+            if (lex_less(ob, ok, dv, kj)) { dv = ob; kj = ok; }
+        }
+        if (lane == 0) {
+            labels[r] = kj;
+            nstat += cnt;
+            if (prev != nullptr && prev[r] != kj) ++nchg;
+        }
+    }
+    if (lane == 0) {
+        if (stats && nstat) atomicAdd(stats, nstat);
+        if (changed != nullptr && prev != nullptr && nchg) atomicAdd(changed, nchg);
+    }
+}
+
 // Row image bound by the host for the duration of one Lloyd call (the rotated
 // rows are fixed while the centroids move): assigns on exactly this (X, n, ldx,
 // d) read it instead of rebuilding it.
@@ -865,15 +934,17 @@ int launch_assign_tc(const void* X, int x_is_f32, long long n, long long ldx, in
     const size_t ovf_bytes = (sizeof(int) * ((size_t)n + 64) + 255) & ~size_t(255);
     const size_t cand_bytes = (9 * (size_t)n + 255) & ~size_t(255);
     const size_t img_bytes = bound ? 0 : assign_image_bytes(n, d);
-    char* base = (char*)scratch(9, bg_bytes + ovf_bytes + cand_bytes + img_bytes, s);
+    const bool labels_only = d2 == nullptr;
+    char* base = (char*)scratch(9, bg_bytes + 2 * ovf_bytes + cand_bytes + img_bytes, s);
     if (!base) return fail_cuda(cudaErrorMemoryAllocation, "assign_tc scratch");
     float* Bg = (float*)base;
     int* ovf_cnt = (int*)(base + bg_bytes);
     int* ovf_rows = ovf_cnt + 64;
     uint8_t* gcand = (uint8_t*)(base + bg_bytes + ovf_bytes);   // [n][8] candidate codewords
     uint8_t* gcnt = gcand + 8 * (size_t)n;                        // [n] counts (0xFF = overflow)
-    const float* Ag = bound ? g_img.img : (const float*)(base + bg_bytes + ovf_bytes + cand_bytes);
-    DA_CUDA(cudaMemsetAsync(ovf_cnt, 0, sizeof(int), s));
+    int* multi_rows = (int*)(base + bg_bytes + ovf_bytes + cand_bytes);   // [n] rows with 2..8 candidates (labels-only)
+    const float* Ag = bound ? g_img.img : (const float*)(base + bg_bytes + 2 * ovf_bytes + cand_bytes);
+    DA_CUDA(cudaMemsetAsync(ovf_cnt, 0, 2 * sizeof(int), s));   // [0] overflow rows, [1] multi-candidate rows
     ProfScope ps(d <= 8 ? "assign_tc_d<=8" : d <= 32 ? "assign_tc_d<=32" : d <= 128 ? "assign_tc_d<=128" : "assign_tc_d>128",
                  s);
     if (!bound) {
@@ -895,10 +966,14 @@ int launch_assign_tc(const void* X, int x_is_f32, long long n, long long ldx, in
         auto kf = assign_tc_kernel<float>;
         { const int rc_ = ensure_smem((const void*)kf, (int)smem); if (rc_) return rc_; }
         kf<<<grid, TC_TP, smem, s>>>((const float*)X, n, ldx, d, K, cc, xx, Ag, Bg, stats, ovf_rows, ovf_cnt, gcand,
-                                     gcnt);
+                                     gcnt, labels_only ? labels : nullptr, prev, changed, multi_rows);
         DA_CHECK_LAUNCH("assign_tc_kernel");
-        assign_recheck_kernel<float><<<rgrid, 32 * RC_WARPS, 0, s>>>((const float*)X, n, ldx, d, C, ldc, cc, xx, gcand,
-                                                                     gcnt, labels, d2, prev, changed, stats);
+        if (labels_only)
+            assign_multi_kernel<float><<<sms, 256, 0, s>>>((const float*)X, ldx, d, C, ldc, cc, xx, gcand, gcnt,
+                                                           multi_rows, ovf_cnt + 1, labels, prev, changed, stats);
+        else
+            assign_recheck_kernel<float><<<rgrid, 32 * RC_WARPS, 0, s>>>((const float*)X, n, ldx, d, C, ldc, cc, xx,
+                                                                         gcand, gcnt, labels, d2, prev, changed, stats);
         DA_CHECK_LAUNCH("assign_recheck_kernel");
         assign_overflow_kernel<float><<<sms, 256, 0, s>>>((const float*)X, ldx, d, C, ldc, K, cc, xx, ovf_rows, ovf_cnt,
                                                           labels, d2, prev, changed);
@@ -906,10 +981,14 @@ int launch_assign_tc(const void* X, int x_is_f32, long long n, long long ldx, in
         auto kf = assign_tc_kernel<double>;
         { const int rc_ = ensure_smem((const void*)kf, (int)smem); if (rc_) return rc_; }
         kf<<<grid, TC_TP, smem, s>>>((const double*)X, n, ldx, d, K, cc, xx, Ag, Bg, stats, ovf_rows, ovf_cnt, gcand,
-                                     gcnt);
+                                     gcnt, labels_only ? labels : nullptr, prev, changed, multi_rows);
         DA_CHECK_LAUNCH("assign_tc_kernel");
-        assign_recheck_kernel<double><<<rgrid, 32 * RC_WARPS, 0, s>>>((const double*)X, n, ldx, d, C, ldc, cc, xx,
-                                                                      gcand, gcnt, labels, d2, prev, changed, stats);
+        if (labels_only)
+            assign_multi_kernel<double><<<sms, 256, 0, s>>>((const double*)X, ldx, d, C, ldc, cc, xx, gcand, gcnt,
+                                                            multi_rows, ovf_cnt + 1, labels, prev, changed, stats);
+        else
+            assign_recheck_kernel<double><<<rgrid, 32 * RC_WARPS, 0, s>>>((const double*)X, n, ldx, d, C, ldc, cc, xx,
+                                                                          gcand, gcnt, labels, d2, prev, changed, stats);
         DA_CHECK_LAUNCH("assign_recheck_kernel");
         assign_overflow_kernel<double><<<sms, 256, 0, s>>>((const double*)X, ldx, d, C, ldc, K, cc, xx, ovf_rows,
                                                            ovf_cnt, labels, d2, prev, changed);
