@@ -823,7 +823,7 @@ __global__ void __launch_bounds__(32 * RC_WARPS) assign_recheck_kernel(
 // BLAS-ordered value as assign_recheck_kernel), first minimum by (value, index).
 template <typename TX>
 __global__ void __launch_bounds__(256) assign_multi_kernel(const TX* __restrict__ X, long long ldx, int d,
-                                                           const double* __restrict__ C, long long ldc,
+                                                           const double* __restrict__ C, long long ldc, int K,
                                                            const double* __restrict__ cc,
                                                            const double* __restrict__ xx_in,
                                                            const uint8_t* __restrict__ gcand,
@@ -838,6 +838,11 @@ __global__ void __launch_bounds__(256) assign_multi_kernel(const TX* __restrict_
     const int nrows = *cnt_p;
     const bool blk = d > (int)BLAS_Q;
     unsigned long long nchg = 0, nstat = 0;
+    if ((((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) >= nrows) return;
+    double cc_max = 0.0;
+    for (int k = lane; k < K; k += 32) cc_max = fmax(cc_max, cc[k]);
+    for (int off = 16; off >= 1; off >>= 1) cc_max = fmax(cc_max, __shfl_xor_sync(FULL, cc_max, off));
+    const double sc_max = sqrt(cc_max) * (1.0 + 1e-12);
     for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nrows;
          w += ((long long)gridDim.x * blockDim.x) >> 5) {
         const long long r = rows[w];
@@ -845,10 +850,54 @@ __global__ void __launch_bounds__(256) assign_multi_kernel(const TX* __restrict_
         const TX* xr = X + r * ldx;
         double dv = __longlong_as_double(0x7ff0000000000000ULL);
         int kj = 0x7fffffff;
-        if (lane < cnt) {
+        const double xx = xx_in ? xx_in[r]
+                                : np_pw_sum([&](long long i) { double t = (double)xr[i]; return dmul(t, t); }, 0, d);
+        // Wide rows: the tensor-core bound grows with d ((4 d + 16) 2^-22), so many rows keep a
+        // few candidates whose exact d-long float64 chains are the cost of this kernel.  The
+        // candidates' values are first recomputed as warp-wide fp32 dots (ceil(d/32) FMAs per
+        // lane + a 5-level shuffle tree: bound E2 below) and the keep rule of the filter is
+        // applied again; a single survivor is the nearest codeword, no float64 dot at all.
+        unsigned keep = cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u);
+        if (d >= 96 && cnt >= 2) {
+            float w2[TC_CMAX];
+            float w2min = __int_as_float(0x7f800000);
+#pragma unroll 1
+            for (int j = 0; j < cnt; ++j) {
+                const int k = gcand[r * 8 + j];
+                const double* crow = C + (long long)k * ldc;
+                float dot = 0.f;
+                for (int i = lane; i < d; i += 32) dot = fmaf((float)xr[i], (float)crow[i], dot);
+                for (int off = 16; off >= 1; off >>= 1) dot += __shfl_xor_sync(FULL, dot, off);
+                const float wv = fmaf(-2.f, dot, (float)cc[k]);
+#pragma unroll
+                for (int q = 0; q < TC_CMAX; ++q) w2[q] = q == j ? wv : w2[q];
+                w2min = fminf(w2min, wv);
+            }
+            const double sx = sqrt(xx) * (1.0 + 1e-12);
+            const double u24 = 5.9604644775390625e-08;
+            const double steps = (double)((d + 31) / 32 + 5);
+            // operand roundings (2 u), the fp32 dot (steps u), cc and the final fma (2 u), the
+            // reference's float64 roundings; sc_max >= max ||c||, cc_max >= max ||c||^2
+            const double E2 = 2.0 * (steps + 4.0) * u24 * sx * sc_max * (1.0 + 1e-9) +
+                              2.0 * u24 * (cc_max + 2.0 * sx * sc_max) +
+                              8.8817841970012523e-16 * (xx + cc_max + 2.0 * sx * sc_max) + 1e-30;
+            const double ub = fmax(xx + (double)w2min + E2, 0.0);
+            unsigned kept = 0;
+#pragma unroll
+            for (int q = 0; q < TC_CMAX; ++q)
+                if (q < cnt && fmax(xx + (double)w2[q] - E2, 0.0) <= ub) kept |= 1u << q;
+            keep = kept;
+        }
+        if (__popc(keep) == 1) {   // decided without float64 work (warp-uniform)
+            kj = gcand[r * 8 + (__ffs(keep) - 1)];
+            if (lane == 0) {
+                labels[r] = kj;
+                if (prev != nullptr && prev[r] != kj) ++nchg;
+            }
+            continue;
+        }
+        if (lane < cnt && ((keep >> lane) & 1u)) {
             kj = gcand[r * 8 + lane];
-            const double xx = xx_in ? xx_in[r]
-                                    : np_pw_sum([&](long long i) { double t = (double)xr[i]; return dmul(t, t); }, 0, d);
             const double* crow = C + (long long)kj * ldc;
             const double xc = blk ? exact_xc<TX, true>(xr, crow, d) : exact_xc<TX, false>(xr, crow, d);
             dv = dadd(dsub(xx, dmul(2.0, xc)), cc[kj]);
@@ -861,7 +910,7 @@ __global__ void __launch_bounds__(256) assign_multi_kernel(const TX* __restrict_
         }
         if (lane == 0) {
             labels[r] = kj;
-            nstat += cnt;
+            nstat += __popc(keep);
             if (prev != nullptr && prev[r] != kj) ++nchg;
         }
     }
@@ -969,7 +1018,7 @@ int launch_assign_tc(const void* X, int x_is_f32, long long n, long long ldx, in
                                      gcnt, labels_only ? labels : nullptr, prev, changed, multi_rows);
         DA_CHECK_LAUNCH("assign_tc_kernel");
         if (labels_only)
-            assign_multi_kernel<float><<<sms, 256, 0, s>>>((const float*)X, ldx, d, C, ldc, cc, xx, gcand, gcnt,
+            assign_multi_kernel<float><<<sms, 256, 0, s>>>((const float*)X, ldx, d, C, ldc, K, cc, xx, gcand, gcnt,
                                                            multi_rows, ovf_cnt + 1, labels, prev, changed, stats);
         else
             assign_recheck_kernel<float><<<rgrid, 32 * RC_WARPS, 0, s>>>((const float*)X, n, ldx, d, C, ldc, cc, xx,
@@ -984,7 +1033,7 @@ int launch_assign_tc(const void* X, int x_is_f32, long long n, long long ldx, in
                                      gcnt, labels_only ? labels : nullptr, prev, changed, multi_rows);
         DA_CHECK_LAUNCH("assign_tc_kernel");
         if (labels_only)
-            assign_multi_kernel<double><<<sms, 256, 0, s>>>((const double*)X, ldx, d, C, ldc, cc, xx, gcand, gcnt,
+            assign_multi_kernel<double><<<sms, 256, 0, s>>>((const double*)X, ldx, d, C, ldc, K, cc, xx, gcand, gcnt,
                                                             multi_rows, ovf_cnt + 1, labels, prev, changed, stats);
         else
             assign_recheck_kernel<double><<<rgrid, 32 * RC_WARPS, 0, s>>>((const double*)X, n, ldx, d, C, ldc, cc, xx,
