@@ -237,11 +237,13 @@ int da_encode(const void* X, int x_f32, int64_t n, int64_t ldx, int D, const flo
               void* stream);
 
 /* Encoder selection (all modes return identical codes/errors):
- *   0 (default) = by beam width: 3 for L <= 2 or L >= 24, else 2 (measured crossover on
- *       B200, config B); 1 = plain float64 score tables;
- *   2 = fp32 score table (3xTF32 on tcgen05; FFMA when the shape does not fit) + fp32
- *       cross-table gathers as a filter with a rigorous error bound, exact float64
- *       recheck of the candidates that can still make the beam;
+ *   0 (default) = mode 2 at every beam width (it measured faster than mode 3 from L = 1 to
+ *       L = 32 on B200, config B); 1 = plain float64 score tables;
+ *   2 = fp32 score table on tcgen05 (tf32-exact rows: two MMAs per k step; otherwise 3xTF32;
+ *       rows wider than ~180 columns: the D-tiled streaming table at L = 1, a chunked FFMA
+ *       table at L >= 2) + fp32 cross-table gathers as a filter with a rigorous error bound
+ *       (greedy kernel at L = 1, two vectors per warp for 2 <= L <= 7, one per warp from
+ *       L = 8), exact float64 recheck of the candidates that can still make the beam;
  *   3 = tcgen05 filter: per stage one 3xTF32 GEMM of the beams' residuals against the
  *       dictionary (score = s + ||c||^2 - 2 r.c), same bound + exact recheck.
  * recheck_counter (device, optional) accumulates the number of exactly rechecked candidates. */
