@@ -484,7 +484,7 @@ def main():
         r = {"bound": "compute", "achieved": a, "unit": "TFLOP/s", "peak_ffma": ffma, "frac_ffma": a / ffma,
              "peak_3xtf32": tf32_peak / 3.0, "frac_3xtf32": a / (tf32_peak / 3.0),
              # /2 when x is exact in tf32 (integer config-B rows): the score table then runs two
-             # tf32 MMAs per k step (table_tc_x_kernel), so this is the tensor-core roof of the encode table
+             # tf32 MMAs per k step (table_tc_stream_kernel<true>), so this is the tensor-core roof of the encode table
              "peak_2xtf32": tf32_peak / 2.0, "frac_2xtf32": a / (tf32_peak / 2.0)}
         if extra:
             r.update(extra)

@@ -1000,398 +1000,27 @@ namespace da {
 
 // ---------------------------------------------------------------------------
 // Score table on the tensor cores: T[v][m*K + k] = ||c_mk||^2 - 2 x_v . c_mk (fp32,
-// 3xTF32 on tcgen05; the gather filter's input, encode_fast.cu).  One persistent
-// CTA per SM; per 128-row tile the [x, 1] rows are split into tf32 hi/lo once and
-// stay in shared memory for all M dictionaries; codeword chunks stream through a
-// 2-slot ring by bulk copy; two TMEM accumulators let dictionary m+1's MMAs run
-// while the threads store dictionary m's 128 x 256 block.
-__global__ void __launch_bounds__(256, 1) table_tc_kernel(const float* __restrict__ X, long long n, long long ldx,
-                                                           int D, int M, int K, int nch, const float* __restrict__ Bg,
-                                                           float* __restrict__ T, long long ldt,
-                                                           const int* __restrict__ inexact) {
-    if (inexact && *inexact == 0) return;                  // table_tc_x_kernel took this call
-    extern __shared__ __align__(1024) unsigned char smem[];
-    constexpr int A_EL = BT_ROWS * BT_BK, B_EL = BT_N * BT_BK;
-    float* Aimg = reinterpret_cast<float*>(smem);             // [nch][hi,lo][A_EL]
-    float* Bbuf = Aimg + (size_t)nch * 2 * A_EL;               // [2][hi,lo][B_EL]
-    __shared__ uint64_t full_bar[2], empty_bar[2], acc_bar[2];
-    __shared__ uint32_t tmem_sh;
-    const int tid = threadIdx.x, warp = tid >> 5;
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(bt_smem_u32(&tmem_sh)),
-                     "r"(2 * BT_N));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    if (tid == 0) {
-        for (int i = 0; i < 2; ++i) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&full_bar[i])));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&empty_bar[i])));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&acc_bar[i])));
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    const uint32_t tmem = tmem_sh;
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BT_N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-    const int row = tid & 127, half = tid >> 7;
-    const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(half * 128);
-    long long q = 0;            // B chunks streamed (ring phases)
-    long long nacc = 0;         // accumulator uses (acc_bar phases)
-    const long long ntiles = (n + 127) / 128;
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const long long r0 = tile * 128;
-        // [x, 1, 0...] rows -> tf32 hi/lo images (all chunks), one 4-wide group per step
-        for (int e = tid; e < 128 * nch * (BT_BK / 4); e += 256) {
-            const int rr = e / (nch * (BT_BK / 4)), rem = e % (nch * (BT_BK / 4));
-            const int ch = rem / (BT_BK / 4), c4 = rem % (BT_BK / 4);
-            const long long gr = r0 + rr;
-            const int k = ch * BT_BK + 4 * c4;
-            float x4[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int kk = k + u;
-                x4[u] = kk < D ? (gr < n ? X[gr * ldx + kk] : 0.f) : (kk == D ? 1.f : 0.f);
-            }
-            bt_store_split(Aimg + (size_t)ch * 2 * A_EL, bt_off(rr, 4 * c4) >> 2, x4);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        for (int m = 0; m <= M; ++m) {
-            if (m < M && tid == 0) {
-                // dictionary m into accumulator (nacc & 1)
-                const int b = (int)(nacc & 1);
-                const uint32_t dacc = tmem + (uint32_t)(b * BT_N);
-                constexpr uint32_t bytes_b = 2 * B_EL * sizeof(float);
-                auto issue = [&](int ch) {
-                    const long long qq = q + ch;
-                    const int st = (int)(qq & 1);
-                    if (qq >= 2) bt_wait(&empty_bar[st], (uint32_t)(((qq >> 1) - 1) & 1));
-                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bt_smem_u32(&full_bar[st])),
-                                 "r"(bytes_b)
-                                 : "memory");
-                    bt_bulk(Bbuf + st * 2 * B_EL, Bg + ((size_t)m * nch + ch) * 2 * B_EL, bytes_b, &full_bar[st]);
-                };
-                issue(0);
-                for (int ch = 0; ch < nch; ++ch) {
-                    if (ch + 1 < nch) issue(ch + 1);
-                    const long long qq = q + ch;
-                    const int st = (int)(qq & 1);
-                    bt_wait(&full_bar[st], (uint32_t)((qq >> 1) & 1));
-                    asm volatile("tcgen05.fence::after_thread_sync;");
-                    const uint32_t ah = bt_smem_u32(Aimg + (size_t)ch * 2 * A_EL), al = ah + A_EL * 4;
-                    const uint32_t bh = bt_smem_u32(Bbuf + st * 2 * B_EL), bl = bh + B_EL * 4;
-#pragma unroll
-                    for (int s2 = 0; s2 < BT_BK / 8; ++s2) {
-                        const uint32_t off = (uint32_t)s2 * 256;
-                        const uint32_t acc0 = (ch > 0 || s2 > 0) ? 1u : 0u;
-                        bt_mma(dacc, bt_desc(ah + off), bt_desc(bh + off), idesc, acc0);
-                        bt_mma(dacc, bt_desc(ah + off), bt_desc(bl + off), idesc, 1u);
-                        bt_mma(dacc, bt_desc(al + off), bt_desc(bh + off), idesc, 1u);
-                    }
-                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                     bt_smem_u32(&empty_bar[st]))
-                                 : "memory");
-                }
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                 bt_smem_u32(&acc_bar[b]))
-                             : "memory");
-            }
-            __syncwarp();
-            if (m < M) { q += nch; }
-            // store dictionary m-1 (previous accumulator) while dictionary m multiplies
-            if (m > 0) {
-                const long long u = nacc - 1;
-                const int b = (int)(u & 1);
-                bt_wait(&acc_bar[b], (uint32_t)((u >> 1) & 1));
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                const long long gr = r0 + row;
-                float* trow = T + gr * ldt + (long long)(m - 1) * K + half * 128;
-#pragma unroll 1
-                for (int c0 = 0; c0 < 128; c0 += 32) {
-                    float v[32];
-                    bt_ld32(taddr + (uint32_t)(b * BT_N) + c0, v);
-                    if (gr < n) {
-                        if ((K & 3) == 0 && half * 128 + c0 + 32 <= K) {
-#pragma unroll
-                            for (int i = 0; i < 32; i += 4)
-                                __stcs(reinterpret_cast<float4*>(trow + c0 + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
-                        } else {
-#pragma unroll
-                            for (int i = 0; i < 32; ++i)
-                                if (half * 128 + c0 + i < K) trow[c0 + i] = v[i];
-                        }
-                    }
-                }
-            }
-            if (m < M) ++nacc;
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            __syncthreads();   // accumulator of m-1 drained before it is reused by m+1
-            asm volatile("tcgen05.fence::after_thread_sync;");
-        }
-    }
-    __syncthreads();
-    if (warp == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BT_N));
-    }
-}
-
-// Score table for tf32-exact inputs (every x equals its tf32 rounding: integer
-// data such as configs B/D/E).  Then x = hi exactly and 3xTF32 needs only
-// x.c_hi + x.c_lo -- two MMAs per k step instead of three, no lo image -- and
-// the fp32 rows themselves are the A operand: they are copied into the
-// canonical K-major layout with 16-byte cp.async, double-buffered, so the next
-// tile's rows arrive while this tile's dictionaries multiply and store.  The
-// error bound is table_err(1, ...) (the dropped x_lo terms are zero).  A
-// pre-pass (tf32_inexact_kernel) sets *inexact; this kernel exits when it is set
-// and table_tc_kernel (launched after it) takes the call instead.
-__global__ void tf32_inexact_kernel(const float* __restrict__ X, long long n, long long ldx, int D,
-                                    int* __restrict__ inexact) {
-    // 16-byte loads (D % 4 == 0 and aligned rows: the caller's x_ok), 32 rows per block pass
-    const int d4 = D >> 2;
-    bool bad = false;
-    for (long long r0 = (long long)blockIdx.x * 32; r0 < n; r0 += (long long)gridDim.x * 32) {
-        for (int e = threadIdx.x; e < 32 * d4; e += blockDim.x) {
-            const int rr = e / d4, c4 = e - rr * d4;
-            if (r0 + rr >= n) break;
-            const float4 v = __ldg(reinterpret_cast<const float4*>(X + (r0 + rr) * ldx) + c4);
-            bad |= (bt_tf32(v.x) != v.x) | (bt_tf32(v.y) != v.y) | (bt_tf32(v.z) != v.z) | (bt_tf32(v.w) != v.w);
-        }
-    }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(inexact, 1);
-}
-
-__device__ __forceinline__ void tx_cp16(uint32_t sdst, const void* gsrc) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst), "l"(gsrc) : "memory");
-}
-
-// Warp-specialised: warps 0-7 stage rows (16-byte cp.async into the canonical
-// layout, double-buffered) and drain accumulators (TMEM -> fp32 table rows);
-// warp 8 streams codeword chunks (bulk copies, 2-slot ring) and issues the MMAs.
-// Everything is ordered by mbarriers, so dictionary m+1 multiplies while m is
-// stored and tile t+1's rows land while tile t multiplies.
-constexpr int TX_EPI = 256;                 // epilogue / staging threads
-constexpr int TX_T = TX_EPI + 32;           // + the producer warp
-constexpr int TX_NS = 2;                    // codeword-chunk ring depth
-__global__ void __launch_bounds__(TX_T, 1) table_tc_x_kernel(const float* __restrict__ X, long long n, long long ldx,
-                                                            int D, int M, int K, int nch, const float* __restrict__ Bg,
-                                                            float* __restrict__ T, long long ldt,
-                                                            const int* __restrict__ inexact, const double* __restrict__ sq,
-                                                            int nch_img) {
-    if (*inexact) return;                                  // table_tc_kernel handles this call
-    extern __shared__ __align__(1024) unsigned char smem[];
-    constexpr int A_EL = BT_ROWS * BT_BK, B_EL = BT_N * BT_BK;
-    float* Aimg = reinterpret_cast<float*>(smem);             // [2][nch][A_EL] (raw x, no lo image)
-    float* Bbuf = Aimg + (size_t)2 * nch * A_EL;               // [TX_NS][hi,lo][B_EL]
-    float* Xpose = Bbuf + (size_t)TX_NS * 2 * B_EL;             // [8 warps][32 x 32] store transpose
-    __shared__ uint64_t full_bar[TX_NS], empty_bar[TX_NS], acc_full[2], acc_empty[2], a_full[2], a_empty[2];
-    __shared__ uint32_t tmem_sh;
-    const int tid = threadIdx.x, warp = tid >> 5;
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(bt_smem_u32(&tmem_sh)),
-                     "r"(2 * BT_N));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    if (tid == 0) {
-        for (int i = 0; i < TX_NS; ++i) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&full_bar[i])));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&empty_bar[i])));
-        }
-        for (int i = 0; i < 2; ++i) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&acc_full[i])));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bt_smem_u32(&acc_empty[i])), "r"(TX_EPI));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bt_smem_u32(&a_full[i])), "r"(TX_EPI));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&a_empty[i])));
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    // padding columns of both buffers (k >= D) are zero: the codeword norms are
-    // added in the epilogue, so no norm column is multiplied
-    const int kpad = nch * BT_BK, d4 = D >> 2;
-    for (int e = tid; e < 2 * BT_ROWS * (kpad - D); e += TX_T) {
-        const int buf = e / (BT_ROWS * (kpad - D)), rem = e % (BT_ROWS * (kpad - D));
-        const int rr = rem / (kpad - D), k = D + rem % (kpad - D);
-        const int ch = k / BT_BK;
-        Aimg[((size_t)buf * nch + ch) * A_EL + (bt_off(rr, k - ch * BT_BK) >> 2)] = 0.f;
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    const uint32_t tmem = tmem_sh;
-    const long long ntiles = (n + 127) / 128;
-    long long my_tiles = 0;
-    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) ++my_tiles;
-
-    if (warp == TX_EPI / 32) {
-        // ---------------- producer: codeword chunks + MMAs
-        if ((tid & 31) == 0) {
-            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BT_N >> 3) << 17) |
-                                   ((uint32_t)(128 >> 4) << 24);
-            constexpr uint32_t bytes_b = 2 * B_EL * sizeof(float);
-            long long q = 0, nacc = 0;
-            for (long long it = 0; it < my_tiles; ++it) {
-                const int buf = (int)(it & 1);
-                bt_wait(&a_full[buf], (uint32_t)((it >> 1) & 1));
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                for (int m = 0; m < M; ++m, ++nacc) {
-                    const int b = (int)(nacc & 1);
-                    if (nacc >= 2) bt_wait(&acc_empty[b], (uint32_t)(((nacc >> 1) - 1) & 1));
-                    asm volatile("tcgen05.fence::after_thread_sync;");
-                    const uint32_t dacc = tmem + (uint32_t)(b * BT_N);
-                    auto issue = [&](int ch) {
-                        const long long qq = q + ch;
-                        const int st = (int)(qq % TX_NS);
-                        if (qq >= TX_NS) bt_wait(&empty_bar[st], (uint32_t)(((qq / TX_NS) - 1) & 1));
-                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                                         bt_smem_u32(&full_bar[st])),
-                                     "r"(bytes_b)
-                                     : "memory");
-                        bt_bulk(Bbuf + st * 2 * B_EL, Bg + ((size_t)m * nch_img + ch) * 2 * B_EL, bytes_b, &full_bar[st]);
-                    };
-                    for (int ch = 0; ch < TX_NS - 1 && ch < nch; ++ch) issue(ch);
-                    for (int ch = 0; ch < nch; ++ch) {
-                        if (ch + TX_NS - 1 < nch) issue(ch + TX_NS - 1);
-                        const long long qq = q + ch;
-                        const int st = (int)(qq % TX_NS);
-                        bt_wait(&full_bar[st], (uint32_t)((qq / TX_NS) & 1));
-                        asm volatile("tcgen05.fence::after_thread_sync;");
-                        const uint32_t ah = bt_smem_u32(Aimg + ((size_t)buf * nch + ch) * A_EL);
-                        const uint32_t bh = bt_smem_u32(Bbuf + st * 2 * B_EL), bl = bh + B_EL * 4;
-#pragma unroll
-                        for (int s2 = 0; s2 < BT_BK / 8; ++s2) {
-                            const uint32_t off = (uint32_t)s2 * 256;
-                            const uint32_t acc0 = (ch > 0 || s2 > 0) ? 1u : 0u;
-                            bt_mma(dacc, bt_desc(ah + off), bt_desc(bh + off), idesc, acc0);
-                            bt_mma(dacc, bt_desc(ah + off), bt_desc(bl + off), idesc, 1u);
-                        }
-                        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                         bt_smem_u32(&empty_bar[st]))
-                                     : "memory");
-                    }
-                    q += nch;
-                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                     bt_smem_u32(&acc_full[b]))
-                                 : "memory");
-                }
-                // every MMA of this tile read buffer `buf`: free it for the tile after next
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                 bt_smem_u32(&a_empty[buf]))
-                             : "memory");
-            }
-        }
-        __syncwarp();
-    } else {
-        // ---------------- staging + epilogue
-        const int row = tid & 127, half = tid >> 7;
-        const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(half * 128);
-        auto stage = [&](long long tile, int buf) {
-            const long long r0 = tile * 128;
-            for (int e = tid; e < 128 * d4; e += TX_EPI) {
-                const int rr = e / d4, g4 = e - rr * d4;
-                const long long gr = r0 + rr;
-                if (gr >= n) continue;
-                const int k = 4 * g4, ch = k / BT_BK;
-                const uint32_t dst = bt_smem_u32(Aimg + ((size_t)buf * nch + ch) * A_EL) + bt_off(rr, k - ch * BT_BK);
-                tx_cp16(dst, X + gr * ldx + k);
-            }
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        };
-        auto publish = [&](int buf) {   // this thread's rows landed: visible to the tensor cores
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bt_smem_u32(&a_full[buf])) : "memory");
-        };
-        if (my_tiles > 0) {
-            stage(blockIdx.x, 0);
-            publish(0);
-        }
-        long long nacc = 0;
-        for (long long it = 0; it < my_tiles; ++it) {
-            const int buf = (int)(it & 1);
-            const long long tile = blockIdx.x + it * gridDim.x;
-            const bool more = it + 1 < my_tiles;
-            if (more) {
-                if (it >= 1) bt_wait(&a_empty[buf ^ 1], (uint32_t)(((it - 1) >> 1) & 1));
-                stage(tile + gridDim.x, buf ^ 1);
-            }
-            const long long gr = tile * 128 + row;
-            for (int m = 0; m < M; ++m, ++nacc) {
-                const int b = (int)(nacc & 1);
-                bt_wait(&acc_full[b], (uint32_t)((nacc >> 1) & 1));
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                // TMEM gives a lane one row (32 columns per load); rows are 8 KB apart in
-                // the table, so the 32 x 32 block goes through a swizzled shared tile and
-                // leaves as 4 full 128-byte row segments per store instruction
-                const double* sqm = sq + (long long)m * K + half * 128;
-                float* xp = Xpose + (size_t)warp * 1024;
-                const int lane = tid & 31;
-                const long long wrow0 = tile * 128 + (warp & 3) * 32;   // first row of this warp's lanes
-#pragma unroll 1
-                for (int c0 = 0; c0 < 128; c0 += 32) {
-                    float v[32];
-                    bt_ld32(taddr + (uint32_t)(b * BT_N) + c0, v);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        *reinterpret_cast<float4*>(xp + lane * 32 + ((j ^ (lane & 7)) << 2)) =
-                            make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-                    __syncwarp();
-                    const int cj = lane & 7, col = half * 128 + c0 + 4 * cj;
-                    float4 nrm = make_float4(0.f, 0.f, 0.f, 0.f);   // + ||c||^2: one fp32 rounding (table_err slack)
-                    if (col < K) nrm.x = (float)__ldg(sqm + c0 + 4 * cj);
-                    if (col + 1 < K) nrm.y = (float)__ldg(sqm + c0 + 4 * cj + 1);
-                    if (col + 2 < K) nrm.z = (float)__ldg(sqm + c0 + 4 * cj + 2);
-                    if (col + 3 < K) nrm.w = (float)__ldg(sqm + c0 + 4 * cj + 3);
-#pragma unroll
-                    for (int rb = 0; rb < 32; rb += 4) {
-                        const int r = rb + (lane >> 3);
-                        float4 w = *reinterpret_cast<const float4*>(xp + r * 32 + ((cj ^ (r & 7)) << 2));
-                        w.x = __fadd_rn(w.x, nrm.x); w.y = __fadd_rn(w.y, nrm.y);
-                        w.z = __fadd_rn(w.z, nrm.z); w.w = __fadd_rn(w.w, nrm.w);
-                        const long long g = wrow0 + r;
-                        if (g < n) {
-                            float* dst = T + g * ldt + (long long)m * K + col;
-                            if ((K & 3) == 0 && col + 3 < K) __stcs(reinterpret_cast<float4*>(dst), w);
-                            else {
-                                if (col < K) dst[0] = w.x;
-                                if (col + 1 < K) dst[1] = w.y;
-                                if (col + 2 < K) dst[2] = w.z;
-                                if (col + 3 < K) dst[3] = w.w;
-                            }
-                        }
-                    }
-                    __syncwarp();
-                }
-                asm volatile("tcgen05.fence::before_thread_sync;");
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bt_smem_u32(&acc_empty[b])) : "memory");
-            }
-            if (more) publish(buf ^ 1);
-        }
-    }
-    __syncthreads();
-    if (warp == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BT_N));
-    }
-}
-
-// ---------------------------------------------------------------------------
-// D-tiled score table (D too wide for a resident row-tile image: config C,
-// D = 960).  A pre-pass writes the [x, 1, 0..] rows of every 128-row tile as
-// tf32 hi/lo images in the canonical K-major layout, one 16-KB block per
-// (tile, 16-wide k chunk); the table kernel then streams (A chunk, B chunk)
-// pairs through a shared-memory ring by bulk copy -- nothing is staged by
-// threads -- and accumulates the 3xTF32 product over all chunks in TMEM.
-// Warp roles: warp 8 loads, warp 9 issues the MMAs (so a slot refill never
-// delays the next chunk's MMAs), warps 0-7 drain accumulators into the table.
-// A work item is (row tile, group of dictionaries); the `msplit` items of a
-// tile run on neighbouring CTAs at the same time, so the tile's image is read
-// from HBM about once and from L2 after that (148 whole-tile images would not
-// fit L2 at D = 960).
+// 3xTF32 on tcgen05, or two MMAs per k step for tf32-exact rows; the gather
+// filter's input, encode_fast.cu / encode_greedy.cu / encode_pair.cu).
+//
+// Both operands stream: a pre-pass writes the [x, 1, 0..] rows of every 128-row
+// tile as tf32 hi/lo images in the canonical K-major layout, one 16-KB block per
+// (tile, 16-wide k chunk), and flags rows that are not tf32-exact; the table
+// kernel then moves (row chunk, codeword chunk) pairs through a shared-memory
+// ring by bulk copy -- nothing is staged by threads -- and accumulates over all
+// chunks in TMEM.  Warp roles: warp 8 loads, warp 9 issues the MMAs (so a slot
+// refill never delays the next chunk's MMAs), warps 0-7 drain accumulators into
+// the table through a swizzled transpose (full 128-byte row segments).  A work
+// item is (row tile, group of dictionaries); the `msplit` items of a tile run on
+// neighbouring CTAs at the same time, so the tile's image is read from HBM about
+// once and from L2 after that (148 whole-tile images would not fit L2 at D = 960).
+// Round 2 replaced two resident-image kernels (whole tile image in shared memory,
+// 2-slot codeword ring, tensor pipe 28 % busy) with this one at every D.
 __global__ void a_tf32_img_kernel(const float* __restrict__ X, long long n, long long ldx, int D, int nch,
-                                  long long ntiles, float* __restrict__ out) {
+                                  long long ntiles, float* __restrict__ out, int* __restrict__ inexact) {
+    // *inexact (optional) is set when some x differs from its tf32 rounding (a nonzero lo
+    // part): the two-MMA table kernel then leaves the call to the three-MMA one
+    bool bad = false;
     constexpr int A_EL = BT_ROWS * BT_BK;
     const bool v4 = (D & 3) == 0 && (ldx & 3) == 0 && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
     const long long total = ntiles * nch * (long long)(BT_ROWS * (BT_BK / 4));
@@ -1419,18 +1048,30 @@ __global__ void a_tf32_img_kernel(const float* __restrict__ X, long long n, long
             }
         }
         bt_store_split(out + (size_t)tc * 2 * A_EL, bt_off(rr, 4 * c4) >> 2, x4);
+        bad |= (bt_tf32(x4[0]) != x4[0]) | (bt_tf32(x4[1]) != x4[1]) | (bt_tf32(x4[2]) != x4[2]) |
+               (bt_tf32(x4[3]) != x4[3]);
     }
+    if (inexact != nullptr && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0 &&
+        *reinterpret_cast<volatile int*>(inexact) == 0)
+        atomicOr(inexact, 1);
 }
 
 constexpr int TS_EPI = 256;            // epilogue threads (warps 0-7)
 constexpr int TS_T = TS_EPI + 64;      // + loader warp + MMA warp
-constexpr int TS_NS = 4;               // ring slots of one (A chunk, B chunk) pair: 48 KB each
+constexpr int TS_NS = 4;               // ring slots of one (A chunk, B chunk) pair: 48 KB each (40 KB when EXACT)
+// EXACT: tf32-exact rows (integer data such as configs B/D/E): x_lo = 0, so the slots carry
+// only the hi image and a k step is two MMAs (x.c_hi + x.c_lo) instead of three.  *flag is the
+// image kernel's inexactness flag: each instance runs only when the rows are its kind.
+template <bool EXACT>
 __global__ void __launch_bounds__(TS_T, 1) table_tc_stream_kernel(const float* __restrict__ Ag, long long n, int M, int K,
                                                                  int nch, const float* __restrict__ Bg,
-                                                                 float* __restrict__ T, long long ldt, int msplit) {
+                                                                 float* __restrict__ T, long long ldt, int msplit,
+                                                                 const int* __restrict__ flag) {
+    if (flag != nullptr && (*flag != 0) == EXACT) return;
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int A_EL = BT_ROWS * BT_BK, B_EL = BT_N * BT_BK;
-    constexpr int SLOT = 2 * A_EL + 2 * B_EL;                  // floats per ring slot: A hi, A lo, B hi, B lo
+    constexpr int A_PART = EXACT ? A_EL : 2 * A_EL;            // floats of the row image per slot
+    constexpr int SLOT = A_PART + 2 * B_EL;                    // floats per ring slot: A hi (, A lo), B hi, B lo
     float* ring = reinterpret_cast<float*>(smem);
     float* Xpose = ring + (size_t)TS_NS * SLOT;                 // [8 warps][32 x 32] store transpose
     __shared__ uint64_t full_bar[TS_NS], empty_bar[TS_NS], acc_full[2], acc_empty[2];
@@ -1465,7 +1106,7 @@ __global__ void __launch_bounds__(TS_T, 1) table_tc_stream_kernel(const float* _
     if (warp == TS_EPI / 32) {
         // ---------------- loader: (A chunk, B chunk) pairs into the ring
         if ((tid & 31) == 0) {
-            constexpr uint32_t bytes_a = 2 * A_EL * sizeof(float), bytes_b = 2 * B_EL * sizeof(float);
+            constexpr uint32_t bytes_a = A_PART * sizeof(float), bytes_b = 2 * B_EL * sizeof(float);
             long long q = 0;
             for (long long it = 0; it < my_items; ++it) {
                 const long long item = blockIdx.x + it * gridDim.x;
@@ -1481,7 +1122,7 @@ __global__ void __launch_bounds__(TS_T, 1) table_tc_stream_kernel(const float* _
                                      : "memory");
                         float* slot = ring + (size_t)st * SLOT;
                         bt_bulk(slot, Ag + ((size_t)tile * nch + ch) * 2 * A_EL, bytes_a, &full_bar[st]);
-                        bt_bulk(slot + 2 * A_EL, Bg + ((size_t)m * nch + ch) * 2 * B_EL, bytes_b, &full_bar[st]);
+                        bt_bulk(slot + A_PART, Bg + ((size_t)m * nch + ch) * 2 * B_EL, bytes_b, &full_bar[st]);
                     }
                 }
             }
@@ -1506,14 +1147,14 @@ __global__ void __launch_bounds__(TS_T, 1) table_tc_stream_kernel(const float* _
                         bt_wait(&full_bar[st], (uint32_t)((q / TS_NS) & 1));
                         asm volatile("tcgen05.fence::after_thread_sync;");
                         const uint32_t ah = bt_smem_u32(ring + (size_t)st * SLOT), al = ah + A_EL * 4;
-                        const uint32_t bh = ah + 2 * A_EL * 4, bl = bh + B_EL * 4;
+                        const uint32_t bh = ah + A_PART * 4, bl = bh + B_EL * 4;
 #pragma unroll
                         for (int s2 = 0; s2 < BT_BK / 8; ++s2) {
                             const uint32_t off = (uint32_t)s2 * 256;
                             const uint32_t acc0 = (ch > 0 || s2 > 0) ? 1u : 0u;
                             bt_mma(dacc, bt_desc(ah + off), bt_desc(bh + off), idesc, acc0);
                             bt_mma(dacc, bt_desc(ah + off), bt_desc(bl + off), idesc, 1u);
-                            bt_mma(dacc, bt_desc(al + off), bt_desc(bh + off), idesc, 1u);
+                            if (!EXACT) bt_mma(dacc, bt_desc(al + off), bt_desc(bh + off), idesc, 1u);
                         }
                         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                                          bt_smem_u32(&empty_bar[st]))
@@ -1583,7 +1224,7 @@ __global__ void __launch_bounds__(TS_T, 1) table_tc_stream_kernel(const float* _
 }
 
 static int launch_table_tc_stream(const float* X, long long n, long long ldx, int D, const float* cw, const double* sq,
-                                  int M, int K, int nch, float* T, long long ldt, cudaStream_t s) {
+                                  int M, int K, int nch, float* T, long long ldt, cudaStream_t s, bool try_exact) {
     constexpr size_t A_EL = (size_t)BT_ROWS * BT_BK, B_EL = (size_t)BT_N * BT_BK;
     const long long ntiles = (n + BT_ROWS - 1) / BT_ROWS;
     float* Bg = (float*)scratch(14, sizeof(float) * (size_t)M * nch * 2 * B_EL, s);
@@ -1591,8 +1232,15 @@ static int launch_table_tc_stream(const float* X, long long n, long long ldx, in
     if (!Bg || !Ag) return fail_cuda(cudaErrorMemoryAllocation, "table_tc_stream scratch");
     cb_tf32_prep_kernel<<<grid_for((long long)M * nch * BT_N * BT_BK, 256, 4096), 256, 0, s>>>(cw, sq, M, K, D, nch, Bg);
     DA_CHECK_LAUNCH("cb_tf32_prep_kernel(stream)");
-    a_tf32_img_kernel<<<grid_for(ntiles * nch * (long long)(BT_ROWS * (BT_BK / 4)), 256, 1 << 16), 256, 0, s>>>(
-        X, n, ldx, D, nch, ntiles, Ag);
+    int* flag = nullptr;
+    if (try_exact) {
+        flag = (int*)scratch(15, sizeof(int), s);
+        if (!flag) return fail_cuda(cudaErrorMemoryAllocation, "table_tc flag");
+        DA_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
+    }
+    // a few thousand blocks with grid-stride loops: one flag check per warp at the end of its loop
+    a_tf32_img_kernel<<<grid_for(ntiles * nch * (long long)(BT_ROWS * (BT_BK / 4)), 256, 148 * 32), 256, 0, s>>>(
+        X, n, ldx, D, nch, ntiles, Ag, flag);
     DA_CHECK_LAUNCH("a_tf32_img_kernel");
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -1602,57 +1250,30 @@ static int launch_table_tc_stream(const float* X, long long n, long long ldx, in
     const size_t smem = sizeof(float) * ((size_t)TS_NS * (2 * A_EL + 2 * B_EL) + 8 * 1024);
     static bool attr_set = false;
     if (!attr_set) {
-        DA_CUDA(cudaFuncSetAttribute(table_tc_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        DA_CUDA(cudaFuncSetAttribute(table_tc_stream_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        DA_CUDA(cudaFuncSetAttribute(table_tc_stream_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = true;
     }
     const int grid = (int)std::min<long long>(ntiles * msplit, sms);
-    table_tc_stream_kernel<<<grid, TS_T, smem, s>>>(Ag, n, M, K, nch, Bg, T, ldt, msplit);
+    if (try_exact) {   // both instances are launched; the image kernel's flag picks one (no host sync)
+        table_tc_stream_kernel<true><<<grid, TS_T, smem, s>>>(Ag, n, M, K, nch, Bg, T, ldt, msplit, flag);
+        DA_CHECK_LAUNCH("table_tc_stream_kernel<exact>");
+    }
+    table_tc_stream_kernel<false><<<grid, TS_T, smem, s>>>(Ag, n, M, K, nch, Bg, T, ldt, msplit, flag);
     DA_CHECK_LAUNCH("table_tc_stream_kernel");
     return 0;
 }
 
-// Returns kNotApplicable when the shape does not fit (K > 256, or the row tile's
-// operand image exceeds shared memory and `stream_ok` is 0); the caller then
-// uses the FFMA table.
+// Returns kNotApplicable when the shape does not fit (K > 256) or, for rows too wide
+// for the tight bound (D > ~143: 6 accumulation steps per 16 columns), when the caller
+// prefers the chunked FFMA table (`stream_ok` = 0; the caller's beam kernel then sees
+// fewer exact rechecks).
 int launch_table_tc(const float* X, long long n, long long ldx, int D, const float* cw, const double* sq, int M, int K,
                     float* T, long long ldt, cudaStream_t s, int stream_ok) {
     if (K > BT_N || K < 1 || n <= 0) return n <= 0 ? 0 : kNotApplicable;
     const int nch = (D + 1 + BT_BK - 1) / BT_BK;
-    const size_t smem = sizeof(float) * ((size_t)nch * 2 * BT_ROWS * BT_BK + 2 * 2 * (size_t)BT_N * BT_BK);
-    if (smem > 220 * 1024) {
-        if (!stream_ok) return kNotApplicable;
-        return launch_table_tc_stream(X, n, ldx, D, cw, sq, M, K, nch, T, ldt, s);
-    }
-    float* Bg = (float*)scratch(14, sizeof(float) * (size_t)M * nch * 2 * BT_N * BT_BK, s);
-    if (!Bg) return fail_cuda(cudaErrorMemoryAllocation, "table_tc scratch");
-    cb_tf32_prep_kernel<<<grid_for((long long)M * nch * BT_N * BT_BK, 256, 4096), 256, 0, s>>>(cw, sq, M, K, D, nch, Bg);
-    DA_CHECK_LAUNCH("cb_tf32_prep_kernel(table)");
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = (int)std::min<long long>((n + 127) / 128, sms);
-    // tf32-exact rows (integer data): the two-MMA kernel with async row staging;
-    // both kernels are launched and the pre-pass flag picks one (no host sync)
-    int* inexact = nullptr;
-    const int nch_x = (D + BT_BK - 1) / BT_BK;   // no norm column: the epilogue adds ||c||^2
-    const size_t smem_x = sizeof(float) * ((size_t)2 * nch_x * BT_ROWS * BT_BK + TX_NS * 2 * (size_t)BT_N * BT_BK +
-                                           8 * 1024);
-    const bool x_ok = (D & 3) == 0 && (ldx & 3) == 0 && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) &&
-                      smem_x <= 227 * 1024 - 512 && getenv("DA_TABLE_X") == nullptr;
-    if (x_ok) {
-        inexact = (int*)scratch(15, sizeof(int), s);
-        if (!inexact) return fail_cuda(cudaErrorMemoryAllocation, "table_tc flag");
-        DA_CUDA(cudaMemsetAsync(inexact, 0, sizeof(int), s));
-        tf32_inexact_kernel<<<(unsigned)std::min<long long>((n + 31) / 32, 4L * sms), 256, 0, s>>>(X, n, ldx, D, inexact);
-        DA_CHECK_LAUNCH("tf32_inexact_kernel");
-        DA_CUDA(cudaFuncSetAttribute(table_tc_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_x));
-        table_tc_x_kernel<<<grid, TX_T, smem_x, s>>>(X, n, ldx, D, M, K, nch_x, Bg, T, ldt, inexact, sq, nch);
-        DA_CHECK_LAUNCH("table_tc_x_kernel");
-    }
-    DA_CUDA(cudaFuncSetAttribute(table_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    table_tc_kernel<<<grid, 256, smem, s>>>(X, n, ldx, D, M, K, nch, Bg, T, ldt, inexact);
-    DA_CHECK_LAUNCH("table_tc_kernel");
-    return 0;
+    if (nch > 9 && !stream_ok) return kNotApplicable;
+    return launch_table_tc_stream(X, n, ldx, D, cw, sq, M, K, nch, T, ldt, s, true);
 }
 
 }  // namespace da

@@ -6,12 +6,12 @@ timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest.log 2>&1; echo
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
 # launch list of the timed encode kernels (cold-cache, serialised: shares only)
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"beam_fast|table_tc|sgemm_table|bound_prep|cb_tf32_prep|greedy|beam_pair" -c 60 --csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"beam_fast|table_tc|a_tf32_img|sgemm_table|bound_prep|cb_tf32_prep|greedy|beam_pair" -c 60 --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-anneal --no-cpu --no-adc --no-atree > gpurun_out/ncu_launch.log 2>&1; echo "launch rc=$?"
 # full captures: L=10 beam kernel, tcgen05 score table, L=1 greedy kernel, ADC scan
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:beam_fast -c 1 -o gpurun_out/prof_beam_fast -f \
     python tools/prof_tc.py 2 10 > gpurun_out/ncu_bf.log 2>&1; echo "full bf rc=$?"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"table_tc_x|greedy" -c 2 -o gpurun_out/prof_l1 -f \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"table_tc_stream|a_tf32_img|greedy" -c 4 -o gpurun_out/prof_l1 -f \
     python tools/prof_tc.py 2 1 > gpurun_out/ncu_l1.log 2>&1; echo "full l1 rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:adc_scan_packed -c 1 -o gpurun_out/prof_adc -f \
     python tools/bench_adc.py 100000000 2000 100000 > gpurun_out/ncu_adc.log 2>&1; echo "full adc rc=$?"
