@@ -1062,18 +1062,37 @@ constexpr int TS_NS = 4;               // ring slots of one (A chunk, B chunk) p
 // EXACT: tf32-exact rows (integer data such as configs B/D/E): x_lo = 0, so the slots carry
 // only the hi image and a k step is two MMAs (x.c_hi + x.c_lo) instead of three.  *flag is the
 // image kernel's inexactness flag: each instance runs only when the rows are its kind.
-template <bool EXACT>
-__global__ void __launch_bounds__(TS_T, 1) table_tc_stream_kernel(const float* __restrict__ Ag, long long n, int M, int K,
-                                                                 int nch, const float* __restrict__ Bg,
-                                                                 float* __restrict__ T, long long ldt, int msplit,
-                                                                 const int* __restrict__ flag) {
-    if (flag != nullptr && (*flag != 0) == EXACT) return;
+// CL = 2: launched as clusters of two CTAs that work on two row tiles with the same dictionary
+// group in lockstep.  Each CTA fetches half of every codeword chunk and multicasts it into both
+// CTAs' rings (the chunk crosses L2 -> SM once per pair); a slot is refilled only after both
+// CTAs' MMAs on it retire (multicast commit onto both `empty` barriers, count 2).
+// Q = threads per row in the epilogue (2 or 4: 8 or 16 epilogue warps; 16 measured no faster).
+__device__ __forceinline__ void bt_bulk_mc(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(
+            bt_smem_u32(dst_smem)),
+        "l"(src), "r"(bytes), "r"(bt_smem_u32(bar)), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void bt_cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <bool EXACT, int CL, int Q>
+__global__ void __launch_bounds__(128 * Q + 64, 1) table_tc_stream_kernel(const float* __restrict__ Ag, long long n, int M,
+                                                                        int K, int nch, const float* __restrict__ Bg,
+                                                                        float* __restrict__ T, long long ldt, int msplit,
+                                                                        const int* __restrict__ flag) {
+    if (flag != nullptr && (*flag != 0) == EXACT) return;   // uniform over the grid (and over a cluster)
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int A_EL = BT_ROWS * BT_BK, B_EL = BT_N * BT_BK;
     constexpr int A_PART = EXACT ? A_EL : 2 * A_EL;            // floats of the row image per slot
     constexpr int SLOT = A_PART + 2 * B_EL;                    // floats per ring slot: A hi (, A lo), B hi, B lo
+    constexpr int TS_EPI = 128 * Q;                            // epilogue threads (shadows the 8-warp constant)
+    constexpr int QC = BT_N / Q;                               // table columns per epilogue thread
     float* ring = reinterpret_cast<float*>(smem);
-    float* Xpose = ring + (size_t)TS_NS * SLOT;                 // [8 warps][32 x 32] store transpose
+    float* Xpose = ring + (size_t)TS_NS * SLOT;                 // [4 Q warps][32 x 32] store transpose
     __shared__ uint64_t full_bar[TS_NS], empty_bar[TS_NS], acc_full[2], acc_empty[2];
     __shared__ uint32_t tmem_sh;
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -1085,7 +1104,7 @@ __global__ void __launch_bounds__(TS_T, 1) table_tc_stream_kernel(const float* _
     if (tid == 0) {
         for (int i = 0; i < TS_NS; ++i) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&full_bar[i])));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&empty_bar[i])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bt_smem_u32(&empty_bar[i])), "r"(CL));
         }
         for (int i = 0; i < 2; ++i) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bt_smem_u32(&acc_full[i])));
@@ -1096,12 +1115,18 @@ __global__ void __launch_bounds__(TS_T, 1) table_tc_stream_kernel(const float* _
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
+    if (CL > 1) bt_cluster_sync();   // the peer's barriers exist before anything is multicast at them
     const uint32_t tmem = tmem_sh;
     const long long ntiles = (n + BT_ROWS - 1) / BT_ROWS;
-    const long long nitems = ntiles * msplit;
     const int mper = (M + msplit - 1) / msplit;               // dictionaries per item
+    // work items: (row tile, dictionary group); a cluster takes CL consecutive tiles of one group
+    uint32_t crank = 0;
+    if (CL > 1) asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+    const long long unit = blockIdx.x / CL, nunits = gridDim.x / CL;
+    const long long nitems = ((ntiles + CL - 1) / CL) * msplit;
     long long my_items = 0;
-    for (long long t = blockIdx.x; t < nitems; t += gridDim.x) ++my_items;
+    for (long long t = unit; t < nitems; t += nunits) ++my_items;
+    auto item_tile = [&](long long item) -> long long { return (item / msplit) * CL + crank; };   // may be >= ntiles (CL = 2)
 
     if (warp == TS_EPI / 32) {
         // ---------------- loader: (A chunk, B chunk) pairs into the ring
@@ -1109,8 +1134,8 @@ __global__ void __launch_bounds__(TS_T, 1) table_tc_stream_kernel(const float* _
             constexpr uint32_t bytes_a = A_PART * sizeof(float), bytes_b = 2 * B_EL * sizeof(float);
             long long q = 0;
             for (long long it = 0; it < my_items; ++it) {
-                const long long item = blockIdx.x + it * gridDim.x;
-                const long long tile = item / msplit;
+                const long long item = unit + it * nunits;
+                const long long tile = min(item_tile(item), ntiles - 1);   // a pair's odd tile past the end re-reads the last one
                 const int m0 = (int)(item % msplit) * mper, m1 = min(M, m0 + mper);
                 for (int m = m0; m < m1; ++m) {
                     for (int ch = 0; ch < nch; ++ch, ++q) {
@@ -1122,7 +1147,13 @@ __global__ void __launch_bounds__(TS_T, 1) table_tc_stream_kernel(const float* _
                                      : "memory");
                         float* slot = ring + (size_t)st * SLOT;
                         bt_bulk(slot, Ag + ((size_t)tile * nch + ch) * 2 * A_EL, bytes_a, &full_bar[st]);
-                        bt_bulk(slot + A_PART, Bg + ((size_t)m * nch + ch) * 2 * B_EL, bytes_b, &full_bar[st]);
+                        const float* bsrc = Bg + ((size_t)m * nch + ch) * 2 * B_EL;
+                        if (CL == 1) {
+                            bt_bulk(slot + A_PART, bsrc, bytes_b, &full_bar[st]);
+                        } else {   // this CTA's half (rank 0: hi image, rank 1: lo image) into both rings
+                            bt_bulk_mc(slot + A_PART + crank * B_EL, bsrc + crank * B_EL, bytes_b / 2, &full_bar[st],
+                                       (uint16_t)((1u << CL) - 1u));
+                        }
                     }
                 }
             }
@@ -1135,7 +1166,7 @@ __global__ void __launch_bounds__(TS_T, 1) table_tc_stream_kernel(const float* _
                                    ((uint32_t)(128 >> 4) << 24);
             long long q = 0, nacc = 0;
             for (long long it = 0; it < my_items; ++it) {
-                const long long item = blockIdx.x + it * gridDim.x;
+                const long long item = unit + it * nunits;
                 const int m0 = (int)(item % msplit) * mper, m1 = min(M, m0 + mper);
                 for (int m = m0; m < m1; ++m, ++nacc) {
                     const int b = (int)(nacc & 1);
@@ -1156,9 +1187,17 @@ __global__ void __launch_bounds__(TS_T, 1) table_tc_stream_kernel(const float* _
                             bt_mma(dacc, bt_desc(ah + off), bt_desc(bl + off), idesc, 1u);
                             if (!EXACT) bt_mma(dacc, bt_desc(al + off), bt_desc(bh + off), idesc, 1u);
                         }
-                        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                         bt_smem_u32(&empty_bar[st]))
-                                     : "memory");
+                        if (CL == 1) {
+                            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                             bt_smem_u32(&empty_bar[st]))
+                                         : "memory");
+                        } else {   // the slot is free once both CTAs' MMAs on it have retired
+                            asm volatile(
+                                "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                                    bt_smem_u32(&empty_bar[st])),
+                                "h"((uint16_t)((1u << CL) - 1u))
+                                : "memory");
+                        }
                     }
                     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                                      bt_smem_u32(&acc_full[b]))
@@ -1169,13 +1208,13 @@ __global__ void __launch_bounds__(TS_T, 1) table_tc_stream_kernel(const float* _
         __syncwarp();
     } else {
         // ---------------- epilogue: TMEM -> 32 x 32 transposes -> full 128-byte row segments
-        const int half = tid >> 7, lane = tid & 31;
-        const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(half * 128);
+        const int half = tid >> 7, lane = tid & 31;   // column group of this thread: [half * QC, (half + 1) * QC)
+        const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(half * QC);
         float* xp = Xpose + (size_t)warp * 1024;
         long long nacc = 0;
         for (long long it = 0; it < my_items; ++it) {
-            const long long item = blockIdx.x + it * gridDim.x;
-            const long long tile = item / msplit;
+            const long long item = unit + it * nunits;
+            const long long tile = item_tile(item);   // rows past n are not stored (g < n below)
             const int m0 = (int)(item % msplit) * mper, m1 = min(M, m0 + mper);
             const long long wrow0 = tile * BT_ROWS + (warp & 3) * 32;
             for (int m = m0; m < m1; ++m, ++nacc) {
@@ -1183,7 +1222,7 @@ __global__ void __launch_bounds__(TS_T, 1) table_tc_stream_kernel(const float* _
                 bt_wait(&acc_full[b], (uint32_t)((nacc >> 1) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll 1
-                for (int c0 = 0; c0 < 128; c0 += 32) {
+                for (int c0 = 0; c0 < QC; c0 += 32) {
                     float v[32];
                     bt_ld32(taddr + (uint32_t)(b * BT_N) + c0, v);
 #pragma unroll
@@ -1191,7 +1230,7 @@ __global__ void __launch_bounds__(TS_T, 1) table_tc_stream_kernel(const float* _
                         *reinterpret_cast<float4*>(xp + lane * 32 + ((j ^ (lane & 7)) << 2)) =
                             make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
                     __syncwarp();
-                    const int cj = lane & 7, col = half * 128 + c0 + 4 * cj;
+                    const int cj = lane & 7, col = half * QC + c0 + 4 * cj;
 #pragma unroll
                     for (int rb = 0; rb < 32; rb += 4) {
                         const int r = rb + (lane >> 3);
@@ -1217,6 +1256,7 @@ __global__ void __launch_bounds__(TS_T, 1) table_tc_stream_kernel(const float* _
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
+    if (CL > 1) bt_cluster_sync();   // no CTA leaves while its peer may still multicast into it
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BT_N));
@@ -1247,19 +1287,44 @@ static int launch_table_tc_stream(const float* X, long long n, long long ldx, in
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int msplit = M % 4 == 0 ? 4 : (M % 2 == 0 ? 2 : 1);
     if (const char* e = getenv("DA_TABLE_MSPLIT")) msplit = std::max(1, std::min(M, atoi(e)));   // A/B runs
+    // 3xTF32 instance: 4 slots of 48 KB + 8 transpose tiles; exact instances: 4 slots of 40 KB + 8 tiles
+    // (16 epilogue warps, Q = 4, measured no faster than 8 at D = 128)
     const size_t smem = sizeof(float) * ((size_t)TS_NS * (2 * A_EL + 2 * B_EL) + 8 * 1024);
+    const size_t smem_x = sizeof(float) * ((size_t)TS_NS * (A_EL + 2 * B_EL) + 8 * 1024);
     static bool attr_set = false;
     if (!attr_set) {
-        DA_CUDA(cudaFuncSetAttribute(table_tc_stream_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        DA_CUDA(cudaFuncSetAttribute(table_tc_stream_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        DA_CUDA(cudaFuncSetAttribute(table_tc_stream_kernel<false, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        DA_CUDA(cudaFuncSetAttribute(table_tc_stream_kernel<true, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_x));
+        DA_CUDA(cudaFuncSetAttribute(table_tc_stream_kernel<true, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_x));
         attr_set = true;
     }
     const int grid = (int)std::min<long long>(ntiles * msplit, sms);
     if (try_exact) {   // both instances are launched; the image kernel's flag picks one (no host sync)
-        table_tc_stream_kernel<true><<<grid, TS_T, smem, s>>>(Ag, n, M, K, nch, Bg, T, ldt, msplit, flag);
+        // pairs of CTAs sharing the codeword stream (DA_TABLE_CLUSTER=1/2 forces one CTA / pairs)
+        static const int cl_env = getenv("DA_TABLE_CLUSTER") ? atoi(getenv("DA_TABLE_CLUSTER")) : -1;
+        const bool pair = cl_env >= 0 ? cl_env == 2 : (nch <= 9 && ntiles >= 4);
+        if (pair) {
+            const long long units = ((ntiles + 1) / 2) * msplit;
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3((unsigned)(2 * std::min<long long>(units, sms / 2)));
+            cfg.blockDim = dim3(TS_T);
+            cfg.dynamicSmemBytes = smem_x;
+            cfg.stream = s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 2;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            DA_CUDA(cudaLaunchKernelEx(&cfg, table_tc_stream_kernel<true, 2, 2>, (const float*)Ag, n, M, K, nch,
+                                       (const float*)Bg, T, ldt, msplit, (const int*)flag));
+        } else {
+            table_tc_stream_kernel<true, 1, 2><<<grid, TS_T, smem_x, s>>>(Ag, n, M, K, nch, Bg, T, ldt, msplit, flag);
+        }
         DA_CHECK_LAUNCH("table_tc_stream_kernel<exact>");
     }
-    table_tc_stream_kernel<false><<<grid, TS_T, smem, s>>>(Ag, n, M, K, nch, Bg, T, ldt, msplit, flag);
+    table_tc_stream_kernel<false, 1, 2><<<grid, TS_T, smem, s>>>(Ag, n, M, K, nch, Bg, T, ldt, msplit, flag);
     DA_CHECK_LAUNCH("table_tc_stream_kernel");
     return 0;
 }
