@@ -232,8 +232,25 @@ def lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, c
     (clustering.py:195, ~1% of updates); they are recomputed there against a
     snapshot of the centroids they belong to.  Centroids and labels are the
     same bits either way."""
-    with assign_image(Xr, active):
-        return _lloyd(Xr, C_init, active, max_iters, comm, not want_trace)
+    Xa = _active_prefix(Xr, active) if comm is None else None
+    with assign_image(Xr if Xa is None else Xa, active):
+        return _lloyd(Xr, C_init, active, max_iters, comm, not want_trace, Xa=Xa)
+
+
+def _active_prefix(Xr: torch.Tensor, active: int):
+    """A compact copy of the active columns for narrow prefixes (one-GPU loop).
+
+    The iterations of a stage read only the first `active` columns of the rotated rows; at
+    D = 128 those are 16-64 bytes out of every 1-KB row, one DRAM granule per row for every
+    gather of the Lloyd update and every assign.  A (n, 8 or 16) float64 copy (64-128 MB at 1M
+    rows, L2-sized below ~1M x 8) serves the whole stage: same values, same order, same bits."""
+    n, D = Xr.shape
+    if active > 16 or D < 64 or n < 32768 or Xr.dtype != F64:
+        return None
+    apad = 8 if active <= 8 else 16
+    Xa = _arena("lloyd_xa", (n, apad), F64, Xr.device)
+    Xa.copy_(Xr[:, :apad])
+    return Xa
 
 
 def _arena(name: str, shape, dtype, dev) -> torch.Tensor:
@@ -259,9 +276,11 @@ def _lloyd_events():
     return _EVENTS[dev]
 
 
-def _lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, comm=None, lazy=False):
+def _lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, comm=None, lazy=False, Xa=None):
     if comm is not None and comm.world == 1 and not os.environ.get("DA_SHARD_LOOP"):
         comm = None   # one shard: nothing to exchange (DA_SHARD_LOOP=1 keeps the shard loop, for timing it)
+    if Xa is None or comm is not None:
+        Xa = Xr       # the rows the iterations read (a compact copy of the active columns, or Xr itself)
     n, D = Xr.shape
     K = C_init.shape[0]
     dev = Xr.device
@@ -274,8 +293,8 @@ def _lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, 
     xx = None
     if n:
         xx = _arena("lloyd_xx", (n,), F64, dev) if comm is None else torch.empty(n, dtype=F64, device=dev)
-        native.da_row_sqnorms(P(Xr), is_f32(Xr), n, Xr.stride(0), active, P(xx), stream())   # fixed for the stage
-    labels, errs = assign(Xr, active, C, xx=xx, want_d2=not lazy)
+        native.da_row_sqnorms(P(Xa), is_f32(Xa), n, Xa.stride(0), active, P(xx), stream())   # fixed for the stage
+    labels, errs = assign(Xa, active, C, xx=xx, want_d2=not lazy)
     if comm is None and n:
         lab2 = _arena("lloyd_lab2", (n,), I32, dev)   # the ring slot iteration 0 reads (labels_prev)
         lab2.copy_(labels)
@@ -323,7 +342,7 @@ def _lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, 
                 nl = lab_ring[(j + 1) % 3]
             ne = None if lazy else d2_ring[j % 3]
             # group means, #empty, assign, flags -> pinned host, event: one call
-            native.da_lloyd_step(P(Xr), n, Xr.stride(0), active, K, P(C_prev), P(Cn), Cn.stride(0),
+            native.da_lloyd_step(P(Xa), n, Xa.stride(0), active, K, P(C_prev), P(Cn), Cn.stride(0),
                                  P(snaps[slot]) if lazy else None, P(labels_prev), P(nl), P(ne), P(xx), P(cn), P(fl),
                                  P(flags_h[slot]), ctypes.c_void_p(done_ev[slot].cuda_event), stream())
             return [slot, labels_prev, nl, ne]
@@ -340,10 +359,10 @@ def _lloyd(Xr: torch.Tensor, C_init: torch.Tensor, active: int, max_iters: int, 
                 spec = None                          # computed from pre-reseed centroids
                 empty = np.flatnonzero(cn.cpu().numpy() == 0)
                 if lazy:
-                    errs = assign(Xr, active, snaps[slot], xx=xx)[1]
+                    errs = assign(Xa, active, snaps[slot], xx=xx)[1]
                 _reseed_single(Xr, errs, empty, Cn)
                 fl.zero_()
-                new_labels, errs_new = assign(Xr, active, Cn, prev=labels_prev, changed=fl[0:1], xx=xx,
+                new_labels, errs_new = assign(Xa, active, Cn, prev=labels_prev, changed=fl[0:1], xx=xx,
                                               want_d2=not lazy)
                 fh = fl.cpu().numpy()
             C = Cn
