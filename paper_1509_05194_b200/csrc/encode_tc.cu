@@ -1291,7 +1291,8 @@ static int launch_table_tc_stream(const float* X, long long n, long long ldx, in
     // (16 epilogue warps, Q = 4, measured no faster than 8 at D = 128)
     const size_t smem = sizeof(float) * ((size_t)TS_NS * (2 * A_EL + 2 * B_EL) + 8 * 1024);
     const size_t smem_x = sizeof(float) * ((size_t)TS_NS * (A_EL + 2 * B_EL) + 8 * 1024);
-    static bool attr_set = false;
+    static bool attr_set_dev[64] = {};   // per device (one process per GPU is the usual case)
+    bool& attr_set = attr_set_dev[dev & 63];
     if (!attr_set) {
         DA_CUDA(cudaFuncSetAttribute(table_tc_stream_kernel<false, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         DA_CUDA(cudaFuncSetAttribute(table_tc_stream_kernel<true, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_x));
